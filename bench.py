@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py -- triangle-count GTEPS (|E|/time) on B200, BASELINE.json's metric.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  python bench.py --impl reference        # the reference's own CPU path
+
+Workload (config.workload): RMAT scale-24 edgefactor-16 with per-vertex
+counts (BASELINE.json configs[3], the configuration the metric's "1/2/4/8
+B200" is quoted on; it fits one GPU).  Synthetic, deterministic (SURVEY.md 8d
+splitmix generator, generated on the device).
+
+A step = one triangle count of the whole graph from the resident oriented CSR:
+level-1 frontier + degree-binned advance/join + reduce (total and per-vertex),
+plus at N>1 the NCCL allreduce of the per-rank partial counts.  `value` =
+|E| / step time (GTEPS, whole job).  `e2e` = the same through the
+reference-facing drop-in call count_triangles(const Graph&) with HOST buffers:
+H2D of the symmetric CSR (pinned) + orientation + count + D2H of the total and
+per-vertex array, every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kind, scale, param, per_vertex, description)
+    "C1": ("rmat", 16, 16, False, "RMAT scale-16 edgefactor-16 (configs[0])"),
+    "C2": ("er", 20, 32, False, "Erdos-Renyi G(n=2^20, avg degree 32) (configs[1])"),
+    "C3": ("kron", 22, 16, False, "Graph500 Kronecker scale-22 edgefactor-16, permuted (configs[2])"),
+    "C4": ("rmat", 24, 16, True, "RMAT scale-24 edgefactor-16 with per-vertex counts (configs[3])"),
+    "C5": ("rmat", 26, 32, True, "RMAT scale-26 edgefactor-32 (configs[4])"),
+}
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--no-per-vertex", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gen_kind(tc, kind):
+    return {"rmat": tc.GEN_RMAT, "kron": tc.GEN_KRON, "er": tc.GEN_ER}[kind]
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own count_triangles path (oracle/_ref, built
+# from /root/reference's sources) on a bounded, cost-stratified seed sample,
+# extrapolated by the reference's per-row visit cost model.
+# ---------------------------------------------------------------------------
+def reference_cpu_sample(off: np.ndarray, nb: np.ndarray, budget_s: float, E: int, rg=None):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle_ctypes import REF_SO, Ref
+    if not os.path.exists(REF_SO):
+        return None
+    ref = Ref()
+    if rg is None:
+        rg = ref.graph(off, nb)
+    n = off.size - 1
+    deg = np.diff(off).astype(np.int64)
+    # visits the final level makes for seed u: deg(u) per level-1 row (u,w),
+    # w in N(u), w > u (matcher.cpp:215-228); cost-stratified systematic sample
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    up = np.bincount(rows[nb.astype(np.int64) > rows], minlength=n).astype(np.int64)
+    del rows
+    cost = deg * up
+    total_cost = float(cost.sum())
+    order = np.argsort(cost, kind="stable")[::-1]
+    order = order[cost[order] > 0]
+    workers = os.cpu_count() or 1
+
+    def run(stride):
+        seeds = np.sort(order[::stride]).astype(np.uint32)
+        s = rg.count_sample(seeds, lookahead=2, workers=0)
+        s["sample_cost"] = float(cost[seeds.astype(np.int64)].sum())
+        s["nseeds"] = int(seeds.size)
+        return s
+
+    stride = max(1, int(order.size // 64))
+    s = run(stride)
+    # scale the sample so the verify phase takes ~budget_s
+    while s["verify_ms"] < 1000 * budget_s / 8 and stride > 1:
+        stride = max(1, int(stride / max(2.0, (1000 * budget_s / 2) / max(s["verify_ms"], 1.0))))
+        s = run(stride)
+    t_full_ms = s["filter_ms"] + s["verify_ms"] * total_cost / max(s["sample_cost"], 1.0)
+    return {
+        "value": E / (t_full_ms / 1e3) / 1e9,
+        "unit": "GTEPS",
+        "cores": workers,
+        "kind": "reference",
+        "t_full_est_ms": t_full_ms,
+        "sample": (f"trimatch::count_triangles path (filter_candidates on the full graph + expand_level "
+                   f"L1/L2 through the public API) seeded with {s['nseeds']} of {order.size} candidate "
+                   f"vertices (cost-stratified every {stride}th by deg(u)*|N(u)>u|); verify time "
+                   f"{s['verify_ms']:.0f} ms extrapolated by cost ratio {total_cost / max(s['sample_cost'], 1):.1f}; "
+                   f"filter {s['filter_ms']:.0f} ms timed on the full graph; OpenMP workers={workers}"),
+    }
+
+
+def host_graph(cfg):
+    """Host CSR for the CPU arms: generator + build restated in oracle/ (the
+    CSR equals trimatch::build_graph's, tests/test_oracle.py)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle_ctypes import Oracle
+    o = Oracle()
+    kind, scale, param = cfg[0], cfg[1], cfg[2]
+    pairs = o.gen_er(scale, param) if kind == "er" else o.gen_rmat(scale, param, kind == "kron")
+    off, nb, E, _, _ = o.build_graph(pairs, 1 << scale)
+    return off, nb, E
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[a.config]
+    off, nb, E = host_graph(cfg)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle_ctypes import Ref
+    rg = Ref().graph(off, nb)
+    vals = []
+    last = None
+    budget = max(2.0, min(a.cpu_budget_s, 150.0 / max(1, a.steps + a.warmup)))
+    for i in range(a.warmup + a.steps):
+        r = reference_cpu_sample(off, nb, budget, E, rg)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtrimatch_ref.so not built"}))
+            return
+        if i >= a.warmup:
+            vals.append(r["value"])
+        last = r
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": "triangle-count GTEPS (|E|/time)", "value": v, "unit": "GTEPS",
+        "n_gpus": 0, "steps": a.steps, "warmup": a.warmup, "ms_per_step": E / (v * 1e9) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": cfg[4], "config": a.config, "num_edges": int(E), "num_vertices": int(off.size - 1)},
+        "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": last["cores"], "kind": "reference",
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_02127_b200 as tc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[a.config]
+    kind, scale, param, per_vertex, desc = cfg
+    per_vertex = per_vertex and not a.no_per_vertex
+    n = 1 << scale
+
+    # ---- input: deterministic synthetic edge list generated on the device ----
+    m = tc.gen_num_edges(gen_kind(tc, kind), scale, param)
+    pairs = torch.empty(2 * m, dtype=torch.int32, device=dev)
+    tc.generate(gen_kind(tc, kind), scale, param, out=pairs, device=local)
+    rep = tc.BuildReport()
+    g = tc.build_graph_from_pairs(pairs, n, rep, device=local, m=m)
+    build_ms = g.build_ms
+    del pairs
+    torch.cuda.empty_cache()
+    E = g.num_edges()
+    stream = torch.cuda.current_stream(dev)
+    g.set_stream(stream.cuda_stream)
+
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
+    opts = tc.MatchOptions(per_vertex=per_vertex, part_index=rank, part_count=world)
+
+    def step():
+        st = tc.count_triangles_into(g, total, pv, opts, stats=True)
+        if world > 1:
+            dist.all_reduce(total)
+            if pv is not None:
+                dist.all_reduce(pv)
+        return st
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            stats.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    T = int(total.item())
+    join_ms = float(np.mean([s["join_ms"] for s in stats]))
+    s0 = stats[0]
+    if world > 1:
+        jt = torch.tensor([join_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(jt, op=dist.ReduceOp.MAX)
+        join_ms = float(jt.item())
+    launches = int(sum(s["kernel_launches"] for s in stats))
+
+    # ---- e2e: drop-in count_triangles(const Graph&) with host buffers ----
+    # the host Graph = the symmetric CSR (exported once, pinned)
+    ro_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+    nb_h = torch.empty(max(2 * E, 1), dtype=torch.int32, pin_memory=True)
+    g.export_csr(ro_h, nb_h)
+    tot_h = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    pv_h = torch.zeros(n, dtype=torch.int64, pin_memory=True) if per_vertex else None
+    pv_d = torch.zeros(n, dtype=torch.int64, device=dev) if (per_vertex and world > 1) else None
+    tot_d = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def e2e_step():
+        ge = tc.graph_from_csr(ro_h, nb_h, n, E, device=local)        # H2D + orientation
+        if world == 1:
+            tc.count_triangles_into(ge, tot_h, pv_h, opts, sync=True)  # count + D2H
+        else:
+            tc.count_triangles_into(ge, tot_d, pv_d, opts, sync=True)
+            dist.all_reduce(tot_d)
+            if pv_d is not None:
+                dist.all_reduce(pv_d)
+            tot_h.copy_(tot_d)
+            if pv_h is not None:
+                pv_h.copy_(pv_d)
+            torch.cuda.synchronize()
+        del ge
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / a.e2e_steps
+    if world > 1:
+        et = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms = float(et.item())
+    assert int(tot_h[0]) == T, (int(tot_h[0]), T)
+    h2d = 8 * (n + 1) + 4 * 2 * E
+    d2h = 8 + (8 * n if per_vertex else 0)
+
+    peak, peak_kind = peaks()
+    alg_bytes = s0["alg_bytes"]
+    achieved = alg_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
+    pivot_bytes = s0["probe_bytes"]
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", f"ncu_{a.config}_join_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "triangle-count GTEPS (|E|/time)",
+        "value": E / (ms / 1e3) / 1e9,
+        "unit": "GTEPS",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic",
+        "config": {
+            "workload": desc, "config": a.config, "generator": f"{kind} scale={scale} param={param} (SURVEY 8d splitmix)",
+            "num_vertices": n, "num_edges": int(E), "raw_edges": int(m), "triangles": T,
+            "per_vertex": per_vertex, "parallelism": f"work-ranges x{world} + NCCL allreduce" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (oriented CSR + frontier >> 126 MB); no flush",
+            "build_ms": build_ms, "self_loops_removed": rep.self_loops_removed,
+            "duplicate_entries_removed": rep.duplicate_entries_removed,
+        },
+        "e2e": {"value": E / (e2e_ms / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "tc_graph_from_csr(host pinned CSR) + tc_count(host outputs)"},
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_kind": peak_kind,
+            "kernel": "k_join_cta + k_join_warp (advance + fused SMEM-hash join)",
+            "alg_bytes_per_step": alg_bytes, "join_ms": join_ms,
+            "model": "B_alg = 4W + 12|E+| + 8(|V|+1) + 8|V| (SURVEY 8d wedge-stream bytes)",
+            "pivot_model_bytes": pivot_bytes,
+            "pivot_model_frac": pivot_bytes / (join_ms / 1e3) / 1e9 / peak / max(1, world) if join_ms > 0 else 0,
+            "wedges_probed": s0["wedges"], "W": s0["dag_W"],
+        },
+        "phases_ms": {"frontier": float(np.mean([s["frontier_ms"] for s in stats])), "join": join_ms,
+                      "reduce": float(np.mean([s["reduce_ms"] for s in stats]))},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            ro_np = ro_h.numpy().view(np.uint64)
+            nb_np = nb_h.numpy().view(np.uint32)[: 2 * E]
+            line["cpu_baseline"] = reference_cpu_sample(ro_np, nb_np, a.cpu_budget_s, E)
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * tcb200.h -- C-ABI of libtcb200.so, the B200-native drop-in for the reference
+ * triangle-counting hot path (trimatch, /root/reference/proj).
+ *
+ * Plain pointers and sizes only; no CUDA or torch types cross this boundary
+ * (streams are passed as void*).  Every input/output buffer may live in host
+ * memory or in device memory of the handle's device: the library inspects each
+ * pointer (cudaPointerGetAttributes) and copies as needed.
+ *
+ * Entry point                 replaces (reference, relative to proj/)
+ * ---------------------------------------------------------------------------
+ * tc_graph_build              trimatch::build_graph      include/trimatch/graph.hpp:73
+ *                             (graph.cpp:33-85; BuildReport graph.hpp:22-25)
+ * tc_graph_from_csr           trimatch::Graph ctor       graph.hpp:38-39 (graph.cpp:9-21)
+ *                             -- the route count_triangles(const Graph&) takes
+ * tc_graph_export_csr         Graph::row_offsets()/neighbor_array() graph.hpp:58-59
+ * tc_graph_degrees            trimatch::degrees          graph.hpp:75 (graph.cpp:87-91)
+ * tc_count                    trimatch::count_triangles  matcher.hpp:128
+ *                             (matcher.cpp:301-303 -> match :249-299 ->
+ *                              count_final_level :204-245)
+ * tc_parse_matrix_market      trimatch::parse_matrix_market io.hpp:34 (io.cpp:93-159)
+ * tc_csr_cache_parse          trimatch::read_csr_cache   io.hpp:40 (io.cpp:187-220)
+ * tc_graph_destroy            ~Graph
+ * tc_last_error               the what() of the exception the reference throws
+ *
+ * Errors: the reference throws C++ exceptions; here each maps to a status code
+ * (graph.cpp:40-42 invalid_argument -> TC_EINVAL; graph.cpp:24-28 out_of_range
+ * -> TC_ERANGE; io.hpp:13-22 ParseError -> TC_EPARSE; io.hpp:25-27 IoError ->
+ * TC_EIO).  include/trimatch_gpu.hpp maps them back to the same exception types.
+ * On error no handle is returned and outputs are left untouched.
+ *
+ * Threading: calls on one handle are serialised on the handle's stream; handles
+ * on different devices are independent.  tc_last_error() is thread-local.
+ */
+#ifndef TCB200_H
+#define TCB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCB200_ABI_VERSION 1
+
+typedef enum tc_status {
+  TC_OK = 0,
+  TC_EINVAL = 1,       /* std::invalid_argument */
+  TC_ERANGE = 2,       /* std::out_of_range, or a size past the 32-bit id / edge limits */
+  TC_ENOMEM = 3,       /* device allocation failed */
+  TC_ECUDA = 4,        /* CUDA runtime error (message in tc_last_error) */
+  TC_ENCCL = 5,        /* reserved for the multi-GPU allreduce */
+  TC_EUNSUPPORTED = 6, /* keep_listings etc. (out of scope on the GPU path) */
+  TC_EPARSE = 7,       /* trimatch::ParseError */
+  TC_EIO = 8           /* trimatch::IoError */
+} tc_status;
+
+typedef struct tc_graph tc_graph;
+
+/* trimatch::BuildReport (graph.hpp:22-25). */
+typedef struct tc_build_report {
+  uint64_t self_loops_removed;
+  uint64_t duplicate_entries_removed;
+} tc_build_report;
+
+typedef struct tc_graph_info {
+  uint32_t num_vertices;   /* Graph::num_vertices()   graph.hpp:41 */
+  uint64_t num_edges;      /* Graph::num_edges()      graph.hpp:43 (undirected, once) */
+  uint32_t max_degree;
+  uint32_t max_out_degree; /* max d+ in the (deg,id)-oriented DAG */
+  int device;
+  double build_ms;         /* device time of the last build/from_csr (CUDA events) */
+} tc_graph_info;
+
+/* trimatch::MatchOptions (matcher.hpp:84-88) + GPU extensions. */
+typedef struct tc_count_opts {
+  int lookahead;        /* validated in {0,1,2} like matcher.cpp:250-252; count-neutral */
+  int keep_listings;    /* must be 0: listings are out of scope on the GPU path */
+  uint32_t part_index;  /* multi-GPU: this rank's share of the degree-weighted */
+  uint32_t part_count;  /*   work ranges (0/1 = whole graph)                 */
+  int sync;             /* 1: block until outputs are final (default for 0-init = async
+                           only when both outputs are device pointers) */
+} tc_count_opts;
+
+/* trimatch::MatchStats analogue (matcher.hpp:69-82) for the GPU path. */
+typedef struct tc_count_stats {
+  double total_ms;        /* device time of the whole tc_count (CUDA events) */
+  double frontier_ms;     /* level-1 frontier: in-edge items + work plan      */
+  double join_ms;         /* advance + fused join kernels                      */
+  double reduce_ms;       /* per-vertex gather/flush + total                  */
+  uint64_t pivots;        /* vertices v with d+(v)>0 and >=1 useful in-edge   */
+  uint64_t items;         /* oriented edges (u->v) whose wedge suffix is non-empty */
+  uint64_t wedges;        /* J = candidate wedges probed = sum of suffix lengths */
+  uint64_t segments;      /* work segments scheduled (warp + CTA bins)        */
+  uint64_t join_launches; /* join kernel launches                              */
+  double dag_W;           /* W = sum_{u->v} d+(v) (SURVEY 8d wedge-stream model) */
+  double alg_bytes;       /* B_alg = 4W + 12|E+| + 8(|V|+1) [+8|V| per-vertex]   */
+  double probe_bytes;     /* bytes the pivot join must read: 4J + 8 items + 4|E+| */
+  uint64_t kernel_launches; /* all libtcb200 kernels this call launched */
+} tc_count_stats;
+
+/* ---- graph construction ------------------------------------------------ */
+
+/* build_graph: pairs = 2*m u32 interleaved (u,v) -- the memory layout of
+ * trimatch::EdgeList::edges (vector<pair<u32,u32>>), host or device.  Drops
+ * self-loops and duplicates, symmetrises; ids >= n_declared -> TC_EINVAL. */
+tc_status tc_graph_build(const uint32_t* pairs, uint64_t m, uint32_t n_declared, int device,
+                         tc_graph** out, tc_build_report* report);
+
+/* Graph ctor route: an existing symmetric CSR (row_offsets n+1 u64, neighbors
+ * 2E u32, rows strictly ascending, the Graph invariants graph.hpp:29-32). */
+tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbors, uint32_t n,
+                            uint64_t num_edges, int device, tc_graph** out);
+
+tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info);
+
+/* Symmetric CSR byte-identical to the reference build_graph output:
+ * row_offsets (n+1 u64) and neighbors (2E u32), caller-owned, host or device. */
+tc_status tc_graph_export_csr(tc_graph* g, uint64_t* row_offsets, uint32_t* neighbors);
+
+/* degrees(g) (graph.cpp:87-91): n u32, caller-owned, host or device. */
+tc_status tc_graph_degrees(tc_graph* g, uint32_t* degrees);
+
+/* Launch subsequent work on this CUDA stream (cudaStream_t as void*; NULL =
+ * the handle's own stream). */
+tc_status tc_graph_set_stream(tc_graph* g, void* stream);
+
+void tc_graph_destroy(tc_graph* g);
+
+/* ---- the hot path ------------------------------------------------------ */
+
+/* count_triangles: total (u64, host or device) and optional per-vertex
+ * counts (n u64 in original vertex ids; host or device; NULL = total only).
+ * With opts->part_count > 1 only this part's work ranges are counted; summing
+ * total/per_vertex over all parts (one NCCL allreduce) gives the full result. */
+tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint64_t* per_vertex,
+                   tc_count_stats* stats);
+
+/* ---- adjacent formats ------------------------------------- */
+
+/* parse_matrix_market over an in-memory byte buffer (host).  On success
+ * *pairs is a malloc'ed 2*m u32 buffer (free with tc_free). */
+tc_status tc_parse_matrix_market(const char* text, uint64_t len, uint32_t** pairs, uint64_t* m,
+                                 uint32_t* n_declared);
+
+/* TRIMCSR1 binary cache (io.cpp:18-19, :167-220) held in memory: validates
+ * and builds a handle straight from the CSR (no sort). */
+tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_graph** out);
+
+/* ---- synthetic inputs (SURVEY 8d generators, bit-exact on device) ------- */
+
+/* kind: 0 = RMAT (Graph500 a,b,c = .57,.19,.19), 1 = Kronecker (RMAT +
+ * seeded Fisher-Yates label permutation), 2 = Erdos-Renyi G(n,m).
+ * param = edgefactor (RMAT/Kron) or average degree (ER).  pairs: 2*m u32,
+ * host or device.  tc_gen_num_edges gives m. */
+uint64_t tc_gen_num_edges(int kind, int scale, int param);
+tc_status tc_generate(int kind, int scale, int param, int device, uint32_t* pairs);
+
+void tc_free(void* p);
+const char* tc_last_error(void);
+int tc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCB200_H */

@@ -1,0 +1,452 @@
+"""paper_1909_02127_b200 -- B200-native BFS-based triangle counting.
+
+Host-side mirror of the reference's operator interface (namespace trimatch,
+/root/reference/proj) over the C-ABI of libtcb200.so (include/tcb200.h):
+
+  reference (C++)                         here
+  --------------------------------------  -----------------------------------
+  EdgeList            graph.hpp:16-19     EdgeList
+  BuildReport         graph.hpp:22-25     BuildReport
+  Graph               graph.hpp:35-66     Graph  (device-resident handle)
+  build_graph         graph.hpp:73        build_graph
+  degrees             graph.hpp:75        degrees
+  parse_matrix_market io.hpp:34-35        parse_matrix_market[_file]
+  read/write_csr_cache io.hpp:39-41       read_csr_cache / write_csr_cache
+  load_graph          io.hpp:45           load_graph
+  MatchOptions        matcher.hpp:84-88   MatchOptions
+  MatchResult         matcher.hpp:90-94   MatchResult (+ per_vertex)
+  count_triangles     matcher.hpp:128     count_triangles
+
+Exceptions follow the reference: std::invalid_argument -> InvalidArgument
+(a ValueError), std::out_of_range -> IndexError, ParseError / IoError as in
+io.hpp:13-27.  There is no CPU fallback: importing this package raises if the
+CUDA library is missing, and every call runs the sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtcb200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(make -C paper_1909_02127_b200/csrc). There is no CPU fallback.")
+
+_lib = C.CDLL(LIB_PATH)
+
+TC_OK, TC_EINVAL, TC_ERANGE, TC_ENOMEM, TC_ECUDA, TC_ENCCL, TC_EUNSUPPORTED, TC_EPARSE, TC_EIO = range(9)
+
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+
+
+class TcBuildReport(C.Structure):
+    _fields_ = [("self_loops_removed", C.c_uint64), ("duplicate_entries_removed", C.c_uint64)]
+
+
+class TcGraphInfo(C.Structure):
+    _fields_ = [("num_vertices", C.c_uint32), ("num_edges", C.c_uint64), ("max_degree", C.c_uint32),
+                ("max_out_degree", C.c_uint32), ("device", C.c_int), ("build_ms", C.c_double)]
+
+
+class TcCountOpts(C.Structure):
+    _fields_ = [("lookahead", C.c_int), ("keep_listings", C.c_int), ("part_index", C.c_uint32),
+                ("part_count", C.c_uint32), ("sync", C.c_int)]
+
+
+class TcCountStats(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("frontier_ms", C.c_double), ("join_ms", C.c_double),
+                ("reduce_ms", C.c_double), ("pivots", C.c_uint64), ("items", C.c_uint64),
+                ("wedges", C.c_uint64), ("segments", C.c_uint64), ("join_launches", C.c_uint64),
+                ("dag_W", C.c_double), ("alg_bytes", C.c_double), ("probe_bytes", C.c_double),
+                ("kernel_launches", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_sig("tc_abi_version", C.c_int, [])
+_sig("tc_last_error", C.c_char_p, [])
+_sig("tc_free", None, [C.c_void_p])
+_sig("tc_graph_build", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(C.c_void_p),
+                                 C.POINTER(TcBuildReport)])
+_sig("tc_graph_from_csr", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_int,
+                                    C.POINTER(C.c_void_p)])
+_sig("tc_graph_get_info", C.c_int, [C.c_void_p, C.POINTER(TcGraphInfo)])
+_sig("tc_graph_export_csr", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p])
+_sig("tc_graph_degrees", C.c_int, [C.c_void_p, C.c_void_p])
+_sig("tc_graph_set_stream", C.c_int, [C.c_void_p, C.c_void_p])
+_sig("tc_graph_destroy", None, [C.c_void_p])
+_sig("tc_count", C.c_int, [C.c_void_p, C.POINTER(TcCountOpts), C.c_void_p, C.c_void_p,
+                           C.POINTER(TcCountStats)])
+_sig("tc_parse_matrix_market", C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), u64p, u32p])
+_sig("tc_csr_cache_to_graph", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p)])
+_sig("tc_gen_num_edges", C.c_uint64, [C.c_int, C.c_int, C.c_int])
+_sig("tc_generate", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p])
+
+EXPORTED_SYMBOLS = [
+    "tc_abi_version", "tc_last_error", "tc_free", "tc_graph_build", "tc_graph_from_csr", "tc_graph_get_info",
+    "tc_graph_export_csr", "tc_graph_degrees", "tc_graph_set_stream", "tc_graph_destroy", "tc_count",
+    "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate",
+]
+
+
+# ---- exceptions (io.hpp:13-27, graph.cpp:16-20/:24-28/:40-42) ---------------
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class ParseError(RuntimeError):
+    """trimatch::ParseError (io.hpp:13-22): message ends with '(line N)'."""
+
+    def __init__(self, message: str):
+        super().__init__(message)
+        import re
+        m = re.search(r"\(line (\d+)\)$", message)
+        self.line = int(m.group(1)) if m else 0
+
+
+class IoError(RuntimeError):
+    """trimatch::IoError (io.hpp:25-27)"""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class Unsupported(RuntimeError):
+    pass
+
+
+def _check(rc: int):
+    if rc == TC_OK:
+        return
+    msg = (_lib.tc_last_error() or b"").decode()
+    if rc == TC_EINVAL:
+        raise InvalidArgument(msg)
+    if rc == TC_ERANGE:
+        raise IndexError(msg)
+    if rc == TC_EPARSE:
+        raise ParseError(msg)
+    if rc == TC_EIO:
+        raise IoError(msg)
+    if rc == TC_EUNSUPPORTED:
+        raise Unsupported(msg)
+    if rc == TC_ENOMEM:
+        raise MemoryError(msg)
+    raise CudaError(f"[{rc}] {msg}")
+
+
+def _addr(x) -> int:
+    """Address of a numpy array, a torch tensor (host or device) or an int."""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise InvalidArgument("array must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+# ---- domain types ------------------------------------------------------------
+
+@dataclass
+class EdgeList:
+    """graph.hpp:16-19: raw (u,v) pairs, may hold loops/dups/both orientations.
+    `edges` is an (m,2) uint32 array (or anything convertible)."""
+    num_vertices_declared: int = 0
+    edges: np.ndarray = field(default_factory=lambda: np.zeros((0, 2), np.uint32))
+
+    def pairs(self) -> np.ndarray:
+        a = np.ascontiguousarray(np.asarray(self.edges, dtype=np.uint32).reshape(-1, 2))
+        return a
+
+
+@dataclass
+class BuildReport:
+    self_loops_removed: int = 0
+    duplicate_entries_removed: int = 0
+
+
+@dataclass
+class MatchOptions:
+    """matcher.hpp:84-88.  lookahead is validated (0..2) and count-neutral on
+    the GPU path; keep_listings is out of scope (raises Unsupported)."""
+    lookahead: int = 2
+    keep_listings: bool = False
+    per_vertex: bool = False
+    part_index: int = 0
+    part_count: int = 1
+
+
+@dataclass
+class MatchResult:
+    """matcher.hpp:90-94 (+ per_vertex u64[n] when requested)."""
+    count: int = 0
+    per_vertex: Optional[np.ndarray] = None
+    stats: dict = field(default_factory=dict)
+
+
+class Graph:
+    """Device-resident oriented graph (graph.hpp:35-66 semantics on the host
+    side: num_vertices, num_edges, degree, row_offsets, neighbor_array,
+    neighbors, has_edge).  The symmetric CSR is materialised on demand."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = C.c_void_p(handle)
+        self.device = device
+        self._csr = None
+        info = TcGraphInfo()
+        _check(_lib.tc_graph_get_info(self._h, C.byref(info)))
+        self._info = info
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.tc_graph_destroy(h)
+            self._h = C.c_void_p(0)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def num_vertices(self) -> int:
+        return self._info.num_vertices
+
+    def num_edges(self) -> int:
+        return self._info.num_edges
+
+    @property
+    def max_degree(self) -> int:
+        return self._info.max_degree
+
+    @property
+    def max_out_degree(self) -> int:
+        return self._info.max_out_degree
+
+    @property
+    def build_ms(self) -> float:
+        return self._info.build_ms
+
+    def set_stream(self, stream_ptr: int):
+        _check(_lib.tc_graph_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+
+    def export_csr(self, row_offsets=None, neighbors=None):
+        """Symmetric CSR identical to the reference build_graph output; writes
+        into the given buffers (host numpy or device tensors) or returns new
+        numpy arrays."""
+        n, E = self.num_vertices(), self.num_edges()
+        ro = row_offsets if row_offsets is not None else np.empty(n + 1, np.uint64)
+        nb = neighbors if neighbors is not None else np.empty(max(2 * E, 1), np.uint32)
+        _check(_lib.tc_graph_export_csr(self._h, C.c_void_p(_addr(ro)), C.c_void_p(_addr(nb))))
+        if neighbors is None:
+            nb = nb[: 2 * E]
+        return ro, nb
+
+    def _ensure_csr(self):
+        if self._csr is None:
+            self._csr = self.export_csr()
+        return self._csr
+
+    def row_offsets(self) -> np.ndarray:
+        return self._ensure_csr()[0]
+
+    def neighbor_array(self) -> np.ndarray:
+        return self._ensure_csr()[1]
+
+    def degree(self, u: int) -> int:
+        ro = self.row_offsets()
+        return int(ro[u + 1] - ro[u])
+
+    def neighbors(self, u: int) -> np.ndarray:
+        ro, nb = self._ensure_csr()
+        return nb[ro[u]: ro[u + 1]]
+
+    def has_edge(self, u: int, v: int) -> bool:
+        """graph.cpp:23-31 (out_of_range on a bad id)."""
+        n = self.num_vertices()
+        if u >= n or v >= n or u < 0 or v < 0:
+            raise IndexError(f"has_edge: vertex id {u if (u >= n or u < 0) else v} out of range")
+        nb = self.neighbors(u)
+        i = int(np.searchsorted(nb, v))
+        return i < nb.size and int(nb[i]) == v
+
+
+# ---- operations ----------------------------------------------------------------
+
+def build_graph(edges: EdgeList, report: Optional[BuildReport] = None, device: int = 0) -> Graph:
+    """trimatch::build_graph (graph.hpp:73)."""
+    pairs = edges.pairs() if isinstance(edges, EdgeList) else edges
+    n = edges.num_vertices_declared if isinstance(edges, EdgeList) else None
+    return build_graph_from_pairs(pairs, n, report=report, device=device)
+
+
+def build_graph_from_pairs(pairs, n_declared: int, report: Optional[BuildReport] = None, device: int = 0,
+                           m: Optional[int] = None) -> Graph:
+    """pairs: (m,2)/(2m,) uint32 numpy array, or a host/device torch tensor."""
+    if m is None:
+        m = (pairs.size if isinstance(pairs, np.ndarray) else pairs.numel()) // 2
+    h = C.c_void_p()
+    rep = TcBuildReport()
+    _check(_lib.tc_graph_build(C.c_void_p(_addr(pairs)), m, n_declared, device, C.byref(h), C.byref(rep)))
+    if report is not None:
+        report.self_loops_removed = rep.self_loops_removed
+        report.duplicate_entries_removed = rep.duplicate_entries_removed
+    return Graph(h.value, device)
+
+
+def graph_from_csr(row_offsets, neighbors, n: Optional[int] = None, num_edges: Optional[int] = None,
+                   device: int = 0) -> Graph:
+    """The trimatch::Graph(num_vertices, num_edges, row_offsets, neighbors)
+    constructor route (graph.hpp:38-39): upload an existing symmetric CSR."""
+    if n is None:
+        n = (row_offsets.size if isinstance(row_offsets, np.ndarray) else row_offsets.numel()) - 1
+    if num_edges is None:
+        num_edges = (neighbors.size if isinstance(neighbors, np.ndarray) else neighbors.numel()) // 2
+    h = C.c_void_p()
+    _check(_lib.tc_graph_from_csr(C.c_void_p(_addr(row_offsets)), C.c_void_p(_addr(neighbors)), n, num_edges,
+                                  device, C.byref(h)))
+    return Graph(h.value, device)
+
+
+def degrees(g: Graph) -> np.ndarray:
+    """trimatch::degrees (graph.hpp:75)."""
+    d = np.empty(max(g.num_vertices(), 1), np.uint32)
+    _check(_lib.tc_graph_degrees(g.handle, C.c_void_p(d.ctypes.data)))
+    return d[: g.num_vertices()]
+
+
+def count_triangles(g: Graph, opts: Optional[MatchOptions] = None) -> MatchResult:
+    """trimatch::count_triangles (matcher.hpp:128) on the GPU."""
+    opts = opts or MatchOptions()
+    o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, 1)
+    total = np.zeros(1, np.uint64)
+    pv = np.zeros(max(g.num_vertices(), 1), np.uint64) if opts.per_vertex else None
+    st = TcCountStats()
+    _check(_lib.tc_count(g.handle, C.byref(o), C.c_void_p(total.ctypes.data),
+                         C.c_void_p(pv.ctypes.data) if pv is not None else None, C.byref(st)))
+    return MatchResult(count=int(total[0]), per_vertex=(pv[: g.num_vertices()] if pv is not None else None),
+                       stats=st.as_dict())
+
+
+def count_triangles_into(g: Graph, total_ptr, per_vertex_ptr=None, opts: Optional[MatchOptions] = None,
+                         stats: bool = False, sync: bool = False):
+    """Low-level: outputs to caller buffers (device tensors for the multi-GPU
+    allreduce path).  Returns the stats dict when stats=True."""
+    opts = opts or MatchOptions()
+    o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, int(sync))
+    st = TcCountStats()
+    _check(_lib.tc_count(g.handle, C.byref(o), C.c_void_p(_addr(total_ptr)),
+                         C.c_void_p(_addr(per_vertex_ptr)) if per_vertex_ptr is not None else None,
+                         C.byref(st) if stats else None))
+    return st.as_dict() if stats else None
+
+
+def parse_matrix_market(text) -> EdgeList:
+    """trimatch::parse_matrix_market (io.hpp:34, io.cpp:93-159)."""
+    if isinstance(text, str):
+        text = text.encode()
+    p = u32p()
+    m = C.c_uint64()
+    n = C.c_uint32()
+    _check(_lib.tc_parse_matrix_market(text, len(text), C.byref(p), C.byref(m), C.byref(n)))
+    arr = np.ctypeslib.as_array(p, shape=(2 * m.value + 2,))[: 2 * m.value].copy()
+    _lib.tc_free(p)
+    return EdgeList(n.value, arr.reshape(-1, 2))
+
+
+def parse_matrix_market_file(path: str) -> EdgeList:
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise IoError(f"cannot open '{path}' for reading")
+    return parse_matrix_market(data)
+
+
+_CSR_MAGIC = b"TRIMCSR1"
+
+
+def is_csr_cache_file(path: str) -> bool:
+    try:
+        with open(path, "rb") as f:
+            return f.read(8) == _CSR_MAGIC
+    except OSError:
+        return False
+
+
+def read_csr_cache(path: str, device: int = 0) -> Graph:
+    """trimatch::read_csr_cache (io.cpp:187-220): validated on ingest."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise IoError(f"cannot open '{path}' for reading")
+    h = C.c_void_p()
+    _check(_lib.tc_csr_cache_to_graph(data, len(data), device, C.byref(h)))
+    return Graph(h.value, device)
+
+
+def write_csr_cache(path: str, g: Graph) -> None:
+    """trimatch::write_csr_cache (io.cpp:167-177): little-endian TRIMCSR1 v1."""
+    ro, nb = g.export_csr()
+    try:
+        with open(path, "wb") as f:
+            f.write(_CSR_MAGIC)
+            f.write(np.array([1, g.num_vertices(), g.num_edges()], dtype="<u8").tobytes())
+            f.write(ro.astype("<u8").tobytes())
+            f.write(nb.astype("<u4").tobytes())
+    except OSError:
+        raise IoError(f"cannot open '{path}' for writing")
+
+
+def load_graph(path: str, report: Optional[BuildReport] = None, device: int = 0) -> Graph:
+    """trimatch::load_graph (io.cpp:222-228): TRIMCSR1 or MatrixMarket."""
+    if is_csr_cache_file(path):
+        if report is not None:
+            report.self_loops_removed = 0
+            report.duplicate_entries_removed = 0
+        return read_csr_cache(path, device)
+    return build_graph(parse_matrix_market_file(path), report, device)
+
+
+# ---- synthetic inputs --------------------------------------------
+
+GEN_RMAT, GEN_KRON, GEN_ER = 0, 1, 2
+
+
+def gen_num_edges(kind: int, scale: int, param: int) -> int:
+    return _lib.tc_gen_num_edges(kind, scale, param)
+
+
+def generate(kind: int, scale: int, param: int, out=None, device: int = 0):
+    """Deterministic RMAT / Kronecker / ER edge list generated on the GPU into
+    `out` (host numpy or device tensor of 2m uint32); returns it."""
+    m = gen_num_edges(kind, scale, param)
+    if out is None:
+        out = np.empty(2 * m, np.uint32)
+    _check(_lib.tc_generate(kind, scale, param, device, C.c_void_p(_addr(out))))
+    return out
+
+
+def abi_version() -> int:
+    return _lib.tc_abi_version()

@@ -1,0 +1,333 @@
+// capi.cu -- the extern "C" boundary of libtcb200.so (include/tcb200.h).
+// Every entry point catches library errors and maps them to tc_status; no
+// C++ exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "graph.cuh"
+#include "io_host.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tc_status set_error(tc_status c, const std::string& m) {
+  g_last_error = m;
+  return c;
+}
+
+#define TC_API_TRY try {
+#define TC_API_CATCH                                                        \
+  }                                                                         \
+  catch (const tcb::Error& e) {                                             \
+    return set_error(e.code, e.what());                                     \
+  }                                                                         \
+  catch (const tcb::IoFail& e) {                                            \
+    return set_error(e.code, e.what());                                     \
+  }                                                                         \
+  catch (const std::bad_alloc&) {                                           \
+    return set_error(TC_ENOMEM, "host allocation failed");                  \
+  }                                                                         \
+  catch (const std::exception& e) {                                         \
+    return set_error(TC_ECUDA, e.what());                                   \
+  }
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Input view: a device pointer as-is, or a host buffer staged to the device.
+template <typename T>
+struct DevIn {
+  const T* p = nullptr;
+  tcb::DBuf<T> staged;
+  DevIn(const T* src, uint64_t count, cudaStream_t s) {
+    if (count == 0 || is_device_ptr(src)) {
+      p = src;
+      return;
+    }
+    staged.alloc(count, s);
+    TC_CUDA(cudaMemcpyAsync(staged.get(), src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    p = staged.get();
+  }
+};
+
+// Output view: a device pointer as-is, or a device temporary copied back to
+// the host buffer by finish().
+template <typename T>
+struct DevOut {
+  T* host = nullptr;
+  T* p = nullptr;
+  uint64_t count = 0;
+  tcb::DBuf<T> tmp;
+  DevOut(T* dst, uint64_t cnt, cudaStream_t s) : count(cnt) {
+    if (!dst) return;
+    if (is_device_ptr(dst)) {
+      p = dst;
+    } else {
+      host = dst;
+      tmp.alloc(cnt ? cnt : 1, s);
+      p = tmp.get();
+    }
+  }
+  void finish(cudaStream_t s) {
+    if (host && count) TC_CUDA(cudaMemcpyAsync(host, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    TC_CUDA(cudaGetDevice(&prev));
+    TC_CUDA(cudaSetDevice(dev));
+    // let the stream-ordered pool keep freed blocks for the next call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+tc_graph* new_handle(int device) {
+  auto* g = new tc_graph();
+  g->device = device;
+  TC_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+  g->stream = g->own_stream;
+  return g;
+}
+
+void destroy_handle(tc_graph* g) {
+  if (!g) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(g->device);
+  {
+    cudaStream_t s = g->stream;
+    g->off.release();
+    g->col.release();
+    g->src.release();
+    g->deg.release();
+    g->id_of.release();
+    g->rank_of.release();
+    cudaStreamSynchronize(s);
+  }
+  if (g->own_stream) cudaStreamDestroy(g->own_stream);
+  delete g;
+  cudaSetDevice(prev);
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    TC_CUDA(cudaEventCreate(&a));
+    TC_CUDA(cudaEventCreate(&b));
+    TC_CUDA(cudaEventRecord(a, s));
+  }
+  double stop() {
+    TC_CUDA(cudaEventRecord(b, s));
+    TC_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int tc_abi_version(void) { return TCB200_ABI_VERSION; }
+
+const char* tc_last_error(void) { return g_last_error.c_str(); }
+
+void tc_free(void* p) { std::free(p); }
+
+tc_status tc_graph_build(const uint32_t* pairs, uint64_t m, uint32_t n_declared, int device, tc_graph** out,
+                         tc_build_report* report) {
+  if (!out) return set_error(TC_EINVAL, "tc_graph_build: out is NULL");
+  if (m && !pairs) return set_error(TC_EINVAL, "tc_graph_build: pairs is NULL");
+  tc_graph* g = nullptr;
+  TC_API_TRY
+  DeviceGuard dg(device);
+  g = new_handle(device);
+  try {
+    Timer t(g->stream);
+    DevIn<uint32_t> in(pairs, 2 * m, g->stream);
+    tc_build_report rep{};
+    tcb::build_from_pairs(*g, in.p, m, n_declared, &rep);
+    g->build_ms = t.stop();
+    if (report) *report = rep;
+  } catch (...) {
+    destroy_handle(g);
+    throw;
+  }
+  *out = g;
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbors, uint32_t n,
+                            uint64_t num_edges, int device, tc_graph** out) {
+  if (!out) return set_error(TC_EINVAL, "tc_graph_from_csr: out is NULL");
+  if (!row_offsets || (num_edges && !neighbors)) return set_error(TC_EINVAL, "tc_graph_from_csr: NULL array");
+  tc_graph* g = nullptr;
+  TC_API_TRY
+  DeviceGuard dg(device);
+  g = new_handle(device);
+  try {
+    Timer t(g->stream);
+    DevIn<uint64_t> off(row_offsets, (uint64_t)n + 1, g->stream);
+    DevIn<uint32_t> nb(neighbors, 2 * num_edges, g->stream);
+    tcb::build_from_csr(*g, off.p, nb.p, n, num_edges);
+    g->build_ms = t.stop();
+  } catch (...) {
+    destroy_handle(g);
+    throw;
+  }
+  *out = g;
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info) {
+  if (!g || !info) return set_error(TC_EINVAL, "tc_graph_get_info: NULL argument");
+  info->num_vertices = g->n;
+  info->num_edges = g->E;
+  info->max_degree = g->max_deg;
+  info->max_out_degree = g->max_dplus;
+  info->device = g->device;
+  info->build_ms = g->build_ms;
+  return TC_OK;
+}
+
+tc_status tc_graph_export_csr(tc_graph* g, uint64_t* row_offsets, uint32_t* neighbors) {
+  if (!g || !row_offsets || (g->E && !neighbors)) return set_error(TC_EINVAL, "tc_graph_export_csr: NULL argument");
+  TC_API_TRY
+  DeviceGuard dg(g->device);
+  DevOut<uint64_t> off(row_offsets, (uint64_t)g->n + 1, g->stream);
+  DevOut<uint32_t> nb(neighbors, 2 * g->E, g->stream);
+  tcb::export_csr(*g, off.p, nb.p);
+  off.finish(g->stream);
+  nb.finish(g->stream);
+  TC_CUDA(cudaStreamSynchronize(g->stream));
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_graph_degrees(tc_graph* g, uint32_t* degrees) {
+  if (!g || (g->n && !degrees)) return set_error(TC_EINVAL, "tc_graph_degrees: NULL argument");
+  TC_API_TRY
+  DeviceGuard dg(g->device);
+  DevOut<uint32_t> d(degrees, g->n, g->stream);
+  tcb::export_degrees(*g, d.p);
+  d.finish(g->stream);
+  TC_CUDA(cudaStreamSynchronize(g->stream));
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_graph_set_stream(tc_graph* g, void* stream) {
+  if (!g) return set_error(TC_EINVAL, "tc_graph_set_stream: NULL graph");
+  g->stream = stream ? static_cast<cudaStream_t>(stream) : g->own_stream;
+  return TC_OK;
+}
+
+void tc_graph_destroy(tc_graph* g) { destroy_handle(g); }
+
+tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint64_t* per_vertex,
+                   tc_count_stats* stats) {
+  if (!g || !total) return set_error(TC_EINVAL, "tc_count: NULL argument");
+  tc_count_opts o{};
+  if (opts) o = *opts;
+  if (o.lookahead < 0 || o.lookahead > 2) return set_error(TC_EINVAL, "lookahead must be 0, 1, or 2");
+  if (o.keep_listings) return set_error(TC_EUNSUPPORTED, "keep_listings is not supported on the GPU path");
+  if (o.part_count > 1 && o.part_index >= o.part_count)
+    return set_error(TC_EINVAL, "tc_count: part_index must be < part_count");
+  TC_API_TRY
+  DeviceGuard dg(g->device);
+  DevOut<uint64_t> t(total, 1, g->stream);
+  DevOut<uint64_t> pv(per_vertex, g->n, g->stream);
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  tcb::count_triangles(*g, o, t.p, per_vertex ? pv.p : nullptr, stats);
+  t.finish(g->stream);
+  pv.finish(g->stream);
+  if (o.sync || t.host || pv.host || stats) TC_CUDA(cudaStreamSynchronize(g->stream));
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_parse_matrix_market(const char* text, uint64_t len, uint32_t** pairs, uint64_t* m,
+                                 uint32_t* n_declared) {
+  if (!pairs || !m || !n_declared || (len && !text)) return set_error(TC_EINVAL, "tc_parse_matrix_market: NULL argument");
+  TC_API_TRY
+  std::vector<uint32_t> v;
+  uint32_t n = 0;
+  tcb::parse_matrix_market(text, len, v, n);
+  uint32_t* p = static_cast<uint32_t*>(std::malloc(v.size() * sizeof(uint32_t) + 8));
+  if (!p) return set_error(TC_ENOMEM, "host allocation failed");
+  if (!v.empty()) std::memcpy(p, v.data(), v.size() * sizeof(uint32_t));
+  *pairs = p;
+  *m = v.size() / 2;
+  *n_declared = n;
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_graph** out) {
+  if (!out || (len && !bytes)) return set_error(TC_EINVAL, "tc_csr_cache_to_graph: NULL argument");
+  TC_API_TRY
+  std::vector<uint64_t> aligned;
+  const void* b = bytes;
+  if (reinterpret_cast<uintptr_t>(bytes) & 7) {
+    aligned.resize(len / 8 + 1);
+    std::memcpy(aligned.data(), bytes, len);
+    b = aligned.data();
+  }
+  tcb::CsrView v;
+  tcb::parse_csr_cache(b, len, v);
+  return tc_graph_from_csr(v.offsets, v.nbrs, v.n, v.num_edges, device, out);
+  TC_API_CATCH
+}
+
+uint64_t tc_gen_num_edges(int kind, int scale, int param) { return tcb::gen_num_edges(kind, scale, param); }
+
+tc_status tc_generate(int kind, int scale, int param, int device, uint32_t* pairs) {
+  if (!pairs) return set_error(TC_EINVAL, "tc_generate: pairs is NULL");
+  TC_API_TRY
+  DeviceGuard dg(device);
+  const uint64_t m = tcb::gen_num_edges(kind, scale, param);
+  cudaStream_t s;
+  TC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  try {
+    DevOut<uint32_t> out(pairs, 2 * m, s);
+    tcb::generate(kind, scale, param, out.p, s);
+    out.finish(s);
+    TC_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  cudaStreamDestroy(s);
+  return TC_OK;
+  TC_API_CATCH
+}
+
+}  // extern "C"

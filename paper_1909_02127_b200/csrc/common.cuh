@@ -1,0 +1,107 @@
+// common.cuh -- shared host/device plumbing for libtcb200.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/tcb200.h"
+
+namespace tcb {
+
+// Library-internal error; converted to a tc_status at the C boundary.
+struct Error : std::runtime_error {
+  tc_status code;
+  Error(tc_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(tc_status c, const std::string& m) { throw Error(c, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    const tc_status c = (e == cudaErrorMemoryAllocation) ? TC_ENOMEM : TC_ECUDA;
+    fail(c, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                std::to_string(line) + ")");
+  }
+}
+#define TC_CUDA(x) ::tcb::cuda_check((x), #x, __FILE__, __LINE__)
+#define TC_LAUNCH() ::tcb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Stream-ordered device buffer (cudaMallocAsync from the device's default
+// mempool, whose release threshold we raise so repeated calls reuse memory).
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) TC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T) + 64, st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  T* get() const { return p; }
+  operator T*() const { return p; }
+};
+
+inline unsigned ceil_div(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
+inline uint64_t ceil_div64(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+inline int bits_for(uint64_t max_value) {  // bits needed to represent values <= max_value
+  int b = 0;
+  while (b < 64 && (max_value >> b) != 0) ++b;
+  return b;
+}
+
+int num_sms(int device);
+
+// ---- device helpers -------------------------------------------------------
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (unsigned)o) v += t;
+  }
+  return v;
+}
+
+}  // namespace tcb

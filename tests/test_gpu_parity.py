@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+vectors and the oracle, bit-exact (integer work: no tolerance)."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _pairs(case):
+    return np.array(case.get("pairs", case.get("edges", [])), dtype=np.uint32).reshape(-1)
+
+
+def _count(tc, g, pv=True):
+    r = tc.count_triangles(g, tc.MatchOptions(per_vertex=pv))
+    return r
+
+
+def test_known_answers(tc, cuda_ok):
+    for name, c in load_golden("known.json").items():
+        if name.startswith("_"):
+            continue
+        rep = tc.BuildReport()
+        g = tc.build_graph(tc.EdgeList(c["n"], _pairs(c)), rep)
+        assert g.num_edges() == c["E"], name
+        assert (rep.self_loops_removed, rep.duplicate_entries_removed) == (c["loops"], c["dups"]), name
+        r = _count(tc, g, pv=not c.get("skip_ref_csr"))
+        assert r.count == c["T"], name
+        if c.get("skip_ref_csr"):
+            continue
+        assert r.per_vertex.tolist() == c["per_vertex"], name
+        ro, nb = g.export_csr()
+        assert ro.tolist() == c["offsets"], name
+        assert nb.tolist() == c["nbrs"], name
+        assert tc.degrees(g).tolist() == np.diff(np.array(c["offsets"], np.int64)).tolist(), name
+
+
+def test_high_ids_and_huge_declared_n(tc, cuda_ok):
+    c = load_golden("known.json")["K3_high_ids"]
+    g = tc.build_graph(tc.EdgeList(c["n"], _pairs(c)))
+    assert g.num_vertices() == 0xFFFFFFFF and g.num_edges() == 3
+    assert tc.count_triangles(g).count == 1
+
+
+def test_errors(tc, cuda_ok):
+    with pytest.raises(tc.InvalidArgument):
+        tc.build_graph(tc.EdgeList(3, np.array([[0, 5]], np.uint32)))
+    with pytest.raises(tc.InvalidArgument):
+        tc.build_graph(tc.EdgeList(0, np.array([[0, 0]], np.uint32)))
+    g = tc.build_graph(tc.EdgeList(3, np.array([[0, 1], [1, 2], [0, 2]], np.uint32)))
+    with pytest.raises(tc.InvalidArgument):
+        tc.count_triangles(g, tc.MatchOptions(lookahead=3))
+    with pytest.raises(tc.Unsupported):
+        tc.count_triangles(g, tc.MatchOptions(keep_listings=True))
+    with pytest.raises(IndexError):
+        g.has_edge(0, 3)
+    assert g.has_edge(0, 2) and not g.has_edge(0, 0)
+    for la in (0, 1, 2):
+        assert tc.count_triangles(g, tc.MatchOptions(lookahead=la)).count == 1
+
+
+def test_gnp_golden(tc, cuda_ok):
+    for i, c in enumerate(load_golden("gnp.json")):
+        rep = tc.BuildReport()
+        g = tc.build_graph(tc.EdgeList(c["n"], _pairs(c)), rep)
+        assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == \
+            (c["E"], c["loops"], c["dups"]), i
+        r = _count(tc, g)
+        assert r.count == c["T"], i
+        assert r.per_vertex.tolist() == c["per_vertex"], i
+
+
+def test_gnp_500_vs_oracle(tc, oracle, cuda_ok):
+    rng = np.random.default_rng(7)
+    for i in range(510):
+        n = int(rng.integers(20, 201))
+        p = (0.02, 0.1, 0.3)[i % 3]
+        iu, ju = np.triu_indices(n, 1)
+        keep = rng.random(iu.size) < p
+        pairs = np.stack([iu[keep], ju[keep]], 1).astype(np.uint32).reshape(-1)
+        off, nb, E, _, _ = oracle.build_graph(pairs, n)
+        T, pv = oracle.count(off, nb, per_vertex=True)
+        g = tc.build_graph_from_pairs(pairs, n)
+        r = _count(tc, g)
+        assert r.count == T and np.array_equal(r.per_vertex, pv), i
+        # the Graph-ctor route (count_triangles(const Graph&))
+        g2 = tc.graph_from_csr(off, nb)
+        assert tc.count_triangles(g2).count == T, i
+
+
+def test_build_graph_csr_parity_random(tc, oracle, cuda_ok):
+    rng = np.random.default_rng(3)
+    for i in range(60):
+        n = int(rng.integers(1, 3000))
+        m = int(rng.integers(0, 20 * n))
+        pairs = rng.integers(0, n, 2 * m).astype(np.uint32)
+        if m and i % 3 == 0:  # heavy duplication + loops
+            pairs[: m // 2] = pairs[0]
+        off, nb, E, lo, du = oracle.build_graph(pairs, n)
+        rep = tc.BuildReport()
+        g = tc.build_graph_from_pairs(pairs, n, rep)
+        assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == (E, lo, du)
+        ro, nbr = g.export_csr()
+        assert np.array_equal(ro, off) and np.array_equal(nbr, nb), i
+
+
+def _stress_graphs():
+    # hubs / cliques: force every bin, large tables and the global-table path
+    out = {}
+    n = 4000
+    star = np.array([[0, i] for i in range(1, n)], np.uint32)
+    ring = np.array([[i, i + 1] for i in range(1, n - 1)], np.uint32)
+    out["wheel"] = (n, np.concatenate([star, ring]))
+    k = 300
+    iu, ju = np.triu_indices(k, 1)
+    out["K300"] = (k, np.stack([iu, ju], 1).astype(np.uint32))
+    rng = np.random.default_rng(5)
+    # dense core (large d+) + sparse fringe attached to it
+    core = 1200
+    iu, ju = np.triu_indices(core, 1)
+    keep = rng.random(iu.size) < 0.5
+    dense = np.stack([iu[keep], ju[keep]], 1)
+    fringe = np.stack([rng.integers(core, 60000, 200000), rng.integers(0, core, 200000)], 1)
+    out["core_fringe"] = (60000, np.concatenate([dense, fringe]).astype(np.uint32))
+    return out
+
+
+@pytest.mark.parametrize("name", ["wheel", "K300", "core_fringe"])
+def test_stress_bins(tc, oracle, cuda_ok, name):
+    n, e = _stress_graphs()[name]
+    pairs = e.reshape(-1)
+    off, nb, E, _, _ = oracle.build_graph(pairs, n)
+    T, pv = oracle.count(off, nb, per_vertex=True)
+    g = tc.build_graph_from_pairs(pairs, n)
+    r = _count(tc, g)
+    assert r.count == T and np.array_equal(r.per_vertex, pv)
+    assert tc.count_triangles(g, tc.MatchOptions(per_vertex=False)).count == T
+
+
+def test_large_clique_global_table(tc, cuda_ok):
+    # K_k: d+ up to k-1; k=24000 needs a 64K-slot table -> the per-CTA global slab
+    k = 24000
+    iu, ju = np.triu_indices(k, 1)
+    pairs = np.stack([iu, ju], 1).astype(np.uint32).reshape(-1)
+    g = tc.build_graph_from_pairs(pairs, k)
+    T = k * (k - 1) * (k - 2) // 6
+    r = _count(tc, g)
+    assert r.count == T
+    assert np.all(r.per_vertex == (k - 1) * (k - 2) // 2)
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_parts_sum_to_total(tc, oracle, cuda_ok, parts):
+    c = load_golden("synthetic.json")["C1_rmat_s16_ef16"]
+    pairs = tc.generate(tc.GEN_RMAT, 16, 16)
+    g = tc.build_graph_from_pairs(pairs, c["n"])
+    tot = 0
+    pv = np.zeros(c["n"], np.uint64)
+    for p in range(parts):
+        r = tc.count_triangles(g, tc.MatchOptions(per_vertex=True, part_index=p, part_count=parts))
+        tot += r.count
+        pv += r.per_vertex
+    assert tot == c["T"]
+    assert oracle.fnv(pv) == c["pv_fnv"]
+
+
+SYN = ["C1_rmat_s16_ef16", "C2_er_s20_d32", "rmat_s18_ef16", "kron_s18_ef16", "rmat_s20_ef16"]
+
+
+@pytest.mark.parametrize("name", SYN)
+def test_synthetic_golden(tc, oracle, cuda_ok, name):
+    c = load_golden("synthetic.json")[name]
+    kind = tc.GEN_ER if c["kind"] == "er" else (tc.GEN_KRON if c["permute"] else tc.GEN_RMAT)
+    pairs = tc.generate(kind, c["scale"], c["edgefactor"])
+    assert oracle.fnv(pairs) == c["pairs_fnv"]
+    rep = tc.BuildReport()
+    g = tc.build_graph_from_pairs(pairs, c["n"], rep)
+    assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == (c["E"], c["loops"], c["dups"])
+    r = _count(tc, g)
+    assert r.count == c["T"]
+    assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+    assert int(r.per_vertex.sum()) == 3 * c["T"] == c["pv_sum"]
+    ro, nb = g.export_csr()
+    assert oracle.fnv(ro) == c["offsets_fnv"] and oracle.fnv(nb) == c["nbrs_fnv"]
+    # Graph-ctor route from the exported CSR gives the same answer
+    g2 = tc.graph_from_csr(ro, nb)
+    assert tc.count_triangles(g2).count == c["T"]
+
+
+def test_device_resident_inputs(tc, cuda_ok):
+    import torch
+    c = load_golden("synthetic.json")["C2_er_s20_d32"]
+    m = tc.gen_num_edges(tc.GEN_ER, 20, 32)
+    d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+    tc.generate(tc.GEN_ER, 20, 32, out=d)
+    g = tc.build_graph_from_pairs(d, c["n"], m=m)
+    total = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pv = torch.zeros(c["n"], dtype=torch.int64, device="cuda")
+    tc.count_triangles_into(g, total, pv, tc.MatchOptions(per_vertex=True), sync=True)
+    assert int(total.item()) == c["T"]
+    assert int(pv.sum().item()) == 3 * c["T"]
+
+
+def test_csr_cache_roundtrip(tc, tmp_path, cuda_ok):
+    c = load_golden("known.json")["two_K4_share_edge"]
+    g = tc.build_graph(tc.EdgeList(c["n"], _pairs(c)))
+    p = str(tmp_path / "g.trimcsr")
+    tc.write_csr_cache(p, g)
+    g2 = tc.load_graph(p)
+    assert g2.num_edges() == c["E"] and tc.count_triangles(g2).count == c["T"]
+    mm = tmp_path / "g.mtx"
+    mm.write_text("%%MatrixMarket matrix coordinate pattern general\n6 6 3\n1 2\n2 3\n3 1\n")
+    rep = tc.BuildReport()
+    g3 = tc.load_graph(str(mm), rep)
+    assert tc.count_triangles(g3).count == 1
+
+
+@pytest.mark.slow
+def test_c3_kron_s22(tc, oracle, cuda_ok):
+    syn = load_golden("synthetic.json")
+    if "C3_kron_s22_ef16" not in syn:
+        pytest.skip("C3 golden not generated")
+    c = syn["C3_kron_s22_ef16"]
+    import torch
+    m = tc.gen_num_edges(tc.GEN_KRON, 22, 16)
+    d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+    tc.generate(tc.GEN_KRON, 22, 16, out=d)
+    rep = tc.BuildReport()
+    g = tc.build_graph_from_pairs(d, c["n"], rep, m=m)
+    assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == (c["E"], c["loops"], c["dups"])
+    r = _count(tc, g)
+    assert r.count == c["T"]
+    assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+
+
+@pytest.mark.slow
+def test_c4_rmat_s24(tc, oracle, cuda_ok):
+    syn = load_golden("synthetic.json")
+    if "C4_rmat_s24_ef16" not in syn:
+        pytest.skip("C4 golden not generated")
+    c = syn["C4_rmat_s24_ef16"]
+    import torch
+    m = tc.gen_num_edges(tc.GEN_RMAT, 24, 16)
+    d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+    tc.generate(tc.GEN_RMAT, 24, 16, out=d)
+    rep = tc.BuildReport()
+    g = tc.build_graph_from_pairs(d, c["n"], rep, m=m)
+    del d
+    assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == (c["E"], c["loops"], c["dups"])
+    r = _count(tc, g)
+    assert r.count == c["T"] == 10282799137
+    assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+    assert int(r.per_vertex.sum()) == 3 * c["T"]
