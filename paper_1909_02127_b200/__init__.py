@@ -221,8 +221,11 @@ class Graph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _lib.tc_graph_destroy(h)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.tc_graph_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = C.c_void_p(0)
 
     @property

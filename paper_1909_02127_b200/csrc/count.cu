@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "graph.cuh"
 #include "prim.cuh"
@@ -44,8 +45,9 @@ constexpr uint32_t kWarpMaxDeg = 48;   // warp bin: d+(v) <= 48 -> 128-slot tabl
 constexpr uint32_t kWarpTable = 128;
 constexpr uint32_t kWarpSegItems = 64;  // items per warp segment
 constexpr uint32_t kCtaSegItems = 512;  // items per CTA segment
-
-__device__ __forceinline__ uint32_t hash_slot(uint32_t x, uint32_t mask) { return x & mask; }
+constexpr uint32_t kTopBitmapBits = 1u << 17;  // membership bitmap window (16 KB)
+constexpr uint32_t kTopCounters = 1u << 13;    // per-vertex SMEM counter window (32 KB)
+constexpr size_t kSmemMax = 200 * 1024;
 
 __host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t dplus) {
   // load factor <= 1/2, at least 32 slots
@@ -62,19 +64,29 @@ struct FrontierSums {
   unsigned long long items;  // useful items
 };
 
+// Wedge work of oriented edge e = u->v as a pivot in-edge: the suffix of
+// N+(u) after v, when v can close triangles (d+(v) > 0).
+__device__ __forceinline__ uint32_t edge_work(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                                              const uint32_t* __restrict__ src, uint64_t e, uint32_t& v,
+                                              uint32_t& end) {
+  v = col[e];
+  const uint32_t dv = off[v + 1] - off[v];
+  end = off[src[e] + 1];
+  return (dv > 0 && e + 1 < end) ? end - (uint32_t)(e + 1) : 0u;
+}
+
 __global__ void k_item_count(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                             const uint32_t* __restrict__ src, uint64_t E, uint32_t* __restrict__ cnt,
-                             FrontierSums* __restrict__ sums) {
+                             const uint32_t* __restrict__ src, uint64_t e0, uint64_t e1,
+                             uint32_t* __restrict__ cnt, FrontierSums* __restrict__ sums) {
   unsigned long long W = 0, J = 0, I = 0;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = col[e];
-    const uint32_t dv = off[v + 1] - off[v];
-    const uint32_t end = off[src[e] + 1];
-    W += dv;
-    if (dv > 0 && e + 1 < end) {
+    uint32_t v, end;
+    const uint32_t w = edge_work(off, col, src, e, v, end);
+    W += off[v + 1] - off[v];
+    if (w) {
       atomicAdd(&cnt[v], 1u);
-      J += end - (e + 1);
+      J += w;
       ++I;
     }
   }
@@ -89,18 +101,47 @@ __global__ void k_item_count(const uint32_t* __restrict__ off, const uint32_t* _
 }
 
 __global__ void k_item_scatter(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                               const uint32_t* __restrict__ src, uint64_t E, const uint32_t* __restrict__ in_off,
-                               uint32_t* __restrict__ fill, uint2* __restrict__ items) {
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+                               const uint32_t* __restrict__ src, uint64_t e0, uint64_t e1,
+                               const uint32_t* __restrict__ in_off, uint32_t* __restrict__ fill,
+                               uint2* __restrict__ items) {
+  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = col[e];
-    const uint32_t dv = off[v + 1] - off[v];
-    const uint32_t end = off[src[e] + 1];
-    if (dv > 0 && e + 1 < end) {
+    uint32_t v, end;
+    if (edge_work(off, col, src, e, v, end)) {
       const uint32_t p = in_off[v] + atomicAdd(&fill[v], 1u);
       items[p] = make_uint2((uint32_t)e + 1, end);
     }
   }
+}
+
+// Multi-GPU partition: prefix of per-edge cost (wedge work + a per-item
+// overhead) over the oriented edges, then P-1 binary searches.  Contiguous
+// edge ranges = contiguous source ranges of the degree-ordered DAG: the
+// north-star "degree-weighted ranges".
+struct EdgeCost {
+  const uint32_t* off;
+  const uint32_t* col;
+  const uint32_t* src;
+  __device__ __forceinline__ uint64_t operator()(uint64_t e) const {
+    uint32_t v, end;
+    const uint32_t w = edge_work(off, col, src, e, v, end);
+    return w ? (uint64_t)w + 8 : 0ull;
+  }
+};
+
+__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint64_t E, uint64_t total, uint32_t parts,
+                              uint64_t* __restrict__ bounds) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > parts) return;
+  if (p == 0) { bounds[0] = 0; return; }
+  if (p == parts) { bounds[parts] = E; return; }
+  const uint64_t target = (uint64_t)((double)total * p / parts);
+  uint64_t lo = 0, hi = E;  // first e with prefix[e] >= target
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (prefix[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  bounds[p] = lo;
 }
 
 struct SegCount {
@@ -135,36 +176,103 @@ __global__ void k_seg_fill(const uint32_t* __restrict__ off, const uint32_t* __r
 
 // ---- the fused advance + join ---------------------------------------------
 
-// Probe x in an open-addressing table (linear probing).  Returns the slot or
-// kEmpty.
-__device__ __forceinline__ uint32_t probe(const uint32_t* tab, uint32_t mask, uint32_t x) {
-  uint32_t s = hash_slot(x, mask);
+// Multiplicative (Fibonacci) hashing: scatters runs of consecutive ranks, so
+// linear-probe clusters stay short (identity hashing of the dense top-rank
+// runs produced long, divergent probe chains -- profiles/README.md).
+__device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t shift) { return (x * 0x9E3779B1u) >> shift; }
+
+__device__ __forceinline__ bool hash_find(const uint32_t* tab, uint32_t mask, uint32_t shift, uint32_t x) {
+  uint32_t s = hslot(x, shift);
   while (true) {
     const uint32_t k = tab[s];
-    if (k == x) return s;
-    if (k == kEmpty) return kEmpty;
+    if (k == x) return true;
+    if (k == kEmpty) return false;
     s = (s + 1) & mask;
   }
 }
 
-__device__ __forceinline__ void insert(uint32_t* tab, uint32_t mask, uint32_t x) {
-  uint32_t s = hash_slot(x, mask);
+__device__ __forceinline__ void hash_insert(uint32_t* tab, uint32_t mask, uint32_t shift, uint32_t x) {
+  uint32_t s = hslot(x, shift);
   while (atomicCAS(&tab[s], kEmpty, x) != kEmpty) s = (s + 1) & mask;
 }
 
-// One warp processes items [i0, i1) of pivot v against the table `tab`.
-// Advance: items -> 16-byte chunks of their suffixes, load-balanced across
-// lanes; join: each element x in the item's [b,e) is probed.  Returns the
-// lane's hit count; per-vertex updates go to slot counters (t[c]), per-item
-// counters (t[a]).
+__host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
+  uint32_t l = 0;
+  while ((1u << l) < ts) ++l;
+  return l;
+}
+
+// Membership test for N+(v) (the closing edge v->x of wedge (u; v, x)):
+// a bitmap over the top-rank window [r0, n) -- where ~all wedge endpoints of
+// a power-law DAG land, and where neighbouring lanes probe neighbouring
+// words -- plus an open-addressing hash for the members below r0.
+struct PivotSet {
+  const uint32_t* bm;
+  const uint32_t* tab;
+  uint32_t r0, mask, shift;
+  __device__ __forceinline__ bool contains(uint32_t x) const {
+    if (x >= r0) {
+      const uint32_t d = x - r0;
+      return (bm[d >> 5] >> (d & 31)) & 1u;
+    }
+    return hash_find(tab, mask, shift, x);
+  }
+};
+
+// Per-vertex hits t[x]: SMEM counters for the top window [rc, n) (flushed
+// once per CTA), global atomics below it.
+struct PvSink {
+  uint32_t* top;
+  uint32_t rc;
+  unsigned long long* t_rank;
+  __device__ __forceinline__ void hit(uint32_t x) const {
+    if (x >= rc) atomicAdd(&top[x - rc], 1u);
+    else atomicAdd(&t_rank[x], 1ull);
+  }
+};
+
+// Locate, for chunk window [w, w+32), the item each lane's chunk w+lane
+// belongs to (items hold >= 1 chunk; start/pre are the lane's item's
+// exclusive/inclusive chunk prefix).
+__device__ __forceinline__ uint32_t item_of(uint32_t w, uint32_t nch, uint32_t pre, uint32_t start) {
+  const unsigned lane = lane_id();
+  const uint32_t kb = __popc(__ballot_sync(0xffffffffu, nch && pre <= w));
+  const uint32_t bit = (nch && start > w && start < w + 32) ? (1u << (start - w)) : 0u;
+  const uint32_t smask = __reduce_or_sync(0xffffffffu, bit);
+  const uint32_t k = kb + __popc(smask & ((2u << lane) - 1u));
+  return k < 32 ? k : 31;
+}
+
+template <bool kPerVertex>
+__device__ __forceinline__ uint32_t probe_chunk(const uint4 q, uint32_t c, uint32_t bk, uint32_t ek,
+                                                const PivotSet& set, const PvSink& sink) {
+  const uint32_t xs[4] = {q.x, q.y, q.z, q.w};
+  const uint32_t p0 = c << 2;
+  uint32_t h = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t p = p0 + t;
+    if (p >= bk && p < ek && set.contains(xs[t])) {
+      ++h;
+      if (kPerVertex) sink.hit(xs[t]);
+    }
+  }
+  return h;
+}
+
+// Advance + join for items [i0, i1) of one pivot, executed by one warp.
+// Advance: the items' suffixes are cut into 16-byte chunks and load-balanced
+// across lanes (two chunks per lane per step, both int4 loads in flight before
+// any probe).  Join: every wedge endpoint x in [b,e) is tested against N+(v).
+// Returns the lane's hit count; per-vertex: t[x] via the sink, t[u] via
+// per-item SMEM counters (one global atomic per item).
 template <bool kPerVertex>
 __device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ items, uint32_t i0, uint32_t i1,
                                                     const uint32_t* __restrict__ col,
-                                                    const uint32_t* __restrict__ src, const uint32_t* tab,
-                                                    uint32_t* slot_cnt, uint32_t mask, uint32_t xmax,
-                                                    uint32_t* item_cnt /* 32 per warp, smem */,
-                                                    unsigned long long* __restrict__ t_rank) {
+                                                    const uint32_t* __restrict__ src, const PivotSet& set,
+                                                    const PvSink& sink, uint32_t* item_cnt) {
   const unsigned lane = lane_id();
+  const uint4* col4 = reinterpret_cast<const uint4*>(col);
   uint32_t hits = 0;
   for (uint32_t ib = i0; ib < i1; ib += 32) {
     const uint32_t my = ib + lane;
@@ -175,50 +283,40 @@ __device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ it
       e = it.y;
       nch = ((e + 3) >> 2) - (b >> 2);
     }
-    const uint32_t pre = warp_inclusive_scan(nch);  // inclusive chunk prefix
+    const uint32_t pre = warp_inclusive_scan(nch);
     const uint32_t start = pre - nch;
     const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
     if (kPerVertex) {
       item_cnt[lane] = 0;
       __syncwarp();
     }
-    for (uint32_t base = 0; base < total; base += 32) {
-      const uint32_t f = base + lane;
-      // item containing chunk `base`: count of items ending at or before it
-      const uint32_t kb = __popc(__ballot_sync(0xffffffffu, nch && pre <= base));
-      const uint32_t bit = (nch && start > base && start < base + 32) ? (1u << (start - base)) : 0u;
-      const uint32_t smask = __reduce_or_sync(0xffffffffu, bit);
-      const uint32_t k = kb + __popc(smask & ((2u << lane) - 1u));
-      const uint32_t kk = k < 32 ? k : 31;
-      const uint32_t bk = __shfl_sync(0xffffffffu, b, kk);
-      const uint32_t ek = __shfl_sync(0xffffffffu, e, kk);
-      const uint32_t sk = __shfl_sync(0xffffffffu, start, kk);
-      if (f < total) {
-        const uint32_t c = (bk >> 2) + (f - sk);
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(col) + c);
-        const uint32_t p0 = c << 2;
-        uint32_t h = 0;
-        const uint32_t xs[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const uint32_t p = p0 + t;
-          const uint32_t x = xs[t];
-          if (p >= bk && p < ek && x <= xmax) {
-            const uint32_t s = probe(tab, mask, x);
-            if (s != kEmpty) {
-              ++h;
-              if (kPerVertex) atomicAdd(&slot_cnt[s], 1u);
-            }
-          }
-        }
+    for (uint32_t base = 0; base < total; base += 64) {
+      const uint32_t k1 = item_of(base, nch, pre, start);
+      const uint32_t k2 = item_of(base + 32, nch, pre, start);
+      const uint32_t b1 = __shfl_sync(0xffffffffu, b, k1), e1 = __shfl_sync(0xffffffffu, e, k1);
+      const uint32_t s1 = __shfl_sync(0xffffffffu, start, k1);
+      const uint32_t b2 = __shfl_sync(0xffffffffu, b, k2), e2 = __shfl_sync(0xffffffffu, e, k2);
+      const uint32_t s2 = __shfl_sync(0xffffffffu, start, k2);
+      const uint32_t f1 = base + lane, f2 = base + 32 + lane;
+      const uint32_t c1 = (b1 >> 2) + (f1 - s1), c2 = (b2 >> 2) + (f2 - s2);
+      uint4 q1 = make_uint4(0, 0, 0, 0), q2 = make_uint4(0, 0, 0, 0);
+      if (f1 < total) q1 = __ldg(col4 + c1);
+      if (f2 < total) q2 = __ldg(col4 + c2);
+      if (f1 < total) {
+        const uint32_t h = probe_chunk<kPerVertex>(q1, c1, b1, e1, set, sink);
         hits += h;
-        if (kPerVertex && h) atomicAdd(&item_cnt[k], h);
+        if (kPerVertex && h) atomicAdd(&item_cnt[k1], h);
+      }
+      if (f2 < total) {
+        const uint32_t h = probe_chunk<kPerVertex>(q2, c2, b2, e2, set, sink);
+        hits += h;
+        if (kPerVertex && h) atomicAdd(&item_cnt[k2], h);
       }
     }
     if (kPerVertex) {
       __syncwarp();
       const uint32_t c = item_cnt[lane];
-      if (c) atomicAdd(&t_rank[src[b - 1]], (unsigned long long)c);
+      if (c) atomicAdd(&sink.t_rank[src[b - 1]], (unsigned long long)c);
       __syncwarp();
     }
   }
@@ -226,146 +324,134 @@ __device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ it
 }
 
 // Warp bin: each warp takes whole segments of small pivots (d+ <= 48) with a
-// warp-private 128-slot table.
+// warp-private 128-slot hash table; the CTA shares the per-vertex top-window
+// counters (dynamic SMEM, pv only).
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
     const uint2* __restrict__ items, const uint32_t* __restrict__ in_off, const uint2* __restrict__ segs,
-    uint32_t nsegs, uint32_t seg_lo, uint32_t seg_stride, unsigned long long* __restrict__ t_rank,
+    uint32_t nsegs, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
+  extern __shared__ uint32_t top_cnt[];
   __shared__ uint32_t s_tab[kJoinWarps][kWarpTable];
-  __shared__ uint32_t s_cnt[kJoinWarps][kPerVertex ? kWarpTable : 1];
   __shared__ uint32_t s_item[kJoinWarps][32];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t* tab = s_tab[warp];
-  uint32_t* scnt = s_cnt[warp];
-  for (uint32_t s = lane; s < kWarpTable; s += 32) {
-    tab[s] = kEmpty;
-    if (kPerVertex) scnt[s] = 0;
+  for (uint32_t s = lane; s < kWarpTable; s += 32) tab[s] = kEmpty;
+  if (kPerVertex) {
+    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) top_cnt[i] = 0;
+    __syncthreads();
   }
   __syncwarp();
+  const uint32_t mask = kWarpTable - 1, shift = 32 - log2_pow2(kWarpTable);
+  const PivotSet set{nullptr, tab, 0xffffffffu, mask, shift};
+  const PvSink sink{top_cnt, rc, t_rank};
   unsigned long long acc = 0;
   const uint32_t gw = blockIdx.x * kJoinWarps + warp, nw = gridDim.x * kJoinWarps;
-  for (uint32_t si = seg_lo + gw * seg_stride; si < nsegs; si += nw * seg_stride) {
+  for (uint32_t si = gw; si < nsegs; si += nw) {
     const uint2 sg = segs[si];
     const uint32_t v = sg.x, i0 = sg.y;
     const uint32_t i1 = min(i0 + kWarpSegItems, in_off[v + 1]);
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
-    const uint32_t mask = kWarpTable - 1;
-    uint32_t xmax = 0;
-    for (uint32_t j = lane; j < dv; j += 32) {
-      const uint32_t x = col[nb + j];
-      insert(tab, mask, x);
-      xmax = max(xmax, x);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) xmax = max(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
-    const uint32_t h = warp_join_items<kPerVertex>(items, i0, i1, col, src, tab, scnt, mask, xmax,
-                                                   s_item[warp], t_rank);
+    const uint32_t h = warp_join_items<kPerVertex>(items, i0, i1, col, src, set, sink, s_item[warp]);
     __syncwarp();
-    const uint32_t hw = warp_sum(h);
     acc += h;
     if (kPerVertex) {
-      for (uint32_t s = lane; s < kWarpTable; s += 32) {
-        const uint32_t c = scnt[s];
-        if (c) {
-          atomicAdd(&t_rank[tab[s]], (unsigned long long)c);
-          scnt[s] = 0;
-        }
-        tab[s] = kEmpty;
-      }
+      const uint32_t hw = warp_sum(h);
       if (lane == 0 && hw) atomicAdd(&t_rank[v], (unsigned long long)hw);
-    } else {
-      for (uint32_t s = lane; s < kWarpTable; s += 32) tab[s] = kEmpty;
     }
+    for (uint32_t s = lane; s < kWarpTable; s += 32) tab[s] = kEmpty;
     __syncwarp();
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
+  if (kPerVertex) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) {
+      const uint32_t c = top_cnt[i];
+      if (c) atomicAdd(&t_rank[rc + i], (unsigned long long)c);
+    }
+  }
 }
 
-// CTA bin: the CTA builds the table of N+(v) once per segment (table in SMEM,
-// or in a per-CTA global slab when d+(v) is too large for SMEM), its warps
-// share it.  Segments are taken from a global queue, heaviest (top-rank
-// pivots) first.
+// CTA bin: per segment the CTA builds N+(v) once (top-window bitmap + hash,
+// in SMEM; the hash goes to a per-CTA global slab when d+(v) is too large for
+// SMEM) and its warps share it.  Segments come from a global queue, heaviest
+// (top-rank pivots) first.
+// Dynamic SMEM: [bitmap nbm words][hash cap words (SMEM table only)][pv: ncnt].
 template <bool kPerVertex, bool kGlobalTable>
 __global__ void __launch_bounds__(kJoinThreads, 2) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
     const uint2* __restrict__ items, const uint32_t* __restrict__ in_off, const uint2* __restrict__ segs,
-    uint32_t nsegs, uint32_t seg_lo, uint32_t seg_stride, unsigned int* __restrict__ queue,
-    uint32_t table_cap, uint32_t* __restrict__ gslab, unsigned long long* __restrict__ t_rank,
+    uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t r0, uint32_t nbm, uint32_t table_cap,
+    uint32_t* __restrict__ gslab, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
   __shared__ uint32_t s_item[kJoinWarps][32];
-  __shared__ uint32_t s_seg, s_xmax, s_hits;
-  uint32_t* tab = kGlobalTable ? gslab + (uint64_t)blockIdx.x * table_cap * (kPerVertex ? 2 : 1) : dyn;
-  uint32_t* scnt = tab + table_cap;
+  __shared__ uint32_t s_seg, s_hits;
+  uint32_t* bm = dyn;
+  uint32_t* tab = kGlobalTable ? gslab + (uint64_t)blockIdx.x * table_cap : dyn + nbm;
+  uint32_t* top_cnt = dyn + nbm + (kGlobalTable ? 0 : table_cap);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t s = threadIdx.x; s < table_cap; s += kJoinThreads) {
-    tab[s] = kEmpty;
-    if (kPerVertex) scnt[s] = 0;
-  }
+  for (uint32_t s = threadIdx.x; s < nbm; s += kJoinThreads) bm[s] = 0;
+  for (uint32_t s = threadIdx.x; s < table_cap; s += kJoinThreads) tab[s] = kEmpty;
+  if (kPerVertex)
+    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) top_cnt[i] = 0;
+  const PvSink sink{top_cnt, rc, t_rank};
   unsigned long long acc = 0;
   while (true) {
     if (threadIdx.x == 0) {
       s_seg = atomicAdd(queue, 1u);
-      s_xmax = 0;
       s_hits = 0;
     }
+    if (kGlobalTable) __threadfence_block();
     __syncthreads();
     const uint32_t q = s_seg;
-    const uint64_t sidx64 = (uint64_t)seg_lo + (uint64_t)q * seg_stride;
-    if (sidx64 >= nsegs) break;
-    const uint32_t si = nsegs - 1 - (uint32_t)sidx64;  // heaviest (top ranks) first
+    if (q >= nsegs) break;
+    const uint32_t si = nsegs - 1 - q;  // heaviest (top ranks) first
     const uint2 sg = segs[si];
     const uint32_t v = sg.x, i0 = sg.y;
     const uint32_t i1 = min(i0 + kCtaSegItems, in_off[v + 1]);
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     const uint32_t ts = table_size_for(dv);
-    const uint32_t mask = ts - 1;
-    uint32_t xmax = 0;
+    const uint32_t mask = ts - 1, shift = 32 - log2_pow2(ts);
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
       const uint32_t x = col[nb + j];
-      insert(tab, mask, x);
-      xmax = max(xmax, x);
+      if (x >= r0) atomicOr(&bm[(x - r0) >> 5], 1u << ((x - r0) & 31));
+      else hash_insert(tab, mask, shift, x);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) xmax = max(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
-    if (lane == 0) atomicMax(&s_xmax, xmax);
     if (kGlobalTable) __threadfence_block();
     __syncthreads();
-    xmax = s_xmax;
-    // warps take 32-item batches of the segment
+    const PivotSet set{bm, tab, r0, mask, shift};
     uint32_t h = 0;
     for (uint32_t ib = i0 + warp * 32; ib < i1; ib += kJoinWarps * 32)
-      h += warp_join_items<kPerVertex>(items, ib, min(ib + 32, i1), col, src, tab, scnt, mask, xmax,
-                                       s_item[warp], t_rank);
+      h += warp_join_items<kPerVertex>(items, ib, min(ib + 32, i1), col, src, set, sink, s_item[warp]);
     acc += h;
     if (kPerVertex) {
       const uint32_t hw = warp_sum(h);
       if (lane == 0 && hw) atomicAdd(&s_hits, hw);
     }
-    if (kGlobalTable) __threadfence_block();
     __syncthreads();
-    if (kPerVertex) {
-      for (uint32_t s = threadIdx.x; s < ts; s += kJoinThreads) {
-        const uint32_t c = scnt[s];
-        if (c) {
-          atomicAdd(&t_rank[tab[s]], (unsigned long long)c);
-          scnt[s] = 0;
-        }
-        tab[s] = kEmpty;
-      }
-      if (threadIdx.x == 0 && s_hits) atomicAdd(&t_rank[v], (unsigned long long)s_hits);
-    } else {
-      for (uint32_t s = threadIdx.x; s < ts; s += kJoinThreads) tab[s] = kEmpty;
+    for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
+      const uint32_t x = col[nb + j];
+      if (x >= r0) bm[(x - r0) >> 5] = 0;
     }
+    for (uint32_t s = threadIdx.x; s < ts; s += kJoinThreads) tab[s] = kEmpty;
+    if (kPerVertex && threadIdx.x == 0 && s_hits) atomicAdd(&t_rank[v], (unsigned long long)s_hits);
     if (kGlobalTable) __threadfence_block();
     __syncthreads();
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
+  if (kPerVertex) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) {
+      const uint32_t c = top_cnt[i];
+      if (c) atomicAdd(&t_rank[rc + i], (unsigned long long)c);
+    }
+  }
 }
 
 __global__ void k_gather_pv(const unsigned long long* __restrict__ t_rank, const uint32_t* __restrict__ rank_of,
@@ -373,6 +459,11 @@ __global__ void k_gather_pv(const unsigned long long* __restrict__ t_rank, const
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x)
     out[v] = t_rank[rank_of[v]];
+}
+
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = getenv(name);
+  return v ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
 }
 
 unsigned grid_gs(uint64_t n, int device) {
@@ -428,13 +519,34 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaMemsetAsync(t_rank.get(), 0, sizeof(unsigned long long) * (n ? n : 1), s));
   }
 
+  // ---- multi-GPU: this part's degree-weighted oriented-edge range ----
+  uint64_t e0 = 0, e1 = E;
+  if (parts > 1 && E) {
+    if (g.cached_parts != parts) {
+      DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
+      kl += scan_exclusive<uint64_t>(EdgeCost{g.off.get(), g.col.get(), g.src.get()}, prefix.get(), E, tot.get(), s);
+      const uint64_t total_cost = read_scalar(tot.get(), s);
+      k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), E, total_cost, parts, bnd.get());
+      TC_LAUNCH();
+      ++kl;
+      g.part_bounds.assign(parts + 1, 0);
+      TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, s));
+      TC_CUDA(cudaStreamSynchronize(s));
+      g.cached_parts = parts;
+    }
+    e0 = g.part_bounds[part];
+    e1 = g.part_bounds[part + 1];
+  }
+
   // ---- level-1 frontier: useful in-edges grouped by pivot ----
   DBuf<uint32_t> cnt(n ? n : 1, s), in_off((uint64_t)n + 1, s);
   DBuf<FrontierSums> sums(1, s);
   TC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
   TC_CUDA(cudaMemsetAsync(sums.get(), 0, sizeof(FrontierSums), s));
-  if (E) {
-    k_item_count<<<grid_gs(E, dev), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), E, cnt.get(), sums.get());
+  if (e1 > e0) {
+    k_item_count<<<grid_gs(e1 - e0, dev), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), e0, e1, cnt.get(),
+                                                       sums.get());
     TC_LAUNCH();
     ++kl;
   }
@@ -445,8 +557,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   if (NI) {
     DBuf<uint32_t> fill(n, s);
     TC_CUDA(cudaMemsetAsync(fill.get(), 0, sizeof(uint32_t) * n, s));
-    k_item_scatter<<<grid_gs(E, dev), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), E, in_off.get(),
-                                                   fill.get(), items.get());
+    k_item_scatter<<<grid_gs(e1 - e0, dev), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), e0, e1,
+                                                         in_off.get(), fill.get(), items.get());
     TC_LAUNCH();
     ++kl;
   }
@@ -463,7 +575,12 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaMemcpyAsync(hn, nseg.get(), 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
   }
-  const uint32_t NSW = hn[0], NSC = hn[1];
+  uint32_t NSW = hn[0], NSC = hn[1];
+  if (const char* dbg = getenv("TCB_DEBUG_BINS")) {  // diagnostics: 1 = warp bin only, 2 = CTA bin only
+    const int m = atoi(dbg);
+    if (!(m & 1)) NSW = 0;
+    if (!(m & 2)) NSC = 0;
+  }
   DBuf<uint2> wsegs(NSW ? NSW : 1, s), csegs(NSC ? NSC : 1, s);
   if (NSW) {
     k_seg_fill<<<grid_gs(n, dev), 256, 0, s>>>(g.off.get(), cnt.get(), in_off.get(), n, 1, kWarpMaxDeg,
@@ -482,47 +599,49 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   // ---- advance + join ----
   const int sms = num_sms(dev);
   uint64_t launches = 0;
+  // top-rank windows: membership bitmap [r0, n) and per-vertex counters [rc, n)
+  // (TCB_TOP_BITMAP_BITS / TCB_TOP_COUNTERS / TCB_SMEM_MAX override the window
+  // sizes so tests can drive every membership/counter path on small graphs)
+  const uint32_t top_bits = env_u32("TCB_TOP_BITMAP_BITS", kTopBitmapBits) & ~31u;
+  const uint32_t top_cnt = env_u32("TCB_TOP_COUNTERS", kTopCounters);
+  const size_t smem_max = env_u32("TCB_SMEM_MAX", (uint32_t)kSmemMax);
+  const uint32_t bm_bits = n < top_bits ? ((n + 31) & ~31u) : top_bits;
+  const uint32_t r0 = n > bm_bits ? n - bm_bits : 0;
+  const uint32_t nbm = bm_bits / 32;
+  const uint32_t ncnt = pv ? (n < top_cnt ? n : top_cnt) : 0;
+  const uint32_t rc = pv ? n - ncnt : 0xffffffffu;
   if (NSW) {
-    // part p of P takes segments p, p+P, ... (interleaved -> balanced)
-    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(NSW, parts), kJoinWarps),
-                                                       (uint64_t)sms * 8);
-    if (pv)
-      k_join_warp<true><<<grid, kJoinThreads, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(),
-                                                      in_off.get(), wsegs.get(), NSW, part, parts,
-                                                      t_rank.get(), acc.get());
-    else
-      k_join_warp<false><<<grid, kJoinThreads, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(),
-                                                       in_off.get(), wsegs.get(), NSW, part, parts,
-                                                       t_rank.get(), acc.get());
+    const size_t smem = (size_t)ncnt * sizeof(uint32_t);
+    auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, smem));
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
+                                         wsegs.get(), NSW, rc, ncnt, t_rank.get(), acc.get());
     TC_LAUNCH();
     ++launches;
   }
   if (NSC) {
     const uint32_t cap = table_size_for(g.max_dplus);
-    const size_t smem = (size_t)cap * sizeof(uint32_t) * (pv ? 2 : 1);
     DBuf<unsigned int> queue(1, s);
     TC_CUDA(cudaMemsetAsync(queue.get(), 0, sizeof(unsigned int), s));
-    const size_t kSmemMax = 160 * 1024;
-    if (smem <= kSmemMax) {
-      auto kern = pv ? k_join_cta<true, false> : k_join_cta<false, false>;
-      TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int occ = 0;
-      TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, smem));
-      if (occ < 1) occ = 1;
-      const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, ceil_div64(NSC, parts));
-      kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
-                                           csegs.get(), NSC, part, parts, queue.get(), cap, nullptr,
-                                           t_rank.get(), acc.get());
-      TC_LAUNCH();
-    } else {
-      auto kern = pv ? k_join_cta<true, true> : k_join_cta<false, true>;
-      const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * 4, ceil_div64(NSC, parts));
-      DBuf<uint32_t> slab((uint64_t)grid * cap * (pv ? 2 : 1), s);
-      kern<<<grid, kJoinThreads, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
-                                        csegs.get(), NSC, part, parts, queue.get(), cap, slab.get(),
+    const size_t base_smem = ((size_t)nbm + ncnt) * sizeof(uint32_t);
+    const size_t smem = base_smem + (size_t)cap * sizeof(uint32_t);
+    const bool global_table = smem > smem_max;
+    auto kern = pv ? (global_table ? k_join_cta<true, true> : k_join_cta<true, false>)
+                   : (global_table ? k_join_cta<false, true> : k_join_cta<false, false>);
+    const size_t dsm = global_table ? base_smem : smem;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    int occ = 0;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, dsm));
+    if (occ < 1) occ = 1;
+    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, (uint64_t)NSC);
+    DBuf<uint32_t> slab(global_table ? (uint64_t)grid * cap : 1, s);
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
+                                        csegs.get(), NSC, queue.get(), r0, nbm, cap, slab.get(), rc, ncnt,
                                         t_rank.get(), acc.get());
-      TC_LAUNCH();
-    }
+    TC_LAUNCH();
     ++launches;
   }
   TC_CUDA(cudaEventRecord(ev.e[2], s));

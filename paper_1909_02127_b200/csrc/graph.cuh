@@ -13,6 +13,8 @@
 // C5 (RMAT s26 ef32) = 34 GB of 180 GB.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 struct tc_graph {
@@ -26,6 +28,10 @@ struct tc_graph {
   int id_bits = 1;  // bits_for(n-1)
   double build_ms = 0;
   tcb::DBuf<uint32_t> off, col, src, deg, id_of, rank_of;
+  // multi-GPU work partition (count.cu): oriented-edge ranges [b[p], b[p+1])
+  // with ~equal wedge work, cached for the last part count requested
+  uint32_t cached_parts = 0;
+  std::vector<uint64_t> part_bounds;
 };
 
 namespace tcb {

@@ -128,8 +128,32 @@ def _stress_graphs():
     return out
 
 
+# membership / counter paths: default windows; tiny windows (most members in
+# the hash, most per-vertex hits as global atomics); hash forced to the global
+# slab
+MODES = {
+    "default": {},
+    "hash": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "32"},
+    "global_table": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "16", "TCB_SMEM_MAX": "1024"},
+}
+
+
+@pytest.fixture
+def mode_env(request):
+    env = MODES[request.param]
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    yield request.param
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+@pytest.mark.parametrize("mode_env", list(MODES), indirect=True)
 @pytest.mark.parametrize("name", ["wheel", "K300", "core_fringe"])
-def test_stress_bins(tc, oracle, cuda_ok, name):
+def test_stress_bins(tc, oracle, cuda_ok, name, mode_env):
     n, e = _stress_graphs()[name]
     pairs = e.reshape(-1)
     off, nb, E, _, _ = oracle.build_graph(pairs, n)
@@ -140,11 +164,13 @@ def test_stress_bins(tc, oracle, cuda_ok, name):
     assert tc.count_triangles(g, tc.MatchOptions(per_vertex=False)).count == T
 
 
-def test_large_clique_global_table(tc, cuda_ok):
-    # K_k: d+ up to k-1; k=24000 needs a 64K-slot table -> the per-CTA global slab
-    k = 24000
-    iu, ju = np.triu_indices(k, 1)
-    pairs = np.stack([iu, ju], 1).astype(np.uint32).reshape(-1)
+@pytest.mark.parametrize("mode_env", ["default", "global_table"], indirect=True)
+def test_large_clique(tc, cuda_ok, mode_env):
+    # K_k: d+ up to k-1 -> 16K-slot tables
+    k = 6000
+    a = np.repeat(np.arange(k, dtype=np.uint32), np.arange(k - 1, -1, -1))
+    b = np.concatenate([np.arange(i + 1, k, dtype=np.uint32) for i in range(k)])
+    pairs = np.stack([a, b], 1).reshape(-1)
     g = tc.build_graph_from_pairs(pairs, k)
     T = k * (k - 1) * (k - 2) // 6
     r = _count(tc, g)
