@@ -47,7 +47,7 @@ constexpr uint32_t kWarpSegItems = 64;  // items per warp segment
 constexpr uint32_t kCtaSegItems = 512;  // items per CTA segment
 constexpr uint32_t kTopBitmapBits = 1u << 17;  // membership bitmap window (16 KB)
 constexpr uint32_t kTopCounters = 1u << 13;    // per-vertex SMEM counter window (32 KB)
-constexpr size_t kSmemMax = 200 * 1024;
+constexpr uint32_t kCtaSmemSlots = 1024;     // below-window hash table in SMEM (4 KB)
 
 __host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t dplus) {
   // load factor <= 1/2, at least 32 slots
@@ -182,7 +182,7 @@ __global__ void k_seg_fill(const uint32_t* __restrict__ off, const uint32_t* __r
 __device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t shift) { return (x * 0x9E3779B1u) >> shift; }
 
 __device__ __forceinline__ bool hash_find(const uint32_t* tab, uint32_t mask, uint32_t shift, uint32_t x) {
-  uint32_t s = hslot(x, shift);
+  uint32_t s = hslot(x, shift) & mask;
   while (true) {
     const uint32_t k = tab[s];
     if (k == x) return true;
@@ -376,71 +376,168 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   }
 }
 
-// CTA bin: per segment the CTA builds N+(v) once (top-window bitmap + hash,
-// in SMEM; the hash goes to a per-CTA global slab when d+(v) is too large for
-// SMEM) and its warps share it.  Segments come from a global queue, heaviest
-// (top-rank pivots) first.
-// Dynamic SMEM: [bitmap nbm words][hash cap words (SMEM table only)][pv: ncnt].
-template <bool kPerVertex, bool kGlobalTable>
+// CTA bin.  Per segment (pivot v, <= kCtaSegItems in-edge items):
+//   1. build N+(v): members >= r0 into the top-window bitmap; the sorted
+//      prefix below r0 (hb members, found in the same pass) into an
+//      open-addressing table -- in SMEM when it fits kCtaSmemSlots, else in a
+//      per-CTA global slab;  stage the items (b, e, chunk prefix) in SMEM;
+//   2. advance + join: the segment's 16-byte chunks are split evenly across
+//      the warps (no warp waits on a long item of another), each warp walks
+//      its chunk range window by window (item of each chunk from the SMEM
+//      prefix via a ballot/redux start mask), two int4 loads in flight/lane;
+//   3. clear the touched bitmap words / table slots, flush per-item counts.
+// Segments come from a global queue, heaviest (top-rank pivots) first.
+// Dynamic SMEM: [bitmap nbm words][hash kCtaSmemSlots][pv: top counters ncnt].
+template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, 2) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
     const uint2* __restrict__ items, const uint32_t* __restrict__ in_off, const uint2* __restrict__ segs,
-    uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t r0, uint32_t nbm, uint32_t table_cap,
-    uint32_t* __restrict__ gslab, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
-    unsigned long long* __restrict__ total) {
+    uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t r0, uint32_t nbm, uint32_t stab_slots,
+    uint32_t slab_cap, uint32_t* __restrict__ gslab, uint32_t rc, uint32_t ncnt,
+    unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
-  __shared__ uint32_t s_item[kJoinWarps][32];
-  __shared__ uint32_t s_seg, s_hits;
+  __shared__ uint32_t s_b[kCtaSegItems], s_e[kCtaSegItems], s_pre[kCtaSegItems + 1];
+  __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
+  __shared__ uint32_t s_seg, s_hits, s_hb, s_tot;
   uint32_t* bm = dyn;
-  uint32_t* tab = kGlobalTable ? gslab + (uint64_t)blockIdx.x * table_cap : dyn + nbm;
-  uint32_t* top_cnt = dyn + nbm + (kGlobalTable ? 0 : table_cap);
+  uint32_t* stab = dyn + nbm;
+  uint32_t* top_cnt = dyn + nbm + kCtaSmemSlots;
+  uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t s = threadIdx.x; s < nbm; s += kJoinThreads) bm[s] = 0;
-  for (uint32_t s = threadIdx.x; s < table_cap; s += kJoinThreads) tab[s] = kEmpty;
-  if (kPerVertex)
+  const uint4* col4 = reinterpret_cast<const uint4*>(col);
+  for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
+  for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
+  if (kPerVertex) {
     for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) top_cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kJoinThreads) s_icnt[i] = 0;
+  }
   const PvSink sink{top_cnt, rc, t_rank};
   unsigned long long acc = 0;
   while (true) {
     if (threadIdx.x == 0) {
       s_seg = atomicAdd(queue, 1u);
       s_hits = 0;
+      s_hb = 0;
     }
-    if (kGlobalTable) __threadfence_block();
     __syncthreads();
     const uint32_t q = s_seg;
     if (q >= nsegs) break;
-    const uint32_t si = nsegs - 1 - q;  // heaviest (top ranks) first
-    const uint2 sg = segs[si];
+    const uint2 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
     const uint32_t v = sg.x, i0 = sg.y;
-    const uint32_t i1 = min(i0 + kCtaSegItems, in_off[v + 1]);
+    const uint32_t ni = min(i0 + kCtaSegItems, in_off[v + 1]) - i0;
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
-    const uint32_t ts = table_size_for(dv);
-    const uint32_t mask = ts - 1, shift = 32 - log2_pow2(ts);
+    // (1) members >= r0 -> bitmap; hb = #members below r0 (sorted prefix)
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
       const uint32_t x = col[nb + j];
-      if (x >= r0) atomicOr(&bm[(x - r0) >> 5], 1u << ((x - r0) & 31));
-      else hash_insert(tab, mask, shift, x);
+      if (x >= r0) {
+        atomicOr(&bm[(x - r0) >> 5], 1u << ((x - r0) & 31));
+        if (j == 0 || col[nb + j - 1] < r0) s_hb = j;
+      } else if (j + 1 == dv) {
+        s_hb = dv;
+      }
     }
-    if (kGlobalTable) __threadfence_block();
+    // stage the segment's items and their chunk prefix
+    uint32_t nch[2], bb[2], ee[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t i = threadIdx.x * 2 + r;
+      nch[r] = 0;
+      if (i < ni) {
+        const uint2 it = __ldcs(items + i0 + i);
+        bb[r] = it.x;
+        ee[r] = it.y;
+        nch[r] = ((it.y + 3) >> 2) - (it.x >> 2);
+      }
+    }
+    const uint32_t ex = block_exclusive_scan(nch[0] + nch[1], &s_tot);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t i = threadIdx.x * 2 + r;
+      if (i < ni) {
+        s_b[i] = bb[r];
+        s_e[i] = ee[r];
+        s_pre[i] = ex + (r ? nch[0] : 0);
+      }
+    }
     __syncthreads();
-    const PivotSet set{bm, tab, r0, mask, shift};
+    const uint32_t hb = s_hb, C = s_tot;
+    if (threadIdx.x == 0) s_pre[ni] = C;
+    uint32_t ts = 0, tmask = 0, tshift = 31;  // no members below r0: probe the always-empty stab[0]
+    uint32_t* tab = stab;
+    if (hb) {
+      ts = table_size_for(hb);
+      tmask = ts - 1;
+      tshift = 32 - log2_pow2(ts);
+      tab = ts <= stab_slots ? stab : gtab;
+      for (uint32_t j = threadIdx.x; j < hb; j += kJoinThreads) hash_insert(tab, tmask, tshift, col[nb + j]);
+      if (tab == gtab) __threadfence_block();
+    }
+    __syncthreads();
+    const PivotSet set{bm, tab, r0, tmask, tshift};
+    // (2) advance + join over this warp's even share of the chunks
+    const uint32_t fb = (uint32_t)(((uint64_t)C * warp) / kJoinWarps);
+    const uint32_t fe = (uint32_t)(((uint64_t)C * (warp + 1)) / kJoinWarps);
     uint32_t h = 0;
-    for (uint32_t ib = i0 + warp * 32; ib < i1; ib += kJoinWarps * 32)
-      h += warp_join_items<kPerVertex>(items, ib, min(ib + 32, i1), col, src, set, sink, s_item[warp]);
+    if (fb < fe) {
+      uint32_t lo = 0, hi = ni;  // item containing chunk fb: last i with s_pre[i] <= fb
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= fb) lo = mid; else hi = mid;
+      }
+      uint32_t k0 = lo;
+      for (uint32_t f = fb; f < fe; f += 64) {
+        // window A = [f, f+32), window B = [f+32, f+64)
+        uint32_t st = s_pre[min(k0 + 1 + lane, ni)];
+        uint32_t bit = (st < f + 32 && k0 + 1 + lane < ni) ? (1u << (st - f)) : 0u;
+        const uint32_t mA = __reduce_or_sync(0xffffffffu, bit);
+        const uint32_t kA = k0 + __popc(mA & ((2u << lane) - 1u));
+        const uint32_t k1 = k0 + __popc(__ballot_sync(0xffffffffu, k0 + 1 + lane < ni && st <= f + 32));
+        st = s_pre[min(k1 + 1 + lane, ni)];
+        bit = (st < f + 64 && k1 + 1 + lane < ni) ? (1u << (st - f - 32)) : 0u;
+        const uint32_t mB = __reduce_or_sync(0xffffffffu, bit);
+        const uint32_t kB = k1 + __popc(mB & ((2u << lane) - 1u));
+        k0 = k1 + __popc(__ballot_sync(0xffffffffu, k1 + 1 + lane < ni && st <= f + 64));
+        const uint32_t fA = f + lane, fB = f + 32 + lane;
+        const bool vA = fA < fe, vB = fB < fe;
+        const uint32_t kAc = vA ? kA : 0, kBc = vB ? kB : 0;
+        const uint32_t bA = s_b[kAc], eA = s_e[kAc], cA = (bA >> 2) + (fA - s_pre[kAc]);
+        const uint32_t bB = s_b[kBc], eB = s_e[kBc], cB = (bB >> 2) + (fB - s_pre[kBc]);
+        uint4 qA = make_uint4(0, 0, 0, 0), qB = make_uint4(0, 0, 0, 0);
+        if (vA) qA = __ldg(col4 + cA);
+        if (vB) qB = __ldg(col4 + cB);
+        if (vA) {
+          const uint32_t x = probe_chunk<kPerVertex>(qA, cA, bA, eA, set, sink);
+          h += x;
+          if (kPerVertex && x) atomicAdd(&s_icnt[kAc], x);
+        }
+        if (vB) {
+          const uint32_t x = probe_chunk<kPerVertex>(qB, cB, bB, eB, set, sink);
+          h += x;
+          if (kPerVertex && x) atomicAdd(&s_icnt[kBc], x);
+        }
+      }
+    }
     acc += h;
     if (kPerVertex) {
       const uint32_t hw = warp_sum(h);
       if (lane == 0 && hw) atomicAdd(&s_hits, hw);
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
-      const uint32_t x = col[nb + j];
-      if (x >= r0) bm[(x - r0) >> 5] = 0;
+    // (3) clear + per-vertex flush
+    for (uint32_t j = hb + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - r0) >> 5] = 0;
+    for (uint32_t j = threadIdx.x; j < ts; j += kJoinThreads) tab[j] = kEmpty;
+    if (kPerVertex) {
+      for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
+        const uint32_t c = s_icnt[i];
+        if (c) {
+          atomicAdd(&t_rank[src[s_b[i] - 1]], (unsigned long long)c);
+          s_icnt[i] = 0;
+        }
+      }
+      if (threadIdx.x == 0 && s_hits) atomicAdd(&t_rank[v], (unsigned long long)s_hits);
     }
-    for (uint32_t s = threadIdx.x; s < ts; s += kJoinThreads) tab[s] = kEmpty;
-    if (kPerVertex && threadIdx.x == 0 && s_hits) atomicAdd(&t_rank[v], (unsigned long long)s_hits);
-    if (kGlobalTable) __threadfence_block();
+    if (ts && tab == gtab) __threadfence_block();
     __syncthreads();
   }
   acc = warp_sum(acc);
@@ -604,7 +701,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   // sizes so tests can drive every membership/counter path on small graphs)
   const uint32_t top_bits = env_u32("TCB_TOP_BITMAP_BITS", kTopBitmapBits) & ~31u;
   const uint32_t top_cnt = env_u32("TCB_TOP_COUNTERS", kTopCounters);
-  const size_t smem_max = env_u32("TCB_SMEM_MAX", (uint32_t)kSmemMax);
+  const uint32_t smem_slots = env_u32("TCB_SMEM_SLOTS", kCtaSmemSlots);  // tests: force the global slab
   const uint32_t bm_bits = n < top_bits ? ((n + 31) & ~31u) : top_bits;
   const uint32_t r0 = n > bm_bits ? n - bm_bits : 0;
   const uint32_t nbm = bm_bits / 32;
@@ -623,23 +720,23 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
   }
   if (NSC) {
-    const uint32_t cap = table_size_for(g.max_dplus);
     DBuf<unsigned int> queue(1, s);
     TC_CUDA(cudaMemsetAsync(queue.get(), 0, sizeof(unsigned int), s));
-    const size_t base_smem = ((size_t)nbm + ncnt) * sizeof(uint32_t);
-    const size_t smem = base_smem + (size_t)cap * sizeof(uint32_t);
-    const bool global_table = smem > smem_max;
-    auto kern = pv ? (global_table ? k_join_cta<true, true> : k_join_cta<true, false>)
-                   : (global_table ? k_join_cta<false, true> : k_join_cta<false, false>);
-    const size_t dsm = global_table ? base_smem : smem;
+    // the below-window table spills to a per-CTA global slab only when a
+    // pivot has more than kCtaSmemSlots/2 members below r0
+    const uint32_t cap = table_size_for(g.max_dplus);
+    const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
+    const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt) * sizeof(uint32_t);
+    auto kern = pv ? k_join_cta<true> : k_join_cta<false>;
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     int occ = 0;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, dsm));
     if (occ < 1) occ = 1;
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, (uint64_t)NSC);
-    DBuf<uint32_t> slab(global_table ? (uint64_t)grid * cap : 1, s);
+    DBuf<uint32_t> slab((uint64_t)grid * slab_cap + 1, s);
     kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
-                                        csegs.get(), NSC, queue.get(), r0, nbm, cap, slab.get(), rc, ncnt,
+                                        csegs.get(), NSC, queue.get(), r0, nbm, std::min(smem_slots, kCtaSmemSlots),
+                                        slab_cap, slab.get(), rc, ncnt,
                                         t_rank.get(), acc.get());
     TC_LAUNCH();
     ++launches;

@@ -134,7 +134,7 @@ def _stress_graphs():
 MODES = {
     "default": {},
     "hash": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "32"},
-    "global_table": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "16", "TCB_SMEM_MAX": "1024"},
+    "global_table": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "16", "TCB_SMEM_SLOTS": "32"},
 }
 
 
