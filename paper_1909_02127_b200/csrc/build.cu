@@ -15,6 +15,8 @@
 //   radix_sort_u64 + run-count + scan -> oriented CSR (off/col/src)
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "graph.cuh"
 #include "prim.cuh"
 
@@ -204,6 +206,30 @@ __global__ void k_gather_deg(const uint32_t* __restrict__ deg_r, const uint32_t*
     out[v] = deg_r[rank_of[v]];
 }
 
+struct HotFlag {
+  const uint32_t* col;
+  uint32_t h0;
+  __device__ __forceinline__ uint32_t operator()(uint64_t e) const { return col[e] >= h0 ? 1u : 0u; }
+};
+
+__global__ void k_hot_scatter(const uint32_t* __restrict__ col, uint64_t E, uint32_t h0,
+                              const uint32_t* __restrict__ hp, uint16_t* __restrict__ colH) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = col[e];
+    if (x >= h0) colH[hp[e]] = (uint16_t)(x - h0);
+  }
+}
+
+__global__ void k_hot_offsets(const uint32_t* __restrict__ off, uint32_t n, uint64_t E,
+                              const uint32_t* __restrict__ hp, uint32_t total_hot, uint32_t* __restrict__ offH) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = off[u];
+    offH[u] = o < E ? hp[o] : total_hot;
+  }
+}
+
 struct DegLoad64 {
   const uint32_t* d;
   __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return d[i]; }
@@ -287,6 +313,29 @@ void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
     TC_LAUNCH();
   }
   g.max_dplus = read_scalar(scal.get(), s);
+
+  // hot window mirror (graph.cuh): 16-bit copy of every row's members >= h0
+  {
+    const char* hb = getenv("TCB_HOT_BITS");  // tests: shrink the window to drive the cold path
+    uint32_t hot = hb ? (uint32_t)strtoul(hb, nullptr, 10) : kHotBits;
+    if (hot < 32) hot = 32;
+    if (hot > kHotBits) hot = kHotBits;
+    g.h0 = n > hot ? n - hot : 0;
+    DBuf<uint32_t> hp(E ? E : 1, s), th(1, s);
+    scan_exclusive<uint32_t>(HotFlag{g.col.get(), g.h0}, hp.get(), E, th.get(), s);
+    const uint32_t total_hot = E ? read_scalar(th.get(), s) : 0;
+    g.colH.alloc((uint64_t)total_hot + 16, s);
+    TC_CUDA(cudaMemsetAsync(g.colH.get(), 0, ((uint64_t)total_hot + 16) * sizeof(uint16_t), s));
+    g.offH.alloc((uint64_t)n + 1, s);
+    if (E) {
+      k_hot_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), E, g.h0, hp.get(), g.colH.get());
+      TC_LAUNCH();
+    }
+    k_hot_offsets<<<grid_gs((uint64_t)n + 1, dev), kT, 0, s>>>(g.off.get(), n, E, hp.get(), total_hot,
+                                                               g.offH.get());
+    TC_LAUNCH();
+  }
+  build_frontier(g);
 }
 
 }  // namespace

@@ -122,6 +122,13 @@ void destroy_handle(tc_graph* g) {
     g->deg.release();
     g->id_of.release();
     g->rank_of.release();
+    g->colH.release();
+    g->offH.release();
+    g->fr_items.release();
+    g->fr_e.release();
+    g->fr_in.release();
+    g->fr_wsegs.release();
+    g->fr_csegs.release();
     cudaStreamSynchronize(s);
   }
   if (g->own_stream) cudaStreamDestroy(g->own_stream);
@@ -215,6 +222,8 @@ tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info) {
   info->max_out_degree = g->max_dplus;
   info->device = g->device;
   info->build_ms = g->build_ms;
+  info->frontier_ms = g->frontier_ms;
+  info->frontier_items = g->fr_nitems;
   return TC_OK;
 }
 

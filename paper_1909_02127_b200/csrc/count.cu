@@ -1,32 +1,32 @@
-// count.cu -- the hot path: level-1 frontier, degree-binned advance and fused
-// SMEM-hash join, warp-shuffle/atomic reduction (north_star (2)-(4)).
+// count.cu -- the hot path: degree-binned advance and fused SMEM join over the
+// level-1 frontier index, warp-shuffle/atomic reduction (north_star (2)-(4)).
 //
 // Reference path replaced (matcher.cpp): count_triangles :301-303 -> match
-// :249-299 -> filter_candidates :46-87 -> expand_level (level 1) :136-198 ->
-// count_final_level :204-245, whose inner loop visits every x in N(u) for each
-// row (u,w) and tests has_edge(w,x) by binary search (graph.cpp:23-31).
+// :249-299 -> count_final_level :204-245, whose inner loop visits every x in
+// N(u) for each level-1 row (u,w) and tests has_edge(w,x) by binary search
+// (graph.cpp:23-31).
 //
-// Formulation on the (deg,id)-ordered DAG in rank space (see DESIGN.md):
+// Formulation on the (deg,id)-ordered DAG in rank space (DESIGN.md section 3):
 //   every triangle a<b<c (ranks) has oriented edges a->b, a->c, b->c and is
-//   found exactly once with PIVOT v=b: for each in-edge u->v (u=a) the advance
-//   expands the wedge candidates x = the suffix of N+(u) after v (x=c is in
-//   it), and the join keeps x iff x in N+(v), probed in an SMEM hash of N+(v).
-//   Candidate wedges J = sum_u C(d+(u),2) (4.2e10 at RMAT s24) instead of the
-//   reference's sum_rows deg(u), and 4.4x fewer than the wedge-stream W.
-//
-// Frontier ("items"): one (b,e) pair per useful in-edge u->v, grouped by pivot
-//   v: [b,e) = the suffix of N+(u) after v in col[].  Items whose suffix is
-//   empty and pivots with d+(v)=0 never enter the frontier (they cannot close
-//   a triangle) -- the GPU analogue of the 2-core filter + look-ahead pruning.
-// Bins (by d+(v) = hash size):
-//   warp bin  d+(v) <= kWarpMaxDeg: one warp per segment, warp-private table
-//   CTA bin   larger: the CTA builds one table, its warps share it
-// Within a warp the items are load-balanced at 16-byte chunk granularity:
-//   lanes take consecutive int4 chunks of the concatenated suffixes (item found
-//   by a ballot/redux start mask), so loads are coalesced, vectorised int4.
-// Per-vertex counts (t[a],t[b],t[c] += 1 per triangle) are aggregated in SMEM:
-//   t[c] per hash slot, t[a] per item, t[b] per segment; <= |E|+items+segments
-//   global atomics instead of 3T.
+//   found exactly once with PIVOT v=b: for each in-edge u->v (u=a, a
+//   frontier item, frontier.cu) the advance expands the candidate wedges
+//   x = the suffix of N+(u) after v (x=c is in it), and the join keeps x iff
+//   x in N+(v).  Candidate wedges J = sum_u C(d+(u),2) (4.2e10 at RMAT s24)
+//   instead of the reference's sum_rows deg(u), and 4.4x fewer than the
+//   wedge-stream W.
+// Bins (by d+(v)):
+//   warp bin  d+(v) <= kWarpMaxDeg: one warp per segment, warp-private hash;
+//             items are (b,e) ranges of the 32-bit col[]
+//   CTA bin   larger: the CTA stages N+(v) once per segment -- members in the
+//             hot window [h0,n) as a bitmap, the rest in a hash -- and its
+//             warps share it.  Items are {hb,he,cb,ce}: the suffix split into
+//             its hot part (16-bit colH, graph.cuh) and cold part (32-bit col)
+// Chunks: suffixes are streamed as 16-byte int4 loads (8 hot / 4 cold ids),
+//   load-balanced across lanes by a ballot/redux start mask, segment chunks
+//   split evenly across warps.
+// Per-vertex counts (t[a],t[b],t[c] += 1 per triangle): t[a] per item, t[b]
+//   per segment, t[c] per hit into SMEM counters for the top ranks (global
+//   atomics below them).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,91 +41,36 @@ namespace {
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr uint32_t kWarpMaxDeg = 48;   // warp bin: d+(v) <= 48 -> 128-slot table
-constexpr uint32_t kWarpTable = 128;
-constexpr uint32_t kWarpSegItems = 64;  // items per warp segment
-constexpr uint32_t kCtaSegItems = 512;  // items per CTA segment
-constexpr uint32_t kTopBitmapBits = 1u << 17;  // membership bitmap window (16 KB)
-constexpr uint32_t kTopCounters = 1u << 13;    // per-vertex SMEM counter window (32 KB)
-constexpr uint32_t kCtaSmemSlots = 1024;     // below-window hash table in SMEM (4 KB)
+constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= 48)
+constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counter window (32 KB)
+constexpr uint32_t kCtaSmemSlots = 1024;     // cold-member hash table in SMEM (4 KB)
 
-__host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t dplus) {
-  // load factor <= 1/2, at least 32 slots
-  uint32_t t = 32;
-  while (t < 2 * dplus) t <<= 1;
+__host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t members) {
+  uint32_t t = 32;  // load factor <= 1/2
+  while (t < 2 * members) t <<= 1;
   return t;
 }
 
-// ---- frontier construction -------------------------------------------------
-
-struct FrontierSums {
-  unsigned long long W;      // sum_{u->v} d+(v)
-  unsigned long long J;      // sum of useful suffix lengths
-  unsigned long long items;  // useful items
-};
-
-// Wedge work of oriented edge e = u->v as a pivot in-edge: the suffix of
-// N+(u) after v, when v can close triangles (d+(v) > 0).
-__device__ __forceinline__ uint32_t edge_work(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                                              const uint32_t* __restrict__ src, uint64_t e, uint32_t& v,
-                                              uint32_t& end) {
-  v = col[e];
-  const uint32_t dv = off[v + 1] - off[v];
-  end = off[src[e] + 1];
-  return (dv > 0 && e + 1 < end) ? end - (uint32_t)(e + 1) : 0u;
+__host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
+  uint32_t l = 0;
+  while ((1u << l) < ts) ++l;
+  return l;
 }
 
-__global__ void k_item_count(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                             const uint32_t* __restrict__ src, uint64_t e0, uint64_t e1,
-                             uint32_t* __restrict__ cnt, FrontierSums* __restrict__ sums) {
-  unsigned long long W = 0, J = 0, I = 0;
-  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t v, end;
-    const uint32_t w = edge_work(off, col, src, e, v, end);
-    W += off[v + 1] - off[v];
-    if (w) {
-      atomicAdd(&cnt[v], 1u);
-      J += w;
-      ++I;
-    }
-  }
-  W = warp_sum(W);
-  J = warp_sum(J);
-  I = warp_sum(I);
-  if (lane_id() == 0) {
-    atomicAdd(&sums->W, W);
-    atomicAdd(&sums->J, J);
-    atomicAdd(&sums->items, I);
-  }
-}
+// ---- multi-GPU partition -------------------------------------------------------
 
-__global__ void k_item_scatter(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                               const uint32_t* __restrict__ src, uint64_t e0, uint64_t e1,
-                               const uint32_t* __restrict__ in_off, uint32_t* __restrict__ fill,
-                               uint2* __restrict__ items) {
-  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t v, end;
-    if (edge_work(off, col, src, e, v, end)) {
-      const uint32_t p = in_off[v] + atomicAdd(&fill[v], 1u);
-      items[p] = make_uint2((uint32_t)e + 1, end);
-    }
-  }
-}
-
-// Multi-GPU partition: prefix of per-edge cost (wedge work + a per-item
-// overhead) over the oriented edges, then P-1 binary searches.  Contiguous
-// edge ranges = contiguous source ranges of the degree-ordered DAG: the
-// north-star "degree-weighted ranges".
+// Prefix of per-edge cost (wedge work + a per-item overhead) over the oriented
+// edges, then P-1 binary searches.  Contiguous edge ranges = contiguous source
+// ranges of the degree-ordered DAG: the north-star "degree-weighted ranges".
 struct EdgeCost {
   const uint32_t* off;
   const uint32_t* col;
   const uint32_t* src;
   __device__ __forceinline__ uint64_t operator()(uint64_t e) const {
-    uint32_t v, end;
-    const uint32_t w = edge_work(off, col, src, e, v, end);
-    return w ? (uint64_t)w + 8 : 0ull;
+    const uint32_t v = col[e];
+    const uint32_t dv = off[v + 1] - off[v];
+    const uint32_t end = off[src[e] + 1];
+    return (dv > 0 && e + 1 < end) ? (uint64_t)(end - (uint32_t)(e + 1)) + 8 : 0ull;
   }
 };
 
@@ -133,8 +78,14 @@ __global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint64_t E, u
                               uint64_t* __restrict__ bounds) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > parts) return;
-  if (p == 0) { bounds[0] = 0; return; }
-  if (p == parts) { bounds[parts] = E; return; }
+  if (p == 0) {
+    bounds[0] = 0;
+    return;
+  }
+  if (p == parts) {
+    bounds[parts] = E;
+    return;
+  }
   const uint64_t target = (uint64_t)((double)total * p / parts);
   uint64_t lo = 0, hi = E;  // first e with prefix[e] >= target
   while (lo < hi) {
@@ -144,41 +95,11 @@ __global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint64_t E, u
   bounds[p] = lo;
 }
 
-struct SegCount {
-  const uint32_t* off;
-  const uint32_t* cnt;
-  uint32_t lo, hi, per;  // d+ range [lo, hi], items per segment
-  __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
-    const uint32_t dv = off[v + 1] - off[v];
-    const uint32_t c = cnt[v];
-    return (c && dv >= lo && dv <= hi) ? (c + per - 1) / per : 0u;
-  }
-};
-
-__global__ void k_seg_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
-                           const uint32_t* __restrict__ in_off, uint32_t n, uint32_t lo, uint32_t hi,
-                           uint32_t per, const uint32_t* __restrict__ seg_off, uint2* __restrict__ segs,
-                           unsigned long long* __restrict__ npivots) {
-  unsigned long long np = 0;
-  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t dv = off[v + 1] - off[v];
-    const uint32_t c = cnt[v];
-    if (!c || dv < lo || dv > hi) continue;
-    const uint32_t ns = (c + per - 1) / per;
-    const uint32_t s0 = seg_off[v];
-    for (uint32_t k = 0; k < ns; ++k) segs[s0 + k] = make_uint2((uint32_t)v, in_off[v] + k * per);
-    ++np;
-  }
-  np = warp_sum(np);
-  if (lane_id() == 0 && np) atomicAdd(npivots, np);
-}
-
-// ---- the fused advance + join ---------------------------------------------
+// ---- membership structures -------------------------------------------------
 
 // Multiplicative (Fibonacci) hashing: scatters runs of consecutive ranks, so
-// linear-probe clusters stay short (identity hashing of the dense top-rank
-// runs produced long, divergent probe chains -- profiles/README.md).
+// linear-probe clusters stay short (identity hashing of dense rank runs gave
+// long, divergent probe chains: profiles/README.md, join v1).
 __device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t shift) { return (x * 0x9E3779B1u) >> shift; }
 
 __device__ __forceinline__ bool hash_find(const uint32_t* tab, uint32_t mask, uint32_t shift, uint32_t x) {
@@ -192,35 +113,12 @@ __device__ __forceinline__ bool hash_find(const uint32_t* tab, uint32_t mask, ui
 }
 
 __device__ __forceinline__ void hash_insert(uint32_t* tab, uint32_t mask, uint32_t shift, uint32_t x) {
-  uint32_t s = hslot(x, shift);
+  uint32_t s = hslot(x, shift) & mask;
   while (atomicCAS(&tab[s], kEmpty, x) != kEmpty) s = (s + 1) & mask;
 }
 
-__host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
-  uint32_t l = 0;
-  while ((1u << l) < ts) ++l;
-  return l;
-}
-
-// Membership test for N+(v) (the closing edge v->x of wedge (u; v, x)):
-// a bitmap over the top-rank window [r0, n) -- where ~all wedge endpoints of
-// a power-law DAG land, and where neighbouring lanes probe neighbouring
-// words -- plus an open-addressing hash for the members below r0.
-struct PivotSet {
-  const uint32_t* bm;
-  const uint32_t* tab;
-  uint32_t r0, mask, shift;
-  __device__ __forceinline__ bool contains(uint32_t x) const {
-    if (x >= r0) {
-      const uint32_t d = x - r0;
-      return (bm[d >> 5] >> (d & 31)) & 1u;
-    }
-    return hash_find(tab, mask, shift, x);
-  }
-};
-
-// Per-vertex hits t[x]: SMEM counters for the top window [rc, n) (flushed
-// once per CTA), global atomics below it.
+// Per-vertex hits t[x]: SMEM counters for the top ranks [rc, n) (flushed once
+// per CTA), global atomics below them.
 struct PvSink {
   uint32_t* top;
   uint32_t rc;
@@ -231,9 +129,63 @@ struct PvSink {
   }
 };
 
-// Locate, for chunk window [w, w+32), the item each lane's chunk w+lane
-// belongs to (items hold >= 1 chunk; start/pre are the lane's item's
-// exclusive/inclusive chunk prefix).
+// ---- chunk decoders ----------------------------------------------------------
+
+// 8 hot ids (16-bit offsets from h0) per 16-byte chunk: bitmap probes.
+__device__ __forceinline__ uint32_t hot_u16(const uint4& q, int i) {
+  const uint32_t w = (i < 2) ? q.x : (i < 4) ? q.y : (i < 6) ? q.z : q.w;
+  return (i & 1) ? (w >> 16) : (w & 0xffffu);
+}
+
+template <bool kPerVertex>
+__device__ __forceinline__ uint32_t probe_hot(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
+                                              const uint32_t* bm, uint32_t h0, const PvSink& sink) {
+  const uint32_t p0 = c << 3;
+  const uint32_t lo = b > p0 ? b - p0 : 0u;
+  const uint32_t hi = e - p0 < 8u ? e - p0 : 8u;
+  const uint32_t valid = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+  uint32_t hits = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t y = hot_u16(q, i);
+    hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
+  }
+  hits &= valid;
+  if (kPerVertex) {
+    uint32_t m = hits;
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t w = (i < 2) ? q.x : (i < 4) ? q.y : (i < 6) ? q.z : q.w;
+      sink.hit(((i & 1) ? (w >> 16) : (w & 0xffffu)) + h0);
+    }
+  }
+  return __popc(hits);
+}
+
+// 4 cold ids (32-bit) per chunk: hash probes.
+template <bool kPerVertex>
+__device__ __forceinline__ uint32_t probe_cold(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
+                                               const uint32_t* tab, uint32_t mask, uint32_t shift,
+                                               const PvSink& sink) {
+  const uint32_t xs[4] = {q.x, q.y, q.z, q.w};
+  const uint32_t p0 = c << 2;
+  uint32_t h = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t p = p0 + t;
+    if (p >= b && p < e && hash_find(tab, mask, shift, xs[t])) {
+      ++h;
+      if (kPerVertex) sink.hit(xs[t]);
+    }
+  }
+  return h;
+}
+
+// ---- load balancing ----------------------------------------------------------
+
+// Item each lane's chunk w+lane belongs to, for items whose chunk starts are
+// given per lane (start/pre = exclusive/inclusive prefix, nch >= 1).
 __device__ __forceinline__ uint32_t item_of(uint32_t w, uint32_t nch, uint32_t pre, uint32_t start) {
   const unsigned lane = lane_id();
   const uint32_t kb = __popc(__ballot_sync(0xffffffffu, nch && pre <= w));
@@ -243,34 +195,70 @@ __device__ __forceinline__ uint32_t item_of(uint32_t w, uint32_t nch, uint32_t p
   return k < 32 ? k : 31;
 }
 
-template <bool kPerVertex>
-__device__ __forceinline__ uint32_t probe_chunk(const uint4 q, uint32_t c, uint32_t bk, uint32_t ek,
-                                                const PivotSet& set, const PvSink& sink) {
-  const uint32_t xs[4] = {q.x, q.y, q.z, q.w};
-  const uint32_t p0 = c << 2;
+// A warp walks chunk range [fb, fe) of a segment list staged in SMEM (item i:
+// chunk start pre[i] (pre[ni] = total), element range [sb[i], se[i]), original
+// index sidx[i]), two chunks per lane in flight.  fn(q, c, b, e) -> hits.
+template <int kIdsPerChunk, typename T, typename ChunkFn>
+__device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t ni, const uint32_t* pre,
+                                              const uint32_t* sb, const uint32_t* se, const uint16_t* sidx,
+                                              uint32_t* icnt, const T* base, ChunkFn fn) {
+  constexpr uint32_t kShift = kIdsPerChunk == 8 ? 3 : 2;
+  const unsigned lane = lane_id();
+  const uint4* base4 = reinterpret_cast<const uint4*>(base);
   uint32_t h = 0;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const uint32_t p = p0 + t;
-    if (p >= bk && p < ek && set.contains(xs[t])) {
-      ++h;
-      if (kPerVertex) sink.hit(xs[t]);
+  if (fb >= fe) return 0;
+  uint32_t lo = 0, hi = ni;  // item containing chunk fb: last i with pre[i] <= fb
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (pre[mid] <= fb) lo = mid; else hi = mid;
+  }
+  uint32_t k0 = lo;
+  for (uint32_t f = fb; f < fe; f += 64) {
+    // window A = [f, f+32), window B = [f+32, f+64)
+    uint32_t j = k0 + 1 + lane;
+    uint32_t st = pre[min(j, ni)];
+    uint32_t bit = (j < ni && st < f + 32) ? (1u << (st - f)) : 0u;
+    const uint32_t mA = __reduce_or_sync(0xffffffffu, bit);
+    const uint32_t kA = k0 + __popc(mA & ((2u << lane) - 1u));
+    const uint32_t k1 = k0 + __popc(__ballot_sync(0xffffffffu, j < ni && st <= f + 32));
+    j = k1 + 1 + lane;
+    st = pre[min(j, ni)];
+    bit = (j < ni && st < f + 64) ? (1u << (st - f - 32)) : 0u;
+    const uint32_t mB = __reduce_or_sync(0xffffffffu, bit);
+    const uint32_t kB = k1 + __popc(mB & ((2u << lane) - 1u));
+    k0 = k1 + __popc(__ballot_sync(0xffffffffu, j < ni && st <= f + 64));
+    const uint32_t fA = f + lane, fB = f + 32 + lane;
+    const bool vA = fA < fe, vB = fB < fe;
+    const uint32_t kAc = vA ? kA : 0, kBc = vB ? kB : 0;
+    const uint32_t bA = sb[kAc], eA = se[kAc], cA = (bA >> kShift) + (fA - pre[kAc]);
+    const uint32_t bB = sb[kBc], eB = se[kBc], cB = (bB >> kShift) + (fB - pre[kBc]);
+    uint4 qA = make_uint4(0, 0, 0, 0), qB = make_uint4(0, 0, 0, 0);
+    if (vA) qA = __ldg(base4 + cA);
+    if (vB) qB = __ldg(base4 + cB);
+    if (vA) {
+      const uint32_t x = fn(qA, cA, bA, eA);
+      h += x;
+      if (icnt && x) atomicAdd(&icnt[sidx[kAc]], x);
+    }
+    if (vB) {
+      const uint32_t x = fn(qB, cB, bB, eB);
+      h += x;
+      if (icnt && x) atomicAdd(&icnt[sidx[kBc]], x);
     }
   }
   return h;
 }
 
-// Advance + join for items [i0, i1) of one pivot, executed by one warp.
-// Advance: the items' suffixes are cut into 16-byte chunks and load-balanced
-// across lanes (two chunks per lane per step, both int4 loads in flight before
-// any probe).  Join: every wedge endpoint x in [b,e) is tested against N+(v).
-// Returns the lane's hit count; per-vertex: t[x] via the sink, t[u] via
-// per-item SMEM counters (one global atomic per item).
+// ---- warp bin ------------------------------------------------------------------
+
+// Advance + join for items [i0, i1) of one small pivot (u32 suffix ranges
+// {b,e} in items[i].x/.y), executed by one warp against its private hash.
 template <bool kPerVertex>
-__device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ items, uint32_t i0, uint32_t i1,
-                                                    const uint32_t* __restrict__ col,
-                                                    const uint32_t* __restrict__ src, const PivotSet& set,
-                                                    const PvSink& sink, uint32_t* item_cnt) {
+__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items, const uint32_t* __restrict__ item_e,
+                                                    uint32_t i0, uint32_t i1, const uint32_t* __restrict__ col,
+                                                    const uint32_t* __restrict__ src, const uint32_t* tab,
+                                                    uint32_t mask, uint32_t shift, const PvSink& sink,
+                                                    uint32_t* item_cnt) {
   const unsigned lane = lane_id();
   const uint4* col4 = reinterpret_cast<const uint4*>(col);
   uint32_t hits = 0;
@@ -278,7 +266,7 @@ __device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ it
     const uint32_t my = ib + lane;
     uint32_t b = 0, e = 0, nch = 0;
     if (my < i1) {
-      const uint2 it = items[my];
+      const uint2 it = __ldcs(reinterpret_cast<const uint2*>(items + my));
       b = it.x;
       e = it.y;
       nch = ((e + 3) >> 2) - (b >> 2);
@@ -290,33 +278,22 @@ __device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ it
       item_cnt[lane] = 0;
       __syncwarp();
     }
-    for (uint32_t base = 0; base < total; base += 64) {
-      const uint32_t k1 = item_of(base, nch, pre, start);
-      const uint32_t k2 = item_of(base + 32, nch, pre, start);
-      const uint32_t b1 = __shfl_sync(0xffffffffu, b, k1), e1 = __shfl_sync(0xffffffffu, e, k1);
-      const uint32_t s1 = __shfl_sync(0xffffffffu, start, k1);
-      const uint32_t b2 = __shfl_sync(0xffffffffu, b, k2), e2 = __shfl_sync(0xffffffffu, e, k2);
-      const uint32_t s2 = __shfl_sync(0xffffffffu, start, k2);
-      const uint32_t f1 = base + lane, f2 = base + 32 + lane;
-      const uint32_t c1 = (b1 >> 2) + (f1 - s1), c2 = (b2 >> 2) + (f2 - s2);
-      uint4 q1 = make_uint4(0, 0, 0, 0), q2 = make_uint4(0, 0, 0, 0);
-      if (f1 < total) q1 = __ldg(col4 + c1);
-      if (f2 < total) q2 = __ldg(col4 + c2);
-      if (f1 < total) {
-        const uint32_t h = probe_chunk<kPerVertex>(q1, c1, b1, e1, set, sink);
-        hits += h;
-        if (kPerVertex && h) atomicAdd(&item_cnt[k1], h);
-      }
-      if (f2 < total) {
-        const uint32_t h = probe_chunk<kPerVertex>(q2, c2, b2, e2, set, sink);
-        hits += h;
-        if (kPerVertex && h) atomicAdd(&item_cnt[k2], h);
+    for (uint32_t base = 0; base < total; base += 32) {
+      const uint32_t k = item_of(base, nch, pre, start);
+      const uint32_t bk = __shfl_sync(0xffffffffu, b, k), ek = __shfl_sync(0xffffffffu, e, k);
+      const uint32_t sk = __shfl_sync(0xffffffffu, start, k);
+      const uint32_t f = base + lane;
+      if (f < total) {
+        const uint32_t c = (bk >> 2) + (f - sk);
+        const uint32_t x = probe_cold<kPerVertex>(__ldg(col4 + c), c, bk, ek, tab, mask, shift, sink);
+        hits += x;
+        if (kPerVertex && x) atomicAdd(&item_cnt[k], x);
       }
     }
     if (kPerVertex) {
       __syncwarp();
       const uint32_t c = item_cnt[lane];
-      if (c) atomicAdd(&sink.t_rank[src[b - 1]], (unsigned long long)c);
+      if (c) atomicAdd(&sink.t_rank[src[item_e[my]]], (unsigned long long)c);
       __syncwarp();
     }
   }
@@ -324,12 +301,12 @@ __device__ __forceinline__ uint32_t warp_join_items(const uint2* __restrict__ it
 }
 
 // Warp bin: each warp takes whole segments of small pivots (d+ <= 48) with a
-// warp-private 128-slot hash table; the CTA shares the per-vertex top-window
+// warp-private 128-slot hash table; the CTA shares the per-vertex top-rank
 // counters (dynamic SMEM, pv only).
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint2* __restrict__ items, const uint32_t* __restrict__ in_off, const uint2* __restrict__ segs,
+    const uint4* __restrict__ items, const uint32_t* __restrict__ item_e, const uint4* __restrict__ segs,
     uint32_t nsegs, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
@@ -344,18 +321,17 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   }
   __syncwarp();
   const uint32_t mask = kWarpTable - 1, shift = 32 - log2_pow2(kWarpTable);
-  const PivotSet set{nullptr, tab, 0xffffffffu, mask, shift};
   const PvSink sink{top_cnt, rc, t_rank};
   unsigned long long acc = 0;
   const uint32_t gw = blockIdx.x * kJoinWarps + warp, nw = gridDim.x * kJoinWarps;
   for (uint32_t si = gw; si < nsegs; si += nw) {
-    const uint2 sg = segs[si];
-    const uint32_t v = sg.x, i0 = sg.y;
-    const uint32_t i1 = min(i0 + kWarpSegItems, in_off[v + 1]);
+    const uint4 sg = segs[si];
+    const uint32_t v = sg.x;
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
-    const uint32_t h = warp_join_items<kPerVertex>(items, i0, i1, col, src, set, sink, s_item[warp]);
+    const uint32_t h =
+        warp_join_small<kPerVertex>(items, item_e, sg.y, sg.z, col, src, tab, mask, shift, sink, s_item[warp]);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
@@ -376,35 +352,38 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   }
 }
 
-// CTA bin.  Per segment (pivot v, <= kCtaSegItems in-edge items):
-//   1. build N+(v): members >= r0 into the top-window bitmap; the sorted
-//      prefix below r0 (hb members, found in the same pass) into an
-//      open-addressing table -- in SMEM when it fits kCtaSmemSlots, else in a
-//      per-CTA global slab;  stage the items (b, e, chunk prefix) in SMEM;
-//   2. advance + join: the segment's 16-byte chunks are split evenly across
-//      the warps (no warp waits on a long item of another), each warp walks
-//      its chunk range window by window (item of each chunk from the SMEM
-//      prefix via a ballot/redux start mask), two int4 loads in flight/lane;
+// ---- CTA bin -------------------------------------------------------------------
+
+// Per segment (pivot v, <= kCtaSegItems in-edge items):
+//   1. stage N+(v): members >= h0 into the hot bitmap; the sorted prefix below
+//      h0 (found in the same pass) into an open-addressing table -- in SMEM
+//      when it fits, else in a per-CTA global slab.  Stage the items,
+//      compacted into a hot list and a cold list with their chunk prefixes;
+//   2. advance + join: each list's chunks are split evenly across the warps;
+//      hot chunks = 8 16-bit ids probed in the bitmap, cold = 4 32-bit ids
+//      probed in the hash;
 //   3. clear the touched bitmap words / table slots, flush per-item counts.
 // Segments come from a global queue, heaviest (top-rank pivots) first.
-// Dynamic SMEM: [bitmap nbm words][hash kCtaSmemSlots][pv: top counters ncnt].
+// Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots][pv: ncnt counters].
 template <bool kPerVertex>
-__global__ void __launch_bounds__(kJoinThreads, 2) k_join_cta(
+__global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint2* __restrict__ items, const uint32_t* __restrict__ in_off, const uint2* __restrict__ segs,
-    uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t r0, uint32_t nbm, uint32_t stab_slots,
-    uint32_t slab_cap, uint32_t* __restrict__ gslab, uint32_t rc, uint32_t ncnt,
+    const uint16_t* __restrict__ colH, const uint4* __restrict__ items, const uint32_t* __restrict__ item_e,
+    const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t h0, uint32_t nbm,
+    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, uint32_t rc, uint32_t ncnt,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
-  __shared__ uint32_t s_b[kCtaSegItems], s_e[kCtaSegItems], s_pre[kCtaSegItems + 1];
+  __shared__ uint32_t s_hb[kCtaSegItems], s_he[kCtaSegItems], s_hpre[kCtaSegItems + 1];
+  __shared__ uint32_t s_cb[kCtaSegItems], s_ce[kCtaSegItems], s_cpre[kCtaSegItems + 1];
+  __shared__ uint16_t s_hidx[kCtaSegItems], s_cidx[kCtaSegItems];
   __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
-  __shared__ uint32_t s_seg, s_hits, s_hb, s_tot;
+  __shared__ uint32_t s_seg, s_hits, s_cold, s_nl;
+  __shared__ unsigned long long s_ctot;
   uint32_t* bm = dyn;
   uint32_t* stab = dyn + nbm;
   uint32_t* top_cnt = dyn + nbm + kCtaSmemSlots;
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint4* col4 = reinterpret_cast<const uint4*>(col);
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
@@ -418,105 +397,104 @@ __global__ void __launch_bounds__(kJoinThreads, 2) k_join_cta(
     if (threadIdx.x == 0) {
       s_seg = atomicAdd(queue, 1u);
       s_hits = 0;
-      s_hb = 0;
+      s_cold = 0;
     }
     __syncthreads();
     const uint32_t q = s_seg;
     if (q >= nsegs) break;
-    const uint2 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
-    const uint32_t v = sg.x, i0 = sg.y;
-    const uint32_t ni = min(i0 + kCtaSegItems, in_off[v + 1]) - i0;
+    const uint4 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
+    const uint32_t v = sg.x, i0 = sg.y, ni = sg.z - sg.y;
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
-    // (1) members >= r0 -> bitmap; hb = #members below r0 (sorted prefix)
+    // (1a) hot members -> bitmap; s_cold = #members below h0 (sorted prefix)
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
       const uint32_t x = col[nb + j];
-      if (x >= r0) {
-        atomicOr(&bm[(x - r0) >> 5], 1u << ((x - r0) & 31));
-        if (j == 0 || col[nb + j - 1] < r0) s_hb = j;
+      if (x >= h0) {
+        atomicOr(&bm[(x - h0) >> 5], 1u << ((x - h0) & 31));
+        if (j == 0 || col[nb + j - 1] < h0) s_cold = j;
       } else if (j + 1 == dv) {
-        s_hb = dv;
+        s_cold = dv;
       }
     }
-    // stage the segment's items and their chunk prefix
-    uint32_t nch[2], bb[2], ee[2];
+    // (1b) stage items, compacted into hot / cold lists with chunk prefixes
+    uint4 it[2];
+    uint32_t nh[2], nc[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const uint32_t i = threadIdx.x * 2 + r;
-      nch[r] = 0;
+      nh[r] = nc[r] = 0;
       if (i < ni) {
-        const uint2 it = __ldcs(items + i0 + i);
-        bb[r] = it.x;
-        ee[r] = it.y;
-        nch[r] = ((it.y + 3) >> 2) - (it.x >> 2);
+        it[r] = __ldcs(items + i0 + i);
+        nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
+        nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
     }
-    const uint32_t ex = block_exclusive_scan(nch[0] + nch[1], &s_tot);
+    // list positions: hot count in the low 16 bits, cold count in the high 16
+    const uint32_t lp = block_exclusive_scan(
+        (uint32_t)((nh[0] > 0) + (nh[1] > 0)) | ((uint32_t)((nc[0] > 0) + (nc[1] > 0)) << 16), &s_nl);
+    // chunk prefixes: hot in the low 32 bits, cold in the high 32
+    const unsigned long long cp = block_exclusive_scan(
+        (unsigned long long)(nh[0] + nh[1]) | ((unsigned long long)(nc[0] + nc[1]) << 32), &s_ctot);
+    {
+      uint32_t ph = lp & 0xffffu, pc = lp >> 16;
+      uint32_t ch = (uint32_t)cp, cc = (uint32_t)(cp >> 32);
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t i = threadIdx.x * 2 + r;
-      if (i < ni) {
-        s_b[i] = bb[r];
-        s_e[i] = ee[r];
-        s_pre[i] = ex + (r ? nch[0] : 0);
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t i = threadIdx.x * 2 + r;
+        if (nh[r]) {
+          s_hb[ph] = it[r].x;
+          s_he[ph] = it[r].y;
+          s_hpre[ph] = ch;
+          s_hidx[ph] = (uint16_t)i;
+          ++ph;
+          ch += nh[r];
+        }
+        if (nc[r]) {
+          s_cb[pc] = it[r].z;
+          s_ce[pc] = it[r].w;
+          s_cpre[pc] = cc;
+          s_cidx[pc] = (uint16_t)i;
+          ++pc;
+          cc += nc[r];
+        }
       }
     }
     __syncthreads();
-    const uint32_t hb = s_hb, C = s_tot;
-    if (threadIdx.x == 0) s_pre[ni] = C;
-    uint32_t ts = 0, tmask = 0, tshift = 31;  // no members below r0: probe the always-empty stab[0]
+    const uint32_t nhot = s_nl & 0xffffu, ncold = s_nl >> 16;
+    const uint32_t cold = s_cold;
+    const uint32_t tchunks_h = (uint32_t)s_ctot, tchunks_c = (uint32_t)(s_ctot >> 32);
+    if (threadIdx.x == 0) {
+      s_hpre[nhot] = tchunks_h;
+      s_cpre[ncold] = tchunks_c;
+    }
+    uint32_t ts = 0, tmask = 0, tshift = 31;  // no cold members: probe the always-empty stab[0]
     uint32_t* tab = stab;
-    if (hb) {
-      ts = table_size_for(hb);
+    if (cold) {
+      ts = table_size_for(cold);
       tmask = ts - 1;
       tshift = 32 - log2_pow2(ts);
       tab = ts <= stab_slots ? stab : gtab;
-      for (uint32_t j = threadIdx.x; j < hb; j += kJoinThreads) hash_insert(tab, tmask, tshift, col[nb + j]);
+      for (uint32_t j = threadIdx.x; j < cold; j += kJoinThreads) hash_insert(tab, tmask, tshift, col[nb + j]);
       if (tab == gtab) __threadfence_block();
     }
     __syncthreads();
-    const PivotSet set{bm, tab, r0, tmask, tshift};
-    // (2) advance + join over this warp's even share of the chunks
-    const uint32_t fb = (uint32_t)(((uint64_t)C * warp) / kJoinWarps);
-    const uint32_t fe = (uint32_t)(((uint64_t)C * (warp + 1)) / kJoinWarps);
+    // (2) advance + join: hot chunks, then cold chunks, evenly split
     uint32_t h = 0;
-    if (fb < fe) {
-      uint32_t lo = 0, hi = ni;  // item containing chunk fb: last i with s_pre[i] <= fb
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_pre[mid] <= fb) lo = mid; else hi = mid;
-      }
-      uint32_t k0 = lo;
-      for (uint32_t f = fb; f < fe; f += 64) {
-        // window A = [f, f+32), window B = [f+32, f+64)
-        uint32_t st = s_pre[min(k0 + 1 + lane, ni)];
-        uint32_t bit = (st < f + 32 && k0 + 1 + lane < ni) ? (1u << (st - f)) : 0u;
-        const uint32_t mA = __reduce_or_sync(0xffffffffu, bit);
-        const uint32_t kA = k0 + __popc(mA & ((2u << lane) - 1u));
-        const uint32_t k1 = k0 + __popc(__ballot_sync(0xffffffffu, k0 + 1 + lane < ni && st <= f + 32));
-        st = s_pre[min(k1 + 1 + lane, ni)];
-        bit = (st < f + 64 && k1 + 1 + lane < ni) ? (1u << (st - f - 32)) : 0u;
-        const uint32_t mB = __reduce_or_sync(0xffffffffu, bit);
-        const uint32_t kB = k1 + __popc(mB & ((2u << lane) - 1u));
-        k0 = k1 + __popc(__ballot_sync(0xffffffffu, k1 + 1 + lane < ni && st <= f + 64));
-        const uint32_t fA = f + lane, fB = f + 32 + lane;
-        const bool vA = fA < fe, vB = fB < fe;
-        const uint32_t kAc = vA ? kA : 0, kBc = vB ? kB : 0;
-        const uint32_t bA = s_b[kAc], eA = s_e[kAc], cA = (bA >> 2) + (fA - s_pre[kAc]);
-        const uint32_t bB = s_b[kBc], eB = s_e[kBc], cB = (bB >> 2) + (fB - s_pre[kBc]);
-        uint4 qA = make_uint4(0, 0, 0, 0), qB = make_uint4(0, 0, 0, 0);
-        if (vA) qA = __ldg(col4 + cA);
-        if (vB) qB = __ldg(col4 + cB);
-        if (vA) {
-          const uint32_t x = probe_chunk<kPerVertex>(qA, cA, bA, eA, set, sink);
-          h += x;
-          if (kPerVertex && x) atomicAdd(&s_icnt[kAc], x);
-        }
-        if (vB) {
-          const uint32_t x = probe_chunk<kPerVertex>(qB, cB, bB, eB, set, sink);
-          h += x;
-          if (kPerVertex && x) atomicAdd(&s_icnt[kBc], x);
-        }
-      }
+    uint32_t* icnt = kPerVertex ? s_icnt : nullptr;
+    {
+      const uint32_t fb = (uint32_t)(((uint64_t)tchunks_h * warp) / kJoinWarps);
+      const uint32_t fe = (uint32_t)(((uint64_t)tchunks_h * (warp + 1)) / kJoinWarps);
+      h += warp_walk<8>(fb, fe, nhot, s_hpre, s_hb, s_he, s_hidx, icnt, colH,
+                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e) {
+                          return probe_hot<kPerVertex>(qq, c, b, e, bm, h0, sink);
+                        });
+    }
+    if (ncold) {
+      const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kJoinWarps);
+      const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kJoinWarps);
+      h += warp_walk<4>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
+                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e) {
+                          return probe_cold<kPerVertex>(qq, c, b, e, tab, tmask, tshift, sink);
+                        });
     }
     acc += h;
     if (kPerVertex) {
@@ -525,13 +503,13 @@ __global__ void __launch_bounds__(kJoinThreads, 2) k_join_cta(
     }
     __syncthreads();
     // (3) clear + per-vertex flush
-    for (uint32_t j = hb + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - r0) >> 5] = 0;
+    for (uint32_t j = cold + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - h0) >> 5] = 0;
     for (uint32_t j = threadIdx.x; j < ts; j += kJoinThreads) tab[j] = kEmpty;
     if (kPerVertex) {
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
         const uint32_t c = s_icnt[i];
         if (c) {
-          atomicAdd(&t_rank[src[s_b[i] - 1]], (unsigned long long)c);
+          atomicAdd(&t_rank[src[item_e[i0 + i]]], (unsigned long long)c);
           s_icnt[i] = 0;
         }
       }
@@ -579,7 +557,7 @@ T read_scalar(const T* d, cudaStream_t s) {
 }
 
 struct Events {
-  cudaEvent_t e[5];
+  cudaEvent_t e[4];
   Events() {
     for (auto& x : e) TC_CUDA(cudaEventCreate(&x));
   }
@@ -616,8 +594,12 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaMemsetAsync(t_rank.get(), 0, sizeof(unsigned long long) * (n ? n : 1), s));
   }
 
-  // ---- multi-GPU: this part's degree-weighted oriented-edge range ----
-  uint64_t e0 = 0, e1 = E;
+  // ---- work segments: the whole frontier, or this part's degree-weighted
+  //      oriented-edge range (multi-GPU) ----
+  const uint4* wsegs = g.fr_wsegs.get();
+  const uint4* csegs = g.fr_csegs.get();
+  uint64_t NSW = g.fr_nwsegs, NSC = g.fr_ncsegs;
+  DBuf<uint4> pw, pc;
   if (parts > 1 && E) {
     if (g.cached_parts != parts) {
       DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
@@ -632,79 +614,20 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
       TC_CUDA(cudaStreamSynchronize(s));
       g.cached_parts = parts;
     }
-    e0 = g.part_bounds[part];
-    e1 = g.part_bounds[part + 1];
-  }
-
-  // ---- level-1 frontier: useful in-edges grouped by pivot ----
-  DBuf<uint32_t> cnt(n ? n : 1, s), in_off((uint64_t)n + 1, s);
-  DBuf<FrontierSums> sums(1, s);
-  TC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
-  TC_CUDA(cudaMemsetAsync(sums.get(), 0, sizeof(FrontierSums), s));
-  if (e1 > e0) {
-    k_item_count<<<grid_gs(e1 - e0, dev), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), e0, e1, cnt.get(),
-                                                       sums.get());
-    TC_LAUNCH();
-    ++kl;
-  }
-  kl += scan_exclusive<uint32_t>(LoadArray<uint32_t>{cnt.get()}, in_off.get(), n, in_off.get() + n, s);
-  FrontierSums hs = read_scalar(sums.get(), s);
-  const uint64_t NI = hs.items;
-  DBuf<uint2> items(NI ? NI : 1, s);
-  if (NI) {
-    DBuf<uint32_t> fill(n, s);
-    TC_CUDA(cudaMemsetAsync(fill.get(), 0, sizeof(uint32_t) * n, s));
-    k_item_scatter<<<grid_gs(e1 - e0, dev), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), e0, e1,
-                                                         in_off.get(), fill.get(), items.get());
-    TC_LAUNCH();
-    ++kl;
-  }
-  // segments per bin
-  DBuf<uint32_t> wseg_off(n ? n : 1, s), cseg_off(n ? n : 1, s), nseg(2, s);
-  DBuf<unsigned long long> npiv(1, s);
-  TC_CUDA(cudaMemsetAsync(npiv.get(), 0, sizeof(unsigned long long), s));
-  uint32_t hn[2] = {0, 0};
-  if (NI) {
-    kl += scan_exclusive<uint32_t>(SegCount{g.off.get(), cnt.get(), 1, kWarpMaxDeg, kWarpSegItems}, wseg_off.get(),
-                                   n, nseg.get(), s);
-    kl += scan_exclusive<uint32_t>(SegCount{g.off.get(), cnt.get(), kWarpMaxDeg + 1, 0xffffffffu, kCtaSegItems},
-                             cseg_off.get(), n, nseg.get() + 1, s);
-    TC_CUDA(cudaMemcpyAsync(hn, nseg.get(), 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-  }
-  uint32_t NSW = hn[0], NSC = hn[1];
-  if (const char* dbg = getenv("TCB_DEBUG_BINS")) {  // diagnostics: 1 = warp bin only, 2 = CTA bin only
-    const int m = atoi(dbg);
-    if (!(m & 1)) NSW = 0;
-    if (!(m & 2)) NSC = 0;
-  }
-  DBuf<uint2> wsegs(NSW ? NSW : 1, s), csegs(NSC ? NSC : 1, s);
-  if (NSW) {
-    k_seg_fill<<<grid_gs(n, dev), 256, 0, s>>>(g.off.get(), cnt.get(), in_off.get(), n, 1, kWarpMaxDeg,
-                                               kWarpSegItems, wseg_off.get(), wsegs.get(), npiv.get());
-    TC_LAUNCH();
-    ++kl;
-  }
-  if (NSC) {
-    k_seg_fill<<<grid_gs(n, dev), 256, 0, s>>>(g.off.get(), cnt.get(), in_off.get(), n, kWarpMaxDeg + 1,
-                                               0xffffffffu, kCtaSegItems, cseg_off.get(), csegs.get(), npiv.get());
-    TC_LAUNCH();
-    ++kl;
+    part_segments(g, g.part_bounds[part], g.part_bounds[part + 1], pw, NSW, pc, NSC);
+    kl += 6;
+    wsegs = pw.get();
+    csegs = pc.get();
   }
   TC_CUDA(cudaEventRecord(ev.e[1], s));
 
   // ---- advance + join ----
   const int sms = num_sms(dev);
   uint64_t launches = 0;
-  // top-rank windows: membership bitmap [r0, n) and per-vertex counters [rc, n)
-  // (TCB_TOP_BITMAP_BITS / TCB_TOP_COUNTERS / TCB_SMEM_MAX override the window
-  // sizes so tests can drive every membership/counter path on small graphs)
-  const uint32_t top_bits = env_u32("TCB_TOP_BITMAP_BITS", kTopBitmapBits) & ~31u;
+  // per-vertex SMEM counters for the top ranks [rc, n); TCB_TOP_COUNTERS /
+  // TCB_SMEM_SLOTS shrink them so tests drive every path on small graphs
   const uint32_t top_cnt = env_u32("TCB_TOP_COUNTERS", kTopCounters);
-  const uint32_t smem_slots = env_u32("TCB_SMEM_SLOTS", kCtaSmemSlots);  // tests: force the global slab
-  const uint32_t bm_bits = n < top_bits ? ((n + 31) & ~31u) : top_bits;
-  const uint32_t r0 = n > bm_bits ? n - bm_bits : 0;
-  const uint32_t nbm = bm_bits / 32;
+  const uint32_t smem_slots = std::min(env_u32("TCB_SMEM_SLOTS", kCtaSmemSlots), kCtaSmemSlots);
   const uint32_t ncnt = pv ? (n < top_cnt ? n : top_cnt) : 0;
   const uint32_t rc = pv ? n - ncnt : 0xffffffffu;
   if (NSW) {
@@ -713,17 +636,19 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, smem));
-    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
-                                         wsegs.get(), NSW, rc, ncnt, t_rank.get(), acc.get());
+    const unsigned grid =
+        (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), g.fr_items.get(), g.fr_e.get(),
+                                         wsegs, (uint32_t)NSW, rc, ncnt, t_rank.get(), acc.get());
     TC_LAUNCH();
     ++launches;
   }
   if (NSC) {
     DBuf<unsigned int> queue(1, s);
     TC_CUDA(cudaMemsetAsync(queue.get(), 0, sizeof(unsigned int), s));
-    // the below-window table spills to a per-CTA global slab only when a
-    // pivot has more than kCtaSmemSlots/2 members below r0
+    const uint32_t nbm = (n - g.h0 + 31) / 32;
+    // cold members spill to a per-CTA global slab only when a pivot has more
+    // than smem_slots/2 members below h0
     const uint32_t cap = table_size_for(g.max_dplus);
     const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
     const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt) * sizeof(uint32_t);
@@ -732,12 +657,11 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     int occ = 0;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, dsm));
     if (occ < 1) occ = 1;
-    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, (uint64_t)NSC);
+    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, NSC);
     DBuf<uint32_t> slab((uint64_t)grid * slab_cap + 1, s);
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), items.get(), in_off.get(),
-                                        csegs.get(), NSC, queue.get(), r0, nbm, std::min(smem_slots, kCtaSmemSlots),
-                                        slab_cap, slab.get(), rc, ncnt,
-                                        t_rank.get(), acc.get());
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), g.colH.get(), g.fr_items.get(),
+                                        g.fr_e.get(), csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
+                                        slab_cap, slab.get(), rc, ncnt, t_rank.get(), acc.get());
     TC_LAUNCH();
     ++launches;
   }
@@ -757,15 +681,18 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     stats->join_ms = ev.ms(1, 2);
     stats->reduce_ms = ev.ms(2, 3);
     stats->total_ms = ev.ms(0, 3);
-    stats->items = NI;
-    stats->wedges = hs.J;
-    stats->segments = (uint64_t)NSW + NSC;
+    stats->items = g.fr_nitems;
+    stats->wedges = g.fr_J;
+    stats->segments = NSW + NSC;
     stats->join_launches = launches;
-    stats->dag_W = (double)hs.W;
-    stats->pivots = read_scalar(npiv.get(), s);
+    stats->dag_W = (double)g.fr_W;
+    stats->pivots = g.fr_pivots;
     stats->kernel_launches = kl + launches;
-    stats->alg_bytes = 4.0 * (double)hs.W + 12.0 * (double)E + 8.0 * ((double)n + 1) + (pv ? 8.0 * n : 0.0);
-    stats->probe_bytes = 4.0 * (double)hs.J + 8.0 * (double)NI + 4.0 * (double)E;
+    stats->alg_bytes = 4.0 * (double)g.fr_W + 12.0 * (double)E + 8.0 * ((double)n + 1) + (pv ? 8.0 * n : 0.0);
+    // bytes the implemented join must stream: hot ids 2 B, cold ids 4 B,
+    // items 16 B, pivot lists 4 B per member (whole graph; a part does ~1/P)
+    stats->probe_bytes = 2.0 * (double)g.fr_hot + 4.0 * (double)(g.fr_J - g.fr_hot) +
+                         16.0 * (double)g.fr_nitems + 4.0 * (double)E;
   }
 }
 

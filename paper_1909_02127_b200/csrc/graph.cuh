@@ -28,6 +28,30 @@ struct tc_graph {
   int id_bits = 1;  // bits_for(n-1)
   double build_ms = 0;
   tcb::DBuf<uint32_t> off, col, src, deg, id_of, rank_of;
+  // Hot window: the top kHotBits ranks [h0, n), where ~97% of wedge endpoints
+  // of a power-law DAG fall (n-x < 2^16 for 97% of probes).  Each
+  // row's members >= h0 form its sorted suffix; they are mirrored as 16-bit
+  // offsets x - h0 in colH (row r at [offH[r], offH[r+1])), halving the bytes
+  // the join streams and letting a probe index the pivot bitmap directly.
+  uint32_t h0 = 0;
+  tcb::DBuf<uint16_t> colH;
+  tcb::DBuf<uint32_t> offH;
+  // Level-1 frontier index (frontier.cu): the useful in-edges u->v of every
+  // pivot v (d+(v) > 0, non-empty suffix), grouped by v and sorted by edge id
+  // e -- the transpose of the oriented CSR restricted to wedge-producing
+  // edges, i.e. the reference's level-1 PartialTable rows (u,v)
+  // (matcher.cpp:136-198).  Graph-static, built once with the CSR.
+  //   fr_items[i] = {hb,he,cb,ce} (CTA-bin pivots: hot range in colH, cold
+  //                 range in col) or {b,e,0,0} (warp-bin pivots: col range)
+  //   fr_e[i]     = the edge id (source u = src[e]; multi-GPU ranges)
+  //   fr_in[v]    = first item of pivot v (n+1)
+  //   fr_wsegs / fr_csegs = {v, i0, i1, 0} work segments per bin (whole graph)
+  tcb::DBuf<uint4> fr_items;
+  tcb::DBuf<uint32_t> fr_e, fr_in;
+  tcb::DBuf<uint4> fr_wsegs, fr_csegs;
+  uint64_t fr_nitems = 0, fr_nwsegs = 0, fr_ncsegs = 0, fr_pivots = 0;
+  uint64_t fr_W = 0, fr_J = 0, fr_hot = 0, fr_nitems_c = 0;
+  double frontier_ms = 0;
   // multi-GPU work partition (count.cu): oriented-edge ranges [b[p], b[p+1])
   // with ~equal wedge work, cached for the last part count requested
   uint32_t cached_parts = 0;
@@ -35,6 +59,17 @@ struct tc_graph {
 };
 
 namespace tcb {
+
+constexpr uint32_t kHotBits = 1u << 16;
+constexpr uint32_t kWarpMaxDeg = 48;    // warp bin: d+(v) <= 48 (128-slot warp table)
+constexpr uint32_t kWarpSegItems = 64;  // items per warp-bin segment
+constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
+
+// Level-1 frontier index (frontier.cu), called at the end of every build.
+void build_frontier(tc_graph& g);
+// Segments of one multi-GPU part (edge range [e0,e1)) -> wsegs/csegs.
+void part_segments(tc_graph& g, uint64_t e0, uint64_t e1, DBuf<uint4>& wsegs, uint64_t& nw, DBuf<uint4>& csegs,
+                   uint64_t& nc);
 
 // Build pipeline entry points (build.cu).
 void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t n,

@@ -133,8 +133,8 @@ def _stress_graphs():
 # slab
 MODES = {
     "default": {},
-    "hash": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "32"},
-    "global_table": {"TCB_TOP_BITMAP_BITS": "64", "TCB_TOP_COUNTERS": "16", "TCB_SMEM_SLOTS": "32"},
+    "hash": {"TCB_HOT_BITS": "64", "TCB_TOP_COUNTERS": "32"},
+    "global_table": {"TCB_HOT_BITS": "64", "TCB_TOP_COUNTERS": "16", "TCB_SMEM_SLOTS": "32"},
 }
 
 
