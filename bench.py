@@ -130,52 +130,77 @@ def gen_kind(tc, kind):
 # from /root/reference's sources) on a bounded, cost-stratified seed sample,
 # extrapolated by the reference's per-row visit cost model.
 # ---------------------------------------------------------------------------
-def reference_cpu_sample(off: np.ndarray, nb: np.ndarray, budget_s: float, E: int, rg=None):
+_CAL = None
+
+
+def calibration():
+    """Ratio (full trimatch::count_triangles time) / (sample estimate) on C1,
+    the one config where the reference's full run takes seconds."""
+    global _CAL
+    if _CAL is None:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle_ctypes import Oracle, Ref
+        o = Oracle()
+        off, nb, E, _, _ = o.build_graph(o.gen_rmat(16, 16), 1 << 16)
+        rg = Ref().graph(off, nb)
+        t0 = time.perf_counter()
+        T = rg.count_triangles(lookahead=2, workers=0)
+        full_ms = (time.perf_counter() - t0) * 1e3
+        est = reference_cpu_sample(off, nb, 2.0, E, rg, calibrate=False)
+        _CAL = {"config": "C1 RMAT s16 ef16", "full_ms": full_ms, "sample_est_ms": est["t_sample_est_ms"],
+                "factor": full_ms / est["t_sample_est_ms"], "triangles": T}
+    return _CAL
+
+
+def reference_cpu_sample(off: np.ndarray, nb: np.ndarray, budget_s: float, E: int, rg=None, calibrate=True):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle_ctypes import REF_SO, Ref
+    from oracle_ctypes import REF_SO, Oracle, Ref
     if not os.path.exists(REF_SO):
         return None
     ref = Ref()
     if rg is None:
         rg = ref.graph(off, nb)
-    n = off.size - 1
-    deg = np.diff(off).astype(np.int64)
     # visits the final level makes for seed u: deg(u) per level-1 row (u,w),
     # w in N(u), w > u (matcher.cpp:215-228); cost-stratified systematic sample
-    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
-    up = np.bincount(rows[nb.astype(np.int64) > rows], minlength=n).astype(np.int64)
-    del rows
-    cost = deg * up
+    cost = Oracle().seed_costs(off, nb)
     total_cost = float(cost.sum())
     order = np.argsort(cost, kind="stable")[::-1]
     order = order[cost[order] > 0]
     workers = os.cpu_count() or 1
-
-    def run(stride):
-        seeds = np.sort(order[::stride]).astype(np.uint32)
-        s = rg.count_sample(seeds, lookahead=2, workers=0)
-        s["sample_cost"] = float(cost[seeds.astype(np.int64)].sum())
-        s["nseeds"] = int(seeds.size)
-        return s
-
-    stride = max(1, int(order.size // 64))
-    s = run(stride)
-    # scale the sample so the verify phase takes ~budget_s
-    while s["verify_ms"] < 1000 * budget_s / 8 and stride > 1:
-        stride = max(1, int(stride / max(2.0, (1000 * budget_s / 2) / max(s["verify_ms"], 1.0))))
-        s = run(stride)
-    t_full_ms = s["filter_ms"] + s["verify_ms"] * total_cost / max(s["sample_cost"], 1.0)
+    # seeds: a cost-stratified systematic sample (~2048 seeds, hubs included)
+    stride = max(1, int(order.size // 2048))
+    seeds = np.sort(order[::stride]).astype(np.uint32)
+    sample_cost = float(cost[seeds.astype(np.int64)].sum())
+    # level-2 rows of those seeds: probe the visit rate on a thin row sample,
+    # then size the row stride so level 2 runs ~budget_s
+    rs = max(1, int(sample_cost / 2e8))
+    s = rg.count_sample(seeds, row_stride=rs, lookahead=2, workers=0)
+    rate = s["visits"] / max(s["l2_ms"] / 1e3, 1e-3)
+    rs2 = max(1, int(sample_cost / max(rate * budget_s, 1.0)))
+    if rs2 < rs:
+        rs = rs2
+        s = rg.count_sample(seeds, row_stride=rs, lookahead=2, workers=0)
+    verify_seeds_ms = s["l1_ms"] + s["l2_ms"] * rs           # all level-2 rows of the seeds
+    t_est_ms = s["filter_ms"] + verify_seeds_ms * total_cost / max(sample_cost, 1.0)
+    # expand_level materialises rows and zero-fills one scratch slot per visit
+    # (frontier.hpp:123), which count_final_level does not: calibrate the
+    # estimator once against a FULL count_triangles run on C1 (RMAT s16)
+    cal = calibration() if calibrate else None
+    t_full_ms = t_est_ms * (cal["factor"] if cal else 1.0)
     return {
         "value": E / (t_full_ms / 1e3) / 1e9,
         "unit": "GTEPS",
         "cores": workers,
         "kind": "reference",
         "t_full_est_ms": t_full_ms,
-        "sample": (f"trimatch::count_triangles path (filter_candidates on the full graph + expand_level "
-                   f"L1/L2 through the public API) seeded with {s['nseeds']} of {order.size} candidate "
-                   f"vertices (cost-stratified every {stride}th by deg(u)*|N(u)>u|); verify time "
-                   f"{s['verify_ms']:.0f} ms extrapolated by cost ratio {total_cost / max(s['sample_cost'], 1):.1f}; "
-                   f"filter {s['filter_ms']:.0f} ms timed on the full graph; OpenMP workers={workers}"),
+        "t_sample_est_ms": t_est_ms,
+        "calibration": cal,
+        "sample": (f"trimatch::count_triangles path through its public API: filter_candidates on the full "
+                   f"graph ({s['filter_ms']:.0f} ms), expand_level L1 for {seeds.size} of {order.size} seeds "
+                   f"(cost-stratified every {stride}th by deg(u)*|N(u)>u|, {s['l1_ms']:.0f} ms), expand_level L2 "
+                   f"(final level, accept+look-ahead+has_edge) on every {rs}th of {s['l1_rows']} L1 rows "
+                   f"({s['visits']} visits, {s['l2_ms']:.0f} ms); extrapolated x{rs} rows and x"
+                   f"{total_cost / max(sample_cost, 1):.1f} seed cost; OpenMP workers={workers}"),
     }
 
 

@@ -297,6 +297,21 @@ uint64_t oracle_fnv1a64(const void* data, uint64_t nbytes) {
   return h;
 }
 
+/* ---- CPU-baseline sampling support --------------------------------------- */
+
+/* cost[u] = deg(u) * |{w in N(u): w > u}| -- the visits the reference's final
+ * level makes for seed u (matcher.cpp:215-228 visits N(u) for each level-1
+ * row (u,w), w > u).  Used to stratify and extrapolate the bounded sample. */
+void oracle_seed_costs(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n, double* cost) {
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t uu = 0; uu < (int64_t)n; ++uu) {
+    const uint32_t u = (uint32_t)uu;
+    const uint64_t b = offsets[u], e = offsets[u + 1];
+    const uint64_t up = e - b - upper_bound_u32(nbrs + b, e - b, u);
+    cost[u] = (double)(e - b) * (double)up;
+  }
+}
+
 /* ---- DAG statistics for the work model ------------------- */
 
 void oracle_dag_stats(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n,

@@ -52,6 +52,10 @@ uint64_t oracle_brute_force(const uint64_t* offsets, const uint32_t* nbrs, uint3
  * the little-endian u64 array. */
 uint64_t oracle_fnv1a64(const void* data, uint64_t nbytes);
 
+/* Per-seed visit cost deg(u)*|N(u) > u| of the reference's final level
+ * (bench.py's bounded CPU sample). */
+void oracle_seed_costs(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n, double* cost);
+
 /* Sum over the oriented DAG (deg,id) of the work model used by bench.py's
  * roofline: fills W = sum_{u->v} d+(v), S2 = sum_u d+(u)^2,
  * and J = sum_u C(d+(u),2) restricted to pivots with d+>0 (the pivot join's

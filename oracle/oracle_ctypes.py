@@ -62,6 +62,14 @@ class Oracle:
         L.oracle_fnv1a64.argtypes = [C.c_void_p, C.c_uint64]
         L.oracle_dag_stats.argtypes = [u64p, u32p, C.c_uint32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double), u32p]
+        L.oracle_seed_costs.argtypes = [u64p, u32p, C.c_uint32, C.POINTER(C.c_double)]
+
+    def seed_costs(self, offsets: np.ndarray, nbrs: np.ndarray) -> np.ndarray:
+        n = offsets.size - 1
+        out = np.zeros(max(n, 1), dtype=np.float64)
+        nb = nbrs if nbrs.size else np.zeros(1, np.uint32)
+        self.lib.oracle_seed_costs(_ptr(offsets, u64p), _ptr(nb, u32p), n, _ptr(out, C.POINTER(C.c_double)))
+        return out[:n]
 
     # generators ---------------------------------------------------------
     def gen_rmat(self, scale: int, edgefactor: int = 16, permute: bool = False) -> np.ndarray:
@@ -157,8 +165,9 @@ class Ref:
         L.ref_segmented_intersect_pv.restype = C.c_int
         L.ref_segmented_intersect_pv.argtypes = [C.c_void_p, C.c_int, u64p, u64p]
         L.ref_count_sample.restype = C.c_int
-        L.ref_count_sample.argtypes = [C.c_void_p, u32p, C.c_uint64, C.c_int, C.c_int,
-                                       C.POINTER(C.c_double), C.POINTER(C.c_double), u64p, u64p]
+        L.ref_count_sample.argtypes = [C.c_void_p, u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       u64p, u64p, u64p]
         L.ref_parse_matrix_market.restype = C.c_int
         L.ref_parse_matrix_market.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(u32p), u64p, u32p]
         L.ref_load_graph.restype = C.c_int
@@ -241,14 +250,17 @@ class RefGraph:
         self.ref._check(self.ref.lib.ref_segmented_intersect(self.h, workers, C.byref(c)))
         return c.value
 
-    def count_sample(self, seeds: np.ndarray, lookahead: int = 2, workers: int = 0):
+    def count_sample(self, seeds: np.ndarray, row_stride: int = 1, max_chunk_visits: int = 1 << 27,
+                     lookahead: int = 2, workers: int = 0):
         seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
-        fm, vm = C.c_double(), C.c_double()
-        cnt, vis = C.c_uint64(), C.c_uint64()
-        self.ref._check(self.ref.lib.ref_count_sample(self.h, _ptr(seeds, u32p), seeds.size, lookahead,
-                                                      workers, C.byref(fm), C.byref(vm), C.byref(cnt),
-                                                      C.byref(vis)))
-        return dict(filter_ms=fm.value, verify_ms=vm.value, count=cnt.value, visits=vis.value)
+        fm, l1, l2 = C.c_double(), C.c_double(), C.c_double()
+        cnt, vis, rows = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.ref._check(self.ref.lib.ref_count_sample(self.h, _ptr(seeds, u32p), seeds.size, row_stride,
+                                                      max_chunk_visits, lookahead, workers, C.byref(fm),
+                                                      C.byref(l1), C.byref(l2), C.byref(cnt), C.byref(vis),
+                                                      C.byref(rows)))
+        return dict(filter_ms=fm.value, l1_ms=l1.value, l2_ms=l2.value, count=cnt.value, visits=vis.value,
+                    l1_rows=rows.value)
 
     def write_csr_cache(self, path: str):
         self.ref._check(self.ref.lib.ref_write_csr_cache(path.encode(), self.h))

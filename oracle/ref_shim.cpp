@@ -205,8 +205,13 @@ int ref_segmented_intersect_pv(void* gp, int workers, uint64_t* count, uint64_t*
 // accept + look-ahead logic count_final_level applies, matcher.cpp:204-245,
 // through the public expand_level).  Reports filter/verify ms and the level-2
 // visits the reference's own LevelStats count.
-int ref_count_sample(void* gp, const uint32_t* seeds, uint64_t nseeds, int lookahead, int workers,
-                     double* filter_ms, double* verify_ms, uint64_t* count, uint64_t* visits) {
+// Level 2 (final) is run on every row_stride-th level-1 row, fed to
+// expand_level in chunks of at most max_chunk_visits scratch entries (the
+// reference's advance allocates one slot per visited edge, frontier.hpp:123,
+// so a hub seed's rows cannot go through in one call).
+int ref_count_sample(void* gp, const uint32_t* seeds, uint64_t nseeds, uint64_t row_stride,
+                     uint64_t max_chunk_visits, int lookahead, int workers, double* filter_ms, double* l1_ms,
+                     double* l2_ms, uint64_t* count, uint64_t* visits, uint64_t* l1_rows) {
   try {
     const Graph& g = *static_cast<Graph*>(gp);
     MatchOptions opts;
@@ -225,12 +230,38 @@ int ref_count_sample(void* gp, const uint32_t* seeds, uint64_t nseeds, int looka
       table.cells().push_back(kInvalidVertex);
       table.cells().push_back(kInvalidVertex);
     }
-    LevelStats s1, s2;
+    LevelStats s1;
     PartialTable l2 = expand_level(g, plan, c, table, 1, opts, &s1);
-    PartialTable l3 = expand_level(g, plan, c, l2, 2, opts, &s2);
-    *verify_ms = ms_since(t1);
-    *count = l3.num_rows();
-    *visits = s2.edges_visited;
+    *l1_ms = ms_since(t1);
+    *l1_rows = l2.num_rows();
+    if (row_stride == 0) row_stride = 1;
+    uint64_t found = 0, vis = 0;
+    double ms2 = 0;
+    PartialTable chunk(3);
+    chunk.set_level(2);
+    uint64_t chunk_vis = 0;
+    auto flush = [&]() {
+      if (chunk.num_rows() == 0) return;
+      auto t2 = std::chrono::steady_clock::now();
+      LevelStats s2;
+      PartialTable l3 = expand_level(g, plan, c, chunk, 2, opts, &s2);
+      ms2 += ms_since(t2);
+      found += l3.num_rows();
+      vis += s2.edges_visited;
+      chunk.cells().clear();
+      chunk_vis = 0;
+    };
+    for (uint64_t r = 0; r < l2.num_rows(); r += row_stride) {
+      auto row = l2.row(r);
+      const uint64_t d = g.degree(row[0]);
+      if (chunk_vis + d > max_chunk_visits) flush();
+      chunk.cells().insert(chunk.cells().end(), row.begin(), row.end());
+      chunk_vis += d;
+    }
+    flush();
+    *l2_ms = ms2;
+    *count = found;
+    *visits = vis;
     return 0;
   } catch (...) {
     return map_exception();
