@@ -42,7 +42,7 @@ constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
 constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= 48)
-constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counter window (32 KB)
+constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counters (16-bit halves: 16 KB)
 constexpr uint32_t kCtaSmemSlots = 1024;     // cold-member hash table in SMEM (4 KB)
 
 __host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t members) {
@@ -119,15 +119,50 @@ __device__ __forceinline__ void hash_insert(uint32_t* tab, uint32_t mask, uint32
 
 // Per-vertex hits t[x]: SMEM counters for the top ranks [rc, n) (flushed once
 // per CTA), global atomics below them.
+__device__ uint32_t g_pv_dbg = 0;
+
+// kHalf: counters are 16-bit halves of 32-bit words (twice the window per
+// byte, which keeps 4 CTAs/SM resident).  The increments stay fire-and-forget
+// (RED, no return value); the CTA kernel flushes before any half could wrap
+// (a segment adds at most its item count to one counter).
+template <bool kHalf>
 struct PvSink {
   uint32_t* top;
   uint32_t rc;
   unsigned long long* t_rank;
+  uint32_t dbg;  // diagnostics (TCB_PV_DBG): bit0 skip t[x], bit1 skip global atomics
   __device__ __forceinline__ void hit(uint32_t x) const {
-    if (x >= rc) atomicAdd(&top[x - rc], 1u);
-    else atomicAdd(&t_rank[x], 1ull);
+    if (dbg & 1) return;
+    if (x >= rc) {
+      const uint32_t i = x - rc;
+      if (kHalf) atomicAdd(&top[i >> 1], 1u << ((i & 1u) << 4));
+      else atomicAdd(&top[i], 1u);
+    } else if (!(dbg & 2)) {
+      atomicAdd(&t_rank[x], 1ull);
+    }
   }
 };
+
+// Add the SMEM counters [rc, rc+ncnt) into t_rank and zero them.
+template <bool kHalf>
+__device__ __forceinline__ void flush_top(uint32_t* top, uint32_t ncnt, uint32_t rc, unsigned long long* t_rank) {
+  if (kHalf) {
+    for (uint32_t j = threadIdx.x; j < ncnt / 2; j += blockDim.x) {
+      const uint32_t w = top[j];
+      if (!w) continue;
+      top[j] = 0;
+      if (w & 0xffffu) atomicAdd(&t_rank[rc + 2 * j], (unsigned long long)(w & 0xffffu));
+      if (w >> 16) atomicAdd(&t_rank[rc + 2 * j + 1], (unsigned long long)(w >> 16));
+    }
+  } else {
+    for (uint32_t j = threadIdx.x; j < ncnt; j += blockDim.x) {
+      const uint32_t w = top[j];
+      if (!w) continue;
+      top[j] = 0;
+      atomicAdd(&t_rank[rc + j], (unsigned long long)w);
+    }
+  }
+}
 
 // ---- chunk decoders ----------------------------------------------------------
 
@@ -137,37 +172,34 @@ __device__ __forceinline__ uint32_t hot_u16(const uint4& q, int i) {
   return (i & 1) ? (w >> 16) : (w & 0xffffu);
 }
 
-template <bool kPerVertex>
+template <bool kPerVertex, typename Sink>
 __device__ __forceinline__ uint32_t probe_hot(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
-                                              const uint32_t* bm, uint32_t h0, const PvSink& sink) {
+                                              const uint32_t* bm, uint32_t h0, const Sink& sink) {
   const uint32_t p0 = c << 3;
   const uint32_t lo = b > p0 ? b - p0 : 0u;
   const uint32_t hi = e - p0 < 8u ? e - p0 : 8u;
   const uint32_t valid = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
   uint32_t hits = 0;
+  uint32_t y[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const uint32_t y = hot_u16(q, i);
-    hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
+    y[i] = hot_u16(q, i);
+    hits |= ((bm[y[i] >> 5] >> (y[i] & 31)) & 1u) << i;
   }
   hits &= valid;
-  if (kPerVertex) {
-    uint32_t m = hits;
-    while (m) {
-      const int i = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t w = (i < 2) ? q.x : (i < 4) ? q.y : (i < 6) ? q.z : q.w;
-      sink.hit(((i & 1) ? (w >> 16) : (w & 0xffffu)) + h0);
-    }
+  if (kPerVertex && hits) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (hits & (1u << i)) sink.hit(y[i] + h0);
   }
   return __popc(hits);
 }
 
 // 4 cold ids (32-bit) per chunk: hash probes.
-template <bool kPerVertex>
+template <bool kPerVertex, typename Sink>
 __device__ __forceinline__ uint32_t probe_cold(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
                                                const uint32_t* tab, uint32_t mask, uint32_t shift,
-                                               const PvSink& sink) {
+                                               const Sink& sink) {
   const uint32_t xs[4] = {q.x, q.y, q.z, q.w};
   const uint32_t p0 = c << 2;
   uint32_t h = 0;
@@ -193,6 +225,25 @@ __device__ __forceinline__ uint32_t item_of(uint32_t w, uint32_t nch, uint32_t p
   const uint32_t smask = __reduce_or_sync(0xffffffffu, bit);
   const uint32_t k = kb + __popc(smask & ((2u << lane) - 1u));
   return k < 32 ? k : 31;
+}
+
+// Per-item hit counts of one chunk window: lanes holding chunks of the same
+// item are a contiguous run (item index is non-decreasing in the lane), so a
+// 5-step segmented suffix sum leaves each run's total in its head lane -- one
+// SMEM atomic per item run instead of one per lane.
+__device__ __forceinline__ void add_item_counts(uint32_t* cnt, const uint16_t* sidx, bool valid, uint32_t k,
+                                                uint32_t x) {
+  const unsigned lane = lane_id();
+  const uint32_t key = valid ? k : 0xffffffffu;
+  uint32_t v = valid ? x : 0u;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_down_sync(0xffffffffu, v, d);
+    const uint32_t k2 = __shfl_down_sync(0xffffffffu, key, d);
+    if (lane + d < 32 && k2 == key) v += t;
+  }
+  const uint32_t kp = __shfl_up_sync(0xffffffffu, key, 1);
+  if (valid && v && (lane == 0 || kp != key)) atomicAdd(&cnt[sidx ? sidx[k] : k], v);
 }
 
 // A warp walks chunk range [fb, fe) of a segment list staged in SMEM (item i:
@@ -253,11 +304,11 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 
 // Advance + join for items [i0, i1) of one small pivot (u32 suffix ranges
 // {b,e} in items[i].x/.y), executed by one warp against its private hash.
-template <bool kPerVertex>
+template <bool kPerVertex, typename Sink>
 __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items, const uint32_t* __restrict__ item_e,
                                                     uint32_t i0, uint32_t i1, const uint32_t* __restrict__ col,
                                                     const uint32_t* __restrict__ src, const uint32_t* tab,
-                                                    uint32_t mask, uint32_t shift, const PvSink& sink,
+                                                    uint32_t mask, uint32_t shift, const Sink& sink,
                                                     uint32_t* item_cnt) {
   const unsigned lane = lane_id();
   const uint4* col4 = reinterpret_cast<const uint4*>(col);
@@ -321,7 +372,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   }
   __syncwarp();
   const uint32_t mask = kWarpTable - 1, shift = 32 - log2_pow2(kWarpTable);
-  const PvSink sink{top_cnt, rc, t_rank};
+  const PvSink<false> sink{top_cnt, rc, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
   const uint32_t gw = blockIdx.x * kJoinWarps + warp, nw = gridDim.x * kJoinWarps;
   for (uint32_t si = gw; si < nsegs; si += nw) {
@@ -345,10 +396,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   if (lane == 0 && acc) atomicAdd(total, acc);
   if (kPerVertex) {
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) {
-      const uint32_t c = top_cnt[i];
-      if (c) atomicAdd(&t_rank[rc + i], (unsigned long long)c);
-    }
+    flush_top<false>(top_cnt, ncnt, rc, t_rank);
   }
 }
 
@@ -388,11 +436,12 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
   if (kPerVertex) {
-    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) top_cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < ncnt / 2; i += kJoinThreads) top_cnt[i] = 0;
     for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kJoinThreads) s_icnt[i] = 0;
   }
-  const PvSink sink{top_cnt, rc, t_rank};
+  const PvSink<true> sink{top_cnt, rc, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
+  uint32_t since_flush = 0;  // items since the last counter flush (bounds every 16-bit half)
   while (true) {
     if (threadIdx.x == 0) {
       s_seg = atomicAdd(queue, 1u);
@@ -404,6 +453,15 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
     if (q >= nsegs) break;
     const uint4 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
     const uint32_t v = sg.x, i0 = sg.y, ni = sg.z - sg.y;
+    if (kPerVertex) {
+      // one segment adds at most ni to any counter: flush before a half could wrap
+      if (since_flush + ni > 0xffffu) {
+        flush_top<true>(top_cnt, ncnt, rc, t_rank);
+        since_flush = 0;
+        __syncthreads();
+      }
+      since_flush += ni;
+    }
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     // (1a) hot members -> bitmap; s_cold = #members below h0 (sorted prefix)
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
@@ -480,7 +538,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
     // (2) advance + join: hot chunks, then cold chunks, evenly split
     uint32_t h = 0;
     uint32_t* icnt = kPerVertex ? s_icnt : nullptr;
-    {
+    if (!(g_pv_dbg & 4)) {
       const uint32_t fb = (uint32_t)(((uint64_t)tchunks_h * warp) / kJoinWarps);
       const uint32_t fe = (uint32_t)(((uint64_t)tchunks_h * (warp + 1)) / kJoinWarps);
       h += warp_walk<8>(fb, fe, nhot, s_hpre, s_hb, s_he, s_hidx, icnt, colH,
@@ -488,7 +546,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
                           return probe_hot<kPerVertex>(qq, c, b, e, bm, h0, sink);
                         });
     }
-    if (ncold) {
+    if (ncold && !(g_pv_dbg & 4)) {
       const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kJoinWarps);
       const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kJoinWarps);
       h += warp_walk<4>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
@@ -522,10 +580,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
   if (lane == 0 && acc) atomicAdd(total, acc);
   if (kPerVertex) {
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) {
-      const uint32_t c = top_cnt[i];
-      if (c) atomicAdd(&t_rank[rc + i], (unsigned long long)c);
-    }
+    flush_top<true>(top_cnt, ncnt, rc, t_rank);
   }
 }
 
@@ -628,10 +683,16 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   // TCB_SMEM_SLOTS shrink them so tests drive every path on small graphs
   const uint32_t top_cnt = env_u32("TCB_TOP_COUNTERS", kTopCounters);
   const uint32_t smem_slots = std::min(env_u32("TCB_SMEM_SLOTS", kCtaSmemSlots), kCtaSmemSlots);
-  const uint32_t ncnt = pv ? (n < top_cnt ? n : top_cnt) : 0;
+  const uint32_t ncnt = pv ? ((n < top_cnt ? n : top_cnt) & ~1u) : 0;
   const uint32_t rc = pv ? n - ncnt : 0xffffffffu;
+  {
+    const uint32_t dbg = env_u32("TCB_PV_DBG", 0);
+    TC_CUDA(cudaMemcpyToSymbolAsync(g_pv_dbg, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, s));
+  }
   if (NSW) {
-    const size_t smem = (size_t)ncnt * sizeof(uint32_t);
+    // warp bin: plain 32-bit counters over half the window
+    const uint32_t ncnt_w = ncnt / 2, rc_w = pv ? n - ncnt_w : 0xffffffffu;
+    const size_t smem = (size_t)ncnt_w * sizeof(uint32_t);
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -639,7 +700,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const unsigned grid =
         (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
     kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), g.fr_items.get(), g.fr_e.get(),
-                                         wsegs, (uint32_t)NSW, rc, ncnt, t_rank.get(), acc.get());
+                                         wsegs, (uint32_t)NSW, rc_w, ncnt_w, t_rank.get(), acc.get());
     TC_LAUNCH();
     ++launches;
   }
@@ -651,7 +712,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     // than smem_slots/2 members below h0
     const uint32_t cap = table_size_for(g.max_dplus);
     const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
-    const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt) * sizeof(uint32_t);
+    const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt / 2) * sizeof(uint32_t);
     auto kern = pv ? k_join_cta<true> : k_join_cta<false>;
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     int occ = 0;
