@@ -139,6 +139,10 @@ void tc_graph_destroy(tc_graph* g);
 tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint64_t* per_vertex,
                    tc_count_stats* stats);
 
+/* Multi-GPU split: bounds[0..parts] (parts+1 u64, host) of the degree-weighted
+ * oriented-edge ranges tc_count uses for part_index/part_count. */
+tc_status tc_partition_bounds(tc_graph* g, uint32_t parts, uint64_t* bounds);
+
 /* ---- adjacent formats ------------------------------------- */
 
 /* parse_matrix_market over an in-memory byte buffer (host).  On success

@@ -96,13 +96,14 @@ _sig("tc_count", C.c_int, [C.c_void_p, C.POINTER(TcCountOpts), C.c_void_p, C.c_v
                            C.POINTER(TcCountStats)])
 _sig("tc_parse_matrix_market", C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), u64p, u32p])
 _sig("tc_csr_cache_to_graph", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p)])
+_sig("tc_partition_bounds", C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p])
 _sig("tc_gen_num_edges", C.c_uint64, [C.c_int, C.c_int, C.c_int])
 _sig("tc_generate", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p])
 
 EXPORTED_SYMBOLS = [
     "tc_abi_version", "tc_last_error", "tc_free", "tc_graph_build", "tc_graph_from_csr", "tc_graph_get_info",
     "tc_graph_export_csr", "tc_graph_degrees", "tc_graph_set_stream", "tc_graph_destroy", "tc_count",
-    "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate",
+    "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate", "tc_partition_bounds",
 ]
 
 
@@ -367,6 +368,14 @@ def count_triangles_into(g: Graph, total_ptr, per_vertex_ptr=None, opts: Optiona
                          C.c_void_p(_addr(per_vertex_ptr)) if per_vertex_ptr is not None else None,
                          C.byref(st) if stats else None))
     return st.as_dict() if stats else None
+
+
+def partition_bounds(g: Graph, parts: int) -> np.ndarray:
+    """Degree-weighted oriented-edge ranges of a `parts`-way multi-GPU split
+    (what tc_count uses for part_index/part_count)."""
+    b = np.zeros(parts + 1, np.uint64)
+    _check(_lib.tc_partition_bounds(g.handle, parts, C.c_void_p(b.ctypes.data)))
+    return b
 
 
 def parse_matrix_market(text) -> EdgeList:

@@ -283,6 +283,16 @@ tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint
   TC_API_CATCH
 }
 
+tc_status tc_partition_bounds(tc_graph* g, uint32_t parts, uint64_t* bounds) {
+  if (!g || !bounds || parts == 0) return set_error(TC_EINVAL, "tc_partition_bounds: bad argument");
+  TC_API_TRY
+  DeviceGuard dg(g->device);
+  const std::vector<uint64_t>& b = tcb::partition_bounds(*g, parts);
+  std::memcpy(bounds, b.data(), ((size_t)parts + 1) * sizeof(uint64_t));
+  return TC_OK;
+  TC_API_CATCH
+}
+
 tc_status tc_parse_matrix_market(const char* text, uint64_t len, uint32_t** pairs, uint64_t* m,
                                  uint32_t* n_declared) {
   if (!pairs || !m || !n_declared || (len && !text)) return set_error(TC_EINVAL, "tc_parse_matrix_market: NULL argument");

@@ -628,6 +628,27 @@ struct Events {
 
 }  // namespace
 
+const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
+  if (g.cached_parts != parts) {
+    cudaStream_t s = g.stream;
+    const uint64_t E = g.E;
+    g.part_bounds.assign((size_t)parts + 1, 0);
+    g.part_bounds[parts] = E;
+    if (E && parts > 1) {
+      DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
+      scan_exclusive<uint64_t>(EdgeCost{g.off.get(), g.col.get(), g.src.get()}, prefix.get(), E, tot.get(), s);
+      const uint64_t total_cost = read_scalar(tot.get(), s);
+      k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), E, total_cost, parts, bnd.get());
+      TC_LAUNCH();
+      TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, s));
+      TC_CUDA(cudaStreamSynchronize(s));
+    }
+    g.cached_parts = parts;
+  }
+  return g.part_bounds;
+}
+
 void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, uint64_t* d_pv,
                      tc_count_stats* stats) {
   cudaStream_t s = g.stream;
@@ -656,20 +677,9 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   uint64_t NSW = g.fr_nwsegs, NSC = g.fr_ncsegs;
   DBuf<uint4> pw, pc;
   if (parts > 1 && E) {
-    if (g.cached_parts != parts) {
-      DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
-      kl += scan_exclusive<uint64_t>(EdgeCost{g.off.get(), g.col.get(), g.src.get()}, prefix.get(), E, tot.get(), s);
-      const uint64_t total_cost = read_scalar(tot.get(), s);
-      k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), E, total_cost, parts, bnd.get());
-      TC_LAUNCH();
-      ++kl;
-      g.part_bounds.assign(parts + 1, 0);
-      TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
-                              cudaMemcpyDeviceToHost, s));
-      TC_CUDA(cudaStreamSynchronize(s));
-      g.cached_parts = parts;
-    }
-    part_segments(g, g.part_bounds[part], g.part_bounds[part + 1], pw, NSW, pc, NSC);
+    if (g.cached_parts != parts) kl += 4;
+    const std::vector<uint64_t>& b = partition_bounds(g, parts);
+    part_segments(g, b[part], b[part + 1], pw, NSW, pc, NSC);
     kl += 6;
     wsegs = pw.get();
     csegs = pc.get();

@@ -82,6 +82,8 @@ void export_degrees(tc_graph& g, uint32_t* d_deg);
 // Count pipeline (count.cu).
 void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total,
                      uint64_t* d_per_vertex, tc_count_stats* stats);
+// Degree-weighted oriented-edge ranges of a P-way split (cached per handle).
+const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts);
 
 // Generators (gen.cu).
 uint64_t gen_num_edges(int kind, int scale, int param);

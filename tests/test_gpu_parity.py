@@ -193,6 +193,17 @@ def test_parts_sum_to_total(tc, oracle, cuda_ok, parts):
     assert oracle.fnv(pv) == c["pv_fnv"]
 
 
+def test_partition_bounds_match_host(tc, oracle, cuda_ok):
+    from paper_1909_02127_b200 import dist as tdist
+    pairs = tc.generate(tc.GEN_RMAT, 14, 16)
+    g = tc.build_graph_from_pairs(pairs, 1 << 14)
+    off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 14)
+    roff, col, src, order = tdist.degree_rank_dag(off, nb)
+    cost = tdist.edge_cost(roff, col, src)
+    for P in (2, 3, 8):
+        assert tc.partition_bounds(g, P).tolist() == tdist.partition_bounds(cost, P).tolist()
+
+
 SYN = ["C1_rmat_s16_ef16", "C2_er_s20_d32", "rmat_s18_ef16", "kron_s18_ef16", "rmat_s20_ef16"]
 
 
