@@ -1,0 +1,306 @@
+// trimatch_gpu.hpp -- C++ drop-in for the reference's triangle-counting entry
+// points (namespace trimatch, /root/reference/proj/include/trimatch/*.hpp),
+// header-only over the C-ABI of libtcb200.so (tcb200.h).
+//
+//   reference                                   here (namespace trimatch_gpu)
+//   EdgeList            graph.hpp:16-19         EdgeList (same fields)
+//   BuildReport         graph.hpp:22-25         BuildReport (same fields)
+//   Graph               graph.hpp:35-66         Graph (device-resident, same accessors)
+//   build_graph         graph.hpp:73            build_graph
+//   degrees             graph.hpp:75            degrees
+//   ParseError/IoError  io.hpp:13-27            ParseError / IoError
+//   parse_matrix_market io.hpp:34-35            parse_matrix_market[_file]
+//   write/read_csr_cache, is_csr_cache_file     same names (io.hpp:39-41)
+//   load_graph          io.hpp:45               load_graph
+//   MatchOptions/Result matcher.hpp:84-94       MatchOptions / MatchResult (+ per_vertex)
+//   count_triangles     matcher.hpp:128         count_triangles
+//
+// Errors map back to the exception types the reference throws:
+// TC_EINVAL -> std::invalid_argument, TC_ERANGE -> std::out_of_range,
+// TC_EPARSE -> ParseError, TC_EIO -> IoError, others -> std::runtime_error.
+// A reference user switches by replacing `trimatch::` with `trimatch_gpu::`;
+// an existing trimatch::Graph can be counted without conversion through
+// count_triangles_csr(g) (any type with num_vertices/num_edges/row_offsets/
+// neighbor_array).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <fstream>
+#include <istream>
+#include <iterator>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tcb200.h"
+
+namespace trimatch_gpu {
+
+using VertexId = std::uint32_t;
+inline constexpr VertexId kInvalidVertex = static_cast<VertexId>(-1);
+
+class ParseError : public std::runtime_error {
+ public:
+  ParseError(const std::string& message, std::uint64_t line)
+      : std::runtime_error(message + " (line " + std::to_string(line) + ")"), line_(line) {}
+  // Built from the library's already-formatted "... (line N)" message.
+  explicit ParseError(const std::string& formatted) : std::runtime_error(formatted), line_(0) {
+    const auto p = formatted.rfind("(line ");
+    if (p != std::string::npos) line_ = std::strtoull(formatted.c_str() + p + 6, nullptr, 10);
+  }
+  std::uint64_t line() const { return line_; }
+
+ private:
+  std::uint64_t line_;
+};
+
+class IoError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(tc_status s) {
+  if (s == TC_OK) return;
+  const std::string msg = tc_last_error();
+  switch (s) {
+    case TC_EINVAL: throw std::invalid_argument(msg);
+    case TC_ERANGE: throw std::out_of_range(msg);
+    case TC_EPARSE: throw ParseError(msg);
+    case TC_EIO: throw IoError(msg);
+    default: throw std::runtime_error("tcb200: " + msg);
+  }
+}
+struct GraphDeleter {
+  void operator()(tc_graph* g) const { tc_graph_destroy(g); }
+};
+}  // namespace detail
+
+struct EdgeList {
+  VertexId num_vertices_declared = 0;
+  std::vector<std::pair<VertexId, VertexId>> edges;
+};
+
+struct BuildReport {
+  std::uint64_t self_loops_removed = 0;
+  std::uint64_t duplicate_entries_removed = 0;
+};
+
+// Immutable undirected simple graph, resident on a B200 as the
+// (deg,id)-oriented CSR.  Copies share the device handle (the reference Graph
+// is safe for concurrent reads; so is this).  The symmetric CSR the accessors
+// expose is materialised on first use.
+class Graph {
+ public:
+  Graph() = default;
+  explicit Graph(tc_graph* h) : h_(h, detail::GraphDeleter{}) { detail::check(tc_graph_get_info(h, &info_)); }
+  // The reference constructor signature (graph.hpp:38-39): upload a CSR.
+  Graph(VertexId num_vertices, std::uint64_t num_edges, std::vector<std::uint64_t> row_offsets,
+        std::vector<VertexId> neighbors, int device = 0) {
+    if (row_offsets.size() != static_cast<std::size_t>(num_vertices) + 1 || row_offsets.back() != 2 * num_edges ||
+        neighbors.size() != 2 * num_edges)
+      throw std::invalid_argument("Graph: inconsistent CSR arrays");
+    tc_graph* h = nullptr;
+    detail::check(tc_graph_from_csr(row_offsets.data(), neighbors.data(), num_vertices, num_edges, device, &h));
+    h_.reset(h, detail::GraphDeleter{});
+    detail::check(tc_graph_get_info(h, &info_));
+    csr_ = std::make_shared<Csr>(Csr{std::move(row_offsets), std::move(neighbors)});
+  }
+
+  VertexId num_vertices() const { return info_.num_vertices; }
+  std::uint64_t num_edges() const { return info_.num_edges; }
+  std::uint32_t degree(VertexId u) const {
+    const auto& o = csr().off;
+    return static_cast<std::uint32_t>(o[u + 1] - o[u]);
+  }
+  std::span<const VertexId> neighbors(VertexId u) const {
+    const auto& c = csr();
+    return {c.nbrs.data() + c.off[u], c.nbrs.data() + c.off[u + 1]};
+  }
+  bool has_edge(VertexId u, VertexId v) const {
+    if (u >= num_vertices() || v >= num_vertices())
+      throw std::out_of_range("has_edge: vertex id " + std::to_string(u >= num_vertices() ? u : v) +
+                              " out of range");
+    auto nb = neighbors(u);
+    auto it = std::lower_bound(nb.begin(), nb.end(), v);
+    return it != nb.end() && *it == v;
+  }
+  const std::vector<std::uint64_t>& row_offsets() const { return csr().off; }
+  const std::vector<VertexId>& neighbor_array() const { return csr().nbrs; }
+
+  tc_graph* handle() const { return h_.get(); }
+  const tc_graph_info& info() const { return info_; }
+
+ private:
+  struct Csr {
+    std::vector<std::uint64_t> off;
+    std::vector<VertexId> nbrs;
+  };
+  const Csr& csr() const {
+    if (!csr_) {
+      auto c = std::make_shared<Csr>();
+      c->off.resize(static_cast<std::size_t>(num_vertices()) + 1);
+      c->nbrs.resize(2 * num_edges());
+      detail::check(tc_graph_export_csr(h_.get(), c->off.data(), c->nbrs.data()));
+      csr_ = std::move(c);
+    }
+    return *csr_;
+  }
+  std::shared_ptr<tc_graph> h_;
+  tc_graph_info info_{};
+  mutable std::shared_ptr<Csr> csr_;
+};
+
+using DegreeArray = std::vector<std::uint32_t>;
+
+inline Graph build_graph(const EdgeList& edges, BuildReport* report = nullptr, int device = 0) {
+  static_assert(sizeof(std::pair<VertexId, VertexId>) == 8, "EdgeList pairs must be two packed u32");
+  tc_graph* h = nullptr;
+  tc_build_report rep{};
+  detail::check(tc_graph_build(reinterpret_cast<const std::uint32_t*>(edges.edges.data()), edges.edges.size(),
+                               edges.num_vertices_declared, device, &h, &rep));
+  if (report) {
+    report->self_loops_removed = rep.self_loops_removed;
+    report->duplicate_entries_removed = rep.duplicate_entries_removed;
+  }
+  return Graph(h);
+}
+
+inline DegreeArray degrees(const Graph& g) {
+  DegreeArray d(g.num_vertices());
+  detail::check(tc_graph_degrees(g.handle(), d.data()));
+  return d;
+}
+
+// ---- io ------------------------------------------------------------------------
+
+inline EdgeList parse_matrix_market(std::istream& in) {
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  std::uint32_t* pairs = nullptr;
+  std::uint64_t m = 0;
+  std::uint32_t n = 0;
+  detail::check(tc_parse_matrix_market(text.data(), text.size(), &pairs, &m, &n));
+  EdgeList el;
+  el.num_vertices_declared = n;
+  el.edges.resize(m);
+  for (std::uint64_t i = 0; i < m; ++i) el.edges[i] = {pairs[2 * i], pairs[2 * i + 1]};
+  tc_free(pairs);
+  return el;
+}
+
+inline EdgeList parse_matrix_market_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("cannot open '" + path + "' for reading");
+  return parse_matrix_market(in);
+}
+
+inline bool is_csr_cache_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  char magic[8] = {};
+  in.read(magic, 8);
+  return in.gcount() == 8 && std::string(magic, 8) == "TRIMCSR1";
+}
+
+inline Graph read_csr_cache(const std::string& path, int device = 0) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("cannot open '" + path + "' for reading");
+  std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  tc_graph* h = nullptr;
+  detail::check(tc_csr_cache_to_graph(bytes.data(), bytes.size(), device, &h));
+  return Graph(h);
+}
+
+inline void write_csr_cache(const std::string& path, const Graph& g) {
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw IoError("cannot open '" + path + "' for writing");
+  auto put64 = [&](std::uint64_t v) {
+    char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xFF);
+    out.write(b, 8);
+  };
+  out.write("TRIMCSR1", 8);
+  put64(1);
+  put64(g.num_vertices());
+  put64(g.num_edges());
+  for (std::uint64_t o : g.row_offsets()) put64(o);
+  for (VertexId v : g.neighbor_array()) {
+    char b[4];
+    for (int i = 0; i < 4; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xFF);
+    out.write(b, 4);
+  }
+  if (!out) throw IoError("write failed for '" + path + "'");
+}
+
+inline Graph load_graph(const std::string& path, BuildReport* report = nullptr, int device = 0) {
+  if (is_csr_cache_file(path)) {
+    if (report) *report = BuildReport{};
+    return read_csr_cache(path, device);
+  }
+  return build_graph(parse_matrix_market_file(path), report, device);
+}
+
+// ---- matcher -------------------------------------------------------------------
+
+struct ExecPolicy {
+  unsigned workers = 0;  // accepted for source compatibility; the GPU ignores it
+};
+
+struct MatchOptions {
+  int lookahead = 2;  // validated (0..2); count-neutral on the GPU path
+  bool keep_listings = false;  // not supported on the GPU path (throws)
+  ExecPolicy exec{};
+  bool per_vertex = false;  // GPU extension: triangles per vertex
+  std::uint32_t part_index = 0, part_count = 1;  // multi-GPU split
+};
+
+struct MatchStats {
+  double filter_millis = 0.0;  // the oriented CSR is built at graph construction
+  double verify_millis = 0.0;  // device time of the count (advance + join + reduce)
+  std::uint64_t candidates = 0;
+  std::uint64_t wedges = 0, items = 0;
+  double total_millis() const { return filter_millis + verify_millis; }
+};
+
+struct MatchResult {
+  std::uint64_t count = 0;
+  std::optional<std::vector<std::uint64_t>> per_vertex;
+  MatchStats stats;
+};
+
+inline MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}) {
+  if (opts.keep_listings) throw std::runtime_error("keep_listings is not supported on the GPU path");
+  tc_count_opts o{};
+  o.lookahead = opts.lookahead;
+  o.part_index = opts.part_index;
+  o.part_count = opts.part_count;
+  o.sync = 1;
+  MatchResult r;
+  tc_count_stats st{};
+  std::vector<std::uint64_t> pv;
+  if (opts.per_vertex) pv.resize(g.num_vertices());
+  detail::check(tc_count(g.handle(), &o, &r.count, opts.per_vertex ? pv.data() : nullptr, &st));
+  if (opts.per_vertex) r.per_vertex = std::move(pv);
+  r.stats.verify_millis = st.total_ms;
+  r.stats.wedges = st.wedges;
+  r.stats.items = st.items;
+  r.stats.candidates = st.pivots;
+  return r;
+}
+
+// Count an existing reference-style graph object (trimatch::Graph or anything
+// exposing the same accessors) without converting it by hand.
+template <typename G>
+MatchResult count_triangles_csr(const G& g, const MatchOptions& opts = {}, int device = 0) {
+  tc_graph* h = nullptr;
+  detail::check(tc_graph_from_csr(g.row_offsets().data(), g.neighbor_array().data(), g.num_vertices(),
+                                  g.num_edges(), device, &h));
+  Graph dg(h);
+  return count_triangles(dg, opts);
+}
+
+}  // namespace trimatch_gpu
