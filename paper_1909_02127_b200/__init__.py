@@ -32,7 +32,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtcb200.so")
+LIB_PATH = os.environ.get("TCB200_LIB") or os.path.join(_HERE, "libtcb200.so")  # TCB200_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -126,6 +126,7 @@ void destroy_handle(tc_graph* g) {
     g->offH.release();
     g->fr_items.release();
     g->fr_e.release();
+    g->fr_moff.release();
     g->fr_in.release();
     g->fr_wsegs.release();
     g->fr_csegs.release();

@@ -44,6 +44,14 @@ constexpr int kJoinWarps = kJoinThreads / 32;
 constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= 48)
 constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counters (16-bit halves: 16 KB)
 constexpr uint32_t kCtaSmemSlots = 1024;     // cold-member hash table in SMEM (4 KB)
+#ifndef TCB_HOT_WIN
+#define TCB_HOT_WIN 2
+#endif
+#ifndef TCB_MIN_BLOCKS
+#define TCB_MIN_BLOCKS 5  // per-vertex build; the total-only build targets one more (A/B: profiles/README.md)
+#endif
+constexpr int kHotWin = TCB_HOT_WIN;              // hot chunk loads in flight per lane
+constexpr int kCtaMinBlocks = TCB_MIN_BLOCKS;     // CTA-bin kernel residency target
 
 __host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t members) {
   uint32_t t = 32;  // load factor <= 1/2
@@ -172,27 +180,20 @@ __device__ __forceinline__ uint32_t hot_u16(const uint4& q, int i) {
   return (i & 1) ? (w >> 16) : (w & 0xffffu);
 }
 
-template <bool kPerVertex, typename Sink>
-__device__ __forceinline__ uint32_t probe_hot(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
-                                              const uint32_t* bm, uint32_t h0, const Sink& sink) {
+// Hit mask (bit i = element i of chunk c is in [b,e) and a member of N+(v)).
+__device__ __forceinline__ uint32_t hot_hit_mask(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
+                                                 const uint32_t* bm) {
   const uint32_t p0 = c << 3;
   const uint32_t lo = b > p0 ? b - p0 : 0u;
   const uint32_t hi = e - p0 < 8u ? e - p0 : 8u;
   const uint32_t valid = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
   uint32_t hits = 0;
-  uint32_t y[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    y[i] = hot_u16(q, i);
-    hits |= ((bm[y[i] >> 5] >> (y[i] & 31)) & 1u) << i;
+    const uint32_t y = hot_u16(q, i);
+    hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
   }
-  hits &= valid;
-  if (kPerVertex && hits) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (hits & (1u << i)) sink.hit(y[i] + h0);
-  }
-  return __popc(hits);
+  return hits & valid;
 }
 
 // 4 cold ids (32-bit) per chunk: hash probes.
@@ -227,29 +228,12 @@ __device__ __forceinline__ uint32_t item_of(uint32_t w, uint32_t nch, uint32_t p
   return k < 32 ? k : 31;
 }
 
-// Per-item hit counts of one chunk window: lanes holding chunks of the same
-// item are a contiguous run (item index is non-decreasing in the lane), so a
-// 5-step segmented suffix sum leaves each run's total in its head lane -- one
-// SMEM atomic per item run instead of one per lane.
-__device__ __forceinline__ void add_item_counts(uint32_t* cnt, const uint16_t* sidx, bool valid, uint32_t k,
-                                                uint32_t x) {
-  const unsigned lane = lane_id();
-  const uint32_t key = valid ? k : 0xffffffffu;
-  uint32_t v = valid ? x : 0u;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t = __shfl_down_sync(0xffffffffu, v, d);
-    const uint32_t k2 = __shfl_down_sync(0xffffffffu, key, d);
-    if (lane + d < 32 && k2 == key) v += t;
-  }
-  const uint32_t kp = __shfl_up_sync(0xffffffffu, key, 1);
-  if (valid && v && (lane == 0 || kp != key)) atomicAdd(&cnt[sidx ? sidx[k] : k], v);
-}
-
 // A warp walks chunk range [fb, fe) of a segment list staged in SMEM (item i:
 // chunk start pre[i] (pre[ni] = total), element range [sb[i], se[i]), original
-// index sidx[i]), two chunks per lane in flight.  fn(q, c, b, e) -> hits.
-template <int kIdsPerChunk, typename T, typename ChunkFn>
+// index sidx[i]), kWin windows of 32 chunks per step: every window's chunk is
+// mapped to its item first, then all kWin int4 loads are issued, then probed
+// (kWin loads in flight per lane).  fn(q, c, b, e, k) -> hits.
+template <int kIdsPerChunk, int kWin, typename T, typename ChunkFn>
 __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t ni, const uint32_t* pre,
                                               const uint32_t* sb, const uint32_t* se, const uint16_t* sidx,
                                               uint32_t* icnt, const T* base, ChunkFn fn) {
@@ -264,37 +248,35 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
     if (pre[mid] <= fb) lo = mid; else hi = mid;
   }
   uint32_t k0 = lo;
-  for (uint32_t f = fb; f < fe; f += 64) {
-    // window A = [f, f+32), window B = [f+32, f+64)
-    uint32_t j = k0 + 1 + lane;
-    uint32_t st = pre[min(j, ni)];
-    uint32_t bit = (j < ni && st < f + 32) ? (1u << (st - f)) : 0u;
-    const uint32_t mA = __reduce_or_sync(0xffffffffu, bit);
-    const uint32_t kA = k0 + __popc(mA & ((2u << lane) - 1u));
-    const uint32_t k1 = k0 + __popc(__ballot_sync(0xffffffffu, j < ni && st <= f + 32));
-    j = k1 + 1 + lane;
-    st = pre[min(j, ni)];
-    bit = (j < ni && st < f + 64) ? (1u << (st - f - 32)) : 0u;
-    const uint32_t mB = __reduce_or_sync(0xffffffffu, bit);
-    const uint32_t kB = k1 + __popc(mB & ((2u << lane) - 1u));
-    k0 = k1 + __popc(__ballot_sync(0xffffffffu, j < ni && st <= f + 64));
-    const uint32_t fA = f + lane, fB = f + 32 + lane;
-    const bool vA = fA < fe, vB = fB < fe;
-    const uint32_t kAc = vA ? kA : 0, kBc = vB ? kB : 0;
-    const uint32_t bA = sb[kAc], eA = se[kAc], cA = (bA >> kShift) + (fA - pre[kAc]);
-    const uint32_t bB = sb[kBc], eB = se[kBc], cB = (bB >> kShift) + (fB - pre[kBc]);
-    uint4 qA = make_uint4(0, 0, 0, 0), qB = make_uint4(0, 0, 0, 0);
-    if (vA) qA = __ldg(base4 + cA);
-    if (vB) qB = __ldg(base4 + cB);
-    if (vA) {
-      const uint32_t x = fn(qA, cA, bA, eA);
-      h += x;
-      if (icnt && x) atomicAdd(&icnt[sidx[kAc]], x);
+  for (uint32_t f = fb; f < fe; f += 32 * kWin) {
+    uint32_t kk[kWin], bb[kWin], ee[kWin], cc[kWin];
+    bool vv[kWin];
+    uint4 qq[kWin];
+#pragma unroll
+    for (int w = 0; w < kWin; ++w) {
+      const uint32_t fw = f + 32 * w;
+      const uint32_t j = k0 + 1 + lane;  // items starting inside (fw, fw+32)
+      const uint32_t st = pre[min(j, ni)];
+      const uint32_t bit = (j < ni && st < fw + 32) ? (1u << (st - fw)) : 0u;
+      const uint32_t m = __reduce_or_sync(0xffffffffu, bit);
+      const uint32_t k = k0 + __popc(m & ((2u << lane) - 1u));
+      k0 += __popc(__ballot_sync(0xffffffffu, j < ni && st <= fw + 32));  // item holding fw+32
+      const uint32_t fl = fw + lane;
+      vv[w] = fl < fe;
+      kk[w] = vv[w] ? k : 0;
+      bb[w] = sb[kk[w]];
+      ee[w] = se[kk[w]];
+      cc[w] = (bb[w] >> kShift) + (fl - pre[kk[w]]);
     }
-    if (vB) {
-      const uint32_t x = fn(qB, cB, bB, eB);
-      h += x;
-      if (icnt && x) atomicAdd(&icnt[sidx[kBc]], x);
+#pragma unroll
+    for (int w = 0; w < kWin; ++w) qq[w] = vv[w] ? __ldg(base4 + cc[w]) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int w = 0; w < kWin; ++w) {
+      if (vv[w]) {
+        const uint32_t x = fn(qq[w], cc[w], bb[w], ee[w], kk[w]);
+        h += x;
+        if (icnt && x) atomicAdd(&icnt[sidx[kk[w]]], x);
+      }
     }
   }
   return h;
@@ -412,15 +394,16 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 //      probed in the hash;
 //   3. clear the touched bitmap words / table slots, flush per-item counts.
 // Segments come from a global queue, heaviest (top-rank pivots) first.
-// Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots][pv: ncnt counters].
+// Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots].
 template <bool kPerVertex>
-__global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
+__global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCtaMinBlocks + 1) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
     const uint16_t* __restrict__ colH, const uint4* __restrict__ items, const uint32_t* __restrict__ item_e,
     const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t h0, uint32_t nbm,
-    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, uint32_t rc, uint32_t ncnt,
-    unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
+    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, const uint64_t* __restrict__ moff_e, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
+    unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
+  __shared__ unsigned long long s_hmo[kPerVertex ? kCtaSegItems : 1];  // hot items' mask offsets
   __shared__ uint32_t s_hb[kCtaSegItems], s_he[kCtaSegItems], s_hpre[kCtaSegItems + 1];
   __shared__ uint32_t s_cb[kCtaSegItems], s_ce[kCtaSegItems], s_cpre[kCtaSegItems + 1];
   __shared__ uint16_t s_hidx[kCtaSegItems], s_cidx[kCtaSegItems];
@@ -429,19 +412,16 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
   __shared__ unsigned long long s_ctot;
   uint32_t* bm = dyn;
   uint32_t* stab = dyn + nbm;
-  uint32_t* top_cnt = dyn + nbm + kCtaSmemSlots;
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
-  if (kPerVertex) {
-    for (uint32_t i = threadIdx.x; i < ncnt / 2; i += kJoinThreads) top_cnt[i] = 0;
+  if (kPerVertex)
     for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kJoinThreads) s_icnt[i] = 0;
-  }
-  const PvSink<true> sink{top_cnt, rc, t_rank, g_pv_dbg};
+  // cold hits (x < h0) go straight to global atomics; hot hits leave as masks
+  const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
-  uint32_t since_flush = 0;  // items since the last counter flush (bounds every 16-bit half)
   while (true) {
     if (threadIdx.x == 0) {
       s_seg = atomicAdd(queue, 1u);
@@ -453,15 +433,6 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
     if (q >= nsegs) break;
     const uint4 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
     const uint32_t v = sg.x, i0 = sg.y, ni = sg.z - sg.y;
-    if (kPerVertex) {
-      // one segment adds at most ni to any counter: flush before a half could wrap
-      if (since_flush + ni > 0xffffu) {
-        flush_top<true>(top_cnt, ncnt, rc, t_rank);
-        since_flush = 0;
-        __syncthreads();
-      }
-      since_flush += ni;
-    }
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     // (1a) hot members -> bitmap; s_cold = #members below h0 (sorted prefix)
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
@@ -502,6 +473,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
           s_hb[ph] = it[r].x;
           s_he[ph] = it[r].y;
           s_hpre[ph] = ch;
+          if (kPerVertex) s_hmo[ph] = moff_e[item_e[i0 + i]];
           s_hidx[ph] = (uint16_t)i;
           ++ph;
           ch += nh[r];
@@ -541,16 +513,21 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
     if (!(g_pv_dbg & 4)) {
       const uint32_t fb = (uint32_t)(((uint64_t)tchunks_h * warp) / kJoinWarps);
       const uint32_t fe = (uint32_t)(((uint64_t)tchunks_h * (warp + 1)) / kJoinWarps);
-      h += warp_walk<8>(fb, fe, nhot, s_hpre, s_hb, s_he, s_hidx, icnt, colH,
-                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e) {
-                          return probe_hot<kPerVertex>(qq, c, b, e, bm, h0, sink);
-                        });
+      // per-vertex: the hot chunk's 8-bit hit mask goes to HBM (one byte store,
+      // coalesced across the lanes of an item); k_pv_rows turns the masks into
+      // t[u] and t[x] row by row, with no per-hit atomics
+      h += warp_walk<8, kHotWin>(fb, fe, nhot, s_hpre, s_hb, s_he, s_hidx, nullptr, colH,
+                                 [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t k) {
+                                   const uint32_t m = hot_hit_mask(qq, c, b, e, bm);
+                                   if (kPerVertex) masks[s_hmo[k] + (c - (b >> 3))] = (uint8_t)m;
+                                   return (uint32_t)__popc(m);
+                                 });
     }
     if (ncold && !(g_pv_dbg & 4)) {
       const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kJoinWarps);
       const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kJoinWarps);
-      h += warp_walk<4>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
-                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e) {
+      h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
+                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
                           return probe_cold<kPerVertex>(qq, c, b, e, tab, tmask, tshift, sink);
                         });
     }
@@ -578,10 +555,230 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_cta(
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
-  if (kPerVertex) {
-    __syncthreads();
-    flush_top<true>(top_cnt, ncnt, rc, t_rank);
+}
+
+// Per-vertex counts from the CTA bin's hot hit masks, one warp per row u.
+// Mask byte (item k, chunk c) has bit j set iff element 8c+j of colH -- an
+// oriented edge u->x -- closed a triangle (u, v_k, x).  For each hot position
+// p of row u, B[p] = sum over u's items of that bit = the triangles whose
+// low->top edge is u->x_p; then t[x_p] += B[p] and t[u] += sum_p B[p].  Lanes own
+// 4 chunks each of a 128-chunk group (coalesced: chunk cg + lane + 32t); each
+// item's byte is spread into 4+4 byte-lane counters by a multiply
+// (b*0x00204081 & 0x01010101), so a row item costs a few instructions per 8
+// positions instead of a per-hit atomic.  Item headers (first chunk, mask
+// offset) are staged per warp in SMEM and read as broadcasts.  Items of a row
+// start at non-decreasing chunks, so a group stops at the first item that
+// starts past it.  Only edges in [pe0, pe1) (this part's range) count.  Rows
+// are taken from the top rank down.
+#ifndef TCB_ROW_MINB
+#define TCB_ROW_MINB 3
+#endif
+#ifndef TCB_ROW_UNROLL
+#define TCB_ROW_UNROLL 4
+#endif
+constexpr int kRowChunksPerLane = 4;
+constexpr int kRowItemUnroll = TCB_ROW_UNROLL;
+constexpr int kRowWarps = 8;
+__global__ void __launch_bounds__(kRowWarps * 32, TCB_ROW_MINB) k_pv_rows(
+    const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
+    const uint64_t* __restrict__ moff_e, const uint8_t* __restrict__ masks, uint32_t n, uint32_t h0, uint32_t rc, uint32_t ncnt, uint64_t pe0,
+    uint64_t pe1, unsigned int* __restrict__ queue, unsigned long long* __restrict__ t_rank) {
+  extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
+  __shared__ uint32_t s_hc[kRowWarps][32];
+  __shared__ unsigned long long s_mo[kRowWarps][32];
+  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
+  __syncthreads();
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
+  constexpr uint32_t kGroup = 32 * kRowChunksPerLane;
+  while (true) {
+    // 32 rows per queue grab (most rows have no hot suffix): one atomic per
+    // batch, the rows with work taken in order from a ballot
+    uint32_t rb = 0;
+    if (lane == 0) rb = atomicAdd(queue, 32u);
+    rb = __shfl_sync(0xffffffffu, rb, 0);
+    if (rb >= n) break;
+    const uint32_t rl = rb + lane;
+    uint32_t ul = 0, hsl = 0, hel = 0;
+    uint64_t e0l = 0, e1l = 0;
+    if (rl < n) {
+      ul = n - 1 - rl;
+      hsl = offH[ul];
+      hel = offH[ul + 1];
+      e0l = max((uint64_t)off[ul], pe0);
+      e1l = min((uint64_t)off[ul + 1], pe1);
+    }
+    uint32_t rows = __ballot_sync(0xffffffffu, hsl != hel && e0l < e1l);
+  while (rows) {
+    const int rj = __ffs(rows) - 1;
+    rows &= rows - 1;
+    const uint32_t u = __shfl_sync(0xffffffffu, ul, rj);
+    const uint32_t hs = __shfl_sync(0xffffffffu, hsl, rj), he = __shfl_sync(0xffffffffu, hel, rj);
+    const uint64_t e0 = __shfl_sync(0xffffffffu, (unsigned long long)e0l, rj);
+    const uint64_t e1 = __shfl_sync(0xffffffffu, (unsigned long long)e1l, rj);
+    const uint32_t c_lo = hs >> 3, c_hi = (he + 7) >> 3;
+    unsigned long long row_total = 0;
+    // stage the row's items [eb, eb+32) that have hot chunks -> warp SMEM slots
+    auto stage = [&](uint64_t eb) -> uint32_t {
+      // an item's masks run from its first hot chunk to the row's last, so
+      // its length in the edge-ordered offsets gives the first chunk
+      const uint64_t e = eb + lane;
+      unsigned long long mo = 0;
+      uint32_t len = 0;
+      if (e < e1) {
+        mo = moff_e[e];
+        len = (uint32_t)(moff_e[e + 1] - mo);
+      }
+      const bool has = len > 0;
+      const uint32_t hc = c_hi - len;
+      const uint32_t vm = __ballot_sync(0xffffffffu, has);
+      __syncwarp();
+      if (has) {
+        const uint32_t slot = __popc(vm & lanemask_lt());
+        s_hc[warp][slot] = hc;
+        s_mo[warp][slot] = mo;
+      }
+      __syncwarp();
+      return __popc(vm);
+    };
+    if (c_hi - c_lo <= 32) {
+      // narrow row: sub-groups of w = pow2 >= chunks lanes, each sub-group on
+      // its own item (one chunk per lane), counts summed across sub-groups
+      const uint32_t lg = 32 - __clz(c_hi - c_lo - 1), w = 1u << lg;  // w >= chunks
+      const uint32_t ipl = 32u >> lg, sub = lane >> lg;
+      const uint32_t c = c_lo + (lane & (w - 1));
+      const bool cvalid = c < c_hi;
+      uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
+      uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      auto flush1 = [&]() {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
+          cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
+        }
+        acc_lo = acc_hi = 0;
+        nacc = 0;
+      };
+      for (uint64_t eb = e0; eb < e1; eb += 32) {
+        const uint32_t nb = stage(eb);
+        for (uint32_t j = 0; j < nb; j += ipl * kRowItemUnroll) {
+          if (nacc + kRowItemUnroll > 255) flush1();
+          uint32_t bits[kRowItemUnroll];
+#pragma unroll
+          for (int k = 0; k < kRowItemUnroll; ++k) {
+            const uint32_t jj = j + k * ipl + sub;
+            bits[k] = 0;
+            if (jj < nb && cvalid) {
+              const uint32_t hj = s_hc[warp][jj];
+              if (c >= hj) bits[k] = masks[s_mo[warp][jj] + (c - hj)];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kRowItemUnroll; ++k) {
+            acc_lo += ((bits[k] & 0xfu) * 0x00204081u) & 0x01010101u;
+            acc_hi += ((bits[k] >> 4) * 0x00204081u) & 0x01010101u;
+          }
+          nacc += kRowItemUnroll;
+        }
+      }
+      flush1();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        for (uint32_t o = w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
+      if (sub == 0 && cvalid) {
+        const uint4 q = colH4[c];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t p = (c << 3) + j;
+          if (cnt[j] && p >= hs && p < he) {
+            const uint32_t x = h0 + hot_u16(q, j);
+            if (x >= rc) atomicAdd(&top[x - rc], cnt[j]);
+            else atomicAdd(&t_rank[x], (unsigned long long)cnt[j]);
+            row_total += cnt[j];
+          }
+        }
+      }
+    } else
+    for (uint32_t cg = c_lo; cg < c_hi; cg += kGroup) {
+      uint32_t acc_lo[kRowChunksPerLane], acc_hi[kRowChunksPerLane], cnt[kRowChunksPerLane][8];
+#pragma unroll
+      for (int t = 0; t < kRowChunksPerLane; ++t) {
+        acc_lo[t] = acc_hi[t] = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cnt[t][j] = 0;
+      }
+      uint32_t nacc = 0;
+      auto flush = [&]() {
+#pragma unroll
+        for (int t = 0; t < kRowChunksPerLane; ++t) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            cnt[t][j] += (acc_lo[t] >> (8 * j)) & 0xffu;
+            cnt[t][4 + j] += (acc_hi[t] >> (8 * j)) & 0xffu;
+          }
+          acc_lo[t] = acc_hi[t] = 0;
+        }
+        nacc = 0;
+      };
+      bool done = false;
+      for (uint64_t eb = e0; eb < e1 && !done; eb += 32) {
+        const uint32_t nb = stage(eb);
+        // kRowItemUnroll items per step: all their byte loads are in flight
+        // together (the loop is load-latency bound, not issue bound)
+        for (uint32_t j = 0; j < nb && !done; j += kRowItemUnroll) {
+          if (nacc + kRowItemUnroll > 255) flush();
+          uint32_t bits[kRowItemUnroll][kRowChunksPerLane];
+#pragma unroll
+          for (int k = 0; k < kRowItemUnroll; ++k) {
+            uint32_t hj = 0xffffffffu;
+            unsigned long long mj = 0;
+            if (j + k < nb) {
+              hj = s_hc[warp][j + k];
+              mj = s_mo[warp][j + k];
+            }
+            if (j + k < nb && hj >= cg + kGroup) done = true;  // starts are non-decreasing
+#pragma unroll
+            for (int t = 0; t < kRowChunksPerLane; ++t) {
+              const uint32_t c = cg + lane + 32 * t;
+              bits[k][t] = (hj != 0xffffffffu && c >= hj && c < c_hi) ? masks[mj + (c - hj)] : 0u;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kRowItemUnroll; ++k) {
+#pragma unroll
+            for (int t = 0; t < kRowChunksPerLane; ++t) {
+              acc_lo[t] += ((bits[k][t] & 0xfu) * 0x00204081u) & 0x01010101u;
+              acc_hi[t] += ((bits[k][t] >> 4) * 0x00204081u) & 0x01010101u;
+            }
+          }
+          nacc += kRowItemUnroll;
+        }
+      }
+      flush();
+#pragma unroll
+      for (int t = 0; t < kRowChunksPerLane; ++t) {
+        const uint32_t c = cg + lane + 32 * t;
+        if (c >= c_hi) continue;
+        const uint4 q = colH4[c];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t p = (c << 3) + j;
+          if (cnt[t][j] && p >= hs && p < he) {
+            const uint32_t x = h0 + hot_u16(q, j);
+            if (x >= rc) atomicAdd(&top[x - rc], cnt[t][j]);
+            else atomicAdd(&t_rank[x], (unsigned long long)cnt[t][j]);
+            row_total += cnt[t][j];
+          }
+        }
+      }
+    }
+    row_total = warp_sum(row_total);
+    if (lane == 0 && row_total) atomicAdd(&t_rank[u], row_total);
   }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x)
+    if (top[i]) atomicAdd(&t_rank[rc + i], (unsigned long long)top[i]);
 }
 
 __global__ void k_gather_pv(const unsigned long long* __restrict__ t_rank, const uint32_t* __restrict__ rank_of,
@@ -676,10 +873,13 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const uint4* csegs = g.fr_csegs.get();
   uint64_t NSW = g.fr_nwsegs, NSC = g.fr_ncsegs;
   DBuf<uint4> pw, pc;
+  uint64_t part_e0 = 0, part_e1 = E;
   if (parts > 1 && E) {
     if (g.cached_parts != parts) kl += 4;
     const std::vector<uint64_t>& b = partition_bounds(g, parts);
-    part_segments(g, b[part], b[part + 1], pw, NSW, pc, NSC);
+    part_e0 = b[part];
+    part_e1 = b[part + 1];
+    part_segments(g, part_e0, part_e1, pw, NSW, pc, NSC);
     kl += 6;
     wsegs = pw.get();
     csegs = pc.get();
@@ -694,7 +894,6 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const uint32_t top_cnt = env_u32("TCB_TOP_COUNTERS", kTopCounters);
   const uint32_t smem_slots = std::min(env_u32("TCB_SMEM_SLOTS", kCtaSmemSlots), kCtaSmemSlots);
   const uint32_t ncnt = pv ? ((n < top_cnt ? n : top_cnt) & ~1u) : 0;
-  const uint32_t rc = pv ? n - ncnt : 0xffffffffu;
   {
     const uint32_t dbg = env_u32("TCB_PV_DBG", 0);
     TC_CUDA(cudaMemcpyToSymbolAsync(g_pv_dbg, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, s));
@@ -722,7 +921,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     // than smem_slots/2 members below h0
     const uint32_t cap = table_size_for(g.max_dplus);
     const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
-    const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt / 2) * sizeof(uint32_t);
+    const size_t dsm = ((size_t)nbm + kCtaSmemSlots) * sizeof(uint32_t);
     auto kern = pv ? k_join_cta<true> : k_join_cta<false>;
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     int occ = 0;
@@ -730,11 +929,28 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     if (occ < 1) occ = 1;
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, NSC);
     DBuf<uint32_t> slab((uint64_t)grid * slab_cap + 1, s);
+    DBuf<uint8_t> masks;
+    if (pv) masks.alloc(g.fr_mask_bytes + 32, s);  // every byte a segment owns is written by the join
     kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), g.colH.get(), g.fr_items.get(),
                                         g.fr_e.get(), csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
-                                        slab_cap, slab.get(), rc, ncnt, t_rank.get(), acc.get());
+                                        slab_cap, slab.get(), g.fr_moff.get(), masks.get(), t_rank.get(),
+                                        acc.get());
     TC_LAUNCH();
     ++launches;
+    if (pv) {
+      // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics)
+      DBuf<unsigned int> rq(1, s);
+      TC_CUDA(cudaMemsetAsync(rq.get(), 0, sizeof(unsigned int), s));
+      const uint32_t rcnt = n < top_cnt ? n : top_cnt;
+      const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
+      TC_CUDA(cudaFuncSetAttribute(k_pv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      int rocc = 0;
+      TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rocc, k_pv_rows, kRowWarps * 32, rsm));
+      k_pv_rows<<<(unsigned)(sms * std::max(rocc, 1)), kRowWarps * 32, rsm, s>>>(
+          g.off.get(), g.colH.get(), g.offH.get(), g.fr_moff.get(), masks.get(), n, g.h0, n - rcnt, rcnt, part_e0, part_e1, rq.get(), t_rank.get());
+      TC_LAUNCH();
+      ++launches;
+    }
   }
   TC_CUDA(cudaEventRecord(ev.e[2], s));
 

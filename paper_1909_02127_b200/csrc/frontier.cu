@@ -68,7 +68,7 @@ struct NotSentinel {
 __global__ void k_fr_items(const uint64_t* __restrict__ keys, uint64_t NI, int be, const uint32_t* __restrict__ off,
                            const uint32_t* __restrict__ src, const uint32_t* __restrict__ offH, uint32_t h0,
                            uint4* __restrict__ items, uint32_t* __restrict__ item_e, uint32_t* __restrict__ cnt,
-                           Sums* __restrict__ sums) {
+                           uint32_t* __restrict__ item_of_e, Sums* __restrict__ sums) {
   const uint64_t emask = (1ull << be) - 1;
   unsigned long long J = 0, H = 0, IC = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -97,6 +97,7 @@ __global__ void k_fr_items(const uint64_t* __restrict__ keys, uint64_t NI, int b
         }
         H += it.y - it.x;
         ++IC;
+        item_of_e[e] = (uint32_t)i;
       }
       items[i] = it;
       item_e[i] = e;
@@ -113,6 +114,25 @@ __global__ void k_fr_items(const uint64_t* __restrict__ keys, uint64_t NI, int b
     atomicAdd(&sums->items_c, IC);
   }
 }
+
+// Per-vertex hit masks (count.cu): one byte per hot chunk of every CTA-bin item.
+// Mask bytes of oriented edge e's CTA-bin item (0 if none / warp bin).  The
+// scan runs in edge order, so each row's masks are contiguous: the per-vertex
+// row pass (count.cu k_pv_rows) streams them instead of gathering per item.
+struct MaskBytes {
+  const uint4* items;
+  const uint32_t* item_of_e;
+  const uint32_t* off;
+  const uint32_t* col;
+  __device__ __forceinline__ uint64_t operator()(uint64_t e) const {
+    const uint32_t i = item_of_e[e];
+    if (i == 0xffffffffu) return 0;
+    const uint32_t v = col[e];
+    if (off[v + 1] - off[v] <= kWarpMaxDeg) return 0;
+    const uint4 it = items[i];
+    return it.y > it.x ? (uint64_t)(((it.y + 7) >> 3) - (it.x >> 3)) : 0ull;
+  }
+};
 
 // Per-pivot item range of a part: [lo, hi) within [in[v], in[v+1]).
 struct PartRange {
@@ -232,17 +252,27 @@ void build_frontier(tc_graph& g) {
     uint64_t* sorted = radix_sort_u64(k1.get(), k2.get(), E, 0, bv + be, s);
     g.fr_items.alloc(NI ? NI : 1, s);
     g.fr_e.alloc(NI ? NI : 1, s);
+    DBuf<uint32_t> item_of_e(E, s);  // CTA-bin item of edge e (~0 if none); build-time only
+    TC_CUDA(cudaMemsetAsync(item_of_e.get(), 0xff, E * sizeof(uint32_t), s));
     DBuf<uint32_t> cnt(n ? n : 1, s);
     TC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
     if (NI) {
       k_fr_items<<<grid_gs(NI, dev), kT, 0, s>>>(sorted, NI, be, g.off.get(), g.src.get(), g.offH.get(), g.h0,
-                                                 g.fr_items.get(), g.fr_e.get(), cnt.get(), sums.get());
+                                                 g.fr_items.get(), g.fr_e.get(), cnt.get(), item_of_e.get(),
+                                                 sums.get());
       TC_LAUNCH();
     }
     scan_exclusive<uint32_t>(LoadArray<uint32_t>{cnt.get()}, g.fr_in.get(), n, g.fr_in.get() + n, s);
+    // per-vertex hit-mask layout: one byte per hot chunk of every CTA-bin
+    // item, in edge order (fr_moff[e], E+1 entries)
+    g.fr_moff.alloc(E + 1, s);
+    scan_exclusive<uint64_t>(MaskBytes{g.fr_items.get(), item_of_e.get(), g.off.get(), g.col.get()},
+                             g.fr_moff.get(), E, g.fr_moff.get() + E, s);
+    g.fr_mask_bytes = read_scalar(g.fr_moff.get() + E, s);
   } else {
     g.fr_items.alloc(1, s);
     g.fr_e.alloc(1, s);
+    g.fr_moff.alloc(1, s);
     TC_CUDA(cudaMemsetAsync(g.fr_in.get(), 0, sizeof(uint32_t) * ((uint64_t)n + 1), s));
   }
   g.fr_nitems = NI;

@@ -48,6 +48,11 @@ struct tc_graph {
   //   fr_wsegs / fr_csegs = {v, i0, i1, 0} work segments per bin (whole graph)
   tcb::DBuf<uint4> fr_items;
   tcb::DBuf<uint32_t> fr_e, fr_in;
+  //   fr_moff[e] = byte offset of edge e's per-vertex hit masks (1 byte per
+  //   hot chunk of its CTA-bin item), exclusive scan in edge order (E+1), so
+  //   a row's masks are contiguous and an item's length gives its first chunk
+  tcb::DBuf<uint64_t> fr_moff;
+  uint64_t fr_mask_bytes = 0;
   tcb::DBuf<uint4> fr_wsegs, fr_csegs;
   uint64_t fr_nitems = 0, fr_nwsegs = 0, fr_ncsegs = 0, fr_pivots = 0;
   uint64_t fr_W = 0, fr_J = 0, fr_hot = 0, fr_nitems_c = 0;
