@@ -370,9 +370,13 @@ def main():
     d2h = 8 + (8 * n if per_vertex else 0)
 
     peak, peak_kind = peaks()
-    alg_bytes = s0["alg_bytes"]
-    achieved = alg_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
+    alg_bytes = s0["alg_bytes"]          # this rank's share (the parts sum to the graph's B_alg)
     pivot_bytes = s0["probe_bytes"]
+    if world > 1:
+        ab = torch.tensor([alg_bytes, pivot_bytes], dtype=torch.float64, device=dev)
+        dist.all_reduce(ab)
+        alg_bytes, pivot_bytes = float(ab[0]), float(ab[1])
+    achieved = alg_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"ncu_{a.config}_join_traffic.json")
     if os.path.exists(tr_path):

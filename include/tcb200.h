@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define TCB200_ABI_VERSION 1
+#define TCB200_ABI_VERSION 2
 
 typedef enum tc_status {
   TC_OK = 0,
@@ -71,8 +71,6 @@ typedef struct tc_graph_info {
   uint32_t max_out_degree; /* max d+ in the (deg,id)-oriented DAG */
   int device;
   double build_ms;         /* device time of the last build/from_csr (CUDA events) */
-  double frontier_ms;      /* part of build_ms: the level-1 frontier index (in-edge items) */
-  uint64_t frontier_items; /* useful in-edges u->v (the reference's level-1 rows) */
 } tc_graph_info;
 
 /* trimatch::MatchOptions (matcher.hpp:84-88) + GPU extensions. */

@@ -53,8 +53,7 @@ class TcBuildReport(C.Structure):
 
 class TcGraphInfo(C.Structure):
     _fields_ = [("num_vertices", C.c_uint32), ("num_edges", C.c_uint64), ("max_degree", C.c_uint32),
-                ("max_out_degree", C.c_uint32), ("device", C.c_int), ("build_ms", C.c_double),
-                ("frontier_ms", C.c_double), ("frontier_items", C.c_uint64)]
+                ("max_out_degree", C.c_uint32), ("device", C.c_int), ("build_ms", C.c_double)]
 
 
 class TcCountOpts(C.Structure):
@@ -251,10 +250,6 @@ class Graph:
     @property
     def build_ms(self) -> float:
         return self._info.build_ms
-
-    @property
-    def frontier_ms(self) -> float:
-        return self._info.frontier_ms
 
     def set_stream(self, stream_ptr: int):
         _check(_lib.tc_graph_set_stream(self._h, C.c_void_p(stream_ptr or 0)))

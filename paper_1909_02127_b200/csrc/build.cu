@@ -335,7 +335,6 @@ void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
                                                                g.offH.get());
     TC_LAUNCH();
   }
-  build_frontier(g);
 }
 
 }  // namespace

@@ -3,6 +3,8 @@
 // C++ exception crosses the ABI.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -101,6 +103,32 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+}  // namespace
+
+tcb::PhaseLog::PhaseLog(cudaStream_t st) : s(st) {
+  const char* e = getenv("TCB_PHASES");
+  on = e && *e == '1';
+  mark("start");
+}
+void tcb::PhaseLog::mark(const char* what) {
+  if (!on || n >= kMax) return;
+  cudaEventCreate(&ev[n]);
+  cudaEventRecord(ev[n], s);
+  name[n++] = what;
+}
+tcb::PhaseLog::~PhaseLog() {
+  if (!on || n == 0) return;
+  cudaEventSynchronize(ev[n - 1]);
+  for (int i = 1; i < n; ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+    fprintf(stderr, "[tcb] %-22s %9.3f ms\n", name[i], ms);
+  }
+  for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+}
+
+namespace {
+
 tc_graph* new_handle(int device) {
   auto* g = new tc_graph();
   g->device = device;
@@ -115,7 +143,10 @@ void destroy_handle(tc_graph* g) {
   cudaGetDevice(&prev);
   cudaSetDevice(g->device);
   {
-    cudaStream_t s = g->stream;
+    // the handle's buffers were used on g->stream (possibly a caller's stream
+    // that is gone by now): drain the device, then free on the own stream
+    cudaDeviceSynchronize();
+    cudaStream_t s = g->own_stream;
     g->off.release();
     g->col.release();
     g->src.release();
@@ -124,12 +155,7 @@ void destroy_handle(tc_graph* g) {
     g->rank_of.release();
     g->colH.release();
     g->offH.release();
-    g->fr_items.release();
-    g->fr_e.release();
-    g->fr_moff.release();
-    g->fr_in.release();
-    g->fr_wsegs.release();
-    g->fr_csegs.release();
+    for (auto& sc : g->scratch) sc.release(s);
     cudaStreamSynchronize(s);
   }
   if (g->own_stream) cudaStreamDestroy(g->own_stream);
@@ -223,8 +249,6 @@ tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info) {
   info->max_out_degree = g->max_dplus;
   info->device = g->device;
   info->build_ms = g->build_ms;
-  info->frontier_ms = g->frontier_ms;
-  info->frontier_items = g->fr_nitems;
   return TC_OK;
 }
 

@@ -65,6 +65,20 @@ struct DBuf {
   operator T*() const { return p; }
 };
 
+// Diagnostics: TCB_PHASES=1 records a CUDA event at every mark() on the stream
+// and prints the intervals to stderr when the log goes out of scope.
+struct PhaseLog {
+  static constexpr int kMax = 32;
+  bool on = false;
+  cudaStream_t s = nullptr;
+  int n = 0;
+  cudaEvent_t ev[kMax];
+  const char* name[kMax];
+  explicit PhaseLog(cudaStream_t st);
+  void mark(const char* what);
+  ~PhaseLog();
+};
+
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
 inline uint64_t ceil_div64(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 

@@ -287,7 +287,7 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 // Advance + join for items [i0, i1) of one small pivot (u32 suffix ranges
 // {b,e} in items[i].x/.y), executed by one warp against its private hash.
 template <bool kPerVertex, typename Sink>
-__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items, const uint32_t* __restrict__ item_e,
+__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items, const uint32_t* __restrict__ item_u,
                                                     uint32_t i0, uint32_t i1, const uint32_t* __restrict__ col,
                                                     const uint32_t* __restrict__ src, const uint32_t* tab,
                                                     uint32_t mask, uint32_t shift, const Sink& sink,
@@ -303,6 +303,18 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
       b = it.x;
       e = it.y;
       nch = ((e + 3) >> 2) - (b >> 2);
+    }
+    // compact the non-empty items to the low lanes (item_of needs nch >= 1);
+    // lane L takes the item of the (L+1)-th non-empty lane
+    uint32_t owner = my;
+    {
+      const uint32_t ne = __ballot_sync(0xffffffffu, nch > 0);
+      const uint32_t from = lane < (uint32_t)__popc(ne) ? __fns(ne, 0, lane + 1) : lane;
+      b = __shfl_sync(0xffffffffu, b, from);
+      e = __shfl_sync(0xffffffffu, e, from);
+      nch = __shfl_sync(0xffffffffu, nch, from);
+      if (lane >= (uint32_t)__popc(ne)) nch = 0;
+      owner = ib + from;
     }
     const uint32_t pre = warp_inclusive_scan(nch);
     const uint32_t start = pre - nch;
@@ -326,7 +338,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
     if (kPerVertex) {
       __syncwarp();
       const uint32_t c = item_cnt[lane];
-      if (c) atomicAdd(&sink.t_rank[src[item_e[my]]], (unsigned long long)c);
+      if (c) atomicAdd(&sink.t_rank[item_u[owner]], (unsigned long long)c);
       __syncwarp();
     }
   }
@@ -339,7 +351,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint4* __restrict__ items, const uint32_t* __restrict__ item_e, const uint4* __restrict__ segs,
+    const uint4* __restrict__ items, const uint32_t* __restrict__ item_u, const uint4* __restrict__ segs,
     uint32_t nsegs, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
@@ -364,7 +376,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
     const uint32_t h =
-        warp_join_small<kPerVertex>(items, item_e, sg.y, sg.z, col, src, tab, mask, shift, sink, s_item[warp]);
+        warp_join_small<kPerVertex>(items, item_u, sg.y, sg.z, col, src, tab, mask, shift, sink, s_item[warp]);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
@@ -398,9 +410,9 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCtaMinBlocks + 1) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint16_t* __restrict__ colH, const uint4* __restrict__ items, const uint32_t* __restrict__ item_e,
+    const uint16_t* __restrict__ colH, const uint4* __restrict__ items, const uint32_t* __restrict__ item_u,
     const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t h0, uint32_t nbm,
-    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, const uint64_t* __restrict__ moff_e, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
+    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, const uint64_t* __restrict__ item_mo, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
   __shared__ unsigned long long s_hmo[kPerVertex ? kCtaSegItems : 1];  // hot items' mask offsets
@@ -473,7 +485,7 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
           s_hb[ph] = it[r].x;
           s_he[ph] = it[r].y;
           s_hpre[ph] = ch;
-          if (kPerVertex) s_hmo[ph] = moff_e[item_e[i0 + i]];
+          if (kPerVertex) s_hmo[ph] = item_mo[i0 + i];
           s_hidx[ph] = (uint16_t)i;
           ++ph;
           ch += nh[r];
@@ -544,7 +556,7 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
         const uint32_t c = s_icnt[i];
         if (c) {
-          atomicAdd(&t_rank[src[item_e[i0 + i]]], (unsigned long long)c);
+          atomicAdd(&t_rank[item_u[i0 + i]], (unsigned long long)c);
           s_icnt[i] = 0;
         }
       }
@@ -561,220 +573,156 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
 // Mask byte (item k, chunk c) has bit j set iff element 8c+j of colH -- an
 // oriented edge u->x -- closed a triangle (u, v_k, x).  For each hot position
 // p of row u, B[p] = sum over u's items of that bit = the triangles whose
-// low->top edge is u->x_p; then t[x_p] += B[p] and t[u] += sum_p B[p].  Lanes own
-// 4 chunks each of a 128-chunk group (coalesced: chunk cg + lane + 32t); each
-// item's byte is spread into 4+4 byte-lane counters by a multiply
-// (b*0x00204081 & 0x01010101), so a row item costs a few instructions per 8
-// positions instead of a per-hit atomic.  Item headers (first chunk, mask
-// offset) are staged per warp in SMEM and read as broadcasts.  Items of a row
-// start at non-decreasing chunks, so a group stops at the first item that
-// starts past it.  Only edges in [pe0, pe1) (this part's range) count.  Rows
-// are taken from the top rank down.
-#ifndef TCB_ROW_MINB
-#define TCB_ROW_MINB 3
-#endif
-#ifndef TCB_ROW_UNROLL
-#define TCB_ROW_UNROLL 4
-#endif
-constexpr int kRowChunksPerLane = 4;
-constexpr int kRowItemUnroll = TCB_ROW_UNROLL;
+// low->top edge is u->x_p; then t[x_p] += B[p] and t[u] += sum_p B[p].
+// The row's mask block has the closed-form layout of graph.cuh RowMasks
+// (item k's bytes at rowbase + P(k), chunks cs_k..c_hi-1), so the pass needs
+// no per-item metadata: lanes own 32 consecutive chunks of the row, the warp
+// walks the items k that reach the group (byte loads of one item are
+// coalesced across the lanes), kRowU items in flight, and each byte is spread
+// into 4+4 byte-lane counters by a multiply (b*0x00204081 & 0x01010101).
+// Warp-bin items' bytes are zero (memset): their hits are counted in
+// k_join_warp.  Rows are taken from the top rank down, 32 per queue grab.
 constexpr int kRowWarps = 8;
-__global__ void __launch_bounds__(kRowWarps * 32, TCB_ROW_MINB) k_pv_rows(
+constexpr int kRowU = 8;
+__global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
-    const uint64_t* __restrict__ moff_e, const uint8_t* __restrict__ masks, uint32_t n, uint32_t h0, uint32_t rc, uint32_t ncnt, uint64_t pe0,
-    uint64_t pe1, unsigned int* __restrict__ queue, unsigned long long* __restrict__ t_rank) {
+    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t u_hi,
+    uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue,
+    unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
-  __shared__ uint32_t s_hc[kRowWarps][32];
-  __shared__ unsigned long long s_mo[kRowWarps][32];
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
   __syncthreads();
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lane = lane_id();
+  const uint32_t nrows = u_hi - u_lo + 1;
   const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
-  constexpr uint32_t kGroup = 32 * kRowChunksPerLane;
   while (true) {
-    // 32 rows per queue grab (most rows have no hot suffix): one atomic per
-    // batch, the rows with work taken in order from a ballot
     uint32_t rb = 0;
     if (lane == 0) rb = atomicAdd(queue, 32u);
     rb = __shfl_sync(0xffffffffu, rb, 0);
-    if (rb >= n) break;
-    const uint32_t rl = rb + lane;
-    uint32_t ul = 0, hsl = 0, hel = 0;
-    uint64_t e0l = 0, e1l = 0;
-    if (rl < n) {
-      ul = n - 1 - rl;
-      hsl = offH[ul];
-      hel = offH[ul + 1];
-      e0l = max((uint64_t)off[ul], pe0);
-      e1l = min((uint64_t)off[ul + 1], pe1);
+    if (rb >= nrows) break;
+    const uint32_t i = rb + lane;
+    uint32_t ul = 0, dl = 0, Ol = 0, hl = 0;
+    if (i < nrows) {
+      ul = u_hi - i;
+      dl = off[ul + 1] - off[ul];
+      Ol = offH[ul];
+      hl = offH[ul + 1] - Ol;
     }
-    uint32_t rows = __ballot_sync(0xffffffffu, hsl != hel && e0l < e1l);
-  while (rows) {
-    const int rj = __ffs(rows) - 1;
-    rows &= rows - 1;
-    const uint32_t u = __shfl_sync(0xffffffffu, ul, rj);
-    const uint32_t hs = __shfl_sync(0xffffffffu, hsl, rj), he = __shfl_sync(0xffffffffu, hel, rj);
-    const uint64_t e0 = __shfl_sync(0xffffffffu, (unsigned long long)e0l, rj);
-    const uint64_t e1 = __shfl_sync(0xffffffffu, (unsigned long long)e1l, rj);
-    const uint32_t c_lo = hs >> 3, c_hi = (he + 7) >> 3;
-    unsigned long long row_total = 0;
-    // stage the row's items [eb, eb+32) that have hot chunks -> warp SMEM slots
-    auto stage = [&](uint64_t eb) -> uint32_t {
-      // an item's masks run from its first hot chunk to the row's last, so
-      // its length in the edge-ordered offsets gives the first chunk
-      const uint64_t e = eb + lane;
-      unsigned long long mo = 0;
-      uint32_t len = 0;
-      if (e < e1) {
-        mo = moff_e[e];
-        len = (uint32_t)(moff_e[e + 1] - mo);
-      }
-      const bool has = len > 0;
-      const uint32_t hc = c_hi - len;
-      const uint32_t vm = __ballot_sync(0xffffffffu, has);
-      __syncwarp();
-      if (has) {
-        const uint32_t slot = __popc(vm & lanemask_lt());
-        s_hc[warp][slot] = hc;
-        s_mo[warp][slot] = mo;
-      }
-      __syncwarp();
-      return __popc(vm);
-    };
-    if (c_hi - c_lo <= 32) {
-      // narrow row: sub-groups of w = pow2 >= chunks lanes, each sub-group on
-      // its own item (one chunk per lane), counts summed across sub-groups
-      const uint32_t lg = 32 - __clz(c_hi - c_lo - 1), w = 1u << lg;  // w >= chunks
-      const uint32_t ipl = 32u >> lg, sub = lane >> lg;
-      const uint32_t c = c_lo + (lane & (w - 1));
-      const bool cvalid = c < c_hi;
-      uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
-      uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      auto flush1 = [&]() {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
-          cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
-        }
-        acc_lo = acc_hi = 0;
-        nacc = 0;
-      };
-      for (uint64_t eb = e0; eb < e1; eb += 32) {
-        const uint32_t nb = stage(eb);
-        for (uint32_t j = 0; j < nb; j += ipl * kRowItemUnroll) {
-          if (nacc + kRowItemUnroll > 255) flush1();
-          uint32_t bits[kRowItemUnroll];
-#pragma unroll
-          for (int k = 0; k < kRowItemUnroll; ++k) {
-            const uint32_t jj = j + k * ipl + sub;
-            bits[k] = 0;
-            if (jj < nb && cvalid) {
-              const uint32_t hj = s_hc[warp][jj];
-              if (c >= hj) bits[k] = masks[s_mo[warp][jj] + (c - hj)];
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < kRowItemUnroll; ++k) {
-            acc_lo += ((bits[k] & 0xfu) * 0x00204081u) & 0x01010101u;
-            acc_hi += ((bits[k] >> 4) * 0x00204081u) & 0x01010101u;
-          }
-          nacc += kRowItemUnroll;
-        }
-      }
-      flush1();
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        for (uint32_t o = w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
-      if (sub == 0 && cvalid) {
+    uint32_t rows = __ballot_sync(0xffffffffu, hl > 0 && dl >= 2);
+    while (rows) {
+      const int rj = __ffs(rows) - 1;
+      rows &= rows - 1;
+      const uint32_t u = __shfl_sync(0xffffffffu, ul, rj);
+      const RowMasks rm(__shfl_sync(0xffffffffu, dl, rj), __shfl_sync(0xffffffffu, Ol, rj),
+                        __shfl_sync(0xffffffffu, hl, rj));
+      const uint8_t* rowm = masks + rowbase[u - u_lo];
+      const uint32_t nk = rm.d - 1;  // items with a non-empty suffix
+      const uint64_t C = rm.c_hi - rm.c_lo;
+      unsigned long long row_total = 0;
+      // t[x_p] += B[p] for the 8 positions of lane chunk c
+      auto emit = [&](uint64_t c, const uint32_t* cnt) {
         const uint4 q = colH4[c];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint32_t p = (c << 3) + j;
-          if (cnt[j] && p >= hs && p < he) {
+          const uint64_t p = 8 * c + j;
+          if (cnt[j] && p >= rm.O && p < rm.O + rm.h) {
             const uint32_t x = h0 + hot_u16(q, j);
             if (x >= rc) atomicAdd(&top[x - rc], cnt[j]);
             else atomicAdd(&t_rank[x], (unsigned long long)cnt[j]);
             row_total += cnt[j];
           }
         }
-      }
-    } else
-    for (uint32_t cg = c_lo; cg < c_hi; cg += kGroup) {
-      uint32_t acc_lo[kRowChunksPerLane], acc_hi[kRowChunksPerLane], cnt[kRowChunksPerLane][8];
+      };
+      if (C <= 16) {
+        // narrow row: sub-groups of w = pow2 >= C lanes, one item each
+        // (every item reaches the last chunk), counters summed across them
+        const uint32_t lg = 32 - __clz((uint32_t)C - 1 | 0u), w = C > 1 ? 1u << lg : 1u;
+        const uint32_t G = 32 / w, sub = lane / w;
+        const uint64_t c = rm.c_lo + (lane & (w - 1));
+        const bool cvalid = c < rm.c_hi;
+        uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
+        uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t k0 = 0; k0 < nk; k0 += G * kRowU) {
+          uint32_t bits[kRowU];
 #pragma unroll
-      for (int t = 0; t < kRowChunksPerLane; ++t) {
-        acc_lo[t] = acc_hi[t] = 0;
+          for (int t = 0; t < kRowU; ++t) {
+            const uint32_t k = k0 + t * G + sub;
+            bits[t] = 0;
+            if (k < nk && cvalid) {
+              const uint64_t cs = rm.first_chunk(k);
+              if (c >= cs) bits[t] = rowm[rm.P(k) + (c - cs)];
+            }
+          }
+          if (nacc + kRowU > 255) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) cnt[t][j] = 0;
-      }
-      uint32_t nacc = 0;
-      auto flush = [&]() {
+            for (int j = 0; j < 4; ++j) {
+              cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
+              cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
+            }
+            acc_lo = acc_hi = nacc = 0;
+          }
 #pragma unroll
-        for (int t = 0; t < kRowChunksPerLane; ++t) {
+          for (int t = 0; t < kRowU; ++t) {
+            acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
+            acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
+          }
+          nacc += kRowU;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
+          cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          for (uint32_t o = w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
+        if (sub == 0 && cvalid) emit(c, cnt);
+      } else {
+        for (uint64_t cg = rm.c_lo; cg < rm.c_hi; cg += 32) {
+          const uint64_t c = cg + lane;
+          const bool cvalid = c < rm.c_hi;
+          // items reaching this group: all k < c0, and k >= c0 while cs_k <= last chunk
+          const uint64_t clast = (cg + 31 < rm.c_hi - 1) ? cg + 31 : rm.c_hi - 1;
+          const uint64_t kk = 8 * clast + 7 - rm.O + rm.c0;  // first k with cs_k > clast
+          const uint32_t K = (uint32_t)(kk < nk ? kk : (uint64_t)nk);
+          uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
+          uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          uint64_t P = 0;  // P(k) of the current k
+          for (uint32_t k0 = 0; k0 < K; k0 += kRowU) {
+            uint32_t bits[kRowU];
+#pragma unroll
+            for (int t = 0; t < kRowU; ++t) {
+              const uint32_t k = k0 + t;
+              const uint64_t cs = rm.first_chunk(k);
+              bits[t] = (k < K && cvalid && c >= cs) ? rowm[P + (c - cs)] : 0u;
+              P += rm.c_hi - cs;
+            }
+            if (nacc + kRowU > 255) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
+                cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
+              }
+              acc_lo = acc_hi = nacc = 0;
+            }
+#pragma unroll
+            for (int t = 0; t < kRowU; ++t) {
+              acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
+              acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
+            }
+            nacc += kRowU;
+          }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            cnt[t][j] += (acc_lo[t] >> (8 * j)) & 0xffu;
-            cnt[t][4 + j] += (acc_hi[t] >> (8 * j)) & 0xffu;
+            cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
+            cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
           }
-          acc_lo[t] = acc_hi[t] = 0;
-        }
-        nacc = 0;
-      };
-      bool done = false;
-      for (uint64_t eb = e0; eb < e1 && !done; eb += 32) {
-        const uint32_t nb = stage(eb);
-        // kRowItemUnroll items per step: all their byte loads are in flight
-        // together (the loop is load-latency bound, not issue bound)
-        for (uint32_t j = 0; j < nb && !done; j += kRowItemUnroll) {
-          if (nacc + kRowItemUnroll > 255) flush();
-          uint32_t bits[kRowItemUnroll][kRowChunksPerLane];
-#pragma unroll
-          for (int k = 0; k < kRowItemUnroll; ++k) {
-            uint32_t hj = 0xffffffffu;
-            unsigned long long mj = 0;
-            if (j + k < nb) {
-              hj = s_hc[warp][j + k];
-              mj = s_mo[warp][j + k];
-            }
-            if (j + k < nb && hj >= cg + kGroup) done = true;  // starts are non-decreasing
-#pragma unroll
-            for (int t = 0; t < kRowChunksPerLane; ++t) {
-              const uint32_t c = cg + lane + 32 * t;
-              bits[k][t] = (hj != 0xffffffffu && c >= hj && c < c_hi) ? masks[mj + (c - hj)] : 0u;
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < kRowItemUnroll; ++k) {
-#pragma unroll
-            for (int t = 0; t < kRowChunksPerLane; ++t) {
-              acc_lo[t] += ((bits[k][t] & 0xfu) * 0x00204081u) & 0x01010101u;
-              acc_hi[t] += ((bits[k][t] >> 4) * 0x00204081u) & 0x01010101u;
-            }
-          }
-          nacc += kRowItemUnroll;
+          if (cvalid) emit(c, cnt);
         }
       }
-      flush();
-#pragma unroll
-      for (int t = 0; t < kRowChunksPerLane; ++t) {
-        const uint32_t c = cg + lane + 32 * t;
-        if (c >= c_hi) continue;
-        const uint4 q = colH4[c];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t p = (c << 3) + j;
-          if (cnt[t][j] && p >= hs && p < he) {
-            const uint32_t x = h0 + hot_u16(q, j);
-            if (x >= rc) atomicAdd(&top[x - rc], cnt[t][j]);
-            else atomicAdd(&t_rank[x], (unsigned long long)cnt[t][j]);
-            row_total += cnt[t][j];
-          }
-        }
-      }
+      row_total = warp_sum(row_total);
+      if (lane == 0 && row_total) atomicAdd(&t_rank[u], row_total);
     }
-    row_total = warp_sum(row_total);
-    if (lane == 0 && row_total) atomicAdd(&t_rank[u], row_total);
-  }
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x)
@@ -826,22 +774,19 @@ struct Events {
 }  // namespace
 
 const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
-  if (g.cached_parts != parts) {
-    cudaStream_t s = g.stream;
-    const uint64_t E = g.E;
-    g.part_bounds.assign((size_t)parts + 1, 0);
-    g.part_bounds[parts] = E;
-    if (E && parts > 1) {
-      DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
-      scan_exclusive<uint64_t>(EdgeCost{g.off.get(), g.col.get(), g.src.get()}, prefix.get(), E, tot.get(), s);
-      const uint64_t total_cost = read_scalar(tot.get(), s);
-      k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), E, total_cost, parts, bnd.get());
-      TC_LAUNCH();
-      TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
-                              cudaMemcpyDeviceToHost, s));
-      TC_CUDA(cudaStreamSynchronize(s));
-    }
-    g.cached_parts = parts;
+  cudaStream_t s = g.stream;
+  const uint64_t E = g.E;
+  g.part_bounds.assign((size_t)parts + 1, 0);
+  g.part_bounds[parts] = E;
+  if (E && parts > 1) {
+    DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
+    scan_exclusive<uint64_t>(EdgeCost{g.off.get(), g.col.get(), g.src.get()}, prefix.get(), E, tot.get(), s);
+    const uint64_t total_cost = read_scalar(tot.get(), s);
+    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), E, total_cost, parts, bnd.get());
+    TC_LAUNCH();
+    TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
   }
   return g.part_bounds;
 }
@@ -858,32 +803,37 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   Events ev;
   TC_CUDA(cudaEventRecord(ev.e[0], s));
   uint64_t kl = 0;  // kernels launched by this call
+  PhaseLog pl(s);
 
   DBuf<unsigned long long> acc(1, s);
   TC_CUDA(cudaMemsetAsync(acc.get(), 0, sizeof(unsigned long long), s));
-  DBuf<unsigned long long> t_rank;
+  unsigned long long* t_rank = nullptr;
   if (pv) {
-    t_rank.alloc(n ? n : 1, s);
-    TC_CUDA(cudaMemsetAsync(t_rank.get(), 0, sizeof(unsigned long long) * (n ? n : 1), s));
+    t_rank = g.scratch[kSlotTRank].get<unsigned long long>(n ? n : 1, s);
+    TC_CUDA(cudaMemsetAsync(t_rank, 0, sizeof(unsigned long long) * (n ? n : 1), s));
   }
 
-  // ---- work segments: the whole frontier, or this part's degree-weighted
-  //      oriented-edge range (multi-GPU) ----
-  const uint4* wsegs = g.fr_wsegs.get();
-  const uint4* csegs = g.fr_csegs.get();
-  uint64_t NSW = g.fr_nwsegs, NSC = g.fr_ncsegs;
-  DBuf<uint4> pw, pc;
+  // ---- level-1 frontier of the whole graph, or of this part's
+  //      degree-weighted oriented-edge range (multi-GPU) ----
   uint64_t part_e0 = 0, part_e1 = E;
   if (parts > 1 && E) {
-    if (g.cached_parts != parts) kl += 4;
+    kl += 4;
     const std::vector<uint64_t>& b = partition_bounds(g, parts);
     part_e0 = b[part];
     part_e1 = b[part + 1];
-    part_segments(g, part_e0, part_e1, pw, NSW, pc, NSC);
-    kl += 6;
-    wsegs = pw.get();
-    csegs = pc.get();
   }
+  Frontier fr;
+  kl += build_frontier(g, part_e0, part_e1, pv, fr);
+  const uint4* wsegs = fr.wsegs;
+  const uint4* csegs = fr.csegs;
+  const uint64_t NSW = fr.nw, NSC = fr.nc;
+  uint8_t* masks = nullptr;
+  if (pv && NSC) {
+    // hot hit masks of the CTA bin; warp-bin items' bytes stay zero
+    masks = g.scratch[kSlotMasks].get<uint8_t>(fr.mask_bytes + 32, s);
+    TC_CUDA(cudaMemsetAsync(masks, 0, fr.mask_bytes + 32, s));
+  }
+  pl.mark("frontier");
   TC_CUDA(cudaEventRecord(ev.e[1], s));
 
   // ---- advance + join ----
@@ -908,10 +858,12 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, smem));
     const unsigned grid =
         (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), g.fr_items.get(), g.fr_e.get(),
-                                         wsegs, (uint32_t)NSW, rc_w, ncnt_w, t_rank.get(), acc.get());
+    pl.mark("warp_setup");
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), fr.items, fr.item_u,
+                                         wsegs, (uint32_t)NSW, rc_w, ncnt_w, t_rank, acc.get());
     TC_LAUNCH();
     ++launches;
+    pl.mark("join_warp");
   }
   if (NSC) {
     DBuf<unsigned int> queue(1, s);
@@ -928,15 +880,14 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, dsm));
     if (occ < 1) occ = 1;
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, NSC);
-    DBuf<uint32_t> slab((uint64_t)grid * slab_cap + 1, s);
-    DBuf<uint8_t> masks;
-    if (pv) masks.alloc(g.fr_mask_bytes + 32, s);  // every byte a segment owns is written by the join
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), g.colH.get(), g.fr_items.get(),
-                                        g.fr_e.get(), csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
-                                        slab_cap, slab.get(), g.fr_moff.get(), masks.get(), t_rank.get(),
-                                        acc.get());
+    uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
+    pl.mark("cta_setup");
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), g.colH.get(), fr.items,
+                                        fr.item_u, csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
+                                        slab_cap, slab, fr.item_mo, masks, t_rank, acc.get());
     TC_LAUNCH();
     ++launches;
+    pl.mark("join_cta");
     if (pv) {
       // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics)
       DBuf<unsigned int> rq(1, s);
@@ -947,9 +898,11 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
       int rocc = 0;
       TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rocc, k_pv_rows, kRowWarps * 32, rsm));
       k_pv_rows<<<(unsigned)(sms * std::max(rocc, 1)), kRowWarps * 32, rsm, s>>>(
-          g.off.get(), g.colH.get(), g.offH.get(), g.fr_moff.get(), masks.get(), n, g.h0, n - rcnt, rcnt, part_e0, part_e1, rq.get(), t_rank.get());
+          g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, fr.u_hi, g.h0, n - rcnt, rcnt,
+          rq.get(), t_rank);
       TC_LAUNCH();
       ++launches;
+      pl.mark("pv_rows");
     }
   }
   TC_CUDA(cudaEventRecord(ev.e[2], s));
@@ -957,7 +910,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   // ---- outputs ----
   TC_CUDA(cudaMemcpyAsync(d_total, acc.get(), sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
   if (pv && n) {
-    k_gather_pv<<<grid_gs(n, dev), 256, 0, s>>>(t_rank.get(), g.rank_of.get(), n, d_pv);
+    k_gather_pv<<<grid_gs(n, dev), 256, 0, s>>>(t_rank, g.rank_of.get(), n, d_pv);
     TC_LAUNCH();
     ++kl;
   }
@@ -968,18 +921,21 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     stats->join_ms = ev.ms(1, 2);
     stats->reduce_ms = ev.ms(2, 3);
     stats->total_ms = ev.ms(0, 3);
-    stats->items = g.fr_nitems;
-    stats->wedges = g.fr_J;
+    stats->items = fr.nitems;
+    stats->wedges = fr.J;
     stats->segments = NSW + NSC;
     stats->join_launches = launches;
-    stats->dag_W = (double)g.fr_W;
-    stats->pivots = g.fr_pivots;
+    stats->dag_W = (double)fr.W;
+    stats->pivots = fr.pivots;
     stats->kernel_launches = kl + launches;
-    stats->alg_bytes = 4.0 * (double)g.fr_W + 12.0 * (double)E + 8.0 * ((double)n + 1) + (pv ? 8.0 * n : 0.0);
+    // this part's share of SURVEY 8d's B_alg (vertex terms on part 0): the
+    // parts' values sum to the whole graph's
+    stats->alg_bytes = 4.0 * (double)fr.W + 12.0 * (double)(part_e1 - part_e0) +
+                       (part == 0 ? 8.0 * ((double)n + 1) + (pv ? 8.0 * n : 0.0) : 0.0);
     // bytes the implemented join must stream: hot ids 2 B, cold ids 4 B,
     // items 16 B, pivot lists 4 B per member (whole graph; a part does ~1/P)
-    stats->probe_bytes = 2.0 * (double)g.fr_hot + 4.0 * (double)(g.fr_J - g.fr_hot) +
-                         16.0 * (double)g.fr_nitems + 4.0 * (double)E;
+    stats->probe_bytes = 2.0 * (double)fr.hot + 4.0 * (double)(fr.J - fr.hot) +
+                         16.0 * (double)fr.nitems + 4.0 * (double)(part_e1 - part_e0);
   }
 }
 

@@ -1,15 +1,26 @@
-// frontier.cu -- the level-1 frontier index: useful in-edges grouped by pivot.
+// frontier.cu -- the level-1 frontier: useful in-edges grouped by pivot, built
+// inside every tc_count (it is part of the timed step, like the reference's
+// level-1 expand_level inside match()).
 //
 // The reference materialises level-1 rows (u, w) with expand_level
 // (matcher.cpp:136-198: advance over N(u), accept w > u, 2-core membership,
-// look-ahead) before its final level.  Here the level-1 frontier is a
-// graph-static index over the (deg,id)-oriented DAG: for every oriented edge
-// e = u->v that can close a triangle as a pivot in-edge (d+(v) > 0 and a
-// non-empty suffix of N+(u) after v) one item, grouped by pivot v and sorted
-// by e (a stable order, so multi-GPU edge ranges select the same items on
-// every rank).  Built once per graph, right after the oriented CSR:
-//   keys (v << be | e) of useful edges -> radix sort -> item geometry ->
-//   per-pivot offsets -> per-bin work segments.
+// look-ahead) before its final level.  Here, for every oriented edge
+// e = u->v of this part's edge range [e0, e1) that can close a triangle as a
+// pivot in-edge (d+(v) > 0 and a non-empty suffix of N+(u) after v), one
+// item, grouped by pivot v:
+//   slots         one item slot per in-edge of every pivot with d+(v) > 0:
+//                 deg(v) - d+(v) for a whole-graph count (no edge pass), a
+//                 counting pass (one RED per edge) for a multi-GPU part
+//   scan          -> per-pivot item offsets in[v]
+//   rowbase       per-vertex only: exclusive scan of each row's hit-mask
+//                 bytes (closed form, graph.cuh RowMasks)
+//   k_fr_scatter  item geometry computed in edge order (the row data u, off,
+//                 offH are read coalesced) and scattered to the pivot's slot
+//                 through an atomic cursor.  Item order inside a pivot is
+//                 arbitrary: every count is an order-independent integer sum.
+//   segments      per-bin work segments (warp bin / CTA bin)
+// A part only ever sees its own edges, so multi-GPU ranks build disjoint
+// frontiers with no exchange.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,260 +52,267 @@ struct Sums {
   unsigned long long W, J, hot, items_c;
 };
 
-// Useful in-edge?  Writes the sort key, or the all-ones sentinel.
-__global__ void k_fr_keys(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                          const uint32_t* __restrict__ src, uint64_t E, int be, uint64_t sentinel,
-                          uint64_t* __restrict__ keys, unsigned long long* __restrict__ W) {
-  unsigned long long w = 0;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = col[e];
-    const uint32_t dv = off[v + 1] - off[v];
-    w += dv;
-    const bool useful = dv > 0 && e + 1 < off[src[e] + 1];
-    keys[e] = useful ? (((uint64_t)v << be) | e) : sentinel;
+// The level-1 item of oriented edge e = u->v (u = src[e], v = col[e]).  Every
+// in-edge of a pivot with d+(v) > 0 gets a slot (claim); the item is useful
+// when the suffix of N+(u) after v is non-empty, else it stays all-zero.
+// Warp-bin pivots (d+(v) <= kWarpMaxDeg): {b, e} range of the 32-bit col[].
+// CTA-bin pivots: {hb, he, cb, ce} = the suffix split into its hot part
+// (16-bit colH) and its cold part (32-bit col).
+struct Geom {
+  uint32_t v, dv, u, k, d, O, h;
+  uint4 it;
+  bool claim, useful;
+};
+struct ItemGeom {
+  const uint32_t* off;
+  const uint32_t* col;
+  const uint32_t* src;
+  const uint32_t* offH;
+  __device__ __forceinline__ void operator()(uint64_t e, Geom& q) const {
+    q.v = col[e];
+    q.dv = off[q.v + 1] - off[q.v];
+    q.u = src[e];
+    const uint32_t beg = off[q.u], end = off[q.u + 1];
+    q.k = (uint32_t)e - beg;
+    q.d = end - beg;
+    q.O = offH[q.u];
+    q.h = offH[q.u + 1] - q.O;
+    q.claim = q.dv > 0;
+    q.useful = q.claim && (uint32_t)e + 1 < end;
+    q.it = make_uint4(0, 0, 0, 0);
+    if (!q.useful) return;
+    if (q.dv <= kWarpMaxDeg) {
+      q.it = make_uint4((uint32_t)e + 1, end, 0, 0);
+    } else {
+      const uint32_t cold_end = end - q.h;
+      if ((uint32_t)e + 1 >= cold_end)  // v is in the hot part: the whole suffix is hot
+        q.it = make_uint4(q.O + ((uint32_t)e + 1 - cold_end), q.O + q.h, 0, 0);
+      else
+        q.it = make_uint4(q.O, q.O + q.h, (uint32_t)e + 1, cold_end);
+    }
   }
-  w = warp_sum(w);
-  if (lane_id() == 0 && w) atomicAdd(W, w);
-}
-
-struct NotSentinel {
-  const uint64_t* k;
-  uint64_t sentinel;
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return k[i] != sentinel ? 1u : 0u; }
 };
 
-// sorted keys -> item geometry, edge ids, per-pivot counts
-__global__ void k_fr_items(const uint64_t* __restrict__ keys, uint64_t NI, int be, const uint32_t* __restrict__ off,
-                           const uint32_t* __restrict__ src, const uint32_t* __restrict__ offH, uint32_t h0,
-                           uint4* __restrict__ items, uint32_t* __restrict__ item_e, uint32_t* __restrict__ cnt,
-                           uint32_t* __restrict__ item_of_e, Sums* __restrict__ sums) {
-  const uint64_t emask = (1ull << be) - 1;
-  unsigned long long J = 0, H = 0, IC = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < NI; i0 += stride) {
-    const uint64_t i = i0 + threadIdx.x;
-    const bool valid = i < NI;
-    uint32_t v = 0xffffffffu;
-    if (valid) {
-      const uint64_t key = keys[i];
-      v = (uint32_t)(key >> be);
-      const uint32_t e = (uint32_t)(key & emask);
-      const uint32_t dv = off[v + 1] - off[v];
-      const uint32_t u = src[e];
-      const uint32_t end = off[u + 1];
-      J += end - (e + 1);
-      uint4 it;
-      if (dv <= kWarpMaxDeg) {
-        it = make_uint4(e + 1, end, 0, 0);
-      } else {
-        const uint32_t ohb = offH[u], ohe = offH[u + 1];
-        const uint32_t cold_end = end - (ohe - ohb);
-        if (v >= h0) {  // v itself is hot: the whole suffix is hot
-          it = make_uint4(ohb + (e - cold_end) + 1, ohe, 0, 0);
-        } else {
-          it = make_uint4(ohb, ohe, e + 1, cold_end);
-        }
-        H += it.y - it.x;
-        ++IC;
-        item_of_e[e] = (uint32_t)i;
-      }
-      items[i] = it;
-      item_e[i] = e;
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, v);
-    if (valid && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&cnt[v], (uint32_t)__popc(peers));
+// Item slots of a whole-graph count: every in-edge of a pivot with d+(v) > 0,
+// i.e. deg(v) - d+(v), with no pass over the edges.
+struct InSlotsWhole {
+  const uint32_t* off;
+  const uint32_t* deg;
+  __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
+    const uint32_t dv = off[v + 1] - off[v];
+    return dv ? deg[v] - dv : 0u;
   }
+};
+
+// Item slots of a multi-GPU part: claimed in-edges inside [e0, e1).
+__global__ void k_fr_count(ItemGeom geo, uint64_t e0, uint64_t e1, uint32_t* __restrict__ cnt) {
+  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = geo.col[e];
+    if (geo.off[v + 1] > geo.off[v]) atomicAdd(&cnt[v], 1u);
+  }
+}
+
+// Mask bytes of row u (rows [u_lo, u_hi] of the part).
+struct RowBytes {
+  const uint32_t* off;
+  const uint32_t* offH;
+  uint32_t u_lo;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    const uint32_t u = u_lo + (uint32_t)i;
+    const uint32_t O = offH[u];
+    return RowMasks(off[u + 1] - off[u], O, offH[u + 1] - O).total();
+  }
+};
+
+// Edge order, kR edges per thread in flight: geometry (row data read
+// coalesced), then the slot claims (atomic cursors), then the scattered item
+// stores.
+constexpr int kScatterR = 4;
+template <bool kPV>
+__global__ void __launch_bounds__(kT) k_fr_scatter(ItemGeom geo, uint64_t e0, uint64_t e1,
+                                                  const uint32_t* __restrict__ in, uint32_t* __restrict__ cursor,
+                                                  uint4* __restrict__ items, uint32_t* __restrict__ item_u,
+                                                  uint64_t* __restrict__ item_mo,
+                                                  const uint64_t* __restrict__ rowbase, uint32_t u_lo,
+                                                  Sums* __restrict__ sums) {
+  unsigned long long W = 0, J = 0, H = 0, IC = 0;
+  for (uint64_t base = e0 + (uint64_t)blockIdx.x * (kT * kScatterR); base < e1;
+       base += (uint64_t)gridDim.x * (kT * kScatterR)) {
+    Geom q[kScatterR];
+    uint32_t pos[kScatterR];
+#pragma unroll
+    for (int r = 0; r < kScatterR; ++r) {
+      const uint64_t e = base + r * kT + threadIdx.x;
+      if (e < e1) {
+        geo(e, q[r]);
+      } else {
+        q[r].claim = q[r].useful = false;
+        q[r].dv = 0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kScatterR; ++r)
+      if (q[r].claim) pos[r] = in[q[r].v] + atomicAdd(&cursor[q[r].v], 1u);
+#pragma unroll
+    for (int r = 0; r < kScatterR; ++r) {
+      W += q[r].dv;
+      if (!q[r].claim) continue;
+      items[pos[r]] = q[r].it;
+      item_u[pos[r]] = q[r].u;
+      if (!q[r].useful) continue;
+      if (q[r].dv <= kWarpMaxDeg) {
+        J += q[r].it.y - q[r].it.x;
+      } else {
+        J += (q[r].it.y - q[r].it.x) + (q[r].it.w - q[r].it.z);
+        H += q[r].it.y - q[r].it.x;
+        ++IC;
+        if (kPV && q[r].it.y > q[r].it.x)
+          item_mo[pos[r]] = rowbase[q[r].u - u_lo] + RowMasks(q[r].d, q[r].O, q[r].h).P(q[r].k);
+      }
+    }
+  }
+  W = warp_sum(W);
   J = warp_sum(J);
   H = warp_sum(H);
   IC = warp_sum(IC);
   if (lane_id() == 0) {
-    atomicAdd(&sums->J, J);
-    atomicAdd(&sums->hot, H);
-    atomicAdd(&sums->items_c, IC);
+    if (W) atomicAdd(&sums->W, W);
+    if (J) atomicAdd(&sums->J, J);
+    if (H) atomicAdd(&sums->hot, H);
+    if (IC) atomicAdd(&sums->items_c, IC);
   }
 }
 
-// Per-vertex hit masks (count.cu): one byte per hot chunk of every CTA-bin item.
-// Mask bytes of oriented edge e's CTA-bin item (0 if none / warp bin).  The
-// scan runs in edge order, so each row's masks are contiguous: the per-vertex
-// row pass (count.cu k_pv_rows) streams them instead of gathering per item.
-struct MaskBytes {
-  const uint4* items;
-  const uint32_t* item_of_e;
-  const uint32_t* off;
-  const uint32_t* col;
-  __device__ __forceinline__ uint64_t operator()(uint64_t e) const {
-    const uint32_t i = item_of_e[e];
-    if (i == 0xffffffffu) return 0;
-    const uint32_t v = col[e];
-    if (off[v + 1] - off[v] <= kWarpMaxDeg) return 0;
-    const uint4 it = items[i];
-    return it.y > it.x ? (uint64_t)(((it.y + 7) >> 3) - (it.x >> 3)) : 0ull;
-  }
-};
-
-// Per-pivot item range of a part: [lo, hi) within [in[v], in[v+1]).
-struct PartRange {
-  const uint32_t* in;
-  const uint32_t* item_e;
-  uint64_t e0, e1;
-  __device__ __forceinline__ uint2 operator()(uint32_t v) const {
-    uint32_t a = in[v], b = in[v + 1];
-    if (e0 == 0 && e1 == ~0ull) return make_uint2(a, b);
-    uint32_t lo = a, hi = b;  // first item with e >= e0
-    while (lo < hi) {
-      const uint32_t m = (lo + hi) >> 1;
-      if (item_e[m] < e0) lo = m + 1; else hi = m;
-    }
-    const uint32_t r0 = lo;
-    hi = b;  // first item with e >= e1
-    while (lo < hi) {
-      const uint32_t m = (lo + hi) >> 1;
-      if (item_e[m] < e1) lo = m + 1; else hi = m;
-    }
-    return make_uint2(r0, lo);
-  }
-};
-
 struct SegCountBin {
   const uint32_t* off;
-  PartRange pr;
+  const uint32_t* in;
   bool warp_bin;
   uint32_t per;
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
     const uint32_t dv = off[v + 1] - off[v];
     if (dv == 0 || (dv <= kWarpMaxDeg) != warp_bin) return 0;
-    const uint2 r = pr((uint32_t)v);
-    return (r.y - r.x + per - 1) / per;
+    return (in[v + 1] - in[v] + per - 1) / per;
   }
 };
 
-__global__ void k_fr_segs(const uint32_t* __restrict__ off, PartRange pr, uint32_t n, bool warp_bin, uint32_t per,
-                          const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
+__global__ void k_fr_segs(const uint32_t* __restrict__ off, const uint32_t* __restrict__ in, uint32_t n,
+                          bool warp_bin, uint32_t per, const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
                           unsigned long long* __restrict__ npivots) {
   unsigned long long np = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t dv = off[v + 1] - off[v];
     if (dv == 0 || (dv <= kWarpMaxDeg) != warp_bin) continue;
-    const uint2 r = pr((uint32_t)v);
-    if (r.y <= r.x) continue;
+    const uint32_t a = in[v], b = in[v + 1];
+    if (b <= a) continue;
     uint32_t s = seg_off[v];
-    for (uint32_t i = r.x; i < r.y; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, r.y), 0);
+    for (uint32_t i = a; i < b; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, b), 0);
     ++np;
   }
   np = warp_sum(np);
   if (lane_id() == 0 && np) atomicAdd(npivots, np);
 }
 
-void make_segments(tc_graph& g, const PartRange& pr, DBuf<uint4>& wsegs, uint64_t& nw, DBuf<uint4>& csegs,
-                   uint64_t& nc, uint64_t* npivots) {
-  cudaStream_t s = g.stream;
-  const uint32_t n = g.n;
-  const uint32_t nn = n ? n : 1;
-  DBuf<uint32_t> woff(nn, s), coff(nn, s), tot(2, s);
-  DBuf<unsigned long long> np(1, s);
-  TC_CUDA(cudaMemsetAsync(np.get(), 0, sizeof(unsigned long long), s));
-  scan_exclusive<uint32_t>(SegCountBin{g.off.get(), pr, true, kWarpSegItems}, woff.get(), n, tot.get(), s);
-  scan_exclusive<uint32_t>(SegCountBin{g.off.get(), pr, false, kCtaSegItems}, coff.get(), n, tot.get() + 1, s);
-  uint32_t h[2] = {0, 0};
-  TC_CUDA(cudaMemcpyAsync(h, tot.get(), 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  TC_CUDA(cudaStreamSynchronize(s));
-  nw = n ? h[0] : 0;
-  nc = n ? h[1] : 0;
-  wsegs.alloc(nw ? nw : 1, s);
-  csegs.alloc(nc ? nc : 1, s);
-  if (nw) {
-    k_fr_segs<<<grid_gs(n, g.device), kT, 0, s>>>(g.off.get(), pr, n, true, kWarpSegItems, woff.get(), wsegs.get(),
-                                                   np.get());
-    TC_LAUNCH();
-  }
-  if (nc) {
-    k_fr_segs<<<grid_gs(n, g.device), kT, 0, s>>>(g.off.get(), pr, n, false, kCtaSegItems, coff.get(),
-                                                   csegs.get(), np.get());
-    TC_LAUNCH();
-  }
-  if (npivots) *npivots = read_scalar(np.get(), s);
-}
-
 }  // namespace
 
-void build_frontier(tc_graph& g) {
+int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Frontier& fr) {
   cudaStream_t s = g.stream;
   const uint32_t n = g.n;
-  const uint64_t E = g.E;
   const int dev = g.device;
-  cudaEvent_t t0, t1;
-  TC_CUDA(cudaEventCreate(&t0));
-  TC_CUDA(cudaEventCreate(&t1));
-  TC_CUDA(cudaEventRecord(t0, s));
-  const int bv = bits_for(n ? n - 1 : 0) ? bits_for(n ? n - 1 : 0) : 1;
-  const int be = bits_for(E ? E - 1 : 0) ? bits_for(E ? E - 1 : 0) : 1;
-  if (bv + be > 64) fail(TC_ERANGE, "frontier key exceeds 64 bits");
-  const uint64_t sentinel = (bv + be >= 64) ? ~0ull : ((1ull << (bv + be)) - 1);
+  const uint32_t nn = n ? n : 1;
+  int kl = 0;
+  PhaseLog pl(s);
+  const ItemGeom geo{g.off.get(), g.col.get(), g.src.get(), g.offH.get()};
   DBuf<Sums> sums(1, s);
   TC_CUDA(cudaMemsetAsync(sums.get(), 0, sizeof(Sums), s));
-  g.fr_in.alloc((uint64_t)n + 1, s);
-  uint64_t NI = 0;
-  if (E) {
-    DBuf<uint64_t> k1(E, s), k2(E, s);
-    k_fr_keys<<<grid_gs(E, dev), kT, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), E, be, sentinel, k1.get(),
-                                             &sums.get()->W);
-    TC_LAUNCH();
-    DBuf<uint32_t> pos(1, s);
-    // count useful (sentinels sort to the end)
-    {
-      DBuf<uint32_t> tmp(E, s);
-      scan_exclusive<uint32_t>(NotSentinel{k1.get(), sentinel}, tmp.get(), E, pos.get(), s);
-      NI = read_scalar(pos.get(), s);
-    }
-    uint64_t* sorted = radix_sort_u64(k1.get(), k2.get(), E, 0, bv + be, s);
-    g.fr_items.alloc(NI ? NI : 1, s);
-    g.fr_e.alloc(NI ? NI : 1, s);
-    DBuf<uint32_t> item_of_e(E, s);  // CTA-bin item of edge e (~0 if none); build-time only
-    TC_CUDA(cudaMemsetAsync(item_of_e.get(), 0xff, E * sizeof(uint32_t), s));
-    DBuf<uint32_t> cnt(n ? n : 1, s);
-    TC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
-    if (NI) {
-      k_fr_items<<<grid_gs(NI, dev), kT, 0, s>>>(sorted, NI, be, g.off.get(), g.src.get(), g.offH.get(), g.h0,
-                                                 g.fr_items.get(), g.fr_e.get(), cnt.get(), item_of_e.get(),
-                                                 sums.get());
-      TC_LAUNCH();
-    }
-    scan_exclusive<uint32_t>(LoadArray<uint32_t>{cnt.get()}, g.fr_in.get(), n, g.fr_in.get() + n, s);
-    // per-vertex hit-mask layout: one byte per hot chunk of every CTA-bin
-    // item, in edge order (fr_moff[e], E+1 entries)
-    g.fr_moff.alloc(E + 1, s);
-    scan_exclusive<uint64_t>(MaskBytes{g.fr_items.get(), item_of_e.get(), g.off.get(), g.col.get()},
-                             g.fr_moff.get(), E, g.fr_moff.get() + E, s);
-    g.fr_mask_bytes = read_scalar(g.fr_moff.get() + E, s);
+  uint32_t* cnt = g.scratch[kSlotCnt].get<uint32_t>(nn, s);
+  TC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nn, s));
+  fr.in = g.scratch[kSlotIn].get<uint32_t>((uint64_t)n + 1, s);
+  fr.e0 = e0;
+  fr.e1 = e1;
+  const bool whole = e0 == 0 && e1 == g.E;
+  if (whole) {
+    kl += scan_exclusive<uint32_t>(InSlotsWhole{g.off.get(), g.deg.get()}, fr.in, n, fr.in + n, s);
   } else {
-    g.fr_items.alloc(1, s);
-    g.fr_e.alloc(1, s);
-    g.fr_moff.alloc(1, s);
-    TC_CUDA(cudaMemsetAsync(g.fr_in.get(), 0, sizeof(uint32_t) * ((uint64_t)n + 1), s));
+    if (e1 > e0) {
+      k_fr_count<<<grid_gs(e1 - e0, dev), kT, 0, s>>>(geo, e0, e1, cnt);
+      TC_LAUNCH();
+      ++kl;
+    }
+    kl += scan_exclusive<uint32_t>(LoadArray<uint32_t>{cnt}, fr.in, n, fr.in + n, s);
+    TC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nn, s));  // the scatter's cursors
   }
-  g.fr_nitems = NI;
+  pl.mark("fr_slots");
+  const uint64_t NI = n ? read_scalar(fr.in + n, s) : 0;
+  fr.nitems = NI;
+  fr.items = g.scratch[kSlotItems].get<uint4>(NI, s);
+  fr.item_u = g.scratch[kSlotItemU].get<uint32_t>(NI, s);
+  // per-vertex: the rows the part's edges come from and their mask blocks
+  fr.mask_bytes = 0;
+  fr.u_lo = 0;
+  fr.u_hi = n ? n - 1 : 0;
+  if (per_vertex && e1 > e0) {
+    if (!whole) {
+      fr.u_lo = read_scalar(g.src.get() + e0, s);
+      fr.u_hi = read_scalar(g.src.get() + e1 - 1, s);
+    }
+    const uint64_t rows = (uint64_t)fr.u_hi - fr.u_lo + 1;
+    fr.rowbase = g.scratch[kSlotRowBase].get<uint64_t>(rows + 1, s);
+    kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get(), fr.u_lo}, fr.rowbase, rows, fr.rowbase + rows,
+                                   s);
+    fr.mask_bytes = read_scalar(fr.rowbase + rows, s);
+    fr.item_mo = g.scratch[kSlotItemMo].get<uint64_t>(NI, s);
+  }
+  pl.mark("fr_rowbase");
+  if (NI) {
+    const unsigned grid = grid_gs(ceil_div64(e1 - e0, kScatterR), dev);
+    if (per_vertex)
+      k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.item_u, fr.item_mo, fr.rowbase,
+                                             fr.u_lo, sums.get());
+    else
+      k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.item_u, nullptr, nullptr, 0,
+                                              sums.get());
+    TC_LAUNCH();
+    ++kl;
+  }
+  pl.mark("fr_scatter");
+  // per-bin work segments
+  {
+    uint32_t* woff = g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s);
+    uint32_t* coff = g.scratch[kSlotCoff].get<uint32_t>((uint64_t)nn + 1, s);
+    DBuf<uint32_t> tot(2, s);
+    DBuf<unsigned long long> np(1, s);
+    TC_CUDA(cudaMemsetAsync(np.get(), 0, sizeof(unsigned long long), s));
+    kl += scan_exclusive<uint32_t>(SegCountBin{g.off.get(), fr.in, true, kWarpSegItems}, woff, n, tot.get(), s);
+    kl += scan_exclusive<uint32_t>(SegCountBin{g.off.get(), fr.in, false, kCtaSegItems}, coff, n, tot.get() + 1, s);
+    uint32_t h[2] = {0, 0};
+    TC_CUDA(cudaMemcpyAsync(h, tot.get(), 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    fr.nw = n ? h[0] : 0;
+    fr.nc = n ? h[1] : 0;
+    fr.wsegs = g.scratch[kSlotWsegs].get<uint4>(fr.nw, s);
+    fr.csegs = g.scratch[kSlotCsegs].get<uint4>(fr.nc, s);
+    if (fr.nw) {
+      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), fr.in, n, true, kWarpSegItems, woff, fr.wsegs, np.get());
+      TC_LAUNCH();
+      ++kl;
+    }
+    if (fr.nc) {
+      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), fr.in, n, false, kCtaSegItems, coff, fr.csegs,
+                                               np.get());
+      TC_LAUNCH();
+      ++kl;
+    }
+    fr.pivots = read_scalar(np.get(), s);
+  }
+  pl.mark("fr_segs");
   const Sums hs = read_scalar(sums.get(), s);
-  g.fr_W = hs.W;
-  g.fr_J = hs.J;
-  g.fr_hot = hs.hot;
-  g.fr_nitems_c = hs.items_c;
-  make_segments(g, PartRange{g.fr_in.get(), g.fr_e.get(), 0, ~0ull}, g.fr_wsegs, g.fr_nwsegs, g.fr_csegs,
-                g.fr_ncsegs, &g.fr_pivots);
-  TC_CUDA(cudaEventRecord(t1, s));
-  TC_CUDA(cudaEventSynchronize(t1));
-  float ms = 0;
-  cudaEventElapsedTime(&ms, t0, t1);
-  g.frontier_ms = ms;
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
-}
-
-void part_segments(tc_graph& g, uint64_t e0, uint64_t e1, DBuf<uint4>& wsegs, uint64_t& nw, DBuf<uint4>& csegs,
-                   uint64_t& nc) {
-  make_segments(g, PartRange{g.fr_in.get(), g.fr_e.get(), e0, e1}, wsegs, nw, csegs, nc, nullptr);
+  fr.W = hs.W;
+  fr.J = hs.J;
+  fr.hot = hs.hot;
+  fr.items_c = hs.items_c;
+  return kl;
 }
 
 }  // namespace tcb

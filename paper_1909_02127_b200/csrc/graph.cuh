@@ -17,6 +17,32 @@
 
 #include "common.cuh"
 
+namespace tcb {
+// Grow-only device scratch owned by a graph handle: the per-count frontier,
+// hit masks and counters are rebuilt by every tc_count in the same buffers,
+// so repeated counts do not remap memory (a cuBLAS-style workspace).
+struct Scratch {
+  DBuf<uint8_t> buf;
+  template <typename T>
+  T* get(uint64_t count, cudaStream_t s) {
+    const uint64_t need = (count ? count : 1) * sizeof(T);
+    if (buf.n < need) {
+      buf.s = s;  // free the old block on the stream that uses it now
+      buf.alloc(need + need / 8, s);
+    }
+    return reinterpret_cast<T*>(buf.get());
+  }
+  void release(cudaStream_t s) {
+    buf.s = s;
+    buf.release();
+  }
+};
+enum ScratchSlot {
+  kSlotCnt, kSlotIn, kSlotItems, kSlotItemU, kSlotItemMo, kSlotRowBase, kSlotWoff, kSlotCoff, kSlotWsegs,
+  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotCount
+};
+}  // namespace tcb
+
 struct tc_graph {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -36,31 +62,10 @@ struct tc_graph {
   uint32_t h0 = 0;
   tcb::DBuf<uint16_t> colH;
   tcb::DBuf<uint32_t> offH;
-  // Level-1 frontier index (frontier.cu): the useful in-edges u->v of every
-  // pivot v (d+(v) > 0, non-empty suffix), grouped by v and sorted by edge id
-  // e -- the transpose of the oriented CSR restricted to wedge-producing
-  // edges, i.e. the reference's level-1 PartialTable rows (u,v)
-  // (matcher.cpp:136-198).  Graph-static, built once with the CSR.
-  //   fr_items[i] = {hb,he,cb,ce} (CTA-bin pivots: hot range in colH, cold
-  //                 range in col) or {b,e,0,0} (warp-bin pivots: col range)
-  //   fr_e[i]     = the edge id (source u = src[e]; multi-GPU ranges)
-  //   fr_in[v]    = first item of pivot v (n+1)
-  //   fr_wsegs / fr_csegs = {v, i0, i1, 0} work segments per bin (whole graph)
-  tcb::DBuf<uint4> fr_items;
-  tcb::DBuf<uint32_t> fr_e, fr_in;
-  //   fr_moff[e] = byte offset of edge e's per-vertex hit masks (1 byte per
-  //   hot chunk of its CTA-bin item), exclusive scan in edge order (E+1), so
-  //   a row's masks are contiguous and an item's length gives its first chunk
-  tcb::DBuf<uint64_t> fr_moff;
-  uint64_t fr_mask_bytes = 0;
-  tcb::DBuf<uint4> fr_wsegs, fr_csegs;
-  uint64_t fr_nitems = 0, fr_nwsegs = 0, fr_ncsegs = 0, fr_pivots = 0;
-  uint64_t fr_W = 0, fr_J = 0, fr_hot = 0, fr_nitems_c = 0;
-  double frontier_ms = 0;
   // multi-GPU work partition (count.cu): oriented-edge ranges [b[p], b[p+1])
-  // with ~equal wedge work, cached for the last part count requested
-  uint32_t cached_parts = 0;
+  // with ~equal wedge work, recomputed by every multi-part count
   std::vector<uint64_t> part_bounds;
+  tcb::Scratch scratch[tcb::kSlotCount];
 };
 
 namespace tcb {
@@ -70,11 +75,68 @@ constexpr uint32_t kWarpMaxDeg = 48;    // warp bin: d+(v) <= 48 (128-slot warp 
 constexpr uint32_t kWarpSegItems = 64;  // items per warp-bin segment
 constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
 
-// Level-1 frontier index (frontier.cu), called at the end of every build.
-void build_frontier(tc_graph& g);
-// Segments of one multi-GPU part (edge range [e0,e1)) -> wsegs/csegs.
-void part_segments(tc_graph& g, uint64_t e0, uint64_t e1, DBuf<uint4>& wsegs, uint64_t& nw, DBuf<uint4>& csegs,
-                   uint64_t& nc);
+// Level-1 frontier of one count (frontier.cu): the useful in-edges u->v of
+// every pivot v (d+(v) > 0, non-empty suffix) in the part's oriented-edge
+// range [e0, e1), grouped by v -- the transpose of the oriented CSR restricted
+// to wedge-producing edges, i.e. the reference's level-1 PartialTable rows
+// (u, v) (matcher.cpp:136-198).  Built inside every tc_count (timed), in the
+// handle's scratch.
+//   items[i]   = {hb,he,cb,ce} (CTA-bin pivots: hot range in colH, cold range
+//                in col) or {b,e,0,0} (warp-bin pivots: col range); an
+//                all-zero item is an in-edge with an empty suffix
+//   item_u[i]  = the source u of the item
+//   item_mo[i] = per-vertex only: byte offset of the item's hit masks (one
+//                byte per hot chunk from its first hot chunk to the row's
+//                last, row_mask_layout() below)
+//   in[v]      = first item of pivot v (n+1)
+//   rowbase[u-u_lo] = per-vertex only: first mask byte of row u (rows
+//                [u_lo, u_hi] of the part)
+//   wsegs / csegs = {v, i0, i1, 0} work segments per bin
+struct Frontier {
+  uint4* items = nullptr;
+  uint32_t* item_u = nullptr;
+  uint64_t* item_mo = nullptr;
+  uint32_t* in = nullptr;
+  uint64_t* rowbase = nullptr;
+  uint4* wsegs = nullptr;
+  uint4* csegs = nullptr;
+  uint64_t e0 = 0, e1 = 0, nitems = 0, nw = 0, nc = 0, pivots = 0, mask_bytes = 0;
+  uint32_t u_lo = 0, u_hi = 0;  // rows the part's edges come from (inclusive)
+  uint64_t W = 0, J = 0, hot = 0, items_c = 0;
+};
+// Returns the number of kernels launched.
+int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Frontier& fr);
+
+// Per-vertex hit-mask layout of row u (closed form, no per-edge scan).  Row u
+// has d = d+(u) out-edges, the last h of them hot (colH[O, O+h), O = offH[u]),
+// c0 = d - h cold.  Item k (edge off[u]+k, suffix positions k+1..d-1) starts
+// its hot part at s_k = max(k+1-c0, 0) and owns one mask byte per chunk
+// cs_k = (O+s_k)>>3 .. c_hi-1, c_hi = (O+h+7)>>3.  The row's block holds the
+// items k = 0..d-2 back to back: P(k) = bytes of items < k.
+struct RowMasks {
+  uint64_t O;
+  uint32_t d, h, c0;
+  uint64_t c_lo, c_hi;
+  __host__ __device__ __forceinline__ RowMasks(uint32_t d_, uint64_t O_, uint32_t h_)
+      : O(O_), d(d_), h(h_), c0(d_ - h_), c_lo(O_ >> 3), c_hi((O_ + h_ + 7) >> 3) {}
+  // sum_{t < x} floor(t/8)
+  __host__ __device__ static __forceinline__ uint64_t F(uint64_t x) {
+    const uint64_t q = x >> 3, r = x & 7;
+    return 4 * q * (q ? q - 1 : 0) + r * q;
+  }
+  __host__ __device__ __forceinline__ uint64_t P(uint32_t k) const {
+    const uint64_t C = c_hi - c_lo;
+    if (k <= c0) return (uint64_t)k * C;
+    const uint64_t S = k - c0;
+    return (uint64_t)c0 * C + S * c_hi - (F(O + S + 1) - F(O + 1));
+  }
+  // total bytes of the row (0 when it has no hot member or < 2 out-edges)
+  __host__ __device__ __forceinline__ uint64_t total() const { return (h == 0 || d < 2) ? 0 : P(d - 1); }
+  __host__ __device__ __forceinline__ uint64_t first_chunk(uint32_t k) const {
+    const uint64_t sk = k + 1 > c0 ? (uint64_t)(k + 1 - c0) : 0;
+    return (O + sk) >> 3;
+  }
+};
 
 // Build pipeline entry points (build.cu).
 void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t n,
@@ -87,7 +149,7 @@ void export_degrees(tc_graph& g, uint32_t* d_deg);
 // Count pipeline (count.cu).
 void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total,
                      uint64_t* d_per_vertex, tc_count_stats* stats);
-// Degree-weighted oriented-edge ranges of a P-way split (cached per handle).
+// Degree-weighted oriented-edge ranges of a P-way split.
 const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts);
 
 // Generators (gen.cu).

@@ -1,0 +1,32 @@
+"""Per-phase device times of tc_count on one config (TCB_PHASES=1 prints them)."""
+import argparse
+import os
+import sys
+
+os.environ.setdefault("TCB_PHASES", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1909_02127_b200 as tc  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--kind", default="rmat")
+ap.add_argument("--scale", type=int, default=24)
+ap.add_argument("--param", type=int, default=16)
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--pv", type=int, default=1)
+a = ap.parse_args()
+k = {"rmat": tc.GEN_RMAT, "kron": tc.GEN_KRON, "er": tc.GEN_ER}[a.kind]
+m = tc.gen_num_edges(k, a.scale, a.param)
+d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+tc.generate(k, a.scale, a.param, out=d)
+g = tc.build_graph_from_pairs(d, 1 << a.scale, m=m)
+del d
+torch.cuda.empty_cache()
+n = 1 << a.scale
+tot = torch.zeros(1, dtype=torch.int64, device="cuda")
+pv = torch.zeros(n, dtype=torch.int64, device="cuda") if a.pv else None
+for i in range(a.iters):
+    print(f"--- iter {i}", file=sys.stderr, flush=True)
+    st = tc.count_triangles_into(g, tot, pv, tc.MatchOptions(per_vertex=bool(a.pv)), stats=True)
+    print(int(tot.item()), {k: round(v, 3) for k, v in st.items() if k.endswith("_ms")}, flush=True)
