@@ -287,7 +287,7 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 // Advance + join for items [i0, i1) of one small pivot (u32 suffix ranges
 // {b,e} in items[i].x/.y), executed by one warp against its private hash.
 template <bool kPerVertex, typename Sink>
-__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items, const uint32_t* __restrict__ item_u,
+__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items,
                                                     uint32_t i0, uint32_t i1, const uint32_t* __restrict__ col,
                                                     const uint32_t* __restrict__ src, const uint32_t* tab,
                                                     uint32_t mask, uint32_t shift, const Sink& sink,
@@ -299,7 +299,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
     const uint32_t my = ib + lane;
     uint32_t b = 0, e = 0, nch = 0;
     if (my < i1) {
-      const uint2 it = __ldcs(reinterpret_cast<const uint2*>(items + my));
+      const uint2 it = __ldcs(reinterpret_cast<const uint2*>(items + (uint64_t)my * (kPerVertex ? 2 : 1)));
       b = it.x;
       e = it.y;
       nch = ((e + 3) >> 2) - (b >> 2);
@@ -338,7 +338,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
     if (kPerVertex) {
       __syncwarp();
       const uint32_t c = item_cnt[lane];
-      if (c) atomicAdd(&sink.t_rank[item_u[owner]], (unsigned long long)c);
+      if (c) atomicAdd(&sink.t_rank[items[(uint64_t)owner * 2 + 1].x], (unsigned long long)c);
       __syncwarp();
     }
   }
@@ -351,7 +351,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint4* __restrict__ items, const uint32_t* __restrict__ item_u, const uint4* __restrict__ segs,
+    const uint4* __restrict__ items, const uint4* __restrict__ segs,
     uint32_t nsegs, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
     const uint32_t h =
-        warp_join_small<kPerVertex>(items, item_u, sg.y, sg.z, col, src, tab, mask, shift, sink, s_item[warp]);
+        warp_join_small<kPerVertex>(items, sg.y, sg.z, col, src, tab, mask, shift, sink, s_item[warp]);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
@@ -410,9 +410,9 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCtaMinBlocks + 1) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint16_t* __restrict__ colH, const uint4* __restrict__ items, const uint32_t* __restrict__ item_u,
+    const uint16_t* __restrict__ colH, const uint4* __restrict__ items,
     const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t h0, uint32_t nbm,
-    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, const uint64_t* __restrict__ item_mo, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
+    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
   __shared__ unsigned long long s_hmo[kPerVertex ? kCtaSegItems : 1];  // hot items' mask offsets
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
       const uint32_t i = threadIdx.x * 2 + r;
       nh[r] = nc[r] = 0;
       if (i < ni) {
-        it[r] = __ldcs(items + i0 + i);
+        it[r] = __ldcs(items + (uint64_t)(i0 + i) * (kPerVertex ? 2 : 1));
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -485,7 +485,10 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
           s_hb[ph] = it[r].x;
           s_he[ph] = it[r].y;
           s_hpre[ph] = ch;
-          if (kPerVertex) s_hmo[ph] = item_mo[i0 + i];
+          if (kPerVertex) {
+            const uint4 ex = __ldcs(items + (uint64_t)(i0 + i) * 2 + 1);
+            s_hmo[ph] = (unsigned long long)ex.z | ((unsigned long long)ex.w << 32);
+          }
           s_hidx[ph] = (uint16_t)i;
           ++ph;
           ch += nh[r];
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
         const uint32_t c = s_icnt[i];
         if (c) {
-          atomicAdd(&t_rank[item_u[i0 + i]], (unsigned long long)c);
+          atomicAdd(&t_rank[items[(uint64_t)(i0 + i) * 2 + 1].x], (unsigned long long)c);
           s_icnt[i] = 0;
         }
       }
@@ -569,26 +572,138 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
   if (lane == 0 && acc) atomicAdd(total, acc);
 }
 
-// Per-vertex counts from the CTA bin's hot hit masks, one warp per row u.
+// Per-vertex counts from the CTA bin's hot hit masks.
 // Mask byte (item k, chunk c) has bit j set iff element 8c+j of colH -- an
 // oriented edge u->x -- closed a triangle (u, v_k, x).  For each hot position
 // p of row u, B[p] = sum over u's items of that bit = the triangles whose
 // low->top edge is u->x_p; then t[x_p] += B[p] and t[u] += sum_p B[p].
 // The row's mask block has the closed-form layout of graph.cuh RowMasks
 // (item k's bytes at rowbase + P(k), chunks cs_k..c_hi-1), so the pass needs
-// no per-item metadata: lanes own 32 consecutive chunks of the row, the warp
-// walks the items k that reach the group (byte loads of one item are
-// coalesced across the lanes), kRowU items in flight, and each byte is spread
-// into 4+4 byte-lane counters by a multiply (b*0x00204081 & 0x01010101).
-// Warp-bin items' bytes are zero (memset): their hits are counted in
-// k_join_warp.  Rows are taken from the top rank down, 32 per queue grab.
+// no per-item metadata.  Lanes own consecutive chunks of the row (groups of
+// 32; narrow rows with C <= 16 chunks split the warp into sub-groups of
+// w = pow2 >= C lanes that take different items), the warp walks the items
+// that reach the group (one item's bytes are coalesced across the lanes),
+// kRowU items in flight, and each byte is spread into 4+4 byte-lane counters
+// by a multiply (b*0x00204081 & 0x01010101).  Warp-bin items' bytes are zero
+// (memset): their hits are counted in k_join_warp.
+//   k_pv_rows        one warp per light row, 32 rows per queue grab (top rank
+//                    down); rows with more than kRowHeavy item-steps are
+//                    appended to a list instead
+//   k_pv_rows_heavy  one CTA per listed row, its 8 warps splitting each
+//                    group's items, partial counters reduced in SMEM
 constexpr int kRowWarps = 8;
 constexpr int kRowU = 8;
+constexpr uint32_t kRowHeavy = 128;
+
+struct RowLanes {
+  uint32_t w, G, sub;  // lanes per sub-group, sub-groups, this lane's sub-group
+  __device__ __forceinline__ RowLanes(uint64_t C, unsigned lane) {
+    if (C > 16) {
+      w = 32;
+    } else {
+      const uint32_t lg = 32 - __clz((uint32_t)C - 1);
+      w = C > 1 ? 1u << lg : 1u;
+    }
+    G = 32 / w;
+    sub = lane / w;
+  }
+};
+
+// Items reaching chunk group [cg, cg+32): all k < c0, and k >= c0 while
+// cs_k <= the group's last chunk.
+__device__ __forceinline__ uint32_t items_reaching(const RowMasks& rm, uint64_t cg, uint32_t span) {
+  const uint64_t clast = (cg + span - 1 < rm.c_hi - 1) ? cg + span - 1 : rm.c_hi - 1;
+  const uint64_t kk = 8 * clast + 7 - rm.O + rm.c0;  // first k with cs_k > clast
+  const uint32_t nk = rm.d - 1;
+  return (uint32_t)(kk < nk ? kk : (uint64_t)nk);
+}
+
+// cnt[j] += bit j of byte (k, c) over items k = ka + sub + G*i in [ka, kb).
+__device__ __forceinline__ void row_accumulate(const RowMasks& rm, const uint8_t* __restrict__ rowm, uint64_t c,
+                                               bool cvalid, const RowLanes& rl, uint32_t ka, uint32_t kb,
+                                               uint32_t (&cnt)[8]) {
+  uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
+  auto fold = [&]() {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
+      cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
+    }
+    acc_lo = acc_hi = nacc = 0;
+  };
+  if (rl.G == 1) {
+    uint64_t P = rm.P(ka);  // incremental: P(k+1) = P(k) + c_hi - cs_k
+    for (uint32_t k0 = ka; k0 < kb; k0 += kRowU) {
+      uint32_t bits[kRowU];
+#pragma unroll
+      for (int t = 0; t < kRowU; ++t) {
+        const uint32_t k = k0 + t;
+        const uint64_t cs = rm.first_chunk(k);
+        bits[t] = (k < kb && cvalid && c >= cs) ? rowm[P + (c - cs)] : 0u;
+        P += rm.c_hi - cs;
+      }
+      if (nacc + kRowU > 255) fold();
+#pragma unroll
+      for (int t = 0; t < kRowU; ++t) {
+        acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
+        acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
+      }
+      nacc += kRowU;
+    }
+  } else {
+    for (uint32_t k0 = ka; k0 < kb; k0 += rl.G * kRowU) {
+      uint32_t bits[kRowU];
+#pragma unroll
+      for (int t = 0; t < kRowU; ++t) {
+        const uint32_t k = k0 + t * rl.G + rl.sub;
+        bits[t] = 0;
+        if (k < kb && cvalid) {
+          const uint64_t cs = rm.first_chunk(k);
+          if (c >= cs) bits[t] = rowm[rm.P(k) + (c - cs)];
+        }
+      }
+      if (nacc + kRowU > 255) fold();
+#pragma unroll
+      for (int t = 0; t < kRowU; ++t) {
+        acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
+        acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
+      }
+      nacc += kRowU;
+    }
+  }
+  fold();
+}
+
+// t[x_p] += B[p] for the 8 positions of chunk c; returns sum B[p].
+__device__ __forceinline__ uint32_t row_emit(const RowMasks& rm, const uint4* __restrict__ colH4, uint64_t c,
+                                             const uint32_t (&cnt)[8], uint32_t h0, uint32_t rc, uint32_t* top,
+                                             unsigned long long* __restrict__ t_rank) {
+  const uint4 q = colH4[c];
+  uint32_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint64_t p = 8 * c + j;
+    if (cnt[j] && p >= rm.O && p < rm.O + rm.h) {
+      const uint32_t x = h0 + hot_u16(q, j);
+      if (x >= rc) atomicAdd(&top[x - rc], cnt[j]);
+      else atomicAdd(&t_rank[x], (unsigned long long)cnt[j]);
+      tot += cnt[j];
+    }
+  }
+  return tot;
+}
+
+__device__ __forceinline__ void flush_top_rows(const uint32_t* top, uint32_t ncnt, uint32_t rc,
+                                               unsigned long long* __restrict__ t_rank) {
+  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x)
+    if (top[i]) atomicAdd(&t_rank[rc + i], (unsigned long long)top[i]);
+}
+
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
     const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t u_hi,
-    uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue,
-    unsigned long long* __restrict__ t_rank) {
+    uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, uint32_t* __restrict__ heavy,
+    unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
   __syncthreads();
@@ -602,13 +717,24 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     if (rb >= nrows) break;
     const uint32_t i = rb + lane;
     uint32_t ul = 0, dl = 0, Ol = 0, hl = 0;
+    bool work = false;
     if (i < nrows) {
       ul = u_hi - i;
       dl = off[ul + 1] - off[ul];
       Ol = offH[ul];
       hl = offH[ul + 1] - Ol;
+      work = hl > 0 && dl >= 2;
+      if (work) {
+        const RowMasks rm(dl, Ol, hl);
+        const uint64_t C = rm.c_hi - rm.c_lo;
+        const uint64_t steps = C > 16 ? (uint64_t)(dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
+        if (steps > kRowHeavy) {
+          heavy[atomicAdd(nheavy, 1u)] = ul;
+          work = false;
+        }
+      }
     }
-    uint32_t rows = __ballot_sync(0xffffffffu, hl > 0 && dl >= 2);
+    uint32_t rows = __ballot_sync(0xffffffffu, work);
     while (rows) {
       const int rj = __ffs(rows) - 1;
       rows &= rows - 1;
@@ -616,117 +742,84 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       const RowMasks rm(__shfl_sync(0xffffffffu, dl, rj), __shfl_sync(0xffffffffu, Ol, rj),
                         __shfl_sync(0xffffffffu, hl, rj));
       const uint8_t* rowm = masks + rowbase[u - u_lo];
-      const uint32_t nk = rm.d - 1;  // items with a non-empty suffix
-      const uint64_t C = rm.c_hi - rm.c_lo;
-      unsigned long long row_total = 0;
-      // t[x_p] += B[p] for the 8 positions of lane chunk c
-      auto emit = [&](uint64_t c, const uint32_t* cnt) {
-        const uint4 q = colH4[c];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint64_t p = 8 * c + j;
-          if (cnt[j] && p >= rm.O && p < rm.O + rm.h) {
-            const uint32_t x = h0 + hot_u16(q, j);
-            if (x >= rc) atomicAdd(&top[x - rc], cnt[j]);
-            else atomicAdd(&t_rank[x], (unsigned long long)cnt[j]);
-            row_total += cnt[j];
-          }
-        }
-      };
-      if (C <= 16) {
-        // narrow row: sub-groups of w = pow2 >= C lanes, one item each
-        // (every item reaches the last chunk), counters summed across them
-        const uint32_t lg = 32 - __clz((uint32_t)C - 1 | 0u), w = C > 1 ? 1u << lg : 1u;
-        const uint32_t G = 32 / w, sub = lane / w;
-        const uint64_t c = rm.c_lo + (lane & (w - 1));
+      const RowLanes rl(rm.c_hi - rm.c_lo, lane);
+      uint32_t row_total = 0;
+      for (uint64_t cg = rm.c_lo; cg < rm.c_hi; cg += rl.w) {
+        const uint64_t c = cg + (lane & (rl.w - 1));
         const bool cvalid = c < rm.c_hi;
-        uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
         uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t k0 = 0; k0 < nk; k0 += G * kRowU) {
-          uint32_t bits[kRowU];
-#pragma unroll
-          for (int t = 0; t < kRowU; ++t) {
-            const uint32_t k = k0 + t * G + sub;
-            bits[t] = 0;
-            if (k < nk && cvalid) {
-              const uint64_t cs = rm.first_chunk(k);
-              if (c >= cs) bits[t] = rowm[rm.P(k) + (c - cs)];
-            }
-          }
-          if (nacc + kRowU > 255) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
-              cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
-            }
-            acc_lo = acc_hi = nacc = 0;
-          }
-#pragma unroll
-          for (int t = 0; t < kRowU; ++t) {
-            acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
-            acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
-          }
-          nacc += kRowU;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
-          cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
-        }
+        row_accumulate(rm, rowm, c, cvalid, rl, 0, items_reaching(rm, cg, rl.w), cnt);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          for (uint32_t o = w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
-        if (sub == 0 && cvalid) emit(c, cnt);
-      } else {
-        for (uint64_t cg = rm.c_lo; cg < rm.c_hi; cg += 32) {
-          const uint64_t c = cg + lane;
-          const bool cvalid = c < rm.c_hi;
-          // items reaching this group: all k < c0, and k >= c0 while cs_k <= last chunk
-          const uint64_t clast = (cg + 31 < rm.c_hi - 1) ? cg + 31 : rm.c_hi - 1;
-          const uint64_t kk = 8 * clast + 7 - rm.O + rm.c0;  // first k with cs_k > clast
-          const uint32_t K = (uint32_t)(kk < nk ? kk : (uint64_t)nk);
-          uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
-          uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          uint64_t P = 0;  // P(k) of the current k
-          for (uint32_t k0 = 0; k0 < K; k0 += kRowU) {
-            uint32_t bits[kRowU];
-#pragma unroll
-            for (int t = 0; t < kRowU; ++t) {
-              const uint32_t k = k0 + t;
-              const uint64_t cs = rm.first_chunk(k);
-              bits[t] = (k < K && cvalid && c >= cs) ? rowm[P + (c - cs)] : 0u;
-              P += rm.c_hi - cs;
-            }
-            if (nacc + kRowU > 255) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
-                cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
-              }
-              acc_lo = acc_hi = nacc = 0;
-            }
-#pragma unroll
-            for (int t = 0; t < kRowU; ++t) {
-              acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
-              acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
-            }
-            nacc += kRowU;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            cnt[j] += (acc_lo >> (8 * j)) & 0xffu;
-            cnt[4 + j] += (acc_hi >> (8 * j)) & 0xffu;
-          }
-          if (cvalid) emit(c, cnt);
-        }
+          for (uint32_t o = rl.w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
+        if (rl.sub == 0 && cvalid) row_total += row_emit(rm, colH4, c, cnt, h0, rc, top, t_rank);
       }
       row_total = warp_sum(row_total);
-      if (lane == 0 && row_total) atomicAdd(&t_rank[u], row_total);
+      if (lane == 0 && row_total) atomicAdd(&t_rank[u], (unsigned long long)row_total);
     }
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x)
-    if (top[i]) atomicAdd(&t_rank[rc + i], (unsigned long long)top[i]);
+  flush_top_rows(top, ncnt, rc, t_rank);
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
+    const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
+    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t h0,
+    uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, const uint32_t* __restrict__ heavy,
+    const unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
+  extern __shared__ uint32_t top[];
+  __shared__ uint32_t red[kRowWarps][8][32];
+  __shared__ uint32_t s_row;
+  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
+  const uint32_t nh = *nheavy;
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_row = atomicAdd(queue, 1u);
+    __syncthreads();
+    const uint32_t r = s_row;
+    if (r >= nh) break;
+    const uint32_t u = heavy[r];
+    const uint32_t d = off[u + 1] - off[u], O = offH[u];
+    const RowMasks rm(d, O, offH[u + 1] - O);
+    const uint8_t* rowm = masks + rowbase[u - u_lo];
+    const RowLanes rl(rm.c_hi - rm.c_lo, lane);
+    uint32_t row_total = 0;
+    for (uint64_t cg = rm.c_lo; cg < rm.c_hi; cg += rl.w) {
+      const uint64_t c = cg + (lane & (rl.w - 1));
+      const bool cvalid = c < rm.c_hi;
+      const uint32_t K = items_reaching(rm, cg, rl.w);
+      // this warp's slice of the items, aligned to the sub-group stride
+      const uint32_t per = (K + kRowWarps - 1) / kRowWarps;
+      const uint32_t ka = min(K, warp * per), kb = min(K, ka + per);
+      uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      row_accumulate(rm, rowm, c, cvalid, rl, ka, kb, cnt);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        for (uint32_t o = rl.w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
+        red[warp][j][lane] = cnt[j];
+      }
+      __syncthreads();
+      if (warp == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t t = 0;
+#pragma unroll
+          for (int w2 = 0; w2 < kRowWarps; ++w2) t += red[w2][j][lane];
+          cnt[j] = t;
+        }
+        if (rl.sub == 0 && cvalid) row_total += row_emit(rm, colH4, c, cnt, h0, rc, top, t_rank);
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      row_total = warp_sum(row_total);
+      if (lane == 0 && row_total) atomicAdd(&t_rank[u], (unsigned long long)row_total);
+    }
+  }
+  __syncthreads();
+  flush_top_rows(top, ncnt, rc, t_rank);
 }
 
 __global__ void k_gather_pv(const unsigned long long* __restrict__ t_rank, const uint32_t* __restrict__ rank_of,
@@ -859,7 +952,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const unsigned grid =
         (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
     pl.mark("warp_setup");
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), fr.items, fr.item_u,
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), fr.items,
                                          wsegs, (uint32_t)NSW, rc_w, ncnt_w, t_rank, acc.get());
     TC_LAUNCH();
     ++launches;
@@ -883,23 +976,32 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
     pl.mark("cta_setup");
     kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), g.colH.get(), fr.items,
-                                        fr.item_u, csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
-                                        slab_cap, slab, fr.item_mo, masks, t_rank, acc.get());
+                                        csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
+                                        slab_cap, slab, masks, t_rank, acc.get());
     TC_LAUNCH();
     ++launches;
     pl.mark("join_cta");
     if (pv) {
       // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics)
-      DBuf<unsigned int> rq(1, s);
-      TC_CUDA(cudaMemsetAsync(rq.get(), 0, sizeof(unsigned int), s));
+      DBuf<unsigned int> rq(3, s);  // light queue, heavy queue, heavy count
+      TC_CUDA(cudaMemsetAsync(rq.get(), 0, 3 * sizeof(unsigned int), s));
+      uint32_t* heavy = g.scratch[kSlotHeavy].get<uint32_t>((uint64_t)(fr.u_hi - fr.u_lo) + 1, s);
       const uint32_t rcnt = n < top_cnt ? n : top_cnt;
       const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
       TC_CUDA(cudaFuncSetAttribute(k_pv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      int rocc = 0;
+      TC_CUDA(cudaFuncSetAttribute(k_pv_rows_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      int rocc = 0, hocc = 0;
       TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rocc, k_pv_rows, kRowWarps * 32, rsm));
+      TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_pv_rows_heavy, kRowWarps * 32, rsm));
       k_pv_rows<<<(unsigned)(sms * std::max(rocc, 1)), kRowWarps * 32, rsm, s>>>(
           g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, fr.u_hi, g.h0, n - rcnt, rcnt,
-          rq.get(), t_rank);
+          rq.get(), heavy, rq.get() + 2, t_rank);
+      TC_LAUNCH();
+      ++launches;
+      pl.mark("pv_rows_light");
+      k_pv_rows_heavy<<<(unsigned)(sms * std::max(hocc, 1)), kRowWarps * 32, rsm, s>>>(
+          g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, g.h0, n - rcnt, rcnt,
+          rq.get() + 1, heavy, rq.get() + 2, t_rank);
       TC_LAUNCH();
       ++launches;
       pl.mark("pv_rows");

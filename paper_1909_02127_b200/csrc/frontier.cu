@@ -132,8 +132,7 @@ constexpr int kScatterR = 4;
 template <bool kPV>
 __global__ void __launch_bounds__(kT) k_fr_scatter(ItemGeom geo, uint64_t e0, uint64_t e1,
                                                   const uint32_t* __restrict__ in, uint32_t* __restrict__ cursor,
-                                                  uint4* __restrict__ items, uint32_t* __restrict__ item_u,
-                                                  uint64_t* __restrict__ item_mo,
+                                                  uint4* __restrict__ items,
                                                   const uint64_t* __restrict__ rowbase, uint32_t u_lo,
                                                   Sums* __restrict__ sums) {
   unsigned long long W = 0, J = 0, H = 0, IC = 0;
@@ -158,8 +157,12 @@ __global__ void __launch_bounds__(kT) k_fr_scatter(ItemGeom geo, uint64_t e0, ui
     for (int r = 0; r < kScatterR; ++r) {
       W += q[r].dv;
       if (!q[r].claim) continue;
-      items[pos[r]] = q[r].it;
-      item_u[pos[r]] = q[r].u;
+      constexpr int S = kPV ? 2 : 1;  // uint4s per item record
+      uint64_t mo = 0;
+      if (kPV && q[r].useful && q[r].dv > kWarpMaxDeg && q[r].it.y > q[r].it.x)
+        mo = rowbase[q[r].u - u_lo] + RowMasks(q[r].d, q[r].O, q[r].h).P(q[r].k);
+      items[(uint64_t)pos[r] * S] = q[r].it;
+      if (kPV) items[(uint64_t)pos[r] * S + 1] = make_uint4(q[r].u, 0u, (uint32_t)mo, (uint32_t)(mo >> 32));
       if (!q[r].useful) continue;
       if (q[r].dv <= kWarpMaxDeg) {
         J += q[r].it.y - q[r].it.x;
@@ -167,8 +170,6 @@ __global__ void __launch_bounds__(kT) k_fr_scatter(ItemGeom geo, uint64_t e0, ui
         J += (q[r].it.y - q[r].it.x) + (q[r].it.w - q[r].it.z);
         H += q[r].it.y - q[r].it.x;
         ++IC;
-        if (kPV && q[r].it.y > q[r].it.x)
-          item_mo[pos[r]] = rowbase[q[r].u - u_lo] + RowMasks(q[r].d, q[r].O, q[r].h).P(q[r].k);
       }
     }
   }
@@ -246,8 +247,7 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   pl.mark("fr_slots");
   const uint64_t NI = n ? read_scalar(fr.in + n, s) : 0;
   fr.nitems = NI;
-  fr.items = g.scratch[kSlotItems].get<uint4>(NI, s);
-  fr.item_u = g.scratch[kSlotItemU].get<uint32_t>(NI, s);
+  fr.items = g.scratch[kSlotItems].get<uint4>(NI * (per_vertex ? 2 : 1), s);
   // per-vertex: the rows the part's edges come from and their mask blocks
   fr.mask_bytes = 0;
   fr.u_lo = 0;
@@ -262,16 +262,15 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get(), fr.u_lo}, fr.rowbase, rows, fr.rowbase + rows,
                                    s);
     fr.mask_bytes = read_scalar(fr.rowbase + rows, s);
-    fr.item_mo = g.scratch[kSlotItemMo].get<uint64_t>(NI, s);
   }
   pl.mark("fr_rowbase");
   if (NI) {
     const unsigned grid = grid_gs(ceil_div64(e1 - e0, kScatterR), dev);
     if (per_vertex)
-      k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.item_u, fr.item_mo, fr.rowbase,
+      k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.rowbase,
                                              fr.u_lo, sums.get());
     else
-      k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.item_u, nullptr, nullptr, 0,
+      k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, nullptr, 0,
                                               sums.get());
     TC_LAUNCH();
     ++kl;

@@ -38,8 +38,8 @@ struct Scratch {
   }
 };
 enum ScratchSlot {
-  kSlotCnt, kSlotIn, kSlotItems, kSlotItemU, kSlotItemMo, kSlotRowBase, kSlotWoff, kSlotCoff, kSlotWsegs,
-  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotCount
+  kSlotCnt, kSlotIn, kSlotItems, kSlotRowBase, kSlotWoff, kSlotCoff, kSlotWsegs,
+  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotCount
 };
 }  // namespace tcb
 
@@ -81,21 +81,20 @@ constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
 // to wedge-producing edges, i.e. the reference's level-1 PartialTable rows
 // (u, v) (matcher.cpp:136-198).  Built inside every tc_count (timed), in the
 // handle's scratch.
-//   items[i]   = {hb,he,cb,ce} (CTA-bin pivots: hot range in colH, cold range
-//                in col) or {b,e,0,0} (warp-bin pivots: col range); an
-//                all-zero item is an in-edge with an empty suffix
-//   item_u[i]  = the source u of the item
-//   item_mo[i] = per-vertex only: byte offset of the item's hit masks (one
-//                byte per hot chunk from its first hot chunk to the row's
-//                last, row_mask_layout() below)
+//   items      one record of S uint4 per item (S = 1, or 2 with per-vertex
+//                counts), written as one 16/32-byte store:
+//                [0] {hb,he,cb,ce} (CTA-bin pivots: hot range in colH, cold
+//                    range in col) or {b,e,0,0} (warp-bin pivots: col range);
+//                    all-zero = an in-edge with an empty suffix
+//                [1] {u, 0, mo_lo, mo_hi}: the source u and the byte offset of
+//                    the item's hit masks (one byte per hot chunk from its
+//                    first hot chunk to the row's last, RowMasks below)
 //   in[v]      = first item of pivot v (n+1)
 //   rowbase[u-u_lo] = per-vertex only: first mask byte of row u (rows
 //                [u_lo, u_hi] of the part)
 //   wsegs / csegs = {v, i0, i1, 0} work segments per bin
 struct Frontier {
   uint4* items = nullptr;
-  uint32_t* item_u = nullptr;
-  uint64_t* item_mo = nullptr;
   uint32_t* in = nullptr;
   uint64_t* rowbase = nullptr;
   uint4* wsegs = nullptr;
