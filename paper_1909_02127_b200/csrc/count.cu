@@ -54,9 +54,16 @@ constexpr int kHotWin = TCB_HOT_WIN;              // hot chunk loads in flight p
 constexpr int kCtaMinBlocks = TCB_MIN_BLOCKS;     // CTA-bin kernel residency target
 
 __host__ __device__ __forceinline__ uint32_t table_size_for(uint32_t members) {
-  uint32_t t = 32;  // load factor <= 1/2
-  while (t < 2 * members) t <<= 1;
+  // smallest power of two >= max(32, 2*members): load factor <= 1/2
+  const uint32_t m2 = 2 * members;
+  if (m2 <= 32) return 32;
+#ifdef __CUDA_ARCH__
+  return 1u << (32 - __clz(m2 - 1));
+#else
+  uint32_t t = 32;
+  while (t < m2) t <<= 1;
   return t;
+#endif
 }
 
 __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
     if (cold) {
       ts = table_size_for(cold);
       tmask = ts - 1;
-      tshift = 32 - log2_pow2(ts);
+      tshift = __clz(ts) + 1;  // 32 - log2(ts), ts a power of two
       tab = ts <= stab_slots ? stab : gtab;
       for (uint32_t j = threadIdx.x; j < cold; j += kJoinThreads) hash_insert(tab, tmask, tshift, col[nb + j]);
       if (tab == gtab) __threadfence_block();
@@ -541,10 +548,16 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
     if (ncold && !(g_pv_dbg & 4)) {
       const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kJoinWarps);
       const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kJoinWarps);
-      h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
-                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
-                          return probe_cold<kPerVertex>(qq, c, b, e, tab, tmask, tshift, sink);
-                        });
+      if (tab == stab)  // SMEM table (LDS probes); the global slab only for huge pivots
+        h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
+                             [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
+                               return probe_cold<kPerVertex>(qq, c, b, e, stab, tmask, tshift, sink);
+                             });
+      else
+        h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
+                             [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
+                               return probe_cold<kPerVertex>(qq, c, b, e, gtab, tmask, tshift, sink);
+                             });
     }
     acc += h;
     if (kPerVertex) {

@@ -15,6 +15,7 @@ ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--param", type=int, default=16)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--pv", type=int, default=1)
+ap.add_argument("--parts", type=int, default=1)
 a = ap.parse_args()
 k = {"rmat": tc.GEN_RMAT, "kron": tc.GEN_KRON, "er": tc.GEN_ER}[a.kind]
 m = tc.gen_num_edges(k, a.scale, a.param)
@@ -28,5 +29,12 @@ tot = torch.zeros(1, dtype=torch.int64, device="cuda")
 pv = torch.zeros(n, dtype=torch.int64, device="cuda") if a.pv else None
 for i in range(a.iters):
     print(f"--- iter {i}", file=sys.stderr, flush=True)
-    st = tc.count_triangles_into(g, tot, pv, tc.MatchOptions(per_vertex=bool(a.pv)), stats=True)
-    print(int(tot.item()), {k: round(v, 3) for k, v in st.items() if k.endswith("_ms")}, flush=True)
+    T, ms = 0, {}
+    for p in range(a.parts):
+        st = tc.count_triangles_into(g, tot, pv, tc.MatchOptions(per_vertex=bool(a.pv), part_index=p,
+                                                                 part_count=a.parts), stats=True)
+        T += int(tot.item())
+        for k, v in st.items():
+            if k.endswith("_ms"):
+                ms[k] = ms.get(k, 0) + v
+    print(T, {k: round(v, 3) for k, v in ms.items()}, flush=True)
