@@ -610,11 +610,11 @@ constexpr uint32_t kRowHeavy = 128;
 
 struct RowLanes {
   uint32_t w, G, sub;  // lanes per sub-group, sub-groups, this lane's sub-group
-  __device__ __forceinline__ RowLanes(uint64_t C, unsigned lane) {
+  __device__ __forceinline__ RowLanes(uint32_t C, unsigned lane) {
     if (C > 16) {
       w = 32;
     } else {
-      const uint32_t lg = 32 - __clz((uint32_t)C - 1);
+      const uint32_t lg = 32 - __clz(C - 1);
       w = C > 1 ? 1u << lg : 1u;
     }
     G = 32 / w;
@@ -622,19 +622,45 @@ struct RowLanes {
   }
 };
 
-// Items reaching chunk group [cg, cg+32): all k < c0, and k >= c0 while
-// cs_k <= the group's last chunk.
-__device__ __forceinline__ uint32_t items_reaching(const RowMasks& rm, uint64_t cg, uint32_t span) {
-  const uint64_t clast = (cg + span - 1 < rm.c_hi - 1) ? cg + span - 1 : rm.c_hi - 1;
-  const uint64_t kk = 8 * clast + 7 - rm.O + rm.c0;  // first k with cs_k > clast
-  const uint32_t nk = rm.d - 1;
-  return (uint32_t)(kk < nk ? kk : (uint64_t)nk);
+// Row geometry relative to the row's first chunk c_lo (32-bit): item k's
+// first chunk is csr_k = (o7 + max(k+1-c0, 0)) >> 3, it owns C - csr_k mask
+// bytes, P(k) = bytes of the items before it.
+struct RowRel {
+  uint32_t o7, c0, C, nk;
+  __device__ __forceinline__ explicit RowRel(const RowMasks& rm)
+      : o7((uint32_t)(rm.O & 7)), c0(rm.c0), C((uint32_t)(rm.c_hi - rm.c_lo)), nk(rm.d - 1) {}
+  __device__ __forceinline__ uint32_t csr(uint32_t k) const {
+    const int sk = max((int)(k + 1 - c0), 0);
+    return (o7 + (uint32_t)sk) >> 3;
+  }
+  __device__ static __forceinline__ uint32_t F(uint32_t x) {  // sum_{t < x} floor(t/8)
+    const uint32_t q = x >> 3, r = x & 7;
+    return 4 * q * (q ? q - 1 : 0) + r * q;
+  }
+  __device__ __forceinline__ uint32_t P(uint32_t k) const {
+    if (k <= c0) return k * C;
+    const uint32_t S = k - c0;
+    return c0 * C + S * C - (F(o7 + S + 1) - F(o7 + 1));
+  }
+  // items reaching relative chunk group [g, g+span): all k < c0, and k >= c0
+  // while csr_k <= the group's last chunk
+  __device__ __forceinline__ uint32_t reaching(uint32_t g, uint32_t span) const {
+    const uint32_t last = min(g + span, C) - 1;
+    const uint32_t kk = 8 * last + 7 - o7 + c0;  // first k with csr_k > last
+    return min(kk, nk);
+  }
+};
+
+// byte b -> its 8 bits spread over 8 byte lanes (x: bits 0-3, y: bits 4-7)
+__device__ __forceinline__ void init_spread(uint2* s_spread) {
+  for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+    s_spread[b] = make_uint2(((b & 0xfu) * 0x00204081u) & 0x01010101u, ((b >> 4) * 0x00204081u) & 0x01010101u);
 }
 
-// cnt[j] += bit j of byte (k, c) over items k = ka + sub + G*i in [ka, kb).
-__device__ __forceinline__ void row_accumulate(const RowMasks& rm, const uint8_t* __restrict__ rowm, uint64_t c,
+// cnt[j] += bit j of byte (k, cr) over items k = ka + sub + G*i in [ka, kb).
+__device__ __forceinline__ void row_accumulate(const RowRel& rr, const uint8_t* __restrict__ rowm, uint32_t cr,
                                                bool cvalid, const RowLanes& rl, uint32_t ka, uint32_t kb,
-                                               uint32_t (&cnt)[8]) {
+                                               const uint2* s_spread, uint32_t (&cnt)[8]) {
   uint32_t acc_lo = 0, acc_hi = 0, nacc = 0;
   auto fold = [&]() {
 #pragma unroll
@@ -644,23 +670,40 @@ __device__ __forceinline__ void row_accumulate(const RowMasks& rm, const uint8_t
     }
     acc_lo = acc_hi = nacc = 0;
   };
+  auto add = [&](uint32_t b) {
+    const uint2 sp = s_spread[b];
+    acc_lo += sp.x;
+    acc_hi += sp.y;
+  };
   if (rl.G == 1) {
-    uint64_t P = rm.P(ka);  // incremental: P(k+1) = P(k) + c_hi - cs_k
-    for (uint32_t k0 = ka; k0 < kb; k0 += kRowU) {
+    // items before c0 start at the row's first chunk: P(k) = k*C
+    const uint32_t kbA = min(kb, rr.c0);
+    uint32_t P = ka * rr.C + cr;
+    for (uint32_t k0 = ka; k0 < kbA; k0 += kRowU) {
       uint32_t bits[kRowU];
 #pragma unroll
       for (int t = 0; t < kRowU; ++t) {
-        const uint32_t k = k0 + t;
-        const uint64_t cs = rm.first_chunk(k);
-        bits[t] = (k < kb && cvalid && c >= cs) ? rowm[P + (c - cs)] : 0u;
-        P += rm.c_hi - cs;
+        bits[t] = (k0 + t < kbA && cvalid) ? rowm[P] : 0u;
+        P += rr.C;
       }
       if (nacc + kRowU > 255) fold();
 #pragma unroll
+      for (int t = 0; t < kRowU; ++t) add(bits[t]);
+      nacc += kRowU;
+    }
+    const uint32_t kaB = max(ka, rr.c0);
+    uint32_t PB = rr.P(kaB);
+    for (uint32_t k0 = kaB; k0 < kb; k0 += kRowU) {
+      uint32_t bits[kRowU];
+#pragma unroll
       for (int t = 0; t < kRowU; ++t) {
-        acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
-        acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
+        const uint32_t cs = (rr.o7 + (k0 + t + 1 - rr.c0)) >> 3;
+        bits[t] = (k0 + t < kb && cvalid && cr >= cs) ? rowm[PB + cr - cs] : 0u;
+        PB += rr.C - cs;
       }
+      if (nacc + kRowU > 255) fold();
+#pragma unroll
+      for (int t = 0; t < kRowU; ++t) add(bits[t]);
       nacc += kRowU;
     }
   } else {
@@ -671,39 +714,29 @@ __device__ __forceinline__ void row_accumulate(const RowMasks& rm, const uint8_t
         const uint32_t k = k0 + t * rl.G + rl.sub;
         bits[t] = 0;
         if (k < kb && cvalid) {
-          const uint64_t cs = rm.first_chunk(k);
-          if (c >= cs) bits[t] = rowm[rm.P(k) + (c - cs)];
+          const uint32_t cs = rr.csr(k);
+          if (cr >= cs) bits[t] = rowm[rr.P(k) + cr - cs];
         }
       }
       if (nacc + kRowU > 255) fold();
 #pragma unroll
-      for (int t = 0; t < kRowU; ++t) {
-        acc_lo += ((bits[t] & 0xfu) * 0x00204081u) & 0x01010101u;
-        acc_hi += ((bits[t] >> 4) * 0x00204081u) & 0x01010101u;
-      }
+      for (int t = 0; t < kRowU; ++t) add(bits[t]);
       nacc += kRowU;
     }
   }
   fold();
 }
 
-// t[x_p] += B[p] for the 8 positions of chunk c; returns sum B[p].
-__device__ __forceinline__ uint32_t row_emit(const RowMasks& rm, const uint4* __restrict__ colH4, uint64_t c,
-                                             const uint32_t (&cnt)[8], uint32_t h0, uint32_t rc, uint32_t* top,
-                                             unsigned long long* __restrict__ t_rank) {
-  const uint4 q = colH4[c];
-  uint32_t tot = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint64_t p = 8 * c + j;
-    if (cnt[j] && p >= rm.O && p < rm.O + rm.h) {
-      const uint32_t x = h0 + hot_u16(q, j);
-      if (x >= rc) atomicAdd(&top[x - rc], cnt[j]);
-      else atomicAdd(&t_rank[x], (unsigned long long)cnt[j]);
-      tot += cnt[j];
-    }
-  }
-  return tot;
+// t[x_p] += cnt for position j of chunk c (global); returns the count added.
+__device__ __forceinline__ uint32_t row_emit1(const RowMasks& rm, const uint4& q, uint64_t c, int j, uint32_t cnt,
+                                              uint32_t h0, uint32_t rc, uint32_t* top,
+                                              unsigned long long* __restrict__ t_rank) {
+  const uint64_t p = 8 * c + j;
+  if (!cnt || p < rm.O || p >= rm.O + rm.h) return 0;
+  const uint32_t x = h0 + hot_u16(q, j);
+  if (x >= rc) atomicAdd(&top[x - rc], cnt);
+  else atomicAdd(&t_rank[x], (unsigned long long)cnt);
+  return cnt;
 }
 
 __device__ __forceinline__ void flush_top_rows(const uint32_t* top, uint32_t ncnt, uint32_t rc,
@@ -718,7 +751,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, uint32_t* __restrict__ heavy,
     unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
+  __shared__ uint2 s_spread[256];
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
+  init_spread(s_spread);
   __syncthreads();
   const unsigned lane = lane_id();
   const uint32_t nrows = u_hi - u_lo + 1;
@@ -739,8 +774,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       work = hl > 0 && dl >= 2;
       if (work) {
         const RowMasks rm(dl, Ol, hl);
-        const uint64_t C = rm.c_hi - rm.c_lo;
-        const uint64_t steps = C > 16 ? (uint64_t)(dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
+        const uint32_t C = (uint32_t)(rm.c_hi - rm.c_lo);
+        const uint32_t steps = C > 16 ? (dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
         if (steps > kRowHeavy) {
           heavy[atomicAdd(nheavy, 1u)] = ul;
           work = false;
@@ -754,18 +789,34 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       const uint32_t u = __shfl_sync(0xffffffffu, ul, rj);
       const RowMasks rm(__shfl_sync(0xffffffffu, dl, rj), __shfl_sync(0xffffffffu, Ol, rj),
                         __shfl_sync(0xffffffffu, hl, rj));
+      const RowRel rr(rm);
       const uint8_t* rowm = masks + rowbase[u - u_lo];
-      const RowLanes rl(rm.c_hi - rm.c_lo, lane);
+      const RowLanes rl(rr.C, lane);
       uint32_t row_total = 0;
-      for (uint64_t cg = rm.c_lo; cg < rm.c_hi; cg += rl.w) {
-        const uint64_t c = cg + (lane & (rl.w - 1));
-        const bool cvalid = c < rm.c_hi;
+      for (uint32_t g = 0; g < rr.C; g += rl.w) {
+        const uint32_t cr = g + (lane & (rl.w - 1));
+        const bool cvalid = cr < rr.C;
         uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        row_accumulate(rm, rowm, c, cvalid, rl, 0, items_reaching(rm, cg, rl.w), cnt);
+        row_accumulate(rr, rowm, cr, cvalid, rl, 0, rr.reaching(g, rl.w), s_spread, cnt);
+        if (rl.G > 1) {  // sum the sub-groups: counts < 2^16 here, two per word
+          uint32_t pk[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          for (uint32_t o = rl.w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
-        if (rl.sub == 0 && cvalid) row_total += row_emit(rm, colH4, c, cnt, h0, rc, top, t_rank);
+          for (int j = 0; j < 4; ++j) pk[j] = cnt[2 * j] | (cnt[2 * j + 1] << 16);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            for (uint32_t o = rl.w; o < 32; o <<= 1) pk[j] += __shfl_xor_sync(0xffffffffu, pk[j], o);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            cnt[2 * j] = pk[j] & 0xffffu;
+            cnt[2 * j + 1] = pk[j] >> 16;
+          }
+        }
+        if (rl.sub == 0 && cvalid) {
+          const uint64_t c = rm.c_lo + cr;
+          const uint4 q = colH4[c];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) row_total += row_emit1(rm, q, c, j, cnt[j], h0, rc, top, t_rank);
+        }
       }
       row_total = warp_sum(row_total);
       if (lane == 0 && row_total) atomicAdd(&t_rank[u], (unsigned long long)row_total);
@@ -782,11 +833,14 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     const unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];
   __shared__ uint32_t red[kRowWarps][8][32];
+  __shared__ uint2 s_spread[256];
   __shared__ uint32_t s_row;
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
+  init_spread(s_spread);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
   const uint32_t nh = *nheavy;
+  uint32_t my_total = 0;  // this warp's share of the current row's t[u]
   while (true) {
     __syncthreads();
     if (threadIdx.x == 0) s_row = atomicAdd(queue, 1u);
@@ -796,40 +850,39 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     const uint32_t u = heavy[r];
     const uint32_t d = off[u + 1] - off[u], O = offH[u];
     const RowMasks rm(d, O, offH[u + 1] - O);
+    const RowRel rr(rm);
     const uint8_t* rowm = masks + rowbase[u - u_lo];
-    const RowLanes rl(rm.c_hi - rm.c_lo, lane);
-    uint32_t row_total = 0;
-    for (uint64_t cg = rm.c_lo; cg < rm.c_hi; cg += rl.w) {
-      const uint64_t c = cg + (lane & (rl.w - 1));
-      const bool cvalid = c < rm.c_hi;
-      const uint32_t K = items_reaching(rm, cg, rl.w);
-      // this warp's slice of the items, aligned to the sub-group stride
+    const RowLanes rl(rr.C, lane);
+    my_total = 0;
+    for (uint32_t g = 0; g < rr.C; g += rl.w) {
+      const uint32_t cr = g + (lane & (rl.w - 1));
+      const bool cvalid = cr < rr.C;
+      const uint32_t K = rr.reaching(g, rl.w);
+      // this warp's slice of the items
       const uint32_t per = (K + kRowWarps - 1) / kRowWarps;
       const uint32_t ka = min(K, warp * per), kb = min(K, ka + per);
       uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      row_accumulate(rm, rowm, c, cvalid, rl, ka, kb, cnt);
+      row_accumulate(rr, rowm, cr, cvalid, rl, ka, kb, s_spread, cnt);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         for (uint32_t o = rl.w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
         red[warp][j][lane] = cnt[j];
       }
       __syncthreads();
-      if (warp == 0) {
+      // warp w emits position j = w of every chunk of the group
+      {
+        uint32_t t = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint32_t t = 0;
-#pragma unroll
-          for (int w2 = 0; w2 < kRowWarps; ++w2) t += red[w2][j][lane];
-          cnt[j] = t;
+        for (int w2 = 0; w2 < kRowWarps; ++w2) t += red[w2][warp][lane];
+        if (rl.sub == 0 && cvalid && t) {
+          const uint64_t c = rm.c_lo + cr;
+          my_total += row_emit1(rm, colH4[c], c, (int)warp, t, h0, rc, top, t_rank);
         }
-        if (rl.sub == 0 && cvalid) row_total += row_emit(rm, colH4, c, cnt, h0, rc, top, t_rank);
       }
       __syncthreads();
     }
-    if (warp == 0) {
-      row_total = warp_sum(row_total);
-      if (lane == 0 && row_total) atomicAdd(&t_rank[u], (unsigned long long)row_total);
-    }
+    my_total = warp_sum(my_total);
+    if (lane == 0 && my_total) atomicAdd(&t_rank[u], (unsigned long long)my_total);
   }
   __syncthreads();
   flush_top_rows(top, ncnt, rc, t_rank);
