@@ -15,7 +15,9 @@
 //   radix_sort_u64 + run-count + scan -> oriented CSR (off/col/src)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "graph.cuh"
 #include "prim.cuh"
@@ -143,44 +145,6 @@ __global__ void k_split_oriented(const uint64_t* __restrict__ ok, uint64_t E, in
   }
 }
 
-// CSR (sorted rows) -> canonical unique keys: entries (u,v) with v > u, in
-// row order, are already sorted and unique.  row_of(i) comes from a scan of
-// "rows ending at i" counts.
-__global__ void k_row_ends(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ ends) {
-  const uint64_t total = off[n];
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-       u += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = off[u + 1];
-    if (e < total) atomicAdd(&ends[e], 1u);
-  }
-}
-
-struct RowOf {
-  const uint32_t* excl;
-  const uint32_t* ends;
-};
-
-struct UpperFlag {  // entry i of row r is kept iff nbrs[i] > r
-  const uint32_t* nbrs;
-  const uint32_t* row_excl;
-  const uint32_t* ends;
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-    const uint32_t r = row_excl[i] + ends[i];
-    return nbrs[i] > r ? 1u : 0u;
-  }
-};
-
-__global__ void k_csr_keys(const uint32_t* __restrict__ nbrs, uint64_t total, const uint32_t* __restrict__ row_excl,
-                           const uint32_t* __restrict__ ends, const uint32_t* __restrict__ pos, int b,
-                           uint64_t* __restrict__ keys) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = row_excl[i] + ends[i];
-    const uint32_t v = nbrs[i];
-    if (v > r) keys[pos[i]] = ((uint64_t)r << b) | v;
-  }
-}
-
 // export: oriented edge -> both directed keys in id space
 __global__ void k_directed_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ col, uint64_t E,
                                 const uint32_t* __restrict__ id_of, int b, uint64_t* __restrict__ keys) {
@@ -230,6 +194,403 @@ __global__ void k_hot_offsets(const uint32_t* __restrict__ off, uint32_t n, uint
   }
 }
 
+// ---- CSR route (tc_graph_from_csr): rank-space rows without a global sort ----
+// The input rows are complete adjacency lists, so each id-row u is handled by
+// one warp (a CTA for rows longer than kBigRow): pass 0 counts the entries
+// kept by the orientation, rank(v) > rank(u), into d+(rank u); pass 1 writes
+// them at off[rank u] + their rank among the row's kept entries (ballot
+// prefix, deterministic); then every rank-space row is sorted in place.
+constexpr uint32_t kBigRow = 4096;
+
+__global__ void k_csr_deg(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ deg,
+                          uint32_t* __restrict__ big, unsigned int* __restrict__ nbig, int* __restrict__ bad) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = off[u], b = off[u + 1];
+    if (b < a) {
+      atomicOr(bad, 1);
+      deg[u] = 0;
+      continue;
+    }
+    const uint32_t d = (uint32_t)(b - a);
+    deg[u] = d;
+    if (d > kBigRow) big[atomicAdd(nbig, 1u)] = (uint32_t)u;
+  }
+}
+
+struct RowCtx {
+  const uint64_t* off;
+  const uint32_t* nbrs;
+  const uint32_t* rank_of;
+  uint32_t n;
+  uint32_t* dplus;   // pass 0
+  const uint32_t* roff;  // pass 1: rank-space row offsets
+  uint32_t* col;
+  uint32_t* src;
+};
+
+// One warp over id-row u; returns (in lane-summed form) the entries v > u.
+template <int kPass>
+__device__ __forceinline__ uint32_t warp_csr_row(const RowCtx& cx, uint32_t u, int& bad) {
+  const unsigned lane = lane_id();
+  const uint64_t a = cx.off[u], b = cx.off[u + 1];
+  const uint32_t ru = cx.rank_of[u];
+  uint32_t run = kPass ? cx.roff[ru] : 0u, upper = 0;
+  constexpr int kU = 4;
+  for (uint64_t i0 = a; i0 < b; i0 += 32 * kU) {
+    uint32_t v[kU], rv[kU];
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const uint64_t i = i0 + 32 * t + lane;
+      v[t] = i < b ? cx.nbrs[i] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const bool valid = i0 + 32 * t + lane < b;
+      if (valid && v[t] >= cx.n) bad = 1;
+      rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
+      upper += (valid && v[t] > u && v[t] < cx.n) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const bool valid = i0 + 32 * t + lane < b && v[t] < cx.n;
+      const bool keep = valid && rv[t] > ru;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (kPass && keep) {
+        const uint32_t pos = run + __popc(m & lanemask_lt());
+        cx.col[pos] = rv[t];
+        cx.src[pos] = ru;
+      }
+      run += __popc(m);
+    }
+  }
+  if (!kPass && lane == 0) cx.dplus[ru] = run;
+  return upper;
+}
+
+// One thread over a short id-row u (<= kShortRow entries).
+template <int kPass>
+__device__ __forceinline__ uint32_t thread_csr_row(const RowCtx& cx, uint32_t u, uint64_t a, uint64_t b, int& bad) {
+  const uint32_t ru = cx.rank_of[u];
+  uint32_t run = kPass ? cx.roff[ru] : 0u, upper = 0;
+  for (uint64_t i0 = a; i0 < b; i0 += 4) {
+    uint32_t v[4], rv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = i0 + t < b ? cx.nbrs[i0 + t] : 0xffffffffu;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool valid = i0 + t < b;
+      if (valid && v[t] >= cx.n) bad = 1;
+      rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool valid = i0 + t < b && v[t] < cx.n;
+      upper += (valid && v[t] > u) ? 1u : 0u;
+      if (valid && rv[t] > ru) {
+        if (kPass) {
+          cx.col[run] = rv[t];
+          cx.src[run] = ru;
+        }
+        ++run;
+      }
+    }
+  }
+  if (!kPass) cx.dplus[ru] = run;
+  return upper;
+}
+
+constexpr uint32_t kShortRow = 24;
+
+template <int kPass>
+__global__ void __launch_bounds__(256) k_csr_rows(RowCtx cx, unsigned long long* __restrict__ upper_total,
+                                                 int* __restrict__ bad_flag) {
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  uint32_t upper = 0;
+  int bad = 0;
+  // short rows: a thread each; the warp's long rows (<= kBigRow) follow, one
+  // at a time, warp-wide
+  for (uint32_t u0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; u0 < cx.n; u0 += warps * 32) {
+    const uint32_t u = u0 + lane_id();
+    uint64_t a = 0, b = 0;
+    if (u < cx.n) {
+      a = cx.off[u];
+      b = cx.off[u + 1];
+    }
+    const bool is_short = u < cx.n && b - a <= kShortRow;
+    if (is_short) upper += thread_csr_row<kPass>(cx, u, a, b, bad);
+    uint32_t longs = __ballot_sync(0xffffffffu, u < cx.n && !is_short && b - a <= kBigRow);
+    while (longs) {
+      const int j = __ffs(longs) - 1;
+      longs &= longs - 1;
+      upper += warp_csr_row<kPass>(cx, u0 + j, bad);
+    }
+  }
+  if (!kPass) {
+    const unsigned long long w = warp_sum((unsigned long long)upper);
+    if (lane_id() == 0 && w) atomicAdd(upper_total, w);
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(bad_flag, 1);
+  }
+}
+
+// Rows longer than kBigRow (hubs) are cut into chunks of kBigRow entries,
+// chunk c = {u, first entry}; a warp per chunk.  Pass 0 adds each chunk's kept
+// count to d+(rank u) and records it; k_chunk_bases turns the counts into
+// per-chunk write bases within the row; pass 1 writes.
+struct Chunk {
+  uint32_t u, c0;  // row, first chunk of the row in the chunk list
+  uint64_t a;      // first entry of the chunk
+};
+
+template <int kPass>
+__global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __restrict__ chunks, uint32_t nchunks,
+                                                    uint32_t* __restrict__ ccount, const uint32_t* __restrict__ cbase,
+                                                    unsigned long long* __restrict__ upper_total,
+                                                    int* __restrict__ bad_flag) {
+  const unsigned lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  uint32_t upper = 0;
+  int bad = 0;
+  for (uint32_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < nchunks; c += warps) {
+    const Chunk ch = chunks[c];
+    const uint64_t rowend = cx.off[ch.u + 1];
+    const uint64_t a = ch.a, b = min(rowend, a + kBigRow);
+    const uint32_t ru = cx.rank_of[ch.u];
+    uint32_t run = kPass ? cx.roff[ru] + cbase[c] : 0u, kept = 0;
+    for (uint64_t i0 = a; i0 < b; i0 += 128) {
+      uint32_t v[4], rv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint64_t i = i0 + 32 * t + lane;
+        v[t] = i < b ? cx.nbrs[i] : 0xffffffffu;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool valid = i0 + 32 * t + lane < b;
+        if (valid && v[t] >= cx.n) bad = 1;
+        rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
+        upper += (valid && v[t] > ch.u && v[t] < cx.n) ? 1u : 0u;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool keep = i0 + 32 * t + lane < b && v[t] < cx.n && rv[t] > ru;
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (kPass && keep) {
+          const uint32_t pos = run + __popc(m & lanemask_lt());
+          cx.col[pos] = rv[t];
+          cx.src[pos] = ru;
+        }
+        run += __popc(m);
+        kept += __popc(m);
+      }
+    }
+    if (!kPass && lane == 0) {
+      ccount[c] = kept;
+      if (kept) atomicAdd(&cx.dplus[ru], kept);
+    }
+  }
+  if (!kPass) {
+    const unsigned long long w = warp_sum((unsigned long long)upper);
+    if (lane == 0 && w) atomicAdd(upper_total, w);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(bad_flag, 1);
+  }
+}
+
+__global__ void k_row_spans(const uint64_t* __restrict__ off, const uint32_t* __restrict__ rows, uint32_t nr,
+                            uint64_t* __restrict__ span) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+    span[2 * i] = off[rows[i]];
+    span[2 * i + 1] = off[rows[i] + 1];
+  }
+}
+
+// per big row (thread): exclusive prefix of its chunks' kept counts
+__global__ void k_chunk_bases(const Chunk* __restrict__ chunks, uint32_t nchunks, const uint32_t* __restrict__ ccount,
+                              uint32_t* __restrict__ cbase) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
+    if (chunks[c].c0 != c) continue;  // first chunk of its row
+    uint32_t run = 0;
+    for (uint32_t k = c; k < nchunks && chunks[k].u == chunks[c].u; ++k) {
+      cbase[k] = run;
+      run += ccount[k];
+    }
+  }
+}
+
+// Rank-space rows, 32 per warp: rows of <= 16 entries are sorted by their
+// lane (register bitonic network), rows of 17..32 by the warp (shuffle
+// bitonic), longer rows are listed for k_seg_sort_block.
+__device__ __forceinline__ void sort16(uint32_t (&x)[16]) {
+#pragma unroll
+  for (int k = 2; k <= 16; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool asc = (i & k) == 0;
+          const uint32_t a = x[i], b = x[l];
+          x[i] = asc ? min(a, b) : max(a, b);
+          x[l] = asc ? max(a, b) : min(a, b);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_seg_sort_warp(const uint32_t* __restrict__ off, uint32_t n,
+                                                       uint32_t* __restrict__ col, uint32_t* __restrict__ longrows,
+                                                       unsigned int* __restrict__ nlong) {
+  const unsigned lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t r0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r0 < n; r0 += warps * 32) {
+    const uint32_t r = r0 + lane;
+    uint32_t o = 0, d = 0;
+    if (r < n) {
+      o = off[r];
+      d = off[r + 1] - o;
+    }
+    if (d >= 2 && d <= 16) {
+      uint32_t x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? col[o + i] : 0xffffffffu;
+      sort16(x);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if ((uint32_t)i < d) col[o + i] = x[i];
+    }
+    if (d > 32) longrows[atomicAdd(nlong, 1u)] = r;
+    uint32_t mid = __ballot_sync(0xffffffffu, d > 16 && d <= 32);
+    while (mid) {
+      const int j = __ffs(mid) - 1;
+      mid &= mid - 1;
+      const uint32_t oj = __shfl_sync(0xffffffffu, o, j), dj = __shfl_sync(0xffffffffu, d, j);
+      uint32_t x = lane < dj ? col[oj + lane] : 0xffffffffu;
+#pragma unroll
+      for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x, jj);
+          const bool asc = (lane & k) == 0, lower = (lane & jj) == 0;
+          x = (lower == asc) ? min(x, y) : max(x, y);
+        }
+      }
+      if (lane < dj) col[oj + lane] = x;
+    }
+  }
+}
+
+// Listed rows of 33..256 entries: a warp each, kE = 2/4/8 entries per lane
+// in registers (position p = lane*kE + i), bitonic network over 32*kE: in-lane
+// stages for j < kE, shuffles for j >= kE.  Longer rows are re-listed for the
+// CTA sort.
+template <int kE>
+__device__ __forceinline__ void warp_sort_row(uint32_t* __restrict__ col, uint32_t o, uint32_t d) {
+  const unsigned lane = lane_id();
+  uint32_t x[kE];
+#pragma unroll
+  for (int i = 0; i < kE; ++i) {
+    const uint32_t p = lane * kE + i;
+    x[i] = p < d ? col[o + p] : 0xffffffffu;
+  }
+#pragma unroll
+  for (int k = 2; k <= 32 * kE; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= kE) {
+#pragma unroll
+        for (int i = 0; i < kE; ++i) {
+          const uint32_t p = lane * kE + i;
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], j / kE);
+          const bool asc = (p & k) == 0, lower = (p & j) == 0;
+          x[i] = (lower == asc) ? min(x[i], y) : max(x[i], y);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kE; ++i) {
+          const int l = i ^ j;
+          if (l > i) {
+            const uint32_t p = lane * kE + i;
+            const bool asc = (p & k) == 0;
+            const uint32_t a = x[i], b = x[l];
+            x[i] = asc ? min(a, b) : max(a, b);
+            x[l] = asc ? max(a, b) : min(a, b);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kE; ++i) {
+    const uint32_t p = lane * kE + i;
+    if (p < d) col[o + p] = x[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_seg_sort_mid(const uint32_t* __restrict__ off, uint32_t* __restrict__ col,
+                                                      const uint32_t* __restrict__ rows,
+                                                      const unsigned int* __restrict__ nrows,
+                                                      uint32_t* __restrict__ longrows,
+                                                      unsigned int* __restrict__ nlong) {
+  const uint32_t nr = *nrows;
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); idx < nr; idx += warps) {
+    const uint32_t r = rows[idx];
+    const uint32_t o = off[r], d = off[r + 1] - o;
+    if (d <= 64) warp_sort_row<2>(col, o, d);
+    else if (d <= 128) warp_sort_row<4>(col, o, d);
+    else if (d <= 256) warp_sort_row<8>(col, o, d);
+    else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
+  }
+}
+
+// Listed rows: one CTA each, SMEM bitonic sort over the next power of two.
+__global__ void __launch_bounds__(256) k_seg_sort_block(const uint32_t* __restrict__ off, uint32_t* __restrict__ col,
+                                                        const uint32_t* __restrict__ rows,
+                                                        const unsigned int* __restrict__ nrows) {
+  extern __shared__ uint32_t sk[];
+  const uint32_t nr = *nrows;
+  for (uint32_t idx = blockIdx.x; idx < nr; idx += gridDim.x) {
+    const uint32_t r = rows[idx];
+    const uint32_t o = off[r], d = off[r + 1] - o;
+    uint32_t P = 64;
+    while (P < d) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < d ? col[o + i] : 0xffffffffu;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
+          const uint32_t i = (t / j) * 2 * j + (t % j), l = i + j;
+          const uint32_t xi = sk[i], xl = sk[l];
+          if ((xi > xl) == ((i & k) == 0)) {
+            sk[i] = xl;
+            sk[l] = xi;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) col[o + i] = sk[i];
+    __syncthreads();
+  }
+}
+
+// fallback for rows longer than the SMEM sort: keys (src<<b | col), sort, split
+__global__ void k_pack_oriented(const uint32_t* __restrict__ src, const uint32_t* __restrict__ col, uint64_t E,
+                                int b, uint64_t* __restrict__ keys) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = ((uint64_t)src[i] << b) | col[i];
+}
+
+__global__ void k_unpack_col(const uint64_t* __restrict__ keys, uint64_t E, int b, uint32_t* __restrict__ col) {
+  const uint64_t mask = (b >= 32) ? 0xffffffffull : ((1ull << b) - 1);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    col[i] = (uint32_t)(keys[i] & mask);
+}
+
 struct DegLoad64 {
   const uint32_t* d;
   __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return d[i]; }
@@ -251,49 +612,103 @@ T read_scalar(const T* d, cudaStream_t s) {
   return h;
 }
 
-// Shared tail: sorted unique canonical id-space keys -> ranks -> oriented CSR.
-void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
+// Degree rank from id-space undirected degrees: stable sort of (deg<<32 | id)
+// on the degree bits -> id_of, rank_of, deg (by rank), max_deg.
+void rank_vertices(tc_graph& g, const uint32_t* deg) {
   cudaStream_t s = g.stream;
   const uint32_t n = g.n;
-  const int b = g.id_bits;
   const int dev = g.device;
-  if (E >= (1ull << 32)) fail(TC_ERANGE, "graph has >= 2^32 undirected edges (u32 oriented offsets)");
-  g.E = E;
-
-  DBuf<uint32_t> deg(n ? n : 1, s);
-  TC_CUDA(cudaMemsetAsync(deg.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
-  if (E) {
-    k_degree<<<grid_gs(E, dev), kT, 0, s>>>(ukeys.get(), E, b, deg.get());
-    TC_LAUNCH();
-  }
-  DBuf<uint32_t> scal(2, s);
-  TC_CUDA(cudaMemsetAsync(scal.get(), 0, 2 * sizeof(uint32_t), s));
+  DBuf<uint32_t> scal(1, s);
+  TC_CUDA(cudaMemsetAsync(scal.get(), 0, sizeof(uint32_t), s));
   if (n) {
-    k_max_u32<<<grid_gs(n, dev), kT, 0, s>>>(deg.get(), n, scal.get());
+    k_max_u32<<<grid_gs(n, dev), kT, 0, s>>>(deg, n, scal.get());
     TC_LAUNCH();
   }
   g.max_deg = read_scalar(scal.get(), s);
-
-  // degree rank: stable sort of (deg<<32 | id) on the degree bits
   g.id_of.alloc(n ? n : 1, s);
   g.rank_of.alloc(n ? n : 1, s);
   g.deg.alloc(n ? n : 1, s);
   if (n) {
     DBuf<uint64_t> rk(n, s), rk2(n, s);
-    k_rank_keys<<<grid_gs(n, dev), kT, 0, s>>>(deg.get(), n, rk.get());
+    k_rank_keys<<<grid_gs(n, dev), kT, 0, s>>>(deg, n, rk.get());
     TC_LAUNCH();
     const int db = bits_for(g.max_deg);
     uint64_t* sorted = radix_sort_u64(rk.get(), rk2.get(), n, 32, 32 + ((db + 7) / 8) * 8, s);
     k_rank_maps<<<grid_gs(n, dev), kT, 0, s>>>(sorted, n, g.id_of.get(), g.rank_of.get(), g.deg.get());
     TC_LAUNCH();
   }
-  deg.release();
+}
 
-  // orientation + oriented CSR
-  g.col.alloc(E + 8, s);
-  g.src.alloc(E ? E : 1, s);
-  g.off.alloc((uint64_t)n + 1, s);
-  TC_CUDA(cudaMemsetAsync(g.col.get(), 0xff, (E + 8) * sizeof(uint32_t), s));
+// out-degrees by rank -> row offsets (g.off) and max d+
+void row_offsets(tc_graph& g, const uint32_t* dplus) {
+  cudaStream_t s = g.stream;
+  const uint32_t n = g.n;
+  scan_exclusive<uint32_t>(LoadArray<uint32_t>{dplus}, g.off.get(), n, g.off.get() + n, s);
+  DBuf<uint32_t> scal(1, s);
+  TC_CUDA(cudaMemsetAsync(scal.get(), 0, sizeof(uint32_t), s));
+  if (n) {
+    k_max_u32<<<grid_gs(n, g.device), kT, 0, s>>>(dplus, n, scal.get());
+    TC_LAUNCH();
+  }
+  g.max_dplus = read_scalar(scal.get(), s);
+}
+
+// Shared tail: the hot-window mirror of the finished oriented CSR.
+void finish_rows(tc_graph& g) {
+  cudaStream_t s = g.stream;
+  const uint32_t n = g.n;
+  const uint64_t E = g.E;
+  const int dev = g.device;
+  // hot window mirror (graph.cuh): 16-bit copy of every row's members >= h0
+  const char* hb = getenv("TCB_HOT_BITS");  // tests: shrink the window to drive the cold path
+  uint32_t hot = hb ? (uint32_t)strtoul(hb, nullptr, 10) : kHotBits;
+  if (hot < 32) hot = 32;
+  if (hot > kHotBits) hot = kHotBits;
+  g.h0 = n > hot ? n - hot : 0;
+  DBuf<uint32_t> hp(E ? E : 1, s), th(1, s);
+  scan_exclusive<uint32_t>(HotFlag{g.col.get(), g.h0}, hp.get(), E, th.get(), s);
+  const uint32_t total_hot = E ? read_scalar(th.get(), s) : 0;
+  g.colH.alloc((uint64_t)total_hot + 16, s);
+  TC_CUDA(cudaMemsetAsync(g.colH.get(), 0, ((uint64_t)total_hot + 16) * sizeof(uint16_t), s));
+  g.offH.alloc((uint64_t)n + 1, s);
+  if (E) {
+    k_hot_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), E, g.h0, hp.get(), g.colH.get());
+    TC_LAUNCH();
+  }
+  k_hot_offsets<<<grid_gs((uint64_t)n + 1, dev), kT, 0, s>>>(g.off.get(), n, E, hp.get(), total_hot,
+                                                             g.offH.get());
+  TC_LAUNCH();
+}
+
+void alloc_rows(tc_graph& g) {
+  cudaStream_t s = g.stream;
+  g.col.alloc(g.E + 8, s);
+  g.src.alloc(g.E ? g.E : 1, s);
+  g.off.alloc((uint64_t)g.n + 1, s);
+  TC_CUDA(cudaMemsetAsync(g.col.get(), 0xff, (g.E + 8) * sizeof(uint32_t), s));
+}
+
+// Sorted unique canonical id-space keys (edge-list route) -> ranks ->
+// oriented CSR: orient each key by rank, radix sort, split.
+void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
+  cudaStream_t s = g.stream;
+  PhaseLog pl(s);
+  const uint32_t n = g.n;
+  const int b = g.id_bits;
+  const int dev = g.device;
+  if (E >= (1ull << 32)) fail(TC_ERANGE, "graph has >= 2^32 undirected edges (u32 oriented offsets)");
+  g.E = E;
+  {
+    DBuf<uint32_t> deg(n ? n : 1, s);
+    TC_CUDA(cudaMemsetAsync(deg.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
+    if (E) {
+      k_degree<<<grid_gs(E, dev), kT, 0, s>>>(ukeys.get(), E, b, deg.get());
+      TC_LAUNCH();
+    }
+    rank_vertices(g, deg.get());
+  }
+  pl.mark("fin_rank");
+  alloc_rows(g);
   DBuf<uint32_t> dplus(n ? n : 1, s);
   TC_CUDA(cudaMemsetAsync(dplus.get(), 0, sizeof(uint32_t) * (n ? n : 1), s));
   if (E) {
@@ -306,35 +721,10 @@ void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
     TC_LAUNCH();
   }
   ukeys.release();
-  scan_exclusive<uint32_t>(LoadArray<uint32_t>{dplus.get()}, g.off.get(), n, g.off.get() + n, s);
-  TC_CUDA(cudaMemsetAsync(scal.get(), 0, sizeof(uint32_t), s));
-  if (n) {
-    k_max_u32<<<grid_gs(n, dev), kT, 0, s>>>(dplus.get(), n, scal.get());
-    TC_LAUNCH();
-  }
-  g.max_dplus = read_scalar(scal.get(), s);
-
-  // hot window mirror (graph.cuh): 16-bit copy of every row's members >= h0
-  {
-    const char* hb = getenv("TCB_HOT_BITS");  // tests: shrink the window to drive the cold path
-    uint32_t hot = hb ? (uint32_t)strtoul(hb, nullptr, 10) : kHotBits;
-    if (hot < 32) hot = 32;
-    if (hot > kHotBits) hot = kHotBits;
-    g.h0 = n > hot ? n - hot : 0;
-    DBuf<uint32_t> hp(E ? E : 1, s), th(1, s);
-    scan_exclusive<uint32_t>(HotFlag{g.col.get(), g.h0}, hp.get(), E, th.get(), s);
-    const uint32_t total_hot = E ? read_scalar(th.get(), s) : 0;
-    g.colH.alloc((uint64_t)total_hot + 16, s);
-    TC_CUDA(cudaMemsetAsync(g.colH.get(), 0, ((uint64_t)total_hot + 16) * sizeof(uint16_t), s));
-    g.offH.alloc((uint64_t)n + 1, s);
-    if (E) {
-      k_hot_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), E, g.h0, hp.get(), g.colH.get());
-      TC_LAUNCH();
-    }
-    k_hot_offsets<<<grid_gs((uint64_t)n + 1, dev), kT, 0, s>>>(g.off.get(), n, E, hp.get(), total_hot,
-                                                               g.offH.get());
-    TC_LAUNCH();
-  }
+  pl.mark("fin_orient_sort");
+  row_offsets(g, dplus.get());
+  finish_rows(g);
+  pl.mark("fin_rows");
 }
 
 }  // namespace
@@ -386,31 +776,117 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   const int dev = g.device;
   g.n = n;
   g.id_bits = n > 1 ? bits_for((uint64_t)n - 1) : 1;
-  const int b = g.id_bits;
   const uint64_t total = 2 * num_edges;
   if (total >= (1ull << 32)) fail(TC_ERANGE, "CSR with >= 2^32 directed entries");
-  DBuf<uint32_t> ends(total ? total : 1, s), row_excl(total ? total : 1, s), pos(total ? total : 1, s);
-  DBuf<uint32_t> ecount(1, s);
-  uint64_t E = 0;
-  if (total) {
-    TC_CUDA(cudaMemsetAsync(ends.get(), 0, total * sizeof(uint32_t), s));
-    k_row_ends<<<grid_gs(n, dev), kT, 0, s>>>(d_off, n, ends.get());
-    TC_LAUNCH();
-    scan_exclusive<uint32_t>(LoadArray<uint32_t>{ends.get()}, row_excl.get(), total, (uint32_t*)nullptr, s);
-    scan_exclusive<uint32_t>(UpperFlag{d_nbrs, row_excl.get(), ends.get()}, pos.get(), total, ecount.get(), s);
-    E = read_scalar(ecount.get(), s);
-    if (E != num_edges) fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
-  }
-  DBuf<uint64_t> ukeys(E ? E : 1, s);
-  if (total) {
-    k_csr_keys<<<grid_gs(total, dev), kT, 0, s>>>(d_nbrs, total, row_excl.get(), ends.get(), pos.get(), b,
-                                                  ukeys.get());
+  if (num_edges >= (1ull << 32)) fail(TC_ERANGE, "graph has >= 2^32 undirected edges (u32 oriented offsets)");
+  PhaseLog pl(s);
+  const uint32_t nn = n ? n : 1;
+  DBuf<uint32_t> deg(nn, s), big(total / kBigRow + 1, s);
+  DBuf<unsigned int> cnts(2, s);  // big rows, long rank-space rows
+  DBuf<int> bad(1, s);
+  DBuf<unsigned long long> upper(1, s);
+  TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
+  TC_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  TC_CUDA(cudaMemsetAsync(upper.get(), 0, sizeof(unsigned long long), s));
+  if (n) {
+    k_csr_deg<<<grid_gs(n, dev), kT, 0, s>>>(d_off, n, deg.get(), big.get(), cnts.get(), bad.get());
     TC_LAUNCH();
   }
-  ends.release();
-  row_excl.release();
-  pos.release();
-  finalize(g, ukeys, E);
+  const uint64_t off_n = n ? read_scalar(d_off + n, s) : 0;
+  if (read_scalar(bad.get(), s) || off_n != total || (n && read_scalar(d_off, s) != 0))
+    fail(TC_EINVAL, "Graph: inconsistent CSR arrays");
+  // hub rows -> chunk list (host: a few thousand rows)
+  std::vector<Chunk> hchunks;
+  {
+    const uint32_t nbig = read_scalar(cnts.get(), s);
+    std::vector<uint32_t> hb(nbig);
+    std::vector<uint64_t> ho(2 * (size_t)nbig);
+    if (nbig) {
+      TC_CUDA(cudaMemcpyAsync(hb.data(), big.get(), nbig * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      TC_CUDA(cudaStreamSynchronize(s));
+      std::sort(hb.begin(), hb.end());
+      DBuf<uint32_t> db(nbig, s);
+      DBuf<uint64_t> dspan(2 * (uint64_t)nbig, s);
+      TC_CUDA(cudaMemcpyAsync(db.get(), hb.data(), nbig * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      k_row_spans<<<ceil_div(nbig, 256), 256, 0, s>>>(d_off, db.get(), nbig, dspan.get());
+      TC_LAUNCH();
+      TC_CUDA(cudaMemcpyAsync(ho.data(), dspan.get(), 2 * (size_t)nbig * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      TC_CUDA(cudaStreamSynchronize(s));
+      for (uint32_t i = 0; i < nbig; ++i) {
+        const uint32_t c0 = (uint32_t)hchunks.size();
+        for (uint64_t a = ho[2 * i]; a < ho[2 * i + 1]; a += kBigRow) hchunks.push_back(Chunk{hb[i], c0, a});
+      }
+    }
+  }
+  const uint32_t nch = (uint32_t)hchunks.size();
+  DBuf<Chunk> chunks(nch ? nch : 1, s);
+  DBuf<uint32_t> ccount(nch ? nch : 1, s), cbase(nch ? nch : 1, s);
+  if (nch) TC_CUDA(cudaMemcpyAsync(chunks.get(), hchunks.data(), nch * sizeof(Chunk), cudaMemcpyHostToDevice, s));
+  rank_vertices(g, deg.get());
+  deg.release();
+  pl.mark("csr_rank");
+  DBuf<uint32_t> dplus(nn, s);
+  TC_CUDA(cudaMemsetAsync(dplus.get(), 0, sizeof(uint32_t) * nn, s));
+  RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), nullptr, nullptr, nullptr};
+  const unsigned gw = (unsigned)num_sms(dev) * 8;
+  if (total) {
+    k_csr_rows<0><<<gw, 256, 0, s>>>(cx, upper.get(), bad.get());
+    TC_LAUNCH();
+    if (nch) {
+      k_csr_chunks<0><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, ccount.get(), cbase.get(), upper.get(), bad.get());
+      TC_LAUNCH();
+      k_chunk_bases<<<ceil_div(nch, 256), 256, 0, s>>>(chunks.get(), nch, ccount.get(), cbase.get());
+      TC_LAUNCH();
+    }
+  }
+  const uint64_t E = read_scalar(upper.get(), s);
+  if (read_scalar(bad.get(), s)) fail(TC_EINVAL, "Graph: neighbor id out of range");
+  if (E != num_edges) fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
+  g.E = E;
+  alloc_rows(g);
+  row_offsets(g, dplus.get());
+  if (n && read_scalar(g.off.get() + n, s) != E)
+    fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
+  pl.mark("csr_count");
+  if (E) {
+    cx.roff = g.off.get();
+    cx.col = g.col.get();
+    cx.src = g.src.get();
+    k_csr_rows<1><<<gw, 256, 0, s>>>(cx, upper.get(), bad.get());
+    TC_LAUNCH();
+    if (nch) {
+      k_csr_chunks<1><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, ccount.get(), cbase.get(), upper.get(), bad.get());
+      TC_LAUNCH();
+    }
+    pl.mark("csr_scatter");
+    // sort every rank-space row
+    uint32_t P = 64;
+    while (P < g.max_dplus) P <<= 1;
+    if (P <= 16384) {
+      DBuf<uint32_t> midrows(nn, s), longrows(nn, s);
+      TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
+      k_seg_sort_warp<<<gw, 256, 0, s>>>(g.off.get(), n, g.col.get(), midrows.get(), cnts.get());
+      TC_LAUNCH();
+      k_seg_sort_mid<<<gw, 256, 0, s>>>(g.off.get(), g.col.get(), midrows.get(), cnts.get(), longrows.get(),
+                                        cnts.get() + 1);
+      TC_LAUNCH();
+      pl.mark("csr_sort_short");
+      const size_t smem = (size_t)P * sizeof(uint32_t);
+      TC_CUDA(cudaFuncSetAttribute(k_seg_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_seg_sort_block<<<gw, 256, smem, s>>>(g.off.get(), g.col.get(), longrows.get(), cnts.get() + 1);
+      TC_LAUNCH();
+    } else {
+      DBuf<uint64_t> k1(E, s), k2(E, s);
+      k_pack_oriented<<<grid_gs(E, dev), kT, 0, s>>>(g.src.get(), g.col.get(), E, g.id_bits, k1.get());
+      TC_LAUNCH();
+      uint64_t* sorted = radix_sort_u64(k1.get(), k2.get(), E, 0, 2 * g.id_bits, s);
+      k_unpack_col<<<grid_gs(E, dev), kT, 0, s>>>(sorted, E, g.id_bits, g.col.get());
+      TC_LAUNCH();
+    }
+    pl.mark("csr_row_sort");
+  }
+  finish_rows(g);
+  pl.mark("csr_hot_mirror");
 }
 
 void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs) {

@@ -228,8 +228,10 @@ tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbo
   g = new_handle(device);
   try {
     Timer t(g->stream);
+    tcb::PhaseLog pl(g->stream);
     DevIn<uint64_t> off(row_offsets, (uint64_t)n + 1, g->stream);
     DevIn<uint32_t> nb(neighbors, 2 * num_edges, g->stream);
+    pl.mark("csr_h2d");
     tcb::build_from_csr(*g, off.p, nb.p, n, num_edges);
     g->build_ms = t.stop();
   } catch (...) {

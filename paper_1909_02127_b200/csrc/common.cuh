@@ -29,8 +29,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define TC_CUDA(x) ::tcb::cuda_check((x), #x, __FILE__, __LINE__)
 #define TC_LAUNCH() ::tcb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
-// Stream-ordered device buffer (cudaMallocAsync from the device's default
-// mempool, whose release threshold we raise so repeated calls reuse memory).
+// Caching device allocator (alloc.cu): freed blocks are kept per device and
+// size class and handed back to the next request of the same class; a block
+// reused on another stream first waits on the event recorded at its free.
+// Repeated calls (a count per step, a graph per e2e step) therefore never
+// remap device memory.
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
+
+// Stream-ordered device buffer on the caching allocator.
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -53,10 +60,10 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count) TC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T) + 64, st));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T) + 64, st));
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) dev_free(p, n * sizeof(T) + 64, s);
     p = nullptr;
     n = 0;
   }
