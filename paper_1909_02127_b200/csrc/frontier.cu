@@ -128,9 +128,15 @@ struct RowBytes {
 // Edge order, kR edges per thread in flight: geometry (row data read
 // coalesced), then the slot claims (atomic cursors), then the scattered item
 // stores.
-constexpr int kScatterR = 4;
+#ifndef TCB_SCATTER_R
+#define TCB_SCATTER_R 4
+#endif
+#ifndef TCB_SCATTER_MINB
+#define TCB_SCATTER_MINB 1
+#endif
+constexpr int kScatterR = TCB_SCATTER_R;
 template <bool kPV>
-__global__ void __launch_bounds__(kT) k_fr_scatter(ItemGeom geo, uint64_t e0, uint64_t e1,
+__global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom geo, uint64_t e0, uint64_t e1,
                                                   const uint32_t* __restrict__ in, uint32_t* __restrict__ cursor,
                                                   uint4* __restrict__ items,
                                                   const uint64_t* __restrict__ rowbase, uint32_t u_lo,
