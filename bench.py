@@ -412,7 +412,7 @@ def main():
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_kind": peak_kind,
-            "kernel": "k_join_cta + k_join_warp (advance + fused SMEM-hash join)",
+            "kernel": "join phase: k_join_warp + k_join_cta (advance + fused SMEM join) + k_pv_rows(_heavy) (per-vertex fold)",
             "alg_bytes_per_step": alg_bytes, "join_ms": join_ms,
             "model": "B_alg = 4W + 12|E+| + 8(|V|+1) + 8|V| (SURVEY 8d wedge-stream bytes)",
             "pivot_model_bytes": pivot_bytes,

@@ -427,7 +427,8 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
   __shared__ uint32_t s_cb[kCtaSegItems], s_ce[kCtaSegItems], s_cpre[kCtaSegItems + 1];
   __shared__ uint16_t s_hidx[kCtaSegItems], s_cidx[kCtaSegItems];
   __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
-  __shared__ uint32_t s_seg, s_hits, s_cold, s_nl;
+  __shared__ uint32_t s_hits, s_cold, s_nl;
+  __shared__ uint32_t s_desc[6];  // current segment: v, i0, ni, off[v], d+(v), queue index
   __shared__ unsigned long long s_ctot;
   uint32_t* bm = dyn;
   uint32_t* stab = dyn + nbm;
@@ -441,18 +442,32 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
   // cold hits (x < h0) go straight to global atomics; hot hits leave as masks
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
+  // segment descriptors are prefetched one segment ahead by thread 0 (queue
+  // grab at the top of a segment, descriptor + pivot row after the staging),
+  // so a segment starts on SMEM values instead of a chain of global latencies
+  auto fetch = [&](uint32_t q) {
+    if (q < nsegs) {
+      const uint4 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
+      s_desc[0] = sg.x;
+      s_desc[1] = sg.y;
+      s_desc[2] = sg.z - sg.y;
+      s_desc[3] = off[sg.x];
+      s_desc[4] = off[sg.x + 1] - s_desc[3];
+    }
+    s_desc[5] = q;
+  };
+  if (threadIdx.x == 0) fetch(atomicAdd(queue, 1u));
   while (true) {
     if (threadIdx.x == 0) {
-      s_seg = atomicAdd(queue, 1u);
       s_hits = 0;
       s_cold = 0;
     }
     __syncthreads();
-    const uint32_t q = s_seg;
-    if (q >= nsegs) break;
-    const uint4 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
-    const uint32_t v = sg.x, i0 = sg.y, ni = sg.z - sg.y;
-    const uint32_t nb = off[v], dv = off[v + 1] - nb;
+    if (s_desc[5] >= nsegs) break;
+    const uint32_t v = s_desc[0], i0 = s_desc[1], ni = s_desc[2];
+    const uint32_t nb = s_desc[3], dv = s_desc[4];
+    uint32_t qnext = 0;
+    if (threadIdx.x == 0) qnext = atomicAdd(queue, 1u);
     // (1a) hot members -> bitmap; s_cold = #members below h0 (sorted prefix)
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
       const uint32_t x = col[nb + j];
@@ -579,7 +594,8 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
       if (threadIdx.x == 0 && s_hits) atomicAdd(&t_rank[v], (unsigned long long)s_hits);
     }
     if (ts && tab == gtab) __threadfence_block();
-    __syncthreads();
+    __syncthreads();  // everyone is done with s_desc of this segment
+    if (threadIdx.x == 0) fetch(qnext);
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
@@ -605,7 +621,8 @@ __global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCt
 //   k_pv_rows_heavy  one CTA per listed row, its 8 warps splitting each
 //                    group's items, partial counters reduced in SMEM
 constexpr int kRowWarps = 8;
-constexpr int kRowU = 8;
+constexpr int kRowULight = 8;   // light rows: a warp each, many warps per SM
+constexpr int kRowUHeavy = 16;  // heavy rows: latency-bound on the byte loads (A/B: profiles/README.md)
 constexpr uint32_t kRowHeavy = 128;
 
 struct RowLanes {
@@ -657,7 +674,9 @@ __device__ __forceinline__ void init_spread(uint2* s_spread) {
     s_spread[b] = make_uint2(((b & 0xfu) * 0x00204081u) & 0x01010101u, ((b >> 4) * 0x00204081u) & 0x01010101u);
 }
 
-// cnt[j] += bit j of byte (k, cr) over items k = ka + sub + G*i in [ka, kb).
+// cnt[j] += bit j of byte (k, cr) over items k = ka + sub + G*i in [ka, kb);
+// kRowU mask-byte loads in flight per lane.
+template <int kRowU>
 __device__ __forceinline__ void row_accumulate(const RowRel& rr, const uint8_t* __restrict__ rowm, uint32_t cr,
                                                bool cvalid, const RowLanes& rl, uint32_t ka, uint32_t kb,
                                                const uint2* s_spread, uint32_t (&cnt)[8]) {
@@ -797,7 +816,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
         const uint32_t cr = g + (lane & (rl.w - 1));
         const bool cvalid = cr < rr.C;
         uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        row_accumulate(rr, rowm, cr, cvalid, rl, 0, rr.reaching(g, rl.w), s_spread, cnt);
+        row_accumulate<kRowULight>(rr, rowm, cr, cvalid, rl, 0, rr.reaching(g, rl.w), s_spread, cnt);
         if (rl.G > 1) {  // sum the sub-groups: counts < 2^16 here, two per word
           uint32_t pk[4];
 #pragma unroll
@@ -862,7 +881,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
       const uint32_t per = (K + kRowWarps - 1) / kRowWarps;
       const uint32_t ka = min(K, warp * per), kb = min(K, ka + per);
       uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      row_accumulate(rr, rowm, cr, cvalid, rl, ka, kb, s_spread, cnt);
+      row_accumulate<kRowUHeavy>(rr, rowm, cr, cvalid, rl, ka, kb, s_spread, cnt);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         for (uint32_t o = rl.w; o < 32; o <<= 1) cnt[j] += __shfl_xor_sync(0xffffffffu, cnt[j], o);
