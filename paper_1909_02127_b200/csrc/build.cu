@@ -200,7 +200,7 @@ __global__ void k_hot_offsets(const uint32_t* __restrict__ off, uint32_t n, uint
 // kept by the orientation, rank(v) > rank(u), into d+(rank u); pass 1 writes
 // them at off[rank u] + their rank among the row's kept entries (ballot
 // prefix, deterministic); then every rank-space row is sorted in place.
-constexpr uint32_t kBigRow = 4096;
+constexpr uint32_t kBigRow = 1024;
 
 __global__ void k_csr_deg(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ deg,
                           uint32_t* __restrict__ big, unsigned int* __restrict__ nbig, int* __restrict__ bad) {
@@ -303,14 +303,19 @@ __device__ __forceinline__ uint32_t thread_csr_row(const RowCtx& cx, uint32_t u,
 constexpr uint32_t kShortRow = 24;
 
 template <int kPass>
-__global__ void __launch_bounds__(256) k_csr_rows(RowCtx cx, unsigned long long* __restrict__ upper_total,
+__global__ void __launch_bounds__(256) k_csr_rows(RowCtx cx, unsigned int* __restrict__ queue,
+                                                 unsigned long long* __restrict__ upper_total,
                                                  int* __restrict__ bad_flag) {
-  const uint32_t warps = gridDim.x * (blockDim.x / 32);
   uint32_t upper = 0;
   int bad = 0;
-  // short rows: a thread each; the warp's long rows (<= kBigRow) follow, one
-  // at a time, warp-wide
-  for (uint32_t u0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; u0 < cx.n; u0 += warps * 32) {
+  // groups of 32 rows from a queue (row lengths are skewed): short rows a
+  // thread each; the group's long rows (<= kBigRow) follow, one at a time,
+  // warp-wide
+  while (true) {
+    uint32_t u0 = 0;
+    if (lane_id() == 0) u0 = atomicAdd(queue, 32u);
+    u0 = __shfl_sync(0xffffffffu, u0, 0);
+    if (u0 >= cx.n) break;
     const uint32_t u = u0 + lane_id();
     uint64_t a = 0, b = 0;
     if (u < cx.n) {
@@ -396,12 +401,27 @@ __global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __re
   }
 }
 
-__global__ void k_row_spans(const uint64_t* __restrict__ off, const uint32_t* __restrict__ rows, uint32_t nr,
-                            uint64_t* __restrict__ span) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
-    span[2 * i] = off[rows[i]];
-    span[2 * i + 1] = off[rows[i] + 1];
+struct ChunkCount {
+  const uint32_t* big;
+  const uint64_t* off;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+    const uint32_t u = big[i];
+    return (uint32_t)((off[u + 1] - off[u] + kBigRow - 1) / kBigRow);
   }
+};
+
+__global__ void k_chunk_fill(const uint32_t* __restrict__ big, uint32_t nbig, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ choff, Chunk* __restrict__ chunks) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nbig; i += gridDim.x * blockDim.x) {
+    const uint32_t u = big[i], c0 = choff[i];
+    const uint64_t a = off[u], b = off[u + 1];
+    uint32_t c = c0;
+    for (uint64_t x = a; x < b; x += kBigRow) chunks[c++] = Chunk{u, c0, x};
+  }
+}
+
+void kl_scan_chunks(const uint32_t* big, uint32_t nbig, const uint64_t* off, uint32_t* choff, cudaStream_t s) {
+  scan_exclusive<uint32_t>(ChunkCount{big, off}, choff, nbig, choff + nbig, s);
 }
 
 // per big row (thread): exclusive prefix of its chunks' kept counts
@@ -481,7 +501,7 @@ __global__ void __launch_bounds__(256) k_seg_sort_warp(const uint32_t* __restric
   }
 }
 
-// Listed rows of 33..256 entries: a warp each, kE = 2/4/8 entries per lane
+// Listed rows of 33..1024 entries: a warp each, kE = 2..32 entries per lane
 // in registers (position p = lane*kE + i), bitonic network over 32*kE: in-lane
 // stages for j < kE, shuffles for j >= kE.  Longer rows are re-listed for the
 // CTA sort.
@@ -541,6 +561,24 @@ __global__ void __launch_bounds__(256) k_seg_sort_mid(const uint32_t* __restrict
     if (d <= 64) warp_sort_row<2>(col, o, d);
     else if (d <= 128) warp_sort_row<4>(col, o, d);
     else if (d <= 256) warp_sort_row<8>(col, o, d);
+    else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
+  }
+}
+
+// Rows of 257..1024 entries (16/32 per lane, its own kernel for the register
+// budget); longer rows are re-listed for the CTA sort.
+__global__ void __launch_bounds__(128) k_seg_sort_mid2(const uint32_t* __restrict__ off, uint32_t* __restrict__ col,
+                                                       const uint32_t* __restrict__ rows,
+                                                       const unsigned int* __restrict__ nrows,
+                                                       uint32_t* __restrict__ longrows,
+                                                       unsigned int* __restrict__ nlong) {
+  const uint32_t nr = *nrows;
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); idx < nr; idx += warps) {
+    const uint32_t r = rows[idx];
+    const uint32_t o = off[r], d = off[r + 1] - o;
+    if (d <= 512) warp_sort_row<16>(col, o, d);
+    else if (d <= 1024) warp_sort_row<32>(col, o, d);
     else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
   }
 }
@@ -782,10 +820,10 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   PhaseLog pl(s);
   const uint32_t nn = n ? n : 1;
   DBuf<uint32_t> deg(nn, s), big(total / kBigRow + 1, s);
-  DBuf<unsigned int> cnts(2, s);  // big rows, long rank-space rows
+  DBuf<unsigned int> cnts(4, s);  // big rows, long rank-space rows, row queues (pass 0, 1)
   DBuf<int> bad(1, s);
   DBuf<unsigned long long> upper(1, s);
-  TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
+  TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 4 * sizeof(unsigned int), s));
   TC_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
   TC_CUDA(cudaMemsetAsync(upper.get(), 0, sizeof(unsigned long long), s));
   if (n) {
@@ -795,33 +833,20 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   const uint64_t off_n = n ? read_scalar(d_off + n, s) : 0;
   if (read_scalar(bad.get(), s) || off_n != total || (n && read_scalar(d_off, s) != 0))
     fail(TC_EINVAL, "Graph: inconsistent CSR arrays");
-  // hub rows -> chunk list (host: a few thousand rows)
-  std::vector<Chunk> hchunks;
-  {
-    const uint32_t nbig = read_scalar(cnts.get(), s);
-    std::vector<uint32_t> hb(nbig);
-    std::vector<uint64_t> ho(2 * (size_t)nbig);
-    if (nbig) {
-      TC_CUDA(cudaMemcpyAsync(hb.data(), big.get(), nbig * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-      TC_CUDA(cudaStreamSynchronize(s));
-      std::sort(hb.begin(), hb.end());
-      DBuf<uint32_t> db(nbig, s);
-      DBuf<uint64_t> dspan(2 * (uint64_t)nbig, s);
-      TC_CUDA(cudaMemcpyAsync(db.get(), hb.data(), nbig * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-      k_row_spans<<<ceil_div(nbig, 256), 256, 0, s>>>(d_off, db.get(), nbig, dspan.get());
-      TC_LAUNCH();
-      TC_CUDA(cudaMemcpyAsync(ho.data(), dspan.get(), 2 * (size_t)nbig * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-      TC_CUDA(cudaStreamSynchronize(s));
-      for (uint32_t i = 0; i < nbig; ++i) {
-        const uint32_t c0 = (uint32_t)hchunks.size();
-        for (uint64_t a = ho[2 * i]; a < ho[2 * i + 1]; a += kBigRow) hchunks.push_back(Chunk{hb[i], c0, a});
-      }
-    }
+  // hub rows -> chunk list (device: chunk counts, scan, fill)
+  const uint32_t nbig = read_scalar(cnts.get(), s);
+  DBuf<uint32_t> choff((uint64_t)nbig + 1, s);
+  uint32_t nch = 0;
+  if (nbig) {
+    kl_scan_chunks(big.get(), nbig, d_off, choff.get(), s);
+    nch = read_scalar(choff.get() + nbig, s);
   }
-  const uint32_t nch = (uint32_t)hchunks.size();
   DBuf<Chunk> chunks(nch ? nch : 1, s);
   DBuf<uint32_t> ccount(nch ? nch : 1, s), cbase(nch ? nch : 1, s);
-  if (nch) TC_CUDA(cudaMemcpyAsync(chunks.get(), hchunks.data(), nch * sizeof(Chunk), cudaMemcpyHostToDevice, s));
+  if (nch) {
+    k_chunk_fill<<<ceil_div(nbig, 256), 256, 0, s>>>(big.get(), nbig, d_off, choff.get(), chunks.get());
+    TC_LAUNCH();
+  }
   rank_vertices(g, deg.get());
   deg.release();
   pl.mark("csr_rank");
@@ -830,7 +855,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), nullptr, nullptr, nullptr};
   const unsigned gw = (unsigned)num_sms(dev) * 8;
   if (total) {
-    k_csr_rows<0><<<gw, 256, 0, s>>>(cx, upper.get(), bad.get());
+    k_csr_rows<0><<<gw, 256, 0, s>>>(cx, cnts.get() + 2, upper.get(), bad.get());
     TC_LAUNCH();
     if (nch) {
       k_csr_chunks<0><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, ccount.get(), cbase.get(), upper.get(), bad.get());
@@ -852,7 +877,8 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     cx.roff = g.off.get();
     cx.col = g.col.get();
     cx.src = g.src.get();
-    k_csr_rows<1><<<gw, 256, 0, s>>>(cx, upper.get(), bad.get());
+    TC_CUDA(cudaMemsetAsync(cnts.get() + 3, 0, sizeof(unsigned int), s));
+    k_csr_rows<1><<<gw, 256, 0, s>>>(cx, cnts.get() + 3, upper.get(), bad.get());
     TC_LAUNCH();
     if (nch) {
       k_csr_chunks<1><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, ccount.get(), cbase.get(), upper.get(), bad.get());
@@ -870,6 +896,13 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
       k_seg_sort_mid<<<gw, 256, 0, s>>>(g.off.get(), g.col.get(), midrows.get(), cnts.get(), longrows.get(),
                                         cnts.get() + 1);
       TC_LAUNCH();
+      // rows of 257..1024: re-listed from longrows into midrows
+      TC_CUDA(cudaMemsetAsync(cnts.get(), 0, sizeof(unsigned int), s));
+      k_seg_sort_mid2<<<gw * 2, 128, 0, s>>>(g.off.get(), g.col.get(), longrows.get(), cnts.get() + 1,
+                                             midrows.get(), cnts.get());
+      TC_LAUNCH();
+      std::swap(midrows, longrows);  // rows > 1024 are now in longrows, count in cnts[0]
+      TC_CUDA(cudaMemcpyAsync(cnts.get() + 1, cnts.get(), sizeof(unsigned int), cudaMemcpyDeviceToDevice, s));
       pl.mark("csr_sort_short");
       const size_t smem = (size_t)P * sizeof(uint32_t);
       TC_CUDA(cudaFuncSetAttribute(k_seg_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
