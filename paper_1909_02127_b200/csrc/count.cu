@@ -48,7 +48,7 @@ constexpr uint32_t kCtaSmemSlots = 1024;     // cold-member hash table in SMEM (
 #define TCB_HOT_WIN 2
 #endif
 #ifndef TCB_MIN_BLOCKS
-#define TCB_MIN_BLOCKS 5  // per-vertex build; the total-only build targets one more (A/B: profiles/README.md)
+#define TCB_MIN_BLOCKS 6  // CTA-bin residency target, both variants (A/B: profiles/README.md)
 #endif
 constexpr int kHotWin = TCB_HOT_WIN;              // hot chunk loads in flight per lane
 constexpr int kCtaMinBlocks = TCB_MIN_BLOCKS;     // CTA-bin kernel residency target
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 // Segments come from a global queue, heaviest (top-rank pivots) first.
 // Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots].
 template <bool kPerVertex>
-__global__ void __launch_bounds__(kJoinThreads, kPerVertex ? kCtaMinBlocks : kCtaMinBlocks + 1) k_join_cta(
+__global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
     const uint16_t* __restrict__ colH, const uint4* __restrict__ items,
     const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t h0, uint32_t nbm,
