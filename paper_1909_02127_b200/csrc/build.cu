@@ -888,7 +888,9 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     // sort every rank-space row
     uint32_t P = 64;
     while (P < g.max_dplus) P <<= 1;
-    if (P <= 16384) {
+    const char* sm = getenv("TCB_ROWSORT_MAX");  // tests: force the radix fallback on small graphs
+    const uint32_t sort_max = sm ? (uint32_t)strtoul(sm, nullptr, 10) : 16384u;
+    if (P <= sort_max) {
       DBuf<uint32_t> midrows(nn, s), longrows(nn, s);
       TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
       k_seg_sort_warp<<<gw, 256, 0, s>>>(g.off.get(), n, g.col.get(), midrows.get(), cnts.get());

@@ -291,3 +291,58 @@ def test_c4_rmat_s24(tc, oracle, cuda_ok):
     assert r.count == c["T"] == 10282799137
     assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
     assert int(r.per_vertex.sum()) == 3 * c["T"]
+
+
+# ---- the Graph-ctor (CSR) route: per-row orientation, hub chunks, row sorts ----
+
+def _clique_pairs(k, base=0):
+    iu, ju = np.triu_indices(k, 1)
+    return np.stack([iu + base, ju + base], 1).astype(np.uint32)
+
+
+@pytest.mark.parametrize("rowsort", ["default", "radix_fallback"])
+def test_csr_route_paths(tc, oracle, cuda_ok, rowsort):
+    """Hub rows longer than one 1024-entry chunk, rank-space rows in every
+    sort class (<=16 lane network, 17..32 warp, 33..256, 257..1024, >1024
+    CTA), and the radix fallback; counts, per-vertex counts and the exported
+    CSR must match the edge-list route and the oracle."""
+    old = os.environ.get("TCB_ROWSORT_MAX")
+    if rowsort == "radix_fallback":
+        os.environ["TCB_ROWSORT_MAX"] = "32"
+    try:
+        rng = np.random.default_rng(11)
+        parts = [_clique_pairs(1300), _clique_pairs(300, 1300), _clique_pairs(60, 1600), _clique_pairs(24, 1660)]
+        n = 9000
+        hub = np.stack([np.full(n - 1700, 1690, np.uint32), np.arange(1700, n, dtype=np.uint32)], 1)
+        fringe = np.stack([rng.integers(1700, n, 30000), rng.integers(0, 1700, 30000)], 1).astype(np.uint32)
+        pairs = np.concatenate(parts + [hub, fringe]).reshape(-1)
+        off, nb, E, _, _ = oracle.build_graph(pairs, n)
+        T, pv = oracle.count(off, nb, per_vertex=True)
+        g = tc.graph_from_csr(off, nb)
+        assert g.num_edges() == E and g.max_out_degree >= 1100
+        r = _count(tc, g)
+        assert r.count == T and np.array_equal(r.per_vertex, pv)
+        ro, nbr = g.export_csr()
+        assert np.array_equal(ro, off) and np.array_equal(nbr, nb)
+        assert np.array_equal(tc.degrees(g), np.diff(off).astype(np.uint32))
+    finally:
+        if old is None:
+            os.environ.pop("TCB_ROWSORT_MAX", None)
+        else:
+            os.environ["TCB_ROWSORT_MAX"] = old
+
+
+def test_csr_route_errors(tc, cuda_ok):
+    """Graph ctor validation (graph.cpp:9-21): inconsistent arrays and ids out
+    of range raise std::invalid_argument (InvalidArgument)."""
+    off = np.array([0, 2, 4, 6], np.uint64)
+    nb = np.array([1, 2, 0, 2, 0, 1], np.uint32)
+    assert tc.count_triangles(tc.graph_from_csr(off, nb)).count == 1
+    with pytest.raises(tc.InvalidArgument):  # asymmetric: 0->1 without 1->0
+        tc.graph_from_csr(np.array([0, 2, 3, 5], np.uint64), np.array([1, 2, 2, 0, 1], np.uint32), 3, 3)
+    with pytest.raises(tc.InvalidArgument):  # neighbour id out of range
+        tc.graph_from_csr(off, np.array([1, 7, 0, 2, 0, 1], np.uint32))
+    with pytest.raises(tc.InvalidArgument):  # decreasing offsets
+        tc.graph_from_csr(np.array([0, 4, 2, 6], np.uint64), nb)
+    with pytest.raises(tc.InvalidArgument):  # offsets[n] != 2|E|
+        tc.graph_from_csr(np.array([0, 2, 4, 5], np.uint64), nb, 3, 3)
