@@ -767,7 +767,7 @@ __device__ __forceinline__ void flush_top_rows(const uint32_t* top, uint32_t ncn
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
     const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t u_hi,
-    uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, uint32_t* __restrict__ heavy,
+    uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,
     unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
   __shared__ uint2 s_spread[256];
@@ -778,10 +778,11 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
   const uint32_t nrows = u_hi - u_lo + 1;
   const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
   while (true) {
-    uint32_t rb = 0;
-    if (lane == 0) rb = atomicAdd(queue, 32u);
-    rb = __shfl_sync(0xffffffffu, rb, 0);
-    if (rb >= nrows) break;
+    unsigned long long rb64 = 0;  // 64-bit queue: row counts may approach 2^32
+    if (lane == 0) rb64 = atomicAdd(queue, 32ull);
+    rb64 = __shfl_sync(0xffffffffu, rb64, 0);
+    if (rb64 >= nrows) break;
+    const uint32_t rb = (uint32_t)rb64;
     const uint32_t i = rb + lane;
     uint32_t ul = 0, dl = 0, Ol = 0, hl = 0;
     bool work = false;
@@ -1068,8 +1069,10 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     pl.mark("join_cta");
     if (pv) {
       // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics)
-      DBuf<unsigned int> rq(3, s);  // light queue, heavy queue, heavy count
+      DBuf<unsigned int> rq(3, s);  // -, heavy queue, heavy count
+      DBuf<unsigned long long> lq(1, s);  // light row queue
       TC_CUDA(cudaMemsetAsync(rq.get(), 0, 3 * sizeof(unsigned int), s));
+      TC_CUDA(cudaMemsetAsync(lq.get(), 0, sizeof(unsigned long long), s));
       uint32_t* heavy = g.scratch[kSlotHeavy].get<uint32_t>((uint64_t)(fr.u_hi - fr.u_lo) + 1, s);
       const uint32_t rcnt = n < top_cnt ? n : top_cnt;
       const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
@@ -1080,7 +1083,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
       TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_pv_rows_heavy, kRowWarps * 32, rsm));
       k_pv_rows<<<(unsigned)(sms * std::max(rocc, 1)), kRowWarps * 32, rsm, s>>>(
           g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, fr.u_hi, g.h0, n - rcnt, rcnt,
-          rq.get(), heavy, rq.get() + 2, t_rank);
+          lq.get(), heavy, rq.get() + 2, t_rank);
       TC_LAUNCH();
       ++launches;
       pl.mark("pv_rows_light");

@@ -259,10 +259,8 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   fr.u_lo = 0;
   fr.u_hi = n ? n - 1 : 0;
   if (per_vertex && e1 > e0) {
-    if (!whole) {
-      fr.u_lo = read_scalar(g.src.get() + e0, s);
-      fr.u_hi = read_scalar(g.src.get() + e1 - 1, s);
-    }
+    fr.u_lo = read_scalar(g.src.get() + e0, s);  // the rows that own the part's edges
+    fr.u_hi = read_scalar(g.src.get() + e1 - 1, s);
     const uint64_t rows = (uint64_t)fr.u_hi - fr.u_lo + 1;
     fr.rowbase = g.scratch[kSlotRowBase].get<uint64_t>(rows + 1, s);
     kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get(), fr.u_lo}, fr.rowbase, rows, fr.rowbase + rows,

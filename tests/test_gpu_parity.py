@@ -179,6 +179,23 @@ def test_large_clique(tc, cuda_ok, mode_env):
 
 
 @pytest.mark.parametrize("parts", [2, 3, 8])
+def test_parts_sum_to_total_er(tc, oracle, cuda_ok, parts):
+    """Multi-part sums on a uniform-degree graph (ER, every pivot in the warp bin)."""
+    c = load_golden("synthetic.json")["C2_er_s20_d32"]
+    pairs = tc.generate(tc.GEN_ER, 20, 32)
+    g = tc.build_graph_from_pairs(pairs, c["n"])
+    assert g.max_out_degree <= 48
+    tot = 0
+    pv = np.zeros(c["n"], np.uint64)
+    for p in range(parts):
+        r = tc.count_triangles(g, tc.MatchOptions(per_vertex=True, part_index=p, part_count=parts))
+        tot += r.count
+        pv += r.per_vertex
+    assert tot == c["T"]
+    assert oracle.fnv(pv) == c["pv_fnv"]
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
 def test_parts_sum_to_total(tc, oracle, cuda_ok, parts):
     c = load_golden("synthetic.json")["C1_rmat_s16_ef16"]
     pairs = tc.generate(tc.GEN_RMAT, 16, 16)

@@ -1,0 +1,5 @@
+#!/bin/bash
+for v in "$@"; do
+  lib=variants/$v.so; [ "$v" = "main" ] && lib=paper_1909_02127_b200/libtcb200.so
+  echo "== $v"; TCB200_LIB=$PWD/$lib python tools/phase_probe.py --kind er --scale 20 --param 32 --pv 1 --iters 3 2>&1 | tail -1
+done
