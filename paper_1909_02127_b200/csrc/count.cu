@@ -74,23 +74,26 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 
 // ---- multi-GPU partition -------------------------------------------------------
 
-// Prefix of per-edge cost (wedge work + a per-item overhead) over the oriented
-// edges, then P-1 binary searches.  Contiguous edge ranges = contiguous source
-// ranges of the degree-ordered DAG: the north-star "degree-weighted ranges".
-struct EdgeCost {
+// Per-item overhead in candidate-probe units (frontier record + segment
+// staging), fitted on the C5 8-part split (~330 for the join's staging and
+// segments, the rest for the frontier record).
+constexpr uint64_t kItemCost = 400;
+
+// Per-row cost of the degree-ordered DAG: row u with d = d+(u) out-edges
+// contributes C(d,2) candidate wedges and d items.  An exclusive scan over the
+// rows, then P-1 binary searches: each part is a contiguous range of source
+// rows (= of oriented edges), the north-star "degree-weighted ranges".  A scan
+// over |V| rows, not |E| edges: it is part of every multi-GPU count.
+struct RowCost {
   const uint32_t* off;
-  const uint32_t* col;
-  const uint32_t* src;
-  __device__ __forceinline__ uint64_t operator()(uint64_t e) const {
-    const uint32_t v = col[e];
-    const uint32_t dv = off[v + 1] - off[v];
-    const uint32_t end = off[src[e] + 1];
-    return (dv > 0 && e + 1 < end) ? (uint64_t)(end - (uint32_t)(e + 1)) + 8 : 0ull;
+  __device__ __forceinline__ uint64_t operator()(uint64_t u) const {
+    const uint64_t d = off[u + 1] - off[u];
+    return d * (d ? d - 1 : 0) / 2 + kItemCost * d;
   }
 };
 
-__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint64_t E, uint64_t total, uint32_t parts,
-                              uint64_t* __restrict__ bounds) {
+__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, const uint32_t* __restrict__ off, uint32_t n,
+                              uint64_t E, uint64_t total, uint32_t parts, uint64_t* __restrict__ bounds) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > parts) return;
   if (p == 0) {
@@ -102,12 +105,12 @@ __global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint64_t E, u
     return;
   }
   const uint64_t target = (uint64_t)((double)total * p / parts);
-  uint64_t lo = 0, hi = E;  // first e with prefix[e] >= target
+  uint64_t lo = 0, hi = n;  // first row r with prefix[r] >= target
   while (lo < hi) {
     const uint64_t mid = (lo + hi) / 2;
     if (prefix[mid] < target) lo = mid + 1; else hi = mid;
   }
-  bounds[p] = lo;
+  bounds[p] = lo < n ? off[lo] : E;
 }
 
 // ---- membership structures -------------------------------------------------
@@ -958,10 +961,12 @@ const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
   g.part_bounds.assign((size_t)parts + 1, 0);
   g.part_bounds[parts] = E;
   if (E && parts > 1) {
-    DBuf<uint64_t> prefix(E, s), tot(1, s), bnd((uint64_t)parts + 1, s);
-    scan_exclusive<uint64_t>(EdgeCost{g.off.get(), g.col.get(), g.src.get()}, prefix.get(), E, tot.get(), s);
+    const uint32_t n = g.n;
+    DBuf<uint64_t> prefix(n, s), tot(1, s), bnd((uint64_t)parts + 1, s);
+    scan_exclusive<uint64_t>(RowCost{g.off.get()}, prefix.get(), n, tot.get(), s);
     const uint64_t total_cost = read_scalar(tot.get(), s);
-    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), E, total_cost, parts, bnd.get());
+    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), g.off.get(), n, E, total_cost, parts,
+                                                          bnd.get());
     TC_LAUNCH();
     TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
                             cudaMemcpyDeviceToHost, s));

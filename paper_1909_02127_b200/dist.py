@@ -7,8 +7,8 @@ part_index=r, part_count=P: contiguous source ranges of the (deg,id) DAG with
 ~equal wedge work), then ONE allreduce (NCCL over NVLink on the GPU box, gloo
 in the CPU tests) sums the u64 total and the per-vertex array.
 
-`edge_cost` / `partition_bounds` restate, on the host, the device partition
-(count.cu EdgeCost + k_part_bounds) so the split can be checked without a GPU.
+`row_cost` / `partition_bounds` restate, on the host, the device partition
+(count.cu RowCost + k_part_bounds) so the split can be checked without a GPU.
 """
 from __future__ import annotations
 
@@ -36,27 +36,30 @@ def degree_rank_dag(offsets: np.ndarray, nbrs: np.ndarray):
     return off, col, src, order
 
 
-def edge_cost(off: np.ndarray, col: np.ndarray, src: np.ndarray) -> np.ndarray:
-    """Per oriented edge e = u->v: suffix length of N+(u) after v plus a per-item
-    overhead of 8, when v can close a triangle (count.cu EdgeCost)."""
-    dv = off[col + 1] - off[col]
-    end = off[src + 1]
-    e = np.arange(col.size, dtype=np.int64)
-    useful = (dv > 0) & (e + 1 < end)
-    return np.where(useful, end - (e + 1) + 8, 0)
+ITEM_COST = 400  # count.cu kItemCost: per-item overhead in candidate-probe units
 
 
-def partition_bounds(cost: np.ndarray, parts: int) -> np.ndarray:
-    """b[0]=0, b[P]=E, b[p] = first e with exclusive-prefix(cost)[e] >= total*p/P
+def row_cost(off: np.ndarray) -> np.ndarray:
+    """Per source row u of the oriented DAG with d = d+(u): C(d,2) candidate
+    wedges + ITEM_COST per item (count.cu RowCost)."""
+    d = np.diff(off.astype(np.int64))
+    return d * np.maximum(d - 1, 0) // 2 + ITEM_COST * d
+
+
+def partition_bounds(cost: np.ndarray, parts: int, off: np.ndarray) -> np.ndarray:
+    """Oriented-edge bounds of a parts-way split: b[0]=0, b[P]=E, b[p] = off[r]
+    for the first row r with exclusive-prefix(cost)[r] >= total*p/P
     (count.cu k_part_bounds; the double rounding mirrors the device)."""
-    E = cost.size
-    prefix = np.concatenate([[0], np.cumsum(cost)[:-1]]) if E else np.zeros(0, np.int64)
+    n = cost.size
+    E = int(off[-1]) if off.size else 0
+    prefix = np.concatenate([[0], np.cumsum(cost)[:-1]]) if n else np.zeros(0, np.int64)
     total = int(cost.sum())
     b = np.zeros(parts + 1, np.int64)
     b[parts] = E
     for p in range(1, parts):
         target = int(float(total) * p / parts)
-        b[p] = int(np.searchsorted(prefix, target, side="left"))
+        r = int(np.searchsorted(prefix, target, side="left"))
+        b[p] = int(off[r]) if r < n else E
     return b
 
 

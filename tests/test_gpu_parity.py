@@ -216,9 +216,9 @@ def test_partition_bounds_match_host(tc, oracle, cuda_ok):
     g = tc.build_graph_from_pairs(pairs, 1 << 14)
     off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 14)
     roff, col, src, order = tdist.degree_rank_dag(off, nb)
-    cost = tdist.edge_cost(roff, col, src)
+    cost = tdist.row_cost(roff)
     for P in (2, 3, 8):
-        assert tc.partition_bounds(g, P).tolist() == tdist.partition_bounds(cost, P).tolist()
+        assert tc.partition_bounds(g, P).tolist() == tdist.partition_bounds(cost, P, roff).tolist()
 
 
 SYN = ["C1_rmat_s16_ef16", "C2_er_s20_d32", "rmat_s18_ef16", "kron_s18_ef16", "rmat_s20_ef16"]

@@ -38,7 +38,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     off, nb, T, pv = _graph()
     roff, col, src, order = tdist.degree_rank_dag(off, nb)
-    b = tdist.partition_bounds(tdist.edge_cost(roff, col, src), world)
+    b = tdist.partition_bounds(tdist.row_cost(roff), world, roff)
     tot, t_rank = tdist.count_part_host(roff, col, src, int(b[rank]), int(b[rank + 1]), off.size - 1)
     total = torch.tensor([tot], dtype=torch.int64)
     per_vertex = torch.from_numpy(t_rank[order.argsort()].astype(np.int64))  # rank -> id space
@@ -83,11 +83,14 @@ def test_partition_is_balanced_and_covering():
     from paper_1909_02127_b200 import dist as tdist
     off, nb, T, pv = _graph()
     roff, col, src, order = tdist.degree_rank_dag(off, nb)
-    cost = tdist.edge_cost(roff, col, src)
+    cost = tdist.row_cost(roff)
     for P in (1, 2, 3, 4, 8):
-        b = tdist.partition_bounds(cost, P)
+        b = tdist.partition_bounds(cost, P, roff)
         assert b[0] == 0 and b[-1] == col.size and np.all(np.diff(b) >= 0)
-        parts = [int(cost[b[p]:b[p + 1]].sum()) for p in range(P)]
+        # rows of each part (the bounds are row starts; empty rows cost 0)
+        rb = np.searchsorted(roff[:-1], b, side="left")
+        rb[-1] = cost.size
+        parts = [int(cost[rb[p]:rb[p + 1]].sum()) for p in range(P)]
         assert sum(parts) == int(cost.sum())
-        # each part within one maximal edge cost of the ideal share
+        # each part within one maximal row cost of the ideal share
         assert max(parts) - cost.sum() / P <= cost.max() + 1
