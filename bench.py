@@ -263,10 +263,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TCB_BENCH_SHARE_GPU=1 (plumbing check only): every rank on cuda:0 over gloo,
+    # so the multi-rank path can be exercised on a 1-GPU box
+    share = os.environ.get("TCB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[a.config]
     kind, scale, param, per_vertex, desc = cfg
     per_vertex = per_vertex and not a.no_per_vertex

@@ -19,6 +19,8 @@
  *                             (matcher.cpp:301-303 -> match :249-299 ->
  *                              count_final_level :204-245)
  * tc_parse_matrix_market      trimatch::parse_matrix_market io.hpp:34 (io.cpp:93-159)
+ * tc_graph_load_matrix_market trimatch::load_graph (MatrixMarket) io.hpp:45
+ * tc_graph_write_csr_cache    trimatch::write_csr_cache  io.hpp:39 (io.cpp:167-177)
  * tc_csr_cache_parse          trimatch::read_csr_cache   io.hpp:40 (io.cpp:187-220)
  * tc_graph_destroy            ~Graph
  * tc_last_error               the what() of the exception the reference throws
@@ -151,6 +153,19 @@ tc_status tc_parse_matrix_market(const char* text, uint64_t len, uint32_t** pair
 /* TRIMCSR1 binary cache (io.cpp:18-19, :167-220) held in memory: validates
  * and builds a handle straight from the CSR (no sort). */
 tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_graph** out);
+
+/* load_graph for MatrixMarket text (io.cpp:222-228 -> parse_matrix_market
+ * io.cpp:93-159 -> build_graph graph.cpp:33-85) held in memory: the banner and
+ * size line on the host, the entry lines tokenized on the device, then the
+ * device build.  Malformed text fails with TC_EPARSE and the reference's
+ * message and line number. */
+tc_status tc_graph_load_matrix_market(const char* text, uint64_t len, int device, tc_graph** out,
+                                      tc_build_report* report);
+
+/* write_csr_cache (io.cpp:167-177) into caller memory: *len bytes (8-byte
+ * aligned buffer), little-endian TRIMCSR1 image of the graph. */
+tc_status tc_graph_csr_cache_size(const tc_graph* g, uint64_t* len);
+tc_status tc_graph_write_csr_cache(tc_graph* g, void* bytes);
 
 /* ---- synthetic inputs (SURVEY 8d generators, bit-exact on device) ------- */
 

@@ -216,23 +216,14 @@ inline Graph read_csr_cache(const std::string& path, int device = 0) {
 }
 
 inline void write_csr_cache(const std::string& path, const Graph& g) {
+  // the TRIMCSR1 image (io.cpp:167-177 layout) assembled by the library
+  std::uint64_t len = 0;
+  detail::check(tc_graph_csr_cache_size(g.handle(), &len));
+  std::vector<std::uint64_t> buf((len + 7) / 8);  // 8-byte aligned
+  detail::check(tc_graph_write_csr_cache(g.handle(), buf.data()));
   std::ofstream out(path, std::ios::binary | std::ios::trunc);
   if (!out) throw IoError("cannot open '" + path + "' for writing");
-  auto put64 = [&](std::uint64_t v) {
-    char b[8];
-    for (int i = 0; i < 8; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xFF);
-    out.write(b, 8);
-  };
-  out.write("TRIMCSR1", 8);
-  put64(1);
-  put64(g.num_vertices());
-  put64(g.num_edges());
-  for (std::uint64_t o : g.row_offsets()) put64(o);
-  for (VertexId v : g.neighbor_array()) {
-    char b[4];
-    for (int i = 0; i < 4; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xFF);
-    out.write(b, 4);
-  }
+  out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(len));
   if (!out) throw IoError("write failed for '" + path + "'");
 }
 
@@ -241,7 +232,18 @@ inline Graph load_graph(const std::string& path, BuildReport* report = nullptr, 
     if (report) *report = BuildReport{};
     return read_csr_cache(path, device);
   }
-  return build_graph(parse_matrix_market_file(path), report, device);
+  // MatrixMarket: entries tokenized and built on the device
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("cannot open '" + path + "' for reading");
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  tc_graph* h = nullptr;
+  tc_build_report rep{};
+  detail::check(tc_graph_load_matrix_market(text.data(), text.size(), device, &h, &rep));
+  if (report) {
+    report->self_loops_removed = rep.self_loops_removed;
+    report->duplicate_entries_removed = rep.duplicate_entries_removed;
+  }
+  return Graph(h);
 }
 
 // ---- matcher -------------------------------------------------------------------

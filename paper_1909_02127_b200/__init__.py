@@ -95,6 +95,10 @@ _sig("tc_count", C.c_int, [C.c_void_p, C.POINTER(TcCountOpts), C.c_void_p, C.c_v
                            C.POINTER(TcCountStats)])
 _sig("tc_parse_matrix_market", C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), u64p, u32p])
 _sig("tc_csr_cache_to_graph", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p)])
+_sig("tc_graph_load_matrix_market", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
+                                              C.c_void_p])
+_sig("tc_graph_csr_cache_size", C.c_int, [C.c_void_p, u64p])
+_sig("tc_graph_write_csr_cache", C.c_int, [C.c_void_p, C.c_void_p])
 _sig("tc_partition_bounds", C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p])
 _sig("tc_gen_num_edges", C.c_uint64, [C.c_int, C.c_int, C.c_int])
 _sig("tc_generate", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p])
@@ -103,6 +107,7 @@ EXPORTED_SYMBOLS = [
     "tc_abi_version", "tc_last_error", "tc_free", "tc_graph_build", "tc_graph_from_csr", "tc_graph_get_info",
     "tc_graph_export_csr", "tc_graph_degrees", "tc_graph_set_stream", "tc_graph_destroy", "tc_count",
     "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate", "tc_partition_bounds",
+    "tc_graph_load_matrix_market", "tc_graph_csr_cache_size", "tc_graph_write_csr_cache",
 ]
 
 
@@ -418,17 +423,38 @@ def read_csr_cache(path: str, device: int = 0) -> Graph:
     return Graph(h.value, device)
 
 
+def csr_cache_bytes(g: Graph) -> np.ndarray:
+    """The TRIMCSR1 image of g (write_csr_cache's bytes), assembled by the
+    library from the device graph."""
+    n = C.c_uint64()
+    _check(_lib.tc_graph_csr_cache_size(g.handle, C.byref(n)))
+    buf = np.empty((n.value + 7) // 8, np.uint64)  # 8-byte aligned
+    _check(_lib.tc_graph_write_csr_cache(g.handle, C.c_void_p(buf.ctypes.data)))
+    return buf.view(np.uint8)[: n.value]
+
+
 def write_csr_cache(path: str, g: Graph) -> None:
     """trimatch::write_csr_cache (io.cpp:167-177): little-endian TRIMCSR1 v1."""
-    ro, nb = g.export_csr()
+    data = csr_cache_bytes(g)
     try:
         with open(path, "wb") as f:
-            f.write(_CSR_MAGIC)
-            f.write(np.array([1, g.num_vertices(), g.num_edges()], dtype="<u8").tobytes())
-            f.write(ro.astype("<u8").tobytes())
-            f.write(nb.astype("<u4").tobytes())
+            f.write(data.tobytes())
     except OSError:
         raise IoError(f"cannot open '{path}' for writing")
+
+
+def load_matrix_market(text, report: Optional[BuildReport] = None, device: int = 0) -> Graph:
+    """load_graph for MatrixMarket bytes: entries tokenized and built on the GPU
+    (tc_graph_load_matrix_market); same errors as parse_matrix_market."""
+    if isinstance(text, str):
+        text = text.encode()
+    h = C.c_void_p()
+    rep = TcBuildReport()
+    _check(_lib.tc_graph_load_matrix_market(text, len(text), device, C.byref(h), C.byref(rep)))
+    if report is not None:
+        report.self_loops_removed = rep.self_loops_removed
+        report.duplicate_entries_removed = rep.duplicate_entries_removed
+    return Graph(h.value, device)
 
 
 def load_graph(path: str, report: Optional[BuildReport] = None, device: int = 0) -> Graph:
@@ -438,7 +464,12 @@ def load_graph(path: str, report: Optional[BuildReport] = None, device: int = 0)
             report.self_loops_removed = 0
             report.duplicate_entries_removed = 0
         return read_csr_cache(path, device)
-    return build_graph(parse_matrix_market_file(path), report, device)
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise IoError(f"cannot open '{path}' for reading")
+    return load_matrix_market(data, report, device)
 
 
 # ---- synthetic inputs --------------------------------------------

@@ -227,7 +227,16 @@ struct RowCtx {
   const uint32_t* roff;  // pass 1: rank-space row offsets
   uint32_t* col;
   uint32_t* src;
+  int strict;  // TRIMCSR1 ingest: also reject self-loops and non-ascending rows (io.cpp:211-216)
 };
+
+// pass-0 validity bits of entry i (row u starting at a): 1 = id out of range,
+// 2 = (strict) self-loop or not strictly ascending
+__device__ __forceinline__ int entry_bad(const RowCtx& cx, uint64_t i, uint64_t a, uint32_t u, uint32_t v) {
+  int bad = v >= cx.n ? 1 : 0;
+  if (cx.strict && (v == u || (i > a && cx.nbrs[i - 1] >= v))) bad |= 2;
+  return bad;
+}
 
 // One warp over id-row u; returns (in lane-summed form) the entries v > u.
 template <int kPass>
@@ -247,7 +256,7 @@ __device__ __forceinline__ uint32_t warp_csr_row(const RowCtx& cx, uint32_t u, i
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
       const bool valid = i0 + 32 * t + lane < b;
-      if (valid && v[t] >= cx.n) bad = 1;
+      if (!kPass && valid) bad |= entry_bad(cx, i0 + 32 * t + lane, a, u, v[t]);
       rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
       upper += (valid && v[t] > u && v[t] < cx.n) ? 1u : 0u;
     }
@@ -280,7 +289,7 @@ __device__ __forceinline__ uint32_t thread_csr_row(const RowCtx& cx, uint32_t u,
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const bool valid = i0 + t < b;
-      if (valid && v[t] >= cx.n) bad = 1;
+      if (!kPass && valid) bad |= entry_bad(cx, i0 + t, a, u, v[t]);
       rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
     }
 #pragma unroll
@@ -334,7 +343,8 @@ __global__ void __launch_bounds__(256) k_csr_rows(RowCtx cx, unsigned int* __res
   if (!kPass) {
     const unsigned long long w = warp_sum((unsigned long long)upper);
     if (lane_id() == 0 && w) atomicAdd(upper_total, w);
-    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(bad_flag, 1);
+    bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)bad);
+    if (bad && lane_id() == 0) atomicOr(bad_flag, bad);
   }
 }
 
@@ -372,7 +382,7 @@ __global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __re
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const bool valid = i0 + 32 * t + lane < b;
-        if (valid && v[t] >= cx.n) bad = 1;
+        if (!kPass && valid) bad |= entry_bad(cx, i0 + 32 * t + lane, cx.off[ch.u], ch.u, v[t]);
         rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
         upper += (valid && v[t] > ch.u && v[t] < cx.n) ? 1u : 0u;
       }
@@ -397,7 +407,8 @@ __global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __re
   if (!kPass) {
     const unsigned long long w = warp_sum((unsigned long long)upper);
     if (lane == 0 && w) atomicAdd(upper_total, w);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(bad_flag, 1);
+    bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)bad);
+    if (bad && lane == 0) atomicOr(bad_flag, bad);
   }
 }
 
@@ -809,7 +820,8 @@ void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t
   finalize(g, ukeys, E);
 }
 
-void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n, uint64_t num_edges) {
+void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n, uint64_t num_edges,
+                    bool strict) {
   cudaStream_t s = g.stream;
   const int dev = g.device;
   g.n = n;
@@ -831,8 +843,10 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     TC_LAUNCH();
   }
   const uint64_t off_n = n ? read_scalar(d_off + n, s) : 0;
-  if (read_scalar(bad.get(), s) || off_n != total || (n && read_scalar(d_off, s) != 0))
+  if (read_scalar(bad.get(), s) || off_n != total || (n && read_scalar(d_off, s) != 0)) {
+    if (strict) fail(TC_EPARSE, "corrupt CSR cache offsets (line 1)");
     fail(TC_EINVAL, "Graph: inconsistent CSR arrays");
+  }
   // hub rows -> chunk list (device: chunk counts, scan, fill)
   const uint32_t nbig = read_scalar(cnts.get(), s);
   DBuf<uint32_t> choff((uint64_t)nbig + 1, s);
@@ -852,7 +866,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   pl.mark("csr_rank");
   DBuf<uint32_t> dplus(nn, s);
   TC_CUDA(cudaMemsetAsync(dplus.get(), 0, sizeof(uint32_t) * nn, s));
-  RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), nullptr, nullptr, nullptr};
+  RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), nullptr, nullptr, nullptr, strict ? 1 : 0};
   const unsigned gw = (unsigned)num_sms(dev) * 8;
   if (total) {
     k_csr_rows<0><<<gw, 256, 0, s>>>(cx, cnts.get() + 2, upper.get(), bad.get());
@@ -865,7 +879,9 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     }
   }
   const uint64_t E = read_scalar(upper.get(), s);
-  if (read_scalar(bad.get(), s)) fail(TC_EINVAL, "Graph: neighbor id out of range");
+  const int badv = read_scalar(bad.get(), s);
+  if (badv && strict) fail(TC_EPARSE, "corrupt CSR cache adjacency (line 1)");
+  if (badv) fail(TC_EINVAL, "Graph: neighbor id out of range");
   if (E != num_edges) fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
   g.E = E;
   alloc_rows(g);

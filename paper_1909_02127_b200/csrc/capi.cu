@@ -218,10 +218,9 @@ tc_status tc_graph_build(const uint32_t* pairs, uint64_t m, uint32_t n_declared,
   TC_API_CATCH
 }
 
-tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbors, uint32_t n,
-                            uint64_t num_edges, int device, tc_graph** out) {
-  if (!out) return set_error(TC_EINVAL, "tc_graph_from_csr: out is NULL");
-  if (!row_offsets || (num_edges && !neighbors)) return set_error(TC_EINVAL, "tc_graph_from_csr: NULL array");
+namespace {
+tc_status from_csr_impl(const uint64_t* row_offsets, const uint32_t* neighbors, uint32_t n, uint64_t num_edges,
+                        int device, tc_graph** out, bool strict) {
   tc_graph* g = nullptr;
   TC_API_TRY
   DeviceGuard dg(device);
@@ -232,7 +231,7 @@ tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbo
     DevIn<uint64_t> off(row_offsets, (uint64_t)n + 1, g->stream);
     DevIn<uint32_t> nb(neighbors, 2 * num_edges, g->stream);
     pl.mark("csr_h2d");
-    tcb::build_from_csr(*g, off.p, nb.p, n, num_edges);
+    tcb::build_from_csr(*g, off.p, nb.p, n, num_edges, strict);
     g->build_ms = t.stop();
   } catch (...) {
     destroy_handle(g);
@@ -241,6 +240,14 @@ tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbo
   *out = g;
   return TC_OK;
   TC_API_CATCH
+}
+}  // namespace
+
+tc_status tc_graph_from_csr(const uint64_t* row_offsets, const uint32_t* neighbors, uint32_t n,
+                            uint64_t num_edges, int device, tc_graph** out) {
+  if (!out) return set_error(TC_EINVAL, "tc_graph_from_csr: out is NULL");
+  if (!row_offsets || (num_edges && !neighbors)) return set_error(TC_EINVAL, "tc_graph_from_csr: NULL array");
+  return from_csr_impl(row_offsets, neighbors, n, num_edges, device, out, false);
 }
 
 tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info) {
@@ -337,6 +344,64 @@ tc_status tc_parse_matrix_market(const char* text, uint64_t len, uint32_t** pair
   TC_API_CATCH
 }
 
+tc_status tc_graph_load_matrix_market(const char* text, uint64_t len, int device, tc_graph** out,
+                                      tc_build_report* report) {
+  if (!out || (len && !text)) return set_error(TC_EINVAL, "tc_graph_load_matrix_market: NULL argument");
+  tc_graph* g = nullptr;
+  TC_API_TRY
+  tcb::MmHeader h;
+  tcb::parse_mm_header(text, len, h);  // banner + size line (host, a few bytes)
+  if (h.nnz >= (1ull << 32)) return set_error(TC_ERANGE, "MatrixMarket: >= 2^32 entries");
+  DeviceGuard dg(device);
+  g = new_handle(device);
+  try {
+    Timer t(g->stream);
+    const uint64_t blen = len - h.body;
+    tcb::DBuf<unsigned char> body(blen ? blen : 1, g->stream);
+    if (blen)
+      TC_CUDA(cudaMemcpyAsync(body.get(), text + h.body, blen, cudaMemcpyHostToDevice, g->stream));
+    tcb::DBuf<uint32_t> pairs;
+    if (!tcb::mm_tokenize(body.get(), blen, h, pairs, device, g->stream)) {
+      // malformed body: the host parser throws the reference's exact ParseError
+      std::vector<uint32_t> v;
+      uint32_t n = 0;
+      tcb::parse_matrix_market(text, len, v, n);
+      tcb::fail(TC_EPARSE, "MatrixMarket: device tokenizer and host parser disagree");
+    }
+    body.release();
+    tc_build_report rep{};
+    tcb::build_from_pairs(*g, pairs.get(), h.nnz, h.n_declared, &rep);
+    g->build_ms = t.stop();
+    if (report) *report = rep;
+  } catch (...) {
+    destroy_handle(g);
+    throw;
+  }
+  *out = g;
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_graph_csr_cache_size(const tc_graph* g, uint64_t* len) {
+  if (!g || !len) return set_error(TC_EINVAL, "tc_graph_csr_cache_size: NULL argument");
+  *len = 32 + 8 * ((uint64_t)g->n + 1) + 4 * (2 * g->E);
+  return TC_OK;
+}
+
+tc_status tc_graph_write_csr_cache(tc_graph* g, void* bytes) {
+  if (!g || !bytes) return set_error(TC_EINVAL, "tc_graph_write_csr_cache: NULL argument");
+  if (reinterpret_cast<uintptr_t>(bytes) & 7) return set_error(TC_EINVAL, "tc_graph_write_csr_cache: buffer not 8-byte aligned");
+  TC_API_TRY
+  unsigned char* b = static_cast<unsigned char*>(bytes);
+  static const char kMagic[8] = {'T', 'R', 'I', 'M', 'C', 'S', 'R', '1'};
+  std::memcpy(b, kMagic, 8);
+  const uint64_t hdr[3] = {1, g->n, g->E};  // version, num_vertices, num_edges (little-endian host)
+  std::memcpy(b + 8, hdr, sizeof(hdr));
+  return tc_graph_export_csr(g, reinterpret_cast<uint64_t*>(b + 32),
+                             reinterpret_cast<uint32_t*>(b + 32 + 8 * ((uint64_t)g->n + 1)));
+  TC_API_CATCH
+}
+
 tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_graph** out) {
   if (!out || (len && !bytes)) return set_error(TC_EINVAL, "tc_csr_cache_to_graph: NULL argument");
   TC_API_TRY
@@ -348,8 +413,8 @@ tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_
     b = aligned.data();
   }
   tcb::CsrView v;
-  tcb::parse_csr_cache(b, len, v);
-  return tc_graph_from_csr(v.offsets, v.nbrs, v.n, v.num_edges, device, out);
+  tcb::parse_csr_cache(b, len, v);  // header checks; offsets and adjacency are validated on the device
+  return from_csr_impl(v.offsets, v.nbrs, v.n, v.num_edges, device, out, true);
   TC_API_CATCH
 }
 

@@ -140,8 +140,10 @@ struct RowMasks {
 // Build pipeline entry points (build.cu).
 void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t n,
                       tc_build_report* rep);
+// strict: TRIMCSR1 ingest -- reject bad offsets / self-loops / unsorted rows
+// with the reference's ParseError messages (io.cpp:206-218)
 void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n,
-                    uint64_t num_edges);
+                    uint64_t num_edges, bool strict = false);
 void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs);
 void export_degrees(tc_graph& g, uint32_t* d_deg);
 
@@ -150,6 +152,12 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total,
                      uint64_t* d_per_vertex, tc_count_stats* stats);
 // Degree-weighted oriented-edge ranges of a P-way split.
 const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts);
+
+// MatrixMarket entry tokenizer (mm.cu): true and device pairs when the body is
+// well formed, false when the host parser must report the error.
+struct MmHeader;
+bool mm_tokenize(const unsigned char* d_body, uint64_t len, const MmHeader& h, DBuf<uint32_t>& d_pairs,
+                 int device, cudaStream_t s);
 
 // Generators (gen.cu).
 uint64_t gen_num_edges(int kind, int scale, int param);

@@ -83,7 +83,7 @@ struct Lines {
 
 }  // namespace
 
-void parse_matrix_market(const char* text, uint64_t len, std::vector<uint32_t>& pairs, uint32_t& n_declared) {
+void parse_mm_header(const char* text, uint64_t len, MmHeader& h) {
   Lines in{text, text + len};
   std::string_view raw;
   uint64_t line_no = 0;
@@ -109,7 +109,23 @@ void parse_matrix_market(const char* text, uint64_t len, std::vector<uint32_t>& 
   }
   const uint64_t declared = std::max(rows, cols);
   if (declared > 0xFFFFFFFFull) parse_error("vertex count exceeds 32-bit id range", line_no);
-  n_declared = (uint32_t)declared;
+  h.rows = rows;
+  h.cols = cols;
+  h.nnz = nnz;
+  h.n_declared = (uint32_t)declared;
+  h.line_no = line_no;
+  h.body = (uint64_t)(in.p - text);
+}
+
+void parse_matrix_market(const char* text, uint64_t len, std::vector<uint32_t>& pairs, uint32_t& n_declared) {
+  MmHeader hd;
+  parse_mm_header(text, len, hd);
+  Lines in{text + hd.body, text + len};
+  std::string_view raw;
+  std::string_view tok[4];
+  uint64_t line_no = hd.line_no;
+  const uint64_t rows = hd.rows, cols = hd.cols, nnz = hd.nnz;
+  n_declared = hd.n_declared;
   pairs.clear();
   pairs.reserve(2 * std::min<uint64_t>(nnz, len / 4 + 1));
 
@@ -136,7 +152,7 @@ void parse_matrix_market(const char* text, uint64_t len, std::vector<uint32_t>& 
   }
 }
 
-// TRIMCSR1 (io.cpp:18-19 magic/version, :187-220 reader + invariant checks).
+// TRIMCSR1 (io.cpp:18-19 magic/version, :187-205 reader header checks).
 void parse_csr_cache(const void* bytes, uint64_t len, CsrView& out) {
   const unsigned char* b = static_cast<const unsigned char*>(bytes);
   static const char kMagic[8] = {'T', 'R', 'I', 'M', 'C', 'S', 'R', '1'};
@@ -158,15 +174,8 @@ void parse_csr_cache(const void* bytes, uint64_t len, CsrView& out) {
   // offsets 32 and 32+8(nv+1)); copy only when the buffer is misaligned.
   out.offsets = reinterpret_cast<const uint64_t*>(b + 32);
   out.nbrs = reinterpret_cast<const uint32_t*>(b + 32 + 8 * (nv + 1));
-  const uint64_t* off = out.offsets;
-  if (off[0] != 0 || off[nv] != 2 * ne) parse_error("corrupt CSR cache offsets", 1);
-  for (uint64_t u = 0; u < nv; ++u)
-    if (off[u] > off[u + 1]) parse_error("corrupt CSR cache offsets", 1);
-  const uint32_t* nb = out.nbrs;
-  for (uint64_t u = 0; u < nv; ++u)
-    for (uint64_t k = off[u]; k < off[u + 1]; ++k)
-      if (nb[k] >= nv || nb[k] == u || (k > off[u] && nb[k - 1] >= nb[k]))
-        parse_error("corrupt CSR cache adjacency", 1);
+  // the O(|V|+|E|) invariant checks (io.cpp:206-218: offsets, then adjacency)
+  // run on the device in the CSR build (build.cu build_from_csr, strict)
 }
 
 }  // namespace tcb

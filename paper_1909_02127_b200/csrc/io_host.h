@@ -22,6 +22,13 @@ struct CsrView {
   const uint32_t* nbrs = nullptr;
 };
 
+// MatrixMarket banner + comments + size line (io.cpp:93-122): the entry body
+// starts at byte `body` of the text; `line_no` = the size line's number.
+struct MmHeader {
+  uint64_t rows = 0, cols = 0, nnz = 0, body = 0, line_no = 0;
+  uint32_t n_declared = 0;
+};
+void parse_mm_header(const char* text, uint64_t len, MmHeader& h);
 void parse_matrix_market(const char* text, uint64_t len, std::vector<uint32_t>& pairs, uint32_t& n_declared);
 void parse_csr_cache(const void* bytes, uint64_t len, CsrView& out);
 

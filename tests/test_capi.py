@@ -85,12 +85,16 @@ def test_matrix_market_error_line(tc):
 def test_csr_cache_rejects_corruption(tc):
     with pytest.raises(tc.ParseError):
         tc._check(tc._lib.tc_csr_cache_to_graph(b"NOTMAGIC" + b"\0" * 40, 48, 0, C.byref(C.c_void_p())))
-    # valid header, non-ascending adjacency
+    # header checks run on the host (the offsets/adjacency invariants on the
+    # device: test_gpu_parity::test_csr_cache_corruption)
     hdr = b"TRIMCSR1" + np.array([1, 2, 1], "<u8").tobytes()
-    body = np.array([0, 1, 2], "<u8").tobytes() + np.array([1, 1], "<u4").tobytes()
     with pytest.raises(tc.ParseError) as ei:
-        tc._check(tc._lib.tc_csr_cache_to_graph(hdr + body, len(hdr + body), 0, C.byref(C.c_void_p())))
-    assert "corrupt CSR cache" in str(ei.value)
+        tc._check(tc._lib.tc_csr_cache_to_graph(hdr + b"\0" * 8, len(hdr) + 8, 0, C.byref(C.c_void_p())))
+    assert "truncated CSR cache" in str(ei.value)
+    bad_ver = b"TRIMCSR1" + np.array([2, 2, 1], "<u8").tobytes() + b"\0" * 32
+    with pytest.raises(tc.ParseError) as ei:
+        tc._check(tc._lib.tc_csr_cache_to_graph(bad_ver, len(bad_ver), 0, C.byref(C.c_void_p())))
+    assert "unsupported CSR cache version" in str(ei.value)
     with pytest.raises(tc.ParseError) as ei:
         tc._check(tc._lib.tc_csr_cache_to_graph(hdr[:20], 20, 0, C.byref(C.c_void_p())))
 

@@ -363,3 +363,114 @@ def test_csr_route_errors(tc, cuda_ok):
         tc.graph_from_csr(np.array([0, 4, 2, 6], np.uint64), nb)
     with pytest.raises(tc.InvalidArgument):  # offsets[n] != 2|E|
         tc.graph_from_csr(np.array([0, 2, 4, 5], np.uint64), nb, 3, 3)
+
+
+# ---- on-disk formats through the device ----
+
+def _csr_image(nv, off, nb):
+    return (b"TRIMCSR1" + np.array([1, nv, len(nb) // 2], "<u8").tobytes() + np.asarray(off, "<u8").tobytes()
+            + np.asarray(nb, "<u4").tobytes())
+
+
+def test_csr_cache_corruption(tc, cuda_ok):
+    """read_csr_cache invariants (io.cpp:206-218), checked on the device with
+    the reference's messages: offsets first, then adjacency."""
+    import ctypes as C
+    ok = _csr_image(3, [0, 2, 4, 6], [1, 2, 0, 2, 0, 1])
+    h = C.c_void_p()
+    tc._check(tc._lib.tc_csr_cache_to_graph(ok, len(ok), 0, C.byref(h)))
+    tc._lib.tc_graph_destroy(h)
+    cases = {
+        "corrupt CSR cache offsets": [_csr_image(3, [1, 2, 4, 6], [1, 2, 0, 2, 0, 1]),   # front != 0
+                                      _csr_image(3, [0, 4, 2, 6], [1, 2, 0, 2, 0, 1])],  # decreasing
+        "corrupt CSR cache adjacency": [_csr_image(3, [0, 2, 4, 6], [2, 1, 0, 2, 0, 1]),  # not ascending
+                                        _csr_image(3, [0, 2, 4, 6], [0, 2, 0, 2, 0, 1]),  # self-loop
+                                        _csr_image(3, [0, 2, 4, 6], [1, 9, 0, 2, 0, 1]),  # out of range
+                                        _csr_image(3, [0, 2, 4, 6], [1, 1, 0, 2, 0, 1])],  # duplicate
+    }
+    for msg, imgs in cases.items():
+        for img in imgs:
+            with pytest.raises(tc.ParseError) as ei:
+                tc._check(tc._lib.tc_csr_cache_to_graph(img, len(img), 0, C.byref(C.c_void_p())))
+            assert msg in str(ei.value) and ei.value.line == 1
+
+
+def test_csr_cache_emit_roundtrip(tc, oracle, cuda_ok):
+    """write_csr_cache from the device graph == the reference's byte layout,
+    and reads back to the same graph."""
+    pairs = tc.generate(tc.GEN_RMAT, 12, 16)
+    off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 12)
+    g = tc.build_graph_from_pairs(pairs, 1 << 12)
+    img = tc.csr_cache_bytes(g)
+    assert img.tobytes() == _csr_image(1 << 12, off, nb)
+    import ctypes as C
+    h = C.c_void_p()
+    tc._check(tc._lib.tc_csr_cache_to_graph(img.tobytes(), img.size, 0, C.byref(h)))
+    g2 = tc.Graph(h.value, 0)
+    assert g2.num_edges() == E and tc.count_triangles(g2).count == oracle.count(off, nb)
+
+
+def _mm_text(rng, n, m, *, crlf=False, values=False, comments=True):
+    lines = ["%%MatrixMarket matrix coordinate pattern general", "% generated"]
+    ij = rng.integers(1, n + 1, (m, 2))
+    lines.append(f"{n} {n} {m}")
+    for k, (i, j) in enumerate(ij):
+        if comments and k % 7 == 3:
+            lines.append("% a comment")
+        if comments and k % 11 == 5:
+            lines.append("   ")
+        sep = "\t" if k % 3 == 0 else " " * (1 + k % 2)
+        lines.append(f"{i}{sep}{j}" + (f" {rng.random():.3f}" if values else ""))
+    lines.append("% trailing comment")
+    nl = "\r\n" if crlf else "\n"
+    return (nl.join(lines) + (nl if rng.random() < 0.5 else "")).encode()
+
+
+def test_matrix_market_device_tokenizer(tc, oracle, cuda_ok):
+    """tc_graph_load_matrix_market (entries tokenized on the GPU) == host
+    parse_matrix_market + build_graph, on well-formed texts with comments,
+    blank lines, tabs, CRLF and value columns."""
+    rng = np.random.default_rng(3)
+    for k in range(12):
+        n, m = int(rng.integers(5, 3000)), int(rng.integers(0, 20000))
+        text = _mm_text(rng, n, m, crlf=k % 2 == 1, values=k % 3 == 0, comments=k % 4 != 0)
+        el = tc.parse_matrix_market(text)
+        rep_h, rep_d = tc.BuildReport(), tc.BuildReport()
+        gh = tc.build_graph(el, rep_h)
+        gd = tc.load_matrix_market(text, rep_d)
+        assert gd.num_vertices() == gh.num_vertices() and gd.num_edges() == gh.num_edges()
+        assert (rep_d.self_loops_removed, rep_d.duplicate_entries_removed) == \
+               (rep_h.self_loops_removed, rep_h.duplicate_entries_removed)
+        ro_h, nb_h = gh.export_csr()
+        ro_d, nb_d = gd.export_csr()
+        assert np.array_equal(ro_h, ro_d) and np.array_equal(nb_h, nb_d)
+
+
+MM_BAD = [
+    b"%%MatrixMarket matrix coordinate\n3 3 2\n1 2\n",                        # too few entries
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n1 x\n",                        # non-integer
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n1\n",                          # one token
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n0 1\n",                        # 1-based range
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n1 4\n",                        # column range
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n-1 2\n",                       # sign
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n1 2\n2 3\n",                   # content after nnz
+    b"%%MatrixMarket matrix coordinate\n3 3 1\n1 2\n\n% ok\nfoo\n",           # content after nnz
+    b"%%MatrixMarket matrix coordinate\n3 3 2\n1 2\n99999999999999999999 1\n",  # u64 overflow
+    b"%%MatrixMarket matrix coordinate\n3 3 0\n1 2\n",                        # nnz = 0 then content
+    b"%%MatrixMarket matrix coordinate\n3 3 2\n% c\n1 2\n  \n2 3x\n",         # trailing garbage
+]
+
+
+def test_matrix_market_device_errors(tc, cuda_ok):
+    """Malformed texts raise the host parser's ParseError (same message and
+    line) through the device loader."""
+    for text in MM_BAD:
+        with pytest.raises(tc.ParseError) as eh:
+            tc.parse_matrix_market(text)
+        with pytest.raises(tc.ParseError) as ed:
+            tc.load_matrix_market(text)
+        assert str(ed.value) == str(eh.value) and ed.value.line == eh.value.line, text
+    g = tc.load_matrix_market(b"%%MatrixMarket matrix coordinate\n3 3 3\n1 2\n2 3\n3 1\n% end\n")
+    assert tc.count_triangles(g).count == 1
+    g0 = tc.load_matrix_market(b"%%MatrixMarket matrix coordinate\n4 4 0\n% nothing\n")
+    assert g0.num_vertices() == 4 and g0.num_edges() == 0 and tc.count_triangles(g0).count == 0
