@@ -20,6 +20,7 @@
  *                              count_final_level :204-245)
  * tc_parse_matrix_market      trimatch::parse_matrix_market io.hpp:34 (io.cpp:93-159)
  * tc_graph_load_matrix_market trimatch::load_graph (MatrixMarket) io.hpp:45
+ * tc_list_triangles           count_triangles(keep_listings).listings matcher.hpp:92
  * tc_graph_write_csr_cache    trimatch::write_csr_cache  io.hpp:39 (io.cpp:167-177)
  * tc_csr_cache_parse          trimatch::read_csr_cache   io.hpp:40 (io.cpp:187-220)
  * tc_graph_destroy            ~Graph
@@ -153,6 +154,13 @@ tc_status tc_parse_matrix_market(const char* text, uint64_t len, uint32_t** pair
 /* TRIMCSR1 binary cache (io.cpp:18-19, :167-220) held in memory: validates
  * and builds a handle straight from the CSR (no sort). */
 tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_graph** out);
+
+/* count_triangles(keep_listings = true) listings (matcher.hpp:92,
+ * matcher.cpp:169-181): every triangle once as 3 u32 vertex ids in ascending
+ * order (the reference's u < w < x).  Writes min(T, capacity) rows to rows
+ * (host or device, 3*capacity u32) and T to *count; capacity 0 sizes the
+ * buffer.  Row order is unspecified. */
+tc_status tc_list_triangles(tc_graph* g, uint32_t* rows, uint64_t capacity, uint64_t* count);
 
 /* load_graph for MatrixMarket text (io.cpp:222-228 -> parse_matrix_market
  * io.cpp:93-159 -> build_graph graph.cpp:33-85) held in memory: the banner and

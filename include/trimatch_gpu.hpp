@@ -36,6 +36,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <array>
 #include <vector>
 
 #include "tcb200.h"
@@ -271,11 +272,13 @@ struct MatchStats {
 struct MatchResult {
   std::uint64_t count = 0;
   std::optional<std::vector<std::uint64_t>> per_vertex;
+  // keep_listings: every triangle once, ids ascending (matcher.hpp:92 rows
+  // u < w < x); row order unspecified
+  std::optional<std::vector<std::array<VertexId, 3>>> listings;
   MatchStats stats;
 };
 
 inline MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}) {
-  if (opts.keep_listings) throw std::runtime_error("keep_listings is not supported on the GPU path");
   tc_count_opts o{};
   o.lookahead = opts.lookahead;
   o.part_index = opts.part_index;
@@ -291,6 +294,14 @@ inline MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}
   r.stats.wedges = st.wedges;
   r.stats.items = st.items;
   r.stats.candidates = st.pivots;
+  if (opts.keep_listings) {
+    std::uint64_t T = 0;
+    detail::check(tc_list_triangles(g.handle(), nullptr, 0, &T));
+    std::vector<std::array<VertexId, 3>> rows(T);
+    std::uint64_t T2 = 0;
+    if (T) detail::check(tc_list_triangles(g.handle(), reinterpret_cast<VertexId*>(rows.data()), T, &T2));
+    r.listings = std::move(rows);
+  }
   return r;
 }
 

@@ -98,6 +98,7 @@ _sig("tc_csr_cache_to_graph", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINT
 _sig("tc_graph_load_matrix_market", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_void_p),
                                               C.c_void_p])
 _sig("tc_graph_csr_cache_size", C.c_int, [C.c_void_p, u64p])
+_sig("tc_list_triangles", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p])
 _sig("tc_graph_write_csr_cache", C.c_int, [C.c_void_p, C.c_void_p])
 _sig("tc_partition_bounds", C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p])
 _sig("tc_gen_num_edges", C.c_uint64, [C.c_int, C.c_int, C.c_int])
@@ -107,7 +108,7 @@ EXPORTED_SYMBOLS = [
     "tc_abi_version", "tc_last_error", "tc_free", "tc_graph_build", "tc_graph_from_csr", "tc_graph_get_info",
     "tc_graph_export_csr", "tc_graph_degrees", "tc_graph_set_stream", "tc_graph_destroy", "tc_count",
     "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate", "tc_partition_bounds",
-    "tc_graph_load_matrix_market", "tc_graph_csr_cache_size", "tc_graph_write_csr_cache",
+    "tc_graph_load_matrix_market", "tc_graph_csr_cache_size", "tc_graph_write_csr_cache", "tc_list_triangles",
 ]
 
 
@@ -196,7 +197,7 @@ class BuildReport:
 @dataclass
 class MatchOptions:
     """matcher.hpp:84-88.  lookahead is validated (0..2) and count-neutral on
-    the GPU path; keep_listings is out of scope (raises Unsupported)."""
+    the GPU path; keep_listings adds MatchResult.listings."""
     lookahead: int = 2
     keep_listings: bool = False
     per_vertex: bool = False
@@ -210,6 +211,7 @@ class MatchResult:
     count: int = 0
     per_vertex: Optional[np.ndarray] = None
     stats: dict = field(default_factory=dict)
+    listings: Optional[np.ndarray] = None  # (T, 3) u32, each row ascending (keep_listings)
 
 
 class Graph:
@@ -345,8 +347,17 @@ def degrees(g: Graph) -> np.ndarray:
 
 
 def count_triangles(g: Graph, opts: Optional[MatchOptions] = None) -> MatchResult:
-    """trimatch::count_triangles (matcher.hpp:128) on the GPU."""
+    """trimatch::count_triangles (matcher.hpp:128) on the GPU.  keep_listings
+    adds the listings (tc_list_triangles): every triangle once, ids ascending."""
     opts = opts or MatchOptions()
+    if opts.keep_listings:
+        if opts.lookahead < 0 or opts.lookahead > 2:
+            raise InvalidArgument("lookahead must be 0, 1, or 2")
+        rows = list_triangles(g)
+        r = count_triangles(g, MatchOptions(lookahead=opts.lookahead, per_vertex=opts.per_vertex,
+                                            part_index=opts.part_index, part_count=opts.part_count))
+        r.listings = rows
+        return r
     o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, 1)
     total = np.zeros(1, np.uint64)
     pv = np.zeros(max(g.num_vertices(), 1), np.uint64) if opts.per_vertex else None
@@ -355,6 +366,17 @@ def count_triangles(g: Graph, opts: Optional[MatchOptions] = None) -> MatchResul
                          C.c_void_p(pv.ctypes.data) if pv is not None else None, C.byref(st)))
     return MatchResult(count=int(total[0]), per_vertex=(pv[: g.num_vertices()] if pv is not None else None),
                        stats=st.as_dict())
+
+
+def list_triangles(g: Graph) -> np.ndarray:
+    """All triangles as a (T, 3) u32 array, each row ascending (the
+    reference's listings rows u < w < x); row order unspecified."""
+    T = C.c_uint64()
+    _check(_lib.tc_list_triangles(g.handle, None, 0, C.byref(T)))
+    rows = np.empty((max(T.value, 1), 3), np.uint32)
+    n2 = C.c_uint64()
+    _check(_lib.tc_list_triangles(g.handle, C.c_void_p(rows.ctypes.data), T.value, C.byref(n2)))
+    return rows[: T.value]
 
 
 def count_triangles_into(g: Graph, total_ptr, per_vertex_ptr=None, opts: Optional[MatchOptions] = None,

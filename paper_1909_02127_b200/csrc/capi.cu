@@ -3,6 +3,7 @@
 // C++ exception crosses the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include <cstdlib>
@@ -378,6 +379,22 @@ tc_status tc_graph_load_matrix_market(const char* text, uint64_t len, int device
     throw;
   }
   *out = g;
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_list_triangles(tc_graph* g, uint32_t* rows, uint64_t capacity, uint64_t* count) {
+  if (!g || !count || (capacity && !rows)) return set_error(TC_EINVAL, "tc_list_triangles: NULL argument");
+  TC_API_TRY
+  DeviceGuard dg(g->device);
+  DevOut<uint32_t> out(capacity ? rows : nullptr, 3 * capacity, g->stream);
+  const uint64_t T = tcb::list_triangles(*g, out.p, capacity);
+  if (capacity) {
+    out.count = 3 * std::min<uint64_t>(T, capacity);
+    out.finish(g->stream);
+  }
+  TC_CUDA(cudaStreamSynchronize(g->stream));
+  *count = T;
   return TC_OK;
   TC_API_CATCH
 }

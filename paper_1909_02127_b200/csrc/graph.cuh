@@ -159,6 +159,10 @@ struct MmHeader;
 bool mm_tokenize(const unsigned char* d_body, uint64_t len, const MmHeader& h, DBuf<uint32_t>& d_pairs,
                  int device, cudaStream_t s);
 
+// Triangle listings (listing.cu): writes min(T, cap) rows (3 u32 ids,
+// ascending) to d_rows, returns T.
+uint64_t list_triangles(tc_graph& g, uint32_t* d_rows, uint64_t cap);
+
 // Generators (gen.cu).
 uint64_t gen_num_edges(int kind, int scale, int param);
 void generate(int kind, int scale, int param, uint32_t* d_pairs, cudaStream_t s);

@@ -53,8 +53,8 @@ def test_errors(tc, cuda_ok):
     g = tc.build_graph(tc.EdgeList(3, np.array([[0, 1], [1, 2], [0, 2]], np.uint32)))
     with pytest.raises(tc.InvalidArgument):
         tc.count_triangles(g, tc.MatchOptions(lookahead=3))
-    with pytest.raises(tc.Unsupported):
-        tc.count_triangles(g, tc.MatchOptions(keep_listings=True))
+    r = tc.count_triangles(g, tc.MatchOptions(keep_listings=True))
+    assert r.count == 1 and r.listings.tolist() == [[0, 1, 2]]
     with pytest.raises(IndexError):
         g.has_edge(0, 3)
     assert g.has_edge(0, 2) and not g.has_edge(0, 0)
@@ -474,3 +474,47 @@ def test_matrix_market_device_errors(tc, cuda_ok):
     assert tc.count_triangles(g).count == 1
     g0 = tc.load_matrix_market(b"%%MatrixMarket matrix coordinate\n4 4 0\n% nothing\n")
     assert g0.num_vertices() == 4 and g0.num_edges() == 0 and tc.count_triangles(g0).count == 0
+
+
+def _check_listings(rows, off, nb, T):
+    """rows = all T triangles exactly once: ascending, distinct, all closed."""
+    assert rows.shape == (T, 3)
+    if T == 0:
+        return
+    assert np.all(rows[:, 0] < rows[:, 1]) and np.all(rows[:, 1] < rows[:, 2])
+    key = (rows[:, 0].astype(np.uint64) << np.uint64(42)) | (rows[:, 1].astype(np.uint64) << np.uint64(21)) | \
+        rows[:, 2].astype(np.uint64)
+    assert np.unique(key).size == T
+
+    def has(a, b):
+        seg = nb[off[a]:off[a + 1]]
+        i = np.searchsorted(seg, b)
+        return i < seg.size and seg[i] == b
+    for a, b, c in rows[:: max(1, T // 2000)]:
+        assert has(a, b) and has(a, c) and has(b, c)
+
+
+def test_listings(tc, oracle, cuda_ok):
+    """keep_listings (matcher.hpp:92): every triangle once, ids ascending --
+    on random G(n,p), an RMAT graph and a clique (all rows checked closed on
+    the small graphs)."""
+    rng = np.random.default_rng(17)
+    for i in range(40):
+        n = int(rng.integers(20, 201))
+        p = (0.02, 0.1, 0.3)[i % 3]
+        iu, ju = np.triu_indices(n, 1)
+        keep = rng.random(iu.size) < p
+        pairs = np.stack([iu[keep], ju[keep]], 1).astype(np.uint32).reshape(-1)
+        off, nb, E, _, _ = oracle.build_graph(pairs, n)
+        T, pv = oracle.count(off, nb, per_vertex=True)
+        r = tc.count_triangles(tc.build_graph_from_pairs(pairs, n), tc.MatchOptions(keep_listings=True))
+        assert r.count == T
+        _check_listings(r.listings, off, nb, T)
+        hist = np.bincount(r.listings.reshape(-1), minlength=n).astype(np.uint64)
+        assert np.array_equal(hist, pv)
+    pairs = tc.generate(tc.GEN_RMAT, 13, 16)
+    off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 13)
+    T, pv = oracle.count(off, nb, per_vertex=True)
+    rows = tc.list_triangles(tc.build_graph_from_pairs(pairs, 1 << 13))
+    _check_listings(rows, off, nb, T)
+    assert np.array_equal(np.bincount(rows.reshape(-1), minlength=1 << 13).astype(np.uint64), pv)
