@@ -431,6 +431,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   __shared__ uint16_t s_hidx[kCtaSegItems], s_cidx[kCtaSegItems];
   __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
   __shared__ uint32_t s_hits, s_cold, s_nl;
+  __shared__ uint32_t s_wl[kJoinWarps];
+  __shared__ unsigned long long s_wc[kJoinWarps];
   __shared__ uint32_t s_desc[6];  // current segment: v, i0, ni, off[v], d+(v), queue index
   __shared__ unsigned long long s_ctot;
   uint32_t* bm = dyn;
@@ -495,11 +497,38 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       }
     }
     // list positions: hot count in the low 16 bits, cold count in the high 16
-    const uint32_t lp = block_exclusive_scan(
-        (uint32_t)((nh[0] > 0) + (nh[1] > 0)) | ((uint32_t)((nc[0] > 0) + (nc[1] > 0)) << 16), &s_nl);
-    // chunk prefixes: hot in the low 32 bits, cold in the high 32
-    const unsigned long long cp = block_exclusive_scan(
-        (unsigned long long)(nh[0] + nh[1]) | ((unsigned long long)(nc[0] + nc[1]) << 32), &s_ctot);
+    // one block scan of the pair (list positions: hot count in the low 16
+    // bits, cold in the high 16; chunk prefixes: hot in the low 32 bits, cold
+    // in the high 32), two barriers
+    uint32_t lp = (uint32_t)((nh[0] > 0) + (nh[1] > 0)) | ((uint32_t)((nc[0] > 0) + (nc[1] > 0)) << 16);
+    unsigned long long cp = (unsigned long long)(nh[0] + nh[1]) | ((unsigned long long)(nc[0] + nc[1]) << 32);
+    {
+      const uint32_t il = warp_inclusive_scan(lp);
+      const unsigned long long ic = warp_inclusive_scan(cp);
+      if (lane == 31) {
+        s_wl[warp] = il;
+        s_wc[warp] = ic;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t xl = lane < kJoinWarps ? s_wl[lane] : 0u;
+        const unsigned long long xc = lane < kJoinWarps ? s_wc[lane] : 0ull;
+        const uint32_t yl = warp_inclusive_scan(xl);
+        const unsigned long long yc = warp_inclusive_scan(xc);
+        if (lane < kJoinWarps) {
+          s_wl[lane] = yl - xl;
+          s_wc[lane] = yc - xc;
+        }
+        if (lane == kJoinWarps - 1) {
+          s_nl = yl;
+          s_ctot = yc;
+        }
+      }
+      __syncthreads();
+      lp = il - lp + s_wl[warp];
+      cp = ic - cp + s_wc[warp];
+      // s_wl/s_wc are rewritten only after the staging barrier below
+    }
     {
       uint32_t ph = lp & 0xffffu, pc = lp >> 16;
       uint32_t ch = (uint32_t)cp, cc = (uint32_t)(cp >> 32);
@@ -584,7 +613,15 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     }
     __syncthreads();
     // (3) clear + per-vertex flush
-    for (uint32_t j = cold + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - h0) >> 5] = 0;
+    // clear the bitmap: whole words by 16-byte stores when the pivot has many
+    // hot members (no global re-read), else the touched words
+    if (dv - cold > nbm / 8) {
+      uint4* bm4 = reinterpret_cast<uint4*>(bm);
+      for (uint32_t i = threadIdx.x; i < nbm / 4; i += kJoinThreads) bm4[i] = make_uint4(0, 0, 0, 0);
+      for (uint32_t i = (nbm & ~3u) + threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
+    } else {
+      for (uint32_t j = cold + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - h0) >> 5] = 0;
+    }
     for (uint32_t j = threadIdx.x; j < ts; j += kJoinThreads) tab[j] = kEmpty;
     if (kPerVertex) {
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
