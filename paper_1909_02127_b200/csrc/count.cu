@@ -641,6 +641,167 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   if (lane == 0 && acc) atomicAdd(total, acc);
 }
 
+// ---- small CTA-bin pivots: one warp each -------------------------------------
+// Pivots with d+ > kWarpMaxDeg but at most kSmallItems in-edge items and
+// kSmallCold members below the hot window (frontier.cu PivotClass 2).  The
+// same staging and walks as k_join_cta, at warp granularity: a warp-private
+// hot bitmap and 256-slot cold hash, warp scans instead of block scans, and
+// no block barriers -- these pivots are 60% of the CTA-bin segments at RMAT
+// s24 but carry 2% of the wedges, so the CTA path's per-segment barriers and
+// latency chain dominated them.
+constexpr int kSmallThreads = 128;
+constexpr int kSmallWarps = kSmallThreads / 32;
+constexpr uint32_t kSmallTable = 256;
+
+struct SmallWarpSmem {
+  uint32_t* bm;
+  uint32_t* tab;
+  uint32_t *hb, *he, *hpre, *cb, *ce, *cpre, *icnt;
+  uint16_t *hidx, *cidx;
+  unsigned long long* hmo;
+  __host__ __device__ static uint32_t bytes(uint32_t nbm) {
+    const uint32_t nb4 = (nbm + 3) & ~3u;
+    // hmo u64[64] | bm[nb4] | tab[256] | hb, he, cb, ce, icnt [64 each] | hpre, cpre [65] | hidx, cidx u16[64]
+    return kSmallItems * 8 + (nb4 + kSmallTable) * 4 + (kSmallItems * 5 + (kSmallItems + 1) * 2) * 4 +
+           kSmallItems * 2 * 2 + 16;
+  }
+  __device__ SmallWarpSmem(uint8_t* base, uint32_t nbm) {
+    const uint32_t nb4 = (nbm + 3) & ~3u;
+    hmo = reinterpret_cast<unsigned long long*>(base);
+    bm = reinterpret_cast<uint32_t*>(base + kSmallItems * 8);
+    tab = bm + nb4;
+    hb = tab + kSmallTable;
+    he = hb + kSmallItems;
+    cb = he + kSmallItems;
+    ce = cb + kSmallItems;
+    icnt = ce + kSmallItems;
+    hpre = icnt + kSmallItems;
+    cpre = hpre + kSmallItems + 1;
+    hidx = reinterpret_cast<uint16_t*>(cpre + kSmallItems + 1);
+    cidx = hidx + kSmallItems;
+  }
+};
+
+template <bool kPerVertex>
+__global__ void __launch_bounds__(kSmallThreads) k_join_small(
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint16_t* __restrict__ colH,
+    const uint4* __restrict__ items, const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue,
+    uint32_t h0, uint32_t nbm, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
+    unsigned long long* __restrict__ total) {
+  extern __shared__ __align__(16) uint8_t dsm_small[];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t wbytes = (SmallWarpSmem::bytes(nbm) + 15) & ~15u;
+  SmallWarpSmem w(dsm_small + warp * wbytes, nbm);
+  for (uint32_t i = lane; i < nbm; i += 32) w.bm[i] = 0;
+  for (uint32_t i = lane; i < kSmallTable; i += 32) w.tab[i] = kEmpty;
+  for (uint32_t i = lane; i < kSmallItems; i += 32) w.icnt[i] = 0;
+  __syncwarp();
+  const uint32_t tmask = kSmallTable - 1, tshift = 32 - 8;  // log2(256) = 8
+  const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, 0};
+  unsigned long long acc = 0;
+  constexpr int S = kPerVertex ? 2 : 1;
+  while (true) {
+    uint32_t q = 0;
+    if (lane == 0) q = atomicAdd(queue, 1u);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= nsegs) break;
+    const uint4 sg = segs[q];
+    const uint32_t v = sg.x, i0 = sg.y, ni = sg.z - sg.y;
+    const uint32_t nb = off[v], dv = off[v + 1] - nb;
+    // (1) members: hot -> bitmap, count the sorted cold prefix
+    uint32_t cold = 0;
+    for (uint32_t j0 = 0; j0 < dv; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t x = j < dv ? col[nb + j] : 0xffffffffu;
+      if (j < dv && x >= h0) atomicOr(&w.bm[(x - h0) >> 5], 1u << ((x - h0) & 31));
+      cold += __popc(__ballot_sync(0xffffffffu, j < dv && x < h0));
+    }
+    for (uint32_t j = lane; j < cold; j += 32) hash_insert(w.tab, tmask, tshift, col[nb + j]);
+    // (2) items (<= 64, two per lane) -> hot / cold lists with chunk prefixes
+    uint4 it[2];
+    uint32_t nh[2], nc[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t i = lane + 32 * r;
+      nh[r] = nc[r] = 0;
+      if (i < ni) {
+        it[r] = __ldcs(items + (uint64_t)(i0 + i) * S);
+        nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
+        nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
+      }
+    }
+    uint32_t ph = 0, pc = 0, ch = 0, cc = 0, nhot = 0, ncold = 0, th = 0, tcc = 0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {  // item lane + 32r: positions after all of round r-1
+      const uint32_t hf = nh[r] > 0, cf = nc[r] > 0;
+      const uint32_t iph = warp_inclusive_scan(hf), ipc = warp_inclusive_scan(cf);
+      const uint32_t ich = warp_inclusive_scan(nh[r]), icc = warp_inclusive_scan(nc[r]);
+      const uint32_t i = lane + 32 * r;
+      ph = nhot + iph - hf;
+      pc = ncold + ipc - cf;
+      ch = th + ich - nh[r];
+      cc = tcc + icc - nc[r];
+      if (hf) {
+        w.hb[ph] = it[r].x;
+        w.he[ph] = it[r].y;
+        w.hpre[ph] = ch;
+        w.hidx[ph] = (uint16_t)i;
+        if (kPerVertex) {
+          const uint4 ex = __ldcs(items + (uint64_t)(i0 + i) * 2 + 1);
+          w.hmo[ph] = (unsigned long long)ex.z | ((unsigned long long)ex.w << 32);
+        }
+      }
+      if (cf) {
+        w.cb[pc] = it[r].z;
+        w.ce[pc] = it[r].w;
+        w.cpre[pc] = cc;
+        w.cidx[pc] = (uint16_t)i;
+      }
+      nhot += __shfl_sync(0xffffffffu, iph, 31);
+      ncold += __shfl_sync(0xffffffffu, ipc, 31);
+      th += __shfl_sync(0xffffffffu, ich, 31);
+      tcc += __shfl_sync(0xffffffffu, icc, 31);
+    }
+    if (lane == 0) {
+      w.hpre[nhot] = th;
+      w.cpre[ncold] = tcc;
+    }
+    __syncwarp();
+    // (3) advance + join
+    uint32_t h = warp_walk<8, kHotWin>(0, th, nhot, w.hpre, w.hb, w.he, w.hidx, nullptr, colH,
+                                       [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t k) {
+                                         const uint32_t m = hot_hit_mask(qq, c, b, e, w.bm);
+                                         if (kPerVertex) masks[w.hmo[k] + (c - (b >> 3))] = (uint8_t)m;
+                                         return (uint32_t)__popc(m);
+                                       });
+    if (ncold)
+      h += warp_walk<4, 2>(0, tcc, ncold, w.cpre, w.cb, w.ce, w.cidx, kPerVertex ? w.icnt : nullptr, col,
+                           [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
+                             return probe_cold<kPerVertex>(qq, c, b, e, w.tab, tmask, tshift, sink);
+                           });
+    acc += h;
+    __syncwarp();
+    if (kPerVertex) {
+      const uint32_t hw = warp_sum(h);
+      if (lane == 0 && hw) atomicAdd(&t_rank[v], (unsigned long long)hw);
+      for (uint32_t i = lane; i < ni; i += 32) {
+        const uint32_t c = w.icnt[i];
+        if (c) {
+          atomicAdd(&t_rank[items[(uint64_t)(i0 + i) * 2 + 1].x], (unsigned long long)c);
+          w.icnt[i] = 0;
+        }
+      }
+    }
+    // (4) clear the touched bitmap words and table slots
+    for (uint32_t j = cold + lane; j < dv; j += 32) w.bm[(col[nb + j] - h0) >> 5] = 0;
+    if (cold)
+      for (uint32_t i = lane; i < kSmallTable; i += 32) w.tab[i] = kEmpty;
+    __syncwarp();
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && acc) atomicAdd(total, acc);
+}
+
 // Per-vertex counts from the CTA bin's hot hit masks.
 // Mask byte (item k, chunk c) has bit j set iff element 8c+j of colH -- an
 // oriented edge u->x -- closed a triangle (u, v_k, x).  For each hot position
@@ -1047,9 +1208,9 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   kl += build_frontier(g, part_e0, part_e1, pv, fr);
   const uint4* wsegs = fr.wsegs;
   const uint4* csegs = fr.csegs;
-  const uint64_t NSW = fr.nw, NSC = fr.nc;
+  const uint64_t NSW = fr.nw, NSC = fr.nc, NSS = fr.ns;
   uint8_t* masks = nullptr;
-  if (pv && NSC) {
+  if (pv && (NSC || NSS)) {
     // hot hit masks of the CTA bin; warp-bin items' bytes stay zero
     masks = g.scratch[kSlotMasks].get<uint8_t>(fr.mask_bytes + 32, s);
     TC_CUDA(cudaMemsetAsync(masks, 0, fr.mask_bytes + 32, s));
@@ -1086,6 +1247,23 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
     pl.mark("join_warp");
   }
+  if (NSS) {
+    DBuf<unsigned int> squeue(1, s);
+    TC_CUDA(cudaMemsetAsync(squeue.get(), 0, sizeof(unsigned int), s));
+    const uint32_t nbm = (n - g.h0 + 31) / 32;
+    const size_t ssm = (size_t)kSmallWarps * ((SmallWarpSmem::bytes(nbm) + 15) & ~15u);
+    auto kern = pv ? k_join_small<true> : k_join_small<false>;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    int occ = 0;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSmallThreads, ssm));
+    const unsigned grid =
+        (unsigned)std::min<uint64_t>((uint64_t)sms * std::max(occ, 1), ceil_div64(NSS, kSmallWarps));
+    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.colH.get(), fr.items, fr.ssegs, (uint32_t)NSS,
+                                         squeue.get(), g.h0, nbm, masks, t_rank, acc.get());
+    TC_LAUNCH();
+    ++launches;
+    pl.mark("join_small");
+  }
   if (NSC) {
     DBuf<unsigned int> queue(1, s);
     TC_CUDA(cudaMemsetAsync(queue.get(), 0, sizeof(unsigned int), s));
@@ -1109,7 +1287,9 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_LAUNCH();
     ++launches;
     pl.mark("join_cta");
-    if (pv) {
+  }
+  if (pv && (NSC || NSS)) {
+    {
       // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics)
       DBuf<unsigned int> rq(3, s);  // -, heavy queue, heavy count
       DBuf<unsigned long long> lq(1, s);  // light row queue
@@ -1155,7 +1335,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     stats->total_ms = ev.ms(0, 3);
     stats->items = fr.nitems;
     stats->wedges = fr.J;
-    stats->segments = NSW + NSC;
+    stats->segments = NSW + NSC + NSS;
     stats->join_launches = launches;
     stats->dag_W = (double)fr.W;
     stats->pivots = fr.pivots;

@@ -191,28 +191,39 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
   }
 }
 
-struct SegCountBin {
+// Pivot class: 0 = warp bin (d+ <= kWarpMaxDeg), 1 = CTA bin, 2 = small CTA
+// pivots (<= kSmallItems items and <= kSmallCold members below the hot
+// window: one warp each, k_join_small), -1 = no work.
+struct PivotClass {
   const uint32_t* off;
+  const uint32_t* offH;
   const uint32_t* in;
-  bool warp_bin;
-  uint32_t per;
-  __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
+  __device__ __forceinline__ int operator()(uint64_t v) const {
     const uint32_t dv = off[v + 1] - off[v];
-    if (dv == 0 || (dv <= kWarpMaxDeg) != warp_bin) return 0;
-    return (in[v + 1] - in[v] + per - 1) / per;
+    if (dv == 0 || in[v + 1] == in[v]) return -1;
+    if (dv <= kWarpMaxDeg) return 0;
+    const uint32_t items = in[v + 1] - in[v], hv = offH[v + 1] - offH[v];
+    return (items <= kSmallItems && dv - hv <= kSmallCold) ? 2 : 1;
   }
 };
 
-__global__ void k_fr_segs(const uint32_t* __restrict__ off, const uint32_t* __restrict__ in, uint32_t n,
-                          bool warp_bin, uint32_t per, const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
-                          unsigned long long* __restrict__ npivots) {
+struct SegCountBin {
+  PivotClass pc;
+  int cls;
+  uint32_t per;
+  __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
+    if (pc(v) != cls) return 0;
+    return (pc.in[v + 1] - pc.in[v] + per - 1) / per;
+  }
+};
+
+__global__ void k_fr_segs(PivotClass pc, uint32_t n, int cls, uint32_t per, const uint32_t* __restrict__ seg_off,
+                          uint4* __restrict__ segs, unsigned long long* __restrict__ npivots) {
   unsigned long long np = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t dv = off[v + 1] - off[v];
-    if (dv == 0 || (dv <= kWarpMaxDeg) != warp_bin) continue;
-    const uint32_t a = in[v], b = in[v + 1];
-    if (b <= a) continue;
+    if (pc(v) != cls) continue;
+    const uint32_t a = pc.in[v], b = pc.in[v + 1];
     uint32_t s = seg_off[v];
     for (uint32_t i = a; i < b; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, b), 0);
     ++np;
@@ -282,28 +293,30 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   pl.mark("fr_scatter");
   // per-bin work segments
   {
-    uint32_t* woff = g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s);
-    uint32_t* coff = g.scratch[kSlotCoff].get<uint32_t>((uint64_t)nn + 1, s);
-    DBuf<uint32_t> tot(2, s);
+    const PivotClass pc{g.off.get(), g.offH.get(), fr.in};
+    uint32_t* segoff[3] = {g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s),
+                           g.scratch[kSlotCoff].get<uint32_t>((uint64_t)nn + 1, s),
+                           g.scratch[kSlotSoff].get<uint32_t>((uint64_t)nn + 1, s)};
+    const uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
+    DBuf<uint32_t> tot(3, s);
     DBuf<unsigned long long> np(1, s);
     TC_CUDA(cudaMemsetAsync(np.get(), 0, sizeof(unsigned long long), s));
-    kl += scan_exclusive<uint32_t>(SegCountBin{g.off.get(), fr.in, true, kWarpSegItems}, woff, n, tot.get(), s);
-    kl += scan_exclusive<uint32_t>(SegCountBin{g.off.get(), fr.in, false, kCtaSegItems}, coff, n, tot.get() + 1, s);
-    uint32_t h[2] = {0, 0};
-    TC_CUDA(cudaMemcpyAsync(h, tot.get(), 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    for (int c = 0; c < 3; ++c)
+      kl += scan_exclusive<uint32_t>(SegCountBin{pc, c, per[c]}, segoff[c], n, tot.get() + c, s);
+    uint32_t h[3] = {0, 0, 0};
+    TC_CUDA(cudaMemcpyAsync(h, tot.get(), 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     fr.nw = n ? h[0] : 0;
     fr.nc = n ? h[1] : 0;
+    fr.ns = n ? h[2] : 0;
     fr.wsegs = g.scratch[kSlotWsegs].get<uint4>(fr.nw, s);
     fr.csegs = g.scratch[kSlotCsegs].get<uint4>(fr.nc, s);
-    if (fr.nw) {
-      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), fr.in, n, true, kWarpSegItems, woff, fr.wsegs, np.get());
-      TC_LAUNCH();
-      ++kl;
-    }
-    if (fr.nc) {
-      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), fr.in, n, false, kCtaSegItems, coff, fr.csegs,
-                                               np.get());
+    fr.ssegs = g.scratch[kSlotSsegs].get<uint4>(fr.ns, s);
+    uint4* segs[3] = {fr.wsegs, fr.csegs, fr.ssegs};
+    const uint64_t cnt[3] = {fr.nw, fr.nc, fr.ns};
+    for (int c = 0; c < 3; ++c) {
+      if (!cnt[c]) continue;
+      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, c, per[c], segoff[c], segs[c], np.get());
       TC_LAUNCH();
       ++kl;
     }

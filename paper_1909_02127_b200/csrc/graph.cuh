@@ -39,7 +39,7 @@ struct Scratch {
 };
 enum ScratchSlot {
   kSlotCnt, kSlotIn, kSlotItems, kSlotRowBase, kSlotWoff, kSlotCoff, kSlotWsegs,
-  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotCount
+  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotSoff, kSlotSsegs, kSlotCount
 };
 }  // namespace tcb
 
@@ -74,6 +74,11 @@ constexpr uint32_t kHotBits = 1u << 16;
 constexpr uint32_t kWarpMaxDeg = 48;    // warp bin: d+(v) <= 48 (128-slot warp table)
 constexpr uint32_t kWarpSegItems = 64;  // items per warp-bin segment
 constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
+// small CTA-bin pivots (d+ > kWarpMaxDeg but few in-edge items and few
+// members below the hot window) are joined one warp each: at RMAT s24 they
+// are 60% of the CTA-bin segments and 2% of the candidate wedges
+constexpr uint32_t kSmallItems = 64;
+constexpr uint32_t kSmallCold = 128;
 
 // Level-1 frontier of one count (frontier.cu): the useful in-edges u->v of
 // every pivot v (d+(v) > 0, non-empty suffix) in the part's oriented-edge
@@ -92,14 +97,15 @@ constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
 //   in[v]      = first item of pivot v (n+1)
 //   rowbase[u-u_lo] = per-vertex only: first mask byte of row u (rows
 //                [u_lo, u_hi] of the part)
-//   wsegs / csegs = {v, i0, i1, 0} work segments per bin
+//   wsegs / csegs / ssegs = {v, i0, i1, 0} work segments per bin
 struct Frontier {
   uint4* items = nullptr;
   uint32_t* in = nullptr;
   uint64_t* rowbase = nullptr;
   uint4* wsegs = nullptr;
   uint4* csegs = nullptr;
-  uint64_t e0 = 0, e1 = 0, nitems = 0, nw = 0, nc = 0, pivots = 0, mask_bytes = 0;
+  uint4* ssegs = nullptr;  // small CTA-bin pivots, one segment each (k_join_small)
+  uint64_t e0 = 0, e1 = 0, nitems = 0, nw = 0, nc = 0, ns = 0, pivots = 0, mask_bytes = 0;
   uint32_t u_lo = 0, u_hi = 0;  // rows the part's edges come from (inclusive)
   uint64_t W = 0, J = 0, hot = 0, items_c = 0;
 };
