@@ -651,7 +651,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
 // latency chain dominated them.
 constexpr int kSmallThreads = 128;
 constexpr int kSmallWarps = kSmallThreads / 32;
-constexpr uint32_t kSmallTable = 256;
+constexpr uint32_t kSmallTable = 2 * kSmallCold;
+constexpr int kSmallR = kSmallItems / 32;  // items per lane
 
 struct SmallWarpSmem {
   uint32_t* bm;
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
   for (uint32_t i = lane; i < kSmallTable; i += 32) w.tab[i] = kEmpty;
   for (uint32_t i = lane; i < kSmallItems; i += 32) w.icnt[i] = 0;
   __syncwarp();
-  const uint32_t tmask = kSmallTable - 1, tshift = 32 - 8;  // log2(256) = 8
+  const uint32_t tmask = kSmallTable - 1, tshift = __clz(kSmallTable) + 1;  // 32 - log2(kSmallTable)
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, 0};
   unsigned long long acc = 0;
   constexpr int S = kPerVertex ? 2 : 1;
@@ -717,11 +718,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
       cold += __popc(__ballot_sync(0xffffffffu, j < dv && x < h0));
     }
     for (uint32_t j = lane; j < cold; j += 32) hash_insert(w.tab, tmask, tshift, col[nb + j]);
-    // (2) items (<= 64, two per lane) -> hot / cold lists with chunk prefixes
-    uint4 it[2];
-    uint32_t nh[2], nc[2];
+    // (2) items (<= kSmallItems, kSmallR per lane) -> hot / cold lists with chunk prefixes
+    uint4 it[kSmallR];
+    uint32_t nh[kSmallR], nc[kSmallR];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < kSmallR; ++r) {
       const uint32_t i = lane + 32 * r;
       nh[r] = nc[r] = 0;
       if (i < ni) {
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
     }
     uint32_t ph = 0, pc = 0, ch = 0, cc = 0, nhot = 0, ncold = 0, th = 0, tcc = 0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {  // item lane + 32r: positions after all of round r-1
+    for (int r = 0; r < kSmallR; ++r) {  // item lane + 32r: positions after all of round r-1
       const uint32_t hf = nh[r] > 0, cf = nc[r] > 0;
       const uint32_t iph = warp_inclusive_scan(hf), ipc = warp_inclusive_scan(cf);
       const uint32_t ich = warp_inclusive_scan(nh[r]), icc = warp_inclusive_scan(nc[r]);

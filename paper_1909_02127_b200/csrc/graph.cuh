@@ -77,8 +77,14 @@ constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
 // small CTA-bin pivots (d+ > kWarpMaxDeg but few in-edge items and few
 // members below the hot window) are joined one warp each: at RMAT s24 they
 // are 60% of the CTA-bin segments and 2% of the candidate wedges
-constexpr uint32_t kSmallItems = 64;
-constexpr uint32_t kSmallCold = 128;
+#ifndef TCB_SMALL_ITEMS
+#define TCB_SMALL_ITEMS 32
+#endif
+#ifndef TCB_SMALL_COLD
+#define TCB_SMALL_COLD 256
+#endif
+constexpr uint32_t kSmallItems = TCB_SMALL_ITEMS;  // multiple of 32
+constexpr uint32_t kSmallCold = TCB_SMALL_COLD;    // power of two
 
 // Level-1 frontier of one count (frontier.cu): the useful in-edges u->v of
 // every pivot v (d+(v) > 0, non-empty suffix) in the part's oriented-edge
