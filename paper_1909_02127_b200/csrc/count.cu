@@ -912,20 +912,33 @@ __device__ __forceinline__ void row_accumulate(const RowRel& rr, const uint8_t* 
       for (int t = 0; t < kRowU; ++t) add(bits[t]);
       nacc += kRowU;
     }
+    // items k >= c0: the first chunk cs_k = (o7 + k + 1 - c0) >> 3 steps every
+    // 8 items, so within an aligned block of 8 items the byte addresses are
+    // an arithmetic sequence (stride C - cs) under one predicate
     const uint32_t kaB = max(ka, rr.c0);
     uint32_t PB = rr.P(kaB);
-    for (uint32_t k0 = kaB; k0 < kb; k0 += kRowU) {
-      uint32_t bits[kRowU];
+    uint32_t k0 = kaB;
+    for (; k0 < kb && ((rr.o7 + k0 + 1 - rr.c0) & 7); ++k0) {  // head up to a block boundary
+      const uint32_t cs = (rr.o7 + (k0 + 1 - rr.c0)) >> 3;
+      const uint32_t b = (cvalid && cr >= cs) ? rowm[PB + cr - cs] : 0u;
+      PB += rr.C - cs;
+      if (nacc + 1 > 255) fold();
+      add(b);
+      ++nacc;
+    }
+    for (; k0 < kb; k0 += 8) {
+      const uint32_t cs = (rr.o7 + (k0 + 1 - rr.c0)) >> 3;  // same for k0..k0+7
+      const uint32_t stride = rr.C - cs;
+      const bool ok = cvalid && cr >= cs;
+      const uint32_t a0 = PB + cr - cs;
+      uint32_t bits[8];
 #pragma unroll
-      for (int t = 0; t < kRowU; ++t) {
-        const uint32_t cs = (rr.o7 + (k0 + t + 1 - rr.c0)) >> 3;
-        bits[t] = (k0 + t < kb && cvalid && cr >= cs) ? rowm[PB + cr - cs] : 0u;
-        PB += rr.C - cs;
-      }
-      if (nacc + kRowU > 255) fold();
+      for (int t = 0; t < 8; ++t) bits[t] = (ok && k0 + t < kb) ? rowm[a0 + t * stride] : 0u;
+      PB += 8 * stride;
+      if (nacc + 8 > 255) fold();
 #pragma unroll
-      for (int t = 0; t < kRowU; ++t) add(bits[t]);
-      nacc += kRowU;
+      for (int t = 0; t < 8; ++t) add(bits[t]);
+      nacc += 8;
     }
   } else {
     for (uint32_t k0 = ka; k0 < kb; k0 += rl.G * kRowU) {
