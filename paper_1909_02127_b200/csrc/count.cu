@@ -1223,12 +1223,9 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const uint4* wsegs = fr.wsegs;
   const uint4* csegs = fr.csegs;
   const uint64_t NSW = fr.nw, NSC = fr.nc, NSS = fr.ns;
-  uint8_t* masks = nullptr;
-  if (pv && (NSC || NSS)) {
-    // hot hit masks of the CTA bin; warp-bin items' bytes stay zero
-    masks = g.scratch[kSlotMasks].get<uint8_t>(fr.mask_bytes + 32, s);
-    TC_CUDA(cudaMemsetAsync(masks, 0, fr.mask_bytes + 32, s));
-  }
+  // hot hit masks of the CTA and small bins (the frontier zeroed the bytes of
+  // every other item)
+  uint8_t* masks = pv ? fr.masks : nullptr;
   pl.mark("frontier");
   TC_CUDA(cudaEventRecord(ev.e[1], s));
 

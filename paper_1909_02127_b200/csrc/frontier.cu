@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
                                                   const uint32_t* __restrict__ in, uint32_t* __restrict__ cursor,
                                                   uint4* __restrict__ items,
                                                   const uint64_t* __restrict__ rowbase, uint32_t u_lo,
+                                                  uint8_t* __restrict__ masks,
                                                   Sums* __restrict__ sums) {
   unsigned long long W = 0, J = 0, H = 0, IC = 0;
   for (uint64_t base = e0 + (uint64_t)blockIdx.x * (kT * kScatterR); base < e1;
@@ -162,6 +163,16 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
 #pragma unroll
     for (int r = 0; r < kScatterR; ++r) {
       W += q[r].dv;
+      // per-vertex: the mask bytes of items the CTA/small-bin joins will not
+      // write (warp-bin pivots, pivots with d+ = 0) are zeroed here, so the
+      // mask buffer needs no memset
+      if (kPV && base + r * kT + threadIdx.x < e1 && (!q[r].claim || q[r].dv <= kWarpMaxDeg) && q[r].h > 0 &&
+          q[r].k + 1 < q[r].d) {
+        const RowMasks rm(q[r].d, q[r].O, q[r].h);
+        uint8_t* z = masks + rowbase[q[r].u - u_lo] + rm.P(q[r].k);
+        const uint32_t nb = (uint32_t)(rm.c_hi - rm.first_chunk(q[r].k));
+        for (uint32_t i = 0; i < nb; ++i) z[i] = 0;
+      }
       if (!q[r].claim) continue;
       constexpr int S = kPV ? 2 : 1;  // uint4s per item record
       uint64_t mo = 0;
@@ -277,16 +288,17 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get(), fr.u_lo}, fr.rowbase, rows, fr.rowbase + rows,
                                    s);
     fr.mask_bytes = read_scalar(fr.rowbase + rows, s);
+    fr.masks = g.scratch[kSlotMasks].get<uint8_t>(fr.mask_bytes + 32, s);
   }
   pl.mark("fr_rowbase");
   if (NI) {
     const unsigned grid = grid_gs(ceil_div64(e1 - e0, kScatterR), dev);
     if (per_vertex)
       k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.rowbase,
-                                             fr.u_lo, sums.get());
+                                             fr.u_lo, fr.masks, sums.get());
     else
       k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, nullptr, 0,
-                                              sums.get());
+                                              nullptr, sums.get());
     TC_LAUNCH();
     ++kl;
   }

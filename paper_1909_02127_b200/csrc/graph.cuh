@@ -108,6 +108,7 @@ struct Frontier {
   uint4* items = nullptr;
   uint32_t* in = nullptr;
   uint64_t* rowbase = nullptr;
+  uint8_t* masks = nullptr;  // per-vertex hit masks (mask_bytes), written by the joins
   uint4* wsegs = nullptr;
   uint4* csegs = nullptr;
   uint4* ssegs = nullptr;  // small CTA-bin pivots, one segment each (k_join_small)
