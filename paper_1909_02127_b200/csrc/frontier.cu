@@ -178,8 +178,15 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
       uint64_t mo = 0;
       if (kPV && q[r].useful && q[r].dv > kWarpMaxDeg && q[r].it.y > q[r].it.x)
         mo = rowbase[q[r].u - u_lo] + RowMasks(q[r].d, q[r].O, q[r].h).P(q[r].k);
-      items[(uint64_t)pos[r] * S] = q[r].it;
-      if (kPV) items[(uint64_t)pos[r] * S + 1] = make_uint4(q[r].u, 0u, (uint32_t)mo, (uint32_t)(mo >> 32));
+      if (kPV) {  // the 32-byte record as one 256-bit store (one full L2 sector)
+        const uint4 a = q[r].it;
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(items + (uint64_t)pos[r] * 2),
+                     "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(q[r].u), "r"(0u), "r"((uint32_t)mo),
+                     "r"((uint32_t)(mo >> 32))
+                     : "memory");
+      } else {
+        items[pos[r]] = q[r].it;
+      }
       if (!q[r].useful) continue;
       if (q[r].dv <= kWarpMaxDeg) {
         J += q[r].it.y - q[r].it.x;
