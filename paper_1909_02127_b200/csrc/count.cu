@@ -309,7 +309,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
     const uint32_t my = ib + lane;
     uint32_t b = 0, e = 0, nch = 0;
     if (my < i1) {
-      const uint2 it = __ldcs(reinterpret_cast<const uint2*>(items + (uint64_t)my * (kPerVertex ? 2 : 1)));
+      const uint2 it = __ldcs(reinterpret_cast<const uint2*>(items + (uint64_t)my * (kPerVertex ? 2 : kItemStrideTotal)));
       b = it.x;
       e = it.y;
       nch = ((e + 3) >> 2) - (b >> 2);
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       const uint32_t i = threadIdx.x * 2 + r;
       nh[r] = nc[r] = 0;
       if (i < ni) {
-        it[r] = __ldcs(items + (uint64_t)(i0 + i) * (kPerVertex ? 2 : 1));
+        it[r] = __ldcs(items + (uint64_t)(i0 + i) * (kPerVertex ? 2 : kItemStrideTotal));
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
   const uint32_t tmask = kSmallTable - 1, tshift = __clz(kSmallTable) + 1;  // 32 - log2(kSmallTable)
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, 0};
   unsigned long long acc = 0;
-  constexpr int S = kPerVertex ? 2 : 1;
+  constexpr int S = kPerVertex ? 2 : kItemStrideTotal;
   while (true) {
     uint32_t q = 0;
     if (lane == 0) q = atomicAdd(queue, 1u);

@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
         for (uint32_t i = 0; i < nb; ++i) z[i] = 0;
       }
       if (!q[r].claim) continue;
-      constexpr int S = kPV ? 2 : 1;  // uint4s per item record
+      constexpr int S = kPV ? 2 : kItemStrideTotal;  // uint4s per item record
       uint64_t mo = 0;
       if (kPV && q[r].useful && q[r].dv > kWarpMaxDeg && q[r].it.y > q[r].it.x)
         mo = rowbase[q[r].u - u_lo] + RowMasks(q[r].d, q[r].O, q[r].h).P(q[r].k);
@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
         asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(items + (uint64_t)pos[r] * 2),
                      "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(q[r].u), "r"(0u), "r"((uint32_t)mo),
                      "r"((uint32_t)(mo >> 32))
+                     : "memory");
+      } else if (S == 2) {  // total-only records padded to a full 32-byte sector
+        const uint4 a = q[r].it;
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(items + (uint64_t)pos[r] * 2),
+                     "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
                      : "memory");
       } else {
         items[pos[r]] = q[r].it;
@@ -282,7 +287,7 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   pl.mark("fr_slots");
   const uint64_t NI = n ? read_scalar(fr.in + n, s) : 0;
   fr.nitems = NI;
-  fr.items = g.scratch[kSlotItems].get<uint4>(NI * (per_vertex ? 2 : 1), s);
+  fr.items = g.scratch[kSlotItems].get<uint4>(NI * (per_vertex ? 2 : kItemStrideTotal), s);
   // per-vertex: the rows the part's edges come from and their mask blocks
   fr.mask_bytes = 0;
   fr.u_lo = 0;

@@ -74,6 +74,12 @@ constexpr uint32_t kHotBits = 1u << 16;
 constexpr uint32_t kWarpMaxDeg = 48;    // warp bin: d+(v) <= 48 (128-slot warp table)
 constexpr uint32_t kWarpSegItems = 64;  // items per warp-bin segment
 constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
+#ifndef TCB_ITEM_STRIDE_TOTAL
+#define TCB_ITEM_STRIDE_TOTAL 1
+#endif
+// uint4s per level-1 item record without per-vertex counts (A/B: padding the
+// 16-byte record to a full 32-byte sector is slower, 10.2 vs 9.6 ms at C4)
+constexpr int kItemStrideTotal = TCB_ITEM_STRIDE_TOTAL;
 // small CTA-bin pivots (d+ > kWarpMaxDeg but few in-edge items and few
 // members below the hot window) are joined one warp each: at RMAT s24 they
 // are 60% of the CTA-bin segments and 2% of the candidate wedges
