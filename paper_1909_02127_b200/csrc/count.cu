@@ -962,11 +962,13 @@ __device__ __forceinline__ void row_accumulate(const RowRel& rr, const uint8_t* 
 }
 
 // t[x_p] += cnt for position j of chunk c (global); returns the count added.
-__device__ __forceinline__ uint32_t row_emit1(const RowMasks& rm, const uint4& q, uint64_t c, int j, uint32_t cnt,
-                                              uint32_t h0, uint32_t rc, uint32_t* top,
+// t[x_p] += cnt for position j of the row's relative chunk cr (p = 8*cr + j
+// relative to the row's first chunk; the row's hot ids sit at [o7, o7 + h)).
+__device__ __forceinline__ uint32_t row_emit1(const RowRel& rr, uint32_t h, const uint4& q, uint32_t cr, int j,
+                                              uint32_t cnt, uint32_t h0, uint32_t rc, uint32_t* top,
                                               unsigned long long* __restrict__ t_rank) {
-  const uint64_t p = 8 * c + j;
-  if (!cnt || p < rm.O || p >= rm.O + rm.h) return 0;
+  const uint32_t p = 8 * cr + j;
+  if (!cnt || p < rr.o7 || p >= rr.o7 + h) return 0;
   const uint32_t x = h0 + hot_u16(q, j);
   if (x >= rc) atomicAdd(&top[x - rc], cnt);
   else atomicAdd(&t_rank[x], (unsigned long long)cnt);
@@ -1050,7 +1052,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
           const uint64_t c = rm.c_lo + cr;
           const uint4 q = colH4[c];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) row_total += row_emit1(rm, q, c, j, cnt[j], h0, rc, top, t_rank);
+          for (int j = 0; j < 8; ++j) row_total += row_emit1(rr, rm.h, q, cr, j, cnt[j], h0, rc, top, t_rank);
         }
       }
       row_total = warp_sum(row_total);
@@ -1111,7 +1113,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
         for (int w2 = 0; w2 < kRowWarps; ++w2) t += red[w2][warp][lane];
         if (rl.sub == 0 && cvalid && t) {
           const uint64_t c = rm.c_lo + cr;
-          my_total += row_emit1(rm, colH4[c], c, (int)warp, t, h0, rc, top, t_rank);
+          my_total += row_emit1(rr, rm.h, colH4[c], cr, (int)warp, t, h0, rc, top, t_rank);
         }
       }
       __syncthreads();
