@@ -1,4 +1,5 @@
 """Summarise an ncu report: key SOL/memory/warp metrics + top SASS lines by stall samples."""
+import re
 import csv, subprocess, sys, io
 rep = sys.argv[1]; kern = sys.argv[2] if len(sys.argv) > 2 else ""
 nlines = int(sys.argv[3]) if len(sys.argv) > 3 else 30
@@ -11,7 +12,7 @@ want = {"Duration", "DRAM Throughput", "L2 Cache Throughput", "L1/TEX Cache Thro
         "Warp Cycles Per Issued Instruction", "Eligible Warps Per Scheduler", "Registers Per Thread",
         "Dynamic Shared Memory Per Block", "Grid Size", "Mem Pipes Busy"}
 for x in r[1:]:
-    if kern in x[ki] and x[mi] in want:
+    if re.search(kern, x[ki]) and x[mi] in want:
         print(f"  {x[mi]:45s} {x[vi]:>14s} {x[ui]}")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
@@ -21,7 +22,7 @@ for name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum"
     if name in hh:
         j = hh.index(name)
         for row in rr[2:]:
-            if kern in row[hh.index("Kernel Name")]:
+            if re.search(kern, row[hh.index("Kernel Name")]):
                 print(f"  {name:45s} {row[j]:>14s} {rr[1][j]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern or '.'}"],
                      capture_output=True, text=True).stdout
