@@ -170,36 +170,46 @@ __global__ void k_gather_deg(const uint32_t* __restrict__ deg_r, const uint32_t*
     out[v] = deg_r[rank_of[v]];
 }
 
-struct HotFlag {
-  const uint32_t* col;
-  uint32_t h0;
-  __device__ __forceinline__ uint32_t operator()(uint64_t e) const { return col[e] >= h0 ? 1u : 0u; }
-};
-
-__global__ void k_hot_scatter(const uint32_t* __restrict__ col, uint64_t E, uint32_t h0,
-                              const uint32_t* __restrict__ hp, uint16_t* __restrict__ colH) {
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t x = col[e];
-    if (x >= h0) colH[hp[e]] = (uint16_t)(x - h0);
+// Hot-window mirror of the finished (sorted) rows: a row's hot members are its
+// suffix >= h0, counted by binary search; entry e of row r = src[e] in that
+// suffix lands at offH[r+1] - (off[r+1] - e).
+__global__ void k_hot_counts(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, uint32_t n,
+                             uint32_t h0, uint32_t* __restrict__ hcnt) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {  // 64-bit: n may be 2^32 - 1
+    const uint32_t b = off[u + 1];
+    uint32_t lo = off[u], hi = b;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (col[mid] < h0) lo = mid + 1; else hi = mid;
+    }
+    hcnt[u] = b - lo;
   }
 }
 
-__global__ void k_hot_offsets(const uint32_t* __restrict__ off, uint32_t n, uint64_t E,
-                              const uint32_t* __restrict__ hp, uint32_t total_hot, uint32_t* __restrict__ offH) {
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n;
-       u += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t o = off[u];
-    offH[u] = o < E ? hp[o] : total_hot;
+__global__ void k_hot_scatter(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                              const uint32_t* __restrict__ src, uint64_t E, uint32_t h0,
+                              const uint32_t* __restrict__ offH, uint16_t* __restrict__ colH) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = col[e];
+    if (x >= h0) {
+      const uint32_t r = src[e];
+      colH[offH[r + 1] - (off[r + 1] - (uint32_t)e)] = (uint16_t)(x - h0);
+    }
   }
 }
 
 // ---- CSR route (tc_graph_from_csr): rank-space rows without a global sort ----
-// The input rows are complete adjacency lists, so each id-row u is handled by
-// one warp (a CTA for rows longer than kBigRow): pass 0 counts the entries
-// kept by the orientation, rank(v) > rank(u), into d+(rank u); pass 1 writes
-// them at off[rank u] + their rank among the row's kept entries (ballot
-// prefix, deterministic); then every rank-space row is sorted in place.
+// The input rows are complete adjacency lists.  Before any neighbour arrives,
+// the offsets alone give every vertex its rank and a padded rank-space slot of
+// deg(u) entries (pad_off = scan of deg by rank).  Then ONE pass per id-row u
+// -- a thread (short rows), a warp (<= kBigRow) or a warp per kBigRow chunk
+// (hubs: count, chunk bases, write) -- keeps the entries with rank(v) >
+// rank(u), packs them at the head of u's padded slot (ballot prefix,
+// deterministic) and records d+(rank u).  Rows are independent, so the pass
+// runs chunk by chunk behind the host->device copy of the neighbour array
+// (build_from_csr); the row sorts then move every slot to its final place.
 constexpr uint32_t kBigRow = 1024;
 
 __global__ void k_csr_deg(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ deg,
@@ -223,14 +233,13 @@ struct RowCtx {
   const uint32_t* nbrs;
   const uint32_t* rank_of;
   uint32_t n;
-  uint32_t* dplus;   // pass 0
-  const uint32_t* roff;  // pass 1: rank-space row offsets
-  uint32_t* col;
-  uint32_t* src;
+  uint32_t* dplus;
+  const uint32_t* pad_off;  // padded rank-space slots (deg entries each)
+  uint32_t* pad;
   int strict;  // TRIMCSR1 ingest: also reject self-loops and non-ascending rows (io.cpp:211-216)
 };
 
-// pass-0 validity bits of entry i (row u starting at a): 1 = id out of range,
+// validity bits of entry i (row u starting at a): 1 = id out of range,
 // 2 = (strict) self-loop or not strictly ascending
 __device__ __forceinline__ int entry_bad(const RowCtx& cx, uint64_t i, uint64_t a, uint32_t u, uint32_t v) {
   int bad = v >= cx.n ? 1 : 0;
@@ -239,12 +248,12 @@ __device__ __forceinline__ int entry_bad(const RowCtx& cx, uint64_t i, uint64_t 
 }
 
 // One warp over id-row u; returns (in lane-summed form) the entries v > u.
-template <int kPass>
 __device__ __forceinline__ uint32_t warp_csr_row(const RowCtx& cx, uint32_t u, int& bad) {
   const unsigned lane = lane_id();
   const uint64_t a = cx.off[u], b = cx.off[u + 1];
   const uint32_t ru = cx.rank_of[u];
-  uint32_t run = kPass ? cx.roff[ru] : 0u, upper = 0;
+  uint32_t* out = cx.pad + cx.pad_off[ru];
+  uint32_t run = 0, upper = 0;
   constexpr int kU = 4;
   for (uint64_t i0 = a; i0 < b; i0 += 32 * kU) {
     uint32_t v[kU], rv[kU];
@@ -256,7 +265,7 @@ __device__ __forceinline__ uint32_t warp_csr_row(const RowCtx& cx, uint32_t u, i
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
       const bool valid = i0 + 32 * t + lane < b;
-      if (!kPass && valid) bad |= entry_bad(cx, i0 + 32 * t + lane, a, u, v[t]);
+      if (valid) bad |= entry_bad(cx, i0 + 32 * t + lane, a, u, v[t]);
       rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
       upper += (valid && v[t] > u && v[t] < cx.n) ? 1u : 0u;
     }
@@ -265,23 +274,19 @@ __device__ __forceinline__ uint32_t warp_csr_row(const RowCtx& cx, uint32_t u, i
       const bool valid = i0 + 32 * t + lane < b && v[t] < cx.n;
       const bool keep = valid && rv[t] > ru;
       const uint32_t m = __ballot_sync(0xffffffffu, keep);
-      if (kPass && keep) {
-        const uint32_t pos = run + __popc(m & lanemask_lt());
-        cx.col[pos] = rv[t];
-        cx.src[pos] = ru;
-      }
+      if (keep) out[run + __popc(m & lanemask_lt())] = rv[t];
       run += __popc(m);
     }
   }
-  if (!kPass && lane == 0) cx.dplus[ru] = run;
+  if (lane == 0) cx.dplus[ru] = run;
   return upper;
 }
 
 // One thread over a short id-row u (<= kShortRow entries).
-template <int kPass>
 __device__ __forceinline__ uint32_t thread_csr_row(const RowCtx& cx, uint32_t u, uint64_t a, uint64_t b, int& bad) {
   const uint32_t ru = cx.rank_of[u];
-  uint32_t run = kPass ? cx.roff[ru] : 0u, upper = 0;
+  uint32_t* out = cx.pad + cx.pad_off[ru];
+  uint32_t run = 0, upper = 0;
   for (uint64_t i0 = a; i0 < b; i0 += 4) {
     uint32_t v[4], rv[4];
 #pragma unroll
@@ -289,69 +294,64 @@ __device__ __forceinline__ uint32_t thread_csr_row(const RowCtx& cx, uint32_t u,
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const bool valid = i0 + t < b;
-      if (!kPass && valid) bad |= entry_bad(cx, i0 + t, a, u, v[t]);
+      if (valid) bad |= entry_bad(cx, i0 + t, a, u, v[t]);
       rv[t] = (valid && v[t] < cx.n) ? cx.rank_of[v[t]] : 0u;
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const bool valid = i0 + t < b && v[t] < cx.n;
       upper += (valid && v[t] > u) ? 1u : 0u;
-      if (valid && rv[t] > ru) {
-        if (kPass) {
-          cx.col[run] = rv[t];
-          cx.src[run] = ru;
-        }
-        ++run;
-      }
+      if (valid && rv[t] > ru) out[run++] = rv[t];
     }
   }
-  if (!kPass) cx.dplus[ru] = run;
+  cx.dplus[ru] = run;
   return upper;
 }
 
 constexpr uint32_t kShortRow = 24;
 
-template <int kPass>
-__global__ void __launch_bounds__(256) k_csr_rows(RowCtx cx, unsigned int* __restrict__ queue,
+// Id-rows [lo, hi) of at most kBigRow entries, groups of 32 from a queue (row
+// lengths are skewed): short rows a thread each, the group's longer rows
+// after, one at a time, warp-wide.
+__global__ void __launch_bounds__(256) k_csr_rows(RowCtx cx, uint32_t lo, uint32_t hi,
+                                                 unsigned int* __restrict__ queue,
                                                  unsigned long long* __restrict__ upper_total,
                                                  int* __restrict__ bad_flag) {
   uint32_t upper = 0;
   int bad = 0;
-  // groups of 32 rows from a queue (row lengths are skewed): short rows a
-  // thread each; the group's long rows (<= kBigRow) follow, one at a time,
-  // warp-wide
   while (true) {
-    uint32_t u0 = 0;
-    if (lane_id() == 0) u0 = atomicAdd(queue, 32u);
-    u0 = __shfl_sync(0xffffffffu, u0, 0);
-    if (u0 >= cx.n) break;
+    uint32_t g0 = 0;
+    if (lane_id() == 0) g0 = atomicAdd(queue, 32u);
+    g0 = __shfl_sync(0xffffffffu, g0, 0);
+    if (g0 >= hi - lo) break;
+    const uint32_t u0 = lo + g0;
     const uint32_t u = u0 + lane_id();
+    const bool live = lane_id() < hi - u0;  // (u < hi without wrap-around)
     uint64_t a = 0, b = 0;
-    if (u < cx.n) {
+    if (live) {
       a = cx.off[u];
       b = cx.off[u + 1];
     }
-    const bool is_short = u < cx.n && b - a <= kShortRow;
-    if (is_short) upper += thread_csr_row<kPass>(cx, u, a, b, bad);
-    uint32_t longs = __ballot_sync(0xffffffffu, u < cx.n && !is_short && b - a <= kBigRow);
+    const bool is_short = live && b - a <= kShortRow;
+    if (is_short) upper += thread_csr_row(cx, u, a, b, bad);
+    uint32_t longs = __ballot_sync(0xffffffffu, live && !is_short && b - a <= kBigRow);
     while (longs) {
       const int j = __ffs(longs) - 1;
       longs &= longs - 1;
-      upper += warp_csr_row<kPass>(cx, u0 + j, bad);
+      upper += warp_csr_row(cx, u0 + j, bad);
     }
   }
-  if (!kPass) {
-    const unsigned long long w = warp_sum((unsigned long long)upper);
-    if (lane_id() == 0 && w) atomicAdd(upper_total, w);
-    bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)bad);
-    if (bad && lane_id() == 0) atomicOr(bad_flag, bad);
-  }
+  const unsigned long long w = warp_sum((unsigned long long)upper);
+  if (lane_id() == 0 && w) atomicAdd(upper_total, w);
+  bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)bad);
+  if (bad && lane_id() == 0) atomicOr(bad_flag, bad);
 }
 
 // Rows longer than kBigRow (hubs) are cut into chunks of kBigRow entries,
 // chunk c = {u, first entry}; a warp per chunk.  Pass 0 adds each chunk's kept
 // count to d+(rank u) and records it; k_chunk_bases turns the counts into
-// per-chunk write bases within the row; pass 1 writes.
+// per-chunk write bases within the row; pass 1 writes.  Only chunks of rows in
+// [lo, hi) (the rows whose entries have arrived) are taken.
 struct Chunk {
   uint32_t u, c0;  // row, first chunk of the row in the chunk list
   uint64_t a;      // first entry of the chunk
@@ -359,7 +359,8 @@ struct Chunk {
 
 template <int kPass>
 __global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __restrict__ chunks, uint32_t nchunks,
-                                                    uint32_t* __restrict__ ccount, const uint32_t* __restrict__ cbase,
+                                                    uint32_t lo, uint32_t hi, uint32_t* __restrict__ ccount,
+                                                    const uint32_t* __restrict__ cbase,
                                                     unsigned long long* __restrict__ upper_total,
                                                     int* __restrict__ bad_flag) {
   const unsigned lane = lane_id();
@@ -368,10 +369,12 @@ __global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __re
   int bad = 0;
   for (uint32_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); c < nchunks; c += warps) {
     const Chunk ch = chunks[c];
+    if (ch.u < lo || ch.u >= hi) continue;
     const uint64_t rowend = cx.off[ch.u + 1];
     const uint64_t a = ch.a, b = min(rowend, a + kBigRow);
     const uint32_t ru = cx.rank_of[ch.u];
-    uint32_t run = kPass ? cx.roff[ru] + cbase[c] : 0u, kept = 0;
+    uint32_t* out = cx.pad + cx.pad_off[ru];
+    uint32_t run = kPass ? cbase[c] : 0u, kept = 0;
     for (uint64_t i0 = a; i0 < b; i0 += 128) {
       uint32_t v[4], rv[4];
 #pragma unroll
@@ -390,11 +393,7 @@ __global__ void __launch_bounds__(256) k_csr_chunks(RowCtx cx, const Chunk* __re
       for (int t = 0; t < 4; ++t) {
         const bool keep = i0 + 32 * t + lane < b && v[t] < cx.n && rv[t] > ru;
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
-        if (kPass && keep) {
-          const uint32_t pos = run + __popc(m & lanemask_lt());
-          cx.col[pos] = rv[t];
-          cx.src[pos] = ru;
-        }
+        if (kPass && keep) out[run + __popc(m & lanemask_lt())] = rv[t];
         run += __popc(m);
         kept += __popc(m);
       }
@@ -436,10 +435,10 @@ void kl_scan_chunks(const uint32_t* big, uint32_t nbig, const uint64_t* off, uin
 }
 
 // per big row (thread): exclusive prefix of its chunks' kept counts
-__global__ void k_chunk_bases(const Chunk* __restrict__ chunks, uint32_t nchunks, const uint32_t* __restrict__ ccount,
-                              uint32_t* __restrict__ cbase) {
+__global__ void k_chunk_bases(const Chunk* __restrict__ chunks, uint32_t nchunks, uint32_t lo, uint32_t hi,
+                              const uint32_t* __restrict__ ccount, uint32_t* __restrict__ cbase) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
-    if (chunks[c].c0 != c) continue;  // first chunk of its row
+    if (chunks[c].c0 != c || chunks[c].u < lo || chunks[c].u >= hi) continue;  // first chunk of an arrived row
     uint32_t run = 0;
     for (uint32_t k = c; k < nchunks && chunks[k].u == chunks[c].u; ++k) {
       cbase[k] = run;
@@ -448,9 +447,19 @@ __global__ void k_chunk_bases(const Chunk* __restrict__ chunks, uint32_t nchunks
   }
 }
 
-// Rank-space rows, 32 per warp: rows of <= 16 entries are sorted by their
-// lane (register bitonic network), rows of 17..32 by the warp (shuffle
-// bitonic), longer rows are listed for k_seg_sort_block.
+// Row sorts: every rank-space row r moves from its padded slot pad[pad_off[r],
+// + d+(r)) to its place col[off[r], off[r+1]), sorted, with src = r.  Rows of
+// <= 16 entries are sorted by their lane (register bitonic network), rows of
+// 17..32 by the warp (shuffle bitonic), longer rows are listed for the warp /
+// CTA sorts below.
+struct RowMove {
+  const uint32_t* off;      // final rank-space offsets
+  const uint32_t* pad_off;  // padded slots
+  const uint32_t* pad;
+  uint32_t* col;
+  uint32_t* src;
+};
+
 __device__ __forceinline__ void sort16(uint32_t (&x)[16]) {
 #pragma unroll
   for (int k = 2; k <= 16; k <<= 1) {
@@ -470,26 +479,30 @@ __device__ __forceinline__ void sort16(uint32_t (&x)[16]) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_seg_sort_warp(const uint32_t* __restrict__ off, uint32_t n,
-                                                       uint32_t* __restrict__ col, uint32_t* __restrict__ longrows,
+__global__ void __launch_bounds__(256) k_seg_sort_warp(RowMove mv, uint32_t n, uint32_t* __restrict__ longrows,
                                                        unsigned int* __restrict__ nlong) {
   const unsigned lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint32_t r0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r0 < n; r0 += warps * 32) {
-    const uint32_t r = r0 + lane;
-    uint32_t o = 0, d = 0;
-    if (r < n) {
-      o = off[r];
-      d = off[r + 1] - o;
+  for (uint64_t r00 = (uint64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r00 < n;
+       r00 += (uint64_t)warps * 32) {
+    const uint32_t r0 = (uint32_t)r00, r = r0 + lane;
+    uint32_t o = 0, d = 0, po = 0;
+    if (r00 + lane < n) {
+      o = mv.off[r];
+      d = mv.off[r + 1] - o;
+      po = mv.pad_off[r];
     }
-    if (d >= 2 && d <= 16) {
+    if (d >= 1 && d <= 16) {
       uint32_t x[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? col[o + i] : 0xffffffffu;
-      sort16(x);
+      for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? mv.pad[po + i] : 0xffffffffu;
+      if (d >= 2) sort16(x);
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if ((uint32_t)i < d) col[o + i] = x[i];
+        if ((uint32_t)i < d) {
+          mv.col[o + i] = x[i];
+          mv.src[o + i] = r;
+        }
     }
     if (d > 32) longrows[atomicAdd(nlong, 1u)] = r;
     uint32_t mid = __ballot_sync(0xffffffffu, d > 16 && d <= 32);
@@ -497,7 +510,8 @@ __global__ void __launch_bounds__(256) k_seg_sort_warp(const uint32_t* __restric
       const int j = __ffs(mid) - 1;
       mid &= mid - 1;
       const uint32_t oj = __shfl_sync(0xffffffffu, o, j), dj = __shfl_sync(0xffffffffu, d, j);
-      uint32_t x = lane < dj ? col[oj + lane] : 0xffffffffu;
+      const uint32_t pj = __shfl_sync(0xffffffffu, po, j);
+      uint32_t x = lane < dj ? mv.pad[pj + lane] : 0xffffffffu;
 #pragma unroll
       for (uint32_t k = 2; k <= 32; k <<= 1) {
 #pragma unroll
@@ -507,110 +521,171 @@ __global__ void __launch_bounds__(256) k_seg_sort_warp(const uint32_t* __restric
           x = (lower == asc) ? min(x, y) : max(x, y);
         }
       }
-      if (lane < dj) col[oj + lane] = x;
+      if (lane < dj) {
+        mv.col[oj + lane] = x;
+        mv.src[oj + lane] = r0 + j;
+      }
     }
   }
 }
 
 // Listed rows of 33..1024 entries: a warp each, kE = 2..32 entries per lane
 // in registers (position p = lane*kE + i), bitonic network over 32*kE: in-lane
-// stages for j < kE, shuffles for j >= kE.  Longer rows are re-listed for the
-// CTA sort.
+// stages for j < kE, shuffles for j >= kE.  The row goes through a per-warp
+// SMEM tile (index p + p/32: conflict-free both ways) so that global loads and
+// stores stay coalesced.  Longer rows are re-listed for the CTA sort.
+// In-lane bitonic stage j (< kE) of merge size k over a lane's kE registers.
+template <int kE, int J>
+__device__ __forceinline__ void lane_stage(uint32_t (&x)[kE], uint32_t pb, uint32_t k) {
+  if (J >= kE) return;
+#pragma unroll
+  for (int i = 0; i < kE; ++i) {
+    const int l = i ^ J;
+    if (l > i && l < kE) {
+      const bool asc = ((pb + i) & k) == 0;
+      const uint32_t a = x[i], b = x[l];
+      x[i] = asc ? min(a, b) : max(a, b);
+      x[l] = asc ? max(a, b) : min(a, b);
+    }
+  }
+}
+
 template <int kE>
-__device__ __forceinline__ void warp_sort_row(uint32_t* __restrict__ col, uint32_t o, uint32_t d) {
+__device__ __forceinline__ void warp_sort_row(const RowMove& mv, uint32_t r, uint32_t o, uint32_t d,
+                                              uint32_t* __restrict__ sm) {
   const unsigned lane = lane_id();
+  const uint32_t* in = mv.pad + mv.pad_off[r];
+#pragma unroll
+  for (int m = 0; m < kE; ++m) {
+    const uint32_t t = m * 32 + lane;
+    sm[t + m] = t < d ? in[t] : 0xffffffffu;
+  }
+  __syncwarp();
   uint32_t x[kE];
 #pragma unroll
   for (int i = 0; i < kE; ++i) {
     const uint32_t p = lane * kE + i;
-    x[i] = p < d ? col[o + p] : 0xffffffffu;
+    x[i] = sm[p + (p >> 5)];
   }
+  // Networks up to 256 are fully unrolled; above, k stays a runtime loop (a
+  // fully unrolled network of 1024 is ~20k instructions and the warps stall
+  // on instruction fetch: 4.6 -> 1.4 ms for the 257..1024 rows at C4).
+  const uint32_t pb = lane * kE;
+  if constexpr (kE <= 8) {
 #pragma unroll
-  for (int k = 2; k <= 32 * kE; k <<= 1) {
+    for (uint32_t k = 2; k <= 32u * kE; k <<= 1) {
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= kE) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        if (j >= (uint32_t)kE) {
+          const bool lower = (pb & j) == 0;
 #pragma unroll
-        for (int i = 0; i < kE; ++i) {
-          const uint32_t p = lane * kE + i;
-          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], j / kE);
-          const bool asc = (p & k) == 0, lower = (p & j) == 0;
-          x[i] = (lower == asc) ? min(x[i], y) : max(x[i], y);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < kE; ++i) {
-          const int l = i ^ j;
-          if (l > i) {
-            const uint32_t p = lane * kE + i;
-            const bool asc = (p & k) == 0;
-            const uint32_t a = x[i], b = x[l];
-            x[i] = asc ? min(a, b) : max(a, b);
-            x[l] = asc ? max(a, b) : min(a, b);
+          for (int i = 0; i < kE; ++i) {
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], j / kE);
+            const bool asc = ((pb + i) & k) == 0;
+            x[i] = (lower == asc) ? min(x[i], y) : max(x[i], y);
           }
+        } else if (j == 4) {
+          lane_stage<kE, 4>(x, pb, k);
+        } else if (j == 2) {
+          lane_stage<kE, 2>(x, pb, k);
+        } else {
+          lane_stage<kE, 1>(x, pb, k);
         }
       }
     }
+  } else {
+#pragma unroll 1
+    for (uint32_t k = 2; k <= 32u * kE; k <<= 1) {
+      uint32_t j = k >> 1;
+#pragma unroll 1
+      for (; j >= (uint32_t)kE; j >>= 1) {
+        const bool lower = (pb & j) == 0;  // j >= kE: partner is lane ^ (j / kE)
+#pragma unroll
+        for (int i = 0; i < kE; ++i) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], j / kE);
+          const bool asc = ((pb + i) & k) == 0;
+          x[i] = (lower == asc) ? min(x[i], y) : max(x[i], y);
+        }
+      }
+      if (j == 16) { lane_stage<kE, 16>(x, pb, k); j = 8; }
+      if (j == 8) { lane_stage<kE, 8>(x, pb, k); j = 4; }
+      if (j == 4) { lane_stage<kE, 4>(x, pb, k); j = 2; }
+      if (j == 2) { lane_stage<kE, 2>(x, pb, k); j = 1; }
+      if (j == 1) lane_stage<kE, 1>(x, pb, k);
+    }
   }
+  __syncwarp();
 #pragma unroll
   for (int i = 0; i < kE; ++i) {
     const uint32_t p = lane * kE + i;
-    if (p < d) col[o + p] = x[i];
+    sm[p + (p >> 5)] = x[i];
   }
+  __syncwarp();
+#pragma unroll
+  for (int m = 0; m < kE; ++m) {
+    const uint32_t t = m * 32 + lane;
+    if (t < d) {
+      mv.col[o + t] = sm[t + m];
+      mv.src[o + t] = r;
+    }
+  }
+  __syncwarp();
 }
 
-__global__ void __launch_bounds__(256) k_seg_sort_mid(const uint32_t* __restrict__ off, uint32_t* __restrict__ col,
-                                                      const uint32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256) k_seg_sort_mid(RowMove mv, const uint32_t* __restrict__ rows,
                                                       const unsigned int* __restrict__ nrows,
                                                       uint32_t* __restrict__ longrows,
                                                       unsigned int* __restrict__ nlong) {
+  __shared__ uint32_t tile[8][8 * 33];
+  uint32_t* sm = tile[threadIdx.x >> 5];
   const uint32_t nr = *nrows;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); idx < nr; idx += warps) {
     const uint32_t r = rows[idx];
-    const uint32_t o = off[r], d = off[r + 1] - o;
-    if (d <= 64) warp_sort_row<2>(col, o, d);
-    else if (d <= 128) warp_sort_row<4>(col, o, d);
-    else if (d <= 256) warp_sort_row<8>(col, o, d);
+    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
+    if (d <= 64) warp_sort_row<2>(mv, r, o, d, sm);
+    else if (d <= 128) warp_sort_row<4>(mv, r, o, d, sm);
+    else if (d <= 256) warp_sort_row<8>(mv, r, o, d, sm);
     else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
   }
 }
 
 // Rows of 257..1024 entries (16/32 per lane, its own kernel for the register
 // budget); longer rows are re-listed for the CTA sort.
-__global__ void __launch_bounds__(128) k_seg_sort_mid2(const uint32_t* __restrict__ off, uint32_t* __restrict__ col,
-                                                       const uint32_t* __restrict__ rows,
+__global__ void __launch_bounds__(128) k_seg_sort_mid2(RowMove mv, const uint32_t* __restrict__ rows,
                                                        const unsigned int* __restrict__ nrows,
                                                        uint32_t* __restrict__ longrows,
                                                        unsigned int* __restrict__ nlong) {
+  __shared__ uint32_t tile[4][32 * 33];
+  uint32_t* sm = tile[threadIdx.x >> 5];
   const uint32_t nr = *nrows;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); idx < nr; idx += warps) {
     const uint32_t r = rows[idx];
-    const uint32_t o = off[r], d = off[r + 1] - o;
-    if (d <= 512) warp_sort_row<16>(col, o, d);
-    else if (d <= 1024) warp_sort_row<32>(col, o, d);
+    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
+    if (d <= 512) warp_sort_row<16>(mv, r, o, d, sm);
+    else if (d <= 1024) warp_sort_row<32>(mv, r, o, d, sm);
     else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
   }
 }
 
 // Listed rows: one CTA each, SMEM bitonic sort over the next power of two.
-__global__ void __launch_bounds__(256) k_seg_sort_block(const uint32_t* __restrict__ off, uint32_t* __restrict__ col,
-                                                        const uint32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256) k_seg_sort_block(RowMove mv, const uint32_t* __restrict__ rows,
                                                         const unsigned int* __restrict__ nrows) {
   extern __shared__ uint32_t sk[];
   const uint32_t nr = *nrows;
   for (uint32_t idx = blockIdx.x; idx < nr; idx += gridDim.x) {
     const uint32_t r = rows[idx];
-    const uint32_t o = off[r], d = off[r + 1] - o;
+    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
+    const uint32_t* in = mv.pad + mv.pad_off[r];
     uint32_t P = 64;
     while (P < d) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < d ? col[o + i] : 0xffffffffu;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < d ? in[i] : 0xffffffffu;
     __syncthreads();
     for (uint32_t k = 2; k <= P; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
         for (uint32_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
-          const uint32_t i = (t / j) * 2 * j + (t % j), l = i + j;
+          const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), l = i + j;  // j is a power of two
           const uint32_t xi = sk[i], xl = sk[l];
           if ((xi > xl) == ((i & k) == 0)) {
             sk[i] = xl;
@@ -620,12 +695,28 @@ __global__ void __launch_bounds__(256) k_seg_sort_block(const uint32_t* __restri
         __syncthreads();
       }
     }
-    for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) col[o + i] = sk[i];
+    for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+      mv.col[o + i] = sk[i];
+      mv.src[o + i] = r;
+    }
     __syncthreads();
   }
 }
 
-// fallback for rows longer than the SMEM sort: keys (src<<b | col), sort, split
+// Radix fallback (rows longer than the CTA sort takes): move the slots as-is.
+__global__ void k_move_rows(RowMove mv, uint32_t n) {
+  const unsigned lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint64_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
+    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
+    const uint32_t* in = mv.pad + mv.pad_off[r];
+    for (uint32_t i = lane; i < d; i += 32) {
+      mv.col[o + i] = in[i];
+      mv.src[o + i] = r;
+    }
+  }
+}
+
 __global__ void k_pack_oriented(const uint32_t* __restrict__ src, const uint32_t* __restrict__ col, uint64_t E,
                                 int b, uint64_t* __restrict__ keys) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
@@ -714,19 +805,23 @@ void finish_rows(tc_graph& g) {
   if (hot < 32) hot = 32;
   if (hot > kHotBits) hot = kHotBits;
   g.h0 = n > hot ? n - hot : 0;
-  DBuf<uint32_t> hp(E ? E : 1, s), th(1, s);
-  scan_exclusive<uint32_t>(HotFlag{g.col.get(), g.h0}, hp.get(), E, th.get(), s);
-  const uint32_t total_hot = E ? read_scalar(th.get(), s) : 0;
-  g.colH.alloc((uint64_t)total_hot + 16, s);
-  TC_CUDA(cudaMemsetAsync(g.colH.get(), 0, ((uint64_t)total_hot + 16) * sizeof(uint16_t), s));
   g.offH.alloc((uint64_t)n + 1, s);
+  {
+    DBuf<uint32_t> hcnt(n ? n : 1, s);
+    if (n) {
+      k_hot_counts<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), g.col.get(), n, g.h0, hcnt.get());
+      TC_LAUNCH();
+    }
+    scan_exclusive<uint32_t>(LoadArray<uint32_t>{hcnt.get()}, g.offH.get(), n, g.offH.get() + n, s);
+  }
+  const uint32_t total_hot = n ? read_scalar(g.offH.get() + n, s) : 0;
+  g.colH.alloc((uint64_t)total_hot + 16, s);
+  TC_CUDA(cudaMemsetAsync(g.colH.get() + total_hot, 0, 16 * sizeof(uint16_t), s));
   if (E) {
-    k_hot_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), E, g.h0, hp.get(), g.colH.get());
+    k_hot_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), E, g.h0, g.offH.get(),
+                                                 g.colH.get());
     TC_LAUNCH();
   }
-  k_hot_offsets<<<grid_gs((uint64_t)n + 1, dev), kT, 0, s>>>(g.off.get(), n, E, hp.get(), total_hot,
-                                                             g.offH.get());
-  TC_LAUNCH();
 }
 
 void alloc_rows(tc_graph& g) {
@@ -821,7 +916,7 @@ void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t
 }
 
 void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n, uint64_t num_edges,
-                    bool strict) {
+                    bool strict, const CsrFeed* feed) {
   cudaStream_t s = g.stream;
   const int dev = g.device;
   g.n = n;
@@ -830,12 +925,51 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   if (total >= (1ull << 32)) fail(TC_ERANGE, "CSR with >= 2^32 directed entries");
   if (num_edges >= (1ull << 32)) fail(TC_ERANGE, "graph has >= 2^32 undirected edges (u32 oriented offsets)");
   PhaseLog pl(s);
+  // The neighbour array streams in behind everything that needs only the
+  // offsets: kChunk-entry pieces on a side stream, one event each.
+  const bool stream_in = feed && total;
+  const char* fc = getenv("TCB_FEED_CHUNK");  // tests: many small pieces
+  const uint64_t chunk = fc ? std::max<uint64_t>(1, strtoull(fc, nullptr, 10)) : kFeedChunk;
+  const uint64_t piece = feed && feed->h_off ? chunk : (total ? total : 1);
+  const uint32_t K = stream_in ? (uint32_t)((total + piece - 1) / piece) : 1;
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ev;
+  struct FeedGuard {
+    cudaStream_t& cs;
+    std::vector<cudaEvent_t>& ev;
+    ~FeedGuard() {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+      if (cs) cudaStreamDestroy(cs);
+    }
+  } feed_guard{cs, ev};
+  uint32_t issued = 0;
+  auto issue = [&](uint32_t upto) {  // copies of pieces [issued, upto)
+    for (; issued < upto && issued < K; ++issued) {
+      const uint64_t a = issued * piece, b = std::min(total, a + piece);
+      TC_CUDA(cudaMemcpyAsync(feed->d_dst + a, feed->h_nbrs + a, (b - a) * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, cs));
+      TC_CUDA(cudaEventRecord(ev[issued], cs));
+    }
+  };
+  if (stream_in) {
+    TC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    ev.resize(K);
+    for (auto& e : ev) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t ready;  // the destination was allocated on s
+    TC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    TC_CUDA(cudaEventRecord(ready, s));
+    TC_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+    TC_CUDA(cudaEventDestroy(ready));
+    issue(2);
+  }
   const uint32_t nn = n ? n : 1;
   DBuf<uint32_t> deg(nn, s), big(total / kBigRow + 1, s);
-  DBuf<unsigned int> cnts(4, s);  // big rows, long rank-space rows, row queues (pass 0, 1)
+  DBuf<unsigned int> cnts(2, s);  // big rows / long rank-space rows
+  DBuf<unsigned int> queues(K, s);
   DBuf<int> bad(1, s);
   DBuf<unsigned long long> upper(1, s);
-  TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 4 * sizeof(unsigned int), s));
+  TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
+  TC_CUDA(cudaMemsetAsync(queues.get(), 0, K * sizeof(unsigned int), s));
   TC_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
   TC_CUDA(cudaMemsetAsync(upper.get(), 0, sizeof(unsigned long long), s));
   if (n) {
@@ -863,21 +997,43 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   }
   rank_vertices(g, deg.get());
   deg.release();
-  pl.mark("csr_rank");
+  // padded rank-space slots: deg(u) entries each, by rank
+  DBuf<uint32_t> pad_off((uint64_t)nn + 1, s), pad(total ? total : 1, s);
+  scan_exclusive<uint32_t>(LoadArray<uint32_t>{g.deg.get()}, pad_off.get(), n, pad_off.get() + n, s);
   DBuf<uint32_t> dplus(nn, s);
   TC_CUDA(cudaMemsetAsync(dplus.get(), 0, sizeof(uint32_t) * nn, s));
-  RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), nullptr, nullptr, nullptr, strict ? 1 : 0};
+  pl.mark("csr_rank");
+  RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), pad_off.get(), pad.get(), strict ? 1 : 0};
   const unsigned gw = (unsigned)num_sms(dev) * 8;
-  if (total) {
-    k_csr_rows<0><<<gw, 256, 0, s>>>(cx, cnts.get() + 2, upper.get(), bad.get());
-    TC_LAUNCH();
-    if (nch) {
-      k_csr_chunks<0><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, ccount.get(), cbase.get(), upper.get(), bad.get());
-      TC_LAUNCH();
-      k_chunk_bases<<<ceil_div(nch, 256), 256, 0, s>>>(chunks.get(), nch, ccount.get(), cbase.get());
-      TC_LAUNCH();
+  uint32_t lo = 0;
+  for (uint32_t k = 0; k < K && total; ++k) {
+    // rows whose entries all lie in the first k+1 pieces
+    uint32_t hi = n;
+    if (stream_in && k + 1 < K) {
+      const uint64_t e = (uint64_t)(k + 1) * piece;
+      hi = (uint32_t)(std::upper_bound(feed->h_off, feed->h_off + (uint64_t)n + 1, e) - feed->h_off) - 1;
     }
+    if (stream_in) {
+      issue(k + 3);
+      TC_CUDA(cudaStreamWaitEvent(s, ev[k], 0));
+    }
+    if (hi > lo) {
+      k_csr_rows<<<gw, 256, 0, s>>>(cx, lo, hi, queues.get() + k, upper.get(), bad.get());
+      TC_LAUNCH();
+      if (nch) {
+        k_csr_chunks<0><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, lo, hi, ccount.get(), cbase.get(), upper.get(),
+                                           bad.get());
+        TC_LAUNCH();
+        k_chunk_bases<<<ceil_div(nch, 256), 256, 0, s>>>(chunks.get(), nch, lo, hi, ccount.get(), cbase.get());
+        TC_LAUNCH();
+        k_csr_chunks<1><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, lo, hi, ccount.get(), cbase.get(), upper.get(),
+                                           bad.get());
+        TC_LAUNCH();
+      }
+    }
+    lo = hi;
   }
+  pl.mark("csr_orient");
   const uint64_t E = read_scalar(upper.get(), s);
   const int badv = read_scalar(bad.get(), s);
   if (badv && strict) fail(TC_EPARSE, "corrupt CSR cache adjacency (line 1)");
@@ -888,20 +1044,9 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   row_offsets(g, dplus.get());
   if (n && read_scalar(g.off.get() + n, s) != E)
     fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
-  pl.mark("csr_count");
   if (E) {
-    cx.roff = g.off.get();
-    cx.col = g.col.get();
-    cx.src = g.src.get();
-    TC_CUDA(cudaMemsetAsync(cnts.get() + 3, 0, sizeof(unsigned int), s));
-    k_csr_rows<1><<<gw, 256, 0, s>>>(cx, cnts.get() + 3, upper.get(), bad.get());
-    TC_LAUNCH();
-    if (nch) {
-      k_csr_chunks<1><<<gw, 256, 0, s>>>(cx, chunks.get(), nch, ccount.get(), cbase.get(), upper.get(), bad.get());
-      TC_LAUNCH();
-    }
-    pl.mark("csr_scatter");
-    // sort every rank-space row
+    // every slot -> its sorted place in col (+ src)
+    const RowMove mv{g.off.get(), pad_off.get(), pad.get(), g.col.get(), g.src.get()};
     uint32_t P = 64;
     while (P < g.max_dplus) P <<= 1;
     const char* sm = getenv("TCB_ROWSORT_MAX");  // tests: force the radix fallback on small graphs
@@ -909,24 +1054,25 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     if (P <= sort_max) {
       DBuf<uint32_t> midrows(nn, s), longrows(nn, s);
       TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
-      k_seg_sort_warp<<<gw, 256, 0, s>>>(g.off.get(), n, g.col.get(), midrows.get(), cnts.get());
+      k_seg_sort_warp<<<gw, 256, 0, s>>>(mv, n, midrows.get(), cnts.get());
       TC_LAUNCH();
-      k_seg_sort_mid<<<gw, 256, 0, s>>>(g.off.get(), g.col.get(), midrows.get(), cnts.get(), longrows.get(),
-                                        cnts.get() + 1);
+      pl.mark("csr_sort_le32");
+      k_seg_sort_mid<<<gw, 256, 0, s>>>(mv, midrows.get(), cnts.get(), longrows.get(), cnts.get() + 1);
       TC_LAUNCH();
+      pl.mark("csr_sort_le256");
       // rows of 257..1024: re-listed from longrows into midrows
       TC_CUDA(cudaMemsetAsync(cnts.get(), 0, sizeof(unsigned int), s));
-      k_seg_sort_mid2<<<gw * 2, 128, 0, s>>>(g.off.get(), g.col.get(), longrows.get(), cnts.get() + 1,
-                                             midrows.get(), cnts.get());
+      k_seg_sort_mid2<<<gw * 2, 128, 0, s>>>(mv, longrows.get(), cnts.get() + 1, midrows.get(), cnts.get());
       TC_LAUNCH();
       std::swap(midrows, longrows);  // rows > 1024 are now in longrows, count in cnts[0]
-      TC_CUDA(cudaMemcpyAsync(cnts.get() + 1, cnts.get(), sizeof(unsigned int), cudaMemcpyDeviceToDevice, s));
-      pl.mark("csr_sort_short");
+      pl.mark("csr_sort_le1024");
       const size_t smem = (size_t)P * sizeof(uint32_t);
       TC_CUDA(cudaFuncSetAttribute(k_seg_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_seg_sort_block<<<gw, 256, smem, s>>>(g.off.get(), g.col.get(), longrows.get(), cnts.get() + 1);
+      k_seg_sort_block<<<gw, 256, smem, s>>>(mv, longrows.get(), cnts.get());
       TC_LAUNCH();
     } else {
+      k_move_rows<<<gw, 256, 0, s>>>(mv, n);
+      TC_LAUNCH();
       DBuf<uint64_t> k1(E, s), k2(E, s);
       k_pack_oriented<<<grid_gs(E, dev), kT, 0, s>>>(g.src.get(), g.col.get(), E, g.id_bits, k1.get());
       TC_LAUNCH();
@@ -936,6 +1082,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     }
     pl.mark("csr_row_sort");
   }
+  pad.release();
   finish_rows(g);
   pl.mark("csr_hot_mirror");
 }

@@ -55,6 +55,7 @@ template <typename T>
 struct DevIn {
   const T* p = nullptr;
   tcb::DBuf<T> staged;
+  bool host() const { return staged.get() != nullptr; }
   DevIn(const T* src, uint64_t count, cudaStream_t s) {
     if (count == 0 || is_device_ptr(src)) {
       p = src;
@@ -230,9 +231,17 @@ tc_status from_csr_impl(const uint64_t* row_offsets, const uint32_t* neighbors, 
     Timer t(g->stream);
     tcb::PhaseLog pl(g->stream);
     DevIn<uint64_t> off(row_offsets, (uint64_t)n + 1, g->stream);
-    DevIn<uint32_t> nb(neighbors, 2 * num_edges, g->stream);
-    pl.mark("csr_h2d");
-    tcb::build_from_csr(*g, off.p, nb.p, n, num_edges, strict);
+    const uint64_t total = 2 * num_edges;
+    if (total == 0 || is_device_ptr(neighbors)) {
+      pl.mark("csr_h2d");
+      tcb::build_from_csr(*g, off.p, neighbors, n, num_edges, strict);
+    } else {
+      // host neighbours: streamed in by the build, behind the orientation pass
+      tcb::DBuf<uint32_t> nb(total, g->stream);
+      const tcb::CsrFeed feed{neighbors, off.host() ? row_offsets : nullptr, nb.get()};
+      pl.mark("csr_h2d_offsets");
+      tcb::build_from_csr(*g, off.p, nb.get(), n, num_edges, strict, &feed);
+    }
     g->build_ms = t.stop();
   } catch (...) {
     destroy_handle(g);

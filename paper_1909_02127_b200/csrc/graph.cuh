@@ -161,8 +161,18 @@ void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t
                       tc_build_report* rep);
 // strict: TRIMCSR1 ingest -- reject bad offsets / self-loops / unsorted rows
 // with the reference's ParseError messages (io.cpp:206-218)
+// Host-resident neighbour array for build_from_csr: copied into d_dst (which
+// is then the d_nbrs argument) in kFeedChunk-entry pieces on a side stream
+// while the rows that have arrived are oriented.  h_off (host copy of the
+// offsets, or null = one piece) places the row boundaries.
+constexpr uint64_t kFeedChunk = 1ull << 25;
+struct CsrFeed {
+  const uint32_t* h_nbrs;
+  const uint64_t* h_off;
+  uint32_t* d_dst;
+};
 void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n,
-                    uint64_t num_edges, bool strict = false);
+                    uint64_t num_edges, bool strict = false, const CsrFeed* feed = nullptr);
 void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs);
 void export_degrees(tc_graph& g, uint32_t* d_deg);
 

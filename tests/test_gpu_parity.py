@@ -317,15 +317,18 @@ def _clique_pairs(k, base=0):
     return np.stack([iu + base, ju + base], 1).astype(np.uint32)
 
 
-@pytest.mark.parametrize("rowsort", ["default", "radix_fallback"])
+@pytest.mark.parametrize("rowsort", ["default", "radix_fallback", "streamed"])
 def test_csr_route_paths(tc, oracle, cuda_ok, rowsort):
     """Hub rows longer than one 1024-entry chunk, rank-space rows in every
     sort class (<=16 lane network, 17..32 warp, 33..256, 257..1024, >1024
-    CTA), and the radix fallback; counts, per-vertex counts and the exported
-    CSR must match the edge-list route and the oracle."""
+    CTA), the radix fallback, and the host neighbour array streamed in 4096-
+    entry pieces (rows, hub rows included, span piece boundaries); counts,
+    per-vertex counts and the exported CSR must match the oracle."""
     old = os.environ.get("TCB_ROWSORT_MAX")
     if rowsort == "radix_fallback":
         os.environ["TCB_ROWSORT_MAX"] = "32"
+    if rowsort == "streamed":
+        os.environ["TCB_FEED_CHUNK"] = "4096"
     try:
         rng = np.random.default_rng(11)
         parts = [_clique_pairs(1300), _clique_pairs(300, 1300), _clique_pairs(60, 1600), _clique_pairs(24, 1660)]
@@ -343,6 +346,7 @@ def test_csr_route_paths(tc, oracle, cuda_ok, rowsort):
         assert np.array_equal(ro, off) and np.array_equal(nbr, nb)
         assert np.array_equal(tc.degrees(g), np.diff(off).astype(np.uint32))
     finally:
+        os.environ.pop("TCB_FEED_CHUNK", None)
         if old is None:
             os.environ.pop("TCB_ROWSORT_MAX", None)
         else:
