@@ -21,6 +21,7 @@
  * tc_parse_matrix_market      trimatch::parse_matrix_market io.hpp:34 (io.cpp:93-159)
  * tc_graph_load_matrix_market trimatch::load_graph (MatrixMarket) io.hpp:45
  * tc_list_triangles           count_triangles(keep_listings).listings matcher.hpp:92
+ * tc_list_triangles_range     the same listing streamed by oriented-edge range  matcher.cpp:169-181
  * tc_graph_write_csr_cache    trimatch::write_csr_cache  io.hpp:39 (io.cpp:167-177)
  * tc_csr_cache_parse          trimatch::read_csr_cache   io.hpp:40 (io.cpp:187-220)
  * tc_graph_destroy            ~Graph
@@ -161,6 +162,14 @@ tc_status tc_csr_cache_to_graph(const void* bytes, uint64_t len, int device, tc_
  * (host or device, 3*capacity u32) and T to *count; capacity 0 sizes the
  * buffer.  Row order is unspecified. */
 tc_status tc_list_triangles(tc_graph* g, uint32_t* rows, uint64_t capacity, uint64_t* count);
+
+/* Streamed listings: the triangles listed from the oriented edges
+ * [first_edge, last_edge) of the degree-ordered DAG (each triangle from
+ * exactly one edge, so consecutive ranges partition the listing; 0 <= first
+ * <= last <= num_edges).  Same output contract as tc_list_triangles, so a
+ * caller with a bounded buffer walks the edges range by range. */
+tc_status tc_list_triangles_range(tc_graph* g, uint64_t first_edge, uint64_t last_edge, uint32_t* rows,
+                                  uint64_t capacity, uint64_t* count);
 
 /* load_graph for MatrixMarket text (io.cpp:222-228 -> parse_matrix_market
  * io.cpp:93-159 -> build_graph graph.cpp:33-85) held in memory: the banner and

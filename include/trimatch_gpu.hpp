@@ -305,6 +305,33 @@ inline MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}
   return r;
 }
 
+// Streamed listings: calls sink(const std::array<VertexId, 3>* rows, size_t k)
+// with chunks of at most max_rows triangles whose union is the full listing,
+// walking the oriented edges range by range with one bounded host buffer
+// (tc_list_triangles_range); a range that overflows is halved and re-listed.
+template <typename Sink>
+void for_each_triangle_chunk(Graph& g, Sink&& sink, std::size_t max_rows = std::size_t(1) << 22) {
+  if (max_rows == 0) throw std::invalid_argument("for_each_triangle_chunk: max_rows must be >= 1");
+  std::vector<std::array<VertexId, 3>> buf(max_rows);
+  tc_graph_info info{};
+  detail::check(tc_graph_get_info(g.handle(), &info));
+  const std::uint64_t E = info.num_edges;
+  std::uint64_t e = 0, span = E < (1u << 16) ? (E ? E : 1) : (1u << 16);
+  while (e < E) {
+    const std::uint64_t b = std::min<std::uint64_t>(E, e + span);
+    std::uint64_t T = 0;
+    detail::check(tc_list_triangles_range(g.handle(), e, b, reinterpret_cast<VertexId*>(buf.data()), max_rows, &T));
+    if (T > max_rows) {
+      if (b - e == 1) throw std::invalid_argument("for_each_triangle_chunk: one edge lists more than max_rows");
+      span = std::max<std::uint64_t>(1, (b - e) / 2);
+      continue;
+    }
+    if (T) sink(static_cast<const std::array<VertexId, 3>*>(buf.data()), static_cast<std::size_t>(T));
+    e = b;
+    if (2 * T <= max_rows) span *= 2;
+  }
+}
+
 // Count an existing reference-style graph object (trimatch::Graph or anything
 // exposing the same accessors) without converting it by hand.
 template <typename G>

@@ -99,6 +99,7 @@ _sig("tc_graph_load_matrix_market", C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C
                                               C.c_void_p])
 _sig("tc_graph_csr_cache_size", C.c_int, [C.c_void_p, u64p])
 _sig("tc_list_triangles", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p])
+_sig("tc_list_triangles_range", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, u64p])
 _sig("tc_graph_write_csr_cache", C.c_int, [C.c_void_p, C.c_void_p])
 _sig("tc_partition_bounds", C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p])
 _sig("tc_gen_num_edges", C.c_uint64, [C.c_int, C.c_int, C.c_int])
@@ -109,6 +110,7 @@ EXPORTED_SYMBOLS = [
     "tc_graph_export_csr", "tc_graph_degrees", "tc_graph_set_stream", "tc_graph_destroy", "tc_count",
     "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate", "tc_partition_bounds",
     "tc_graph_load_matrix_market", "tc_graph_csr_cache_size", "tc_graph_write_csr_cache", "tc_list_triangles",
+    "tc_list_triangles_range",
 ]
 
 
@@ -368,15 +370,51 @@ def count_triangles(g: Graph, opts: Optional[MatchOptions] = None) -> MatchResul
                        stats=st.as_dict())
 
 
-def list_triangles(g: Graph) -> np.ndarray:
+def list_triangles(g: Graph, first_edge: int = 0, last_edge: Optional[int] = None) -> np.ndarray:
     """All triangles as a (T, 3) u32 array, each row ascending (the
-    reference's listings rows u < w < x); row order unspecified."""
+    reference's listings rows u < w < x); row order unspecified.  With an
+    oriented-edge range, only the triangles listed from those edges
+    (tc_list_triangles_range; consecutive ranges partition the listing)."""
+    last = g.num_edges() if last_edge is None else last_edge
     T = C.c_uint64()
-    _check(_lib.tc_list_triangles(g.handle, None, 0, C.byref(T)))
+    _check(_lib.tc_list_triangles_range(g.handle, first_edge, last, None, 0, C.byref(T)))
     rows = np.empty((max(T.value, 1), 3), np.uint32)
     n2 = C.c_uint64()
-    _check(_lib.tc_list_triangles(g.handle, C.c_void_p(rows.ctypes.data), T.value, C.byref(n2)))
+    _check(_lib.tc_list_triangles_range(g.handle, first_edge, last, C.c_void_p(rows.ctypes.data), T.value,
+                                        C.byref(n2)))
     return rows[: T.value]
+
+
+def iter_listings(g: Graph, max_rows: int = 1 << 22, out=None):
+    """Streamed listings: yields (k, 3) u32 arrays of at most max_rows rows
+    whose concatenation is list_triangles(g), walking the oriented edges range
+    by range with one bounded buffer (host, or a device tensor passed as out
+    with room for max_rows rows).  A range whose triangles overflow the buffer
+    is halved and re-listed; one that fits grows the next range.  Each yielded
+    array is a view of the buffer, valid until the next step."""
+    if max_rows < 1:
+        raise InvalidArgument("iter_listings: max_rows must be >= 1")
+    if out is None:
+        out = np.empty((max_rows, 3), np.uint32)
+        ptr = out.ctypes.data
+    else:
+        ptr = out.data_ptr()
+    E = g.num_edges()
+    e, span = 0, max(1, min(E, 1 << 16))
+    T = C.c_uint64()
+    while e < E:
+        b = min(E, e + span)
+        _check(_lib.tc_list_triangles_range(g.handle, e, b, C.c_void_p(ptr), max_rows, C.byref(T)))
+        if T.value > max_rows:
+            if b - e == 1:  # one edge's triangles exceed the buffer
+                raise InvalidArgument(f"iter_listings: edge {e} lists {T.value} triangles > max_rows")
+            span = max(1, (b - e) // 2)
+            continue
+        if T.value:
+            yield out[: T.value]
+        e = b
+        if 2 * T.value <= max_rows:
+            span *= 2
 
 
 def count_triangles_into(g: Graph, total_ptr, per_vertex_ptr=None, opts: Optional[MatchOptions] = None,

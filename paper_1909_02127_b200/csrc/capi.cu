@@ -392,12 +392,15 @@ tc_status tc_graph_load_matrix_market(const char* text, uint64_t len, int device
   TC_API_CATCH
 }
 
-tc_status tc_list_triangles(tc_graph* g, uint32_t* rows, uint64_t capacity, uint64_t* count) {
+tc_status tc_list_triangles_range(tc_graph* g, uint64_t first_edge, uint64_t last_edge, uint32_t* rows,
+                                  uint64_t capacity, uint64_t* count) {
   if (!g || !count || (capacity && !rows)) return set_error(TC_EINVAL, "tc_list_triangles: NULL argument");
+  if (first_edge > last_edge || last_edge > g->E)
+    return set_error(TC_EINVAL, "tc_list_triangles_range: edge range outside [0, num_edges]");
   TC_API_TRY
   DeviceGuard dg(g->device);
   DevOut<uint32_t> out(capacity ? rows : nullptr, 3 * capacity, g->stream);
-  const uint64_t T = tcb::list_triangles(*g, out.p, capacity);
+  const uint64_t T = tcb::list_triangles(*g, out.p, capacity, first_edge, last_edge);
   if (capacity) {
     out.count = 3 * std::min<uint64_t>(T, capacity);
     out.finish(g->stream);
@@ -406,6 +409,11 @@ tc_status tc_list_triangles(tc_graph* g, uint32_t* rows, uint64_t capacity, uint
   *count = T;
   return TC_OK;
   TC_API_CATCH
+}
+
+tc_status tc_list_triangles(tc_graph* g, uint32_t* rows, uint64_t capacity, uint64_t* count) {
+  if (!g) return set_error(TC_EINVAL, "tc_list_triangles: NULL argument");
+  return tc_list_triangles_range(g, 0, g->E, rows, capacity, count);
 }
 
 tc_status tc_graph_csr_cache_size(const tc_graph* g, uint64_t* len) {

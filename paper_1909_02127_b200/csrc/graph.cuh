@@ -190,7 +190,7 @@ bool mm_tokenize(const unsigned char* d_body, uint64_t len, const MmHeader& h, D
 
 // Triangle listings (listing.cu): writes min(T, cap) rows (3 u32 ids,
 // ascending) to d_rows, returns T.
-uint64_t list_triangles(tc_graph& g, uint32_t* d_rows, uint64_t cap);
+uint64_t list_triangles(tc_graph& g, uint32_t* d_rows, uint64_t cap, uint64_t e0, uint64_t e1);
 
 // Generators (gen.cu).
 uint64_t gen_num_edges(int kind, int scale, int param);

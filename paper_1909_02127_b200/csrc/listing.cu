@@ -10,6 +10,11 @@
 // past the caller's capacity are counted but not written, so a first call
 // with capacity 0 sizes the buffer.  Row order is unspecified (as the
 // reference's is a property of its parallel schedule); each row is sorted.
+//
+// Streamed output: a triangle is listed from exactly one oriented edge (its
+// lowest-ranked vertex u -> its middle one v), so edge ranges [e0, e1) of the
+// oriented CSR partition the listing; a caller with a bounded buffer walks the
+// edges range by range (tc_list_triangles_range).
 #include <cuda_runtime.h>
 
 #include "graph.cuh"
@@ -28,11 +33,11 @@ __device__ __forceinline__ bool in_sorted(const uint32_t* __restrict__ a, uint32
 
 __global__ void __launch_bounds__(256) k_list(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
                                               const uint32_t* __restrict__ src, const uint32_t* __restrict__ id_of,
-                                              uint64_t E, uint64_t cap, uint32_t* __restrict__ rows,
+                                              uint64_t e0, uint64_t e1, uint64_t cap, uint32_t* __restrict__ rows,
                                               unsigned long long* __restrict__ cursor) {
   const unsigned lane = lane_id();
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t e = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); e < E; e += warps) {
+  for (uint64_t e = e0 + (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); e < e1; e += warps) {
     const uint32_t u = src[e], v = col[e];
     const uint32_t end = off[u + 1];
     const uint32_t vb = off[v], dv = off[v + 1] - vb;
@@ -70,13 +75,14 @@ __global__ void __launch_bounds__(256) k_list(const uint32_t* __restrict__ off, 
 
 }  // namespace
 
-uint64_t list_triangles(tc_graph& g, uint32_t* d_rows, uint64_t cap) {
+uint64_t list_triangles(tc_graph& g, uint32_t* d_rows, uint64_t cap, uint64_t e0, uint64_t e1) {
   cudaStream_t s = g.stream;
   DBuf<unsigned long long> cursor(1, s);
   TC_CUDA(cudaMemsetAsync(cursor.get(), 0, sizeof(unsigned long long), s));
-  if (g.E) {
+  if (e1 > g.E) e1 = g.E;
+  if (e0 < e1) {
     const unsigned grid = (unsigned)num_sms(g.device) * 8;
-    k_list<<<grid, 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), g.id_of.get(), g.E, cap, d_rows,
+    k_list<<<grid, 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), g.id_of.get(), e0, e1, cap, d_rows,
                                 cursor.get());
     TC_LAUNCH();
   }

@@ -122,6 +122,14 @@ int main(int argc, char** argv) {
     // the Graph(n, E, offsets, nbrs) constructor route gives the same answer
     tg::Graph g_csr(g.num_vertices(), g.num_edges(), g.row_offsets(), g.neighbor_array());
     CHECK(tg::count_triangles(g_csr).count == T);
+    // streamed listings through a 777-row buffer: T rows, each ascending
+    std::uint64_t listed = 0, ascending = 0;
+    tg::for_each_triangle_chunk(g, [&](const std::array<tg::VertexId, 3>* rows, std::size_t k) {
+      CHECK(k <= 777);
+      listed += k;
+      for (std::size_t i = 0; i < k; ++i) ascending += rows[i][0] < rows[i][1] && rows[i][1] < rows[i][2];
+    }, 777);
+    CHECK(listed == T && ascending == T);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

@@ -522,3 +522,32 @@ def test_listings(tc, oracle, cuda_ok):
     rows = tc.list_triangles(tc.build_graph_from_pairs(pairs, 1 << 13))
     _check_listings(rows, off, nb, T)
     assert np.array_equal(np.bincount(rows.reshape(-1), minlength=1 << 13).astype(np.uint64), pv)
+
+
+def test_listings_streamed(tc, oracle, cuda_ok):
+    """Streamed listings (tc_list_triangles_range / iter_listings): edge ranges
+    partition the listing, and a bounded buffer (host or device) walks the
+    whole RMAT s13 graph; the concatenated chunks equal the full listing."""
+    import torch
+    pairs = tc.generate(tc.GEN_RMAT, 13, 16)
+    off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 13)
+    T, pv = oracle.count(off, nb, per_vertex=True)
+    g = tc.build_graph_from_pairs(pairs, 1 << 13)
+    Eo = g.num_edges()
+    cuts = [0, 1, 17, Eo // 3, Eo // 3, Eo - 5, Eo]
+    parts = [tc.list_triangles(g, a, b) for a, b in zip(cuts, cuts[1:])]
+    assert sum(p.shape[0] for p in parts) == T
+    _check_listings(np.concatenate(parts), off, nb, T)
+    for cap in (1000, 50000):
+        chunks = [c.copy() for c in tc.iter_listings(g, max_rows=cap)]
+        assert all(0 < c.shape[0] <= cap for c in chunks)
+        rows = np.concatenate(chunks)
+        _check_listings(rows, off, nb, T)
+        assert np.array_equal(np.bincount(rows.reshape(-1), minlength=1 << 13).astype(np.uint64), pv)
+    dev = torch.empty((4096, 3), dtype=torch.int32, device="cuda")
+    rows = np.concatenate([c.cpu().numpy().view(np.uint32) for c in tc.iter_listings(g, max_rows=4096, out=dev)])
+    _check_listings(rows, off, nb, T)
+    with pytest.raises(tc.InvalidArgument):
+        tc.list_triangles(g, 5, 3)
+    with pytest.raises(tc.InvalidArgument):
+        tc.list_triangles(g, 0, Eo + 1)
