@@ -74,10 +74,11 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 
 // ---- multi-GPU partition -------------------------------------------------------
 
-// Per-item overhead in candidate-probe units (frontier record + segment
-// staging), fitted on the C5 8-part split (~330 for the join's staging and
-// segments, the rest for the frontier record).
-constexpr uint64_t kItemCost = 400;
+// Per-item overhead in candidate-probe units (frontier record, segment
+// staging, and the re-staging of a pivot's row in every part that holds some
+// of its items), fitted on the C4 2/4/8-part splits (tools/phase_probe.py
+// --parts P, TCB_ITEM_COST): max part at P=8 400 -> 14.4 ms, 1000 -> 13.4 ms.
+constexpr uint64_t kItemCost = 1000;
 
 // Per-row cost of the degree-ordered DAG: row u with d = d+(u) out-edges
 // contributes C(d,2) candidate wedges and d items.  An exclusive scan over the
@@ -86,9 +87,10 @@ constexpr uint64_t kItemCost = 400;
 // over |V| rows, not |E| edges: it is part of every multi-GPU count.
 struct RowCost {
   const uint32_t* off;
+  uint64_t item_cost;
   __device__ __forceinline__ uint64_t operator()(uint64_t u) const {
     const uint64_t d = off[u + 1] - off[u];
-    return d * (d ? d - 1 : 0) / 2 + kItemCost * d;
+    return d * (d ? d - 1 : 0) / 2 + item_cost * d;
   }
 };
 
@@ -1177,7 +1179,9 @@ const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
   if (E && parts > 1) {
     const uint32_t n = g.n;
     DBuf<uint64_t> prefix(n, s), tot(1, s), bnd((uint64_t)parts + 1, s);
-    scan_exclusive<uint64_t>(RowCost{g.off.get()}, prefix.get(), n, tot.get(), s);
+    const char* ic = getenv("TCB_ITEM_COST");  // tuning knob for the cost model
+    const uint64_t item_cost = ic ? strtoull(ic, nullptr, 10) : kItemCost;
+    scan_exclusive<uint64_t>(RowCost{g.off.get(), item_cost}, prefix.get(), n, tot.get(), s);
     const uint64_t total_cost = read_scalar(tot.get(), s);
     k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), g.off.get(), n, E, total_cost, parts,
                                                           bnd.get());

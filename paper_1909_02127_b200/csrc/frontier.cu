@@ -230,23 +230,38 @@ struct PivotClass {
   }
 };
 
+// One pass over the pivots: class (PivotClass + 1, 0 = no work) in the top
+// two bits, the pivot's segment count in its bin below; the three per-class
+// scans and segment fills then read 4 bytes per pivot.
+constexpr uint32_t kSegBits = 30;
+__global__ void k_fr_class(PivotClass pc, uint32_t n, uint32_t* __restrict__ packed) {
+  constexpr uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = pc(v);
+    uint32_t w = 0;
+    if (c >= 0) w = ((uint32_t)(c + 1) << kSegBits) | ((pc.in[v + 1] - pc.in[v] + per[c] - 1) / per[c]);
+    packed[v] = w;
+  }
+}
+
 struct SegCountBin {
-  PivotClass pc;
-  int cls;
-  uint32_t per;
+  const uint32_t* packed;
+  uint32_t cls;  // PivotClass + 1
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
-    if (pc(v) != cls) return 0;
-    return (pc.in[v + 1] - pc.in[v] + per - 1) / per;
+    const uint32_t w = packed[v];
+    return (w >> kSegBits) == cls ? (w & ((1u << kSegBits) - 1)) : 0u;
   }
 };
 
-__global__ void k_fr_segs(PivotClass pc, uint32_t n, int cls, uint32_t per, const uint32_t* __restrict__ seg_off,
-                          uint4* __restrict__ segs, unsigned long long* __restrict__ npivots) {
+__global__ void k_fr_segs(const uint32_t* __restrict__ packed, const uint32_t* __restrict__ in, uint32_t n,
+                          uint32_t cls, uint32_t per, const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
+                          unsigned long long* __restrict__ npivots) {
   unsigned long long np = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    if (pc(v) != cls) continue;
-    const uint32_t a = pc.in[v], b = pc.in[v + 1];
+    if ((packed[v] >> kSegBits) != cls) continue;
+    const uint32_t a = in[v], b = in[v + 1];
     uint32_t s = seg_off[v];
     for (uint32_t i = a; i < b; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, b), 0);
     ++np;
@@ -325,8 +340,14 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     DBuf<uint32_t> tot(3, s);
     DBuf<unsigned long long> np(1, s);
     TC_CUDA(cudaMemsetAsync(np.get(), 0, sizeof(unsigned long long), s));
+    uint32_t* packed = cnt;  // the slot cursors are spent
+    if (n) {
+      k_fr_class<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, packed);
+      TC_LAUNCH();
+      ++kl;
+    }
     for (int c = 0; c < 3; ++c)
-      kl += scan_exclusive<uint32_t>(SegCountBin{pc, c, per[c]}, segoff[c], n, tot.get() + c, s);
+      kl += scan_exclusive<uint32_t>(SegCountBin{packed, (uint32_t)c + 1}, segoff[c], n, tot.get() + c, s);
     uint32_t h[3] = {0, 0, 0};
     TC_CUDA(cudaMemcpyAsync(h, tot.get(), 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
@@ -340,7 +361,8 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     const uint64_t cnt[3] = {fr.nw, fr.nc, fr.ns};
     for (int c = 0; c < 3; ++c) {
       if (!cnt[c]) continue;
-      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, c, per[c], segoff[c], segs[c], np.get());
+      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(packed, fr.in, n, (uint32_t)c + 1, per[c], segoff[c], segs[c],
+                                                 np.get());
       TC_LAUNCH();
       ++kl;
     }

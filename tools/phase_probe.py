@@ -29,12 +29,15 @@ tot = torch.zeros(1, dtype=torch.int64, device="cuda")
 pv = torch.zeros(n, dtype=torch.int64, device="cuda") if a.pv else None
 for i in range(a.iters):
     print(f"--- iter {i}", file=sys.stderr, flush=True)
-    T, ms = 0, {}
+    T, ms, per = 0, {}, []
     for p in range(a.parts):
         st = tc.count_triangles_into(g, tot, pv, tc.MatchOptions(per_vertex=bool(a.pv), part_index=p,
                                                                  part_count=a.parts), stats=True)
         T += int(tot.item())
+        per.append(round(st["total_ms"], 2))
         for k, v in st.items():
             if k.endswith("_ms"):
                 ms[k] = ms.get(k, 0) + v
     print(T, {k: round(v, 3) for k, v in ms.items()}, flush=True)
+    if a.parts > 1:
+        print(f"parts={a.parts} max={max(per)} sum={round(sum(per), 2)} per={per}", flush=True)
