@@ -8,10 +8,10 @@
 // e = u->v of this part's edge range [e0, e1) that can close a triangle as a
 // pivot in-edge (d+(v) > 0 and a non-empty suffix of N+(u) after v), one
 // item, grouped by pivot v:
-//   slots         one item slot per in-edge of every pivot with d+(v) > 0:
-//                 deg(v) - d+(v) for a whole-graph count (no edge pass), a
-//                 counting pass (one RED per edge) for a multi-GPU part
-//   scan          -> per-pivot item offsets in[v]
+//   slots         one item slot per in-edge of every pivot with d+(v) > 0,
+//                 deg(v) - d+(v) (no edge pass), scanned -> in[v]; a
+//                 multi-GPU part fills only the slots of its own edges, and
+//                 every pivot's item count is its scatter cursor
 //   rowbase       per-vertex only: exclusive scan of each row's hit-mask
 //                 bytes (closed form, graph.cuh RowMasks)
 //   k_fr_scatter  item geometry computed in edge order (the row data u, off,
@@ -49,7 +49,7 @@ T read_scalar(const T* d, cudaStream_t s) {
 }
 
 struct Sums {
-  unsigned long long W, J, hot, items_c;
+  unsigned long long W, J, hot, items_c, claims;
 };
 
 // The level-1 item of oriented edge e = u->v (u = src[e], v = col[e]).  Every
@@ -104,15 +104,6 @@ struct InSlotsWhole {
   }
 };
 
-// Item slots of a multi-GPU part: claimed in-edges inside [e0, e1).
-__global__ void k_fr_count(ItemGeom geo, uint64_t e0, uint64_t e1, uint32_t* __restrict__ cnt) {
-  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = geo.col[e];
-    if (geo.off[v + 1] > geo.off[v]) atomicAdd(&cnt[v], 1u);
-  }
-}
-
 // Mask bytes of row u (rows [u_lo, u_hi] of the part).
 struct RowBytes {
   const uint32_t* off;
@@ -142,7 +133,7 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
                                                   const uint64_t* __restrict__ rowbase, uint32_t u_lo,
                                                   uint8_t* __restrict__ masks,
                                                   Sums* __restrict__ sums) {
-  unsigned long long W = 0, J = 0, H = 0, IC = 0;
+  unsigned long long W = 0, J = 0, H = 0, IC = 0, CL = 0;
   for (uint64_t base = e0 + (uint64_t)blockIdx.x * (kT * kScatterR); base < e1;
        base += (uint64_t)gridDim.x * (kT * kScatterR)) {
     Geom q[kScatterR];
@@ -174,6 +165,7 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
         for (uint32_t i = 0; i < nb; ++i) z[i] = 0;
       }
       if (!q[r].claim) continue;
+      ++CL;
       constexpr int S = kPV ? 2 : kItemStrideTotal;  // uint4s per item record
       uint64_t mo = 0;
       if (kPV && q[r].useful && q[r].dv > kWarpMaxDeg && q[r].it.y > q[r].it.x)
@@ -206,7 +198,9 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
   J = warp_sum(J);
   H = warp_sum(H);
   IC = warp_sum(IC);
+  CL = warp_sum(CL);
   if (lane_id() == 0) {
+    if (CL) atomicAdd(&sums->claims, CL);
     if (W) atomicAdd(&sums->W, W);
     if (J) atomicAdd(&sums->J, J);
     if (H) atomicAdd(&sums->hot, H);
@@ -220,48 +214,43 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
 struct PivotClass {
   const uint32_t* off;
   const uint32_t* offH;
-  const uint32_t* in;
+  const uint32_t* cnt;  // items of each pivot (its scatter cursor)
   __device__ __forceinline__ int operator()(uint64_t v) const {
     const uint32_t dv = off[v + 1] - off[v];
-    if (dv == 0 || in[v + 1] == in[v]) return -1;
+    if (dv == 0 || cnt[v] == 0) return -1;
     if (dv <= kWarpMaxDeg) return 0;
-    const uint32_t items = in[v + 1] - in[v], hv = offH[v + 1] - offH[v];
+    const uint32_t items = cnt[v], hv = offH[v + 1] - offH[v];
     return (items <= kSmallItems && dv - hv <= kSmallCold) ? 2 : 1;
   }
 };
 
-// One pass over the pivots: class (PivotClass + 1, 0 = no work) in the top
-// two bits, the pivot's segment count in its bin below; the three per-class
-// scans and segment fills then read 4 bytes per pivot.
-constexpr uint32_t kSegBits = 30;
-__global__ void k_fr_class(PivotClass pc, uint32_t n, uint32_t* __restrict__ packed) {
-  constexpr uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
+// One pass over the pivots: class + 1 (0 = no work), one byte each; the three
+// per-class scans and segment fills then read 5 bytes per pivot.
+__global__ void k_fr_class(PivotClass pc, uint32_t n, uint8_t* __restrict__ cls) {
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * blockDim.x) {
-    const int c = pc(v);
-    uint32_t w = 0;
-    if (c >= 0) w = ((uint32_t)(c + 1) << kSegBits) | ((pc.in[v + 1] - pc.in[v] + per[c] - 1) / per[c]);
-    packed[v] = w;
-  }
+       v += (uint64_t)gridDim.x * blockDim.x)
+    cls[v] = (uint8_t)(pc(v) + 1);
 }
 
 struct SegCountBin {
-  const uint32_t* packed;
-  uint32_t cls;  // PivotClass + 1
+  const uint8_t* cls;
+  const uint32_t* cnt;
+  uint32_t c;  // PivotClass + 1
+  uint32_t per;
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
-    const uint32_t w = packed[v];
-    return (w >> kSegBits) == cls ? (w & ((1u << kSegBits) - 1)) : 0u;
+    return cls[v] == c ? (cnt[v] + per - 1) / per : 0u;
   }
 };
 
-__global__ void k_fr_segs(const uint32_t* __restrict__ packed, const uint32_t* __restrict__ in, uint32_t n,
-                          uint32_t cls, uint32_t per, const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
+__global__ void k_fr_segs(const uint8_t* __restrict__ cls, const uint32_t* __restrict__ in,
+                          const uint32_t* __restrict__ cnt, uint32_t n, uint32_t c, uint32_t per,
+                          const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
                           unsigned long long* __restrict__ npivots) {
   unsigned long long np = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    if ((packed[v] >> kSegBits) != cls) continue;
-    const uint32_t a = in[v], b = in[v + 1];
+    if (cls[v] != c) continue;
+    const uint32_t a = in[v], b = a + cnt[v];
     uint32_t s = seg_off[v];
     for (uint32_t i = a; i < b; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, b), 0);
     ++np;
@@ -287,18 +276,7 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   fr.in = g.scratch[kSlotIn].get<uint32_t>((uint64_t)n + 1, s);
   fr.e0 = e0;
   fr.e1 = e1;
-  const bool whole = e0 == 0 && e1 == g.E;
-  if (whole) {
-    kl += scan_exclusive<uint32_t>(InSlotsWhole{g.off.get(), g.deg.get()}, fr.in, n, fr.in + n, s);
-  } else {
-    if (e1 > e0) {
-      k_fr_count<<<grid_gs(e1 - e0, dev), kT, 0, s>>>(geo, e0, e1, cnt);
-      TC_LAUNCH();
-      ++kl;
-    }
-    kl += scan_exclusive<uint32_t>(LoadArray<uint32_t>{cnt}, fr.in, n, fr.in + n, s);
-    TC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nn, s));  // the scatter's cursors
-  }
+  kl += scan_exclusive<uint32_t>(InSlotsWhole{g.off.get(), g.deg.get()}, fr.in, n, fr.in + n, s);
   pl.mark("fr_slots");
   const uint64_t NI = n ? read_scalar(fr.in + n, s) : 0;
   fr.nitems = NI;
@@ -332,36 +310,28 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   pl.mark("fr_scatter");
   // per-bin work segments
   {
-    const PivotClass pc{g.off.get(), g.offH.get(), fr.in};
-    uint32_t* segoff[3] = {g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s),
-                           g.scratch[kSlotCoff].get<uint32_t>((uint64_t)nn + 1, s),
-                           g.scratch[kSlotSoff].get<uint32_t>((uint64_t)nn + 1, s)};
+    const PivotClass pc{g.off.get(), g.offH.get(), cnt};
+    // one offsets array, reused class by class (n can be 2^32 - 1)
+    uint32_t* segoff = g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s);
     const uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
-    DBuf<uint32_t> tot(3, s);
+    DBuf<uint32_t> tot(1, s);
     DBuf<unsigned long long> np(1, s);
     TC_CUDA(cudaMemsetAsync(np.get(), 0, sizeof(unsigned long long), s));
-    uint32_t* packed = cnt;  // the slot cursors are spent
+    uint8_t* cls = g.scratch[kSlotPacked].get<uint8_t>(nn, s);
     if (n) {
-      k_fr_class<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, packed);
+      k_fr_class<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, cls);
       TC_LAUNCH();
       ++kl;
     }
-    for (int c = 0; c < 3; ++c)
-      kl += scan_exclusive<uint32_t>(SegCountBin{packed, (uint32_t)c + 1}, segoff[c], n, tot.get() + c, s);
-    uint32_t h[3] = {0, 0, 0};
-    TC_CUDA(cudaMemcpyAsync(h, tot.get(), 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-    fr.nw = n ? h[0] : 0;
-    fr.nc = n ? h[1] : 0;
-    fr.ns = n ? h[2] : 0;
-    fr.wsegs = g.scratch[kSlotWsegs].get<uint4>(fr.nw, s);
-    fr.csegs = g.scratch[kSlotCsegs].get<uint4>(fr.nc, s);
-    fr.ssegs = g.scratch[kSlotSsegs].get<uint4>(fr.ns, s);
-    uint4* segs[3] = {fr.wsegs, fr.csegs, fr.ssegs};
-    const uint64_t cnt[3] = {fr.nw, fr.nc, fr.ns};
+    const ScratchSlot slot[3] = {kSlotWsegs, kSlotCsegs, kSlotSsegs};
+    uint64_t* nseg[3] = {&fr.nw, &fr.nc, &fr.ns};
+    uint4** segs[3] = {&fr.wsegs, &fr.csegs, &fr.ssegs};
     for (int c = 0; c < 3; ++c) {
-      if (!cnt[c]) continue;
-      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(packed, fr.in, n, (uint32_t)c + 1, per[c], segoff[c], segs[c],
+      kl += scan_exclusive<uint32_t>(SegCountBin{cls, cnt, (uint32_t)c + 1, per[c]}, segoff, n, tot.get(), s);
+      *nseg[c] = n ? read_scalar(tot.get(), s) : 0;
+      *segs[c] = g.scratch[slot[c]].get<uint4>(*nseg[c], s);
+      if (!*nseg[c]) continue;
+      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(cls, fr.in, cnt, n, (uint32_t)c + 1, per[c], segoff, *segs[c],
                                                  np.get());
       TC_LAUNCH();
       ++kl;
@@ -374,6 +344,7 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   fr.J = hs.J;
   fr.hot = hs.hot;
   fr.items_c = hs.items_c;
+  fr.nitems = hs.claims;  // this part's items (the slots of other parts' edges stay empty)
   return kl;
 }
 

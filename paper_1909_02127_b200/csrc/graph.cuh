@@ -38,8 +38,8 @@ struct Scratch {
   }
 };
 enum ScratchSlot {
-  kSlotCnt, kSlotIn, kSlotItems, kSlotRowBase, kSlotWoff, kSlotCoff, kSlotWsegs,
-  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotSoff, kSlotSsegs, kSlotCount
+  kSlotCnt, kSlotIn, kSlotItems, kSlotRowBase, kSlotWoff, kSlotWsegs,
+  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotSsegs, kSlotPacked, kSlotCount
 };
 }  // namespace tcb
 
@@ -106,7 +106,9 @@ constexpr uint32_t kSmallCold = TCB_SMALL_COLD;    // power of two
 //                [1] {u, 0, mo_lo, mo_hi}: the source u and the byte offset of
 //                    the item's hit masks (one byte per hot chunk from its
 //                    first hot chunk to the row's last, RowMasks below)
-//   in[v]      = first item of pivot v (n+1)
+//   in[v]      = first item slot of pivot v (n+1; deg(v) - d+(v) slots each);
+//                its items are in[v] .. in[v] + cursor[v] (a multi-GPU part
+//                fills only the slots of its own edges)
 //   rowbase[u-u_lo] = per-vertex only: first mask byte of row u (rows
 //                [u_lo, u_hi] of the part)
 //   wsegs / csegs / ssegs = {v, i0, i1, 0} work segments per bin
