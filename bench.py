@@ -94,6 +94,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.n_during = len(self.lines)
+        if self.proc and not self.lines:
+            # a timed region shorter than nvidia-smi's start-up: take the first
+            # sample right after it (flagged in the summary)
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3 and self.proc.poll() is None:
+                time.sleep(0.01)
         if self.proc:
             self.proc.terminate()
             try:
@@ -118,7 +125,10 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "n_during", 1) == 0:
+            out["sampled"] = "right after the timed region (shorter than nvidia-smi start-up)"
+        return out
 
 
 def gen_kind(tc, kind):

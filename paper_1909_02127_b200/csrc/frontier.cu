@@ -128,7 +128,7 @@ struct RowBytes {
 constexpr int kScatterR = TCB_SCATTER_R;
 template <bool kPV>
 __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom geo, uint64_t e0, uint64_t e1,
-                                                  const uint32_t* __restrict__ in, uint32_t* __restrict__ cursor,
+                                                  uint32_t* __restrict__ cursor,
                                                   uint4* __restrict__ items,
                                                   const uint64_t* __restrict__ rowbase, uint32_t u_lo,
                                                   uint8_t* __restrict__ masks,
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
     }
 #pragma unroll
     for (int r = 0; r < kScatterR; ++r)
-      if (q[r].claim) pos[r] = in[q[r].v] + atomicAdd(&cursor[q[r].v], 1u);
+      if (q[r].claim) pos[r] = atomicAdd(&cursor[q[r].v], 1u);  // cursors start at in[v]
 #pragma unroll
     for (int r = 0; r < kScatterR; ++r) {
       W += q[r].dv;
@@ -214,12 +214,14 @@ __global__ void __launch_bounds__(kT, TCB_SCATTER_MINB) k_fr_scatter(ItemGeom ge
 struct PivotClass {
   const uint32_t* off;
   const uint32_t* offH;
-  const uint32_t* cnt;  // items of each pivot (its scatter cursor)
+  const uint32_t* in;
+  const uint32_t* end;  // in[v] + items of v (the spent scatter cursor)
   __device__ __forceinline__ int operator()(uint64_t v) const {
     const uint32_t dv = off[v + 1] - off[v];
-    if (dv == 0 || cnt[v] == 0) return -1;
+    const uint32_t items = end[v] - in[v];
+    if (dv == 0 || items == 0) return -1;
     if (dv <= kWarpMaxDeg) return 0;
-    const uint32_t items = cnt[v], hv = offH[v + 1] - offH[v];
+    const uint32_t hv = offH[v + 1] - offH[v];
     return (items <= kSmallItems && dv - hv <= kSmallCold) ? 2 : 1;
   }
 };
@@ -234,23 +236,24 @@ __global__ void k_fr_class(PivotClass pc, uint32_t n, uint8_t* __restrict__ cls)
 
 struct SegCountBin {
   const uint8_t* cls;
-  const uint32_t* cnt;
+  const uint32_t* in;
+  const uint32_t* end;
   uint32_t c;  // PivotClass + 1
   uint32_t per;
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
-    return cls[v] == c ? (cnt[v] + per - 1) / per : 0u;
+    return cls[v] == c ? (end[v] - in[v] + per - 1) / per : 0u;
   }
 };
 
 __global__ void k_fr_segs(const uint8_t* __restrict__ cls, const uint32_t* __restrict__ in,
-                          const uint32_t* __restrict__ cnt, uint32_t n, uint32_t c, uint32_t per,
+                          const uint32_t* __restrict__ end, uint32_t n, uint32_t c, uint32_t per,
                           const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
                           unsigned long long* __restrict__ npivots) {
   unsigned long long np = 0;
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     if (cls[v] != c) continue;
-    const uint32_t a = in[v], b = a + cnt[v];
+    const uint32_t a = in[v], b = end[v];
     uint32_t s = seg_off[v];
     for (uint32_t i = a; i < b; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, b), 0);
     ++np;
@@ -271,12 +274,12 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   const ItemGeom geo{g.off.get(), g.col.get(), g.src.get(), g.offH.get()};
   DBuf<Sums> sums(1, s);
   TC_CUDA(cudaMemsetAsync(sums.get(), 0, sizeof(Sums), s));
-  uint32_t* cnt = g.scratch[kSlotCnt].get<uint32_t>(nn, s);
-  TC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nn, s));
+  uint32_t* cnt = g.scratch[kSlotCnt].get<uint32_t>(nn, s);  // scatter cursors, from in[v]
   fr.in = g.scratch[kSlotIn].get<uint32_t>((uint64_t)n + 1, s);
   fr.e0 = e0;
   fr.e1 = e1;
   kl += scan_exclusive<uint32_t>(InSlotsWhole{g.off.get(), g.deg.get()}, fr.in, n, fr.in + n, s);
+  if (n) TC_CUDA(cudaMemcpyAsync(cnt, fr.in, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
   pl.mark("fr_slots");
   const uint64_t NI = n ? read_scalar(fr.in + n, s) : 0;
   fr.nitems = NI;
@@ -299,10 +302,10 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   if (NI) {
     const unsigned grid = grid_gs(ceil_div64(e1 - e0, kScatterR), dev);
     if (per_vertex)
-      k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, fr.rowbase,
+      k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, cnt, fr.items, fr.rowbase,
                                              fr.u_lo, fr.masks, sums.get());
     else
-      k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, fr.in, cnt, fr.items, nullptr, 0,
+      k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, cnt, fr.items, nullptr, 0,
                                               nullptr, sums.get());
     TC_LAUNCH();
     ++kl;
@@ -310,7 +313,7 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   pl.mark("fr_scatter");
   // per-bin work segments
   {
-    const PivotClass pc{g.off.get(), g.offH.get(), cnt};
+    const PivotClass pc{g.off.get(), g.offH.get(), fr.in, cnt};
     // one offsets array, reused class by class (n can be 2^32 - 1)
     uint32_t* segoff = g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s);
     const uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
@@ -327,7 +330,7 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     uint64_t* nseg[3] = {&fr.nw, &fr.nc, &fr.ns};
     uint4** segs[3] = {&fr.wsegs, &fr.csegs, &fr.ssegs};
     for (int c = 0; c < 3; ++c) {
-      kl += scan_exclusive<uint32_t>(SegCountBin{cls, cnt, (uint32_t)c + 1, per[c]}, segoff, n, tot.get(), s);
+      kl += scan_exclusive<uint32_t>(SegCountBin{cls, fr.in, cnt, (uint32_t)c + 1, per[c]}, segoff, n, tot.get(), s);
       *nseg[c] = n ? read_scalar(tot.get(), s) : 0;
       *segs[c] = g.scratch[slot[c]].get<uint4>(*nseg[c], s);
       if (!*nseg[c]) continue;
