@@ -551,3 +551,26 @@ def test_listings_streamed(tc, oracle, cuda_ok):
         tc.list_triangles(g, 5, 3)
     with pytest.raises(tc.InvalidArgument):
         tc.list_triangles(g, 0, Eo + 1)
+
+
+def test_csr_route_input_residency(tc, oracle, cuda_ok):
+    """tc_graph_from_csr with the CSR on the device, on the host (pageable and
+    pinned, streamed in pieces) and mixed: identical graphs and counts."""
+    import torch
+    pairs = tc.generate(tc.GEN_RMAT, 14, 16)
+    off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 14)
+    T, pv = oracle.count(off, nb, per_vertex=True)
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    d_nb = torch.from_numpy(nb.view(np.int32)).cuda()
+    p_off = torch.from_numpy(off.view(np.int64)).pin_memory()
+    p_nb = torch.from_numpy(nb.view(np.int32)).pin_memory()
+    os.environ["TCB_FEED_CHUNK"] = "100000"
+    try:
+        for o, b in ((d_off, d_nb), (off, nb), (p_off, p_nb), (off, d_nb), (d_off, nb)):
+            g = tc.graph_from_csr(o, b, 1 << 14, E)
+            r = _count(tc, g)
+            assert r.count == T and np.array_equal(r.per_vertex, pv)
+            ro, nbr = g.export_csr()
+            assert np.array_equal(ro, off) and np.array_equal(nbr, nb)
+    finally:
+        os.environ.pop("TCB_FEED_CHUNK", None)
