@@ -486,11 +486,13 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       }
     }
     // (1b) stage items, compacted into hot / cold lists with chunk prefixes
-    uint4 it[2];
-    uint32_t nh[2], nc[2];
+    constexpr int kIPT = kCtaSegItems / kJoinThreads;  // items per thread
+    static_assert(kCtaSegItems % kJoinThreads == 0, "segment items must be a multiple of the CTA size");
+    uint4 it[kIPT];
+    uint32_t nh[kIPT], nc[kIPT];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t i = threadIdx.x * 2 + r;
+    for (int r = 0; r < kIPT; ++r) {
+      const uint32_t i = threadIdx.x * kIPT + r;
       nh[r] = nc[r] = 0;
       if (i < ni) {
         it[r] = __ldcs(items + (uint64_t)(i0 + i) * (kPerVertex ? 2 : kItemStrideTotal));
@@ -502,8 +504,13 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     // one block scan of the pair (list positions: hot count in the low 16
     // bits, cold in the high 16; chunk prefixes: hot in the low 32 bits, cold
     // in the high 32), two barriers
-    uint32_t lp = (uint32_t)((nh[0] > 0) + (nh[1] > 0)) | ((uint32_t)((nc[0] > 0) + (nc[1] > 0)) << 16);
-    unsigned long long cp = (unsigned long long)(nh[0] + nh[1]) | ((unsigned long long)(nc[0] + nc[1]) << 32);
+    uint32_t lp = 0;
+    unsigned long long cp = 0;
+#pragma unroll
+    for (int r = 0; r < kIPT; ++r) {
+      lp += (uint32_t)(nh[r] > 0) | ((uint32_t)(nc[r] > 0) << 16);
+      cp += (unsigned long long)nh[r] | ((unsigned long long)nc[r] << 32);
+    }
     {
       const uint32_t il = warp_inclusive_scan(lp);
       const unsigned long long ic = warp_inclusive_scan(cp);
@@ -535,8 +542,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       uint32_t ph = lp & 0xffffu, pc = lp >> 16;
       uint32_t ch = (uint32_t)cp, cc = (uint32_t)(cp >> 32);
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t i = threadIdx.x * 2 + r;
+      for (int r = 0; r < kIPT; ++r) {
+        const uint32_t i = threadIdx.x * kIPT + r;
         if (nh[r]) {
           s_hb[ph] = it[r].x;
           s_he[ph] = it[r].y;

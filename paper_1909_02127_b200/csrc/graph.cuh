@@ -73,7 +73,10 @@ namespace tcb {
 constexpr uint32_t kHotBits = 1u << 16;
 constexpr uint32_t kWarpMaxDeg = 48;    // warp bin: d+(v) <= 48 (128-slot warp table)
 constexpr uint32_t kWarpSegItems = 64;  // items per warp-bin segment
-constexpr uint32_t kCtaSegItems = 512;  // items per CTA-bin segment
+#ifndef TCB_CTA_SEG_ITEMS
+#define TCB_CTA_SEG_ITEMS 512
+#endif
+constexpr uint32_t kCtaSegItems = TCB_CTA_SEG_ITEMS;  // items per CTA-bin segment
 #ifndef TCB_ITEM_STRIDE_TOTAL
 #define TCB_ITEM_STRIDE_TOTAL 1
 #endif
