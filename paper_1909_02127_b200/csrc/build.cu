@@ -937,7 +937,8 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   struct FeedGuard {
     cudaStream_t& cs;
     std::vector<cudaEvent_t>& ev;
-    ~FeedGuard() {
+    ~FeedGuard() {  // an error path may leave pieces in flight into the caller's buffers
+      if (cs) cudaStreamSynchronize(cs);
       for (cudaEvent_t e : ev) cudaEventDestroy(e);
       if (cs) cudaStreamDestroy(cs);
     }

@@ -574,3 +574,25 @@ def test_csr_route_input_residency(tc, oracle, cuda_ok):
             assert np.array_equal(ro, off) and np.array_equal(nbr, nb)
     finally:
         os.environ.pop("TCB_FEED_CHUNK", None)
+
+
+def test_csr_route_errors_streamed(tc, oracle, cuda_ok):
+    """Validation failures while the neighbour array is still streaming in
+    (bad offsets fail before any row is oriented, bad ids after): the call
+    raises, no copy outlives it, and the next build is clean."""
+    pairs = tc.generate(tc.GEN_RMAT, 12, 16)
+    off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 12)
+    T = oracle.count(off, nb)
+    os.environ["TCB_FEED_CHUNK"] = "5000"
+    try:
+        bad_off = off.copy()
+        bad_off[7] = bad_off[8] + 1  # non-monotone
+        with pytest.raises(tc.InvalidArgument):
+            tc.graph_from_csr(bad_off, nb, 1 << 12, E)
+        bad_nb = nb.copy()
+        bad_nb[len(nb) - 3] = 1 << 20  # out of range, in the last piece
+        with pytest.raises(tc.InvalidArgument):
+            tc.graph_from_csr(off, bad_nb, 1 << 12, E)
+        assert tc.count_triangles(tc.graph_from_csr(off, nb, 1 << 12, E)).count == T
+    finally:
+        os.environ.pop("TCB_FEED_CHUNK", None)
