@@ -40,4 +40,17 @@ import ctypes as C  # noqa: E402
 h = C.c_void_p()
 tc._check(tc._lib.tc_csr_cache_to_graph(img.tobytes(), img.size, 0, C.byref(h)))
 assert tc.count_triangles(tc.Graph(h.value, 0)).count == T
+# the CSR route streamed in small pieces (rows across piece boundaries) with
+# rank-space rows in the lane / warp / <=256 / <=1024 sort classes, and the
+# streamed listings
+os.environ["TCB_FEED_CHUNK"] = "3000"
+k2 = 300
+iu, ju = np.triu_indices(k2, 1)
+cp = np.concatenate([np.stack([iu, ju], 1).astype(np.uint32).reshape(-1), (pairs + k2).astype(np.uint32)])
+off3, nb3, E3, _, _ = o.build_graph(cp, n + k2)
+T3 = o.count(off3, nb3)
+g3 = tc.graph_from_csr(off3, nb3)
+assert tc.count_triangles(g3).count == T3
+del os.environ["TCB_FEED_CHUNK"]
+assert sum(c.shape[0] for c in tc.iter_listings(g2, max_rows=500)) == T
 print("sanitize cases ok", T)
