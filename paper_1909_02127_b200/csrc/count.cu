@@ -494,6 +494,9 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     for (int r = 0; r < kIPT; ++r) {
       const uint32_t i = threadIdx.x * kIPT + r;
       nh[r] = nc[r] = 0;
+      // defined on every path, it[] stays out of local memory: total-only
+      // 31.2 -> 30.9 ms at C4; the per-vertex variant measured 0.2 ms slower
+      if constexpr (!kPerVertex) it[r] = make_uint4(0, 0, 0, 0);
       if (i < ni) {
         it[r] = __ldcs(items + (uint64_t)(i0 + i) * (kPerVertex ? 2 : kItemStrideTotal));
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
