@@ -447,17 +447,25 @@ __global__ void k_chunk_bases(const Chunk* __restrict__ chunks, uint32_t nchunks
   }
 }
 
-// Row sorts: every rank-space row r moves from its padded slot pad[pad_off[r],
-// + d+(r)) to its place col[off[r], off[r+1]), sorted, with src = r.  Rows of
-// <= 16 entries are sorted by their lane (register bitonic network), rows of
-// 17..32 by the warp (shuffle bitonic), longer rows are listed for the warp /
-// CTA sorts below.
-struct RowMove {
-  const uint32_t* off;      // final rank-space offsets
-  const uint32_t* pad_off;  // padded slots
-  const uint32_t* pad;
-  uint32_t* col;
-  uint32_t* src;
+// Row sorts.  Every rank-space row r is sorted IN its padded slot
+// pad[pad_off[r], + d+(r)) as soon as its id-row has been oriented (piece by
+// piece, behind the host copy), and its hot count hcnt[r] (members >= h0, the
+// sorted suffix) recorded; after the last piece one compaction pass moves the
+// slots to col/src and writes the hot mirror.  Rows of <= 16 entries are
+// sorted by their lane (register bitonic network), rows of 17..32 by the warp
+// (shuffle bitonic), 33..1024 by a warp through a conflict-free SMEM tile,
+// longer rows by a CTA in SMEM; rows longer than sort_max are listed for the
+// radix fallback.
+struct SlotSort {
+  const uint32_t* rank_of;
+  const uint32_t* pad_off;
+  uint32_t* pad;
+  const uint32_t* dplus;
+  uint32_t h0;
+  uint32_t sort_max;
+  uint32_t* hcnt;
+  uint32_t* huge;  // rows over sort_max
+  unsigned int* nhuge;
 };
 
 __device__ __forceinline__ void sort16(uint32_t (&x)[16]) {
@@ -479,39 +487,48 @@ __device__ __forceinline__ void sort16(uint32_t (&x)[16]) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_seg_sort_warp(RowMove mv, uint32_t n, uint32_t* __restrict__ longrows,
-                                                       unsigned int* __restrict__ nlong) {
+// The id-rows [lo, hi) of one piece, 32 per warp: their rank-space rows.
+__global__ void __launch_bounds__(256) k_slot_sort_warp(SlotSort ss, uint32_t lo, uint32_t hi,
+                                                        uint32_t* __restrict__ longrows,
+                                                        unsigned int* __restrict__ nlong) {
   const unsigned lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint64_t r00 = (uint64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r00 < n;
-       r00 += (uint64_t)warps * 32) {
-    const uint32_t r0 = (uint32_t)r00, r = r0 + lane;
-    uint32_t o = 0, d = 0, po = 0;
-    if (r00 + lane < n) {
-      o = mv.off[r];
-      d = mv.off[r + 1] - o;
-      po = mv.pad_off[r];
+  for (uint64_t u0 = lo + (uint64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; u0 < hi;
+       u0 += (uint64_t)warps * 32) {
+    uint32_t r = 0, d = 0, po = 0;
+    if (u0 + lane < hi) {
+      r = ss.rank_of[u0 + lane];
+      d = ss.dplus[r];
+      po = ss.pad_off[r];
     }
-    if (d >= 1 && d <= 16) {
+    if (d > ss.sort_max) {
+      ss.huge[atomicAdd(ss.nhuge, 1u)] = r;
+      d = 0;
+    } else if (d > 32) {
+      longrows[atomicAdd(nlong, 1u)] = r;
+      d = 0;
+    }
+    if (d >= 1 && d <= 16) {  // (hcnt is zeroed up front for empty rows)
       uint32_t x[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? mv.pad[po + i] : 0xffffffffu;
+      for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? ss.pad[po + i] : 0xffffffffu;
       if (d >= 2) sort16(x);
+      uint32_t h = 0;
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         if ((uint32_t)i < d) {
-          mv.col[o + i] = x[i];
-          mv.src[o + i] = r;
+          ss.pad[po + i] = x[i];
+          h += x[i] >= ss.h0;
         }
+      ss.hcnt[r] = h;
     }
-    if (d > 32) longrows[atomicAdd(nlong, 1u)] = r;
     uint32_t mid = __ballot_sync(0xffffffffu, d > 16 && d <= 32);
     while (mid) {
       const int j = __ffs(mid) - 1;
       mid &= mid - 1;
-      const uint32_t oj = __shfl_sync(0xffffffffu, o, j), dj = __shfl_sync(0xffffffffu, d, j);
-      const uint32_t pj = __shfl_sync(0xffffffffu, po, j);
-      uint32_t x = lane < dj ? mv.pad[pj + lane] : 0xffffffffu;
+      const uint32_t dj = __shfl_sync(0xffffffffu, d, j), pj = __shfl_sync(0xffffffffu, po, j);
+      const uint32_t rj = __shfl_sync(0xffffffffu, r, j);
+      uint32_t x = lane < dj ? ss.pad[pj + lane] : 0xffffffffu;
 #pragma unroll
       for (uint32_t k = 2; k <= 32; k <<= 1) {
 #pragma unroll
@@ -521,9 +538,25 @@ __global__ void __launch_bounds__(256) k_seg_sort_warp(RowMove mv, uint32_t n, u
           x = (lower == asc) ? min(x, y) : max(x, y);
         }
       }
-      if (lane < dj) {
-        mv.col[oj + lane] = x;
-        mv.src[oj + lane] = r0 + j;
+      if (lane < dj) ss.pad[pj + lane] = x;
+      const uint32_t h = __popc(__ballot_sync(0xffffffffu, lane < dj && x >= ss.h0));
+      if (lane == 0) ss.hcnt[rj] = h;
+    }
+  }
+}
+
+// In-lane bitonic stage j (< kE) of merge size k over a lane's kE registers.
+template <int kE, int J>
+__device__ __forceinline__ void lane_stage(uint32_t (&x)[kE], uint32_t pb, uint32_t k) {
+  if constexpr (J < kE) {
+#pragma unroll
+    for (int i = 0; i < kE; ++i) {
+      const int l = i ^ J;
+      if (l > i && l < kE) {
+        const bool asc = ((pb + i) & k) == 0;
+        const uint32_t a = x[i], b = x[l];
+        x[i] = asc ? min(a, b) : max(a, b);
+        x[l] = asc ? max(a, b) : min(a, b);
       }
     }
   }
@@ -533,32 +566,15 @@ __global__ void __launch_bounds__(256) k_seg_sort_warp(RowMove mv, uint32_t n, u
 // in registers (position p = lane*kE + i), bitonic network over 32*kE: in-lane
 // stages for j < kE, shuffles for j >= kE.  The row goes through a per-warp
 // SMEM tile (index p + p/32: conflict-free both ways) so that global loads and
-// stores stay coalesced.  Longer rows are re-listed for the CTA sort.
-// In-lane bitonic stage j (< kE) of merge size k over a lane's kE registers.
-template <int kE, int J>
-__device__ __forceinline__ void lane_stage(uint32_t (&x)[kE], uint32_t pb, uint32_t k) {
-  if (J >= kE) return;
-#pragma unroll
-  for (int i = 0; i < kE; ++i) {
-    const int l = i ^ J;
-    if (l > i && l < kE) {
-      const bool asc = ((pb + i) & k) == 0;
-      const uint32_t a = x[i], b = x[l];
-      x[i] = asc ? min(a, b) : max(a, b);
-      x[l] = asc ? max(a, b) : min(a, b);
-    }
-  }
-}
-
+// stores stay coalesced.  Sorted in place; returns the row's hot count.
 template <int kE>
-__device__ __forceinline__ void warp_sort_row(const RowMove& mv, uint32_t r, uint32_t o, uint32_t d,
-                                              uint32_t* __restrict__ sm) {
+__device__ __forceinline__ uint32_t warp_sort_row(uint32_t* __restrict__ row, uint32_t d, uint32_t h0,
+                                                  uint32_t* __restrict__ sm) {
   const unsigned lane = lane_id();
-  const uint32_t* in = mv.pad + mv.pad_off[r];
 #pragma unroll
   for (int m = 0; m < kE; ++m) {
     const uint32_t t = m * 32 + lane;
-    sm[t + m] = t < d ? in[t] : 0xffffffffu;
+    sm[t + m] = t < d ? row[t] : 0xffffffffu;
   }
   __syncwarp();
   uint32_t x[kE];
@@ -621,66 +637,82 @@ __device__ __forceinline__ void warp_sort_row(const RowMove& mv, uint32_t r, uin
     sm[p + (p >> 5)] = x[i];
   }
   __syncwarp();
+  uint32_t h = 0;
 #pragma unroll
   for (int m = 0; m < kE; ++m) {
     const uint32_t t = m * 32 + lane;
     if (t < d) {
-      mv.col[o + t] = sm[t + m];
-      mv.src[o + t] = r;
+      const uint32_t y = sm[t + m];
+      row[t] = y;
+      h += y >= h0;
     }
   }
   __syncwarp();
+  return warp_sum(h);
 }
 
-__global__ void __launch_bounds__(256) k_seg_sort_mid(RowMove mv, const uint32_t* __restrict__ rows,
-                                                      const unsigned int* __restrict__ nrows,
-                                                      uint32_t* __restrict__ longrows,
-                                                      unsigned int* __restrict__ nlong) {
+__global__ void __launch_bounds__(256) k_slot_sort_mid(SlotSort ss, const uint32_t* __restrict__ rows,
+                                                       const unsigned int* __restrict__ nrows,
+                                                       uint32_t* __restrict__ longrows,
+                                                       unsigned int* __restrict__ nlong) {
   __shared__ uint32_t tile[8][8 * 33];
   uint32_t* sm = tile[threadIdx.x >> 5];
   const uint32_t nr = *nrows;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); idx < nr; idx += warps) {
-    const uint32_t r = rows[idx];
-    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
-    if (d <= 64) warp_sort_row<2>(mv, r, o, d, sm);
-    else if (d <= 128) warp_sort_row<4>(mv, r, o, d, sm);
-    else if (d <= 256) warp_sort_row<8>(mv, r, o, d, sm);
-    else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
+    const uint32_t r = rows[idx], d = ss.dplus[r];
+    uint32_t* row = ss.pad + ss.pad_off[r];
+    uint32_t h = 0;
+    if (d <= 64) h = warp_sort_row<2>(row, d, ss.h0, sm);
+    else if (d <= 128) h = warp_sort_row<4>(row, d, ss.h0, sm);
+    else if (d <= 256) h = warp_sort_row<8>(row, d, ss.h0, sm);
+    else {
+      if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
+      continue;
+    }
+    if (lane_id() == 0) ss.hcnt[r] = h;
   }
 }
 
 // Rows of 257..1024 entries (16/32 per lane, its own kernel for the register
 // budget); longer rows are re-listed for the CTA sort.
-__global__ void __launch_bounds__(128) k_seg_sort_mid2(RowMove mv, const uint32_t* __restrict__ rows,
-                                                       const unsigned int* __restrict__ nrows,
-                                                       uint32_t* __restrict__ longrows,
-                                                       unsigned int* __restrict__ nlong) {
+__global__ void __launch_bounds__(128) k_slot_sort_mid2(SlotSort ss, const uint32_t* __restrict__ rows,
+                                                        const unsigned int* __restrict__ nrows,
+                                                        uint32_t* __restrict__ longrows,
+                                                        unsigned int* __restrict__ nlong) {
   __shared__ uint32_t tile[4][32 * 33];
   uint32_t* sm = tile[threadIdx.x >> 5];
   const uint32_t nr = *nrows;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t idx = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); idx < nr; idx += warps) {
-    const uint32_t r = rows[idx];
-    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
-    if (d <= 512) warp_sort_row<16>(mv, r, o, d, sm);
-    else if (d <= 1024) warp_sort_row<32>(mv, r, o, d, sm);
-    else if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
+    const uint32_t r = rows[idx], d = ss.dplus[r];
+    uint32_t* row = ss.pad + ss.pad_off[r];
+    uint32_t h = 0;
+    if (d <= 512) h = warp_sort_row<16>(row, d, ss.h0, sm);
+    else if (d <= 1024) h = warp_sort_row<32>(row, d, ss.h0, sm);
+    else {
+      if (lane_id() == 0) longrows[atomicAdd(nlong, 1u)] = r;
+      continue;
+    }
+    if (lane_id() == 0) ss.hcnt[r] = h;
   }
 }
 
-// Listed rows: one CTA each, SMEM bitonic sort over the next power of two.
-__global__ void __launch_bounds__(256) k_seg_sort_block(RowMove mv, const uint32_t* __restrict__ rows,
-                                                        const unsigned int* __restrict__ nrows) {
+// Listed rows (<= sort_max entries): one CTA each, SMEM bitonic sort over the
+// next power of two.
+constexpr uint32_t kSortMax = 16384;
+__global__ void __launch_bounds__(256) k_slot_sort_block(SlotSort ss, const uint32_t* __restrict__ rows,
+                                                         const unsigned int* __restrict__ nrows) {
   extern __shared__ uint32_t sk[];
+  __shared__ uint32_t s_h;
   const uint32_t nr = *nrows;
   for (uint32_t idx = blockIdx.x; idx < nr; idx += gridDim.x) {
-    const uint32_t r = rows[idx];
-    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
-    const uint32_t* in = mv.pad + mv.pad_off[r];
+    const uint32_t r = rows[idx], d = ss.dplus[r];
+    uint32_t* row = ss.pad + ss.pad_off[r];
     uint32_t P = 64;
     while (P < d) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < d ? in[i] : 0xffffffffu;
+    if (threadIdx.x == 0) s_h = 0;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < d ? row[i] : 0xffffffffu;
     __syncthreads();
     for (uint32_t k = 2; k <= P; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -695,24 +727,63 @@ __global__ void __launch_bounds__(256) k_seg_sort_block(RowMove mv, const uint32
         __syncthreads();
       }
     }
+    uint32_t h = 0;
     for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
-      mv.col[o + i] = sk[i];
-      mv.src[o + i] = r;
+      row[i] = sk[i];
+      h += sk[i] >= ss.h0;
     }
+    h = warp_sum(h);
+    if (lane_id() == 0 && h) atomicAdd(&s_h, h);
     __syncthreads();
+    if (threadIdx.x == 0) ss.hcnt[r] = s_h;
   }
 }
 
-// Radix fallback (rows longer than the CTA sort takes): move the slots as-is.
-__global__ void k_move_rows(RowMove mv, uint32_t n) {
+// Every slot -> col[off[r], off[r+1]) with src = r, and (hot: its sorted
+// suffix >= h0) -> colH[offH[r], offH[r+1]) as 16-bit offsets.  Rows by
+// lane (<= 16 entries) or, for longer ones, by the warp.
+__global__ void __launch_bounds__(256) k_slot_compact(const uint32_t* __restrict__ off,
+                                                      const uint32_t* __restrict__ pad_off,
+                                                      const uint32_t* __restrict__ pad, uint32_t n,
+                                                      uint32_t* __restrict__ col, uint32_t* __restrict__ src,
+                                                      const uint32_t* __restrict__ offH, uint32_t h0,
+                                                      uint16_t* __restrict__ colH) {
   const unsigned lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint64_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
-    const uint32_t o = mv.off[r], d = mv.off[r + 1] - o;
-    const uint32_t* in = mv.pad + mv.pad_off[r];
-    for (uint32_t i = lane; i < d; i += 32) {
-      mv.col[o + i] = in[i];
-      mv.src[o + i] = r;
+  for (uint64_t r00 = (uint64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r00 < n;
+       r00 += (uint64_t)warps * 32) {
+    const uint32_t r = (uint32_t)r00 + lane;
+    uint32_t o = 0, d = 0, po = 0, hb = 0, hs = 0;
+    if (r00 + lane < n) {
+      o = off[r];
+      d = off[r + 1] - o;
+      po = pad_off[r];
+      if (colH) {
+        hb = offH[r];
+        hs = d - (offH[r + 1] - hb);  // first hot position of the row
+      }
+    }
+    if (d <= 16) {
+      for (uint32_t i = 0; i < d; ++i) {
+        const uint32_t x = pad[po + i];
+        col[o + i] = x;
+        src[o + i] = r;
+        if (colH && i >= hs) colH[hb + i - hs] = (uint16_t)(x - h0);
+      }
+    }
+    uint32_t big = __ballot_sync(0xffffffffu, d > 16);
+    while (big) {
+      const int j = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t oj = __shfl_sync(0xffffffffu, o, j), dj = __shfl_sync(0xffffffffu, d, j);
+      const uint32_t pj = __shfl_sync(0xffffffffu, po, j), rj = (uint32_t)r00 + j;
+      const uint32_t hbj = __shfl_sync(0xffffffffu, hb, j), hsj = __shfl_sync(0xffffffffu, hs, j);
+      for (uint32_t i = lane; i < dj; i += 32) {
+        const uint32_t x = pad[pj + i];
+        col[oj + i] = x;
+        src[oj + i] = rj;
+        if (colH && i >= hsj) colH[hbj + i - hsj] = (uint16_t)(x - h0);
+      }
     }
   }
 }
@@ -794,17 +865,22 @@ void row_offsets(tc_graph& g, const uint32_t* dplus) {
 }
 
 // Shared tail: the hot-window mirror of the finished oriented CSR.
+// First rank of the hot window [h0, n) (graph.cuh).
+uint32_t hot_window_start(uint32_t n) {
+  const char* hb = getenv("TCB_HOT_BITS");  // tests: shrink the window to drive the cold path
+  uint32_t hot = hb ? (uint32_t)strtoul(hb, nullptr, 10) : kHotBits;
+  if (hot < 32) hot = 32;
+  if (hot > kHotBits) hot = kHotBits;
+  return n > hot ? n - hot : 0;
+}
+
 void finish_rows(tc_graph& g) {
   cudaStream_t s = g.stream;
   const uint32_t n = g.n;
   const uint64_t E = g.E;
   const int dev = g.device;
   // hot window mirror (graph.cuh): 16-bit copy of every row's members >= h0
-  const char* hb = getenv("TCB_HOT_BITS");  // tests: shrink the window to drive the cold path
-  uint32_t hot = hb ? (uint32_t)strtoul(hb, nullptr, 10) : kHotBits;
-  if (hot < 32) hot = 32;
-  if (hot > kHotBits) hot = kHotBits;
-  g.h0 = n > hot ? n - hot : 0;
+  g.h0 = hot_window_start(n);
   g.offH.alloc((uint64_t)n + 1, s);
   {
     DBuf<uint32_t> hcnt(n ? n : 1, s);
@@ -1005,6 +1081,20 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   TC_CUDA(cudaMemsetAsync(dplus.get(), 0, sizeof(uint32_t) * nn, s));
   pl.mark("csr_rank");
   RowCtx cx{d_off, d_nbrs, g.rank_of.get(), n, dplus.get(), pad_off.get(), pad.get(), strict ? 1 : 0};
+  // per piece: orient its rows, then sort their slots in place (hot counts)
+  g.h0 = hot_window_start(n);
+  const char* smx = getenv("TCB_ROWSORT_MAX");  // tests: force the radix fallback on small graphs
+  const uint32_t sort_max = std::min<uint32_t>(smx ? (uint32_t)strtoul(smx, nullptr, 10) : kSortMax, kSortMax);
+  DBuf<uint32_t> hcnt(nn, s), huge(nn, s), rows_a(nn, s), rows_b(nn, s);
+  DBuf<unsigned int> lists(3 * K + 1, s);  // per piece: mid / long / CTA list counts; + huge count
+  TC_CUDA(cudaMemsetAsync(hcnt.get(), 0, sizeof(uint32_t) * nn, s));
+  TC_CUDA(cudaMemsetAsync(lists.get(), 0, (3 * K + 1) * sizeof(unsigned int), s));
+  const SlotSort ss{g.rank_of.get(), pad_off.get(), pad.get(), dplus.get(), g.h0, sort_max, hcnt.get(),
+                    huge.get(), lists.get() + 3 * K};
+  uint32_t Pb = 64;
+  while (Pb < sort_max) Pb <<= 1;
+  TC_CUDA(cudaFuncSetAttribute(k_slot_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(Pb * sizeof(uint32_t))));
   const unsigned gw = (unsigned)num_sms(dev) * 8;
   uint32_t lo = 0;
   for (uint32_t k = 0; k < K && total; ++k) {
@@ -1031,10 +1121,19 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
                                            bad.get());
         TC_LAUNCH();
       }
+      unsigned int* cnt3 = lists.get() + 3 * k;
+      k_slot_sort_warp<<<gw, 256, 0, s>>>(ss, lo, hi, rows_a.get(), cnt3);
+      TC_LAUNCH();
+      k_slot_sort_mid<<<gw, 256, 0, s>>>(ss, rows_a.get(), cnt3, rows_b.get(), cnt3 + 1);
+      TC_LAUNCH();
+      k_slot_sort_mid2<<<gw * 2, 128, 0, s>>>(ss, rows_b.get(), cnt3 + 1, rows_a.get(), cnt3 + 2);
+      TC_LAUNCH();
+      k_slot_sort_block<<<gw, 256, Pb * sizeof(uint32_t), s>>>(ss, rows_a.get(), cnt3 + 2);
+      TC_LAUNCH();
     }
     lo = hi;
   }
-  pl.mark("csr_orient");
+  pl.mark("csr_orient_sort");
   const uint64_t E = read_scalar(upper.get(), s);
   const int badv = read_scalar(bad.get(), s);
   if (badv && strict) fail(TC_EPARSE, "corrupt CSR cache adjacency (line 1)");
@@ -1045,47 +1144,37 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   row_offsets(g, dplus.get());
   if (n && read_scalar(g.off.get() + n, s) != E)
     fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
-  if (E) {
-    // every slot -> its sorted place in col (+ src)
-    const RowMove mv{g.off.get(), pad_off.get(), pad.get(), g.col.get(), g.src.get()};
-    uint32_t P = 64;
-    while (P < g.max_dplus) P <<= 1;
-    const char* sm = getenv("TCB_ROWSORT_MAX");  // tests: force the radix fallback on small graphs
-    const uint32_t sort_max = sm ? (uint32_t)strtoul(sm, nullptr, 10) : 16384u;
-    if (P <= sort_max) {
-      DBuf<uint32_t> midrows(nn, s), longrows(nn, s);
-      TC_CUDA(cudaMemsetAsync(cnts.get(), 0, 2 * sizeof(unsigned int), s));
-      k_seg_sort_warp<<<gw, 256, 0, s>>>(mv, n, midrows.get(), cnts.get());
-      TC_LAUNCH();
-      pl.mark("csr_sort_le32");
-      k_seg_sort_mid<<<gw, 256, 0, s>>>(mv, midrows.get(), cnts.get(), longrows.get(), cnts.get() + 1);
-      TC_LAUNCH();
-      pl.mark("csr_sort_le256");
-      // rows of 257..1024: re-listed from longrows into midrows
-      TC_CUDA(cudaMemsetAsync(cnts.get(), 0, sizeof(unsigned int), s));
-      k_seg_sort_mid2<<<gw * 2, 128, 0, s>>>(mv, longrows.get(), cnts.get() + 1, midrows.get(), cnts.get());
-      TC_LAUNCH();
-      std::swap(midrows, longrows);  // rows > 1024 are now in longrows, count in cnts[0]
-      pl.mark("csr_sort_le1024");
-      const size_t smem = (size_t)P * sizeof(uint32_t);
-      TC_CUDA(cudaFuncSetAttribute(k_seg_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_seg_sort_block<<<gw, 256, smem, s>>>(mv, longrows.get(), cnts.get());
-      TC_LAUNCH();
-    } else {
-      k_move_rows<<<gw, 256, 0, s>>>(mv, n);
-      TC_LAUNCH();
-      DBuf<uint64_t> k1(E, s), k2(E, s);
-      k_pack_oriented<<<grid_gs(E, dev), kT, 0, s>>>(g.src.get(), g.col.get(), E, g.id_bits, k1.get());
-      TC_LAUNCH();
-      uint64_t* sorted = radix_sort_u64(k1.get(), k2.get(), E, 0, 2 * g.id_bits, s);
-      k_unpack_col<<<grid_gs(E, dev), kT, 0, s>>>(sorted, E, g.id_bits, g.col.get());
+  const uint32_t nhuge = read_scalar(lists.get() + 3 * K, s);
+  if (nhuge == 0) {
+    // slots -> col/src + the hot mirror in one pass
+    g.offH.alloc((uint64_t)n + 1, s);
+    scan_exclusive<uint32_t>(LoadArray<uint32_t>{hcnt.get()}, g.offH.get(), n, g.offH.get() + n, s);
+    const uint32_t total_hot = n ? read_scalar(g.offH.get() + n, s) : 0;
+    g.colH.alloc((uint64_t)total_hot + 16, s);
+    TC_CUDA(cudaMemsetAsync(g.colH.get() + total_hot, 0, 16 * sizeof(uint16_t), s));
+    if (E) {
+      k_slot_compact<<<gw, 256, 0, s>>>(g.off.get(), pad_off.get(), pad.get(), n, g.col.get(), g.src.get(),
+                                        g.offH.get(), g.h0, g.colH.get());
       TC_LAUNCH();
     }
-    pl.mark("csr_row_sort");
+    pl.mark("csr_compact_hot");
+  } else {
+    // rows longer than the CTA sort: move the slots, one global radix sort
+    k_slot_compact<<<gw, 256, 0, s>>>(g.off.get(), pad_off.get(), pad.get(), n, g.col.get(), g.src.get(), nullptr,
+                                      0, nullptr);
+    TC_LAUNCH();
+    DBuf<uint64_t> k1(E, s), k2(E, s);
+    k_pack_oriented<<<grid_gs(E, dev), kT, 0, s>>>(g.src.get(), g.col.get(), E, g.id_bits, k1.get());
+    TC_LAUNCH();
+    uint64_t* sorted = radix_sort_u64(k1.get(), k2.get(), E, 0, 2 * g.id_bits, s);
+    k_unpack_col<<<grid_gs(E, dev), kT, 0, s>>>(sorted, E, g.id_bits, g.col.get());
+    TC_LAUNCH();
+    k1.release();
+    k2.release();
+    pad.release();
+    finish_rows(g);
+    pl.mark("csr_radix_fallback");
   }
-  pad.release();
-  finish_rows(g);
-  pl.mark("csr_hot_mirror");
 }
 
 void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs) {
