@@ -740,51 +740,61 @@ __global__ void __launch_bounds__(256) k_slot_sort_block(SlotSort ss, const uint
 }
 
 // Every slot -> col[off[r], off[r+1]) with src = r, and (hot: its sorted
-// suffix >= h0) -> colH[offH[r], offH[r+1]) as 16-bit offsets.  Rows by
-// lane (<= 16 entries) or, for longer ones, by the warp.
+// suffix >= h0) -> colH[offH[r], offH[r+1]) as 16-bit offsets.  A warp takes
+// 32 consecutive rows, whose outputs are one contiguous range of col: lanes
+// walk that range 32 positions at a time (coalesced stores) and find their row
+// by a 5-step search over the group's offsets in SMEM.
 __global__ void __launch_bounds__(256) k_slot_compact(const uint32_t* __restrict__ off,
                                                       const uint32_t* __restrict__ pad_off,
                                                       const uint32_t* __restrict__ pad, uint32_t n,
                                                       uint32_t* __restrict__ col, uint32_t* __restrict__ src,
                                                       const uint32_t* __restrict__ offH, uint32_t h0,
                                                       uint16_t* __restrict__ colH) {
-  const unsigned lane = lane_id();
+  __shared__ uint32_t s_off[8][33], s_po[8][32], s_hb[8][32], s_hs[8][32];
+  const unsigned lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint64_t r00 = (uint64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r00 < n;
-       r00 += (uint64_t)warps * 32) {
-    const uint32_t r = (uint32_t)r00 + lane;
-    uint32_t o = 0, d = 0, po = 0, hb = 0, hs = 0;
-    if (r00 + lane < n) {
-      o = off[r];
-      d = off[r + 1] - o;
-      po = pad_off[r];
+  for (uint64_t r00 = (uint64_t)(blockIdx.x * (blockDim.x / 32) + w) * 32; r00 < n; r00 += (uint64_t)warps * 32) {
+    const uint64_t r = r00 + lane;
+    const uint32_t rr = r < n ? (uint32_t)r : n;
+    const uint32_t o = off[rr];
+    s_off[w][lane] = o;
+    if (lane == 31) s_off[w][32] = off[r00 + 32 < n ? (uint32_t)(r00 + 32) : n];
+    uint32_t po = 0, hb = 0, hs = 0xffffffffu;
+    if (r < n) {
+      po = pad_off[rr];
       if (colH) {
-        hb = offH[r];
-        hs = d - (offH[r + 1] - hb);  // first hot position of the row
+        hb = offH[rr];
+        hs = (off[rr + 1] - o) - (offH[rr + 1] - hb);  // first hot position of the row
       }
     }
-    if (d <= 16) {
-      for (uint32_t i = 0; i < d; ++i) {
-        const uint32_t x = pad[po + i];
-        col[o + i] = x;
-        src[o + i] = r;
-        if (colH && i >= hs) colH[hb + i - hs] = (uint16_t)(x - h0);
+    s_po[w][lane] = po;
+    s_hb[w][lane] = hb;
+    s_hs[w][lane] = hs;
+    __syncwarp();
+    const uint32_t a = s_off[w][0], b = s_off[w][32];
+    for (uint32_t p0 = a + lane; p0 < b; p0 += 32 * 4) {  // 4 independent positions in flight
+      uint32_t j[4], i[4], x[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t p = p0 + 32 * t;
+        uint32_t jj = 0;
+#pragma unroll
+        for (uint32_t st = 16; st > 0; st >>= 1)
+          if (s_off[w][jj + st] <= p) jj += st;
+        j[t] = jj;
+        i[t] = p - s_off[w][jj];
+        x[t] = p < b ? pad[s_po[w][jj] + i[t]] : 0u;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t p = p0 + 32 * t;
+        if (p >= b) break;
+        col[p] = x[t];
+        src[p] = (uint32_t)r00 + j[t];
+        if (colH && i[t] >= s_hs[w][j[t]]) colH[s_hb[w][j[t]] + i[t] - s_hs[w][j[t]]] = (uint16_t)(x[t] - h0);
       }
     }
-    uint32_t big = __ballot_sync(0xffffffffu, d > 16);
-    while (big) {
-      const int j = __ffs(big) - 1;
-      big &= big - 1;
-      const uint32_t oj = __shfl_sync(0xffffffffu, o, j), dj = __shfl_sync(0xffffffffu, d, j);
-      const uint32_t pj = __shfl_sync(0xffffffffu, po, j), rj = (uint32_t)r00 + j;
-      const uint32_t hbj = __shfl_sync(0xffffffffu, hb, j), hsj = __shfl_sync(0xffffffffu, hs, j);
-      for (uint32_t i = lane; i < dj; i += 32) {
-        const uint32_t x = pad[pj + i];
-        col[oj + i] = x;
-        src[oj + i] = rj;
-        if (colH && i >= hsj) colH[hbj + i - hsj] = (uint16_t)(x - h0);
-      }
-    }
+    __syncwarp();
   }
 }
 
@@ -905,7 +915,8 @@ void alloc_rows(tc_graph& g) {
   g.col.alloc(g.E + 8, s);
   g.src.alloc(g.E ? g.E : 1, s);
   g.off.alloc((uint64_t)g.n + 1, s);
-  TC_CUDA(cudaMemsetAsync(g.col.get(), 0xff, (g.E + 8) * sizeof(uint32_t), s));
+  // every col[0, E) is written by the build; the 8-word tail pad reads as "no id"
+  TC_CUDA(cudaMemsetAsync(g.col.get() + g.E, 0xff, 8 * sizeof(uint32_t), s));
 }
 
 // Sorted unique canonical id-space keys (edge-list route) -> ranks ->
@@ -1145,6 +1156,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   if (n && read_scalar(g.off.get() + n, s) != E)
     fail(TC_EINVAL, "Graph: inconsistent CSR arrays (asymmetric adjacency)");
   const uint32_t nhuge = read_scalar(lists.get() + 3 * K, s);
+  pl.mark("csr_offsets");
   if (nhuge == 0) {
     // slots -> col/src + the hot mirror in one pass
     g.offH.alloc((uint64_t)n + 1, s);
@@ -1152,6 +1164,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     const uint32_t total_hot = n ? read_scalar(g.offH.get() + n, s) : 0;
     g.colH.alloc((uint64_t)total_hot + 16, s);
     TC_CUDA(cudaMemsetAsync(g.colH.get() + total_hot, 0, 16 * sizeof(uint16_t), s));
+    pl.mark("csr_hot_offsets");
     if (E) {
       k_slot_compact<<<gw, 256, 0, s>>>(g.off.get(), pad_off.get(), pad.get(), n, g.col.get(), g.src.get(),
                                         g.offH.get(), g.h0, g.colH.get());
