@@ -355,6 +355,21 @@ def main():
     pv_d = torch.zeros(n, dtype=torch.int64, device=dev) if (per_vertex and world > 1) else None
     tot_d = torch.zeros(1, dtype=torch.int64, device=dev)
 
+    # the box's host->device link rate for the same bytes (a plain pinned copy):
+    # e2e is bound below by h2d_bytes / this rate, which varies across boxes
+    link_gbps = None
+    if E:
+        tmp = torch.empty_like(nb_h, device=dev)
+        rates = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tmp.copy_(nb_h, non_blocking=True)
+            torch.cuda.synchronize()
+            rates.append(nb_h.numel() * 4 / (time.perf_counter() - t0) / 1e9)
+        link_gbps = max(rates)
+        del tmp
+
     def e2e_step():
         ge = tc.graph_from_csr(ro_h, nb_h, n, E, device=local)        # H2D + orientation
         if world == 1:
@@ -426,6 +441,8 @@ def main():
         },
         "e2e": {"value": E / (e2e_ms / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "h2d_link_gbps": link_gbps,
+                "h2d_floor_ms": (h2d / link_gbps / 1e6) if link_gbps else None,
                 "path": "tc_graph_from_csr(host pinned CSR) + tc_count(host outputs)"},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
