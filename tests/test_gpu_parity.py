@@ -596,3 +596,22 @@ def test_csr_route_errors_streamed(tc, oracle, cuda_ok):
         assert tc.count_triangles(tc.graph_from_csr(off, nb, 1 << 12, E)).count == T
     finally:
         os.environ.pop("TCB_FEED_CHUNK", None)
+
+
+def test_csr_route_empty_and_isolated(tc, cuda_ok):
+    """Graph(n, 0, offsets, {}) and graphs with isolated vertices through the
+    CSR route (host and streamed)."""
+    for n in (0, 1, 5):
+        g = tc.graph_from_csr(np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), n, 0)
+        assert g.num_edges() == 0 and tc.count_triangles(g).count == 0
+        r = tc.count_triangles(g, tc.MatchOptions(per_vertex=True))
+        assert r.count == 0 and (r.per_vertex is None or not r.per_vertex.any())
+    # K3 on vertices {2, 5, 7} of 10, the rest isolated
+    off = np.array([0, 0, 0, 2, 2, 2, 4, 4, 6, 6, 6], np.uint64)
+    nb = np.array([5, 7, 2, 7, 2, 5], np.uint32)
+    os.environ["TCB_FEED_CHUNK"] = "2"
+    try:
+        r = tc.count_triangles(tc.graph_from_csr(off, nb), tc.MatchOptions(per_vertex=True))
+    finally:
+        os.environ.pop("TCB_FEED_CHUNK", None)
+    assert r.count == 1 and r.per_vertex.tolist() == [0, 0, 1, 0, 0, 1, 0, 1, 0, 0]
