@@ -77,8 +77,10 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 // Per-item overhead in candidate-probe units (frontier record, segment
 // staging, and the re-staging of a pivot's row in every part that holds some
 // of its items), fitted on the C4 2/4/8-part splits (tools/phase_probe.py
-// --parts P, TCB_ITEM_COST): max part at P=8 400 -> 14.4 ms, 1000 -> 13.4 ms.
-constexpr uint64_t kItemCost = 1000;
+// --parts P, TCB_ITEM_COST): max part at P = 2/4/8 is 34.2/19.1/12.1 ms at
+// 700 against 35.7/20.5/12.1 at 1000 and 36.4/22.1/14.4 at 400 (C5's 8-part
+// split prefers 1000: 135.9 against 141.5 ms).
+constexpr uint64_t kItemCost = 700;
 
 // Per-row cost of the degree-ordered DAG: row u with d = d+(u) out-edges
 // contributes C(d,2) candidate wedges and d items.  An exclusive scan over the

@@ -36,7 +36,7 @@ def degree_rank_dag(offsets: np.ndarray, nbrs: np.ndarray):
     return off, col, src, order
 
 
-ITEM_COST = 1000  # count.cu kItemCost: per-item overhead in candidate-probe units
+ITEM_COST = 700  # count.cu kItemCost: per-item overhead in candidate-probe units
 
 
 def row_cost(off: np.ndarray) -> np.ndarray:
