@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
 #include <cstdlib>
 #include <vector>
 
@@ -1013,43 +1014,19 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   if (num_edges >= (1ull << 32)) fail(TC_ERANGE, "graph has >= 2^32 undirected edges (u32 oriented offsets)");
   PhaseLog pl(s);
   // The neighbour array streams in behind everything that needs only the
-  // offsets: kChunk-entry pieces on a side stream, one event each.
+  // offsets: pieces of kFeedChunk entries (8 M from pageable memory, which
+  // goes through pinned bounce slots), one event each (feed.cu).
   const bool stream_in = feed && total;
   const char* fc = getenv("TCB_FEED_CHUNK");  // tests: many small pieces
-  const uint64_t chunk = fc ? std::max<uint64_t>(1, strtoull(fc, nullptr, 10)) : kFeedChunk;
-  const uint64_t piece = feed && feed->h_off ? chunk : (total ? total : 1);
-  const uint32_t K = stream_in ? (uint32_t)((total + piece - 1) / piece) : 1;
-  cudaStream_t cs = nullptr;
-  std::vector<cudaEvent_t> ev;
-  struct FeedGuard {
-    cudaStream_t& cs;
-    std::vector<cudaEvent_t>& ev;
-    ~FeedGuard() {  // an error path may leave pieces in flight into the caller's buffers
-      if (cs) cudaStreamSynchronize(cs);
-      for (cudaEvent_t e : ev) cudaEventDestroy(e);
-      if (cs) cudaStreamDestroy(cs);
-    }
-  } feed_guard{cs, ev};
-  uint32_t issued = 0;
-  auto issue = [&](uint32_t upto) {  // copies of pieces [issued, upto)
-    for (; issued < upto && issued < K; ++issued) {
-      const uint64_t a = issued * piece, b = std::min(total, a + piece);
-      TC_CUDA(cudaMemcpyAsync(feed->d_dst + a, feed->h_nbrs + a, (b - a) * sizeof(uint32_t),
-                              cudaMemcpyHostToDevice, cs));
-      TC_CUDA(cudaEventRecord(ev[issued], cs));
-    }
-  };
+  uint64_t chunk = fc ? std::max<uint64_t>(1, strtoull(fc, nullptr, 10)) : kFeedChunk;
+  std::unique_ptr<PieceFeed> pf;
+  uint64_t piece = total ? total : 1;
   if (stream_in) {
-    TC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    ev.resize(K);
-    for (auto& e : ev) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cudaEvent_t ready;  // the destination was allocated on s
-    TC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    TC_CUDA(cudaEventRecord(ready, s));
-    TC_CUDA(cudaStreamWaitEvent(cs, ready, 0));
-    TC_CUDA(cudaEventDestroy(ready));
-    issue(2);
+    if (!fc && pageable_host(feed->h_nbrs)) chunk = std::min<uint64_t>(chunk, 1ull << 23);
+    piece = feed->h_off ? chunk : total;
+    pf.reset(new PieceFeed(feed->h_nbrs, feed->d_dst, total, piece, s));
   }
+  const uint32_t K = pf ? pf->pieces() : 1;
   const uint32_t nn = n ? n : 1;
   DBuf<uint32_t> deg(nn, s), big(total / kBigRow + 1, s);
   DBuf<unsigned int> cnts(2, s);  // big rows / long rank-space rows
@@ -1115,10 +1092,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
       const uint64_t e = (uint64_t)(k + 1) * piece;
       hi = (uint32_t)(std::upper_bound(feed->h_off, feed->h_off + (uint64_t)n + 1, e) - feed->h_off) - 1;
     }
-    if (stream_in) {
-      issue(k + 3);
-      TC_CUDA(cudaStreamWaitEvent(s, ev[k], 0));
-    }
+    if (pf) pf->wait_piece(k, s);
     if (hi > lo) {
       k_csr_rows<<<gw, 256, 0, s>>>(cx, lo, hi, queues.get() + k, upper.get(), bad.get());
       TC_LAUNCH();

@@ -13,6 +13,11 @@
 // C5 (RMAT s26 ef32) = 34 GB of 180 GB.
 #pragma once
 
+#include <atomic>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -178,6 +183,43 @@ struct CsrFeed {
 };
 void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n,
                     uint64_t num_edges, bool strict = false, const CsrFeed* feed = nullptr);
+
+// Host memory that is neither pinned nor registered with CUDA.
+bool pageable_host(const void* p);
+
+// The piece-by-piece host->device copy behind build_from_csr (feed.cu):
+// pinned sources are DMA'd directly; pageable ones go through pinned bounce
+// slots filled by worker threads.  wait_piece(k, s) makes s wait for piece k;
+// the destructor waits for every piece in flight.
+class PieceFeed {
+ public:
+  PieceFeed(const uint32_t* h, uint32_t* d, uint64_t total, uint64_t piece, cudaStream_t after);
+  ~PieceFeed();
+  PieceFeed(const PieceFeed&) = delete;
+  PieceFeed& operator=(const PieceFeed&) = delete;
+  uint32_t pieces() const { return K_; }
+  bool pageable() const { return pageable_; }
+  void wait_piece(uint32_t k, cudaStream_t s);
+
+ private:
+  void issue(uint32_t upto);
+  void work(uint32_t t);
+  const uint32_t* h_;
+  uint32_t* d_;
+  uint64_t total_, piece_;
+  uint32_t K_ = 0, W_ = 1, issued_ = 0;
+  int dev_ = 0;
+  bool pageable_ = false;
+  std::vector<cudaEvent_t> ev_, slot_done_;
+  std::vector<cudaStream_t> streams_;
+  std::vector<std::thread> workers_;
+  std::unique_lock<std::mutex> lock_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<char> recorded_;
+  std::exception_ptr err_;
+  std::atomic<bool> abort_{false};
+};
 void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs);
 void export_degrees(tc_graph& g, uint32_t* d_deg);
 
