@@ -30,3 +30,12 @@ for name, (o, b) in (("pinned", (ro, nb)), ("pageable", (ro_p, nb_p))):
         t1 = time.perf_counter()
         del ge
         print(f"{name} from_csr {1e3 * (t1 - t0):.1f} ms", flush=True)
+# per-vertex output (134 MB) into pinned vs pageable host memory
+ge = tc.graph_from_csr(ro, nb, n, E)
+tot = np.zeros(1, np.uint64)
+for name, pv in (("pinned", torch.zeros(n, dtype=torch.int64, pin_memory=True)), ("pageable", np.zeros(n, np.uint64))):
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tc.count_triangles_into(ge, tot, pv, tc.MatchOptions(per_vertex=True), sync=True)
+        print(f"{name} count+D2H {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
