@@ -228,10 +228,30 @@ struct PivotClass {
 
 // One pass over the pivots: class + 1 (0 = no work), one byte each; the three
 // per-class scans and segment fills then read 5 bytes per pivot.
-__global__ void k_fr_class(PivotClass pc, uint32_t n, uint8_t* __restrict__ cls) {
+// ... and the per-class segment totals + the pivot count (tot[0..3]), so the
+// host sizes every segment list after one read and skips empty classes.
+__global__ void k_fr_class(PivotClass pc, uint32_t n, uint8_t* __restrict__ cls,
+                           unsigned long long* __restrict__ tot) {
+  constexpr uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
+  unsigned long long t[4] = {0, 0, 0, 0};
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * blockDim.x)
-    cls[v] = (uint8_t)(pc(v) + 1);
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = pc(v);
+    cls[v] = (uint8_t)(c + 1);
+    if (c >= 0) {
+      const uint32_t items = pc.end[v] - pc.in[v];
+      const unsigned long long ns = (items + per[c] - 1) / per[c];
+      t[0] += c == 0 ? ns : 0;
+      t[1] += c == 1 ? ns : 0;
+      t[2] += c == 2 ? ns : 0;
+      t[3] += 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long w = warp_sum(t[i]);
+    if (lane_id() == 0 && w) atomicAdd(&tot[i], w);
+  }
 }
 
 struct SegCountBin {
@@ -247,19 +267,14 @@ struct SegCountBin {
 
 __global__ void k_fr_segs(const uint8_t* __restrict__ cls, const uint32_t* __restrict__ in,
                           const uint32_t* __restrict__ end, uint32_t n, uint32_t c, uint32_t per,
-                          const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs,
-                          unsigned long long* __restrict__ npivots) {
-  unsigned long long np = 0;
+                          const uint32_t* __restrict__ seg_off, uint4* __restrict__ segs) {
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     if (cls[v] != c) continue;
     const uint32_t a = in[v], b = end[v];
     uint32_t s = seg_off[v];
     for (uint32_t i = a; i < b; i += per) segs[s++] = make_uint4((uint32_t)v, i, min(i + per, b), 0);
-    ++np;
   }
-  np = warp_sum(np);
-  if (lane_id() == 0 && np) atomicAdd(npivots, np);
 }
 
 }  // namespace
@@ -318,28 +333,30 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     uint32_t* segoff = g.scratch[kSlotWoff].get<uint32_t>((uint64_t)nn + 1, s);
     const uint32_t per[3] = {kWarpSegItems, kCtaSegItems, kSmallItems};
     DBuf<uint32_t> tot(1, s);
-    DBuf<unsigned long long> np(1, s);
-    TC_CUDA(cudaMemsetAsync(np.get(), 0, sizeof(unsigned long long), s));
+    DBuf<unsigned long long> ctot(4, s);
+    TC_CUDA(cudaMemsetAsync(ctot.get(), 0, 4 * sizeof(unsigned long long), s));
     uint8_t* cls = g.scratch[kSlotPacked].get<uint8_t>(nn, s);
     if (n) {
-      k_fr_class<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, cls);
+      k_fr_class<<<grid_gs(n, dev), kT, 0, s>>>(pc, n, cls, ctot.get());
       TC_LAUNCH();
       ++kl;
     }
+    unsigned long long h[4] = {0, 0, 0, 0};
+    TC_CUDA(cudaMemcpyAsync(h, ctot.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
     const ScratchSlot slot[3] = {kSlotWsegs, kSlotCsegs, kSlotSsegs};
     uint64_t* nseg[3] = {&fr.nw, &fr.nc, &fr.ns};
     uint4** segs[3] = {&fr.wsegs, &fr.csegs, &fr.ssegs};
     for (int c = 0; c < 3; ++c) {
-      kl += scan_exclusive<uint32_t>(SegCountBin{cls, fr.in, cnt, (uint32_t)c + 1, per[c]}, segoff, n, tot.get(), s);
-      *nseg[c] = n ? read_scalar(tot.get(), s) : 0;
+      *nseg[c] = h[c];
       *segs[c] = g.scratch[slot[c]].get<uint4>(*nseg[c], s);
-      if (!*nseg[c]) continue;
-      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(cls, fr.in, cnt, n, (uint32_t)c + 1, per[c], segoff, *segs[c],
-                                                 np.get());
+      if (!*nseg[c]) continue;  // (empty classes: no scan, no fill)
+      kl += scan_exclusive<uint32_t>(SegCountBin{cls, fr.in, cnt, (uint32_t)c + 1, per[c]}, segoff, n, tot.get(), s);
+      k_fr_segs<<<grid_gs(n, dev), kT, 0, s>>>(cls, fr.in, cnt, n, (uint32_t)c + 1, per[c], segoff, *segs[c]);
       TC_LAUNCH();
       ++kl;
     }
-    fr.pivots = read_scalar(np.get(), s);
+    fr.pivots = h[3];
   }
   pl.mark("fr_segs");
   const Sums hs = read_scalar(sums.get(), s);
