@@ -1358,6 +1358,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   TC_CUDA(cudaEventRecord(ev.e[3], s));
   if (stats) {
     TC_CUDA(cudaEventSynchronize(ev.e[3]));
+    read_frontier_sums(fr, s);
     stats->frontier_ms = ev.ms(0, 1);
     stats->join_ms = ev.ms(1, 2);
     stats->reduce_ms = ev.ms(2, 3);

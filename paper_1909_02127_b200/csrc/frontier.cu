@@ -287,8 +287,9 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   int kl = 0;
   PhaseLog pl(s);
   const ItemGeom geo{g.off.get(), g.col.get(), g.src.get(), g.offH.get()};
-  DBuf<Sums> sums(1, s);
-  TC_CUDA(cudaMemsetAsync(sums.get(), 0, sizeof(Sums), s));
+  Sums* sums = g.scratch[kSlotSums].get<Sums>(1, s);  // read only for stats (read_frontier_sums)
+  TC_CUDA(cudaMemsetAsync(sums, 0, sizeof(Sums), s));
+  fr.sums = sums;
   uint32_t* cnt = g.scratch[kSlotCnt].get<uint32_t>(nn, s);  // scatter cursors, from in[v]
   fr.in = g.scratch[kSlotIn].get<uint32_t>((uint64_t)n + 1, s);
   fr.e0 = e0;
@@ -296,32 +297,39 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
   kl += scan_exclusive<uint32_t>(InSlotsWhole{g.off.get(), g.deg.get()}, fr.in, n, fr.in + n, s);
   if (n) TC_CUDA(cudaMemcpyAsync(cnt, fr.in, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
   pl.mark("fr_slots");
-  const uint64_t NI = n ? read_scalar(fr.in + n, s) : 0;
-  fr.nitems = NI;
-  fr.items = g.scratch[kSlotItems].get<uint4>(NI * (per_vertex ? 2 : kItemStrideTotal), s);
-  // per-vertex: the rows the part's edges come from and their mask blocks
+  // per-vertex: the rows the part's edges come from (the whole graph: all
+  // rows) and their mask blocks; one read for the item and mask-byte totals
   fr.mask_bytes = 0;
   fr.u_lo = 0;
   fr.u_hi = n ? n - 1 : 0;
+  uint64_t rows = 0;
   if (per_vertex && e1 > e0) {
-    fr.u_lo = read_scalar(g.src.get() + e0, s);  // the rows that own the part's edges
-    fr.u_hi = read_scalar(g.src.get() + e1 - 1, s);
-    const uint64_t rows = (uint64_t)fr.u_hi - fr.u_lo + 1;
+    if (e0 != 0 || e1 != g.E) {
+      fr.u_lo = read_scalar(g.src.get() + e0, s);
+      fr.u_hi = read_scalar(g.src.get() + e1 - 1, s);
+    }
+    rows = (uint64_t)fr.u_hi - fr.u_lo + 1;
     fr.rowbase = g.scratch[kSlotRowBase].get<uint64_t>(rows + 1, s);
     kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get(), fr.u_lo}, fr.rowbase, rows, fr.rowbase + rows,
                                    s);
-    fr.mask_bytes = read_scalar(fr.rowbase + rows, s);
-    fr.masks = g.scratch[kSlotMasks].get<uint8_t>(fr.mask_bytes + 32, s);
   }
+  uint32_t NI32 = 0;
+  if (n) TC_CUDA(cudaMemcpyAsync(&NI32, fr.in + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  if (rows) TC_CUDA(cudaMemcpyAsync(&fr.mask_bytes, fr.rowbase + rows, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  TC_CUDA(cudaStreamSynchronize(s));
+  const uint64_t NI = NI32;
+  fr.nitems = NI;
+  fr.items = g.scratch[kSlotItems].get<uint4>(NI * (per_vertex ? 2 : kItemStrideTotal), s);
+  if (rows) fr.masks = g.scratch[kSlotMasks].get<uint8_t>(fr.mask_bytes + 32, s);
   pl.mark("fr_rowbase");
   if (NI) {
     const unsigned grid = grid_gs(ceil_div64(e1 - e0, kScatterR), dev);
     if (per_vertex)
       k_fr_scatter<true><<<grid, kT, 0, s>>>(geo, e0, e1, cnt, fr.items, fr.rowbase,
-                                             fr.u_lo, fr.masks, sums.get());
+                                             fr.u_lo, fr.masks, sums);
     else
       k_fr_scatter<false><<<grid, kT, 0, s>>>(geo, e0, e1, cnt, fr.items, nullptr, 0,
-                                              nullptr, sums.get());
+                                              nullptr, sums);
     TC_LAUNCH();
     ++kl;
   }
@@ -359,13 +367,16 @@ int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Front
     fr.pivots = h[3];
   }
   pl.mark("fr_segs");
-  const Sums hs = read_scalar(sums.get(), s);
+  return kl;
+}
+
+void read_frontier_sums(Frontier& fr, cudaStream_t s) {
+  const Sums hs = read_scalar(static_cast<const Sums*>(fr.sums), s);
   fr.W = hs.W;
   fr.J = hs.J;
   fr.hot = hs.hot;
   fr.items_c = hs.items_c;
   fr.nitems = hs.claims;  // this part's items (the slots of other parts' edges stay empty)
-  return kl;
 }
 
 }  // namespace tcb

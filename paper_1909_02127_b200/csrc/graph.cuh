@@ -44,7 +44,7 @@ struct Scratch {
 };
 enum ScratchSlot {
   kSlotCnt, kSlotIn, kSlotItems, kSlotRowBase, kSlotWoff, kSlotWsegs,
-  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotSsegs, kSlotPacked, kSlotCount
+  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotSsegs, kSlotPacked, kSlotSums, kSlotCount
 };
 }  // namespace tcb
 
@@ -130,10 +130,13 @@ struct Frontier {
   uint4* ssegs = nullptr;  // small CTA-bin pivots, one segment each (k_join_small)
   uint64_t e0 = 0, e1 = 0, nitems = 0, nw = 0, nc = 0, ns = 0, pivots = 0, mask_bytes = 0;
   uint32_t u_lo = 0, u_hi = 0;  // rows the part's edges come from (inclusive)
-  uint64_t W = 0, J = 0, hot = 0, items_c = 0;
+  uint64_t W = 0, J = 0, hot = 0, items_c = 0;  // counters: filled by read_frontier_sums (stats only)
+  const void* sums = nullptr;
 };
 // Returns the number of kernels launched.
 int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Frontier& fr);
+// The frontier's counters (W, J, hot, items) -- a read, so only for stats.
+void read_frontier_sums(Frontier& fr, cudaStream_t s);
 
 // Per-vertex hit-mask layout of row u (closed form, no per-edge scan).  Row u
 // has d = d+(u) out-edges, the last h of them hot (colH[O, O+h), O = offH[u]),
