@@ -41,7 +41,7 @@ namespace {
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= 48)
+constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= kWarpMaxDeg = 64)
 constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counters (16-bit halves: 16 KB)
 constexpr uint32_t kCtaSmemSlots = 1024;     // cold-member hash table in SMEM (4 KB)
 #ifndef TCB_HOT_WIN
@@ -359,7 +359,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
   return hits;
 }
 
-// Warp bin: each warp takes whole segments of small pivots (d+ <= 48) with a
+// Warp bin: each warp takes whole segments of small pivots (d+ <= 64) with a
 // warp-private 128-slot hash table; the CTA shares the per-vertex top-rank
 // counters (dynamic SMEM, pv only).
 template <bool kPerVertex>
