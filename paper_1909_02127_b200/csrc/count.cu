@@ -839,7 +839,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
 constexpr int kRowWarps = 8;
 constexpr int kRowULight = 8;   // light rows: a warp each, many warps per SM
 constexpr int kRowUHeavy = 16;  // heavy rows: latency-bound on the byte loads (A/B: profiles/README.md)
-constexpr uint32_t kRowHeavy = 128;
+// rows with more item-steps go to the CTA-per-row kernel (A/B at C4: 128 ->
+// 2048 moves the 128..2048-step rows to the warp-per-row kernel, where they
+// run faster: row pass 11.5 -> 9.9 ms; 4096 overloads single warps)
+#ifndef TCB_ROW_HEAVY
+#define TCB_ROW_HEAVY 2048
+#endif
+constexpr uint32_t kRowHeavy = TCB_ROW_HEAVY;
 
 struct RowLanes {
   uint32_t w, G, sub;  // lanes per sub-group, sub-groups, this lane's sub-group
