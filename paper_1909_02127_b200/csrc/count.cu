@@ -837,7 +837,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
 //   k_pv_rows_heavy  one CTA per listed row, its 8 warps splitting each
 //                    group's items, partial counters reduced in SMEM
 constexpr int kRowWarps = 8;
-constexpr int kRowULight = 8;   // light rows: a warp each, many warps per SM
+#ifndef TCB_ROWU_LIGHT
+#define TCB_ROWU_LIGHT 8
+#endif
+constexpr int kRowULight = TCB_ROWU_LIGHT;  // light rows: a warp each, many warps per SM
 constexpr int kRowUHeavy = 16;  // heavy rows: latency-bound on the byte loads (A/B: profiles/README.md)
 // rows with more item-steps go to the CTA-per-row kernel (A/B at C4: 128 ->
 // 2048 moves the 128..2048-step rows to the warp-per-row kernel, where they

@@ -82,7 +82,10 @@ constexpr uint32_t kHotBits = 1u << 16;
 // warp bin: d+(v) <= 64 (128-slot warp table; A/B at C4: 48 -> 64 saves 0.4 ms,
 // 96 costs 0.5 ms at C3)
 constexpr uint32_t kWarpMaxDeg = TCB_WARP_MAX_DEG;
-constexpr uint32_t kWarpSegItems = 64;  // items per warp-bin segment
+#ifndef TCB_WARP_SEG_ITEMS
+#define TCB_WARP_SEG_ITEMS 64
+#endif
+constexpr uint32_t kWarpSegItems = TCB_WARP_SEG_ITEMS;  // items per warp-bin segment
 #ifndef TCB_CTA_SEG_ITEMS
 #define TCB_CTA_SEG_ITEMS 512
 #endif
