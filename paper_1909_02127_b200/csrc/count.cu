@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
 // by a multiply (b*0x00204081 & 0x01010101).  Warp-bin items' bytes are zero
 // (memset): their hits are counted in k_join_warp.
 //   k_pv_rows        one warp per light row, 32 rows per queue grab (top rank
-//                    down); rows with more than kRowHeavy item-steps are
+//                    down); rows with more than row_heavy_threshold item-steps are
 //                    appended to a list instead
 //   k_pv_rows_heavy  one CTA per listed row, its 8 warps splitting each
 //                    group's items, partial counters reduced in SMEM
@@ -842,13 +842,21 @@ constexpr int kRowWarps = 8;
 #endif
 constexpr int kRowULight = TCB_ROWU_LIGHT;  // light rows: a warp each, many warps per SM
 constexpr int kRowUHeavy = 16;  // heavy rows: latency-bound on the byte loads (A/B: profiles/README.md)
-// rows with more item-steps go to the CTA-per-row kernel (A/B at C4: 128 ->
-// 2048 moves the 128..2048-step rows to the warp-per-row kernel, where they
-// run faster: row pass 11.5 -> 9.9 ms; 4096 overloads single warps)
+// Rows with more item-steps than the threshold go to the CTA-per-row kernel.
+// With many rows the warp-per-row kernel balances rows of up to 2048 steps
+// and runs them faster (C4 whole count: 128 -> 2048 takes the row pass from
+// 11.5 to 9.9 ms; 4096 overloads single warps); a multi-GPU part holding few,
+// long rows (the top ranks) needs the CTA kernel sooner.  Threshold =
+// rows / 8192 clamped to [kRowHeavyMin, kRowHeavyMax].
 #ifndef TCB_ROW_HEAVY
 #define TCB_ROW_HEAVY 2048
 #endif
-constexpr uint32_t kRowHeavy = TCB_ROW_HEAVY;
+constexpr uint32_t kRowHeavyMax = TCB_ROW_HEAVY;
+constexpr uint32_t kRowHeavyMin = 128;
+__host__ __device__ __forceinline__ uint32_t row_heavy_threshold(uint64_t rows) {
+  const uint64_t t = rows / 8192;
+  return (uint32_t)(t < kRowHeavyMin ? kRowHeavyMin : t > kRowHeavyMax ? kRowHeavyMax : t);
+}
 
 struct RowLanes {
   uint32_t w, G, sub;  // lanes per sub-group, sub-groups, this lane's sub-group
@@ -1008,7 +1016,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
     const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t u_hi,
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,
-    unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
+    unsigned int* __restrict__ nheavy, uint32_t heavy_thr, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
   __shared__ uint2 s_spread[256];
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
@@ -1036,7 +1044,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
         const RowMasks rm(dl, Ol, hl);
         const uint32_t C = (uint32_t)(rm.c_hi - rm.c_lo);
         const uint32_t steps = C > 16 ? (dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
-        if (steps > kRowHeavy) {
+        if (steps > heavy_thr) {
           heavy[atomicAdd(nheavy, 1u)] = ul;
           work = false;
         }
@@ -1343,7 +1351,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
       TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_pv_rows_heavy, kRowWarps * 32, rsm));
       k_pv_rows<<<(unsigned)(sms * std::max(rocc, 1)), kRowWarps * 32, rsm, s>>>(
           g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, fr.u_hi, g.h0, n - rcnt, rcnt,
-          lq.get(), heavy, rq.get() + 2, t_rank);
+          lq.get(), heavy, rq.get() + 2, row_heavy_threshold((uint64_t)fr.u_hi - fr.u_lo + 1), t_rank);
       TC_LAUNCH();
       ++launches;
       pl.mark("pv_rows_light");
