@@ -43,7 +43,10 @@ constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
 constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= kWarpMaxDeg = 64)
 constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counters (16-bit halves: 16 KB)
-constexpr uint32_t kCtaSmemSlots = 1024;     // cold-member hash table in SMEM (4 KB)
+#ifndef TCB_CTA_SMEM_SLOTS
+#define TCB_CTA_SMEM_SLOTS 1024
+#endif
+constexpr uint32_t kCtaSmemSlots = TCB_CTA_SMEM_SLOTS;  // cold-member hash table in SMEM (4 KB)
 #ifndef TCB_HOT_WIN
 #define TCB_HOT_WIN 2
 #endif
