@@ -168,6 +168,7 @@ def reference_cpu_sample(off: np.ndarray, nb: np.ndarray, budget_s: float, E: in
     if not os.path.exists(REF_SO):
         return None
     ref = Ref()
+    t_wall0 = time.perf_counter()
     if rg is None:
         rg = ref.graph(off, nb)
     # visits the final level makes for seed u: deg(u) per level-1 row (u,w),
@@ -204,6 +205,7 @@ def reference_cpu_sample(off: np.ndarray, nb: np.ndarray, budget_s: float, E: in
         "kind": "reference",
         "t_full_est_ms": t_full_ms,
         "t_sample_est_ms": t_est_ms,
+        "sample_wall_s": time.perf_counter() - t_wall0,
         "calibration": cal,
         "sample": (f"trimatch::count_triangles path through its public API: filter_candidates on the full "
                    f"graph ({s['filter_ms']:.0f} ms), expand_level L1 for {seeds.size} of {order.size} seeds "
@@ -259,6 +261,56 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+def measured_reference_counts(configs=("C1", "C2")):
+    """The reference's own trimatch::count_triangles (oracle/_ref, all host
+    cores, lookahead=2) timed in full -- best of 3 -- on the configs where it
+    finishes in seconds (matcher.cpp:301-303)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle_ctypes import REF_SO, Ref
+    if not os.path.exists(REF_SO):
+        return None
+    out = {}
+    for name in configs:
+        off, nb, E = host_graph(CONFIGS[name])
+        rg = Ref().graph(off, nb)
+        best = None
+        T = 0
+        for _ in range(3):
+            t0 = time.perf_counter()
+            T = rg.count_triangles(lookahead=2, workers=0)
+            dt = (time.perf_counter() - t0) * 1e3
+            best = dt if best is None else min(best, dt)
+        out[name] = {"ms": best, "gteps": E / (best / 1e3) / 1e9, "triangles": int(T), "num_edges": int(E),
+                     "cores": os.cpu_count(), "runs": 3, "stat": "best of 3"}
+    return out
+
+
+def lib_sha256():
+    import hashlib
+    h = hashlib.sha256()
+    with open(os.path.join(ROOT, "paper_1909_02127_b200", "libtcb200.so"), "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()
+
+
+def measured_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the ncu capture made
+    for THIS build (profiles/ncu_traffic_<config>.json, written by
+    tools/ncu_traffic.py with the library's sha256); None when stale/absent."""
+    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except Exception:
+        return None, "absent"
+    if d.get("lib_sha256") != lib_sha256():
+        return None, f"stale ({path} measured another build)"
+    k = d.get("kernels", {}).get(kernel)
+    if not k:
+        return None, f"kernel {kernel} not in {path}"
+    return k, "measured (ncu --set full, this build)"
+
+
 # ---------------------------------------------------------------------------
 def main():
     a = parse()
@@ -273,26 +325,31 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # TCB_BENCH_SHARE_GPU=1 (plumbing check only): every rank on cuda:0 over gloo,
-    # so the multi-rank path can be exercised on a 1-GPU box
+    # TCB_BENCH_SHARE_GPU=1 (plumbing check only): every rank on cuda:0
     share = os.environ.get("TCB_BENCH_SHARE_GPU") == "1"
     if share:
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        # torch.distributed is the rendezvous only (gloo: NCCL id, barriers,
+        # max over ranks); the count's allreduce is the library's own NCCL
+        # communicator on the count stream (tc_count_allreduce)
+        dist.init_process_group("gloo")
+        from paper_1909_02127_b200 import dist as tdist
+        comm = tdist.init_comm(local)
     cfg = CONFIGS[a.config]
     kind, scale, param, per_vertex, desc = cfg
     per_vertex = per_vertex and not a.no_per_vertex
     n = 1 << scale
+    stream = torch.cuda.Stream(dev)  # a real stream: the handle's work and the events share it
 
     # ---- input: deterministic synthetic edge list generated on the device ----
     m = tc.gen_num_edges(gen_kind(tc, kind), scale, param)
-    pairs = torch.empty(2 * m, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(stream):
+        pairs = torch.empty(2 * m, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
     tc.generate(gen_kind(tc, kind), scale, param, out=pairs, device=local)
     rep = tc.BuildReport()
     g = tc.build_graph_from_pairs(pairs, n, rep, device=local, m=m)
@@ -300,20 +357,18 @@ def main():
     del pairs
     torch.cuda.empty_cache()
     E = g.num_edges()
-    stream = torch.cuda.current_stream(dev)
     g.set_stream(stream.cuda_stream)
 
-    total = torch.zeros(1, dtype=torch.int64, device=dev)
-    pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
-    opts = tc.MatchOptions(per_vertex=per_vertex, part_index=rank, part_count=world)
+    with torch.cuda.stream(stream):
+        total = torch.zeros(1, dtype=torch.int64, device=dev)
+        pv = torch.zeros(n, dtype=torch.int64, device=dev) if per_vertex else None
+    torch.cuda.synchronize()
+    opts = tc.MatchOptions(per_vertex=per_vertex)
 
-    def step():
-        st = tc.count_triangles_into(g, total, pv, opts, stats=True)
-        if world > 1:
-            dist.all_reduce(total)
-            if pv is not None:
-                dist.all_reduce(pv)
-        return st
+    def step(stats=False, work=False):
+        if comm is not None:
+            return comm.count_into(g, total, pv, opts, stats=stats)
+        return tc.count_triangles_into(g, total, pv, opts, stats=stats, work_counters=work)
 
     for _ in range(a.warmup):
         step()
@@ -322,41 +377,37 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stats = []
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(a.steps):
-            stats.append(step())
+            step()
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+        ms = tdist.max_over_ranks(ms)
     T = int(total.item())
-    join_ms = float(np.mean([s["join_ms"] for s in stats]))
-    s0 = stats[0]
+    # phase split (untimed counts with CUDA events) and the work counters
+    stats = [step(stats=True) for _ in range(3)]
+    sw = tc.count_triangles_into(g, total, pv, tc.MatchOptions(per_vertex=per_vertex, part_index=rank,
+                                                               part_count=world),
+                                 stats=True, work_counters=True)
+    join_ms = float(np.mean([s_["join_ms"] for s_ in stats]))
     if world > 1:
-        jt = torch.tensor([join_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(jt, op=dist.ReduceOp.MAX)
-        join_ms = float(jt.item())
-    launches = int(sum(s["kernel_launches"] for s in stats))
+        join_ms = tdist.max_over_ranks(join_ms)
+    launches = int(sw["kernel_launches"]) * a.steps
 
     # ---- e2e: drop-in count_triangles(const Graph&) with host buffers ----
-    # the host Graph = the symmetric CSR (exported once, pinned)
+    # the host Graph = the symmetric CSR (exported once); pinned (the contract)
+    # and pageable (a caller's std::vector / numpy arrays) legs
     ro_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
     nb_h = torch.empty(max(2 * E, 1), dtype=torch.int32, pin_memory=True)
     g.export_csr(ro_h, nb_h)
     tot_h = torch.zeros(1, dtype=torch.int64, pin_memory=True)
     pv_h = torch.zeros(n, dtype=torch.int64, pin_memory=True) if per_vertex else None
-    pv_d = torch.zeros(n, dtype=torch.int64, device=dev) if (per_vertex and world > 1) else None
-    tot_d = torch.zeros(1, dtype=torch.int64, device=dev)
 
-    # the box's host->device link rate for the same bytes (a plain pinned copy):
-    # e2e is bound below by h2d_bytes / this rate, which varies across boxes
     link_gbps = None
     if E:
         tmp = torch.empty_like(nb_h, device=dev)
@@ -370,54 +421,50 @@ def main():
         link_gbps = max(rates)
         del tmp
 
-    def e2e_step():
-        ge = tc.graph_from_csr(ro_h, nb_h, n, E, device=local)        # H2D + orientation
-        if world == 1:
-            tc.count_triangles_into(ge, tot_h, pv_h, opts, sync=True)  # count + D2H
+    def e2e_step(ro, nb, tot_out, pv_out):
+        ge = tc.graph_from_csr(ro, nb, n, E, device=local)          # H2D + orientation + in-edge index
+        if comm is not None:
+            comm.count_into(ge, tot_out, pv_out, opts, sync=True)  # count + allreduce + D2H
         else:
-            tc.count_triangles_into(ge, tot_d, pv_d, opts, sync=True)
-            dist.all_reduce(tot_d)
-            if pv_d is not None:
-                dist.all_reduce(pv_d)
-            tot_h.copy_(tot_d)
-            if pv_h is not None:
-                pv_h.copy_(pv_d)
-            torch.cuda.synchronize()
+            tc.count_triangles_into(ge, tot_out, pv_out, opts, sync=True)  # count + D2H
         del ge
 
-    e2e_step()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(a.e2e_steps):
-        e2e_step()
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / a.e2e_steps
-    if world > 1:
-        et = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e_ms = float(et.item())
+    def time_e2e(ro, nb, tot_out, pv_out, steps):
+        e2e_step(ro, nb, tot_out, pv_out)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            e2e_step(ro, nb, tot_out, pv_out)
+        torch.cuda.synchronize()
+        e = (time.perf_counter() - t0) * 1e3 / steps
+        return tdist.max_over_ranks(e) if world > 1 else e
+
+    e2e_ms = time_e2e(ro_h, nb_h, tot_h, pv_h, a.e2e_steps)
     assert int(tot_h[0]) == T, (int(tot_h[0]), T)
+    # pageable leg: plain numpy arrays
+    ro_p = ro_h.numpy().view(np.uint64).copy()
+    nb_p = nb_h.numpy().view(np.uint32).copy()
+    tot_p = np.zeros(1, np.uint64)
+    pv_p = np.zeros(n, np.uint64) if per_vertex else None
+    e2e_pg_ms = time_e2e(ro_p, nb_p, tot_p, pv_p, max(1, a.e2e_steps - 1))
+    assert int(tot_p[0]) == T
+    del ro_p, nb_p
     h2d = 8 * (n + 1) + 4 * 2 * E
     d2h = 8 + (8 * n if per_vertex else 0)
 
     peak, peak_kind = peaks()
-    alg_bytes = s0["alg_bytes"]          # this rank's share (the parts sum to the graph's B_alg)
-    pivot_bytes = s0["probe_bytes"]
+    alg_bytes = sw["alg_bytes"]          # this rank's share (the parts sum to the graph's B_alg)
+    impl_bytes = sw["probe_bytes"]
     if world > 1:
-        ab = torch.tensor([alg_bytes, pivot_bytes], dtype=torch.float64, device=dev)
+        ab = torch.tensor([alg_bytes, impl_bytes], dtype=torch.float64)
         dist.all_reduce(ab)
-        alg_bytes, pivot_bytes = float(ab[0]), float(ab[1])
-    achieved = alg_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", f"ncu_{a.config}_join_traffic.json")
-    if os.path.exists(tr_path):
-        try:
-            traffic = json.load(open(tr_path)).get("dram_bytes_per_step")
-        except Exception:
-            traffic = None
-
+        alg_bytes, impl_bytes = float(ab[0]), float(ab[1])
+    # roofline of the dominant phase (advance + join + per-vertex row pass):
+    # the bytes the implemented algorithm must stream / its device time
+    achieved = impl_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
+    traffic, traffic_src = measured_traffic(a.config, "k_join_cta")
     line = {
         "metric": "triangle-count GTEPS (|E|/time)",
         "value": E / (ms / 1e3) / 1e9,
@@ -434,8 +481,10 @@ def main():
         "config": {
             "workload": desc, "config": a.config, "generator": f"{kind} scale={scale} param={param} (SURVEY 8d splitmix)",
             "num_vertices": n, "num_edges": int(E), "raw_edges": int(m), "triangles": T,
-            "per_vertex": per_vertex, "parallelism": f"work-ranges x{world} + NCCL allreduce" if world > 1 else "1 GPU",
-            "l2": "inputs larger than L2 (oriented CSR + frontier >> 126 MB); no flush",
+            "per_vertex": per_vertex,
+            "parallelism": (f"pivot ranges x{world} + one NCCL allreduce (tc_count_allreduce)" if world > 1
+                            else "1 GPU"),
+            "l2": "inputs larger than L2 (oriented CSR + in-edge index + masks >> 126 MB); no flush",
             "build_ms": build_ms, "self_loops_removed": rep.self_loops_removed,
             "duplicate_entries_removed": rep.duplicate_entries_removed,
         },
@@ -443,31 +492,49 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "h2d_link_gbps": link_gbps,
                 "h2d_floor_ms": (h2d / link_gbps / 1e6) if link_gbps else None,
-                "path": "tc_graph_from_csr(host pinned CSR) + tc_count(host outputs)"},
+                "path": "tc_graph_from_csr(host pinned CSR) + tc_count(host outputs)",
+                "pageable": {"value": E / (e2e_pg_ms / 1e3) / 1e9, "ms_per_step": e2e_pg_ms,
+                             "path": "the same from pageable numpy arrays (a caller's std::vector)"}},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_kind": peak_kind,
-            "kernel": "join phase: k_join_warp + k_join_cta (advance + fused SMEM join) + k_pv_rows(_heavy) (per-vertex fold)",
-            "alg_bytes_per_step": alg_bytes, "join_ms": join_ms,
-            "model": "B_alg = 4W + 12|E+| + 8(|V|+1) + 8|V| (SURVEY 8d wedge-stream bytes)",
-            "pivot_model_bytes": pivot_bytes,
-            "pivot_model_frac": pivot_bytes / (join_ms / 1e3) / 1e9 / peak / max(1, world) if join_ms > 0 else 0,
-            "wedges_probed": s0["wedges"], "W": s0["dag_W"],
+            "traffic": traffic["dram_bytes"] if traffic else None, "traffic_source": traffic_src,
+            "peak_kind": peak_kind,
+            "kernel": "join phase: k_join_cta (advance + fused SMEM join, dominant) + k_join_warp/small "
+                      "+ k_pv_rows(_heavy) (per-vertex row pass)",
+            "model": "implemented bytes: 2 B per hot candidate + 4 B per cold candidate + 28 B per in-edge "
+                     "(record + row geometry + pivot-row member) + per-vertex masks written and read + counters",
+            "bytes_per_step": impl_bytes, "join_ms": join_ms,
+            "wedges_probed": sw["wedges"],
+            "wedge_stream_equiv": {"B_alg": alg_bytes, "W": sw["dag_W"],
+                                   "ratio": alg_bytes / (join_ms / 1e3) / 1e9 / peak / max(1, world),
+                                   "note": "SURVEY 8d B_alg = 4W + 12|E+| + 8(|V|+1) + 8|V| over the join time: "
+                                           "counts W wedge reads the pivot join never makes (J << W), so it "
+                                           "is a model-equivalent rate, not a bandwidth"},
         },
-        "phases_ms": {"frontier": float(np.mean([s["frontier_ms"] for s in stats])), "join": join_ms,
-                      "reduce": float(np.mean([s["reduce_ms"] for s in stats]))},
+        "phases_ms": {"frontier": float(np.mean([s_["frontier_ms"] for s_ in stats])), "join": join_ms,
+                      "reduce": float(np.mean([s_["reduce_ms"] for s_ in stats]))},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if traffic:
+        line["roofline"]["traffic_kernel_ms"] = traffic.get("ms")
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             ro_np = ro_h.numpy().view(np.uint64)
             nb_np = nb_h.numpy().view(np.uint32)[: 2 * E]
-            line["cpu_baseline"] = reference_cpu_sample(ro_np, nb_np, a.cpu_budget_s, E)
+            cb = reference_cpu_sample(ro_np, nb_np, a.cpu_budget_s, E)
+            if cb is not None:
+                cb["kind"] = "reference"
+                cb["value_is"] = ("extrapolated: the full reference count at this config does not finish "
+                                  "(~2.6e12 visits); bounded sample + calibration, see sample")
+                cb["measured"] = measured_reference_counts()
+            line["cpu_baseline"] = cb
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

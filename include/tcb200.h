@@ -25,6 +25,10 @@
  * tc_graph_write_csr_cache    trimatch::write_csr_cache  io.hpp:39 (io.cpp:167-177)
  * tc_csr_cache_parse          trimatch::read_csr_cache   io.hpp:40 (io.cpp:187-220)
  * tc_graph_destroy            ~Graph
+ * tc_comm_init_rank / tc_count_allreduce   multi-GPU count, one process per GPU
+ * tc_multi_create / tc_count_multi         multi-GPU count, one process (SURVEY 8b
+ *                             tc_count_multi; the reference is single-node CPU,
+ *                             this is the north-star's 8-GPU split)
  * tc_last_error               the what() of the exception the reference throws
  *
  * Errors: the reference throws C++ exceptions; here each maps to a status code
@@ -46,7 +50,7 @@
 extern "C" {
 #endif
 
-#define TCB200_ABI_VERSION 2
+#define TCB200_ABI_VERSION 3
 
 typedef enum tc_status {
   TC_OK = 0,
@@ -54,7 +58,7 @@ typedef enum tc_status {
   TC_ERANGE = 2,       /* std::out_of_range, or a size past the 32-bit id / edge limits */
   TC_ENOMEM = 3,       /* device allocation failed */
   TC_ECUDA = 4,        /* CUDA runtime error (message in tc_last_error) */
-  TC_ENCCL = 5,        /* reserved for the multi-GPU allreduce */
+  TC_ENCCL = 5,        /* NCCL error in the multi-GPU allreduce */
   TC_EUNSUPPORTED = 6, /* keep_listings etc. (out of scope on the GPU path) */
   TC_EPARSE = 7,       /* trimatch::ParseError */
   TC_EIO = 8           /* trimatch::IoError */
@@ -80,28 +84,31 @@ typedef struct tc_graph_info {
 /* trimatch::MatchOptions (matcher.hpp:84-88) + GPU extensions. */
 typedef struct tc_count_opts {
   int lookahead;        /* validated in {0,1,2} like matcher.cpp:250-252; count-neutral */
-  int keep_listings;    /* must be 0: listings are out of scope on the GPU path */
+  int keep_listings;    /* must be 0 here: listings are tc_list_triangles */
   uint32_t part_index;  /* multi-GPU: this rank's share of the degree-weighted */
-  uint32_t part_count;  /*   work ranges (0/1 = whole graph)                 */
+  uint32_t part_count;  /*   pivot rank ranges (0/1 = whole graph)            */
   int sync;             /* 1: block until outputs are final (default for 0-init = async
                            only when both outputs are device pointers) */
+  int work_counters;    /* 1 (with stats): also count W, J, items (one extra pass) */
 } tc_count_opts;
 
 /* trimatch::MatchStats analogue (matcher.hpp:69-82) for the GPU path. */
 typedef struct tc_count_stats {
   double total_ms;        /* device time of the whole tc_count (CUDA events) */
-  double frontier_ms;     /* level-1 frontier: in-edge items + work plan      */
-  double join_ms;         /* advance + fused join kernels                      */
-  double reduce_ms;       /* per-vertex gather/flush + total                  */
-  uint64_t pivots;        /* vertices v with d+(v)>0 and >=1 useful in-edge   */
-  uint64_t items;         /* oriented edges (u->v) whose wedge suffix is non-empty */
-  uint64_t wedges;        /* J = candidate wedges probed = sum of suffix lengths */
-  uint64_t segments;      /* work segments scheduled (warp + CTA bins)        */
+  double frontier_ms;     /* level-1 frontier plan: pivot classes + work segments */
+  double join_ms;         /* advance + fused join kernels + per-vertex row pass */
+  double reduce_ms;       /* per-vertex gather + total                         */
+  uint64_t pivots;        /* vertices v with d+(v)>0 and >=1 useful in-edge   (work_counters) */
+  uint64_t items;         /* in-edges (u->v) whose wedge suffix is non-empty  (work_counters) */
+  uint64_t wedges;        /* J = candidate wedges probed = sum of suffix lengths (work_counters) */
+  uint64_t segments;      /* reserved */
   uint64_t join_launches; /* join kernel launches                              */
-  double dag_W;           /* W = sum_{u->v} d+(v) (SURVEY 8d wedge-stream model) */
-  double alg_bytes;       /* B_alg = 4W + 12|E+| + 8(|V|+1) [+8|V| per-vertex]   */
-  double probe_bytes;     /* bytes the pivot join must read: 4J + 8 items + 4|E+| */
+  double dag_W;           /* W = sum_{u->v} d+(v) (SURVEY 8d wedge-stream model; work_counters) */
+  double alg_bytes;       /* B_alg = 4W + 12|E+| + 8(|V|+1) [+8|V| per-vertex]  (work_counters) */
+  double probe_bytes;     /* bytes the implemented join streams (work_counters) */
   uint64_t kernel_launches; /* all libtcb200 kernels this call launched */
+  uint64_t part_first_vertex; /* this part's pivot rank range [first, last) */
+  uint64_t part_last_vertex;
 } tc_count_stats;
 
 /* ---- graph construction ------------------------------------------------ */
@@ -142,8 +149,43 @@ tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint
                    tc_count_stats* stats);
 
 /* Multi-GPU split: bounds[0..parts] (parts+1 u64, host) of the degree-weighted
- * oriented-edge ranges tc_count uses for part_index/part_count. */
+ * pivot rank ranges tc_count uses for part_index/part_count: part p counts the
+ * triangles whose middle vertex (in (deg,id) order) has rank in
+ * [bounds[p], bounds[p+1]).  Computed once per graph and part count. */
 tc_status tc_partition_bounds(tc_graph* g, uint32_t parts, uint64_t* bounds);
+
+/* ---- multi-GPU ----------------------------------------------
+ * Every GPU holds a replica of the graph (built from the same edge list or
+ * CSR: no communication).  Part p of P counts the triangles whose middle
+ * vertex lies in its degree-weighted pivot range (tc_partition_bounds); ONE
+ * ncclAllReduce(ncclUint64, ncclSum) over NVLink of [per-vertex | total] on the
+ * count stream combines the parts.  Outputs as tc_count (host or device of the
+ * handle's device; with device outputs and opts->sync = 0 the call does not
+ * block). */
+typedef struct tc_comm tc_comm;
+typedef struct tc_multi tc_multi;
+#define TC_COMM_ID_BYTES 128
+
+/* One process per GPU (torchrun style): rank 0 makes the 128-byte id, the
+ * host framework hands it to every rank, each rank joins with its device. */
+tc_status tc_comm_unique_id(void* id);
+tc_status tc_comm_init_rank(const void* id, int nranks, int rank, int device, tc_comm** out);
+void tc_comm_destroy(tc_comm* comm);
+/* This rank's part (part_index = rank, part_count = nranks) + the allreduce:
+ * every rank receives the whole graph's total / per-vertex counts. */
+tc_status tc_count_allreduce(tc_comm* comm, tc_graph* g, const tc_count_opts* opts, uint64_t* total,
+                             uint64_t* per_vertex, tc_count_stats* stats);
+
+/* One process driving several GPUs (ncclCommInitAll, one stream per GPU):
+ * devices[p] = the device of part p (a device may repeat: its parts run back
+ * to back and are summed locally before the allreduce). */
+tc_status tc_multi_create(const int* devices, int nparts, tc_multi** out);
+void tc_multi_destroy(tc_multi* m);
+/* graphs[p] = the replica on devices[p] (one handle may serve several parts of
+ * its device).  Outputs on the host or on part 0's device; blocks until final.
+ * stats (nullable): part 0's phases, total_ms = the slowest part. */
+tc_status tc_count_multi(tc_multi* m, tc_graph* const* graphs, const tc_count_opts* opts, uint64_t* total,
+                         uint64_t* per_vertex, tc_count_stats* stats);
 
 /* ---- adjacent formats ------------------------------------- */
 
@@ -194,6 +236,14 @@ uint64_t tc_gen_num_edges(int kind, int scale, int param);
 tc_status tc_generate(int kind, int scale, int param, int device, uint32_t* pairs);
 
 void tc_free(void* p);
+
+/* Device memory: graph handles and count scratch come from a caching
+ * allocator (freed blocks are reused by the next handle / count without
+ * remapping).  The cache is bounded (TCB_CACHE_MB, default 40% of the
+ * device); this returns every cached block of `device` (-1 = all) to the
+ * driver and reports the bytes released, e.g. before a host framework in the
+ * same process allocates. */
+uint64_t tc_release_cached_memory(int device);
 const char* tc_last_error(void);
 int tc_abi_version(void);
 

@@ -371,3 +371,193 @@ void oracle_dag_stats(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n,
   *J = j;
   if (max_dplus) *max_dplus = mx;
 }
+
+/* ---- degree-ordered DAG count: the independent big-config checker -------- */
+
+/* SURVEY.md 8c "planned GPU algorithm, validated on the host": orient by
+ * (deg, id), every triangle a<b<c (ranks) is found once with pivot b -- for
+ * each in-edge a->b scan the suffix of N+(a) after b and test membership in
+ * N+(b).  Same counts as segmented_intersect with above_dst_only
+ * (frontier.cpp:51-81) because both are total orders; the
+ * per-vertex histogram is t[a], t[b], t[c] += 1 per triangle, as the
+ * reference's listings give it (frontier.cpp:65-79, matcher.hpp:92).  It
+ * exists because the id-order restatement above needs hours at C5 (RMAT s26
+ * ef32); tests/test_oracle.py pins it against the reference goldens before it
+ * is trusted.  J = sum_a C(d+(a),2) bitmap probes instead of the id-order
+ * merge's sum over id-ordered pairs. */
+static int cmp_u32b(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return (x > y) - (x < y);
+}
+
+uint64_t oracle_count_dag(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n,
+                          uint64_t* per_vertex, int threads) {
+#ifdef _OPENMP
+  if (threads <= 0) threads = omp_get_max_threads();
+#else
+  threads = 1;
+#endif
+  if (per_vertex) memset(per_vertex, 0, (size_t)n * sizeof(uint64_t));
+  if (n == 0) return 0;
+  /* rank = position of (deg, id): counting sort by degree, stable in id */
+  uint64_t maxd = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint64_t d = offsets[v + 1] - offsets[v];
+    if (d > maxd) maxd = d;
+  }
+  uint64_t* bucket = (uint64_t*)calloc(maxd + 2, sizeof(uint64_t));
+  for (uint64_t v = 0; v < n; ++v) ++bucket[offsets[v + 1] - offsets[v] + 1];
+  for (uint64_t d = 0; d <= maxd; ++d) bucket[d + 1] += bucket[d];
+  uint32_t* order = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+  uint32_t* rank = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint64_t r = bucket[offsets[v + 1] - offsets[v]]++;
+    order[r] = (uint32_t)v;
+    rank[v] = (uint32_t)r;
+  }
+  free(bucket);
+  /* oriented CSR in rank space (rows sorted) and its transpose (in-edges) */
+  uint64_t* oo = (uint64_t*)calloc((size_t)n + 1, sizeof(uint64_t));
+  uint64_t* io = (uint64_t*)calloc((size_t)n + 1, sizeof(uint64_t));
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4096)
+  for (int64_t rr = 0; rr < (int64_t)n; ++rr) {
+    const uint32_t v = order[rr];
+    uint64_t c = 0;
+    for (uint64_t k = offsets[v]; k < offsets[v + 1]; ++k) c += rank[nbrs[k]] > (uint32_t)rr;
+    oo[rr + 1] = c;
+    io[rr + 1] = (offsets[v + 1] - offsets[v]) - c;
+  }
+  for (uint64_t r = 0; r < n; ++r) {
+    oo[r + 1] += oo[r];
+    io[r + 1] += io[r];
+  }
+  const uint64_t E = oo[n];
+  uint32_t* oc = (uint32_t*)malloc((E ? E : 1) * sizeof(uint32_t));
+  uint32_t* ic = (uint32_t*)malloc((E ? E : 1) * sizeof(uint32_t));
+  uint64_t* icur = (uint64_t*)malloc((size_t)n * sizeof(uint64_t));
+  memcpy(icur, io, (size_t)n * sizeof(uint64_t));
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1024)
+  for (int64_t rr = 0; rr < (int64_t)n; ++rr) {
+    const uint32_t v = order[rr];
+    uint64_t p = oo[rr];
+    for (uint64_t k = offsets[v]; k < offsets[v + 1]; ++k) {
+      const uint32_t x = rank[nbrs[k]];
+      if (x > (uint32_t)rr) {
+        oc[p++] = x;
+        const uint64_t q = __atomic_fetch_add(&icur[x], 1, __ATOMIC_RELAXED);
+        ic[q] = (uint32_t)rr;
+      }
+    }
+    if (p - oo[rr] > 1) qsort(oc + oo[rr], p - oo[rr], sizeof(uint32_t), cmp_u32b);
+  }
+  free(icur);
+  free(rank);
+  /* pivot join: per-thread membership bitmap and per-vertex counters */
+  const uint64_t words = ((uint64_t)n + 63) / 64;
+  uint64_t total = 0;
+  uint64_t** tl = (uint64_t**)calloc((size_t)threads, sizeof(uint64_t*));
+#pragma omp parallel num_threads(threads) reduction(+ : total)
+  {
+#ifdef _OPENMP
+    const int tid = omp_get_thread_num();
+#else
+    const int tid = 0;
+#endif
+    uint64_t* bm = (uint64_t*)calloc(words, sizeof(uint64_t));
+    uint64_t* t = per_vertex ? (uint64_t*)calloc((size_t)n, sizeof(uint64_t)) : NULL;
+    tl[tid] = t;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t bb = (int64_t)n - 1; bb >= 0; --bb) {
+      const uint32_t b = (uint32_t)bb;
+      const uint64_t b0 = oo[b], b1 = oo[b + 1];
+      if (b1 == b0 || io[b + 1] == io[b]) continue;
+      for (uint64_t k = b0; k < b1; ++k) bm[oc[k] >> 6] |= 1ull << (oc[k] & 63);
+      uint64_t hb = 0;
+      for (uint64_t q = io[b]; q < io[b + 1]; ++q) {
+        const uint32_t a = ic[q];
+        const uint32_t* na = oc + oo[a];
+        const uint64_t da = oo[a + 1] - oo[a];
+        uint64_t c = 0;
+        for (uint64_t k = upper_bound_u32(na, da, b); k < da; ++k) {
+          const uint32_t x = na[k];
+          if ((bm[x >> 6] >> (x & 63)) & 1) {
+            ++c;
+            if (t) ++t[x];
+          }
+        }
+        if (t) t[a] += c;
+        hb += c;
+      }
+      if (t) t[b] += hb;
+      total += hb;
+      for (uint64_t k = b0; k < b1; ++k) bm[oc[k] >> 6] = 0;
+    }
+    free(bm);
+  }
+  if (per_vertex) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t rr = 0; rr < (int64_t)n; ++rr) {
+      uint64_t s = 0;
+      for (int t = 0; t < threads; ++t) s += tl[t][rr];
+      per_vertex[order[rr]] = s;
+    }
+    for (int t = 0; t < threads; ++t) free(tl[t]);
+  }
+  free(tl);
+  free(oo);
+  free(io);
+  free(oc);
+  free(ic);
+  free(order);
+  return total;
+}
+
+/* ---- streamed generation for the big-config goldens ---------------------- */
+
+/* Edges [i0, i1) of the SURVEY 8d generators (kind 0 = RMAT/Kronecker,
+ * 1 = ER), bit-identical to oracle_gen_rmat / oracle_gen_er; perm (nullable)
+ * is the Kronecker relabelling of oracle_kron_perm.  Lets a driver build a
+ * 2^31-edge graph without holding the 17 GB pair array. */
+void oracle_gen_range(int kind, int scale, int param, uint64_t i0, uint64_t i1, const uint32_t* perm,
+                      uint32_t* pairs) {
+  const double A = .57, B = .19, C = .19;
+  const double AB = A + B, ABC = AB + C;
+  const uint64_t mask = (1ULL << scale) - 1;
+  (void)param;
+#pragma omp parallel for schedule(static)
+  for (int64_t ii = (int64_t)i0; ii < (int64_t)i1; ++ii) {
+    const uint64_t i = (uint64_t)ii;
+    uint64_t st = sm64(i * 0x100000001ULL + 12345ULL);
+    uint32_t u = 0, v = 0;
+    if (kind == 1) {
+      st = sm64(st);
+      u = (uint32_t)(st & mask);
+      st = sm64(st);
+      v = (uint32_t)(st & mask);
+    } else {
+      for (int b = 0; b < scale; ++b) {
+        st = sm64(st);
+        const double p = (double)(st >> 11) * 0x1.0p-53;
+        u |= (uint32_t)(p > AB) << b;
+        v |= (uint32_t)((p > A && p <= AB) || p > ABC) << b;
+      }
+      if (perm) {
+        u = perm[u];
+        v = perm[v];
+      }
+    }
+    pairs[2 * (i - i0)] = u;
+    pairs[2 * (i - i0) + 1] = v;
+  }
+}
+
+void oracle_kron_perm(int scale, uint32_t* perm) {
+  const uint64_t n = 1ULL << scale;
+  for (uint64_t i = 0; i < n; ++i) perm[i] = (uint32_t)i;
+  for (uint64_t i = n - 1; i >= 1; --i) {
+    const uint64_t j = sm64(0xABCDEFULL ^ i) % (i + 1);
+    const uint32_t t = perm[i];
+    perm[i] = perm[j];
+    perm[j] = t;
+  }
+}

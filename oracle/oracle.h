@@ -26,6 +26,12 @@ uint64_t oracle_rmat_num_edges(int scale, int edgefactor);
 void oracle_gen_rmat(int scale, int edgefactor, int permute, uint32_t* pairs);
 uint64_t oracle_er_num_edges(int scale, int avg_degree);
 void oracle_gen_er(int scale, int avg_degree, uint32_t* pairs);
+/* Edges [i0, i1) only (kind 0 = RMAT/Kronecker with perm = nullable
+ * relabelling from oracle_kron_perm, 1 = ER): the big-config driver
+ * (oracle/big_golden.c) streams a 2^31-edge graph through it. */
+void oracle_gen_range(int kind, int scale, int param, uint64_t i0, uint64_t i1, const uint32_t* perm,
+                      uint32_t* pairs);
+void oracle_kron_perm(int scale, uint32_t* perm);
 
 /* build_graph restatement (graph.cpp:33-85).  Returns 0 on success, -1 when an
  * id is out of range (the reference throws std::invalid_argument,
@@ -43,6 +49,14 @@ void oracle_free(void* p);
  * count_triangles(keep_listings=true) returns, matcher.hpp:92). */
 uint64_t oracle_count(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n,
                       uint64_t* per_vertex, int threads);
+
+/* Degree-ordered DAG count (pivot join over the (deg,id) orientation, the
+ * SURVEY.md 8c host-validated algorithm): same total and per-vertex array as
+ * oracle_count, orders of magnitude faster on skewed graphs.  The independent
+ * checker for configs where oracle_count does not finish (C5); pinned against
+ * the reference goldens by tests/test_oracle.py. */
+uint64_t oracle_count_dag(const uint64_t* offsets, const uint32_t* nbrs, uint32_t n,
+                          uint64_t* per_vertex, int threads);
 
 /* Brute force a<b<c over has_edge, n <= 5000 guard.
  * Returns UINT64_MAX when the guard trips. */

@@ -56,6 +56,8 @@ class Oracle:
         L.oracle_free.argtypes = [C.c_void_p]
         L.oracle_count.restype = C.c_uint64
         L.oracle_count.argtypes = [u64p, u32p, C.c_uint32, u64p, C.c_int]
+        L.oracle_count_dag.restype = C.c_uint64
+        L.oracle_count_dag.argtypes = [u64p, u32p, C.c_uint32, u64p, C.c_int]
         L.oracle_brute_force.restype = C.c_uint64
         L.oracle_brute_force.argtypes = [u64p, u32p, C.c_uint32]
         L.oracle_fnv1a64.restype = C.c_uint64
@@ -111,6 +113,15 @@ class Oracle:
         nb = nbrs if nbrs.size else np.zeros(1, np.uint32)
         t = self.lib.oracle_count(_ptr(offsets, u64p), _ptr(nb, u32p), n,
                                   _ptr(pv, u64p) if per_vertex else None, threads)
+        return (t, pv) if per_vertex else t
+
+    def count_dag(self, offsets: np.ndarray, nbrs: np.ndarray, per_vertex: bool = False, threads: int = 0):
+        """The degree-ordered pivot-join checker (oracle_count_dag)."""
+        n = offsets.size - 1
+        pv = np.zeros(n, dtype=np.uint64) if per_vertex else None
+        nb = nbrs if nbrs.size else np.zeros(1, np.uint32)
+        t = self.lib.oracle_count_dag(_ptr(offsets, u64p), _ptr(nb, u32p), n,
+                                      _ptr(pv, u64p) if per_vertex else None, threads)
         return (t, pv) if per_vertex else t
 
     def brute_force(self, offsets: np.ndarray, nbrs: np.ndarray) -> int:

@@ -58,7 +58,7 @@ class TcGraphInfo(C.Structure):
 
 class TcCountOpts(C.Structure):
     _fields_ = [("lookahead", C.c_int), ("keep_listings", C.c_int), ("part_index", C.c_uint32),
-                ("part_count", C.c_uint32), ("sync", C.c_int)]
+                ("part_count", C.c_uint32), ("sync", C.c_int), ("work_counters", C.c_int)]
 
 
 class TcCountStats(C.Structure):
@@ -66,7 +66,8 @@ class TcCountStats(C.Structure):
                 ("reduce_ms", C.c_double), ("pivots", C.c_uint64), ("items", C.c_uint64),
                 ("wedges", C.c_uint64), ("segments", C.c_uint64), ("join_launches", C.c_uint64),
                 ("dag_W", C.c_double), ("alg_bytes", C.c_double), ("probe_bytes", C.c_double),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("part_first_vertex", C.c_uint64),
+                ("part_last_vertex", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -104,13 +105,24 @@ _sig("tc_graph_write_csr_cache", C.c_int, [C.c_void_p, C.c_void_p])
 _sig("tc_partition_bounds", C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p])
 _sig("tc_gen_num_edges", C.c_uint64, [C.c_int, C.c_int, C.c_int])
 _sig("tc_generate", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p])
+_sig("tc_release_cached_memory", C.c_uint64, [C.c_int])
+_sig("tc_comm_unique_id", C.c_int, [C.c_void_p])
+_sig("tc_comm_init_rank", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)])
+_sig("tc_comm_destroy", None, [C.c_void_p])
+_sig("tc_count_allreduce", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(TcCountOpts), C.c_void_p, C.c_void_p,
+                                     C.POINTER(TcCountStats)])
+_sig("tc_multi_create", C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)])
+_sig("tc_multi_destroy", None, [C.c_void_p])
+_sig("tc_count_multi", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(TcCountOpts), C.c_void_p,
+                                 C.c_void_p, C.POINTER(TcCountStats)])
 
 EXPORTED_SYMBOLS = [
     "tc_abi_version", "tc_last_error", "tc_free", "tc_graph_build", "tc_graph_from_csr", "tc_graph_get_info",
     "tc_graph_export_csr", "tc_graph_degrees", "tc_graph_set_stream", "tc_graph_destroy", "tc_count",
     "tc_parse_matrix_market", "tc_csr_cache_to_graph", "tc_gen_num_edges", "tc_generate", "tc_partition_bounds",
     "tc_graph_load_matrix_market", "tc_graph_csr_cache_size", "tc_graph_write_csr_cache", "tc_list_triangles",
-    "tc_list_triangles_range",
+    "tc_list_triangles_range", "tc_release_cached_memory", "tc_comm_unique_id", "tc_comm_init_rank",
+    "tc_comm_destroy", "tc_count_allreduce", "tc_multi_create", "tc_multi_destroy", "tc_count_multi",
 ]
 
 
@@ -161,17 +173,28 @@ def _check(rc: int):
     raise CudaError(f"[{rc}] {msg}")
 
 
-def _addr(x) -> int:
-    """Address of a numpy array, a torch tensor (host or device) or an int."""
+def _addr(x, itemsize: Optional[int] = None, what: str = "buffer", integer: bool = True) -> int:
+    """Address of a numpy array, a torch tensor (host or device) or an int.
+    With itemsize, the element width is checked (the C-ABI reads raw words:
+    a scipy int32 indptr passed as u64 offsets would be read past its end),
+    and so are contiguity and an integer dtype."""
     if x is None:
         return 0
     if isinstance(x, int):
         return x
     if isinstance(x, np.ndarray):
         if not x.flags.c_contiguous:
-            raise InvalidArgument("array must be C-contiguous")
+            raise InvalidArgument(f"{what} must be C-contiguous")
+        if itemsize is not None and (x.dtype.itemsize != itemsize or (integer and x.dtype.kind not in "iu")):
+            raise InvalidArgument(f"{what} must be a {8 * itemsize}-bit integer array, got {x.dtype}")
         return x.ctypes.data
     if hasattr(x, "data_ptr"):
+        if hasattr(x, "is_contiguous") and not x.is_contiguous():
+            raise InvalidArgument(f"{what} must be contiguous")
+        if itemsize is not None:
+            es = x.element_size()
+            if es != itemsize or (integer and (x.is_floating_point() or x.is_complex())):
+                raise InvalidArgument(f"{what} must be a {8 * itemsize}-bit integer tensor, got {x.dtype}")
         return x.data_ptr()
     raise TypeError(f"cannot take the address of {type(x)}")
 
@@ -270,7 +293,8 @@ class Graph:
         n, E = self.num_vertices(), self.num_edges()
         ro = row_offsets if row_offsets is not None else np.empty(n + 1, np.uint64)
         nb = neighbors if neighbors is not None else np.empty(max(2 * E, 1), np.uint32)
-        _check(_lib.tc_graph_export_csr(self._h, C.c_void_p(_addr(ro)), C.c_void_p(_addr(nb))))
+        _check(_lib.tc_graph_export_csr(self._h, C.c_void_p(_addr(ro, 8, "row_offsets")),
+                                        C.c_void_p(_addr(nb, 4, "neighbors"))))
         if neighbors is None:
             nb = nb[: 2 * E]
         return ro, nb
@@ -320,7 +344,7 @@ def build_graph_from_pairs(pairs, n_declared: int, report: Optional[BuildReport]
         m = (pairs.size if isinstance(pairs, np.ndarray) else pairs.numel()) // 2
     h = C.c_void_p()
     rep = TcBuildReport()
-    _check(_lib.tc_graph_build(C.c_void_p(_addr(pairs)), m, n_declared, device, C.byref(h), C.byref(rep)))
+    _check(_lib.tc_graph_build(C.c_void_p(_addr(pairs, 4, "pairs")), m, n_declared, device, C.byref(h), C.byref(rep)))
     if report is not None:
         report.self_loops_removed = rep.self_loops_removed
         report.duplicate_entries_removed = rep.duplicate_entries_removed
@@ -336,7 +360,8 @@ def graph_from_csr(row_offsets, neighbors, n: Optional[int] = None, num_edges: O
     if num_edges is None:
         num_edges = (neighbors.size if isinstance(neighbors, np.ndarray) else neighbors.numel()) // 2
     h = C.c_void_p()
-    _check(_lib.tc_graph_from_csr(C.c_void_p(_addr(row_offsets)), C.c_void_p(_addr(neighbors)), n, num_edges,
+    _check(_lib.tc_graph_from_csr(C.c_void_p(_addr(row_offsets, 8, "row_offsets")),
+                                  C.c_void_p(_addr(neighbors, 4, "neighbors")), n, num_edges,
                                   device, C.byref(h)))
     return Graph(h.value, device)
 
@@ -360,7 +385,7 @@ def count_triangles(g: Graph, opts: Optional[MatchOptions] = None) -> MatchResul
                                             part_index=opts.part_index, part_count=opts.part_count))
         r.listings = rows
         return r
-    o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, 1)
+    o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, 1, 1)
     total = np.zeros(1, np.uint64)
     pv = np.zeros(max(g.num_vertices(), 1), np.uint64) if opts.per_vertex else None
     st = TcCountStats()
@@ -418,21 +443,115 @@ def iter_listings(g: Graph, max_rows: int = 1 << 22, out=None):
 
 
 def count_triangles_into(g: Graph, total_ptr, per_vertex_ptr=None, opts: Optional[MatchOptions] = None,
-                         stats: bool = False, sync: bool = False):
+                         stats: bool = False, sync: bool = False, work_counters: bool = False):
     """Low-level: outputs to caller buffers (device tensors for the multi-GPU
-    allreduce path).  Returns the stats dict when stats=True."""
+    allreduce path).  Returns the stats dict when stats=True (phase times;
+    work_counters=True adds W / J / items / byte models, one extra pass)."""
     opts = opts or MatchOptions()
-    o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, int(sync))
+    o = TcCountOpts(opts.lookahead, int(opts.keep_listings), opts.part_index, opts.part_count, int(sync),
+                    int(work_counters))
     st = TcCountStats()
-    _check(_lib.tc_count(g.handle, C.byref(o), C.c_void_p(_addr(total_ptr)),
-                         C.c_void_p(_addr(per_vertex_ptr)) if per_vertex_ptr is not None else None,
+    _check(_lib.tc_count(g.handle, C.byref(o), C.c_void_p(_addr(total_ptr, 8, "total")),
+                         C.c_void_p(_addr(per_vertex_ptr, 8, "per_vertex")) if per_vertex_ptr is not None else None,
                          C.byref(st) if stats else None))
     return st.as_dict() if stats else None
 
 
+# ---- multi-GPU (tcb200.h tc_comm_* / tc_multi_*) -------------------------------
+
+COMM_ID_BYTES = 128
+
+
+class Comm:
+    """One rank of a one-process-per-GPU group (torchrun style).  The count
+    splits the graph's pivots over the ranks and ONE NCCL allreduce over
+    NVLink combines them (tc_count_allreduce); torch.distributed is only the
+    rendezvous that carries the 128-byte NCCL id (see dist.py)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(COMM_ID_BYTES)
+        _check(_lib.tc_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        if len(uid) != COMM_ID_BYTES:
+            raise InvalidArgument(f"NCCL id must be {COMM_ID_BYTES} bytes")
+        h = C.c_void_p()
+        _check(_lib.tc_comm_init_rank(C.create_string_buffer(uid, COMM_ID_BYTES), nranks, rank, device, C.byref(h)))
+        self._h, self.nranks, self.rank, self.device = h, nranks, rank, device
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.tc_comm_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    __del__ = close
+
+    def count_into(self, g: Graph, total, per_vertex=None, opts: Optional[MatchOptions] = None, stats: bool = False,
+                   sync: bool = False):
+        """This rank's part + the allreduce, into caller buffers (device
+        tensors keep the call asynchronous on the graph's stream)."""
+        opts = opts or MatchOptions()
+        o = TcCountOpts(opts.lookahead, int(opts.keep_listings), 0, 0, int(sync), 0)
+        st = TcCountStats()
+        _check(_lib.tc_count_allreduce(self._h, g.handle, C.byref(o), C.c_void_p(_addr(total, 8, "total")),
+                                       C.c_void_p(_addr(per_vertex, 8, "per_vertex")) if per_vertex is not None
+                                       else None, C.byref(st) if stats else None))
+        return st.as_dict() if stats else None
+
+    def count_triangles(self, g: Graph, opts: Optional[MatchOptions] = None) -> MatchResult:
+        opts = opts or MatchOptions()
+        total = np.zeros(1, np.uint64)
+        pv = np.zeros(max(g.num_vertices(), 1), np.uint64) if opts.per_vertex else None
+        st = self.count_into(g, total, pv, opts, stats=True, sync=True)
+        return MatchResult(count=int(total[0]), per_vertex=(pv[: g.num_vertices()] if pv is not None else None),
+                           stats=st)
+
+
+class MultiGPU:
+    """One process driving several GPUs (tc_multi_create / tc_count_multi):
+    devices[p] is the device of part p; a device may repeat (its parts run back
+    to back and are summed before the allreduce)."""
+
+    def __init__(self, devices):
+        self.devices = [int(d) for d in devices]
+        arr = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        _check(_lib.tc_multi_create(arr, len(self.devices), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.tc_multi_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    __del__ = close
+
+    def count_triangles(self, graphs, opts: Optional[MatchOptions] = None, total=None, per_vertex=None):
+        """graphs[p] = the replica on devices[p].  Host outputs by default."""
+        if len(graphs) != len(self.devices):
+            raise InvalidArgument("one graph per part")
+        opts = opts or MatchOptions()
+        hs = (C.c_void_p * len(graphs))(*[g.handle.value for g in graphs])
+        n = graphs[0].num_vertices()
+        tot = total if total is not None else np.zeros(1, np.uint64)
+        pv = per_vertex if per_vertex is not None else (np.zeros(max(n, 1), np.uint64) if opts.per_vertex else None)
+        o = TcCountOpts(opts.lookahead, int(opts.keep_listings), 0, 0, 1, 0)
+        st = TcCountStats()
+        _check(_lib.tc_count_multi(self._h, hs, C.byref(o), C.c_void_p(_addr(tot, 8, "total")),
+                                   C.c_void_p(_addr(pv, 8, "per_vertex")) if pv is not None else None,
+                                   C.byref(st)))
+        if total is not None:
+            return st.as_dict()
+        return MatchResult(count=int(tot[0]), per_vertex=(pv[:n] if pv is not None and per_vertex is None else pv),
+                           stats=st.as_dict())
+
+
 def partition_bounds(g: Graph, parts: int) -> np.ndarray:
-    """Degree-weighted oriented-edge ranges of a `parts`-way multi-GPU split
-    (what tc_count uses for part_index/part_count)."""
+    """Degree-weighted pivot rank ranges of a `parts`-way multi-GPU split
+    (what tc_count uses for part_index/part_count): part p counts the
+    triangles whose middle vertex has (deg,id) rank in [b[p], b[p+1])."""
     b = np.zeros(parts + 1, np.uint64)
     _check(_lib.tc_partition_bounds(g.handle, parts, C.c_void_p(b.ctypes.data)))
     return b
@@ -547,8 +666,13 @@ def generate(kind: int, scale: int, param: int, out=None, device: int = 0):
     m = gen_num_edges(kind, scale, param)
     if out is None:
         out = np.empty(2 * m, np.uint32)
-    _check(_lib.tc_generate(kind, scale, param, device, C.c_void_p(_addr(out))))
+    _check(_lib.tc_generate(kind, scale, param, device, C.c_void_p(_addr(out, 4, "out"))))
     return out
+
+
+def release_cached_memory(device: int = -1) -> int:
+    """Return the library's cached device blocks to the driver (bytes freed)."""
+    return int(_lib.tc_release_cached_memory(device))
 
 
 def abi_version() -> int:

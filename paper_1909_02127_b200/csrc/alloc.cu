@@ -2,14 +2,26 @@
 //
 // Size classes: 512-byte granules below 1 MiB, 2 MiB granules above.  A freed
 // block keeps the stream it was last used on and an event recorded at the
-// free; dev_alloc takes a cached block of the same class and device, making
-// the new stream wait on that event when the streams differ.  On
-// cudaErrorMemoryAllocation the cache is drained (device synchronised, every
-// cached block returned) and the request retried once.
+// free; dev_alloc takes the smallest cached block of a fitting class (the
+// exact class below 1 MiB, up to 1.25x the request above: best fit, so a
+// graph of another size still reuses the cache) on the same device, making the
+// new stream wait on that event when the streams differ.  The real class of
+// every live block is tracked, so a block handed out for a smaller request
+// goes back under its own class.
+//
+// The cache is bounded: freed bytes above the per-device limit (TCB_CACHE_MB,
+// default 40% of the device's memory) go straight back to cudaFree, oldest
+// first, and tc_release_cached_memory() returns everything on demand -- a host
+// framework in the same process (PyTorch) can always reclaim what the library
+// is not using.  On cudaErrorMemoryAllocation the cache is drained (device
+// synchronised, every cached block returned) and the request retried once.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <deque>
 #include <map>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -19,13 +31,23 @@ namespace {
 
 struct Block {
   void* p;
+  size_t cls;
   cudaStream_t s;
   cudaEvent_t ev;
+  uint64_t seq;  // free order (oldest first when trimming)
+};
+
+struct DevCache {
+  std::map<size_t, std::vector<Block>> free;  // class -> blocks
+  size_t cached = 0;                          // bytes held in `free`
+  size_t limit = 0;                           // 0 = not yet initialised
 };
 
 struct Cache {
   std::mutex mu;
-  std::map<std::pair<int, size_t>, std::vector<Block>> free;  // (device, class) -> blocks
+  std::map<int, DevCache> dev;
+  std::unordered_map<void*, size_t> live;  // pointer -> real class
+  uint64_t seq = 0;
 };
 
 Cache& cache() {
@@ -38,19 +60,61 @@ size_t size_class(size_t bytes) {
   return (bytes + g - 1) / g * g;
 }
 
-void drain_locked(Cache& c) {
-  cudaDeviceSynchronize();
-  for (auto& kv : c.free) {
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(kv.first.first);
-    for (Block& b : kv.second) {
-      cudaEventDestroy(b.ev);
-      cudaFree(b.p);
-    }
-    cudaSetDevice(prev);
+size_t cache_limit(int dev) {
+  if (const char* e = getenv("TCB_CACHE_MB")) return (size_t)strtoull(e, nullptr, 10) << 20;
+  size_t fr = 0, tot = 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(dev);
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    tot = 0;
   }
-  c.free.clear();
+  cudaSetDevice(prev);
+  return tot ? tot / 5 * 2 : ((size_t)16 << 30);
+}
+
+void release_block(int dev, Block& b) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(dev);
+  cudaEventSynchronize(b.ev);
+  cudaEventDestroy(b.ev);
+  cudaFree(b.p);
+  cudaSetDevice(prev);
+}
+
+void drain_locked(Cache& c, int only_dev) {
+  for (auto& d : c.dev) {
+    if (only_dev >= 0 && d.first != only_dev) continue;
+    for (auto& kv : d.second.free)
+      for (Block& b : kv.second) release_block(d.first, b);
+    d.second.free.clear();
+    d.second.cached = 0;
+  }
+}
+
+// Oldest cached blocks of the device back to cudaFree until the cache fits.
+void trim_locked(Cache& c, int dev) {
+  DevCache& d = c.dev[dev];
+  while (d.cached > d.limit) {
+    auto oldest = d.free.end();
+    size_t idx = 0;
+    uint64_t best = UINT64_MAX;
+    for (auto it = d.free.begin(); it != d.free.end(); ++it)
+      for (size_t i = 0; i < it->second.size(); ++i)
+        if (it->second[i].seq < best) {
+          best = it->second[i].seq;
+          oldest = it;
+          idx = i;
+        }
+    if (oldest == d.free.end()) break;
+    Block b = oldest->second[idx];
+    oldest->second.erase(oldest->second.begin() + idx);
+    if (oldest->second.empty()) d.free.erase(oldest);
+    d.cached -= b.cls;
+    release_block(dev, b);
+  }
 }
 
 }  // namespace
@@ -62,12 +126,17 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   Cache& c = cache();
   {
     std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.free.find({dev, cls});
-    if (it != c.free.end() && !it->second.empty()) {
+    DevCache& d = c.dev[dev];
+    const size_t max_cls = cls < (1u << 20) ? cls : cls + cls / 4;
+    auto it = d.free.lower_bound(cls);
+    if (it != d.free.end() && it->first <= max_cls && !it->second.empty()) {
       Block b = it->second.back();
       it->second.pop_back();
+      if (it->second.empty()) d.free.erase(it);
+      d.cached -= b.cls;
       if (b.s != s) TC_CUDA(cudaStreamWaitEvent(s, b.ev, 0));
       cudaEventDestroy(b.ev);
+      c.live[b.p] = b.cls;
       return b.p;
     }
   }
@@ -76,10 +145,13 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     std::lock_guard<std::mutex> lk(c.mu);
-    drain_locked(c);
+    cudaDeviceSynchronize();
+    drain_locked(c, -1);
     e = cudaMalloc(&p, cls);
   }
   TC_CUDA(e);
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.live[p] = cls;
   return p;
 }
 
@@ -87,7 +159,17 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (!p) return;
   int dev = 0;
   cudaGetDevice(&dev);
-  Block b{p, s, nullptr};
+  Cache& c = cache();
+  size_t cls = size_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.live.find(p);
+    if (it != c.live.end()) {
+      cls = it->second;
+      c.live.erase(it);
+    }
+  }
+  Block b{p, cls, s, nullptr, 0};
   if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventRecord(b.ev, s) != cudaSuccess) {
     cudaGetLastError();
@@ -95,9 +177,23 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
     cudaFree(p);
     return;
   }
+  std::lock_guard<std::mutex> lk(c.mu);
+  DevCache& d = c.dev[dev];
+  if (!d.limit) d.limit = cache_limit(dev);
+  b.seq = ++c.seq;
+  d.free[cls].push_back(b);
+  d.cached += cls;
+  if (d.cached > d.limit) trim_locked(c, dev);
+}
+
+size_t release_cached(int device) {
   Cache& c = cache();
   std::lock_guard<std::mutex> lk(c.mu);
-  c.free[{dev, size_class(bytes)}].push_back(b);
+  size_t n = 0;
+  for (auto& d : c.dev)
+    if (device < 0 || d.first == device) n += d.second.cached;
+  drain_locked(c, device);
+  return n;
 }
 
 }  // namespace tcb

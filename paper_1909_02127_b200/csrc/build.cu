@@ -920,6 +920,62 @@ void alloc_rows(tc_graph& g) {
   TC_CUDA(cudaMemsetAsync(g.col.get() + g.E, 0xff, 8 * sizeof(uint32_t), s));
 }
 
+// ---- in-edge index (graph.cuh tc_graph::ine) ----------------------------------
+// din(v) = deg(v) - d+(v): the in-edges of rank v, no edge pass.
+struct InDeg {
+  const uint32_t* off;
+  const uint32_t* deg;
+  __device__ __forceinline__ uint32_t operator()(uint64_t v) const { return deg[v] - (off[v + 1] - off[v]); }
+};
+
+// Every oriented edge e = u->v to its head's slot, warp-aggregated per head
+// (hub heads take one atomic per warp): ine[slot] = {e, u}.
+__global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* __restrict__ src, uint64_t E,
+                             uint32_t* __restrict__ cur, uint2* __restrict__ ine) {
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = base + threadIdx.x;
+    const bool ok = e < E;
+    const uint32_t v = ok ? col[e] : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, v);
+    const unsigned lane = threadIdx.x & 31u;
+    const int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (ok && (int)lane == leader) b = atomicAdd(&cur[v], (unsigned)__popc(peers));
+    b = __shfl_sync(0xffffffffu, b, leader);
+    if (ok) ine[b + __popc(peers & lanemask_lt())] = make_uint2((uint32_t)e, src[e]);
+  }
+}
+
+__global__ void k_rowdesc(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, uint32_t n,
+                          uint4* __restrict__ rowd) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x)
+    rowd[u] = make_uint4(off[u], off[u + 1], offH[u], offH[u + 1]);
+}
+
+// Plan capacities: work segments per pivot class (per-vertex superset: d+ = 0
+// pivots in the warp bin) and the per-vertex mask bytes of all rows.
+__global__ void k_plan_caps(PivotClass pc, uint32_t n, unsigned long long* __restrict__ tot) {
+  unsigned long long t[4] = {0, 0, 0, 0};
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t din = 0;
+    const int c = pc((uint32_t)v, din);
+    if (c >= 0) {
+      const uint32_t per = segs_per_class(c);
+      const unsigned long long ns = (din + per - 1) / per;
+      t[0] += c == 0 ? ns : 0;
+      t[1] += c == 1 ? ns : 0;
+      t[2] += c == 2 ? ns : 0;
+    }
+    const uint32_t O = pc.offH[v];
+    t[3] += RowMasks(pc.off[v + 1] - pc.off[v], O, pc.offH[v + 1] - O).total();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long w = warp_sum(t[i]);
+    if ((threadIdx.x & 31u) == 0 && w) atomicAdd(&tot[i], w);
+  }
+}
+
 // Sorted unique canonical id-space keys (edge-list route) -> ranks ->
 // oriented CSR: orient each key by rank, radix sort, split.
 void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
@@ -957,6 +1013,44 @@ void finalize(tc_graph& g, DBuf<uint64_t>& ukeys, uint64_t E) {
   row_offsets(g, dplus.get());
   finish_rows(g);
   pl.mark("fin_rows");
+}
+
+// Shared tail of both build routes: the in-edge index and the count-plan
+// capacities (one small read-back; the count itself never synchronises).
+void finish_graph(tc_graph& g) {
+  cudaStream_t s = g.stream;
+  const uint32_t n = g.n;
+  const uint64_t E = g.E;
+  const int dev = g.device;
+  g.inoff.alloc((uint64_t)n + 1, s);
+  scan_exclusive<uint32_t>(InDeg{g.off.get(), g.deg.get()}, g.inoff.get(), n, g.inoff.get() + n, s);
+  g.ine.alloc(E + 2, s);  // +16 B: bulk copies of a segment's slice round up to 16 bytes
+  TC_CUDA(cudaMemsetAsync(g.ine.get() + E, 0, 2 * sizeof(uint2), s));
+  if (E) {
+    DBuf<uint32_t> cur(n, s);
+    TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+    k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.ine.get());
+    TC_LAUNCH();
+  }
+  g.rowd.alloc(n ? n : 1, s);
+  if (n) {
+    k_rowdesc<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), n, g.rowd.get());
+    TC_LAUNCH();
+  }
+  DBuf<unsigned long long> tot(4, s);
+  TC_CUDA(cudaMemsetAsync(tot.get(), 0, 4 * sizeof(unsigned long long), s));
+  if (n) {
+    k_plan_caps<<<grid_gs(n, dev), kT, 0, s>>>(PivotClass{g.off.get(), g.offH.get(), g.inoff.get(), true}, n,
+                                              tot.get());
+    TC_LAUNCH();
+  }
+  unsigned long long h[4];
+  TC_CUDA(cudaMemcpyAsync(h, tot.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+  TC_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < 3; ++c) g.seg_cap[c] = h[c];
+  g.mask_total = h[3];
+  g.part_bounds.clear();
+  g.part_bounds_P = 0;
 }
 
 }  // namespace
@@ -1001,6 +1095,7 @@ void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t
     rep->duplicate_entries_removed = m - loops - E;
   }
   finalize(g, ukeys, E);
+  finish_graph(g);
 }
 
 void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, uint32_t n, uint64_t num_edges,
@@ -1162,6 +1257,8 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
     finish_rows(g);
     pl.mark("csr_radix_fallback");
   }
+  finish_graph(g);
+  pl.mark("csr_in_index");
 }
 
 void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs) {

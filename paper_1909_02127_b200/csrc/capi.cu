@@ -95,12 +95,6 @@ struct DeviceGuard {
   explicit DeviceGuard(int dev) {
     TC_CUDA(cudaGetDevice(&prev));
     TC_CUDA(cudaSetDevice(dev));
-    // let the stream-ordered pool keep freed blocks for the next call
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
@@ -157,6 +151,9 @@ void destroy_handle(tc_graph* g) {
     g->rank_of.release();
     g->colH.release();
     g->offH.release();
+    g->inoff.release();
+    g->ine.release();
+    g->rowd.release();
     for (auto& sc : g->scratch) sc.release(s);
     cudaStreamSynchronize(s);
   }
@@ -195,6 +192,8 @@ int tc_abi_version(void) { return TCB200_ABI_VERSION; }
 const char* tc_last_error(void) { return g_last_error.c_str(); }
 
 void tc_free(void* p) { std::free(p); }
+
+uint64_t tc_release_cached_memory(int device) { return tcb::release_cached(device); }
 
 tc_status tc_graph_build(const uint32_t* pairs, uint64_t m, uint32_t n_declared, int device, tc_graph** out,
                          tc_build_report* report) {
@@ -274,6 +273,7 @@ tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info) {
 tc_status tc_graph_export_csr(tc_graph* g, uint64_t* row_offsets, uint32_t* neighbors) {
   if (!g || !row_offsets || (g->E && !neighbors)) return set_error(TC_EINVAL, "tc_graph_export_csr: NULL argument");
   TC_API_TRY
+  std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   DevOut<uint64_t> off(row_offsets, (uint64_t)g->n + 1, g->stream);
   DevOut<uint32_t> nb(neighbors, 2 * g->E, g->stream);
@@ -288,6 +288,7 @@ tc_status tc_graph_export_csr(tc_graph* g, uint64_t* row_offsets, uint32_t* neig
 tc_status tc_graph_degrees(tc_graph* g, uint32_t* degrees) {
   if (!g || (g->n && !degrees)) return set_error(TC_EINVAL, "tc_graph_degrees: NULL argument");
   TC_API_TRY
+  std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   DevOut<uint32_t> d(degrees, g->n, g->stream);
   tcb::export_degrees(*g, d.p);
@@ -299,6 +300,7 @@ tc_status tc_graph_degrees(tc_graph* g, uint32_t* degrees) {
 
 tc_status tc_graph_set_stream(tc_graph* g, void* stream) {
   if (!g) return set_error(TC_EINVAL, "tc_graph_set_stream: NULL graph");
+  std::lock_guard<std::mutex> lk(g->mu);
   g->stream = stream ? static_cast<cudaStream_t>(stream) : g->own_stream;
   return TC_OK;
 }
@@ -315,6 +317,7 @@ tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint
   if (o.part_count > 1 && o.part_index >= o.part_count)
     return set_error(TC_EINVAL, "tc_count: part_index must be < part_count");
   TC_API_TRY
+  std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   DevOut<uint64_t> t(total, 1, g->stream);
   DevOut<uint64_t> pv(per_vertex, g->n, g->stream);
@@ -327,9 +330,89 @@ tc_status tc_count(tc_graph* g, const tc_count_opts* opts, uint64_t* total, uint
   TC_API_CATCH
 }
 
+namespace {
+tc_status check_count_opts(const tc_count_opts& o) {
+  if (o.lookahead < 0 || o.lookahead > 2) return set_error(TC_EINVAL, "lookahead must be 0, 1, or 2");
+  if (o.keep_listings) return set_error(TC_EUNSUPPORTED, "keep_listings is not supported on the GPU path");
+  return TC_OK;
+}
+}  // namespace
+
+tc_status tc_comm_unique_id(void* id) {
+  if (!id) return set_error(TC_EINVAL, "tc_comm_unique_id: NULL id");
+  TC_API_TRY
+  tcb::comm_unique_id(id);
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_comm_init_rank(const void* id, int nranks, int rank, int device, tc_comm** out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return set_error(TC_EINVAL, "tc_comm_init_rank: bad argument");
+  TC_API_TRY
+  *out = tcb::comm_init_rank(id, nranks, rank, device);
+  return TC_OK;
+  TC_API_CATCH
+}
+
+void tc_comm_destroy(tc_comm* comm) { tcb::comm_destroy(comm); }
+
+tc_status tc_count_allreduce(tc_comm* comm, tc_graph* g, const tc_count_opts* opts, uint64_t* total,
+                             uint64_t* per_vertex, tc_count_stats* stats) {
+  if (!comm || !g || !total) return set_error(TC_EINVAL, "tc_count_allreduce: NULL argument");
+  tc_count_opts o{};
+  if (opts) o = *opts;
+  if (tc_status st = check_count_opts(o)) return st;
+  TC_API_TRY
+  DeviceGuard dg(g->device);
+  DevOut<uint64_t> t(total, 1, g->stream);
+  DevOut<uint64_t> pv(per_vertex, g->n, g->stream);
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  tcb::count_allreduce(comm, *g, o, t.p, per_vertex ? pv.p : nullptr, stats);
+  t.finish(g->stream);
+  pv.finish(g->stream);
+  if (o.sync || t.host || pv.host || stats) TC_CUDA(cudaStreamSynchronize(g->stream));
+  return TC_OK;
+  TC_API_CATCH
+}
+
+tc_status tc_multi_create(const int* devices, int nparts, tc_multi** out) {
+  if (!devices || nparts < 1 || !out) return set_error(TC_EINVAL, "tc_multi_create: bad argument");
+  TC_API_TRY
+  *out = tcb::multi_create(devices, nparts);
+  return TC_OK;
+  TC_API_CATCH
+}
+
+void tc_multi_destroy(tc_multi* m) { tcb::multi_destroy(m); }
+
+tc_status tc_count_multi(tc_multi* m, tc_graph* const* graphs, const tc_count_opts* opts, uint64_t* total,
+                         uint64_t* per_vertex, tc_count_stats* stats) {
+  if (!m || !graphs || !total) return set_error(TC_EINVAL, "tc_count_multi: NULL argument");
+  const int P = tcb::multi_parts(m);
+  for (int p = 0; p < P; ++p)
+    if (!graphs[p]) return set_error(TC_EINVAL, "tc_count_multi: NULL graph");
+  tc_count_opts o{};
+  if (opts) o = *opts;
+  if (tc_status st = check_count_opts(o)) return st;
+  TC_API_TRY
+  tc_graph* g0 = graphs[0];
+  DeviceGuard dg(g0->device);
+  DevOut<uint64_t> t(total, 1, g0->stream);
+  DevOut<uint64_t> pv(per_vertex, g0->n, g0->stream);
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  tcb::count_multi(m, graphs, o, t.p, per_vertex ? pv.p : nullptr, stats);
+  t.finish(g0->stream);
+  pv.finish(g0->stream);
+  TC_CUDA(cudaStreamSynchronize(g0->stream));
+  return TC_OK;
+  TC_API_CATCH
+}
+
 tc_status tc_partition_bounds(tc_graph* g, uint32_t parts, uint64_t* bounds) {
   if (!g || !bounds || parts == 0) return set_error(TC_EINVAL, "tc_partition_bounds: bad argument");
   TC_API_TRY
+  std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   const std::vector<uint64_t>& b = tcb::partition_bounds(*g, parts);
   std::memcpy(bounds, b.data(), ((size_t)parts + 1) * sizeof(uint64_t));
@@ -398,6 +481,7 @@ tc_status tc_list_triangles_range(tc_graph* g, uint64_t first_edge, uint64_t las
   if (first_edge > last_edge || last_edge > g->E)
     return set_error(TC_EINVAL, "tc_list_triangles_range: edge range outside [0, num_edges]");
   TC_API_TRY
+  std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   DevOut<uint32_t> out(capacity ? rows : nullptr, 3 * capacity, g->stream);
   const uint64_t T = tcb::list_triangles(*g, out.p, capacity, first_edge, last_edge);

@@ -77,47 +77,65 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 
 // ---- multi-GPU partition -------------------------------------------------------
 
-// Per-item overhead in candidate-probe units (frontier record, segment
-// staging, and the re-staging of a pivot's row in every part that holds some
-// of its items), fitted on the C4 2/4/8-part splits (tools/phase_probe.py
-// --parts P, TCB_ITEM_COST): max part at P = 2/4/8 is 34.2/19.1/12.1 ms at
-// 700 against 35.7/20.5/12.1 at 1000 and 36.4/22.1/14.4 at 400 (C5's 8-part
-// split prefers 1000: 135.9 against 141.5 ms).
-constexpr uint64_t kItemCost = 700;
+// Work of pivot v (pivot-range parts): its candidate wedges J_v = sum over
+// in-edges u->v of the suffix length |N+(u) after v|, plus a per-item and a
+// per-segment overhead in candidate-probe units (item geometry / staging and
+// the pivot row staged once per segment).  Accumulated edge-parallel (one
+// coalesced pass over col; warp-aggregated per head), then an exclusive scan
+// over the pivots and P-1 binary searches: part p = pivots [b[p], b[p+1]),
+// contiguous rank ranges of ~equal work.  Every pivot's row is staged by one
+// part only (no re-staging across parts), and the per-vertex row pass of a
+// part reads only the items of its pivots (k_pv_rows PartRange).
+#ifndef TCB_ITEM_COST
+#define TCB_ITEM_COST 24
+#endif
+#ifndef TCB_SEG_COST
+#define TCB_SEG_COST 4
+#endif
+constexpr uint64_t kItemCost = TCB_ITEM_COST;
+constexpr uint64_t kSegRowCost = TCB_SEG_COST;  // per member of N+(v), per segment
 
-// Per-row cost of the degree-ordered DAG: row u with d = d+(u) out-edges
-// contributes C(d,2) candidate wedges and d items.  An exclusive scan over the
-// rows, then P-1 binary searches: each part is a contiguous range of source
-// rows (= of oriented edges), the north-star "degree-weighted ranges".  A scan
-// over |V| rows, not |E| edges: it is part of every multi-GPU count.
-struct RowCost {
+__global__ void k_pivot_wedges(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                               const uint32_t* __restrict__ src, uint64_t E, unsigned long long* __restrict__ jv) {
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = base + threadIdx.x;
+    const bool ok = e < E;
+    const uint32_t v = ok ? col[e] : 0xffffffffu;
+    // suffix length of e in its row (<= max d+, so a warp's sum fits 32 bits)
+    const uint32_t w = ok ? off[src[e] + 1] - (uint32_t)e - 1 : 0u;
+    const unsigned peers = __match_any_sync(0xffffffffu, v);
+    const uint32_t sum = __reduce_add_sync(peers, w);
+    if (ok && (int)lane_id() == __ffs(peers) - 1 && sum) atomicAdd(&jv[v], (unsigned long long)sum);
+  }
+}
+
+struct PivotCost {
   const uint32_t* off;
-  uint64_t item_cost;
-  __device__ __forceinline__ uint64_t operator()(uint64_t u) const {
-    const uint64_t d = off[u + 1] - off[u];
-    return d * (d ? d - 1 : 0) / 2 + item_cost * d;
+  const uint32_t* inoff;
+  const unsigned long long* jv;
+  uint64_t item_cost, seg_cost;
+  __device__ __forceinline__ uint64_t operator()(uint64_t v) const {
+    const uint64_t dv = off[v + 1] - off[v], din = inoff[v + 1] - inoff[v];
+    if (!dv || !din) return 0;
+    return jv[v] + item_cost * din + seg_cost * dv * ((din + kCtaSegItems - 1) / kCtaSegItems);
   }
 };
 
-__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, const uint32_t* __restrict__ off, uint32_t n,
-                              uint64_t E, uint64_t total, uint32_t parts, uint64_t* __restrict__ bounds) {
+__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint32_t n, uint64_t total, uint32_t parts,
+                              uint64_t* __restrict__ bounds) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > parts) return;
-  if (p == 0) {
-    bounds[0] = 0;
-    return;
-  }
-  if (p == parts) {
-    bounds[parts] = E;
+  if (p == 0 || p == parts) {
+    bounds[p] = p == 0 ? 0 : n;
     return;
   }
   const uint64_t target = (uint64_t)((double)total * p / parts);
-  uint64_t lo = 0, hi = n;  // first row r with prefix[r] >= target
+  uint64_t lo = 0, hi = n;  // first pivot r with prefix[r] >= target
   while (lo < hi) {
     const uint64_t mid = (lo + hi) / 2;
     if (prefix[mid] < target) lo = mid + 1; else hi = mid;
   }
-  bounds[p] = lo < n ? off[lo] : E;
+  bounds[p] = lo;
 }
 
 // ---- membership structures -------------------------------------------------
@@ -299,39 +317,86 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
   return h;
 }
 
+// ---- item geometry (from the in-edge index) --------------------------------------
+
+// Level-1 item = in-edge (e, u) of pivot v = col[e]: its wedge suffix is
+// col[e+1 .. off[u+1]).  CTA/small bins take it split into the hot part
+// (16-bit colH, the row's sorted suffix >= h0) and the cold part (col):
+// {hb, he, cb, ce}; all-zero = empty suffix.  mo = the item's first per-vertex
+// mask byte (rowbase[u] + RowMasks::P(k), k = e - off[u]).
+struct ItemGeo {
+  const uint4* rowd;  // tc_graph::rowd: {off[u], off[u+1], offH[u], offH[u+1]}
+  const uint64_t* rowbase;
+  __device__ __forceinline__ uint4 hotcold(uint2 eu, uint64_t* mo) const {
+    const uint32_t e = eu.x, u = eu.y;
+    const uint4 rd = rowd[u];  // one 16-byte load (one sector) per item
+    const uint32_t end = rd.y;
+    const uint32_t O = rd.z, h = rd.w - rd.z;
+    if (e + 1 >= end) return make_uint4(0, 0, 0, 0);
+    const uint32_t cold_end = end - h;
+    const uint4 it = (e + 1 >= cold_end) ? make_uint4(O + (e + 1 - cold_end), O + h, 0, 0)
+                                         : make_uint4(O, O + h, e + 1, cold_end);
+    if (mo != nullptr && it.y > it.x) {
+      const uint32_t beg = rd.x;
+      *mo = rowbase[u] + RowMasks(end - beg, O, h).P(e - beg);
+    }
+    return it;
+  }
+};
+
 // ---- warp bin ------------------------------------------------------------------
 
-// Advance + join for items [i0, i1) of one small pivot (u32 suffix ranges
-// {b,e} in items[i].x/.y), executed by one warp against its private hash.
+// Advance + join for in-edges [i0, i1) of one small pivot (d+ <= 64), one
+// warp against its private hash; items are the u32 suffix ranges
+// {e+1, off[u+1]} of col.  Per-vertex: the CTA bin's row pass reads hit masks
+// for every item, so this bin zeroes its items' mask bytes (its hits go to
+// per-hit counters instead); d+(v) = 0 pivots come here for that alone.
 template <bool kPerVertex, typename Sink>
-__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ items,
-                                                    uint32_t i0, uint32_t i1, const uint32_t* __restrict__ col,
-                                                    const uint32_t* __restrict__ src, const uint32_t* tab,
-                                                    uint32_t mask, uint32_t shift, const Sink& sink,
+__device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ ine, uint32_t i0, uint32_t i1,
+                                                    const uint32_t* __restrict__ off,
+                                                    const uint32_t* __restrict__ offH,
+                                                    const uint32_t* __restrict__ col, const uint32_t* tab,
+                                                    uint32_t mask, uint32_t shift, bool probe, const Sink& sink,
+                                                    const uint64_t* __restrict__ rowbase, uint8_t* __restrict__ masks,
                                                     uint32_t* item_cnt) {
   const unsigned lane = lane_id();
   const uint4* col4 = reinterpret_cast<const uint4*>(col);
   uint32_t hits = 0;
   for (uint32_t ib = i0; ib < i1; ib += 32) {
     const uint32_t my = ib + lane;
-    uint32_t b = 0, e = 0, nch = 0;
+    uint32_t b = 0, e = 0, nch = 0, u = 0;
     if (my < i1) {
-      const uint2 it = __ldcs(reinterpret_cast<const uint2*>(items + (uint64_t)my * (kPerVertex ? 2 : kItemStrideTotal)));
-      b = it.x;
-      e = it.y;
-      nch = ((e + 3) >> 2) - (b >> 2);
+      const uint2 eu = ine[my];
+      u = eu.y;
+      const uint32_t beg = off[u], end = off[u + 1];
+      if (eu.x + 1 < end) {
+        b = eu.x + 1;
+        e = end;
+        nch = ((e + 3) >> 2) - (b >> 2);
+        if (kPerVertex) {
+          const uint32_t O = offH[u], h = offH[u + 1] - O;
+          if (h > 0) {
+            const RowMasks rm(end - beg, O, h);
+            const uint32_t k = eu.x - beg;
+            uint8_t* z = masks + rowbase[u] + rm.P(k);
+            const uint32_t nb = (uint32_t)(rm.c_hi - rm.first_chunk(k));
+            for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
+          }
+        }
+      }
     }
+    if (!probe) continue;
     // compact the non-empty items to the low lanes (item_of needs nch >= 1);
     // lane L takes the item of the (L+1)-th non-empty lane
-    uint32_t owner = my;
+    uint32_t owner_u = u;
     {
       const uint32_t ne = __ballot_sync(0xffffffffu, nch > 0);
       const uint32_t from = lane < (uint32_t)__popc(ne) ? __fns(ne, 0, lane + 1) : lane;
       b = __shfl_sync(0xffffffffu, b, from);
       e = __shfl_sync(0xffffffffu, e, from);
       nch = __shfl_sync(0xffffffffu, nch, from);
+      owner_u = __shfl_sync(0xffffffffu, u, from);
       if (lane >= (uint32_t)__popc(ne)) nch = 0;
-      owner = ib + from;
     }
     const uint32_t pre = warp_inclusive_scan(nch);
     const uint32_t start = pre - nch;
@@ -355,7 +420,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
     if (kPerVertex) {
       __syncwarp();
       const uint32_t c = item_cnt[lane];
-      if (c) atomicAdd(&sink.t_rank[items[(uint64_t)owner * 2 + 1].x], (unsigned long long)c);
+      if (c) atomicAdd(&sink.t_rank[owner_u], (unsigned long long)c);
       __syncwarp();
     }
   }
@@ -364,17 +429,18 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ it
 
 // Warp bin: each warp takes whole segments of small pivots (d+ <= 64) with a
 // warp-private 128-slot hash table; the CTA shares the per-vertex top-rank
-// counters (dynamic SMEM, pv only).
+// counters (dynamic SMEM, pv only).  The segment count is read on the device.
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint4* __restrict__ items, const uint4* __restrict__ segs,
-    uint32_t nsegs, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
-    unsigned long long* __restrict__ total) {
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, const uint32_t* __restrict__ col,
+    const uint2* __restrict__ ine, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
+    uint32_t rc, uint32_t ncnt, const uint64_t* __restrict__ rowbase, uint8_t* __restrict__ masks,
+    unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
   __shared__ uint32_t s_tab[kJoinWarps][kWarpTable];
   __shared__ uint32_t s_item[kJoinWarps][32];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t nsegs = *nsegs_p;
   uint32_t* tab = s_tab[warp];
   for (uint32_t s = lane; s < kWarpTable; s += 32) tab[s] = kEmpty;
   if (kPerVertex) {
@@ -392,8 +458,8 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
-    const uint32_t h =
-        warp_join_small<kPerVertex>(items, sg.y, sg.z, col, src, tab, mask, shift, sink, s_item[warp]);
+    const uint32_t h = warp_join_small<kPerVertex>(ine, sg.y, sg.z, off, offH, col, tab, mask, shift, dv > 0, sink,
+                                                   rowbase, masks, s_item[warp]);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
@@ -426,11 +492,11 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 // Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots].
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
-    const uint16_t* __restrict__ colH, const uint4* __restrict__ items,
-    const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue, uint32_t h0, uint32_t nbm,
-    uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
-    unsigned long long* __restrict__ total) {
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd,
+    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine, const uint64_t* __restrict__ rowbase,
+    const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
+    uint32_t h0, uint32_t nbm, uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab,
+    uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
   __shared__ unsigned long long s_hmo[kPerVertex ? kCtaSegItems : 1];  // hot items' mask offsets
   __shared__ uint32_t s_hb[kCtaSegItems], s_he[kCtaSegItems], s_hpre[kCtaSegItems + 1];
@@ -442,10 +508,16 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   __shared__ unsigned long long s_wc[kJoinWarps];
   __shared__ uint32_t s_desc[6];  // current segment: v, i0, ni, off[v], d+(v), queue index
   __shared__ unsigned long long s_ctot;
+  // the segment's in-edge records {e, u}, bulk-copied (TMA) one segment ahead
+  __shared__ __align__(16) uint2 s_ine[kCtaSegItems + 2];
+  __shared__ __align__(8) unsigned long long s_mbar;
+  __shared__ uint4 s_sgn;  // the next segment, held by thread 0
   uint32_t* bm = dyn;
   uint32_t* stab = dyn + nbm;
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t nsegs = *nsegs_p;
+  const ItemGeo geo{rowd, rowbase};
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
@@ -454,12 +526,14 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   // cold hits (x < h0) go straight to global atomics; hot hits leave as masks
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
-  // segment descriptors are prefetched one segment ahead by thread 0 (queue
-  // grab at the top of a segment, descriptor + pivot row after the staging),
-  // so a segment starts on SMEM values instead of a chain of global latencies
-  auto fetch = [&](uint32_t q) {
+  // Segments are pipelined one ahead by thread 0: the next segment is taken
+  // from the queue at the top of the current one, and once the current
+  // segment's in-edge records have been read (after the staging scans) the
+  // next segment's slice of the in-edge index is bulk-copied into s_ine by the
+  // TMA unit, landing while this segment is walked.  A segment therefore
+  // starts on SMEM descriptors and records instead of a chain of global loads.
+  auto load_desc = [&](uint32_t q, const uint4& sg) {
     if (q < nsegs) {
-      const uint4 sg = segs[nsegs - 1 - q];  // heaviest (top ranks) first
       s_desc[0] = sg.x;
       s_desc[1] = sg.y;
       s_desc[2] = sg.z - sg.y;
@@ -468,7 +542,23 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     }
     s_desc[5] = q;
   };
-  if (threadIdx.x == 0) fetch(atomicAdd(queue, 1u));
+  // in-edge slice [i0, i1) -> s_ine[(i0 & 1) ..]: 16-byte aligned source, size
+  // rounded up to 16 bytes (the index carries 16 bytes of tail padding)
+  auto issue_ine = [&](const uint4& sg) {
+    const uint32_t a = sg.y & ~1u;
+    const uint32_t bytes = ((sg.z - a) * 8u + 15u) & ~15u;
+    bulk_g2s(s_ine, ine + a, bytes, &s_mbar);
+  };
+  uint32_t phase = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_mbar, 1);
+    const uint32_t q = atomicAdd(queue, 1u);
+    if (q < nsegs) {
+      s_sgn = segs[nsegs - 1 - q];  // heaviest (top ranks) first
+      issue_ine(s_sgn);
+    }
+    load_desc(q, s_sgn);
+  }
   while (true) {
     if (threadIdx.x == 0) {
       s_hits = 0;
@@ -479,7 +569,10 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     const uint32_t v = s_desc[0], i0 = s_desc[1], ni = s_desc[2];
     const uint32_t nb = s_desc[3], dv = s_desc[4];
     uint32_t qnext = 0;
-    if (threadIdx.x == 0) qnext = atomicAdd(queue, 1u);
+    if (threadIdx.x == 0) {
+      qnext = atomicAdd(queue, 1u);
+      if (qnext < nsegs) s_sgn = segs[nsegs - 1 - qnext];
+    }
     // (1a) hot members -> bitmap; s_cold = #members below h0 (sorted prefix)
     for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
       const uint32_t x = col[nb + j];
@@ -494,16 +587,18 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     constexpr int kIPT = kCtaSegItems / kJoinThreads;  // items per thread
     static_assert(kCtaSegItems % kJoinThreads == 0, "segment items must be a multiple of the CTA size");
     uint4 it[kIPT];
+    uint64_t mo[kIPT];
     uint32_t nh[kIPT], nc[kIPT];
+    mbar_wait(&s_mbar, phase);  // this segment's in-edge records have landed
+    phase ^= 1u;
 #pragma unroll
     for (int r = 0; r < kIPT; ++r) {
       const uint32_t i = threadIdx.x * kIPT + r;
       nh[r] = nc[r] = 0;
-      // defined on every path, it[] stays out of local memory: total-only
-      // 31.2 -> 30.9 ms at C4; the per-vertex variant measured 0.2 ms slower
-      if constexpr (!kPerVertex) it[r] = make_uint4(0, 0, 0, 0);
+      it[r] = make_uint4(0, 0, 0, 0);
+      mo[r] = 0;
       if (i < ni) {
-        it[r] = __ldcs(items + (uint64_t)(i0 + i) * (kPerVertex ? 2 : kItemStrideTotal));
+        it[r] = geo.hotcold(s_ine[i + (i0 & 1u)], kPerVertex ? &mo[r] : nullptr);
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -542,6 +637,11 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
         }
       }
       __syncthreads();
+      // every thread is past its s_ine reads: start the next segment's copy
+      if (threadIdx.x == 0 && qnext < nsegs) {
+        fence_proxy_async_smem();
+        issue_ine(s_sgn);
+      }
       lp = il - lp + s_wl[warp];
       cp = ic - cp + s_wc[warp];
       // s_wl/s_wc are rewritten only after the staging barrier below
@@ -556,10 +656,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
           s_hb[ph] = it[r].x;
           s_he[ph] = it[r].y;
           s_hpre[ph] = ch;
-          if (kPerVertex) {
-            const uint4 ex = __ldcs(items + (uint64_t)(i0 + i) * 2 + 1);
-            s_hmo[ph] = (unsigned long long)ex.z | ((unsigned long long)ex.w << 32);
-          }
+          if (kPerVertex) s_hmo[ph] = mo[r];
           s_hidx[ph] = (uint16_t)i;
           ++ph;
           ch += nh[r];
@@ -644,7 +741,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
         const uint32_t c = s_icnt[i];
         if (c) {
-          atomicAdd(&t_rank[items[(uint64_t)(i0 + i) * 2 + 1].x], (unsigned long long)c);
+          atomicAdd(&t_rank[ine[i0 + i].y], (unsigned long long)c);
           s_icnt[i] = 0;
         }
       }
@@ -652,7 +749,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     }
     if (ts && tab == gtab) __threadfence_block();
     __syncthreads();  // everyone is done with s_desc of this segment
-    if (threadIdx.x == 0) fetch(qnext);
+    if (threadIdx.x == 0) load_desc(qnext, s_sgn);
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
@@ -702,12 +799,15 @@ struct SmallWarpSmem {
 
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kSmallThreads) k_join_small(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint16_t* __restrict__ colH,
-    const uint4* __restrict__ items, const uint4* __restrict__ segs, uint32_t nsegs, unsigned int* __restrict__ queue,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd,
+    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine, const uint64_t* __restrict__ rowbase,
+    const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
     uint32_t h0, uint32_t nbm, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
     unsigned long long* __restrict__ total) {
   extern __shared__ __align__(16) uint8_t dsm_small[];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t nsegs = *nsegs_p;
+  const ItemGeo geo{rowd, rowbase};
   const uint32_t wbytes = (SmallWarpSmem::bytes(nbm) + 15) & ~15u;
   SmallWarpSmem w(dsm_small + warp * wbytes, nbm);
   for (uint32_t i = lane; i < nbm; i += 32) w.bm[i] = 0;
@@ -717,7 +817,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
   const uint32_t tmask = kSmallTable - 1, tshift = __clz(kSmallTable) + 1;  // 32 - log2(kSmallTable)
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, 0};
   unsigned long long acc = 0;
-  constexpr int S = kPerVertex ? 2 : kItemStrideTotal;
   while (true) {
     uint32_t q = 0;
     if (lane == 0) q = atomicAdd(queue, 1u);
@@ -737,13 +836,16 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
     for (uint32_t j = lane; j < cold; j += 32) hash_insert(w.tab, tmask, tshift, col[nb + j]);
     // (2) items (<= kSmallItems, kSmallR per lane) -> hot / cold lists with chunk prefixes
     uint4 it[kSmallR];
+    uint64_t mo[kSmallR];
     uint32_t nh[kSmallR], nc[kSmallR];
 #pragma unroll
     for (int r = 0; r < kSmallR; ++r) {
       const uint32_t i = lane + 32 * r;
       nh[r] = nc[r] = 0;
+      it[r] = make_uint4(0, 0, 0, 0);
+      mo[r] = 0;
       if (i < ni) {
-        it[r] = __ldcs(items + (uint64_t)(i0 + i) * S);
+        it[r] = geo.hotcold(ine[i0 + i], kPerVertex ? &mo[r] : nullptr);
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -764,10 +866,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
         w.he[ph] = it[r].y;
         w.hpre[ph] = ch;
         w.hidx[ph] = (uint16_t)i;
-        if (kPerVertex) {
-          const uint4 ex = __ldcs(items + (uint64_t)(i0 + i) * 2 + 1);
-          w.hmo[ph] = (unsigned long long)ex.z | ((unsigned long long)ex.w << 32);
-        }
+        if (kPerVertex) w.hmo[ph] = mo[r];
       }
       if (cf) {
         w.cb[pc] = it[r].z;
@@ -805,7 +904,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
       for (uint32_t i = lane; i < ni; i += 32) {
         const uint32_t c = w.icnt[i];
         if (c) {
-          atomicAdd(&t_rank[items[(uint64_t)(i0 + i) * 2 + 1].x], (unsigned long long)c);
+          atomicAdd(&t_rank[ine[i0 + i].y], (unsigned long long)c);
           w.icnt[i] = 0;
         }
       }
@@ -1015,9 +1114,32 @@ __device__ __forceinline__ void flush_top_rows(const uint32_t* top, uint32_t ncn
     if (top[i]) atomicAdd(&t_rank[rc + i], (unsigned long long)top[i]);
 }
 
+// Items of row u whose pivot lies in the part's rank range [v_lo, v_hi): a
+// contiguous range [k_lo, k_hi) of N+(u) (rows are sorted); the whole row
+// when the count is not split.
+struct PartRange {
+  const uint32_t* col;
+  uint32_t v_lo, v_hi;
+  bool split;
+  __device__ static __forceinline__ uint32_t lb(const uint32_t* a, uint32_t b, uint32_t e, uint32_t key) {
+    while (b < e) {
+      const uint32_t m = (b + e) >> 1;
+      if (a[m] < key) b = m + 1; else e = m;
+    }
+    return b;
+  }
+  __device__ __forceinline__ void items(uint32_t beg, uint32_t d, uint32_t& k_lo, uint32_t& k_hi) const {
+    k_lo = 0;
+    k_hi = d ? d - 1 : 0;  // item d-1 has an empty suffix (no mask bytes)
+    if (!split || d == 0) return;
+    k_lo = lb(col, beg, beg + d, v_lo) - beg;
+    k_hi = min(k_hi, lb(col, beg + k_lo, beg + d, v_hi) - beg);
+  }
+};
+
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
-    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t u_hi,
+    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t n, PartRange pr,
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,
     unsigned int* __restrict__ nheavy, uint32_t heavy_thr, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
@@ -1026,7 +1148,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
   init_spread(s_spread);
   __syncthreads();
   const unsigned lane = lane_id();
-  const uint32_t nrows = u_hi - u_lo + 1;
+  const uint32_t nrows = n;
   const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
   while (true) {
     unsigned long long rb64 = 0;  // 64-bit queue: row counts may approach 2^32
@@ -1035,14 +1157,17 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     if (rb64 >= nrows) break;
     const uint32_t rb = (uint32_t)rb64;
     const uint32_t i = rb + lane;
-    uint32_t ul = 0, dl = 0, Ol = 0, hl = 0;
+    uint32_t ul = 0, dl = 0, Ol = 0, hl = 0, kl = 0, kh = 0;
     bool work = false;
     if (i < nrows) {
-      ul = u_hi - i;
-      dl = off[ul + 1] - off[ul];
+      ul = n - 1 - i;
+      const uint32_t beg = off[ul];
+      dl = off[ul + 1] - beg;
       Ol = offH[ul];
       hl = offH[ul + 1] - Ol;
       work = hl > 0 && dl >= 2;
+      if (work) pr.items(beg, dl, kl, kh);
+      work = work && kh > kl;
       if (work) {
         const RowMasks rm(dl, Ol, hl);
         const uint32_t C = (uint32_t)(rm.c_hi - rm.c_lo);
@@ -1058,17 +1183,19 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       const int rj = __ffs(rows) - 1;
       rows &= rows - 1;
       const uint32_t u = __shfl_sync(0xffffffffu, ul, rj);
+      const uint32_t ka = __shfl_sync(0xffffffffu, kl, rj), kb = __shfl_sync(0xffffffffu, kh, rj);
       const RowMasks rm(__shfl_sync(0xffffffffu, dl, rj), __shfl_sync(0xffffffffu, Ol, rj),
                         __shfl_sync(0xffffffffu, hl, rj));
       const RowRel rr(rm);
-      const uint8_t* rowm = masks + rowbase[u - u_lo];
+      const uint8_t* rowm = masks + rowbase[u];
       const RowLanes rl(rr.C, lane);
       uint32_t row_total = 0;
       for (uint32_t g = 0; g < rr.C; g += rl.w) {
         const uint32_t cr = g + (lane & (rl.w - 1));
         const bool cvalid = cr < rr.C;
         uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        row_accumulate<kRowULight>(rr, rowm, cr, cvalid, rl, 0, rr.reaching(g, rl.w), s_spread, cnt);
+        const uint32_t reach = min(rr.reaching(g, rl.w), kb);
+        row_accumulate<kRowULight>(rr, rowm, cr, cvalid, rl, min(ka, reach), reach, s_spread, cnt);
         if (rl.G > 1) {  // sum the sub-groups: counts < 2^16 here, two per word
           uint32_t pk[4];
 #pragma unroll
@@ -1099,7 +1226,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
 
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
-    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t u_lo, uint32_t h0,
+    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, PartRange pr, uint32_t h0,
     uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, const uint32_t* __restrict__ heavy,
     const unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];
@@ -1119,19 +1246,22 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     const uint32_t r = s_row;
     if (r >= nh) break;
     const uint32_t u = heavy[r];
-    const uint32_t d = off[u + 1] - off[u], O = offH[u];
+    const uint32_t beg = off[u], d = off[u + 1] - beg, O = offH[u];
+    uint32_t k_lo = 0, k_hi = 0;
+    pr.items(beg, d, k_lo, k_hi);
     const RowMasks rm(d, O, offH[u + 1] - O);
     const RowRel rr(rm);
-    const uint8_t* rowm = masks + rowbase[u - u_lo];
+    const uint8_t* rowm = masks + rowbase[u];
     const RowLanes rl(rr.C, lane);
     my_total = 0;
     for (uint32_t g = 0; g < rr.C; g += rl.w) {
       const uint32_t cr = g + (lane & (rl.w - 1));
       const bool cvalid = cr < rr.C;
-      const uint32_t K = rr.reaching(g, rl.w);
+      const uint32_t K = min(rr.reaching(g, rl.w), k_hi);
+      const uint32_t K0 = min(k_lo, K);
       // this warp's slice of the items
-      const uint32_t per = (K + kRowWarps - 1) / kRowWarps;
-      const uint32_t ka = min(K, warp * per), kb = min(K, ka + per);
+      const uint32_t per = (K - K0 + kRowWarps - 1) / kRowWarps;
+      const uint32_t ka = min(K, K0 + warp * per), kb = min(K, ka + per);
       uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       row_accumulate<kRowUHeavy>(rr, rowm, cr, cvalid, rl, ka, kb, s_spread, cnt);
 #pragma unroll
@@ -1204,68 +1334,78 @@ struct Events {
 }  // namespace
 
 const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
+  if (g.part_bounds_P == parts && g.part_bounds.size() == (size_t)parts + 1) return g.part_bounds;
   cudaStream_t s = g.stream;
-  const uint64_t E = g.E;
+  const uint32_t n = g.n;
   g.part_bounds.assign((size_t)parts + 1, 0);
-  g.part_bounds[parts] = E;
-  if (E && parts > 1) {
-    const uint32_t n = g.n;
+  g.part_bounds[parts] = n;
+  if (g.E && parts > 1) {
+    DBuf<unsigned long long> jv(n, s);
     DBuf<uint64_t> prefix(n, s), tot(1, s), bnd((uint64_t)parts + 1, s);
-    const char* ic = getenv("TCB_ITEM_COST");  // tuning knob for the cost model
-    const uint64_t item_cost = ic ? strtoull(ic, nullptr, 10) : kItemCost;
-    scan_exclusive<uint64_t>(RowCost{g.off.get(), item_cost}, prefix.get(), n, tot.get(), s);
+    TC_CUDA(cudaMemsetAsync(jv.get(), 0, sizeof(unsigned long long) * n, s));
+    k_pivot_wedges<<<grid_gs(g.E, g.device), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), g.E, jv.get());
+    TC_LAUNCH();
+    const uint64_t item_cost = env_u32("TCB_ITEM_COST", (uint32_t)kItemCost);  // cost-model knobs
+    const uint64_t seg_cost = env_u32("TCB_SEG_COST", (uint32_t)kSegRowCost);
+    scan_exclusive<uint64_t>(PivotCost{g.off.get(), g.inoff.get(), jv.get(), item_cost, seg_cost}, prefix.get(), n,
+                             tot.get(), s);
     const uint64_t total_cost = read_scalar(tot.get(), s);
-    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), g.off.get(), n, E, total_cost, parts,
-                                                          bnd.get());
+    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), n, total_cost, parts, bnd.get());
     TC_LAUNCH();
     TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
                             cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
   }
+  g.part_bounds_P = parts;
   return g.part_bounds;
 }
+
+namespace {
+template <typename K>
+int occupancy(K kern, int threads, size_t smem) {
+  TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  return occ < 1 ? 1 : occ;
+}
+}  // namespace
 
 void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, uint64_t* d_pv,
                      tc_count_stats* stats) {
   cudaStream_t s = g.stream;
   const int dev = g.device;
   const uint32_t n = g.n;
-  const uint64_t E = g.E;
   const uint32_t parts = opts.part_count ? opts.part_count : 1;
   const uint32_t part = opts.part_count ? opts.part_index : 0;
   const bool pv = d_pv != nullptr;
+  const bool timing = stats != nullptr;
   Events ev;
-  TC_CUDA(cudaEventRecord(ev.e[0], s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[0], s));
   uint64_t kl = 0;  // kernels launched by this call
   PhaseLog pl(s);
 
-  DBuf<unsigned long long> acc(1, s);
-  TC_CUDA(cudaMemsetAsync(acc.get(), 0, sizeof(unsigned long long), s));
+  unsigned long long* acc = g.scratch[kSlotAcc].get<unsigned long long>(2, s);  // [0] total, [1] row queue
+  TC_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), s));
   unsigned long long* t_rank = nullptr;
   if (pv) {
     t_rank = g.scratch[kSlotTRank].get<unsigned long long>(n ? n : 1, s);
     TC_CUDA(cudaMemsetAsync(t_rank, 0, sizeof(unsigned long long) * (n ? n : 1), s));
   }
 
-  // ---- level-1 frontier of the whole graph, or of this part's
-  //      degree-weighted oriented-edge range (multi-GPU) ----
-  uint64_t part_e0 = 0, part_e1 = E;
-  if (parts > 1 && E) {
-    kl += 4;
-    const std::vector<uint64_t>& b = partition_bounds(g, parts);
-    part_e0 = b[part];
-    part_e1 = b[part + 1];
+  // ---- level-1 frontier plan of the whole graph, or of this part's
+  //      degree-weighted pivot rank range (multi-GPU) ----
+  uint32_t v_lo = 0, v_hi = n;
+  if (parts > 1 && g.E) {
+    const std::vector<uint64_t>& b = partition_bounds(g, parts);  // cached per P
+    v_lo = (uint32_t)b[part];
+    v_hi = (uint32_t)b[part + 1];
   }
-  Frontier fr;
-  kl += build_frontier(g, part_e0, part_e1, pv, fr);
-  const uint4* wsegs = fr.wsegs;
-  const uint4* csegs = fr.csegs;
-  const uint64_t NSW = fr.nw, NSC = fr.nc, NSS = fr.ns;
-  // hot hit masks of the CTA and small bins (the frontier zeroed the bytes of
-  // every other item)
-  uint8_t* masks = pv ? fr.masks : nullptr;
-  pl.mark("frontier");
-  TC_CUDA(cudaEventRecord(ev.e[1], s));
+  const bool split = v_lo != 0 || v_hi != n;
+  Plan plan;
+  kl += build_plan(g, v_lo, v_hi, pv, stats != nullptr && opts.work_counters != 0, plan);
+  uint8_t* masks = plan.masks;
+  pl.mark("plan");
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[1], s));
 
   // ---- advance + join ----
   const int sms = num_sms(dev);
@@ -1279,125 +1419,118 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const uint32_t dbg = env_u32("TCB_PV_DBG", 0);
     TC_CUDA(cudaMemcpyToSymbolAsync(g_pv_dbg, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, s));
   }
-  if (NSW) {
+  const uint32_t nbm = (n - g.h0 + 31) / 32;
+  unsigned int* queues = g.scratch[kSlotCounters].get<unsigned int>(8, s) + 4;  // [0..3] = plan.nseg
+  TC_CUDA(cudaMemsetAsync(queues, 0, 4 * sizeof(unsigned int), s));
+  if (plan.cap[0]) {
     // warp bin: plain 32-bit counters over half the window
     const uint32_t ncnt_w = ncnt / 2, rc_w = pv ? n - ncnt_w : 0xffffffffu;
     const size_t smem = (size_t)ncnt_w * sizeof(uint32_t);
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
-    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, smem));
-    const unsigned grid =
-        (unsigned)std::min<uint64_t>(ceil_div64(NSW, kJoinWarps), (uint64_t)sms * std::max(occ, 1));
-    pl.mark("warp_setup");
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.col.get(), g.src.get(), fr.items,
-                                         wsegs, (uint32_t)NSW, rc_w, ncnt_w, t_rank, acc.get());
+    const int occ = occupancy(kern, kJoinThreads, smem);
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(plan.cap[0], kJoinWarps), (uint64_t)sms * occ);
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.offH.get(), g.col.get(), g.ine.get(), plan.wsegs,
+                                         plan.nseg + 0, rc_w, ncnt_w, plan.rowbase, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_warp");
   }
-  if (NSS) {
-    DBuf<unsigned int> squeue(1, s);
-    TC_CUDA(cudaMemsetAsync(squeue.get(), 0, sizeof(unsigned int), s));
-    const uint32_t nbm = (n - g.h0 + 31) / 32;
+  if (plan.cap[2]) {
     const size_t ssm = (size_t)kSmallWarps * ((SmallWarpSmem::bytes(nbm) + 15) & ~15u);
     auto kern = pv ? k_join_small<true> : k_join_small<false>;
-    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    int occ = 0;
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSmallThreads, ssm));
-    const unsigned grid =
-        (unsigned)std::min<uint64_t>((uint64_t)sms * std::max(occ, 1), ceil_div64(NSS, kSmallWarps));
-    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.colH.get(), fr.items, fr.ssegs, (uint32_t)NSS,
-                                         squeue.get(), g.h0, nbm, masks, t_rank, acc.get());
+    const int occ = occupancy(kern, kSmallThreads, ssm);
+    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, ceil_div64(plan.cap[2], kSmallWarps));
+    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.colH.get(), g.ine.get(),
+                                         plan.rowbase, plan.ssegs, plan.nseg + 2, queues + 0, g.h0, nbm, masks,
+                                         t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_small");
   }
-  if (NSC) {
-    DBuf<unsigned int> queue(1, s);
-    TC_CUDA(cudaMemsetAsync(queue.get(), 0, sizeof(unsigned int), s));
-    const uint32_t nbm = (n - g.h0 + 31) / 32;
+  if (plan.cap[1]) {
     // cold members spill to a per-CTA global slab only when a pivot has more
     // than smem_slots/2 members below h0
     const uint32_t cap = table_size_for(g.max_dplus);
     const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
     const size_t dsm = ((size_t)nbm + kCtaSmemSlots) * sizeof(uint32_t);
     auto kern = pv ? k_join_cta<true> : k_join_cta<false>;
-    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-    int occ = 0;
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kJoinThreads, dsm));
-    if (occ < 1) occ = 1;
-    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, NSC);
+    const int occ = occupancy(kern, kJoinThreads, dsm);
+    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, plan.cap[1]);
     uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
-    pl.mark("cta_setup");
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.src.get(), g.colH.get(), fr.items,
-                                        csegs, (uint32_t)NSC, queue.get(), g.h0, nbm, smem_slots,
-                                        slab_cap, slab, masks, t_rank, acc.get());
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.colH.get(), g.ine.get(),
+                                        plan.rowbase, plan.csegs, plan.nseg + 1, queues + 1, g.h0, nbm, smem_slots,
+                                        slab_cap, slab, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_cta");
   }
-  if (pv && (NSC || NSS)) {
-    {
-      // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics)
-      DBuf<unsigned int> rq(3, s);  // -, heavy queue, heavy count
-      DBuf<unsigned long long> lq(1, s);  // light row queue
-      TC_CUDA(cudaMemsetAsync(rq.get(), 0, 3 * sizeof(unsigned int), s));
-      TC_CUDA(cudaMemsetAsync(lq.get(), 0, sizeof(unsigned long long), s));
-      uint32_t* heavy = g.scratch[kSlotHeavy].get<uint32_t>((uint64_t)(fr.u_hi - fr.u_lo) + 1, s);
-      const uint32_t rcnt = n < top_cnt ? n : top_cnt;
-      const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
-      TC_CUDA(cudaFuncSetAttribute(k_pv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      TC_CUDA(cudaFuncSetAttribute(k_pv_rows_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      int rocc = 0, hocc = 0;
-      TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rocc, k_pv_rows, kRowWarps * 32, rsm));
-      TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_pv_rows_heavy, kRowWarps * 32, rsm));
-      k_pv_rows<<<(unsigned)(sms * std::max(rocc, 1)), kRowWarps * 32, rsm, s>>>(
-          g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, fr.u_hi, g.h0, n - rcnt, rcnt,
-          lq.get(), heavy, rq.get() + 2, row_heavy_threshold((uint64_t)fr.u_hi - fr.u_lo + 1), t_rank);
-      TC_LAUNCH();
-      ++launches;
-      pl.mark("pv_rows_light");
-      k_pv_rows_heavy<<<(unsigned)(sms * std::max(hocc, 1)), kRowWarps * 32, rsm, s>>>(
-          g.off.get(), g.colH.get(), g.offH.get(), fr.rowbase, masks, fr.u_lo, g.h0, n - rcnt, rcnt,
-          rq.get() + 1, heavy, rq.get() + 2, t_rank);
-      TC_LAUNCH();
-      ++launches;
-      pl.mark("pv_rows");
-    }
+  if (pv && n && g.mask_total) {
+    // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics); a split
+    // count folds only the items of its own pivots
+    unsigned int* rq = queues + 2;  // heavy queue, heavy count
+    unsigned long long* lq = g.scratch[kSlotAcc].get<unsigned long long>(2, s) + 1;
+    TC_CUDA(cudaMemsetAsync(lq, 0, sizeof(unsigned long long), s));
+    uint32_t* heavy = g.scratch[kSlotHeavy].get<uint32_t>(n, s);
+    const uint32_t rcnt = n < top_cnt ? n : top_cnt;
+    const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
+    const int rocc = occupancy(k_pv_rows, kRowWarps * 32, rsm);
+    const int hocc = occupancy(k_pv_rows_heavy, kRowWarps * 32, rsm);
+    const PartRange pr{g.col.get(), v_lo, v_hi, split};
+    k_pv_rows<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
+        g.off.get(), g.colH.get(), g.offH.get(), plan.rowbase, masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1,
+        row_heavy_threshold(n), t_rank);
+    TC_LAUNCH();
+    ++launches;
+    pl.mark("pv_rows_light");
+    k_pv_rows_heavy<<<(unsigned)(sms * hocc), kRowWarps * 32, rsm, s>>>(
+        g.off.get(), g.colH.get(), g.offH.get(), plan.rowbase, masks, pr, g.h0, n - rcnt, rcnt, rq, heavy, rq + 1,
+        t_rank);
+    TC_LAUNCH();
+    ++launches;
+    pl.mark("pv_rows");
   }
-  TC_CUDA(cudaEventRecord(ev.e[2], s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[2], s));
 
   // ---- outputs ----
-  TC_CUDA(cudaMemcpyAsync(d_total, acc.get(), sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  TC_CUDA(cudaMemcpyAsync(d_total, acc, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
   if (pv && n) {
     k_gather_pv<<<grid_gs(n, dev), 256, 0, s>>>(t_rank, g.rank_of.get(), n, d_pv);
     TC_LAUNCH();
     ++kl;
   }
-  TC_CUDA(cudaEventRecord(ev.e[3], s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[3], s));
   if (stats) {
     TC_CUDA(cudaEventSynchronize(ev.e[3]));
-    read_frontier_sums(fr, s);
+    read_plan_sums(plan, s);
     stats->frontier_ms = ev.ms(0, 1);
     stats->join_ms = ev.ms(1, 2);
     stats->reduce_ms = ev.ms(2, 3);
     stats->total_ms = ev.ms(0, 3);
-    stats->items = fr.nitems;
-    stats->wedges = fr.J;
-    stats->segments = NSW + NSC + NSS;
     stats->join_launches = launches;
-    stats->dag_W = (double)fr.W;
-    stats->pivots = fr.pivots;
     stats->kernel_launches = kl + launches;
-    // this part's share of SURVEY 8d's B_alg (vertex terms on part 0): the
-    // parts' values sum to the whole graph's
-    stats->alg_bytes = 4.0 * (double)fr.W + 12.0 * (double)(part_e1 - part_e0) +
-                       (part == 0 ? 8.0 * ((double)n + 1) + (pv ? 8.0 * n : 0.0) : 0.0);
-    // bytes the implemented join must stream: hot ids 2 B, cold ids 4 B,
-    // items 16 B, pivot lists 4 B per member (whole graph; a part does ~1/P)
-    stats->probe_bytes = 2.0 * (double)fr.hot + 4.0 * (double)(fr.J - fr.hot) +
-                         16.0 * (double)fr.nitems + 4.0 * (double)(part_e1 - part_e0);
+    stats->part_first_vertex = v_lo;
+    stats->part_last_vertex = v_hi;
+    if (opts.work_counters) {
+      stats->items = plan.items;
+      stats->wedges = plan.J;
+      stats->pivots = plan.pivots;
+      stats->dag_W = (double)plan.W;
+      // this part's share of SURVEY 8d's B_alg (vertex terms on part 0): the
+      // parts' values sum to the whole graph's.  |E+| is counted per in-edge
+      // of the part's pivots.
+      uint32_t in_lo = 0, in_hi = 0;
+      TC_CUDA(cudaMemcpy(&in_lo, g.inoff.get() + v_lo, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      TC_CUDA(cudaMemcpy(&in_hi, g.inoff.get() + v_hi, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      const double Ep = (double)(in_hi - in_lo);
+      stats->alg_bytes = 4.0 * (double)plan.W + 12.0 * Ep +
+                         (part == 0 ? 8.0 * ((double)n + 1) + (pv ? 8.0 * n : 0.0) : 0.0);
+      // bytes the implemented join streams per count: hot ids 2 B, cold ids
+      // 4 B, the in-edge record 8 B + its row geometry 16 B per item, the
+      // pivot rows 4 B per member per segment; per-vertex: the hit masks
+      // written and read back (1 B per hot chunk, twice) and the u64 counters
+      stats->probe_bytes = 2.0 * (double)plan.hot + 4.0 * (double)(plan.J - plan.hot) + 24.0 * Ep +
+                           4.0 * Ep + (pv ? 2.0 * (double)g.mask_total + 16.0 * n : 0.0);
+    }
   }
 }
 

@@ -43,8 +43,8 @@ struct Scratch {
   }
 };
 enum ScratchSlot {
-  kSlotCnt, kSlotIn, kSlotItems, kSlotRowBase, kSlotWoff, kSlotWsegs,
-  kSlotCsegs, kSlotMasks, kSlotSlab, kSlotTRank, kSlotHeavy, kSlotSsegs, kSlotPacked, kSlotSums, kSlotCount
+  kSlotRowBase, kSlotSegOff, kSlotWsegs, kSlotCsegs, kSlotSsegs, kSlotMasks, kSlotSlab, kSlotTRank,
+  kSlotHeavy, kSlotCls, kSlotSums, kSlotCounters, kSlotAcc, kSlotCount
 };
 }  // namespace tcb
 
@@ -67,10 +67,32 @@ struct tc_graph {
   uint32_t h0 = 0;
   tcb::DBuf<uint16_t> colH;
   tcb::DBuf<uint32_t> offH;
-  // multi-GPU work partition (count.cu): oriented-edge ranges [b[p], b[p+1])
-  // with ~equal wedge work, recomputed by every multi-part count
+  // In-edge index: the oriented edges grouped by head, ine[inoff[v] ..
+  // inoff[v+1]) = {e, u} for every u->v (e = its position in col).  Together
+  // with off/col this is the reference's symmetric adjacency split by
+  // orientation (N+(v) and N-(v)); it is what makes the level-1 frontier of a
+  // count a plan over |V| instead of a scatter over |E| (plan.cu).
+  tcb::DBuf<uint32_t> inoff;
+  tcb::DBuf<uint2> ine;
+  // Row geometry interleaved per rank, {off[u], off[u+1], offH[u], offH[u+1]}:
+  // a join stages an item's suffix with one 16-byte load instead of four.
+  tcb::DBuf<uint4> rowd;
+  // Count-plan capacities (graph properties, recorded once at build): work
+  // segments per pivot class over the whole graph (any part has at most as
+  // many) and the per-vertex mask bytes of all rows.
+  uint64_t seg_cap[3] = {0, 0, 0};
+  uint64_t mask_total = 0;
+  // multi-GPU work partition (count.cu): pivot rank ranges [b[p], b[p+1])
+  // with ~equal join work; computed on the first P-part count, then reused
   std::vector<uint64_t> part_bounds;
+  uint32_t part_bounds_P = 0;
   tcb::Scratch scratch[tcb::kSlotCount];
+  // Every call that touches the handle's scratch, stream or partition state
+  // (count, listings, export, degrees, partition bounds, set_stream) holds
+  // this for its whole duration: concurrent calls on one Graph (allowed by the
+  // reference, graph.hpp:33-34) are serialised, never interleaved on the
+  // shared per-count buffers.
+  std::mutex mu;
 };
 
 namespace tcb {
@@ -108,43 +130,59 @@ constexpr int kItemStrideTotal = TCB_ITEM_STRIDE_TOTAL;
 constexpr uint32_t kSmallItems = TCB_SMALL_ITEMS;  // multiple of 32
 constexpr uint32_t kSmallCold = TCB_SMALL_COLD;    // power of two
 
-// Level-1 frontier of one count (frontier.cu): the useful in-edges u->v of
-// every pivot v (d+(v) > 0, non-empty suffix) in the part's oriented-edge
-// range [e0, e1), grouped by v -- the transpose of the oriented CSR restricted
-// to wedge-producing edges, i.e. the reference's level-1 PartialTable rows
-// (u, v) (matcher.cpp:136-198).  Built inside every tc_count (timed), in the
-// handle's scratch.
-//   items      one record of S uint4 per item (S = 1, or 2 with per-vertex
-//                counts), written as one 16/32-byte store:
-//                [0] {hb,he,cb,ce} (CTA-bin pivots: hot range in colH, cold
-//                    range in col) or {b,e,0,0} (warp-bin pivots: col range);
-//                    all-zero = an in-edge with an empty suffix
-//                [1] {u, 0, mo_lo, mo_hi}: the source u and the byte offset of
-//                    the item's hit masks (one byte per hot chunk from its
-//                    first hot chunk to the row's last, RowMasks below)
-//   in[v]      = first item slot of pivot v (n+1; deg(v) - d+(v) slots each);
-//                its items are in[v] .. in[v] + cursor[v] (a multi-GPU part
-//                fills only the slots of its own edges)
-//   rowbase[u-u_lo] = per-vertex only: first mask byte of row u (rows
-//                [u_lo, u_hi] of the part)
-//   wsegs / csegs / ssegs = {v, i0, i1, 0} work segments per bin
-struct Frontier {
-  uint4* items = nullptr;
-  uint32_t* in = nullptr;
-  uint64_t* rowbase = nullptr;
-  uint8_t* masks = nullptr;  // per-vertex hit masks (mask_bytes), written by the joins
+// Count plan of one part (plan.cu): the pivots v in the part's rank range
+// [v_lo, v_hi) that can close a triangle, classified and cut into work
+// segments {v, i0, i1, 0} over the in-edge index positions
+// [inoff[v], inoff[v+1]).  An item of pivot v is in-edge ine[i] = {e, u}: the
+// reference's level-1 row (u, v) (matcher.cpp:136-198), whose wedge suffix is
+// col[e+1 .. off[u+1]) -- its geometry (hot part in colH, cold part in col,
+// per-vertex mask offset) is computed by the join when it stages the segment.
+// Everything here is built inside every tc_count (timed) with no host
+// synchronisation: list lengths live in device memory (nseg), list capacities
+// are graph properties recorded at build (tc_graph::seg_cap).
+//   wsegs  warp bin   (d+(v) <= kWarpMaxDeg, and d+(v) = 0 pivots whose
+//                      per-vertex mask bytes must be zeroed)
+//   csegs  CTA bin    (kCtaSegItems items per segment)
+//   ssegs  small bin  (<= kSmallItems items, <= kSmallCold cold members)
+//   rowbase[u] = first mask byte of row u (per-vertex; all rows, RowMasks)
+struct Plan {
   uint4* wsegs = nullptr;
   uint4* csegs = nullptr;
-  uint4* ssegs = nullptr;  // small CTA-bin pivots, one segment each (k_join_small)
-  uint64_t e0 = 0, e1 = 0, nitems = 0, nw = 0, nc = 0, ns = 0, pivots = 0, mask_bytes = 0;
-  uint32_t u_lo = 0, u_hi = 0;  // rows the part's edges come from (inclusive)
-  uint64_t W = 0, J = 0, hot = 0, items_c = 0;  // counters: filled by read_frontier_sums (stats only)
-  const void* sums = nullptr;
+  uint4* ssegs = nullptr;
+  uint32_t* nseg = nullptr;  // device: [0] warp, [1] CTA, [2] small segment counts
+  uint64_t* rowbase = nullptr;
+  uint8_t* masks = nullptr;
+  uint32_t v_lo = 0, v_hi = 0;
+  uint64_t cap[3] = {0, 0, 0};
+  uint64_t W = 0, J = 0, hot = 0, items = 0, pivots = 0;  // stats (read_plan_sums)
+  void* sums = nullptr;
 };
 // Returns the number of kernels launched.
-int build_frontier(tc_graph& g, uint64_t e0, uint64_t e1, bool per_vertex, Frontier& fr);
-// The frontier's counters (W, J, hot, items) -- a read, so only for stats.
-void read_frontier_sums(Frontier& fr, cudaStream_t s);
+int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool want_sums, Plan& p);
+// The plan's work counters (W, J, hot, items, pivots) -- a read, only for stats.
+void read_plan_sums(Plan& p, cudaStream_t s);
+
+// Pivot class (graph property): 0 = warp bin (d+(v) <= kWarpMaxDeg; with
+// per-vertex counts also d+(v) = 0 pivots, whose items' mask bytes the warp
+// join zeroes), 1 = CTA bin, 2 = small CTA pivots (<= kSmallItems in-edges
+// and <= kSmallCold members below the hot window: one warp each), -1 = none.
+__host__ __device__ __forceinline__ uint32_t segs_per_class(int c) {
+  return c == 0 ? kWarpSegItems : c == 1 ? kCtaSegItems : kSmallItems;
+}
+struct PivotClass {
+  const uint32_t* off;
+  const uint32_t* offH;
+  const uint32_t* inoff;
+  bool pv;
+  __device__ __forceinline__ int operator()(uint32_t v, uint32_t& din) const {
+    const uint32_t dv = off[v + 1] - off[v];
+    din = inoff[v + 1] - inoff[v];
+    if (din == 0 || (dv == 0 && !pv)) return -1;
+    if (dv <= kWarpMaxDeg) return 0;
+    const uint32_t hv = offH[v + 1] - offH[v];
+    return (din <= kSmallItems && dv - hv <= kSmallCold) ? 2 : 1;
+  }
+};
 
 // Per-vertex hit-mask layout of row u (closed form, no per-edge scan).  Row u
 // has d = d+(u) out-edges, the last h of them hot (colH[O, O+h), O = offH[u]),
@@ -239,6 +277,19 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total,
                      uint64_t* d_per_vertex, tc_count_stats* stats);
 // Degree-weighted oriented-edge ranges of a P-way split.
 const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts);
+
+// Multi-GPU (multi.cu).
+void comm_unique_id(void* id);
+tc_comm* comm_init_rank(const void* id, int nranks, int rank, int device);
+void comm_destroy(tc_comm* c);
+void count_allreduce(tc_comm* c, tc_graph& g, const tc_count_opts& o, uint64_t* d_total, uint64_t* d_pv,
+                     tc_count_stats* st);
+tc_multi* multi_create(const int* devices, int nparts);
+void multi_destroy(tc_multi* m);
+int multi_parts(const tc_multi* m);
+int multi_part_device(const tc_multi* m, int p);
+void count_multi(tc_multi* m, tc_graph* const* graphs, const tc_count_opts& o, uint64_t* d_total, uint64_t* d_pv,
+                 tc_count_stats* st);
 
 // MatrixMarket entry tokenizer (mm.cu): true and device pairs when the body is
 // well formed, false when the host parser must report the error.

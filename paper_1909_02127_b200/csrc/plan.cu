@@ -1,0 +1,214 @@
+// plan.cu -- the level-1 frontier of one count as a work plan over |V|.
+//
+// The reference materialises level-1 rows (u, w) with expand_level
+// (matcher.cpp:136-198: advance over N(u), accept w > u, 2-core membership,
+// look-ahead) before its final level.  Here the level-1 rows of pivot v are
+// exactly its in-edges u->v, which the graph holds grouped by head (the
+// in-edge index ine, build.cu finish_graph), so the frontier of a count is
+// only a plan: every pivot in the part's rank range [v_lo, v_hi) is
+// classified (graph.cuh PivotClass) and cut into work segments {v, i0, i1}
+// over its in-edge positions.  The joins compute each item's geometry when
+// they stage the segment (count.cu).
+//   k_plan_class   class + 1 per pivot (one byte)
+//   two scans      segment offsets: warp|CTA packed in a u64, small in a u32
+//   k_plan_segs    segment lists; the list lengths go to device memory
+//   rowbase        per-vertex only: exclusive scan of each row's hit-mask
+//                  bytes (closed form, graph.cuh RowMasks), all rows
+// No host synchronisation: list capacities are the graph's seg_cap.
+#include <cuda_runtime.h>
+
+#include "graph.cuh"
+#include "prim.cuh"
+
+namespace tcb {
+namespace {
+
+constexpr int kT = 256;
+
+unsigned grid_gs(uint64_t n, int device) {
+  const uint64_t cap = (uint64_t)num_sms(device) * 16;
+  uint64_t g = ceil_div64(n, kT);
+  if (g < 1) g = 1;
+  return (unsigned)(g < cap ? g : cap);
+}
+
+struct Sums {
+  unsigned long long W, J, hot, items, pivots;
+};
+
+__global__ void k_plan_class(PivotClass pc, uint32_t v_lo, uint32_t v_hi, uint8_t* __restrict__ cls) {
+  for (uint64_t v = v_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < v_hi;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t din = 0;
+    cls[v - v_lo] = (uint8_t)(pc((uint32_t)v, din) + 1);
+  }
+}
+
+// Segment counts of pivot v_lo + i: warp bin in the low 32 bits, CTA bin in
+// the high 32 (SegWC); small bin (SegS).
+struct SegWC {
+  const uint8_t* cls;
+  const uint32_t* inoff;
+  uint32_t v_lo;
+  __device__ __forceinline__ unsigned long long operator()(uint64_t i) const {
+    const uint32_t c = cls[i];
+    if (c != 1 && c != 2) return 0ull;
+    const uint32_t din = inoff[v_lo + i + 1] - inoff[v_lo + i];
+    return c == 1 ? (unsigned long long)((din + kWarpSegItems - 1) / kWarpSegItems)
+                  : (unsigned long long)((din + kCtaSegItems - 1) / kCtaSegItems) << 32;
+  }
+};
+struct SegS {
+  const uint8_t* cls;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return cls[i] == 3 ? 1u : 0u; }
+};
+
+__global__ void k_plan_segs(const uint8_t* __restrict__ cls, const uint32_t* __restrict__ inoff, uint32_t v_lo,
+                            uint32_t v_hi, const unsigned long long* __restrict__ off_wc,
+                            const uint32_t* __restrict__ off_s, const unsigned long long* __restrict__ tot_wc,
+                            const uint32_t* __restrict__ tot_s, uint4* __restrict__ wsegs, uint4* __restrict__ csegs,
+                            uint4* __restrict__ ssegs, uint32_t* __restrict__ nseg) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    nseg[0] = (uint32_t)*tot_wc;
+    nseg[1] = (uint32_t)(*tot_wc >> 32);
+    nseg[2] = *tot_s;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (uint64_t)(v_hi - v_lo);
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = cls[i];
+    if (c == 0) continue;
+    const uint32_t v = v_lo + (uint32_t)i;
+    const uint32_t a = inoff[v], b = inoff[v + 1];
+    if (c == 3) {
+      ssegs[off_s[i]] = make_uint4(v, a, b, 0);
+      continue;
+    }
+    const uint32_t per = c == 1 ? kWarpSegItems : kCtaSegItems;
+    uint4* out = c == 1 ? wsegs : csegs;
+    uint32_t s = c == 1 ? (uint32_t)off_wc[i] : (uint32_t)(off_wc[i] >> 32);
+    for (uint32_t j = a; j < b; j += per) out[s++] = make_uint4(v, j, min(j + per, b), 0);
+  }
+}
+
+// Mask bytes of row u (all rows).
+struct RowBytes {
+  const uint32_t* off;
+  const uint32_t* offH;
+  __device__ __forceinline__ uint64_t operator()(uint64_t u) const {
+    const uint32_t O = offH[u];
+    return RowMasks(off[u + 1] - off[u], O, offH[u + 1] - O).total();
+  }
+};
+
+// Work counters of the part (stats only): per in-edge its suffix length (J)
+// and hot share, per pivot W = din * d+ (SURVEY 8d wedge stream).
+__global__ void k_plan_work(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH,
+                            const uint32_t* __restrict__ inoff, const uint2* __restrict__ ine, uint32_t v_lo,
+                            uint32_t v_hi, Sums* __restrict__ sums) {
+  unsigned long long W = 0, J = 0, H = 0, I = 0, P = 0;
+  for (uint64_t v = v_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < v_hi;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t dv = off[v + 1] - off[v];
+    const uint32_t a = inoff[v], b = inoff[v + 1];
+    if (!dv || a == b) continue;
+    W += (unsigned long long)dv * (b - a);
+    bool any = false;
+    for (uint32_t i = a; i < b; ++i) {
+      const uint2 eu = ine[i];
+      const uint32_t end = off[eu.y + 1];
+      if (eu.x + 1 >= end) continue;
+      any = true;
+      ++I;
+      const uint32_t O = offH[eu.y], h = offH[eu.y + 1] - O;
+      const uint32_t suf = end - eu.x - 1;
+      J += suf;
+      H += suf < h ? suf : h;
+    }
+    P += any;
+  }
+  W = warp_sum(W);
+  J = warp_sum(J);
+  H = warp_sum(H);
+  I = warp_sum(I);
+  P = warp_sum(P);
+  if (lane_id() == 0) {
+    if (W) atomicAdd(&sums->W, W);
+    if (J) atomicAdd(&sums->J, J);
+    if (H) atomicAdd(&sums->hot, H);
+    if (I) atomicAdd(&sums->items, I);
+    if (P) atomicAdd(&sums->pivots, P);
+  }
+}
+
+}  // namespace
+
+int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool want_sums, Plan& p) {
+  cudaStream_t s = g.stream;
+  const uint32_t n = g.n;
+  const int dev = g.device;
+  int kl = 0;
+  PhaseLog pl(s);
+  p.v_lo = v_lo;
+  p.v_hi = v_hi;
+  const uint32_t np = v_hi - v_lo;
+  p.nseg = g.scratch[kSlotCounters].get<uint32_t>(8, s);  // [0..3] segment counts, [4..7] join queues
+  for (int c = 0; c < 3; ++c) p.cap[c] = g.seg_cap[c];
+  p.wsegs = g.scratch[kSlotWsegs].get<uint4>(p.cap[0], s);
+  p.csegs = g.scratch[kSlotCsegs].get<uint4>(p.cap[1], s);
+  p.ssegs = g.scratch[kSlotSsegs].get<uint4>(p.cap[2], s);
+  if (np == 0) {
+    TC_CUDA(cudaMemsetAsync(p.nseg, 0, 4 * sizeof(uint32_t), s));
+  } else {
+    uint8_t* cls = g.scratch[kSlotCls].get<uint8_t>(np, s);
+    const PivotClass pc{g.off.get(), g.offH.get(), g.inoff.get(), per_vertex};
+    k_plan_class<<<grid_gs(np, dev), kT, 0, s>>>(pc, v_lo, v_hi, cls);
+    TC_LAUNCH();
+    ++kl;
+    // [0, np) u64 warp|CTA offsets, then [np, 2np) u32 small offsets, totals at the end
+    unsigned long long* off_wc = g.scratch[kSlotSegOff].get<unsigned long long>(2 * (uint64_t)np + 2, s);
+    uint32_t* off_s = reinterpret_cast<uint32_t*>(off_wc + np);
+    unsigned long long* tot_wc = off_wc + 2 * (uint64_t)np;
+    uint32_t* tot_s = reinterpret_cast<uint32_t*>(off_wc + 2 * (uint64_t)np + 1);
+    kl += scan_exclusive<unsigned long long>(SegWC{cls, g.inoff.get(), v_lo}, off_wc, np, tot_wc, s);
+    kl += scan_exclusive<uint32_t>(SegS{cls}, off_s, np, tot_s, s);
+    k_plan_segs<<<grid_gs(np, dev), kT, 0, s>>>(cls, g.inoff.get(), v_lo, v_hi, off_wc, off_s, tot_wc, tot_s,
+                                                p.wsegs, p.csegs, p.ssegs, p.nseg);
+    TC_LAUNCH();
+    ++kl;
+  }
+  pl.mark("plan_segs");
+  p.rowbase = nullptr;
+  p.masks = nullptr;
+  if (per_vertex && n) {
+    p.rowbase = g.scratch[kSlotRowBase].get<uint64_t>((uint64_t)n + 1, s);
+    kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get()}, p.rowbase, n, p.rowbase + n, s);
+    p.masks = g.scratch[kSlotMasks].get<uint8_t>(g.mask_total + 32, s);
+    pl.mark("plan_rowbase");
+  }
+  p.sums = nullptr;
+  if (want_sums) {
+    Sums* sums = g.scratch[kSlotSums].get<Sums>(1, s);
+    TC_CUDA(cudaMemsetAsync(sums, 0, sizeof(Sums), s));
+    if (np) {
+      k_plan_work<<<grid_gs(np, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.inoff.get(), g.ine.get(), v_lo,
+                                                  v_hi, sums);
+      TC_LAUNCH();
+    }
+    p.sums = sums;
+  }
+  return kl;
+}
+
+void read_plan_sums(Plan& p, cudaStream_t s) {
+  if (!p.sums) return;
+  Sums h;
+  TC_CUDA(cudaMemcpyAsync(&h, p.sums, sizeof(Sums), cudaMemcpyDeviceToHost, s));
+  TC_CUDA(cudaStreamSynchronize(s));
+  p.W = h.W;
+  p.J = h.J;
+  p.hot = h.hot;
+  p.items = h.items;
+  p.pivots = h.pivots;
+}
+
+}  // namespace tcb

@@ -1,0 +1,84 @@
+"""Host restatement of the multi-GPU work split (TEST INFRASTRUCTURE).
+
+The device split (count.cu k_pivot_wedges + PivotCost + k_part_bounds) gives
+part p the pivots -- the middle vertices of the (deg,id) order -- with rank in
+[b[p], b[p+1]): contiguous rank ranges of ~equal join work.  This restates it
+with numpy so the split can be checked on CPU (tests/test_multigpu_gloo.py)
+and pinned to the device bounds (test_gpu_parity::test_partition_bounds_match_host).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+ITEM_COST = 24     # count.cu kItemCost: per in-edge item, in candidate-probe units
+SEG_COST = 4       # count.cu kSegRowCost: per member of N+(v), per CTA segment
+CTA_SEG_ITEMS = 512
+
+
+def degree_rank_dag(offsets: np.ndarray, nbrs: np.ndarray):
+    """(deg,id)-oriented DAG in rank space from a symmetric CSR: returns
+    (off, col, src, order) with rows = ranks and N+(r) ascending (graph.cuh)."""
+    n = offsets.size - 1
+    deg = np.diff(offsets).astype(np.int64)
+    order = np.lexsort((np.arange(n), deg))          # rank -> id, by (deg, id)
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    u = np.repeat(np.arange(n, dtype=np.int64), deg)
+    v = nbrs.astype(np.int64)
+    ru, rv = rank[u], rank[v]
+    keep = ru < rv
+    src, col = ru[keep], rv[keep]
+    idx = np.lexsort((col, src))
+    src, col = src[idx], col[idx]
+    off = np.zeros(n + 1, np.int64)
+    np.add.at(off, src + 1, 1)
+    off = np.cumsum(off)
+    return off, col, src, order
+
+
+def pivot_cost(off: np.ndarray, col: np.ndarray, src: np.ndarray) -> np.ndarray:
+    """Per pivot v: J_v (sum of its in-edges' suffix lengths) + ITEM_COST per
+    in-edge + SEG_COST * d+(v) per CTA segment; 0 without work."""
+    n = off.size - 1
+    e = np.arange(col.size, dtype=np.int64)
+    suffix = off[src + 1] - e - 1
+    jv = np.zeros(n, np.int64)
+    np.add.at(jv, col, suffix)
+    din = np.bincount(col, minlength=n).astype(np.int64)
+    dv = np.diff(off)
+    segs = (din + CTA_SEG_ITEMS - 1) // CTA_SEG_ITEMS
+    cost = jv + ITEM_COST * din + SEG_COST * dv * segs
+    return np.where((dv > 0) & (din > 0), cost, 0)
+
+
+def partition_bounds(cost: np.ndarray, parts: int) -> np.ndarray:
+    """Pivot rank bounds: b[0]=0, b[P]=n, b[p] = first r with
+    exclusive-prefix(cost)[r] >= total*p/P (double rounding as on the device)."""
+    n = cost.size
+    prefix = np.concatenate([[0], np.cumsum(cost)[:-1]]) if n else np.zeros(0, np.int64)
+    total = int(cost.sum())
+    b = np.zeros(parts + 1, np.int64)
+    b[parts] = n
+    for p in range(1, parts):
+        target = int(float(total) * p / parts)
+        b[p] = int(np.searchsorted(prefix, target, side="left"))
+    return b
+
+
+def count_part_host(off, col, src, v_lo: int, v_hi: int, n: int):
+    """Triangles whose middle vertex (pivot) has rank in [v_lo, v_hi), with
+    per-vertex counts in RANK space -- a slow host check for small graphs."""
+    total = 0
+    t = np.zeros(n, np.int64)
+    for e in np.nonzero((col >= v_lo) & (col < v_hi))[0]:
+        u, v = int(src[e]), int(col[e])
+        suffix = col[e + 1: off[u + 1]]
+        nv = col[off[v]: off[v + 1]]
+        common = np.intersect1d(suffix, nv, assume_unique=True)
+        c = common.size
+        if c:
+            total += c
+            t[u] += c
+            t[v] += c
+            t[common] += 1
+    return total, t

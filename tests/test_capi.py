@@ -24,7 +24,7 @@ def test_library_exports_header_symbols(tc):
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(tc.EXPORTED_SYMBOLS)
-    assert tc.abi_version() == 2
+    assert tc.abi_version() == 3
 
 
 def test_sm100a_only_binary(tc):

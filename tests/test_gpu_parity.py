@@ -210,15 +210,81 @@ def test_parts_sum_to_total(tc, oracle, cuda_ok, parts):
     assert oracle.fnv(pv) == c["pv_fnv"]
 
 
+@pytest.mark.parametrize("parts", [1, 3, 8])
+def test_count_multi_one_gpu(tc, oracle, cuda_ok, parts):
+    """tc_count_multi: P parts of the pivot split on device 0 --
+    counted back to back, summed, then the NCCL allreduce (a 1-rank
+    communicator here) -- against the reference goldens."""
+    c = load_golden("synthetic.json")["C1_rmat_s16_ef16"]
+    g = tc.build_graph_from_pairs(tc.generate(tc.GEN_RMAT, 16, 16), c["n"])
+    mg = tc.MultiGPU([0] * parts)
+    r = mg.count_triangles([g] * parts, tc.MatchOptions(per_vertex=True))
+    assert r.count == c["T"]
+    assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+    r2 = mg.count_triangles([g] * parts)
+    assert r2.count == c["T"] and r2.per_vertex is None
+    # device outputs
+    import torch
+    tot = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pv = torch.zeros(c["n"], dtype=torch.int64, device="cuda")
+    mg.count_triangles([g] * parts, tc.MatchOptions(per_vertex=True), total=tot, per_vertex=pv)
+    assert int(tot.item()) == c["T"]
+    assert oracle.fnv(pv.cpu().numpy().view(np.uint64)) == c["pv_fnv"]
+    mg.close()
+
+
+def test_comm_allreduce_single_rank(tc, oracle, cuda_ok):
+    """tc_comm_init_rank + tc_count_allreduce (one process per GPU) with a
+    1-rank group: the count path plus the NCCL allreduce on the count stream."""
+    c = load_golden("synthetic.json")["C2_er_s20_d32"]
+    g = tc.build_graph_from_pairs(tc.generate(tc.GEN_ER, 20, 32), c["n"])
+    comm = tc.Comm(tc.Comm.unique_id(), 1, 0, 0)
+    r = comm.count_triangles(g, tc.MatchOptions(per_vertex=True))
+    assert r.count == c["T"]
+    assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+    assert comm.count_triangles(g).count == c["T"]
+    comm.close()
+
+
+def test_multi_errors(tc, cuda_ok):
+    g1 = tc.build_graph_from_pairs(np.array([0, 1, 1, 2, 2, 0], np.uint32), 3)
+    g2 = tc.build_graph_from_pairs(np.array([0, 1, 1, 2], np.uint32), 3)
+    mg = tc.MultiGPU([0, 0])
+    with pytest.raises(tc.InvalidArgument):
+        mg.count_triangles([g1, g2])  # not replicas
+    with pytest.raises(tc.InvalidArgument):
+        mg.count_triangles([g1])      # one graph per part
+    with pytest.raises(tc.InvalidArgument):
+        tc.Comm(b"x" * 12, 1, 0, 0)
+    mg.close()
+
+
+@pytest.mark.slow
+def test_c4_count_multi_8_parts(tc, oracle, cuda_ok):
+    syn = load_golden("synthetic.json")
+    c = syn["C4_rmat_s24_ef16"]
+    import torch
+    m = tc.gen_num_edges(tc.GEN_RMAT, 24, 16)
+    d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+    tc.generate(tc.GEN_RMAT, 24, 16, out=d)
+    g = tc.build_graph_from_pairs(d, c["n"], m=m)
+    del d
+    mg = tc.MultiGPU([0] * 8)
+    r = mg.count_triangles([g] * 8, tc.MatchOptions(per_vertex=True))
+    assert r.count == c["T"]
+    assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+    mg.close()
+
+
 def test_partition_bounds_match_host(tc, oracle, cuda_ok):
-    from paper_1909_02127_b200 import dist as tdist
+    import dist_ref
     pairs = tc.generate(tc.GEN_RMAT, 14, 16)
     g = tc.build_graph_from_pairs(pairs, 1 << 14)
     off, nb, E, _, _ = oracle.build_graph(pairs, 1 << 14)
-    roff, col, src, order = tdist.degree_rank_dag(off, nb)
-    cost = tdist.row_cost(roff)
+    roff, col, src, order = dist_ref.degree_rank_dag(off, nb)
+    cost = dist_ref.pivot_cost(roff, col, src)
     for P in (2, 3, 8):
-        assert tc.partition_bounds(g, P).tolist() == tdist.partition_bounds(cost, P, roff).tolist()
+        assert tc.partition_bounds(g, P).tolist() == dist_ref.partition_bounds(cost, P).tolist()
 
 
 SYN = ["C1_rmat_s16_ef16", "C2_er_s20_d32", "rmat_s18_ef16", "kron_s18_ef16", "rmat_s20_ef16"]
