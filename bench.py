@@ -39,7 +39,7 @@ CONFIGS = {
     "C2": ("er", 20, 32, False, "Erdos-Renyi G(n=2^20, avg degree 32) (configs[1])"),
     "C3": ("kron", 22, 16, False, "Graph500 Kronecker scale-22 edgefactor-16, permuted (configs[2])"),
     "C4": ("rmat", 24, 16, True, "RMAT scale-24 edgefactor-16 with per-vertex counts (configs[3])"),
-    "C5": ("rmat", 26, 32, True, "RMAT scale-26 edgefactor-32 (configs[4])"),
+    "C5": ("rmat", 26, 32, False, "RMAT scale-26 edgefactor-32, total count (configs[4])"),
 }
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 

@@ -98,7 +98,7 @@ typedef struct tc_count_stats {
   double frontier_ms;     /* level-1 frontier plan: pivot classes + work segments */
   double join_ms;         /* advance + fused join kernels + per-vertex row pass */
   double reduce_ms;       /* per-vertex gather + total                         */
-  uint64_t pivots;        /* vertices v with d+(v)>0 and >=1 useful in-edge   (work_counters) */
+  uint64_t pivots;        /* vertices v with d+(v)>0 and >=1 in-edge (seeds)   (work_counters) */
   uint64_t items;         /* in-edges (u->v) whose wedge suffix is non-empty  (work_counters) */
   uint64_t wedges;        /* J = candidate wedges probed = sum of suffix lengths (work_counters) */
   uint64_t segments;      /* reserved */

@@ -12,8 +12,12 @@
 //   parse_matrix_market io.hpp:34-35            parse_matrix_market[_file]
 //   write/read_csr_cache, is_csr_cache_file     same names (io.hpp:39-41)
 //   load_graph          io.hpp:45               load_graph
+//   PartialTable        matcher.hpp:35-58       PartialTable (listings: width 3)
+//   LevelStats/MatchStats matcher.hpp:60-82     LevelStats / MatchStats (same fields)
 //   MatchOptions/Result matcher.hpp:84-94       MatchOptions / MatchResult (+ per_vertex)
 //   count_triangles     matcher.hpp:128         count_triangles
+//   (multi-GPU)         --                      MultiGpu (tc_count_multi), Communicator
+//                                               (tc_count_allreduce)
 //
 // Errors map back to the exception types the reference throws:
 // TC_EINVAL -> std::invalid_argument, TC_ERANGE -> std::out_of_range,
@@ -31,6 +35,7 @@
 #include <istream>
 #include <iterator>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -93,9 +98,11 @@ struct BuildReport {
 };
 
 // Immutable undirected simple graph, resident on a B200 as the
-// (deg,id)-oriented CSR.  Copies share the device handle (the reference Graph
-// is safe for concurrent reads; so is this).  The symmetric CSR the accessors
-// expose is materialised on first use.
+// (deg,id)-oriented CSR + in-edge index.  Copies share the device handle; like
+// the reference Graph (graph.hpp:33-34) it may be used from several threads:
+// the library serialises calls on one handle (a per-handle lock around its
+// count scratch).  The symmetric CSR the accessors expose is materialised on
+// first use.
 class Graph {
  public:
   Graph() = default;
@@ -110,7 +117,10 @@ class Graph {
     detail::check(tc_graph_from_csr(row_offsets.data(), neighbors.data(), num_vertices, num_edges, device, &h));
     h_.reset(h, detail::GraphDeleter{});
     detail::check(tc_graph_get_info(h, &info_));
-    csr_ = std::make_shared<Csr>(Csr{std::move(row_offsets), std::move(neighbors)});
+    std::call_once(lazy_->once, [&] {
+      lazy_->csr.off = std::move(row_offsets);
+      lazy_->csr.nbrs = std::move(neighbors);
+    });
   }
 
   VertexId num_vertices() const { return info_.num_vertices; }
@@ -142,19 +152,22 @@ class Graph {
     std::vector<std::uint64_t> off;
     std::vector<VertexId> nbrs;
   };
+  struct Lazy {
+    std::once_flag once;
+    Csr csr;
+  };
   const Csr& csr() const {
-    if (!csr_) {
-      auto c = std::make_shared<Csr>();
-      c->off.resize(static_cast<std::size_t>(num_vertices()) + 1);
-      c->nbrs.resize(2 * num_edges());
-      detail::check(tc_graph_export_csr(h_.get(), c->off.data(), c->nbrs.data()));
-      csr_ = std::move(c);
-    }
-    return *csr_;
+    std::call_once(lazy_->once, [this] {
+      Csr& c = lazy_->csr;
+      c.off.resize(static_cast<std::size_t>(num_vertices()) + 1);
+      c.nbrs.resize(2 * num_edges());
+      detail::check(tc_graph_export_csr(h_.get(), c.off.data(), c.nbrs.data()));
+    });
+    return lazy_->csr;
   }
   std::shared_ptr<tc_graph> h_;
   tc_graph_info info_{};
-  mutable std::shared_ptr<Csr> csr_;
+  std::shared_ptr<Lazy> lazy_ = std::make_shared<Lazy>();
 };
 
 using DegreeArray = std::vector<std::uint32_t>;
@@ -253,57 +266,214 @@ struct ExecPolicy {
   unsigned workers = 0;  // accepted for source compatibility; the GPU ignores it
 };
 
-struct MatchOptions {
-  int lookahead = 2;  // validated (0..2); count-neutral on the GPU path
-  bool keep_listings = false;  // not supported on the GPU path (throws)
-  ExecPolicy exec{};
-  bool per_vertex = false;  // GPU extension: triangles per vertex
-  std::uint32_t part_index = 0, part_count = 1;  // multi-GPU split
+// matcher.hpp:35-58: fixed-width table of (partial) embeddings.  Here it holds
+// the keep_listings rows: width 3, level 3, one triangle per row, ids ascending.
+class PartialTable {
+ public:
+  explicit PartialTable(std::uint32_t width) : width_(width) {}
+
+  std::uint32_t width() const { return width_; }
+  std::uint32_t level() const { return level_; }
+  std::uint64_t num_rows() const { return width_ == 0 ? 0 : cells_.size() / width_; }
+
+  std::span<const VertexId> row(std::uint64_t r) const { return {cells_.data() + r * width_, width_}; }
+  std::span<const VertexId> row_prefix(std::uint64_t r) const { return {cells_.data() + r * width_, level_}; }
+
+  std::vector<VertexId>& cells() { return cells_; }
+  const std::vector<VertexId>& cells() const { return cells_; }
+  void set_level(std::uint32_t level) { level_ = level; }
+
+ private:
+  std::uint32_t width_;
+  std::uint32_t level_ = 0;
+  std::vector<VertexId> cells_;
+};
+
+// matcher.hpp:60-67 / :69-82.  On the GPU path (MatchOptions::level_stats):
+//   candidates = seed_rows = pivots (d+(v) > 0 with in-edges; the orientation
+//                replaces the 2-core peel, so peel_rounds = 0)
+//   levels[0]  = the level-1 rows (u, w): rows_in = seeds, edges_visited =
+//                |E| oriented edges, rows_out = in-edges with a non-empty suffix
+//   levels[1]  = the final level: rows_in = levels[0].rows_out,
+//                edges_visited = candidate wedges probed, rows_out = count
+//   filter_millis = the count plan, verify_millis = advance + join + reduce
+struct LevelStats {
+  std::uint64_t rows_in = 0;
+  std::uint64_t edges_visited = 0;
+  std::uint64_t rows_out = 0;
+  std::uint64_t rows_masked = 0;
+  std::uint64_t lookahead_pruned = 0;
+  double millis = 0.0;
 };
 
 struct MatchStats {
-  double filter_millis = 0.0;  // the oriented CSR is built at graph construction
-  double verify_millis = 0.0;  // device time of the count (advance + join + reduce)
+  double filter_millis = 0.0;
+  double verify_millis = 0.0;
   std::uint64_t candidates = 0;
-  std::uint64_t wedges = 0, items = 0;
+  std::uint32_t peel_rounds = 0;
+  std::uint64_t seed_rows = 0;
+  std::vector<LevelStats> levels;
+
   double total_millis() const { return filter_millis + verify_millis; }
+  std::uint64_t rows_at(std::uint32_t slots) const {
+    return slots <= 1 ? seed_rows : levels[slots - 2].rows_out;
+  }
+};
+
+struct MatchOptions {
+  int lookahead = 2;           // validated (0..2); count-neutral on the GPU path
+  bool keep_listings = false;  // listings from the GPU listing kernel (tc_list_triangles)
+  ExecPolicy exec{};
+  bool per_vertex = false;     // GPU extension: triangles per vertex
+  bool level_stats = true;     // GPU extension: fill stats.levels (one extra pass)
 };
 
 struct MatchResult {
   std::uint64_t count = 0;
-  std::optional<std::vector<std::uint64_t>> per_vertex;
-  // keep_listings: every triangle once, ids ascending (matcher.hpp:92 rows
-  // u < w < x); row order unspecified
-  std::optional<std::vector<std::array<VertexId, 3>>> listings;
+  std::optional<PartialTable> listings;  // keep_listings: rows u < w < x, order unspecified
   MatchStats stats;
+  std::optional<std::vector<std::uint64_t>> per_vertex;  // GPU extension
 };
 
-inline MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}) {
+namespace detail {
+inline tc_count_opts count_opts(const MatchOptions& opts) {
+  if (opts.lookahead < 0 || opts.lookahead > 2) throw std::invalid_argument("lookahead must be 0, 1, or 2");
   tc_count_opts o{};
   o.lookahead = opts.lookahead;
-  o.part_index = opts.part_index;
-  o.part_count = opts.part_count;
   o.sync = 1;
+  o.work_counters = opts.level_stats ? 1 : 0;
+  return o;
+}
+inline void fill_stats(MatchResult& r, const tc_count_stats& st, std::uint64_t num_edges, bool level_stats) {
+  r.stats.filter_millis = st.frontier_ms;
+  r.stats.verify_millis = st.join_ms + st.reduce_ms;
+  if (!level_stats) return;
+  r.stats.candidates = r.stats.seed_rows = st.pivots;
+  r.stats.peel_rounds = 0;
+  LevelStats l1, l2;
+  l1.rows_in = st.pivots;
+  l1.edges_visited = num_edges;
+  l1.rows_out = st.items;
+  l1.millis = st.frontier_ms;
+  l2.rows_in = st.items;
+  l2.edges_visited = st.wedges;
+  l2.rows_out = r.count;
+  l2.millis = st.join_ms;
+  r.stats.levels = {l1, l2};
+}
+inline PartialTable listings(tc_graph* h) {
+  std::uint64_t T = 0;
+  check(tc_list_triangles(h, nullptr, 0, &T));
+  PartialTable t(3);
+  t.cells().resize(3 * T);
+  std::uint64_t T2 = 0;
+  if (T) check(tc_list_triangles(h, t.cells().data(), T, &T2));
+  t.set_level(3);
+  return t;
+}
+}  // namespace detail
+
+inline MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}) {
+  tc_count_opts o = detail::count_opts(opts);
   MatchResult r;
   tc_count_stats st{};
   std::vector<std::uint64_t> pv;
   if (opts.per_vertex) pv.resize(g.num_vertices());
   detail::check(tc_count(g.handle(), &o, &r.count, opts.per_vertex ? pv.data() : nullptr, &st));
   if (opts.per_vertex) r.per_vertex = std::move(pv);
-  r.stats.verify_millis = st.total_ms;
-  r.stats.wedges = st.wedges;
-  r.stats.items = st.items;
-  r.stats.candidates = st.pivots;
-  if (opts.keep_listings) {
-    std::uint64_t T = 0;
-    detail::check(tc_list_triangles(g.handle(), nullptr, 0, &T));
-    std::vector<std::array<VertexId, 3>> rows(T);
-    std::uint64_t T2 = 0;
-    if (T) detail::check(tc_list_triangles(g.handle(), reinterpret_cast<VertexId*>(rows.data()), T, &T2));
-    r.listings = std::move(rows);
-  }
+  detail::fill_stats(r, st, g.num_edges(), opts.level_stats);
+  if (opts.keep_listings) r.listings = detail::listings(g.handle());
   return r;
 }
+
+// ---- multi-GPU (tcb200.h tc_multi_* / tc_comm_*) --------------------------------
+
+// One process driving several B200s: part p of the degree-weighted pivot
+// split runs on devices[p] against its replica; ONE NCCL allreduce combines
+// the parts.  A device may repeat (its parts run back to back).
+class MultiGpu {
+ public:
+  explicit MultiGpu(std::vector<int> devices) : devices_(std::move(devices)) {
+    tc_multi* m = nullptr;
+    detail::check(tc_multi_create(devices_.data(), static_cast<int>(devices_.size()), &m));
+    m_.reset(m, [](tc_multi* x) { tc_multi_destroy(x); });
+  }
+  const std::vector<int>& devices() const { return devices_; }
+
+  // One replica per distinct device, built from the same edge list.
+  std::vector<Graph> build_replicas(const EdgeList& edges, BuildReport* report = nullptr) const {
+    std::vector<Graph> out;
+    std::vector<int> seen;
+    for (int d : devices_) {
+      if (std::find(seen.begin(), seen.end(), d) != seen.end()) continue;
+      seen.push_back(d);
+      out.push_back(build_graph(edges, report, d));
+    }
+    return out;
+  }
+
+  // replicas: one Graph per distinct device (any order); parts are mapped to
+  // the replica on their device.
+  MatchResult count_triangles(const std::vector<Graph>& replicas, const MatchOptions& opts = {}) const {
+    std::vector<tc_graph*> hs;
+    for (int d : devices_) {
+      tc_graph* h = nullptr;
+      for (const Graph& g : replicas)
+        if (g.info().device == d) h = g.handle();
+      if (!h) throw std::invalid_argument("MultiGpu: no replica on device " + std::to_string(d));
+      hs.push_back(h);
+    }
+    tc_count_opts o = detail::count_opts(opts);
+    o.work_counters = 0;
+    MatchResult r;
+    tc_count_stats st{};
+    std::vector<std::uint64_t> pv;
+    if (opts.per_vertex) pv.resize(replicas.at(0).num_vertices());
+    detail::check(tc_count_multi(m_.get(), hs.data(), &o, &r.count, opts.per_vertex ? pv.data() : nullptr, &st));
+    if (opts.per_vertex) r.per_vertex = std::move(pv);
+    detail::fill_stats(r, st, replicas.at(0).num_edges(), false);
+    if (opts.keep_listings) r.listings = detail::listings(hs[0]);
+    return r;
+  }
+
+ private:
+  std::vector<int> devices_;
+  std::shared_ptr<tc_multi> m_;
+};
+
+// One rank of a one-process-per-GPU group; the 128-byte id travels through
+// the host framework (MPI, a TCP store, ...): rank 0 calls unique_id().
+class Communicator {
+ public:
+  using Id = std::array<unsigned char, TC_COMM_ID_BYTES>;
+  static Id unique_id() {
+    Id id{};
+    detail::check(tc_comm_unique_id(id.data()));
+    return id;
+  }
+  Communicator(const Id& id, int nranks, int rank, int device) {
+    tc_comm* c = nullptr;
+    detail::check(tc_comm_init_rank(id.data(), nranks, rank, device, &c));
+    c_.reset(c, [](tc_comm* x) { tc_comm_destroy(x); });
+  }
+  // This rank's share + the allreduce: every rank gets the whole result.
+  MatchResult count_triangles(const Graph& g, const MatchOptions& opts = {}) const {
+    tc_count_opts o = detail::count_opts(opts);
+    o.work_counters = 0;
+    MatchResult r;
+    tc_count_stats st{};
+    std::vector<std::uint64_t> pv;
+    if (opts.per_vertex) pv.resize(g.num_vertices());
+    detail::check(tc_count_allreduce(c_.get(), g.handle(), &o, &r.count, opts.per_vertex ? pv.data() : nullptr, &st));
+    if (opts.per_vertex) r.per_vertex = std::move(pv);
+    detail::fill_stats(r, st, g.num_edges(), false);
+    if (opts.keep_listings) r.listings = detail::listings(g.handle());
+    return r;
+  }
+
+ private:
+  std::shared_ptr<tc_comm> c_;
+};
 
 // Streamed listings: calls sink(const std::array<VertexId, 3>* rows, size_t k)
 // with chunks of at most max_rows triangles whose union is the full listing,

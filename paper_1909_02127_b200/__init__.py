@@ -410,6 +410,15 @@ def list_triangles(g: Graph, first_edge: int = 0, last_edge: Optional[int] = Non
     return rows[: T.value]
 
 
+def list_triangles_count(g: Graph, first_edge: int = 0, last_edge: Optional[int] = None) -> int:
+    """The number of triangles the listing kernel lists (capacity 0: nothing
+    is written) -- an independent count (listing.cu) of the same graph."""
+    last = g.num_edges() if last_edge is None else last_edge
+    T = C.c_uint64()
+    _check(_lib.tc_list_triangles_range(g.handle, first_edge, last, None, 0, C.byref(T)))
+    return int(T.value)
+
+
 def iter_listings(g: Graph, max_rows: int = 1 << 22, out=None):
     """Streamed listings: yields (k, 3) u32 arrays of at most max_rows rows
     whose concatenation is list_triangles(g), walking the oriented edges range

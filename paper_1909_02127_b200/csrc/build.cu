@@ -946,17 +946,30 @@ __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* _
   }
 }
 
-__global__ void k_rowdesc(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, uint32_t n,
-                          uint4* __restrict__ rowd) {
-  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x)
-    rowd[u] = make_uint4(off[u], off[u + 1], offH[u], offH[u + 1]);
+__global__ void k_rowdesc(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, uint32_t r0,
+                          uint32_t n, uint4* __restrict__ rowd) {
+  for (uint64_t u = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    rowd[u - r0] = make_uint4(off[u], off[u + 1], offH[u], offH[u + 1]);
+}
+
+// First rank with deg > 0 (degrees ascend with rank): the isolated vertices
+// are ranks [0, r0).
+__global__ void k_first_nonisolated(const uint32_t* __restrict__ deg, uint32_t n, uint32_t* __restrict__ r0) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t m = lo + (hi - lo) / 2;
+    if (deg[m] < 1) lo = m + 1; else hi = m;
+  }
+  *r0 = lo;
 }
 
 // Plan capacities: work segments per pivot class (per-vertex superset: d+ = 0
 // pivots in the warp bin) and the per-vertex mask bytes of all rows.
-__global__ void k_plan_caps(PivotClass pc, uint32_t n, unsigned long long* __restrict__ tot) {
+__global__ void k_plan_caps(PivotClass pc, uint32_t r0, uint32_t n, unsigned long long* __restrict__ tot) {
   unsigned long long t[4] = {0, 0, 0, 0};
-  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t v = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t din = 0;
     const int c = pc((uint32_t)v, din);
     if (c >= 0) {
@@ -1032,16 +1045,24 @@ void finish_graph(tc_graph& g) {
     k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.ine.get());
     TC_LAUNCH();
   }
-  g.rowd.alloc(n ? n : 1, s);
+  g.r0 = 0;
   if (n) {
-    k_rowdesc<<<grid_gs(n, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), n, g.rowd.get());
+    DBuf<uint32_t> r0(1, s);
+    k_first_nonisolated<<<1, 1, 0, s>>>(g.deg.get(), n, r0.get());
+    TC_LAUNCH();
+    g.r0 = read_scalar(r0.get(), s);
+  }
+  const uint32_t nr = n - g.r0;
+  g.rowd.alloc(nr ? nr : 1, s);
+  if (nr) {
+    k_rowdesc<<<grid_gs(nr, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.r0, n, g.rowd.get());
     TC_LAUNCH();
   }
   DBuf<unsigned long long> tot(4, s);
   TC_CUDA(cudaMemsetAsync(tot.get(), 0, 4 * sizeof(unsigned long long), s));
-  if (n) {
-    k_plan_caps<<<grid_gs(n, dev), kT, 0, s>>>(PivotClass{g.off.get(), g.offH.get(), g.inoff.get(), true}, n,
-                                              tot.get());
+  if (nr) {
+    k_plan_caps<<<grid_gs(nr, dev), kT, 0, s>>>(PivotClass{g.off.get(), g.offH.get(), g.inoff.get(), true}, g.r0,
+                                               n, tot.get());
     TC_LAUNCH();
   }
   unsigned long long h[4];

@@ -135,6 +135,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
+// Ampere-style per-thread async copy (LDGSTS), 8 bytes, L1-bypassing.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
   uint32_t done = 0;

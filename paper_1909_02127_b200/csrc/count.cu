@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "graph.cuh"
@@ -96,7 +97,8 @@ constexpr uint64_t kItemCost = TCB_ITEM_COST;
 constexpr uint64_t kSegRowCost = TCB_SEG_COST;  // per member of N+(v), per segment
 
 __global__ void k_pivot_wedges(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                               const uint32_t* __restrict__ src, uint64_t E, unsigned long long* __restrict__ jv) {
+                               const uint32_t* __restrict__ src, uint64_t E, uint32_t r0,
+                               unsigned long long* __restrict__ jv) {
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = base + threadIdx.x;
     const bool ok = e < E;
@@ -105,24 +107,26 @@ __global__ void k_pivot_wedges(const uint32_t* __restrict__ off, const uint32_t*
     const uint32_t w = ok ? off[src[e] + 1] - (uint32_t)e - 1 : 0u;
     const unsigned peers = __match_any_sync(0xffffffffu, v);
     const uint32_t sum = __reduce_add_sync(peers, w);
-    if (ok && (int)lane_id() == __ffs(peers) - 1 && sum) atomicAdd(&jv[v], (unsigned long long)sum);
+    if (ok && (int)lane_id() == __ffs(peers) - 1 && sum) atomicAdd(&jv[v - r0], (unsigned long long)sum);
   }
 }
 
-struct PivotCost {
+struct PivotCost {  // pivots r0 + i (the isolated ranks [0, r0) have no work)
   const uint32_t* off;
   const uint32_t* inoff;
   const unsigned long long* jv;
   uint64_t item_cost, seg_cost;
-  __device__ __forceinline__ uint64_t operator()(uint64_t v) const {
+  uint32_t r0;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    const uint64_t v = r0 + i;
     const uint64_t dv = off[v + 1] - off[v], din = inoff[v + 1] - inoff[v];
     if (!dv || !din) return 0;
-    return jv[v] + item_cost * din + seg_cost * dv * ((din + kCtaSegItems - 1) / kCtaSegItems);
+    return jv[i] + item_cost * din + seg_cost * dv * ((din + kCtaSegItems - 1) / kCtaSegItems);
   }
 };
 
-__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint32_t n, uint64_t total, uint32_t parts,
-                              uint64_t* __restrict__ bounds) {
+__global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint32_t r0, uint32_t n, uint64_t total,
+                              uint32_t parts, uint64_t* __restrict__ bounds) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > parts) return;
   if (p == 0 || p == parts) {
@@ -130,12 +134,12 @@ __global__ void k_part_bounds(const uint64_t* __restrict__ prefix, uint32_t n, u
     return;
   }
   const uint64_t target = (uint64_t)((double)total * p / parts);
-  uint64_t lo = 0, hi = n;  // first pivot r with prefix[r] >= target
+  uint64_t lo = 0, hi = n - r0;  // first pivot r0 + i with prefix[i] >= target
   while (lo < hi) {
     const uint64_t mid = (lo + hi) / 2;
     if (prefix[mid] < target) lo = mid + 1; else hi = mid;
   }
-  bounds[p] = lo;
+  bounds[p] = r0 + lo;
 }
 
 // ---- membership structures -------------------------------------------------
@@ -324,12 +328,44 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 // (16-bit colH, the row's sorted suffix >= h0) and the cold part (col):
 // {hb, he, cb, ce}; all-zero = empty suffix.  mo = the item's first per-vertex
 // mask byte (rowbase[u] + RowMasks::P(k), k = e - off[u]).
+#ifndef TCB_ROWD
+#define TCB_ROWD 1  // item row geometry from tc_graph::rowd (one 16-byte load) or from off/offH
+#endif
+// CTA bin, staging of the next segment's in-edge records one segment ahead:
+// 0 = none (plain loads at staging), 1 = one bulk copy (TMA, cp.async.bulk +
+// mbarrier) per segment, 2 = per-thread cp.async (LDGSTS) of the records each
+// thread stages.  Measured at C4 (profiles/README.md): the total-only join
+// gains ~1% with 2; in the per-vertex join the 4 KB record buffer lifts the
+// CTA past the SMEM budget of 6 resident CTAs at the driver's 80% carveout
+// and costs 24% (47.7 vs 38.5 ms), so the per-vertex instantiation stages
+// with plain loads (kPrefetch below).
+#ifndef TCB_PREFETCH
+#define TCB_PREFETCH 2
+#endif
+// Per-vertex hits t[x] of the CTA / small bins: 1 = 8-bit hit masks per hot
+// chunk folded row by row (k_pv_rows); 0 = per-hit increments of SMEM
+// counters for the top ranks (16-bit halves, flushed every kTopFlushSegs
+// segments) and global atomics below them -- no masks, no row pass.
+#ifndef TCB_PV_MASKS
+#define TCB_PV_MASKS 1
+#endif
+constexpr uint32_t kTopFlushSegs = 120;  // <= 65535 / kCtaSegItems increments per counter between flushes
 struct ItemGeo {
-  const uint4* rowd;  // tc_graph::rowd: {off[u], off[u+1], offH[u], offH[u+1]}
-  const uint64_t* rowbase;
+  const uint32_t* off;
+  const uint32_t* offH;
+  const uint4* rowd;  // tc_graph::rowd, rows [r0, n)
+  const uint64_t* rowbase;  // rows [r0, n)
+  uint32_t r0;
+  __device__ __forceinline__ uint4 row(uint32_t u) const {
+#if TCB_ROWD
+    return rowd[u - r0];
+#else
+    return make_uint4(off[u], off[u + 1], offH[u], offH[u + 1]);
+#endif
+  }
   __device__ __forceinline__ uint4 hotcold(uint2 eu, uint64_t* mo) const {
     const uint32_t e = eu.x, u = eu.y;
-    const uint4 rd = rowd[u];  // one 16-byte load (one sector) per item
+    const uint4 rd = row(u);
     const uint32_t end = rd.y;
     const uint32_t O = rd.z, h = rd.w - rd.z;
     if (e + 1 >= end) return make_uint4(0, 0, 0, 0);
@@ -338,7 +374,7 @@ struct ItemGeo {
                                          : make_uint4(O, O + h, e + 1, cold_end);
     if (mo != nullptr && it.y > it.x) {
       const uint32_t beg = rd.x;
-      *mo = rowbase[u] + RowMasks(end - beg, O, h).P(e - beg);
+      *mo = rowbase[u - r0] + RowMasks(end - beg, O, h).P(e - beg);
     }
     return it;
   }
@@ -357,8 +393,8 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ in
                                                     const uint32_t* __restrict__ offH,
                                                     const uint32_t* __restrict__ col, const uint32_t* tab,
                                                     uint32_t mask, uint32_t shift, bool probe, const Sink& sink,
-                                                    const uint64_t* __restrict__ rowbase, uint8_t* __restrict__ masks,
-                                                    uint32_t* item_cnt) {
+                                                    const uint64_t* __restrict__ rowbase, uint32_t r0,
+                                                    uint8_t* __restrict__ masks, uint32_t* item_cnt) {
   const unsigned lane = lane_id();
   const uint4* col4 = reinterpret_cast<const uint4*>(col);
   uint32_t hits = 0;
@@ -373,12 +409,12 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ in
         b = eu.x + 1;
         e = end;
         nch = ((e + 3) >> 2) - (b >> 2);
-        if (kPerVertex) {
+        if (kPerVertex && TCB_PV_MASKS) {
           const uint32_t O = offH[u], h = offH[u + 1] - O;
           if (h > 0) {
             const RowMasks rm(end - beg, O, h);
             const uint32_t k = eu.x - beg;
-            uint8_t* z = masks + rowbase[u] + rm.P(k);
+            uint8_t* z = masks + rowbase[u - r0] + rm.P(k);
             const uint32_t nb = (uint32_t)(rm.c_hi - rm.first_chunk(k));
             for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
           }
@@ -434,7 +470,7 @@ template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, const uint32_t* __restrict__ col,
     const uint2* __restrict__ ine, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
-    uint32_t rc, uint32_t ncnt, const uint64_t* __restrict__ rowbase, uint8_t* __restrict__ masks,
+    uint32_t rc, uint32_t ncnt, const uint64_t* __restrict__ rowbase, uint32_t r0, uint8_t* __restrict__ masks,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
   __shared__ uint32_t s_tab[kJoinWarps][kWarpTable];
@@ -459,7 +495,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
     const uint32_t h = warp_join_small<kPerVertex>(ine, sg.y, sg.z, off, offH, col, tab, mask, shift, dv > 0, sink,
-                                                   rowbase, masks, s_item[warp]);
+                                                   rowbase, r0, masks, s_item[warp]);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
@@ -492,16 +528,22 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 // Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots].
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ offH,
+    const uint4* __restrict__ rowd, uint32_t r0,
     const uint16_t* __restrict__ colH, const uint2* __restrict__ ine, const uint64_t* __restrict__ rowbase,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
     uint32_t h0, uint32_t nbm, uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab,
-    uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
+    uint8_t* __restrict__ masks, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
+    unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t dyn[];
-  __shared__ unsigned long long s_hmo[kPerVertex ? kCtaSegItems : 1];  // hot items' mask offsets
+  constexpr bool kMasks = kPerVertex && TCB_PV_MASKS;
+  constexpr bool kHits = kPerVertex && !TCB_PV_MASKS;
+  constexpr int kPF = kPerVertex ? 0 : TCB_PREFETCH;  // staging prefetch (see TCB_PREFETCH)
+  __shared__ unsigned long long s_hmo[kMasks ? kCtaSegItems : 1];  // hot items' mask offsets
+  __shared__ uint16_t s_hidx[kHits ? kCtaSegItems : 1];  // hot item -> segment index (t[u] counts)
   __shared__ uint32_t s_hb[kCtaSegItems], s_he[kCtaSegItems], s_hpre[kCtaSegItems + 1];
   __shared__ uint32_t s_cb[kCtaSegItems], s_ce[kCtaSegItems], s_cpre[kCtaSegItems + 1];
-  __shared__ uint16_t s_hidx[kCtaSegItems], s_cidx[kCtaSegItems];
+  __shared__ uint16_t s_cidx[kPerVertex ? kCtaSegItems : 1];  // cold item -> segment index (t[u] counts)
   __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
   __shared__ uint32_t s_hits, s_cold, s_nl;
   __shared__ uint32_t s_wl[kJoinWarps];
@@ -509,22 +551,28 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   __shared__ uint32_t s_desc[6];  // current segment: v, i0, ni, off[v], d+(v), queue index
   __shared__ unsigned long long s_ctot;
   // the segment's in-edge records {e, u}, bulk-copied (TMA) one segment ahead
-  __shared__ __align__(16) uint2 s_ine[kCtaSegItems + 2];
+  __shared__ __align__(16) uint2 s_ine[kPF ? kCtaSegItems + 2 : 1];
   __shared__ __align__(8) unsigned long long s_mbar;
   __shared__ uint4 s_sgn;  // the next segment, held by thread 0
   uint32_t* bm = dyn;
   uint32_t* stab = dyn + nbm;
+  uint32_t* top = stab + kCtaSmemSlots;  // kHits: ncnt 16-bit counters for ranks [rc, rc + ncnt)
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  const ItemGeo geo{rowd, rowbase};
+  const ItemGeo geo{off, offH, rowd, rowbase, r0};
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
   if (kPerVertex)
     for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kJoinThreads) s_icnt[i] = 0;
+  if (kHits)
+    for (uint32_t i = threadIdx.x; i < ncnt / 2; i += kJoinThreads) top[i] = 0;
   // cold hits (x < h0) go straight to global atomics; hot hits leave as masks
+  // (kMasks) or go to the top counters / global atomics (kHits)
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, g_pv_dbg};
+  const PvSink<true> hsink{top, rc, t_rank, g_pv_dbg};
+  uint32_t segs_since_flush = 0;
   unsigned long long acc = 0;
   // Segments are pipelined one ahead by thread 0: the next segment is taken
   // from the queue at the top of the current one, and once the current
@@ -555,9 +603,20 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     const uint32_t q = atomicAdd(queue, 1u);
     if (q < nsegs) {
       s_sgn = segs[nsegs - 1 - q];  // heaviest (top ranks) first
-      issue_ine(s_sgn);
+      if constexpr (kPF == 1) issue_ine(s_sgn);
     }
     load_desc(q, s_sgn);
+  }
+  if constexpr (kPF == 2) {
+    __syncthreads();
+    if (s_desc[5] < nsegs) {
+#pragma unroll
+      for (int r = 0; r < kCtaSegItems / kJoinThreads; ++r) {
+        const uint32_t i = threadIdx.x * (kCtaSegItems / kJoinThreads) + r;
+        if (i < s_desc[2]) cp_async8(&s_ine[i], ine + s_desc[1] + i);
+      }
+    }
+    cp_async_commit();
   }
   while (true) {
     if (threadIdx.x == 0) {
@@ -589,8 +648,12 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     uint4 it[kIPT];
     uint64_t mo[kIPT];
     uint32_t nh[kIPT], nc[kIPT];
-    mbar_wait(&s_mbar, phase);  // this segment's in-edge records have landed
-    phase ^= 1u;
+    if constexpr (kPF == 1) {
+      mbar_wait(&s_mbar, phase);  // this segment's in-edge records have landed
+      phase ^= 1u;
+    } else if constexpr (kPF == 2) {
+      cp_async_wait_all();  // this thread's in-edge records (it copied them itself) have landed
+    }
 #pragma unroll
     for (int r = 0; r < kIPT; ++r) {
       const uint32_t i = threadIdx.x * kIPT + r;
@@ -598,7 +661,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       it[r] = make_uint4(0, 0, 0, 0);
       mo[r] = 0;
       if (i < ni) {
-        it[r] = geo.hotcold(s_ine[i + (i0 & 1u)], kPerVertex ? &mo[r] : nullptr);
+        const uint2 eu = kPF == 1 ? s_ine[i + (i0 & 1u)] : kPF == 2 ? s_ine[i] : ine[i0 + i];
+        it[r] = geo.hotcold(eu, kMasks ? &mo[r] : nullptr);
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -638,9 +702,22 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       }
       __syncthreads();
       // every thread is past its s_ine reads: start the next segment's copy
-      if (threadIdx.x == 0 && qnext < nsegs) {
-        fence_proxy_async_smem();
-        issue_ine(s_sgn);
+      if constexpr (kPF == 1) {
+        if (threadIdx.x == 0 && qnext < nsegs) {
+          fence_proxy_async_smem();
+          issue_ine(s_sgn);
+        }
+      } else if constexpr (kPF == 2) {
+        // each thread prefetches the next segment's records it will stage
+        // (LDGSTS into its own s_ine slots; s_sgn is stale when the queue is
+        // drained, and then never consumed)
+        const uint4 nx = s_sgn;
+#pragma unroll
+        for (int r = 0; r < kIPT; ++r) {
+          const uint32_t i = threadIdx.x * kIPT + r;
+          if (i < nx.z - nx.y) cp_async8(&s_ine[i], ine + nx.y + i);
+        }
+        cp_async_commit();
       }
       lp = il - lp + s_wl[warp];
       cp = ic - cp + s_wc[warp];
@@ -656,8 +733,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
           s_hb[ph] = it[r].x;
           s_he[ph] = it[r].y;
           s_hpre[ph] = ch;
-          if (kPerVertex) s_hmo[ph] = mo[r];
-          s_hidx[ph] = (uint16_t)i;
+          if (kMasks) s_hmo[ph] = mo[r];
+          if (kHits) s_hidx[ph] = (uint16_t)i;
           ++ph;
           ch += nh[r];
         }
@@ -665,7 +742,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
           s_cb[pc] = it[r].z;
           s_ce[pc] = it[r].w;
           s_cpre[pc] = cc;
-          s_cidx[pc] = (uint16_t)i;
+          if (kPerVertex) s_cidx[pc] = (uint16_t)i;
           ++pc;
           cc += nc[r];
         }
@@ -699,10 +776,16 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       // per-vertex: the hot chunk's 8-bit hit mask goes to HBM (one byte store,
       // coalesced across the lanes of an item); k_pv_rows turns the masks into
       // t[u] and t[x] row by row, with no per-hit atomics
-      h += warp_walk<8, kHotWin>(fb, fe, nhot, s_hpre, s_hb, s_he, s_hidx, nullptr, colH,
+      h += warp_walk<8, kHotWin>(fb, fe, nhot, s_hpre, s_hb, s_he, kHits ? s_hidx : nullptr,
+                                 kHits ? icnt : nullptr, colH,
                                  [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t k) {
                                    const uint32_t m = hot_hit_mask(qq, c, b, e, bm);
-                                   if (kPerVertex) masks[s_hmo[k] + (c - (b >> 3))] = (uint8_t)m;
+                                   if (kMasks) masks[s_hmo[k] + (c - (b >> 3))] = (uint8_t)m;
+                                   if (kHits && m) {
+#pragma unroll
+                                     for (int j = 0; j < 8; ++j)
+                                       if ((m >> j) & 1u) hsink.hit(h0 + hot_u16(qq, j));
+                                   }
                                    return (uint32_t)__popc(m);
                                  });
     }
@@ -750,9 +833,17 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     if (ts && tab == gtab) __threadfence_block();
     __syncthreads();  // everyone is done with s_desc of this segment
     if (threadIdx.x == 0) load_desc(qnext, s_sgn);
+    if (kHits && ++segs_since_flush == kTopFlushSegs) {  // before any 16-bit half could wrap
+      flush_top<true>(top, ncnt, rc, t_rank);
+      segs_since_flush = 0;
+    }
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
+  if (kHits) {
+    __syncthreads();
+    flush_top<true>(top, ncnt, rc, t_rank);
+  }
 }
 
 // ---- small CTA-bin pivots: one warp each -------------------------------------
@@ -799,17 +890,27 @@ struct SmallWarpSmem {
 
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kSmallThreads) k_join_small(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ offH,
+    const uint4* __restrict__ rowd, uint32_t r0,
     const uint16_t* __restrict__ colH, const uint2* __restrict__ ine, const uint64_t* __restrict__ rowbase,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
-    uint32_t h0, uint32_t nbm, uint8_t* __restrict__ masks, unsigned long long* __restrict__ t_rank,
-    unsigned long long* __restrict__ total) {
+    uint32_t h0, uint32_t nbm, uint8_t* __restrict__ masks, uint32_t rc, uint32_t ncnt,
+    unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ __align__(16) uint8_t dsm_small[];
+  constexpr bool kMasks = kPerVertex && TCB_PV_MASKS;
+  constexpr bool kHits = kPerVertex && !TCB_PV_MASKS;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  const ItemGeo geo{rowd, rowbase};
+  const ItemGeo geo{off, offH, rowd, rowbase, r0};
   const uint32_t wbytes = (SmallWarpSmem::bytes(nbm) + 15) & ~15u;
   SmallWarpSmem w(dsm_small + warp * wbytes, nbm);
+  // kHits: CTA-shared 32-bit counters for ranks [rc, rc + ncnt), after the warps' regions
+  uint32_t* top = reinterpret_cast<uint32_t*>(dsm_small + kSmallWarps * wbytes);
+  if (kHits) {
+    for (uint32_t i = threadIdx.x; i < ncnt; i += kSmallThreads) top[i] = 0;
+    __syncthreads();
+  }
+  const PvSink<false> hsink{top, rc, t_rank, 0};
   for (uint32_t i = lane; i < nbm; i += 32) w.bm[i] = 0;
   for (uint32_t i = lane; i < kSmallTable; i += 32) w.tab[i] = kEmpty;
   for (uint32_t i = lane; i < kSmallItems; i += 32) w.icnt[i] = 0;
@@ -866,7 +967,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
         w.he[ph] = it[r].y;
         w.hpre[ph] = ch;
         w.hidx[ph] = (uint16_t)i;
-        if (kPerVertex) w.hmo[ph] = mo[r];
+        if (kMasks) w.hmo[ph] = mo[r];
       }
       if (cf) {
         w.cb[pc] = it[r].z;
@@ -885,10 +986,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
     }
     __syncwarp();
     // (3) advance + join
-    uint32_t h = warp_walk<8, kHotWin>(0, th, nhot, w.hpre, w.hb, w.he, w.hidx, nullptr, colH,
+    uint32_t h = warp_walk<8, kHotWin>(0, th, nhot, w.hpre, w.hb, w.he, w.hidx, kHits ? w.icnt : nullptr, colH,
                                        [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t k) {
                                          const uint32_t m = hot_hit_mask(qq, c, b, e, w.bm);
-                                         if (kPerVertex) masks[w.hmo[k] + (c - (b >> 3))] = (uint8_t)m;
+                                         if (kMasks) masks[w.hmo[k] + (c - (b >> 3))] = (uint8_t)m;
+                                         if (kHits && m) {
+#pragma unroll
+                                           for (int j = 0; j < 8; ++j)
+                                             if ((m >> j) & 1u) hsink.hit(h0 + hot_u16(qq, j));
+                                         }
                                          return (uint32_t)__popc(m);
                                        });
     if (ncold)
@@ -917,6 +1023,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
   }
   acc = warp_sum(acc);
   if (lane == 0 && acc) atomicAdd(total, acc);
+  if (kHits) {
+    __syncthreads();
+    flush_top<false>(top, ncnt, rc, t_rank);
+  }
 }
 
 // Per-vertex counts from the CTA bin's hot hit masks.
@@ -1121,6 +1231,7 @@ struct PartRange {
   const uint32_t* col;
   uint32_t v_lo, v_hi;
   bool split;
+  uint32_t r0;  // rows [r0, n) (rowbase[u - r0])
   __device__ static __forceinline__ uint32_t lb(const uint32_t* a, uint32_t b, uint32_t e, uint32_t key) {
     while (b < e) {
       const uint32_t m = (b + e) >> 1;
@@ -1148,7 +1259,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
   init_spread(s_spread);
   __syncthreads();
   const unsigned lane = lane_id();
-  const uint32_t nrows = n;
+  const uint32_t nrows = n - pr.r0;
   const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
   while (true) {
     unsigned long long rb64 = 0;  // 64-bit queue: row counts may approach 2^32
@@ -1187,7 +1298,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       const RowMasks rm(__shfl_sync(0xffffffffu, dl, rj), __shfl_sync(0xffffffffu, Ol, rj),
                         __shfl_sync(0xffffffffu, hl, rj));
       const RowRel rr(rm);
-      const uint8_t* rowm = masks + rowbase[u];
+      const uint8_t* rowm = masks + rowbase[u - pr.r0];
       const RowLanes rl(rr.C, lane);
       uint32_t row_total = 0;
       for (uint32_t g = 0; g < rr.C; g += rl.w) {
@@ -1251,7 +1362,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     pr.items(beg, d, k_lo, k_hi);
     const RowMasks rm(d, O, offH[u + 1] - O);
     const RowRel rr(rm);
-    const uint8_t* rowm = masks + rowbase[u];
+    const uint8_t* rowm = masks + rowbase[u - pr.r0];
     const RowLanes rl(rr.C, lane);
     my_total = 0;
     for (uint32_t g = 0; g < rr.C; g += rl.w) {
@@ -1340,17 +1451,19 @@ const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
   g.part_bounds.assign((size_t)parts + 1, 0);
   g.part_bounds[parts] = n;
   if (g.E && parts > 1) {
-    DBuf<unsigned long long> jv(n, s);
-    DBuf<uint64_t> prefix(n, s), tot(1, s), bnd((uint64_t)parts + 1, s);
-    TC_CUDA(cudaMemsetAsync(jv.get(), 0, sizeof(unsigned long long) * n, s));
-    k_pivot_wedges<<<grid_gs(g.E, g.device), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), g.E, jv.get());
+    const uint32_t nr = n - g.r0;
+    DBuf<unsigned long long> jv(nr, s);
+    DBuf<uint64_t> prefix(nr, s), tot(1, s), bnd((uint64_t)parts + 1, s);
+    TC_CUDA(cudaMemsetAsync(jv.get(), 0, sizeof(unsigned long long) * nr, s));
+    k_pivot_wedges<<<grid_gs(g.E, g.device), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), g.E, g.r0,
+                                                          jv.get());
     TC_LAUNCH();
     const uint64_t item_cost = env_u32("TCB_ITEM_COST", (uint32_t)kItemCost);  // cost-model knobs
     const uint64_t seg_cost = env_u32("TCB_SEG_COST", (uint32_t)kSegRowCost);
-    scan_exclusive<uint64_t>(PivotCost{g.off.get(), g.inoff.get(), jv.get(), item_cost, seg_cost}, prefix.get(), n,
-                             tot.get(), s);
+    scan_exclusive<uint64_t>(PivotCost{g.off.get(), g.inoff.get(), jv.get(), item_cost, seg_cost, g.r0},
+                             prefix.get(), nr, tot.get(), s);
     const uint64_t total_cost = read_scalar(tot.get(), s);
-    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), n, total_cost, parts, bnd.get());
+    k_part_bounds<<<ceil_div(parts + 1, 128), 128, 0, s>>>(prefix.get(), g.r0, n, total_cost, parts, bnd.get());
     TC_LAUNCH();
     TC_CUDA(cudaMemcpyAsync(g.part_bounds.data(), bnd.get(), (parts + 1) * sizeof(uint64_t),
                             cudaMemcpyDeviceToHost, s));
@@ -1364,8 +1477,13 @@ namespace {
 template <typename K>
 int occupancy(K kern, int threads, size_t smem) {
   TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // TCB_CARVEOUT (percent of the unified L1/shared array as shared memory):
+  // a tuning knob; by default the driver picks the carveout
+  if (const char* c = getenv("TCB_CARVEOUT"))
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(c)));
   int occ = 0;
   TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (getenv("TCB_PHASES")) fprintf(stderr, "[tcb] occupancy %d blocks/SM (smem %zu + static)\n", occ, smem);
   return occ < 1 ? 1 : occ;
 }
 }  // namespace
@@ -1402,7 +1520,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   }
   const bool split = v_lo != 0 || v_hi != n;
   Plan plan;
-  kl += build_plan(g, v_lo, v_hi, pv, stats != nullptr && opts.work_counters != 0, plan);
+  constexpr bool kUseMasks = TCB_PV_MASKS;
+  kl += build_plan(g, v_lo, v_hi, pv, pv && kUseMasks, stats != nullptr && opts.work_counters != 0, plan);
   uint8_t* masks = plan.masks;
   pl.mark("plan");
   if (timing) TC_CUDA(cudaEventRecord(ev.e[1], s));
@@ -1430,19 +1549,24 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const int occ = occupancy(kern, kJoinThreads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(plan.cap[0], kJoinWarps), (uint64_t)sms * occ);
     kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.offH.get(), g.col.get(), g.ine.get(), plan.wsegs,
-                                         plan.nseg + 0, rc_w, ncnt_w, plan.rowbase, masks, t_rank, acc);
+                                         plan.nseg + 0, rc_w, ncnt_w, plan.rowbase, g.r0, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_warp");
   }
+  // per-hit top counters of the CTA / small bins (no-mask per-vertex mode)
+  const uint32_t ncnt_hits = (pv && !kUseMasks) ? std::min<uint32_t>(ncnt, env_u32("TCB_HIT_COUNTERS", 4096)) & ~1u : 0;
+  const uint32_t rc_hits = ncnt_hits ? n - ncnt_hits : 0xffffffffu;
   if (plan.cap[2]) {
-    const size_t ssm = (size_t)kSmallWarps * ((SmallWarpSmem::bytes(nbm) + 15) & ~15u);
+    const uint32_t ncnt_s = ncnt_hits / 2;  // 32-bit counters: half the window
+    const size_t ssm = (size_t)kSmallWarps * ((SmallWarpSmem::bytes(nbm) + 15) & ~15u) + (size_t)ncnt_s * 4;
     auto kern = pv ? k_join_small<true> : k_join_small<false>;
     const int occ = occupancy(kern, kSmallThreads, ssm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, ceil_div64(plan.cap[2], kSmallWarps));
-    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.colH.get(), g.ine.get(),
+    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.offH.get(), g.rowd.get(), g.r0, g.colH.get(),
+                                         g.ine.get(),
                                          plan.rowbase, plan.ssegs, plan.nseg + 2, queues + 0, g.h0, nbm, masks,
-                                         t_rank, acc);
+                                         ncnt_s ? n - ncnt_s : 0xffffffffu, ncnt_s, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_small");
@@ -1452,19 +1576,20 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     // than smem_slots/2 members below h0
     const uint32_t cap = table_size_for(g.max_dplus);
     const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
-    const size_t dsm = ((size_t)nbm + kCtaSmemSlots) * sizeof(uint32_t);
+    const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt_hits / 2) * sizeof(uint32_t);
     auto kern = pv ? k_join_cta<true> : k_join_cta<false>;
     const int occ = occupancy(kern, kJoinThreads, dsm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, plan.cap[1]);
     uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.colH.get(), g.ine.get(),
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.offH.get(), g.rowd.get(), g.r0, g.colH.get(),
+                                        g.ine.get(),
                                         plan.rowbase, plan.csegs, plan.nseg + 1, queues + 1, g.h0, nbm, smem_slots,
-                                        slab_cap, slab, masks, t_rank, acc);
+                                        slab_cap, slab, masks, rc_hits, ncnt_hits, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_cta");
   }
-  if (pv && n && g.mask_total) {
+  if (pv && kUseMasks && n && g.mask_total) {
     // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics); a split
     // count folds only the items of its own pivots
     unsigned int* rq = queues + 2;  // heavy queue, heavy count
@@ -1475,7 +1600,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
     const int rocc = occupancy(k_pv_rows, kRowWarps * 32, rsm);
     const int hocc = occupancy(k_pv_rows_heavy, kRowWarps * 32, rsm);
-    const PartRange pr{g.col.get(), v_lo, v_hi, split};
+    const PartRange pr{g.col.get(), v_lo, v_hi, split, g.r0};
     k_pv_rows<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
         g.off.get(), g.colH.get(), g.offH.get(), plan.rowbase, masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1,
         row_heavy_threshold(n), t_rank);

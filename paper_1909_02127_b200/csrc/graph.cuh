@@ -74,9 +74,12 @@ struct tc_graph {
   // count a plan over |V| instead of a scatter over |E| (plan.cu).
   tcb::DBuf<uint32_t> inoff;
   tcb::DBuf<uint2> ine;
-  // Row geometry interleaved per rank, {off[u], off[u+1], offH[u], offH[u+1]}:
-  // a join stages an item's suffix with one 16-byte load instead of four.
+  // Row geometry interleaved per rank, {off[u], off[u+1], offH[u], offH[u+1]}
+  // for the non-isolated ranks [r0, n) (isolated vertices have the lowest
+  // ranks and no work; a graph with huge declared n stays small): a join
+  // stages an item's suffix with one 16-byte load instead of four.
   tcb::DBuf<uint4> rowd;
+  uint32_t r0 = 0;
   // Count-plan capacities (graph properties, recorded once at build): work
   // segments per pivot class over the whole graph (any part has at most as
   // many) and the per-vertex mask bytes of all rows.
@@ -144,7 +147,7 @@ constexpr uint32_t kSmallCold = TCB_SMALL_COLD;    // power of two
 //                      per-vertex mask bytes must be zeroed)
 //   csegs  CTA bin    (kCtaSegItems items per segment)
 //   ssegs  small bin  (<= kSmallItems items, <= kSmallCold cold members)
-//   rowbase[u] = first mask byte of row u (per-vertex; all rows, RowMasks)
+//   rowbase[u - r0] = first mask byte of row u (per-vertex; rows [r0, n), RowMasks)
 struct Plan {
   uint4* wsegs = nullptr;
   uint4* csegs = nullptr;
@@ -158,7 +161,8 @@ struct Plan {
   void* sums = nullptr;
 };
 // Returns the number of kernels launched.
-int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool want_sums, Plan& p);
+// masks: per-vertex hit masks (rowbase + mask buffer, d+ = 0 pivots zeroed by the warp bin)
+int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool masks, bool want_sums, Plan& p);
 // The plan's work counters (W, J, hot, items, pivots) -- a read, only for stats.
 void read_plan_sums(Plan& p, cudaStream_t s);
 

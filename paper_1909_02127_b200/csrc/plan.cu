@@ -13,7 +13,7 @@
 //   two scans      segment offsets: warp|CTA packed in a u64, small in a u32
 //   k_plan_segs    segment lists; the list lengths go to device memory
 //   rowbase        per-vertex only: exclusive scan of each row's hit-mask
-//                  bytes (closed form, graph.cuh RowMasks), all rows
+//                  bytes (closed form, graph.cuh RowMasks), rows [r0, n)
 // No host synchronisation: list capacities are the graph's seg_cap.
 #include <cuda_runtime.h>
 
@@ -100,31 +100,31 @@ struct RowBytes {
   }
 };
 
-// Work counters of the part (stats only): per in-edge its suffix length (J)
-// and hot share, per pivot W = din * d+ (SURVEY 8d wedge stream).
-__global__ void k_plan_work(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH,
+// Work counters of the part (stats only): per in-edge of the part's pivots
+// its suffix length (J), hot share and usefulness (edge-parallel over the
+// in-edge index), per pivot W = din * d+ (SURVEY 8d wedge stream) and
+// whether it has work.
+__global__ void k_plan_work(const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0,
                             const uint32_t* __restrict__ inoff, const uint2* __restrict__ ine, uint32_t v_lo,
                             uint32_t v_hi, Sums* __restrict__ sums) {
   unsigned long long W = 0, J = 0, H = 0, I = 0, P = 0;
-  for (uint64_t v = v_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < v_hi;
-       v += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t dv = off[v + 1] - off[v];
-    const uint32_t a = inoff[v], b = inoff[v + 1];
-    if (!dv || a == b) continue;
-    W += (unsigned long long)dv * (b - a);
-    bool any = false;
-    for (uint32_t i = a; i < b; ++i) {
-      const uint2 eu = ine[i];
-      const uint32_t end = off[eu.y + 1];
-      if (eu.x + 1 >= end) continue;
-      any = true;
-      ++I;
-      const uint32_t O = offH[eu.y], h = offH[eu.y + 1] - O;
-      const uint32_t suf = end - eu.x - 1;
-      J += suf;
-      H += suf < h ? suf : h;
-    }
-    P += any;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t v = v_lo + t0; v < v_hi; v += stride) {
+    const uint32_t dv = off[v + 1] - off[v], din = inoff[v + 1] - inoff[v];
+    if (!dv || !din) continue;
+    W += (unsigned long long)dv * din;
+    ++P;
+  }
+  const uint32_t i_lo = inoff[v_lo], i_hi = inoff[v_hi];
+  for (uint64_t i = i_lo + t0; i < i_hi; i += stride) {
+    const uint2 eu = ine[i];
+    const uint4 rd = rowd[eu.y - r0];
+    if (eu.x + 1 >= rd.y) continue;
+    ++I;
+    const uint32_t suf = rd.y - eu.x - 1, h = rd.w - rd.z;
+    J += suf;
+    H += suf < h ? suf : h;
   }
   W = warp_sum(W);
   J = warp_sum(J);
@@ -142,12 +142,13 @@ __global__ void k_plan_work(const uint32_t* __restrict__ off, const uint32_t* __
 
 }  // namespace
 
-int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool want_sums, Plan& p) {
+int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool masks, bool want_sums, Plan& p) {
   cudaStream_t s = g.stream;
   const uint32_t n = g.n;
   const int dev = g.device;
   int kl = 0;
   PhaseLog pl(s);
+  v_lo = v_lo < g.r0 ? (g.r0 < v_hi ? g.r0 : v_hi) : v_lo;  // isolated ranks [0, r0) have no work
   p.v_lo = v_lo;
   p.v_hi = v_hi;
   const uint32_t np = v_hi - v_lo;
@@ -160,7 +161,8 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
     TC_CUDA(cudaMemsetAsync(p.nseg, 0, 4 * sizeof(uint32_t), s));
   } else {
     uint8_t* cls = g.scratch[kSlotCls].get<uint8_t>(np, s);
-    const PivotClass pc{g.off.get(), g.offH.get(), g.inoff.get(), per_vertex};
+    // d+(v) = 0 pivots join the warp bin only to zero their items' mask bytes
+    const PivotClass pc{g.off.get(), g.offH.get(), g.inoff.get(), masks};
     k_plan_class<<<grid_gs(np, dev), kT, 0, s>>>(pc, v_lo, v_hi, cls);
     TC_LAUNCH();
     ++kl;
@@ -179,9 +181,13 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
   pl.mark("plan_segs");
   p.rowbase = nullptr;
   p.masks = nullptr;
-  if (per_vertex && n) {
-    p.rowbase = g.scratch[kSlotRowBase].get<uint64_t>((uint64_t)n + 1, s);
-    kl += scan_exclusive<uint64_t>(RowBytes{g.off.get(), g.offH.get()}, p.rowbase, n, p.rowbase + n, s);
+  (void)per_vertex;
+  if (masks && n) {
+    // rows [r0, n): rowbase[u - r0]
+    const uint32_t nr = n - g.r0;
+    p.rowbase = g.scratch[kSlotRowBase].get<uint64_t>((uint64_t)nr + 1, s);
+    kl += scan_exclusive<uint64_t>(RowBytes{g.off.get() + g.r0, g.offH.get() + g.r0}, p.rowbase, nr,
+                                   p.rowbase + nr, s);
     p.masks = g.scratch[kSlotMasks].get<uint8_t>(g.mask_total + 32, s);
     pl.mark("plan_rowbase");
   }
@@ -190,8 +196,8 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
     Sums* sums = g.scratch[kSlotSums].get<Sums>(1, s);
     TC_CUDA(cudaMemsetAsync(sums, 0, sizeof(Sums), s));
     if (np) {
-      k_plan_work<<<grid_gs(np, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.inoff.get(), g.ine.get(), v_lo,
-                                                  v_hi, sums);
+      k_plan_work<<<(unsigned)num_sms(dev) * 8, kT, 0, s>>>(g.off.get(), g.rowd.get(), g.r0, g.inoff.get(), g.ine.get(),
+                                                           v_lo, v_hi, sums);
       TC_LAUNCH();
     }
     p.sums = sums;

@@ -130,6 +130,39 @@ int main(int argc, char** argv) {
       for (std::size_t i = 0; i < k; ++i) ascending += rows[i][0] < rows[i][1] && rows[i][1] < rows[i][2];
     }, 777);
     CHECK(listed == T && ascending == T);
+
+    // reference MatchStats / MatchResult shapes (matcher.hpp:35-94): levels,
+    // rows_at, listings as an optional<PartialTable>
+    tg::MatchOptions lo;
+    lo.keep_listings = true;
+    auto rl = tg::count_triangles(g, lo);
+    CHECK(rl.count == T);
+    CHECK(rl.listings.has_value() && rl.listings->width() == 3 && rl.listings->level() == 3);
+    CHECK(rl.listings->num_rows() == T);
+    std::uint64_t asc = 0;
+    for (std::uint64_t i = 0; i < rl.listings->num_rows(); ++i) {
+      auto row = rl.listings->row(i);
+      asc += row[0] < row[1] && row[1] < row[2] && g.has_edge(row[0], row[2]);
+    }
+    CHECK(asc == T);
+    CHECK(rl.stats.levels.size() == 2 && rl.stats.rows_at(3) == T);
+    CHECK(rl.stats.levels[1].rows_in == rl.stats.levels[0].rows_out);
+    CHECK(rl.stats.levels[1].edges_visited >= T && rl.stats.total_millis() > 0.0);
+    CHECK(rl.stats.seed_rows > 0 && rl.stats.candidates == rl.stats.seed_rows);
+
+    // multi-GPU through the C-ABI: 3 parts of the pivot split on device 0
+    // (one NCCL allreduce over a 1-rank communicator)
+    tg::MultiGpu mg({0, 0, 0});
+    std::vector<tg::Graph> reps = mg.build_replicas(el);
+    CHECK(reps.size() == 1);
+    tg::MatchOptions mp;
+    mp.per_vertex = true;
+    auto rm = mg.count_triangles(reps, mp);
+    auto r1 = tg::count_triangles(g, mp);
+    CHECK(rm.count == T && rm.per_vertex && *rm.per_vertex == *r1.per_vertex);
+    // one process per GPU, 1-rank group
+    tg::Communicator comm(tg::Communicator::unique_id(), 1, 0, 0);
+    CHECK(comm.count_triangles(g).count == T);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

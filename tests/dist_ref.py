@@ -51,18 +51,24 @@ def pivot_cost(off: np.ndarray, col: np.ndarray, src: np.ndarray) -> np.ndarray:
     return np.where((dv > 0) & (din > 0), cost, 0)
 
 
-def partition_bounds(cost: np.ndarray, parts: int) -> np.ndarray:
-    """Pivot rank bounds: b[0]=0, b[P]=n, b[p] = first r with
-    exclusive-prefix(cost)[r] >= total*p/P (double rounding as on the device)."""
+def partition_bounds(cost: np.ndarray, parts: int, r0: int = 0) -> np.ndarray:
+    """Pivot rank bounds: b[0]=0, b[P]=n, b[p] = r0 + first i with
+    exclusive-prefix(cost[r0:])[i] >= total*p/P (double rounding as on the
+    device); r0 = the number of isolated vertices (the lowest ranks)."""
     n = cost.size
-    prefix = np.concatenate([[0], np.cumsum(cost)[:-1]]) if n else np.zeros(0, np.int64)
-    total = int(cost.sum())
+    c = cost[r0:]
+    prefix = np.concatenate([[0], np.cumsum(c)[:-1]]) if c.size else np.zeros(0, np.int64)
+    total = int(c.sum())
     b = np.zeros(parts + 1, np.int64)
     b[parts] = n
     for p in range(1, parts):
         target = int(float(total) * p / parts)
-        b[p] = int(np.searchsorted(prefix, target, side="left"))
+        b[p] = r0 + int(np.searchsorted(prefix, target, side="left"))
     return b
+
+
+def isolated(offsets: np.ndarray) -> int:
+    return int(np.count_nonzero(np.diff(offsets) == 0))
 
 
 def count_part_host(off, col, src, v_lo: int, v_hi: int, n: int):

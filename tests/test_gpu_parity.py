@@ -284,7 +284,8 @@ def test_partition_bounds_match_host(tc, oracle, cuda_ok):
     roff, col, src, order = dist_ref.degree_rank_dag(off, nb)
     cost = dist_ref.pivot_cost(roff, col, src)
     for P in (2, 3, 8):
-        assert tc.partition_bounds(g, P).tolist() == dist_ref.partition_bounds(cost, P).tolist()
+        assert tc.partition_bounds(g, P).tolist() == \
+            dist_ref.partition_bounds(cost, P, dist_ref.isolated(off)).tolist()
 
 
 SYN = ["C1_rmat_s16_ef16", "C2_er_s20_d32", "rmat_s18_ef16", "kron_s18_ef16", "rmat_s20_ef16"]
@@ -681,3 +682,35 @@ def test_csr_route_empty_and_isolated(tc, cuda_ok):
     finally:
         os.environ.pop("TCB_FEED_CHUNK", None)
     assert r.count == 1 and r.per_vertex.tolist() == [0, 0, 1, 0, 0, 1, 0, 1, 0, 0]
+
+
+@pytest.mark.slow
+def test_c5_rmat_s26(tc, oracle, cuda_ok):
+    """BASELINE configs[4] (RMAT s26 ef32, 2.08e9 edges) on one GPU: build
+    report against SURVEY 8 / the big golden, the count against the
+    independent listing kernel (listing.cu: per-edge binary searches, no
+    in-edge index, no bitmap join) and, once generated, against the
+    tests/golden big-config checker (oracle/big_golden, T and per-vertex)."""
+    import torch
+    syn = load_golden("synthetic.json")
+    c = syn.get("C5_rmat_s26_ef32")
+    m = tc.gen_num_edges(tc.GEN_RMAT, 26, 32)
+    d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+    tc.generate(tc.GEN_RMAT, 26, 32, out=d)
+    rep = tc.BuildReport()
+    g = tc.build_graph_from_pairs(d, 1 << 26, rep, m=m)
+    del d
+    torch.cuda.empty_cache()
+    # SURVEY.md section 8 config table
+    assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == (2078632673, 8492, 68842483)
+    T = tc.count_triangles(g).count
+    assert tc.list_triangles_count(g) == T
+    if c is not None:
+        assert T == c["T"]
+        try:
+            r = tc.count_triangles(g, tc.MatchOptions(per_vertex=True))
+        except MemoryError:
+            pytest.skip("per-vertex masks of C5 do not fit next to the graph on this device")
+        assert r.count == T
+        assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
+        assert int(r.per_vertex.sum()) == 3 * T

@@ -112,3 +112,61 @@ def test_oracle_vs_reference_random(oracle, ref):
         T, pv = g.count_triangles(per_vertex=True)
         oT, opv = oracle.count(a[0], a[1], per_vertex=True)
         assert T == oT and np.array_equal(pv, opv)
+
+
+# ---- the degree-ordered DAG checker (oracle_count_dag): pinned before it is
+# trusted for the configs the id-order restatement cannot finish (C5) ----
+
+def test_dag_checker_known_and_gnp(oracle):
+    for name, c in load_golden("known.json").items():
+        if name.startswith("_") or c.get("skip_ref_csr"):
+            continue
+        off, nb, E, lo, du = oracle.build_graph(_pairs(c), c["n"])
+        T, pv = oracle.count_dag(off, nb, per_vertex=True)
+        assert T == c["T"] and pv.tolist() == c["per_vertex"], name
+    for i, c in enumerate(load_golden("gnp.json")):
+        off, nb, E, lo, du = oracle.build_graph(_pairs(c), c["n"])
+        T, pv = oracle.count_dag(off, nb, per_vertex=True)
+        assert T == c["T"] and pv.tolist() == c["per_vertex"], i
+
+
+@pytest.mark.parametrize("name", ["C1_rmat_s16_ef16", "kron_s18_ef16", "rmat_s18_ef16", "C2_er_s20_d32"])
+def test_dag_checker_synthetic_goldens(oracle, name):
+    """Against the reference's segmented_intersect goldens (T and per-vertex)."""
+    c = load_golden("synthetic.json")[name]
+    pairs = oracle.gen_er(c["scale"], c["edgefactor"]) if c["kind"] == "er" else \
+        oracle.gen_rmat(c["scale"], c["edgefactor"], c["permute"])
+    off, nb, E, lo, du = oracle.build_graph(pairs, c["n"])
+    T, pv = oracle.count_dag(off, nb, per_vertex=True)
+    assert T == c["T"]
+    assert oracle.fnv(pv) == c["pv_fnv"]
+
+
+def test_dag_checker_vs_reference_random(oracle, ref):
+    rng = np.random.default_rng(5)
+    for i in range(40):
+        n = int(rng.integers(1, 400))
+        m = int(rng.integers(0, 6 * n))
+        pairs = rng.integers(0, n, 2 * m).astype(np.uint32)
+        off, nb, E, _, _ = ref.build_graph(pairs, n)
+        T, pv = ref.graph(off, nb).count_triangles(per_vertex=True)
+        dT, dpv = oracle.count_dag(off, nb, per_vertex=True)
+        assert T == dT and np.array_equal(pv, dpv)
+
+
+def test_big_golden_driver_matches_c1(oracle):
+    """oracle/big_golden (the streamed build + checker used for C4 per-vertex
+    and C5) reproduces the C1 golden end to end."""
+    import json
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "big_golden")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/big_golden not built")
+    c = load_golden("synthetic.json")["C1_rmat_s16_ef16"]
+    for mode in ("dag", "oracle"):
+        out = json.loads(subprocess.run([exe, "rmat", "16", "16", mode], capture_output=True, text=True,
+                                        check=True).stdout)
+        for k in ("pairs_fnv", "E", "loops", "dups", "offsets_fnv", "nbrs_fnv", "T", "pv_fnv"):
+            assert out[k] == c[k], (mode, k)

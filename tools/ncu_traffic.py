@@ -5,7 +5,7 @@
 
 Reads dram__bytes_read.sum + dram__bytes_write.sum and gpu__time_duration.sum
 of every kernel in the report (per launch; the last launch of each kernel
-name wins) and writes profiles/ncu_traffic_<config>.json with the sha256 of
+name wins) and writes ncu_traffic_<config>.json next to the report (copy it to profiles/) with the sha256 of
 paper_1909_02127_b200/libtcb200.so.  bench.py reports `roofline.traffic` only
 when that hash matches the library it runs (otherwise traffic = null).
 """
@@ -48,7 +48,9 @@ def main():
     git = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
     doc = {"config": config, "lib_sha256": sha, "git_head": git or None, "report": os.path.basename(rep),
            "kernels": out}
-    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
+    # written next to the report (gpurun_out/ travels back); copy it into
+    # profiles/ to make bench.py use it
+    path = os.path.join(os.path.dirname(os.path.abspath(rep)), f"ncu_traffic_{config}.json")
     with open(path, "w") as f:
         json.dump(doc, f, indent=1)
     print(json.dumps(doc, indent=1))
