@@ -79,6 +79,8 @@ typedef struct tc_graph_info {
   uint32_t max_out_degree; /* max d+ in the (deg,id)-oriented DAG */
   int device;
   double build_ms;         /* device time of the last build/from_csr (CUDA events) */
+  uint32_t core_ranks;     /* dense core: the top core_ranks ranks (0 = no dense rows) */
+  uint32_t dense_rows;     /* rows whose core members are held as a core bitmap */
 } tc_graph_info;
 
 /* trimatch::MatchOptions (matcher.hpp:84-88) + GPU extensions. */

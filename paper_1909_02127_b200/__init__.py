@@ -53,7 +53,8 @@ class TcBuildReport(C.Structure):
 
 class TcGraphInfo(C.Structure):
     _fields_ = [("num_vertices", C.c_uint32), ("num_edges", C.c_uint64), ("max_degree", C.c_uint32),
-                ("max_out_degree", C.c_uint32), ("device", C.c_int), ("build_ms", C.c_double)]
+                ("max_out_degree", C.c_uint32), ("device", C.c_int), ("build_ms", C.c_double),
+                ("core_ranks", C.c_uint32), ("dense_rows", C.c_uint32)]
 
 
 class TcCountOpts(C.Structure):
@@ -278,6 +279,16 @@ class Graph:
     @property
     def max_out_degree(self) -> int:
         return self._info.max_out_degree
+
+    @property
+    def core_ranks(self) -> int:
+        """Dense core size (top ranks held as row bitmaps; 0 = none)."""
+        return self._info.core_ranks
+
+    @property
+    def dense_rows(self) -> int:
+        """Rows whose core members are intersected word-parallel."""
+        return self._info.dense_rows
 
     @property
     def build_ms(self) -> float:

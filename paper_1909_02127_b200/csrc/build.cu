@@ -946,11 +946,118 @@ __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* _
   }
 }
 
-__global__ void k_rowdesc(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, uint32_t r0,
-                          uint32_t n, uint4* __restrict__ rowd) {
+// ---- dense core (graph.cuh RowGeo) -------------------------------------------
+// Core members of row u: its hot suffix entries >= cb - h0 (colH is sorted
+// per row), found by binary search; the row is dense with >= core_min.
+// ccnt[u - r0] = core members if dense, else 0.
+__global__ void k_core_rows(const uint32_t* __restrict__ offH, const uint16_t* __restrict__ colH, uint32_t r0,
+                            uint32_t n, uint32_t cbh, uint32_t core_min, uint32_t* __restrict__ ccnt) {
   for (uint64_t u = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-       u += (uint64_t)gridDim.x * blockDim.x)
-    rowd[u - r0] = make_uint4(off[u], off[u + 1], offH[u], offH[u + 1]);
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = offH[u], hi = offH[u + 1];
+    const uint32_t end = hi;
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (colH[m] < cbh) lo = m + 1; else hi = m;
+    }
+    const uint32_t c = end - lo;
+    ccnt[u - r0] = (c >= core_min && c > 0) ? c : 0u;
+  }
+}
+
+struct DenseFlag {
+  const uint32_t* ccnt;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return ccnt[i] ? 1u : 0u; }
+};
+
+// Row descriptors (32 bytes per rank, graph.cuh RowGeo), without rowbase.
+__global__ void k_rowdesc(const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, uint32_t r0,
+                          uint32_t n, const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ dpos,
+                          uint4* __restrict__ rowd) {
+  for (uint64_t u = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = ccnt ? ccnt[u - r0] : 0u;
+    const uint32_t Hf = offH[u + 1];
+    rowd[2 * (u - r0)] = make_uint4(off[u], off[u + 1], offH[u], Hf - c);
+    rowd[2 * (u - r0) + 1] = make_uint4(Hf, c ? dpos[u - r0] : kNoDense, 0, 0);
+  }
+}
+
+// Mask bytes of row r0 + i (the sparse hot part, RowGeo::masks).
+struct RowBytesGeo {
+  const uint4* rowd;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    return RowGeo(rowd[2 * i], rowd[2 * i + 1]).masks().total();
+  }
+};
+__global__ void k_rowbase_put(const uint64_t* __restrict__ rb, uint32_t nr, uint4* __restrict__ rowd) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 b = rowd[2 * i + 1];
+    b.z = (uint32_t)rb[i];
+    b.w = (uint32_t)(rb[i] >> 32);
+    rowd[2 * i + 1] = b;
+  }
+}
+
+// Dense in-edge list: in-edge i = {e, u} of pivot v is a dense item when u's
+// row is dense and its suffix after v is non-empty.
+struct DenseIn {
+  const uint2* ine;
+  const uint4* rowd;
+  uint32_t r0;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+    const uint2 eu = ine[i];
+    const uint4* p = rowd + 2 * (uint64_t)(eu.y - r0);
+    return (p[1].y != kNoDense && eu.x + 1 < p[0].y) ? 1u : 0u;
+  }
+};
+__global__ void k_dense_scatter(const uint2* __restrict__ ine, uint64_t E, const uint4* __restrict__ rowd,
+                                uint32_t r0, const uint32_t* __restrict__ dpos, uint32_t* __restrict__ dine) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 eu = ine[i];
+    const uint4* p = rowd + 2 * (uint64_t)(eu.y - r0);
+    const uint32_t didx = p[1].y;
+    if (didx != kNoDense && eu.x + 1 < p[0].y) dine[dpos[i]] = didx;
+  }
+}
+// Dense segments of pivot v: its dense items [dpos[inoff[v]], dpos[inoff[v+1]])
+struct DenseSegs {
+  const uint32_t* inoff;
+  const uint32_t* dpos;
+  __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
+    const uint32_t c = dpos[inoff[v + 1]] - dpos[inoff[v]];
+    return (c + kDenseSeg - 1) / kDenseSeg;
+  }
+};
+__global__ void k_dense_segs(const uint32_t* __restrict__ inoff, const uint32_t* __restrict__ dpos, uint32_t n,
+                             const uint32_t* __restrict__ dsoff, uint4* __restrict__ dseg) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = dpos[inoff[v]], b = dpos[inoff[v + 1]];
+    uint32_t s = dsoff[v];
+    for (uint32_t i = a; i < b; i += kDenseSeg) dseg[s++] = make_uint4((uint32_t)v, i, min(i + kDenseSeg, b), 0);
+  }
+}
+__global__ void k_dense_rows(const uint4* __restrict__ rowd, uint32_t r0, uint32_t nr, uint32_t* __restrict__ drow) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t didx = rowd[2 * i + 1].y;
+    if (didx != kNoDense) drow[didx] = r0 + (uint32_t)i;
+  }
+}
+
+// Core bitmaps: one warp per dense row sets the bits of its core members.
+__global__ void k_core_fill(const uint4* __restrict__ rowd, uint32_t nr, const uint16_t* __restrict__ colH,
+                            uint32_t cbh, uint32_t words, uint32_t* __restrict__ cbits) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nr;
+       i += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const RowGeo r(rowd[2 * i], rowd[2 * i + 1]);
+    if (r.didx == kNoDense) continue;
+    uint32_t* bm = cbits + (uint64_t)r.didx * words;
+    for (uint32_t p = r.Ht + lane; p < r.Hf; p += 32) {
+      const uint32_t y = colH[p] - cbh;
+      atomicOr(&bm[y >> 5], 1u << (y & 31));
+    }
+  }
 }
 
 // First rank with deg > 0 (degrees ascend with rank): the isolated vertices
@@ -965,7 +1072,7 @@ __global__ void k_first_nonisolated(const uint32_t* __restrict__ deg, uint32_t n
 }
 
 // Plan capacities: work segments per pivot class (per-vertex superset: d+ = 0
-// pivots in the warp bin) and the per-vertex mask bytes of all rows.
+// pivots in the warp bin).
 __global__ void k_plan_caps(PivotClass pc, uint32_t r0, uint32_t n, unsigned long long* __restrict__ tot) {
   unsigned long long t[4] = {0, 0, 0, 0};
   for (uint64_t v = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
@@ -979,8 +1086,6 @@ __global__ void k_plan_caps(PivotClass pc, uint32_t r0, uint32_t n, unsigned lon
       t[1] += c == 1 ? ns : 0;
       t[2] += c == 2 ? ns : 0;
     }
-    const uint32_t O = pc.offH[v];
-    t[3] += RowMasks(pc.off[v + 1] - pc.off[v], O, pc.offH[v + 1] - O).total();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -1053,10 +1158,86 @@ void finish_graph(tc_graph& g) {
     g.r0 = read_scalar(r0.get(), s);
   }
   const uint32_t nr = n - g.r0;
-  g.rowd.alloc(nr ? nr : 1, s);
-  if (nr) {
-    k_rowdesc<<<grid_gs(nr, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.r0, n, g.rowd.get());
+  g.rowd.alloc(2 * (uint64_t)(nr ? nr : 1), s);
+  // dense core: rows with >= core_min members among the top core_bits ranks
+  // (TCB_CORE_BITS / TCB_CORE_MIN: tests shrink the core to drive the dense
+  // path on small graphs; TCB_CORE_BITS=0 disables it)
+  uint32_t core_bits = env_u32("TCB_CORE_BITS", kCoreBits) & ~31u;
+  if (core_bits > 32u * 32u * kCoreWordsMax) core_bits = 32u * 32u * kCoreWordsMax;
+  const uint32_t core_min = std::max<uint32_t>(1, env_u32("TCB_CORE_MIN", core_bits / 32));
+  g.cb = 0;
+  g.core_words = 0;
+  g.ndense = 0;
+  g.cbits.release();
+  DBuf<uint32_t> ccnt, dpos;
+  if (nr && core_bits && n >= core_bits && n - core_bits >= g.h0) {
+    // core = ranks [cb, n), cb - h0 a multiple of 32 so the core words are
+    // words of the joins' hot bitmap; n - cb <= core_bits
+    const uint32_t cbh = (n - core_bits - g.h0 + 31) & ~31u, cb = g.h0 + cbh;
+    ccnt.alloc(nr, s);
+    dpos.alloc((uint64_t)nr + 1, s);
+    k_core_rows<<<grid_gs(nr, dev), kT, 0, s>>>(g.offH.get(), g.colH.get(), g.r0, n, cbh, core_min, ccnt.get());
     TC_LAUNCH();
+    scan_exclusive<uint32_t>(DenseFlag{ccnt.get()}, dpos.get(), nr, dpos.get() + nr, s);
+    const uint32_t nd = read_scalar(dpos.get() + nr, s);
+    if (nd > 0) {
+      g.cb = cb;
+      g.core_words = (n - cb + 31) / 32;
+      g.ndense = nd;
+      g.core_min = core_min;
+    } else {
+      ccnt.release();  // no dense rows (or too many to index): every row stays sparse
+    }
+  }
+  if (nr) {
+    k_rowdesc<<<grid_gs(nr, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.r0, n, g.ndense ? ccnt.get() : nullptr,
+                                              dpos.get(), g.rowd.get());
+    TC_LAUNCH();
+  }
+  if (g.ndense) {
+    g.cbits.alloc((uint64_t)g.ndense * g.core_words, s);
+    TC_CUDA(cudaMemsetAsync(g.cbits.get(), 0, sizeof(uint32_t) * (uint64_t)g.ndense * g.core_words, s));
+    k_core_fill<<<grid_gs(32 * (uint64_t)nr, dev), kT, 0, s>>>(g.rowd.get(), nr, g.colH.get(), g.cb - g.h0,
+                                                                g.core_words, g.cbits.get());
+    TC_LAUNCH();
+  }
+  ccnt.release();
+  dpos.release();
+  // dense in-edge list and its segments (k_join_dense)
+  g.dine.release();
+  g.dseg.release();
+  g.drow.release();
+  g.ndine = 0;
+  g.dsoff.alloc((uint64_t)n + 1, s);
+  TC_CUDA(cudaMemsetAsync(g.dsoff.get(), 0, sizeof(uint32_t) * ((uint64_t)n + 1), s));
+  if (g.ndense && E) {
+    DBuf<uint32_t> ip(E + 1, s);
+    scan_exclusive<uint32_t>(DenseIn{g.ine.get(), g.rowd.get(), g.r0}, ip.get(), E, ip.get() + E, s);
+    g.ndine = read_scalar(ip.get() + E, s);
+    g.dine.alloc(g.ndine ? g.ndine : 1, s);
+    if (g.ndine) {
+      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.ine.get(), E, g.rowd.get(), g.r0, ip.get(), g.dine.get());
+      TC_LAUNCH();
+    }
+    scan_exclusive<uint32_t>(DenseSegs{g.inoff.get(), ip.get()}, g.dsoff.get(), n, g.dsoff.get() + n, s);
+    const uint32_t nseg = read_scalar(g.dsoff.get() + n, s);
+    g.dseg.alloc(nseg ? nseg : 1, s);
+    if (nseg) {
+      k_dense_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.inoff.get(), ip.get(), n, g.dsoff.get(), g.dseg.get());
+      TC_LAUNCH();
+    }
+    g.drow.alloc(g.ndense, s);
+    k_dense_rows<<<grid_gs(nr, dev), kT, 0, s>>>(g.rowd.get(), g.r0, nr, g.drow.get());
+    TC_LAUNCH();
+  }
+  // per-vertex mask base of every row (graph property; RowGeo::rowbase)
+  g.mask_total = 0;
+  if (nr) {
+    DBuf<uint64_t> rb((uint64_t)nr + 1, s);
+    scan_exclusive<uint64_t>(RowBytesGeo{g.rowd.get()}, rb.get(), nr, rb.get() + nr, s);
+    k_rowbase_put<<<grid_gs(nr, dev), kT, 0, s>>>(rb.get(), nr, g.rowd.get());
+    TC_LAUNCH();
+    g.mask_total = read_scalar(rb.get() + nr, s);
   }
   DBuf<unsigned long long> tot(4, s);
   TC_CUDA(cudaMemsetAsync(tot.get(), 0, 4 * sizeof(unsigned long long), s));
@@ -1069,7 +1250,6 @@ void finish_graph(tc_graph& g) {
   TC_CUDA(cudaMemcpyAsync(h, tot.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
   TC_CUDA(cudaStreamSynchronize(s));
   for (int c = 0; c < 3; ++c) g.seg_cap[c] = h[c];
-  g.mask_total = h[3];
   g.part_bounds.clear();
   g.part_bounds_P = 0;
 }

@@ -154,6 +154,11 @@ void destroy_handle(tc_graph* g) {
     g->inoff.release();
     g->ine.release();
     g->rowd.release();
+    g->cbits.release();
+    g->dine.release();
+    g->dsoff.release();
+    g->drow.release();
+    g->dseg.release();
     for (auto& sc : g->scratch) sc.release(s);
     cudaStreamSynchronize(s);
   }
@@ -267,6 +272,8 @@ tc_status tc_graph_get_info(const tc_graph* g, tc_graph_info* info) {
   info->max_out_degree = g->max_dplus;
   info->device = g->device;
   info->build_ms = g->build_ms;
+  info->core_ranks = g->core_words ? g->n - g->cb : 0;
+  info->dense_rows = g->ndense;
   return TC_OK;
 }
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <stdexcept>
 #include <string>
@@ -88,6 +89,12 @@ struct PhaseLog {
   void mark(const char* what);
   ~PhaseLog();
 };
+
+// Tuning / test knobs read from the environment (unset = default).
+inline uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = getenv(name);
+  return v ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
+}
 
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
 inline uint64_t ceil_div64(uint64_t a, uint64_t b) { return (a + b - 1) / b; }

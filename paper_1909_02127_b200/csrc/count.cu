@@ -324,13 +324,12 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 // ---- item geometry (from the in-edge index) --------------------------------------
 
 // Level-1 item = in-edge (e, u) of pivot v = col[e]: its wedge suffix is
-// col[e+1 .. off[u+1]).  CTA/small bins take it split into the hot part
-// (16-bit colH, the row's sorted suffix >= h0) and the cold part (col):
-// {hb, he, cb, ce}; all-zero = empty suffix.  mo = the item's first per-vertex
-// mask byte (rowbase[u] + RowMasks::P(k), k = e - off[u]).
-#ifndef TCB_ROWD
-#define TCB_ROWD 1  // item row geometry from tc_graph::rowd (one 16-byte load) or from off/offH
-#endif
+// col[e+1 .. off[u+1]).  CTA/small bins take it from the row descriptor
+// (graph.cuh RowGeo, one 32-byte sector) split into the sparse hot part
+// (16-bit colH up to Ht) and the cold part (col): {hb, he, cb, ce} (empty
+// ranges have he <= hb / ce <= cb).  mo = the item's first per-vertex mask
+// byte (rowbase + RowMasks::P(k), k = e - beg, sparse hot part only).
+// A dense row's core part is joined by k_join_dense.
 // CTA bin, staging of the next segment's in-edge records one segment ahead:
 // 0 = none (plain loads at staging), 1 = one bulk copy (TMA, cp.async.bulk +
 // mbarrier) per segment, 2 = per-thread cp.async (LDGSTS) of the records each
@@ -351,31 +350,16 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 #endif
 constexpr uint32_t kTopFlushSegs = 120;  // <= 65535 / kCtaSegItems increments per counter between flushes
 struct ItemGeo {
-  const uint32_t* off;
-  const uint32_t* offH;
   const uint4* rowd;  // tc_graph::rowd, rows [r0, n)
-  const uint64_t* rowbase;  // rows [r0, n)
   uint32_t r0;
-  __device__ __forceinline__ uint4 row(uint32_t u) const {
-#if TCB_ROWD
-    return rowd[u - r0];
-#else
-    return make_uint4(off[u], off[u + 1], offH[u], offH[u + 1]);
-#endif
-  }
   __device__ __forceinline__ uint4 hotcold(uint2 eu, uint64_t* mo) const {
-    const uint32_t e = eu.x, u = eu.y;
-    const uint4 rd = row(u);
-    const uint32_t end = rd.y;
-    const uint32_t O = rd.z, h = rd.w - rd.z;
-    if (e + 1 >= end) return make_uint4(0, 0, 0, 0);
-    const uint32_t cold_end = end - h;
-    const uint4 it = (e + 1 >= cold_end) ? make_uint4(O + (e + 1 - cold_end), O + h, 0, 0)
-                                         : make_uint4(O, O + h, e + 1, cold_end);
-    if (mo != nullptr && it.y > it.x) {
-      const uint32_t beg = rd.x;
-      *mo = rowbase[u - r0] + RowMasks(end - beg, O, h).P(e - beg);
-    }
+    const uint32_t e = eu.x;
+    const RowGeo r = load_row(rowd, r0, eu.y);
+    if (e + 1 >= r.end) return make_uint4(0, 0, 0, 0);
+    const uint32_t cold_end = r.cold_end();
+    const uint4 it = (e + 1 >= cold_end) ? make_uint4(r.O + (e + 1 - cold_end), r.Ht, 0, 0)
+                                         : make_uint4(r.O, r.Ht, e + 1, cold_end);
+    if (mo != nullptr && it.y > it.x) *mo = r.rowbase + r.masks().P(e - r.beg);
     return it;
   }
 };
@@ -384,16 +368,14 @@ struct ItemGeo {
 
 // Advance + join for in-edges [i0, i1) of one small pivot (d+ <= 64), one
 // warp against its private hash; items are the u32 suffix ranges
-// {e+1, off[u+1]} of col.  Per-vertex: the CTA bin's row pass reads hit masks
+// {e+1, off[u+1] - cc(u)} of col (a dense row's core part is k_join_dense's).  Per-vertex: the CTA bin's row pass reads hit masks
 // for every item, so this bin zeroes its items' mask bytes (its hits go to
 // per-hit counters instead); d+(v) = 0 pivots come here for that alone.
 template <bool kPerVertex, typename Sink>
 __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ ine, uint32_t i0, uint32_t i1,
-                                                    const uint32_t* __restrict__ off,
-                                                    const uint32_t* __restrict__ offH,
+                                                    const uint4* __restrict__ rowd, uint32_t r0,
                                                     const uint32_t* __restrict__ col, const uint32_t* tab,
                                                     uint32_t mask, uint32_t shift, bool probe, const Sink& sink,
-                                                    const uint64_t* __restrict__ rowbase, uint32_t r0,
                                                     uint8_t* __restrict__ masks, uint32_t* item_cnt) {
   const unsigned lane = lane_id();
   const uint4* col4 = reinterpret_cast<const uint4*>(col);
@@ -404,17 +386,19 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ in
     if (my < i1) {
       const uint2 eu = ine[my];
       u = eu.y;
-      const uint32_t beg = off[u], end = off[u + 1];
-      if (eu.x + 1 < end) {
+      const RowGeo r = load_row(rowd, r0, u);
+      if (eu.x + 1 < r.end) {
+        // a dense row's core members (its last cc) are joined by k_join_dense
         b = eu.x + 1;
-        e = end;
-        nch = ((e + 3) >> 2) - (b >> 2);
+        e = r.end - r.cc();
+        nch = b < e ? ((e + 3) >> 2) - (b >> 2) : 0u;
         if (kPerVertex && TCB_PV_MASKS) {
-          const uint32_t O = offH[u], h = offH[u + 1] - O;
-          if (h > 0) {
-            const RowMasks rm(end - beg, O, h);
-            const uint32_t k = eu.x - beg;
-            uint8_t* z = masks + rowbase[u - r0] + rm.P(k);
+          // the row pass reads every item's sparse hot mask bytes: zero this
+          // item's (its hits are counted here, per hit)
+          const RowMasks rm = r.masks();
+          const uint32_t k = eu.x - r.beg;
+          if (rm.h > 0 && k + 1 < rm.d) {
+            uint8_t* z = masks + r.rowbase + rm.P(k);
             const uint32_t nb = (uint32_t)(rm.c_hi - rm.first_chunk(k));
             for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
           }
@@ -468,9 +452,9 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ in
 // counters (dynamic SMEM, pv only).  The segment count is read on the device.
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ offH, const uint32_t* __restrict__ col,
+    const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ col,
     const uint2* __restrict__ ine, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
-    uint32_t rc, uint32_t ncnt, const uint64_t* __restrict__ rowbase, uint32_t r0, uint8_t* __restrict__ masks,
+    uint32_t rc, uint32_t ncnt, uint8_t* __restrict__ masks,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
   __shared__ uint32_t s_tab[kJoinWarps][kWarpTable];
@@ -494,8 +478,8 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
-    const uint32_t h = warp_join_small<kPerVertex>(ine, sg.y, sg.z, off, offH, col, tab, mask, shift, dv > 0, sink,
-                                                   rowbase, r0, masks, s_item[warp]);
+    const uint32_t h = warp_join_small<kPerVertex>(ine, sg.y, sg.z, rowd, r0, col, tab, mask, shift, dv > 0, sink,
+                                                   masks, s_item[warp]);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
@@ -510,6 +494,166 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   if (kPerVertex) {
     __syncthreads();
     flush_top<false>(top_cnt, ncnt, rc, t_rank);
+  }
+}
+
+// ---- dense core join ------------------------------------------------------------
+// The core part of every dense item (graph.cuh tc_graph::dine): the item's
+// row keeps its members among the top ranks [cb, n) as a bitmap of cw words,
+// and so does the pivot (its own bitmap when its row is dense, else built
+// from its few core members), so the join is a word-parallel AND + popcount
+// -- no per-candidate probes.  One warp per segment (<= kDenseSeg items of
+// one pivot); lane j holds pivot words j + 32k (P[k]; every member ranks
+// above v, so no suffix bound is needed) and loads the same words of each
+// item's row (coalesced, 128 B per k; lanes whose pivot word is zero skip
+// the load), 4 items in flight.
+// Per-vertex: t[u] += the item's hits, t[v] += the segment's; t[x] for the
+// hit bits through per-lane bit-sliced counters: the 4 items' hit words are
+// added into kPlanes bit planes per word by carry-save adders (c0..c(P-1),
+// count = sum c_p 2^p; ~6 ops per item-word instead of an atomic per hit)
+// and folded into the CTA's SMEM counters every (2^kPlanes - 4) items.
+constexpr int kDenseThreads = 256;
+constexpr int kDenseWarps = kDenseThreads / 32;
+constexpr int kPlanes = 10;
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
+
+template <bool kPV>
+__global__ void __launch_bounds__(kDenseThreads) k_join_dense(
+    const uint4* __restrict__ dseg, const uint32_t* __restrict__ dsoff, uint32_t v_lo, uint32_t v_hi,
+    unsigned int* __restrict__ queue, const uint32_t* __restrict__ dine, const uint32_t* __restrict__ drow,
+    const uint32_t* __restrict__ cbits, uint32_t cw, uint32_t cb, uint32_t cbh, uint32_t core_min,
+    const uint4* __restrict__ rowd, uint32_t r0, const uint16_t* __restrict__ colH,
+    unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
+  constexpr int kCW = kCoreWordsMax;
+  __shared__ uint32_t s_p[kDenseWarps][32 * kCW];              // pivot core words (non-dense pivots)
+  __shared__ uint32_t s_cnt[kPV ? 32 * 32 * kCW : 1];          // t[x] of core ranks, this CTA
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  if (kPV) {
+    for (uint32_t i = threadIdx.x; i < 32 * 32 * kCW; i += kDenseThreads) s_cnt[i] = 0;
+    __syncthreads();
+  }
+  for (uint32_t i = lane; i < 32 * kCW; i += 32) s_p[warp][i] = 0;
+  __syncwarp();
+  const uint32_t sb = dsoff[v_lo], se = dsoff[v_hi];  // this part's segments (pivots [v_lo, v_hi))
+  uint32_t c[kPV ? kPlanes : 1][kCW];
+#pragma unroll
+  for (int p = 0; p < (kPV ? kPlanes : 1); ++p)
+#pragma unroll
+    for (int k = 0; k < kCW; ++k) c[p][k] = 0;
+  uint32_t since = 0;  // items added to the planes since the last fold
+  auto fold = [&]() {
+#pragma unroll
+    for (int k = 0; k < kCW; ++k) {
+      const uint32_t j = lane + 32 * k;
+      if (j >= cw) continue;
+      uint32_t any = 0;
+#pragma unroll
+      for (int p = 0; p < kPlanes; ++p) any |= c[kPV ? p : 0][k];
+      while (any) {
+        const uint32_t b = __ffs(any) - 1;
+        any &= any - 1;
+        uint32_t v = 0;
+#pragma unroll
+        for (int p = 0; p < kPlanes; ++p) v |= ((c[kPV ? p : 0][k] >> b) & 1u) << p;
+        atomicAdd(&s_cnt[32 * j + b], v);
+      }
+#pragma unroll
+      for (int p = 0; p < (kPV ? kPlanes : 1); ++p) c[p][k] = 0;
+    }
+    since = 0;
+  };
+  unsigned long long acc = 0;
+  while (true) {
+    uint32_t q = 0;
+    if (lane == 0) q = atomicAdd(queue, 1u);
+    q = sb + __shfl_sync(0xffffffffu, q, 0);
+    if (q >= se) break;
+    const uint4 sg = dseg[q];
+    const uint32_t v = sg.x;
+    // pivot core words
+    uint32_t P[kCW];
+    {
+      const RowGeo rv = load_row(rowd, r0, v);
+      if (rv.didx != kNoDense) {
+#pragma unroll
+        for (int k = 0; k < kCW; ++k) {
+          const uint32_t j = lane + 32 * k;
+          P[k] = j < cw ? __ldg(cbits + (uint64_t)rv.didx * cw + j) : 0u;
+        }
+      } else {
+        // fewer than core_min core members: the last entries of its hot row
+        const uint32_t h = rv.h();
+        for (uint32_t l = lane; l < core_min && l < h; l += 32) {
+          const uint32_t y = colH[rv.Hf - 1 - l];
+          if (y >= cbh) atomicOr(&s_p[warp][(y - cbh) >> 5], 1u << ((y - cbh) & 31));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kCW; ++k) {
+          P[k] = s_p[warp][lane + 32 * k];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kCW; ++k) s_p[warp][lane + 32 * k] = 0;
+        __syncwarp();
+      }
+    }
+    uint32_t hseg = 0;
+    for (uint32_t i = sg.y; i < sg.z; i += 4) {
+      uint32_t d[4], m[4][kCW];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) d[a] = i + a < sg.z ? __ldg(dine + i + a) : kNoDense;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < kCW; ++k)
+          m[a][k] = (d[a] != kNoDense && P[k]) ? __ldg(cbits + (uint64_t)d[a] * cw + lane + 32 * k) & P[k] : 0u;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        uint32_t hi = 0;
+#pragma unroll
+        for (int k = 0; k < kCW; ++k) hi += __popc(m[a][k]);
+        hseg += hi;
+        if (kPV) {
+          const uint32_t sum = __reduce_add_sync(0xffffffffu, hi);
+          if (lane == 0 && sum) atomicAdd(&t_rank[__ldg(drow + d[a])], (unsigned long long)sum);
+        }
+      }
+      if (kPV) {
+#pragma unroll
+        for (int k = 0; k < kCW; ++k) {
+          // carry-save: c0 + m0 + m1 + m2 + m3 + 2 c1 -> c0 + 2 c1 + 4 k4
+          const uint32_t k1 = maj3(c[0][k], m[0][k], m[1][k]);
+          c[0][k] ^= m[0][k] ^ m[1][k];
+          const uint32_t k2 = maj3(c[0][k], m[2][k], m[3][k]);
+          c[0][k] ^= m[2][k] ^ m[3][k];
+          uint32_t k4 = maj3(c[kPV ? 1 : 0][k], k1, k2);
+          c[kPV ? 1 : 0][k] ^= k1 ^ k2;
+#pragma unroll
+          for (int p = 2; p < (kPV ? kPlanes : 1); ++p) {
+            const uint32_t t = c[p][k] & k4;
+            c[p][k] ^= k4;
+            k4 = t;
+          }
+        }
+        since += 4;
+        if (since > (1u << kPlanes) - 1 - 4) fold();
+      }
+    }
+    acc += hseg;
+    if (kPV) {
+      const uint32_t hv = warp_sum(hseg);
+      if (lane == 0 && hv) atomicAdd(&t_rank[v], (unsigned long long)hv);
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && acc) atomicAdd(total, acc);
+  if (kPV) {
+    if (since) fold();
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 32 * cw; i += kDenseThreads)
+      if (s_cnt[i]) atomicAdd(&t_rank[cb + i], (unsigned long long)s_cnt[i]);
   }
 }
 
@@ -528,9 +672,8 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
 // Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots].
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ offH,
-    const uint4* __restrict__ rowd, uint32_t r0,
-    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine, const uint64_t* __restrict__ rowbase,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd, uint32_t r0,
+    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
     uint32_t h0, uint32_t nbm, uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab,
     uint8_t* __restrict__ masks, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
@@ -560,7 +703,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  const ItemGeo geo{off, offH, rowd, rowbase, r0};
+  const ItemGeo geo{rowd, r0};
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
@@ -667,7 +810,6 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
     }
-    // list positions: hot count in the low 16 bits, cold count in the high 16
     // one block scan of the pair (list positions: hot count in the low 16
     // bits, cold in the high 16; chunk prefixes: hot in the low 32 bits, cold
     // in the high 32), two barriers
@@ -890,9 +1032,8 @@ struct SmallWarpSmem {
 
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kSmallThreads) k_join_small(
-    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint32_t* __restrict__ offH,
-    const uint4* __restrict__ rowd, uint32_t r0,
-    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine, const uint64_t* __restrict__ rowbase,
+    const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd, uint32_t r0,
+    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
     uint32_t h0, uint32_t nbm, uint8_t* __restrict__ masks, uint32_t rc, uint32_t ncnt,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
@@ -901,7 +1042,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
   constexpr bool kHits = kPerVertex && !TCB_PV_MASKS;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  const ItemGeo geo{off, offH, rowd, rowbase, r0};
+  const ItemGeo geo{rowd, r0};
   const uint32_t wbytes = (SmallWarpSmem::bytes(nbm) + 15) & ~15u;
   SmallWarpSmem w(dsm_small + warp * wbytes, nbm);
   // kHits: CTA-shared 32-bit counters for ranks [rc, rc + ncnt), after the warps' regions
@@ -1249,8 +1390,8 @@ struct PartRange {
 };
 
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
-    const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
-    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, uint32_t n, PartRange pr,
+    const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks, uint32_t n,
+    PartRange pr,
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,
     unsigned int* __restrict__ nheavy, uint32_t heavy_thr, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
@@ -1269,15 +1410,20 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint32_t rb = (uint32_t)rb64;
     const uint32_t i = rb + lane;
     uint32_t ul = 0, dl = 0, Ol = 0, hl = 0, kl = 0, kh = 0;
+    uint64_t rbl = 0;
     bool work = false;
     if (i < nrows) {
       ul = n - 1 - i;
-      const uint32_t beg = off[ul];
-      dl = off[ul + 1] - beg;
-      Ol = offH[ul];
-      hl = offH[ul + 1] - Ol;
+      const RowGeo r = load_row(rowd, pr.r0, ul);
+      // the sparse hot part only (a dense row's core members are counted in
+      // the joins' dense step)
+      dl = r.d() - r.cc();
+      Ol = r.O;
+      hl = r.Ht - r.O;
+      rbl = r.rowbase;
       work = hl > 0 && dl >= 2;
-      if (work) pr.items(beg, dl, kl, kh);
+      if (work) pr.items(r.beg, r.d(), kl, kh);
+      kh = min(kh, dl - 1);
       work = work && kh > kl;
       if (work) {
         const RowMasks rm(dl, Ol, hl);
@@ -1298,7 +1444,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       const RowMasks rm(__shfl_sync(0xffffffffu, dl, rj), __shfl_sync(0xffffffffu, Ol, rj),
                         __shfl_sync(0xffffffffu, hl, rj));
       const RowRel rr(rm);
-      const uint8_t* rowm = masks + rowbase[u - pr.r0];
+      const uint8_t* rowm = masks + __shfl_sync(0xffffffffu, rbl, rj);
       const RowLanes rl(rr.C, lane);
       uint32_t row_total = 0;
       for (uint32_t g = 0; g < rr.C; g += rl.w) {
@@ -1336,8 +1482,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
 }
 
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
-    const uint32_t* __restrict__ off, const uint16_t* __restrict__ colH, const uint32_t* __restrict__ offH,
-    const uint64_t* __restrict__ rowbase, const uint8_t* __restrict__ masks, PartRange pr, uint32_t h0,
+    const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks,
+    PartRange pr, uint32_t h0,
     uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, const uint32_t* __restrict__ heavy,
     const unsigned int* __restrict__ nheavy, unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];
@@ -1357,12 +1503,13 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     const uint32_t r = s_row;
     if (r >= nh) break;
     const uint32_t u = heavy[r];
-    const uint32_t beg = off[u], d = off[u + 1] - beg, O = offH[u];
+    const RowGeo rg = load_row(rowd, pr.r0, u);
     uint32_t k_lo = 0, k_hi = 0;
-    pr.items(beg, d, k_lo, k_hi);
-    const RowMasks rm(d, O, offH[u + 1] - O);
+    pr.items(rg.beg, rg.d(), k_lo, k_hi);
+    const RowMasks rm = rg.masks();
+    k_hi = min(k_hi, rm.d - 1);
     const RowRel rr(rm);
-    const uint8_t* rowm = masks + rowbase[u - pr.r0];
+    const uint8_t* rowm = masks + rg.rowbase;
     const RowLanes rl(rr.C, lane);
     my_total = 0;
     for (uint32_t g = 0; g < rr.C; g += rl.w) {
@@ -1405,11 +1552,6 @@ __global__ void k_gather_pv(const unsigned long long* __restrict__ t_rank, const
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x)
     out[v] = t_rank[rank_of[v]];
-}
-
-uint32_t env_u32(const char* name, uint32_t dflt) {
-  const char* v = getenv(name);
-  return v ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
 }
 
 unsigned grid_gs(uint64_t n, int device) {
@@ -1539,8 +1681,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaMemcpyToSymbolAsync(g_pv_dbg, &dbg, sizeof(dbg), 0, cudaMemcpyHostToDevice, s));
   }
   const uint32_t nbm = (n - g.h0 + 31) / 32;
-  unsigned int* queues = g.scratch[kSlotCounters].get<unsigned int>(8, s) + 4;  // [0..3] = plan.nseg
-  TC_CUDA(cudaMemsetAsync(queues, 0, 4 * sizeof(unsigned int), s));
+  unsigned int* queues = g.scratch[kSlotCounters].get<unsigned int>(16, s) + 4;  // [0..3] = plan.nseg
+  TC_CUDA(cudaMemsetAsync(queues, 0, 8 * sizeof(unsigned int), s));
   if (plan.cap[0]) {
     // warp bin: plain 32-bit counters over half the window
     const uint32_t ncnt_w = ncnt / 2, rc_w = pv ? n - ncnt_w : 0xffffffffu;
@@ -1548,8 +1690,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
     const int occ = occupancy(kern, kJoinThreads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(plan.cap[0], kJoinWarps), (uint64_t)sms * occ);
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.offH.get(), g.col.get(), g.ine.get(), plan.wsegs,
-                                         plan.nseg + 0, rc_w, ncnt_w, plan.rowbase, g.r0, masks, t_rank, acc);
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.ine.get(), plan.wsegs,
+                                         plan.nseg + 0, rc_w, ncnt_w, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_warp");
@@ -1563,9 +1705,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     auto kern = pv ? k_join_small<true> : k_join_small<false>;
     const int occ = occupancy(kern, kSmallThreads, ssm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, ceil_div64(plan.cap[2], kSmallWarps));
-    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.offH.get(), g.rowd.get(), g.r0, g.colH.get(),
-                                         g.ine.get(),
-                                         plan.rowbase, plan.ssegs, plan.nseg + 2, queues + 0, g.h0, nbm, masks,
+    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.ine.get(),
+                                         plan.ssegs, plan.nseg + 2, queues + 0, g.h0, nbm, masks,
                                          ncnt_s ? n - ncnt_s : 0xffffffffu, ncnt_s, t_rank, acc);
     TC_LAUNCH();
     ++launches;
@@ -1581,13 +1722,23 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const int occ = occupancy(kern, kJoinThreads, dsm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, plan.cap[1]);
     uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.offH.get(), g.rowd.get(), g.r0, g.colH.get(),
-                                        g.ine.get(),
-                                        plan.rowbase, plan.csegs, plan.nseg + 1, queues + 1, g.h0, nbm, smem_slots,
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.ine.get(),
+                                        plan.csegs, plan.nseg + 1, queues + 1, g.h0, nbm, smem_slots,
                                         slab_cap, slab, masks, rc_hits, ncnt_hits, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_cta");
+  }
+  if (g.ndine) {
+    // dense core parts: word-parallel intersections (k_join_dense)
+    auto kern = pv ? k_join_dense<true> : k_join_dense<false>;
+    const int occ = occupancy(kern, kDenseThreads, 0);
+    kern<<<(unsigned)(sms * occ), kDenseThreads, 0, s>>>(
+        g.dseg.get(), g.dsoff.get(), v_lo, v_hi, queues + 4, g.dine.get(), g.drow.get(), g.cbits.get(), g.core_words,
+        g.cb, g.cb - g.h0, g.core_min, g.rowd.get(), g.r0, g.colH.get(), t_rank, acc);
+    TC_LAUNCH();
+    ++launches;
+    pl.mark("join_dense");
   }
   if (pv && kUseMasks && n && g.mask_total) {
     // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics); a split
@@ -1602,14 +1753,13 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const int hocc = occupancy(k_pv_rows_heavy, kRowWarps * 32, rsm);
     const PartRange pr{g.col.get(), v_lo, v_hi, split, g.r0};
     k_pv_rows<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
-        g.off.get(), g.colH.get(), g.offH.get(), plan.rowbase, masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1,
-        row_heavy_threshold(n), t_rank);
+        g.rowd.get(), g.colH.get(), masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1, row_heavy_threshold(n),
+        t_rank);
     TC_LAUNCH();
     ++launches;
     pl.mark("pv_rows_light");
     k_pv_rows_heavy<<<(unsigned)(sms * hocc), kRowWarps * 32, rsm, s>>>(
-        g.off.get(), g.colH.get(), g.offH.get(), plan.rowbase, masks, pr, g.h0, n - rcnt, rcnt, rq, heavy, rq + 1,
-        t_rank);
+        g.rowd.get(), g.colH.get(), masks, pr, g.h0, n - rcnt, rcnt, rq, heavy, rq + 1, t_rank);
     TC_LAUNCH();
     ++launches;
     pl.mark("pv_rows");

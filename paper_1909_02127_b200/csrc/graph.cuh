@@ -43,7 +43,7 @@ struct Scratch {
   }
 };
 enum ScratchSlot {
-  kSlotRowBase, kSlotSegOff, kSlotWsegs, kSlotCsegs, kSlotSsegs, kSlotMasks, kSlotSlab, kSlotTRank,
+  kSlotSegOff, kSlotWsegs, kSlotCsegs, kSlotSsegs, kSlotMasks, kSlotSlab, kSlotTRank,
   kSlotHeavy, kSlotCls, kSlotSums, kSlotCounters, kSlotAcc, kSlotCount
 };
 }  // namespace tcb
@@ -74,15 +74,34 @@ struct tc_graph {
   // count a plan over |V| instead of a scatter over |E| (plan.cu).
   tcb::DBuf<uint32_t> inoff;
   tcb::DBuf<uint2> ine;
-  // Row geometry interleaved per rank, {off[u], off[u+1], offH[u], offH[u+1]}
-  // for the non-isolated ranks [r0, n) (isolated vertices have the lowest
-  // ranks and no work; a graph with huge declared n stays small): a join
-  // stages an item's suffix with one 16-byte load instead of four.
+  // Row descriptors, one 32-byte record (two uint4, one DRAM sector) per rank
+  // of the non-isolated ranks [r0, n) (isolated vertices have the lowest
+  // ranks and no work): tcb::RowGeo -- a join stages an item's whole row
+  // geometry (offsets, hot/core split, dense index, per-vertex mask base)
+  // with one sector read.
   tcb::DBuf<uint4> rowd;
   uint32_t r0 = 0;
+  // Dense core: the top core_bits ranks [cb, n) (inside the hot window).  A
+  // row with at least core_min members there ("dense row") keeps them as a
+  // core_bits-bit bitmap (cbits + didx * core_words) instead of in its
+  // sparse hot suffix: a join intersects such an item's core part with the
+  // pivot's core words word-parallel (count.cu dense step).  At RMAT s24,
+  // 1.9e5 rows (49 MB of bitmaps) carry 45% of the candidate wedges.
+  uint32_t cb = 0, core_words = 0;  // core_words = 0: no dense rows
+  uint32_t ndense = 0, core_min = 0;
+  tcb::DBuf<uint32_t> cbits;
+  // Dense in-edge list (graph-static, like ine): for every pivot v, the
+  // dense index of each in-neighbour u whose row is dense and whose suffix
+  // after v is non-empty -- the items k_join_dense intersects -- grouped by
+  // pivot (dine), cut into segments of <= kDenseSeg items {v, i0, i1}
+  // (dseg; pivot v's are [dsoff[v], dsoff[v+1])); drow[didx] = the row's rank.
+  tcb::DBuf<uint32_t> dine, dsoff, drow;
+  tcb::DBuf<uint4> dseg;
+  uint64_t ndine = 0;
   // Count-plan capacities (graph properties, recorded once at build): work
   // segments per pivot class over the whole graph (any part has at most as
-  // many) and the per-vertex mask bytes of all rows.
+  // many) and the per-vertex mask bytes of all rows (RowGeo::rowbase is the
+  // exclusive scan of the rows' mask bytes).
   uint64_t seg_cap[3] = {0, 0, 0};
   uint64_t mask_total = 0;
   // multi-GPU work partition (count.cu): pivot rank ranges [b[p], b[p+1])
@@ -147,13 +166,12 @@ constexpr uint32_t kSmallCold = TCB_SMALL_COLD;    // power of two
 //                      per-vertex mask bytes must be zeroed)
 //   csegs  CTA bin    (kCtaSegItems items per segment)
 //   ssegs  small bin  (<= kSmallItems items, <= kSmallCold cold members)
-//   rowbase[u - r0] = first mask byte of row u (per-vertex; rows [r0, n), RowMasks)
+//   masks  per-vertex hit masks (row u's block at RowGeo::rowbase)
 struct Plan {
   uint4* wsegs = nullptr;
   uint4* csegs = nullptr;
   uint4* ssegs = nullptr;
   uint32_t* nseg = nullptr;  // device: [0] warp, [1] CTA, [2] small segment counts
-  uint64_t* rowbase = nullptr;
   uint8_t* masks = nullptr;
   uint32_t v_lo = 0, v_hi = 0;
   uint64_t cap[3] = {0, 0, 0};
@@ -161,7 +179,7 @@ struct Plan {
   void* sums = nullptr;
 };
 // Returns the number of kernels launched.
-// masks: per-vertex hit masks (rowbase + mask buffer, d+ = 0 pivots zeroed by the warp bin)
+// masks: per-vertex hit masks (d+ = 0 pivots' items zeroed by the warp bin)
 int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool masks, bool want_sums, Plan& p);
 // The plan's work counters (W, J, hot, items, pivots) -- a read, only for stats.
 void read_plan_sums(Plan& p, cudaStream_t s);
@@ -218,6 +236,42 @@ struct RowMasks {
     return (O + sk) >> 3;
   }
 };
+
+// Dense-core parameters: core_bits ranks (a multiple of 32, <= 32 * 32 *
+// kCoreWordsMax), rows with >= core_min core members are dense.
+#ifndef TCB_CORE_BITS
+#define TCB_CORE_BITS 2048
+#endif
+constexpr uint32_t kCoreBits = TCB_CORE_BITS;
+constexpr int kCoreWordsMax = 2;  // core words per lane of a warp (core_bits <= 2048)
+constexpr uint32_t kDenseSeg = 64;  // dense items per k_join_dense segment
+
+// Row descriptor of rank u (tc_graph::rowd[2(u - r0)], [2(u - r0) + 1]):
+//   a = {beg = off[u], end = off[u+1], O = offH[u], Ht}
+//   b = {Hf = offH[u+1], didx, rowbase lo, rowbase hi}
+// The row's members: cold col[beg, beg + c0), hot colH[O, Hf) (ids >= h0,
+// sorted); of the hot ones the sparse part is colH[O, Ht) and, for a dense
+// row, the core part colH[Ht, Hf) (ids >= cb) lives in its core bitmap
+// (didx; kNoDense otherwise, Ht = Hf).  Per-vertex hit masks cover the sparse
+// hot part only: RowMasks(d - cc, O, Ht - O) at rowbase.
+constexpr uint32_t kNoDense = 0xffffffffu;
+struct RowGeo {
+  uint32_t beg, end, O, Ht, Hf, didx;
+  uint64_t rowbase;
+  __host__ __device__ __forceinline__ RowGeo(const uint4& a, const uint4& b)
+      : beg(a.x), end(a.y), O(a.z), Ht(a.w), Hf(b.x), didx(b.y), rowbase(b.z | ((uint64_t)b.w << 32)) {}
+  __host__ __device__ __forceinline__ uint32_t d() const { return end - beg; }
+  __host__ __device__ __forceinline__ uint32_t h() const { return Hf - O; }   // hot members
+  __host__ __device__ __forceinline__ uint32_t cc() const { return Hf - Ht; }  // core members cut out
+  __host__ __device__ __forceinline__ uint32_t cold_end() const { return end - (Hf - O); }
+  __host__ __device__ __forceinline__ RowMasks masks() const { return RowMasks(d() - cc(), O, Ht - O); }
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ RowGeo load_row(const uint4* __restrict__ rowd, uint32_t r0, uint32_t u) {
+  const uint4* p = rowd + 2 * (uint64_t)(u - r0);
+  return RowGeo(__ldg(p), __ldg(p + 1));
+}
+#endif
 
 // Build pipeline entry points (build.cu).
 void build_from_pairs(tc_graph& g, const uint32_t* d_pairs, uint64_t m, uint32_t n,

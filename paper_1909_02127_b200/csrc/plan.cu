@@ -12,8 +12,6 @@
 //   k_plan_class   class + 1 per pivot (one byte)
 //   two scans      segment offsets: warp|CTA packed in a u64, small in a u32
 //   k_plan_segs    segment lists; the list lengths go to device memory
-//   rowbase        per-vertex only: exclusive scan of each row's hit-mask
-//                  bytes (closed form, graph.cuh RowMasks), rows [r0, n)
 // No host synchronisation: list capacities are the graph's seg_cap.
 #include <cuda_runtime.h>
 
@@ -90,16 +88,6 @@ __global__ void k_plan_segs(const uint8_t* __restrict__ cls, const uint32_t* __r
   }
 }
 
-// Mask bytes of row u (all rows).
-struct RowBytes {
-  const uint32_t* off;
-  const uint32_t* offH;
-  __device__ __forceinline__ uint64_t operator()(uint64_t u) const {
-    const uint32_t O = offH[u];
-    return RowMasks(off[u + 1] - off[u], O, offH[u + 1] - O).total();
-  }
-};
-
 // Work counters of the part (stats only): per in-edge of the part's pivots
 // its suffix length (J), hot share and usefulness (edge-parallel over the
 // in-edge index), per pivot W = din * d+ (SURVEY 8d wedge stream) and
@@ -119,10 +107,10 @@ __global__ void k_plan_work(const uint32_t* __restrict__ off, const uint4* __res
   const uint32_t i_lo = inoff[v_lo], i_hi = inoff[v_hi];
   for (uint64_t i = i_lo + t0; i < i_hi; i += stride) {
     const uint2 eu = ine[i];
-    const uint4 rd = rowd[eu.y - r0];
-    if (eu.x + 1 >= rd.y) continue;
+    const RowGeo rd = load_row(rowd, r0, eu.y);
+    if (eu.x + 1 >= rd.end) continue;
     ++I;
-    const uint32_t suf = rd.y - eu.x - 1, h = rd.w - rd.z;
+    const uint32_t suf = rd.end - eu.x - 1, h = rd.h();
     J += suf;
     H += suf < h ? suf : h;
   }
@@ -152,7 +140,7 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
   p.v_lo = v_lo;
   p.v_hi = v_hi;
   const uint32_t np = v_hi - v_lo;
-  p.nseg = g.scratch[kSlotCounters].get<uint32_t>(8, s);  // [0..3] segment counts, [4..7] join queues
+  p.nseg = g.scratch[kSlotCounters].get<uint32_t>(16, s);  // [0..3] segment counts, [4..11] join queues
   for (int c = 0; c < 3; ++c) p.cap[c] = g.seg_cap[c];
   p.wsegs = g.scratch[kSlotWsegs].get<uint4>(p.cap[0], s);
   p.csegs = g.scratch[kSlotCsegs].get<uint4>(p.cap[1], s);
@@ -179,18 +167,9 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
     ++kl;
   }
   pl.mark("plan_segs");
-  p.rowbase = nullptr;
   p.masks = nullptr;
   (void)per_vertex;
-  if (masks && n) {
-    // rows [r0, n): rowbase[u - r0]
-    const uint32_t nr = n - g.r0;
-    p.rowbase = g.scratch[kSlotRowBase].get<uint64_t>((uint64_t)nr + 1, s);
-    kl += scan_exclusive<uint64_t>(RowBytes{g.off.get() + g.r0, g.offH.get() + g.r0}, p.rowbase, nr,
-                                   p.rowbase + nr, s);
-    p.masks = g.scratch[kSlotMasks].get<uint8_t>(g.mask_total + 32, s);
-    pl.mark("plan_rowbase");
-  }
+  if (masks && n) p.masks = g.scratch[kSlotMasks].get<uint8_t>(g.mask_total + 32, s);
   p.sums = nullptr;
   if (want_sums) {
     Sums* sums = g.scratch[kSlotSums].get<Sums>(1, s);

@@ -135,6 +135,11 @@ MODES = {
     "default": {},
     "hash": {"TCB_HOT_BITS": "64", "TCB_TOP_COUNTERS": "32"},
     "global_table": {"TCB_HOT_BITS": "64", "TCB_TOP_COUNTERS": "16", "TCB_SMEM_SLOTS": "32"},
+    # dense core (RowGeo): a small core with a low threshold makes most rows
+    # dense; no core at all (every row sparse)
+    "dense_small": {"TCB_CORE_BITS": "96", "TCB_CORE_MIN": "1"},
+    "dense_hash": {"TCB_HOT_BITS": "256", "TCB_CORE_BITS": "224", "TCB_CORE_MIN": "2", "TCB_TOP_COUNTERS": "32"},
+    "no_core": {"TCB_CORE_BITS": "0"},
 }
 
 
@@ -164,7 +169,7 @@ def test_stress_bins(tc, oracle, cuda_ok, name, mode_env):
     assert tc.count_triangles(g, tc.MatchOptions(per_vertex=False)).count == T
 
 
-@pytest.mark.parametrize("mode_env", ["default", "global_table"], indirect=True)
+@pytest.mark.parametrize("mode_env", ["default", "global_table", "no_core"], indirect=True)
 def test_large_clique(tc, cuda_ok, mode_env):
     # K_k: d+ up to k-1 -> 16K-slot tables
     k = 6000
@@ -176,6 +181,34 @@ def test_large_clique(tc, cuda_ok, mode_env):
     r = _count(tc, g)
     assert r.count == T
     assert np.all(r.per_vertex == (k - 1) * (k - 2) // 2)
+
+
+@pytest.mark.parametrize("mode_env", ["dense_small", "dense_hash"], indirect=True)
+def test_gnp_dense_core(tc, oracle, cuda_ok, mode_env):
+    """The dense-core step (word-parallel core intersections, graph.cuh
+    RowGeo) against the oracle: every bin, both routes, per-vertex, parts."""
+    rng = np.random.default_rng(11)
+    for i in range(90):
+        n = int(rng.integers(64, 700))
+        p = (0.05, 0.2, 0.5)[i % 3]
+        iu, ju = np.triu_indices(n, 1)
+        keep = rng.random(iu.size) < p
+        pairs = np.stack([iu[keep], ju[keep]], 1).astype(np.uint32).reshape(-1)
+        off, nb, E, _, _ = oracle.build_graph(pairs, n)
+        T, pv = oracle.count(off, nb, per_vertex=True)
+        g = tc.build_graph_from_pairs(pairs, n)
+        r = _count(tc, g)
+        assert r.count == T and np.array_equal(r.per_vertex, pv), i
+        assert tc.count_triangles(g, tc.MatchOptions(per_vertex=False)).count == T, i
+        g2 = tc.graph_from_csr(off, nb)
+        assert tc.count_triangles(g2).count == T, i
+        if i % 9 == 0:
+            tot, acc = 0, np.zeros(n, np.uint64)
+            for q in range(3):
+                rq = tc.count_triangles(g, tc.MatchOptions(per_vertex=True, part_index=q, part_count=3))
+                tot += rq.count
+                acc += rq.per_vertex
+            assert tot == T and np.array_equal(acc, pv), i
 
 
 @pytest.mark.parametrize("parts", [2, 3, 8])
@@ -371,10 +404,12 @@ def test_c4_rmat_s24(tc, oracle, cuda_ok):
     g = tc.build_graph_from_pairs(d, c["n"], rep, m=m)
     del d
     assert (g.num_edges(), rep.self_loops_removed, rep.duplicate_entries_removed) == (c["E"], c["loops"], c["dups"])
+    assert g.core_ranks == 2048 and g.dense_rows > 100000  # the dense-core step carries ~45% of the wedges here
     r = _count(tc, g)
     assert r.count == c["T"] == 10282799137
     assert oracle.fnv(r.per_vertex) == c["pv_fnv"]
     assert int(r.per_vertex.sum()) == 3 * c["T"]
+    assert tc.count_triangles(g, tc.MatchOptions(per_vertex=False)).count == c["T"]
 
 
 # ---- the Graph-ctor (CSR) route: per-row orientation, hub chunks, row sorts ----

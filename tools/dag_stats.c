@@ -51,10 +51,10 @@ int main(int argc, char** argv) {
   const uint32_t h0 = n > 65536 ? n - 65536 : 0;
   double cand[NB] = {0}, hits[NB] = {0}, J = 0, T = 0, items = 0, items_hot = 0;
   double core_c[3] = {0}, core_elig_items[3] = {0}, core_elig_c[3] = {0}; const uint32_t K[3] = {1024, 2048, 4096};
-  double words_hot = 0;  /* distinct 32-bit bitmap words touched per item's hot suffix, summed */
+  double words_hot = 0, words64_hot = 0, cand_hot = 0;  /* distinct 32-bit bitmap words touched per item's hot suffix, summed */
   double segs512 = 0, piv = 0, dplus_hist[6] = {0}; /* J by pivot d+ class: <=64, <=256, <=1024, >1024 */
   const uint64_t W = (n + 63) / 64;
-#pragma omp parallel reduction(+:cand[:NB], hits[:NB], J, T, items, items_hot, core_c[:3], core_elig_items[:3], core_elig_c[:3], words_hot, segs512, piv, dplus_hist[:6])
+#pragma omp parallel reduction(+:cand[:NB], hits[:NB], J, T, items, items_hot, core_c[:3], core_elig_items[:3], core_elig_c[:3], words_hot, words64_hot, cand_hot, segs512, piv, dplus_hist[:6])
   { uint64_t* bm = calloc(W, 8);
 #pragma omp for schedule(dynamic, 64)
     for (int64_t bb = n - 1; bb >= 0; --bb) { uint32_t b = bb;
@@ -69,7 +69,7 @@ int main(int argc, char** argv) {
         ++items; uint32_t lastw = 0xffffffffu; uint64_t cc[3] = {0,0,0}; int anyhot = 0;
         for (uint64_t k = lo; k < da; ++k) { uint32_t x = na[k]; uint32_t td = n - 1 - x; int bi = 0; while (td >= edges_[bi]) ++bi;
           cand[bi] += 1; J += 1; jb += 1;
-          if (x >= h0) { anyhot = 1; uint32_t w = (x - h0) >> 5; if (w != lastw) { words_hot += 1; lastw = w; } }
+          if (x >= h0) { anyhot = 1; cand_hot += 1; uint32_t w = (x - h0) >> 5; if (w != lastw) { words_hot += 1; if ((w >> 1) != (lastw >> 1) || lastw == 0xffffffffu) words64_hot += 1; lastw = w; } }
           for (int t = 0; t < 3; ++t) if (td < K[t]) cc[t]++;
           if ((bm[x>>6] >> (x&63)) & 1) { hits[bi] += 1; T += 1; } }
         items_hot += anyhot;
@@ -79,6 +79,7 @@ int main(int argc, char** argv) {
     free(bm); }
   printf("n=%u E=%llu J=%.4g T=%.4g items=%.4g items_hot=%.4g pivots=%.4g segs512=%.4g words_hot=%.4g\n", n,
          (unsigned long long)E, J, T, items, items_hot, piv, segs512, words_hot);
+  printf("hot cands=%.4g words32=%.4g (%.2f ids/word) words64=%.4g (%.2f ids/word)\n", cand_hot, words_hot, cand_hot/words_hot, words64_hot, cand_hot/words64_hot);
   printf("top-distance buckets (<256 <1K <2K <4K <8K <16K <32K <64K cold):\n cand%%:");
   for (int i = 0; i < NB; ++i) printf(" %.2f", 100 * cand[i] / J);
   printf("\n hits%%:");

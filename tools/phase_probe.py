@@ -24,6 +24,8 @@ tc.generate(k, a.scale, a.param, out=d)
 g = tc.build_graph_from_pairs(d, 1 << a.scale, m=m)
 del d
 torch.cuda.empty_cache()
+print(f"graph: |E|={g.num_edges()} build_ms={g.build_ms:.1f} core_ranks={g.core_ranks} dense_rows={g.dense_rows}",
+      flush=True)
 n = 1 << a.scale
 tot = torch.zeros(1, dtype=torch.int64, device="cuda")
 pv = torch.zeros(n, dtype=torch.int64, device="cuda") if a.pv else None
