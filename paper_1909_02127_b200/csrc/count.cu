@@ -93,18 +93,39 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 #ifndef TCB_SEG_COST
 #define TCB_SEG_COST 4
 #endif
+#ifndef TCB_DENSE_COST
+#define TCB_DENSE_COST 48  // one dense item (k_join_dense, ~50 warp instructions) in candidate-probe units
+#endif
+#ifndef TCB_COLD_COST
+#define TCB_COLD_COST 3  // a cold (prefiltered hash) probe
+#endif
+#ifndef TCB_WARP_COST
+#define TCB_WARP_COST 4  // a warp-bin (hash) probe
+#endif
 constexpr uint64_t kItemCost = TCB_ITEM_COST;
 constexpr uint64_t kSegRowCost = TCB_SEG_COST;  // per member of N+(v), per segment
 
-__global__ void k_pivot_wedges(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
-                               const uint32_t* __restrict__ src, uint64_t E, uint32_t r0,
-                               unsigned long long* __restrict__ jv) {
+__global__ void k_pivot_wedges(const uint4* __restrict__ rowd, const uint32_t* __restrict__ col,
+                               const uint32_t* __restrict__ src, uint64_t E, uint32_t r0, uint32_t dense_cost,
+                               uint32_t cold_cost, uint32_t warp_cost, unsigned long long* __restrict__ jv) {
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = base + threadIdx.x;
     const bool ok = e < E;
     const uint32_t v = ok ? col[e] : 0xffffffffu;
-    // suffix length of e in its row (<= max d+, so a warp's sum fits 32 bits)
-    const uint32_t w = ok ? off[src[e] + 1] - (uint32_t)e - 1 : 0u;
+    // cost of item e in candidate-probe units: its sparse suffix (bitmap
+    // probes 1, cold hash probes cold_cost, warp-bin probes warp_cost) and
+    // its dense core part, if any, as one k_join_dense item (dense_cost);
+    // a warp's sum fits 32 bits
+    uint32_t w = 0;
+    if (ok) {
+      const RowGeo r = load_row(rowd, r0, src[e]);
+      const uint32_t a = (uint32_t)e + 1, se = r.end - r.cc(), ce = min(r.cold_end(), se);
+      const uint32_t cold = ce > a ? ce - a : 0u;          // hash-probed candidates
+      const uint32_t hot = se > max(a, ce) ? se - max(a, ce) : 0u;  // bitmap-probed
+      const RowGeo rv = load_row(rowd, r0, v);
+      w = rv.d() <= kWarpMaxDeg ? warp_cost * (cold + hot) : hot + cold_cost * cold;
+      if (r.didx != kNoDense && a < r.end) w += dense_cost;
+    }
     const unsigned peers = __match_any_sync(0xffffffffu, v);
     const uint32_t sum = __reduce_add_sync(peers, w);
     if (ok && (int)lane_id() == __ffs(peers) - 1 && sum) atomicAdd(&jv[v - r0], (unsigned long long)sum);
@@ -235,18 +256,30 @@ __device__ __forceinline__ uint32_t hot_hit_mask(const uint4& q, uint32_t c, uin
   return hits & valid;
 }
 
-// 4 cold ids (32-bit) per chunk: hash probes.
+// Cold-member prefilter of a pivot: one bit per 11-bit Fibonacci hash of
+// each member below the hot window (2048 bits of SMEM).  Cold candidates
+// close a triangle about once in 10^3 probes at RMAT s24, so a filter miss
+// (one LDS + shift) replaces most linear-probe chains.
+constexpr uint32_t kColdFilterWords = 64;
+__device__ __forceinline__ uint32_t cfilt_bit(uint32_t x) { return (x * 0x9E3779B1u) >> 21; }
+__device__ __forceinline__ bool cfilt_test(const uint32_t* cf, uint32_t x) {
+  const uint32_t f = cfilt_bit(x);
+  return (cf[f >> 5] >> (f & 31)) & 1u;
+}
+
+// 4 cold ids (32-bit) per chunk: hash probes (behind the prefilter cf when
+// given).
 template <bool kPerVertex, typename Sink>
 __device__ __forceinline__ uint32_t probe_cold(const uint4& q, uint32_t c, uint32_t b, uint32_t e,
                                                const uint32_t* tab, uint32_t mask, uint32_t shift,
-                                               const Sink& sink) {
+                                               const Sink& sink, const uint32_t* cf = nullptr) {
   const uint32_t xs[4] = {q.x, q.y, q.z, q.w};
   const uint32_t p0 = c << 2;
   uint32_t h = 0;
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const uint32_t p = p0 + t;
-    if (p >= b && p < e && hash_find(tab, mask, shift, xs[t])) {
+    if (p >= b && p < e && (cf == nullptr || cfilt_test(cf, xs[t])) && hash_find(tab, mask, shift, xs[t])) {
       ++h;
       if (kPerVertex) sink.hit(xs[t]);
     }
@@ -604,11 +637,16 @@ __global__ void __launch_bounds__(kDenseThreads) k_join_dense(
       uint32_t d[4], m[4][kCW];
 #pragma unroll
       for (int a = 0; a < 4; ++a) d[a] = i + a < sg.z ? __ldg(dine + i + a) : kNoDense;
+      // lane a < 4 owns item a's t[u] update: its row rank is loaded now,
+      // under the bitmap loads
+      const uint32_t dl = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
+      const uint32_t urow = (kPV && lane < 4 && dl != kNoDense) ? __ldg(drow + dl) : 0u;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int k = 0; k < kCW; ++k)
           m[a][k] = (d[a] != kNoDense && P[k]) ? __ldg(cbits + (uint64_t)d[a] * cw + lane + 32 * k) & P[k] : 0u;
+      uint32_t mysum = 0;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         uint32_t hi = 0;
@@ -617,9 +655,10 @@ __global__ void __launch_bounds__(kDenseThreads) k_join_dense(
         hseg += hi;
         if (kPV) {
           const uint32_t sum = __reduce_add_sync(0xffffffffu, hi);
-          if (lane == 0 && sum) atomicAdd(&t_rank[__ldg(drow + d[a])], (unsigned long long)sum);
+          if (lane == (unsigned)a) mysum = sum;
         }
       }
+      if (kPV && lane < 4 && mysum) atomicAdd(&t_rank[urow], (unsigned long long)mysum);
       if (kPV) {
 #pragma unroll
         for (int k = 0; k < kCW; ++k) {
@@ -688,6 +727,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   __shared__ uint32_t s_cb[kCtaSegItems], s_ce[kCtaSegItems], s_cpre[kCtaSegItems + 1];
   __shared__ uint16_t s_cidx[kPerVertex ? kCtaSegItems : 1];  // cold item -> segment index (t[u] counts)
   __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
+  __shared__ uint32_t s_cf[kColdFilterWords];  // cold-member prefilter
   __shared__ uint32_t s_hits, s_cold, s_nl;
   __shared__ uint32_t s_wl[kJoinWarps];
   __shared__ unsigned long long s_wc[kJoinWarps];
@@ -707,6 +747,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
+  for (uint32_t i = threadIdx.x; i < kColdFilterWords; i += kJoinThreads) s_cf[i] = 0;
   if (kPerVertex)
     for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kJoinThreads) s_icnt[i] = 0;
   if (kHits)
@@ -905,7 +946,12 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       tmask = ts - 1;
       tshift = __clz(ts) + 1;  // 32 - log2(ts), ts a power of two
       tab = ts <= stab_slots ? stab : gtab;
-      for (uint32_t j = threadIdx.x; j < cold; j += kJoinThreads) hash_insert(tab, tmask, tshift, col[nb + j]);
+      for (uint32_t j = threadIdx.x; j < cold; j += kJoinThreads) {
+        const uint32_t x = col[nb + j];
+        hash_insert(tab, tmask, tshift, x);
+        const uint32_t f = cfilt_bit(x);
+        atomicOr(&s_cf[f >> 5], 1u << (f & 31));
+      }
       if (tab == gtab) __threadfence_block();
     }
     __syncthreads();
@@ -937,12 +983,12 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       if (tab == stab)  // SMEM table (LDS probes); the global slab only for huge pivots
         h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
                              [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
-                               return probe_cold<kPerVertex>(qq, c, b, e, stab, tmask, tshift, sink);
+                               return probe_cold<kPerVertex>(qq, c, b, e, stab, tmask, tshift, sink, s_cf);
                              });
       else
         h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
                              [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
-                               return probe_cold<kPerVertex>(qq, c, b, e, gtab, tmask, tshift, sink);
+                               return probe_cold<kPerVertex>(qq, c, b, e, gtab, tmask, tshift, sink, s_cf);
                              });
     }
     acc += h;
@@ -962,6 +1008,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       for (uint32_t j = cold + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - h0) >> 5] = 0;
     }
     for (uint32_t j = threadIdx.x; j < ts; j += kJoinThreads) tab[j] = kEmpty;
+    if (cold)
+      for (uint32_t j = threadIdx.x; j < kColdFilterWords; j += kJoinThreads) s_cf[j] = 0;
     if (kPerVertex) {
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
         const uint32_t c = s_icnt[i];
@@ -1004,6 +1052,7 @@ constexpr int kSmallR = kSmallItems / 32;  // items per lane
 struct SmallWarpSmem {
   uint32_t* bm;
   uint32_t* tab;
+  uint32_t* cf;  // cold-member prefilter
   uint32_t *hb, *he, *hpre, *cb, *ce, *cpre, *icnt;
   uint16_t *hidx, *cidx;
   unsigned long long* hmo;
@@ -1011,7 +1060,7 @@ struct SmallWarpSmem {
     const uint32_t nb4 = (nbm + 3) & ~3u;
     // hmo u64[64] | bm[nb4] | tab[256] | hb, he, cb, ce, icnt [64 each] | hpre, cpre [65] | hidx, cidx u16[64]
     return kSmallItems * 8 + (nb4 + kSmallTable) * 4 + (kSmallItems * 5 + (kSmallItems + 1) * 2) * 4 +
-           kSmallItems * 2 * 2 + 16;
+           kSmallItems * 2 * 2 + kColdFilterWords * 4 + 16;
   }
   __device__ SmallWarpSmem(uint8_t* base, uint32_t nbm) {
     const uint32_t nb4 = (nbm + 3) & ~3u;
@@ -1025,7 +1074,8 @@ struct SmallWarpSmem {
     icnt = ce + kSmallItems;
     hpre = icnt + kSmallItems;
     cpre = hpre + kSmallItems + 1;
-    hidx = reinterpret_cast<uint16_t*>(cpre + kSmallItems + 1);
+    cf = cpre + kSmallItems + 1;
+    hidx = reinterpret_cast<uint16_t*>(cf + kColdFilterWords);
     cidx = hidx + kSmallItems;
   }
 };
@@ -1055,6 +1105,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
   for (uint32_t i = lane; i < nbm; i += 32) w.bm[i] = 0;
   for (uint32_t i = lane; i < kSmallTable; i += 32) w.tab[i] = kEmpty;
   for (uint32_t i = lane; i < kSmallItems; i += 32) w.icnt[i] = 0;
+  for (uint32_t i = lane; i < kColdFilterWords; i += 32) w.cf[i] = 0;
   __syncwarp();
   const uint32_t tmask = kSmallTable - 1, tshift = __clz(kSmallTable) + 1;  // 32 - log2(kSmallTable)
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, 0};
@@ -1075,7 +1126,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
       if (j < dv && x >= h0) atomicOr(&w.bm[(x - h0) >> 5], 1u << ((x - h0) & 31));
       cold += __popc(__ballot_sync(0xffffffffu, j < dv && x < h0));
     }
-    for (uint32_t j = lane; j < cold; j += 32) hash_insert(w.tab, tmask, tshift, col[nb + j]);
+    for (uint32_t j = lane; j < cold; j += 32) {
+      const uint32_t x = col[nb + j];
+      hash_insert(w.tab, tmask, tshift, x);
+      const uint32_t f = cfilt_bit(x);
+      atomicOr(&w.cf[f >> 5], 1u << (f & 31));
+    }
     // (2) items (<= kSmallItems, kSmallR per lane) -> hot / cold lists with chunk prefixes
     uint4 it[kSmallR];
     uint64_t mo[kSmallR];
@@ -1141,7 +1197,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
     if (ncold)
       h += warp_walk<4, 2>(0, tcc, ncold, w.cpre, w.cb, w.ce, w.cidx, kPerVertex ? w.icnt : nullptr, col,
                            [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
-                             return probe_cold<kPerVertex>(qq, c, b, e, w.tab, tmask, tshift, sink);
+                             return probe_cold<kPerVertex>(qq, c, b, e, w.tab, tmask, tshift, sink, w.cf);
                            });
     acc += h;
     __syncwarp();
@@ -1158,8 +1214,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
     }
     // (4) clear the touched bitmap words and table slots
     for (uint32_t j = cold + lane; j < dv; j += 32) w.bm[(col[nb + j] - h0) >> 5] = 0;
-    if (cold)
+    if (cold) {
       for (uint32_t i = lane; i < kSmallTable; i += 32) w.tab[i] = kEmpty;
+      for (uint32_t i = lane; i < kColdFilterWords; i += 32) w.cf[i] = 0;
+    }
     __syncwarp();
   }
   acc = warp_sum(acc);
@@ -1384,8 +1442,8 @@ struct PartRange {
     k_lo = 0;
     k_hi = d ? d - 1 : 0;  // item d-1 has an empty suffix (no mask bytes)
     if (!split || d == 0) return;
-    k_lo = lb(col, beg, beg + d, v_lo) - beg;
-    k_hi = min(k_hi, lb(col, beg + k_lo, beg + d, v_hi) - beg);
+    if (v_lo) k_lo = lb(col, beg, beg + d, v_lo) - beg;
+    if (v_hi != 0xffffffffu) k_hi = min(k_hi, lb(col, beg + k_lo, beg + d, v_hi) - beg);
   }
 };
 
@@ -1393,7 +1451,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks, uint32_t n,
     PartRange pr,
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,
-    unsigned int* __restrict__ nheavy, uint32_t heavy_thr, unsigned long long* __restrict__ t_rank) {
+    unsigned int* __restrict__ nheavy, uint32_t heavy_thr, uint32_t row_first,
+    unsigned long long* __restrict__ t_rank) {
   extern __shared__ uint32_t top[];  // 32-bit counters for ranks [rc, rc+ncnt)
   __shared__ uint2 s_spread[256];
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) top[i] = 0;
@@ -1404,10 +1463,10 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
   const uint4* colH4 = reinterpret_cast<const uint4*>(colH);
   while (true) {
     unsigned long long rb64 = 0;  // 64-bit queue: row counts may approach 2^32
-    if (lane == 0) rb64 = atomicAdd(queue, 32ull);
+    if (lane == 0) rb64 = atomicAdd(queue, 32ull) + row_first;
     rb64 = __shfl_sync(0xffffffffu, rb64, 0);
     if (rb64 >= nrows) break;
-    const uint32_t rb = (uint32_t)rb64;
+    const uint32_t rb = (uint32_t)rb64;  // from the part's first row with items (u < v_hi)
     const uint32_t i = rb + lane;
     uint32_t ul = 0, dl = 0, Ol = 0, hl = 0, kl = 0, kh = 0;
     uint64_t rbl = 0;
@@ -1597,8 +1656,10 @@ const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
     DBuf<unsigned long long> jv(nr, s);
     DBuf<uint64_t> prefix(nr, s), tot(1, s), bnd((uint64_t)parts + 1, s);
     TC_CUDA(cudaMemsetAsync(jv.get(), 0, sizeof(unsigned long long) * nr, s));
-    k_pivot_wedges<<<grid_gs(g.E, g.device), 256, 0, s>>>(g.off.get(), g.col.get(), g.src.get(), g.E, g.r0,
-                                                          jv.get());
+    k_pivot_wedges<<<grid_gs(g.E, g.device), 256, 0, s>>>(g.rowd.get(), g.col.get(), g.src.get(), g.E, g.r0,
+                                                          env_u32("TCB_DENSE_COST", TCB_DENSE_COST),
+                                                          env_u32("TCB_COLD_COST", TCB_COLD_COST),
+                                                          env_u32("TCB_WARP_COST", TCB_WARP_COST), jv.get());
     TC_LAUNCH();
     const uint64_t item_cost = env_u32("TCB_ITEM_COST", (uint32_t)kItemCost);  // cost-model knobs
     const uint64_t seg_cost = env_u32("TCB_SEG_COST", (uint32_t)kSegRowCost);
@@ -1751,10 +1812,12 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
     const int rocc = occupancy(k_pv_rows, kRowWarps * 32, rsm);
     const int hocc = occupancy(k_pv_rows_heavy, kRowWarps * 32, rsm);
-    const PartRange pr{g.col.get(), v_lo, v_hi, split, g.r0};
+    // items u -> v of pivots [v_lo, v_hi) have u < v_hi: rows [v_hi, n) skip
+    // (the light pass walks rows top-down from queue position n - v_hi)
+    const PartRange pr{g.col.get(), v_lo, v_hi == n ? 0xffffffffu : v_hi, split, g.r0};
     k_pv_rows<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
         g.rowd.get(), g.colH.get(), masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1, row_heavy_threshold(n),
-        t_rank);
+        n - v_hi, t_rank);
     TC_LAUNCH();
     ++launches;
     pl.mark("pv_rows_light");

@@ -243,7 +243,7 @@ struct RowMasks {
 #define TCB_CORE_BITS 2048
 #endif
 constexpr uint32_t kCoreBits = TCB_CORE_BITS;
-constexpr int kCoreWordsMax = 2;  // core words per lane of a warp (core_bits <= 2048)
+constexpr int kCoreWordsMax = (TCB_CORE_BITS + 1023) / 1024;  // core words per lane of a warp
 constexpr uint32_t kDenseSeg = 64;  // dense items per k_join_dense segment
 
 // Row descriptor of rank u (tc_graph::rowd[2(u - r0)], [2(u - r0) + 1]):

@@ -12,7 +12,27 @@ import numpy as np
 
 ITEM_COST = 24     # count.cu kItemCost: per in-edge item, in candidate-probe units
 SEG_COST = 4       # count.cu kSegRowCost: per member of N+(v), per CTA segment
+DENSE_COST = 48    # count.cu TCB_DENSE_COST: one dense-core item (k_join_dense)
+COLD_COST = 3      # count.cu TCB_COLD_COST: a cold (hash) probe
+WARP_COST = 4      # count.cu TCB_WARP_COST: a warp-bin probe
+WARP_MAX_DEG = 64  # graph.cuh kWarpMaxDeg
 CTA_SEG_ITEMS = 512
+HOT_BITS = 1 << 16  # graph.cuh kHotBits
+CORE_BITS = 2048    # graph.cuh kCoreBits; dense rows have >= CORE_BITS / 32 core members
+
+
+def dense_core(off: np.ndarray, col: np.ndarray):
+    """build.cu finish_graph: core ranks [cb, n) (cb - h0 a multiple of 32)
+    and the core members cut out of every dense row (0 for sparse rows)."""
+    n = off.size - 1
+    h0 = n - HOT_BITS if n > HOT_BITS else 0
+    cc = np.zeros(n, np.int64)
+    if n < CORE_BITS or n - CORE_BITS < h0:
+        return n, cc
+    cb = h0 + ((n - CORE_BITS - h0 + 31) & ~31)
+    src = np.repeat(np.arange(n), np.diff(off))
+    c = np.bincount(src[col >= cb], minlength=n).astype(np.int64)
+    return cb, np.where(c >= CORE_BITS // 32, c, 0)
 
 
 def degree_rank_dag(offsets: np.ndarray, nbrs: np.ndarray):
@@ -37,11 +57,25 @@ def degree_rank_dag(offsets: np.ndarray, nbrs: np.ndarray):
 
 
 def pivot_cost(off: np.ndarray, col: np.ndarray, src: np.ndarray) -> np.ndarray:
-    """Per pivot v: J_v (sum of its in-edges' suffix lengths) + ITEM_COST per
-    in-edge + SEG_COST * d+(v) per CTA segment; 0 without work."""
+    """Per pivot v (count.cu k_pivot_wedges + PivotCost): the probe cost of
+    its in-edges' sparse suffixes (bitmap probes 1, cold hash probes
+    COLD_COST, warp-bin probes WARP_COST; a dense row's core members are one
+    DENSE_COST item) + ITEM_COST per in-edge + SEG_COST * d+(v) per CTA
+    segment; 0 without work."""
     n = off.size - 1
     e = np.arange(col.size, dtype=np.int64)
-    suffix = off[src + 1] - e - 1
+    _, cc = dense_core(off, col)
+    h0 = n - HOT_BITS if n > HOT_BITS else 0
+    nhot = np.bincount(src[col >= h0], minlength=n).astype(np.int64)  # hot members per row
+    end = off[src + 1]
+    a = e + 1
+    se = end - cc[src]                               # sparse part ends
+    ce = np.minimum(end - nhot[src], se)             # cold part ends
+    cold = np.maximum(ce - a, 0)
+    hot = np.maximum(se - np.maximum(a, ce), 0)
+    dpv = np.diff(off)[col]                          # pivot's d+
+    suffix = np.where(dpv <= WARP_MAX_DEG, WARP_COST * (cold + hot), hot + COLD_COST * cold)
+    suffix = suffix + np.where((cc[src] > 0) & (a < end), DENSE_COST, 0)
     jv = np.zeros(n, np.int64)
     np.add.at(jv, col, suffix)
     din = np.bincount(col, minlength=n).astype(np.int64)
