@@ -88,7 +88,7 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 // part only (no re-staging across parts), and the per-vertex row pass of a
 // part reads only the items of its pivots (k_pv_rows PartRange).
 #ifndef TCB_ITEM_COST
-#define TCB_ITEM_COST 24
+#define TCB_ITEM_COST 64
 #endif
 #ifndef TCB_SEG_COST
 #define TCB_SEG_COST 4
@@ -97,10 +97,10 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 #define TCB_DENSE_COST 48  // one dense item (k_join_dense, ~50 warp instructions) in candidate-probe units
 #endif
 #ifndef TCB_COLD_COST
-#define TCB_COLD_COST 3  // a cold (prefiltered hash) probe
+#define TCB_COLD_COST 12  // a cold (prefiltered hash) probe (8-part A/B: profiles/)
 #endif
 #ifndef TCB_WARP_COST
-#define TCB_WARP_COST 4  // a warp-bin (hash) probe
+#define TCB_WARP_COST 16  // a warp-bin (hash) probe
 #endif
 constexpr uint64_t kItemCost = TCB_ITEM_COST;
 constexpr uint64_t kSegRowCost = TCB_SEG_COST;  // per member of N+(v), per segment
@@ -633,52 +633,56 @@ __global__ void __launch_bounds__(kDenseThreads) k_join_dense(
       }
     }
     uint32_t hseg = 0;
-    for (uint32_t i = sg.y; i < sg.z; i += 4) {
-      uint32_t d[4], m[4][kCW];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) d[a] = i + a < sg.z ? __ldg(dine + i + a) : kNoDense;
-      // lane a < 4 owns item a's t[u] update: its row rank is loaded now,
-      // under the bitmap loads
-      const uint32_t dl = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
-      const uint32_t urow = (kPV && lane < 4 && dl != kNoDense) ? __ldg(drow + dl) : 0u;
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int k = 0; k < kCW; ++k)
-          m[a][k] = (d[a] != kNoDense && P[k]) ? __ldg(cbits + (uint64_t)d[a] * cw + lane + 32 * k) & P[k] : 0u;
+    const uint32_t* cl = cbits + lane;  // this lane's words: + didx * cw + 32 k
+    for (uint32_t base = sg.y; base < sg.z; base += 32) {
+      // 32 items per round: lane l loads item l's dense index (coalesced) and,
+      // per-vertex, its row rank; lane l also owns item l's t[u] update
+      const uint32_t cnt = min(32u, sg.z - base);
+      const uint32_t myd = lane < cnt ? __ldg(dine + base + lane) : kNoDense;
+      const uint32_t myu = (kPV && lane < cnt) ? __ldg(drow + myd) : 0u;
       uint32_t mysum = 0;
+      for (uint32_t a0 = 0; a0 < cnt; a0 += 4) {
+        uint32_t m[4][kCW];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        uint32_t hi = 0;
+        for (int a = 0; a < 4; ++a) {
+          const uint32_t d = __shfl_sync(0xffffffffu, myd, (a0 + a) & 31);
+          const uint32_t* row = cl + d * cw;  // d * cw < 2^32 (ndense * core_words words)
 #pragma unroll
-        for (int k = 0; k < kCW; ++k) hi += __popc(m[a][k]);
-        hseg += hi;
-        if (kPV) {
-          const uint32_t sum = __reduce_add_sync(0xffffffffu, hi);
-          if (lane == (unsigned)a) mysum = sum;
+          for (int k = 0; k < kCW; ++k) m[a][k] = (a0 + a < cnt && P[k]) ? __ldg(row + 32 * k) & P[k] : 0u;
         }
-      }
-      if (kPV && lane < 4 && mysum) atomicAdd(&t_rank[urow], (unsigned long long)mysum);
-      if (kPV) {
 #pragma unroll
-        for (int k = 0; k < kCW; ++k) {
-          // carry-save: c0 + m0 + m1 + m2 + m3 + 2 c1 -> c0 + 2 c1 + 4 k4
-          const uint32_t k1 = maj3(c[0][k], m[0][k], m[1][k]);
-          c[0][k] ^= m[0][k] ^ m[1][k];
-          const uint32_t k2 = maj3(c[0][k], m[2][k], m[3][k]);
-          c[0][k] ^= m[2][k] ^ m[3][k];
-          uint32_t k4 = maj3(c[kPV ? 1 : 0][k], k1, k2);
-          c[kPV ? 1 : 0][k] ^= k1 ^ k2;
+        for (int a = 0; a < 4; ++a) {
+          uint32_t hi = 0;
 #pragma unroll
-          for (int p = 2; p < (kPV ? kPlanes : 1); ++p) {
-            const uint32_t t = c[p][k] & k4;
-            c[p][k] ^= k4;
-            k4 = t;
+          for (int k = 0; k < kCW; ++k) hi += __popc(m[a][k]);
+          hseg += hi;
+          if (kPV) {
+            const uint32_t sum = __reduce_add_sync(0xffffffffu, hi);
+            mysum = lane == a0 + a ? sum : mysum;
           }
         }
-        since += 4;
-        if (since > (1u << kPlanes) - 1 - 4) fold();
+        if (kPV) {
+#pragma unroll
+          for (int k = 0; k < kCW; ++k) {
+            // carry-save: c0 + m0 + m1 + m2 + m3 + 2 c1 -> c0 + 2 c1 + 4 k4
+            const uint32_t k1 = maj3(c[0][k], m[0][k], m[1][k]);
+            c[0][k] ^= m[0][k] ^ m[1][k];
+            const uint32_t k2 = maj3(c[0][k], m[2][k], m[3][k]);
+            c[0][k] ^= m[2][k] ^ m[3][k];
+            uint32_t k4 = maj3(c[kPV ? 1 : 0][k], k1, k2);
+            c[kPV ? 1 : 0][k] ^= k1 ^ k2;
+#pragma unroll
+            for (int p = 2; p < (kPV ? kPlanes : 1); ++p) {
+              const uint32_t t = c[p][k] & k4;
+              c[p][k] ^= k4;
+              k4 = t;
+            }
+          }
+          since += 4;
+          if (since > (1u << kPlanes) - 1 - 4) fold();
+        }
       }
+      if (kPV && mysum) atomicAdd(&t_rank[myu], (unsigned long long)mysum);
     }
     acc += hseg;
     if (kPV) {
@@ -1253,6 +1257,10 @@ constexpr int kRowWarps = 8;
 #endif
 constexpr int kRowULight = TCB_ROWU_LIGHT;  // light rows: a warp each, many warps per SM
 constexpr int kRowUHeavy = 16;  // heavy rows: latency-bound on the byte loads (A/B: profiles/README.md)
+#ifndef TCB_TINY_ITEMS
+#define TCB_TINY_ITEMS 64
+#endif
+constexpr uint32_t kTinyItems = TCB_TINY_ITEMS;  // one-chunk rows folded lane by lane (<= 255)
 // Rows with more item-steps than the threshold go to the CTA-per-row kernel.
 // With many rows the warp-per-row kernel balances rows of up to 2048 steps
 // and runs them faster (C4 whole count: 128 -> 2048 takes the row pass from
@@ -1487,10 +1495,40 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       if (work) {
         const RowMasks rm(dl, Ol, hl);
         const uint32_t C = (uint32_t)(rm.c_hi - rm.c_lo);
-        const uint32_t steps = C > 16 ? (dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
-        if (steps > heavy_thr) {
-          heavy[atomicAdd(nheavy, 1u)] = ul;
+        if (C == 1 && kh - kl <= kTinyItems) {
+          // tiny row: its sparse hot members share one mask chunk, so item k
+          // owns exactly byte k (RowMasks::P(k) = k): the lane folds the
+          // row's kh - kl bytes itself, no warp-serial row step
+          const uint8_t* rowm = masks + rbl;
+          uint32_t lo = 0, hi = 0;
+          for (uint32_t k = kl; k < kh; ++k) {  // <= kTinyItems bytes: no byte-lane overflow
+            const uint2 sp = s_spread[rowm[k]];
+            lo += sp.x;
+            hi += sp.y;
+          }
+          if (lo | hi) {
+            const uint4 q = colH4[rm.c_lo];
+            const uint32_t o7 = (uint32_t)(rm.O & 7);
+            uint32_t tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t cj = ((j < 4 ? lo : hi) >> (8 * (j & 3))) & 0xffu;
+              if (cj && (uint32_t)j >= o7 && (uint32_t)j < o7 + hl) {
+                const uint32_t x = h0 + hot_u16(q, j);
+                if (x >= rc) atomicAdd(&top[x - rc], cj);
+                else atomicAdd(&t_rank[x], (unsigned long long)cj);
+                tot += cj;
+              }
+            }
+            if (tot) atomicAdd(&t_rank[ul], (unsigned long long)tot);
+          }
           work = false;
+        } else {
+          const uint32_t steps = C > 16 ? (dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
+          if (steps > heavy_thr) {
+            heavy[atomicAdd(nheavy, 1u)] = ul;
+            work = false;
+          }
         }
       }
     }
