@@ -389,8 +389,11 @@ def main():
     if world > 1:
         ms = tdist.max_over_ranks(ms)
     T = int(total.item())
-    # phase split (untimed counts with CUDA events) and the work counters
-    stats = [step(stats=True) for _ in range(3)]
+    # per-kernel device times: the same K steps again, CUDA events recorded by
+    # the library around every join kernel on the launch stream (a stats call
+    # also synchronises once at its end, so this is a second timed region,
+    # not the headline one), and the work counters
+    stats = [step(stats=True) for _ in range(max(3, a.steps))]
     sw = tc.count_triangles_into(g, total, pv, tc.MatchOptions(per_vertex=per_vertex, part_index=rank,
                                                                part_count=world),
                                  stats=True, work_counters=True)
@@ -457,13 +460,18 @@ def main():
     peak, peak_kind = peaks()
     alg_bytes = sw["alg_bytes"]          # this rank's share (the parts sum to the graph's B_alg)
     impl_bytes = sw["probe_bytes"]
+    cta_bytes = sw["cta_bytes"]
+    kms = {k: float(np.mean([s_[k + "_ms"] for s_ in stats])) for k in ("warp", "small", "cta", "dense", "rows")}
+    cta_ms = kms["cta"]
     if world > 1:
-        ab = torch.tensor([alg_bytes, impl_bytes], dtype=torch.float64)
+        ab = torch.tensor([alg_bytes, impl_bytes, cta_bytes], dtype=torch.float64)
         dist.all_reduce(ab)
-        alg_bytes, impl_bytes = float(ab[0]), float(ab[1])
-    # roofline of the dominant phase (advance + join + per-vertex row pass):
-    # the bytes the implemented algorithm must stream / its device time
-    achieved = impl_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
+        alg_bytes, impl_bytes, cta_bytes = float(ab[0]), float(ab[1]), float(ab[2])
+        cta_ms = tdist.max_over_ranks(cta_ms)
+    # roofline of the dominant kernel (k_join_cta): its algorithmic bytes per
+    # launch / its average launch duration (library CUDA events, above)
+    achieved = cta_bytes / (cta_ms / 1e3) / 1e9 / max(1, world) if cta_ms > 0 else 0.0
+    phase_achieved = impl_bytes / (join_ms / 1e3) / 1e9 / max(1, world) if join_ms > 0 else 0.0
     traffic, traffic_src = measured_traffic(a.config, "k_join_cta")
     line = {
         "metric": "triangle-count GTEPS (|E|/time)",
@@ -499,11 +507,16 @@ def main():
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic["dram_bytes"] if traffic else None, "traffic_source": traffic_src,
             "peak_kind": peak_kind,
-            "kernel": "join phase: k_join_cta (advance + fused SMEM join, dominant) + k_join_warp/small "
-                      "+ k_pv_rows(_heavy) (per-vertex row pass)",
-            "model": "implemented bytes: 2 B per hot candidate + 4 B per cold candidate + 28 B per in-edge "
-                     "(record + row geometry + pivot-row member) + per-vertex masks written and read + counters",
-            "bytes_per_step": impl_bytes, "join_ms": join_ms,
+            "kernel": "k_join_cta (sparse advance + fused SMEM join, the dominant kernel)",
+            "model": "k_join_cta algorithmic bytes per launch: 2 B per sparse hot candidate + 4 B per cold "
+                     "candidate + 40 B per item (in-edge record + 32-byte row descriptor) + 1 B per per-vertex "
+                     "mask chunk + 4 B per pivot member and 16 B per CTA segment",
+            "bytes_per_launch": cta_bytes, "kernel_ms": cta_ms,
+            "kernels_ms": kms,
+            "join_phase": {"achieved": phase_achieved, "frac": phase_achieved / peak, "bytes_per_step": impl_bytes,
+                           "join_ms": join_ms,
+                           "model": "all join kernels + row pass: 2 B per hot candidate + 4 B per cold candidate "
+                                    "+ 28 B per in-edge + per-vertex masks written and read + counters"},
             "wedges_probed": sw["wedges"],
             "wedge_stream_equiv": {"B_alg": alg_bytes, "W": sw["dag_W"],
                                    "ratio": alg_bytes / (join_ms / 1e3) / 1e9 / peak / max(1, world),

@@ -111,6 +111,20 @@ typedef struct tc_count_stats {
   uint64_t kernel_launches; /* all libtcb200 kernels this call launched */
   uint64_t part_first_vertex; /* this part's pivot rank range [first, last) */
   uint64_t part_last_vertex;
+  /* per-kernel device times of this call (CUDA events around each launch) */
+  double warp_ms;         /* k_join_warp   (pivots with d+ <= 64)            */
+  double small_ms;        /* k_join_small  (pivots with <= 32 in-edges)      */
+  double cta_ms;          /* k_join_cta    (sparse join, the dominant kernel) */
+  double dense_ms;        /* k_join_dense  (dense-core items)                */
+  double rows_ms;         /* k_pv_rows + k_pv_rows_heavy (per-vertex masks)  */
+  /* algorithmic bytes of one launch (work_counters): what the kernel's
+   * algorithm must move -- k_join_cta: 2 B per sparse hot candidate + 4 B per
+   * cold candidate + 40 B per item (in-edge record + row descriptor) + its
+   * per-vertex mask bytes + 4 B per pivot member and 16 B per segment;
+   * k_join_dense: 8 B per dense item (list entry, row rank) + 4 B per core
+   * word of its row + 288 B per segment (pivot descriptor + core words) */
+  double cta_bytes;
+  double dense_bytes;
 } tc_count_stats;
 
 /* ---- graph construction ------------------------------------------------ */

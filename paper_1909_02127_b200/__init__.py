@@ -68,7 +68,9 @@ class TcCountStats(C.Structure):
                 ("wedges", C.c_uint64), ("segments", C.c_uint64), ("join_launches", C.c_uint64),
                 ("dag_W", C.c_double), ("alg_bytes", C.c_double), ("probe_bytes", C.c_double),
                 ("kernel_launches", C.c_uint64), ("part_first_vertex", C.c_uint64),
-                ("part_last_vertex", C.c_uint64)]
+                ("part_last_vertex", C.c_uint64), ("warp_ms", C.c_double), ("small_ms", C.c_double),
+                ("cta_ms", C.c_double), ("dense_ms", C.c_double), ("rows_ms", C.c_double),
+                ("cta_bytes", C.c_double), ("dense_bytes", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -157,6 +157,31 @@ __global__ void k_directed_keys(const uint32_t* __restrict__ src, const uint32_t
   }
 }
 
+// The directed entries whose source id is in [u_lo, u_hi), keyed
+// (source - u_lo) << b | target, appended through one warp-aggregated counter
+// (their order is restored by the sort).
+__global__ void k_directed_keys_range(const uint32_t* __restrict__ src, const uint32_t* __restrict__ col, uint64_t E,
+                                      const uint32_t* __restrict__ id_of, int b, uint32_t u_lo, uint32_t u_hi,
+                                      uint64_t* __restrict__ keys, unsigned long long* __restrict__ cnt) {
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < E; i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t a = 0, c = 0;
+    if (i < E) {
+      a = id_of[src[i]];
+      c = id_of[col[i]];
+    }
+    const bool ka = i < E && a >= u_lo && a < u_hi, kc = i < E && c >= u_lo && c < u_hi;
+    const uint32_t na = __popc(__ballot_sync(0xffffffffu, ka)), nc = __popc(__ballot_sync(0xffffffffu, kc));
+    unsigned long long w = 0;
+    if (lane_id() == 0 && na + nc) w = atomicAdd(cnt, (unsigned long long)(na + nc));
+    w = __shfl_sync(0xffffffffu, w, 0);
+    const uint32_t pa = __popc(__ballot_sync(0xffffffffu, ka) & lanemask_lt());
+    const uint32_t pc = na + __popc(__ballot_sync(0xffffffffu, kc) & lanemask_lt());
+    if (ka) keys[w + pa] = ((uint64_t)(a - u_lo) << b) | c;
+    if (kc) keys[w + pc] = ((uint64_t)(c - u_lo) << b) | a;
+  }
+}
+
 __global__ void k_low_bits(const uint64_t* __restrict__ keys, uint64_t n, int b, uint32_t* __restrict__ out) {
   const uint64_t mask = (b >= 32) ? 0xffffffffull : ((1ull << b) - 1);
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -212,6 +237,7 @@ __global__ void k_hot_scatter(const uint32_t* __restrict__ off, const uint32_t* 
 // runs chunk by chunk behind the host->device copy of the neighbour array
 // (build_from_csr); the row sorts then move every slot to its final place.
 constexpr uint32_t kBigRow = 1024;
+constexpr uint64_t kExportChunk = 1ull << 31;  // directed entries per export sort
 
 __global__ void k_csr_deg(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ deg,
                           uint32_t* __restrict__ big, unsigned int* __restrict__ nbig, int* __restrict__ bad) {
@@ -235,7 +261,7 @@ struct RowCtx {
   const uint32_t* rank_of;
   uint32_t n;
   uint32_t* dplus;
-  const uint32_t* pad_off;  // padded rank-space slots (deg entries each)
+  const uint64_t* pad_off;  // padded rank-space slots (deg entries each; 2E may exceed 2^32)
   uint32_t* pad;
   int strict;  // TRIMCSR1 ingest: also reject self-loops and non-ascending rows (io.cpp:211-216)
 };
@@ -459,7 +485,7 @@ __global__ void k_chunk_bases(const Chunk* __restrict__ chunks, uint32_t nchunks
 // radix fallback.
 struct SlotSort {
   const uint32_t* rank_of;
-  const uint32_t* pad_off;
+  const uint64_t* pad_off;
   uint32_t* pad;
   const uint32_t* dplus;
   uint32_t h0;
@@ -496,7 +522,8 @@ __global__ void __launch_bounds__(256) k_slot_sort_warp(SlotSort ss, uint32_t lo
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint64_t u0 = lo + (uint64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 32; u0 < hi;
        u0 += (uint64_t)warps * 32) {
-    uint32_t r = 0, d = 0, po = 0;
+    uint32_t r = 0, d = 0;
+    uint64_t po = 0;
     if (u0 + lane < hi) {
       r = ss.rank_of[u0 + lane];
       d = ss.dplus[r];
@@ -527,7 +554,8 @@ __global__ void __launch_bounds__(256) k_slot_sort_warp(SlotSort ss, uint32_t lo
     while (mid) {
       const int j = __ffs(mid) - 1;
       mid &= mid - 1;
-      const uint32_t dj = __shfl_sync(0xffffffffu, d, j), pj = __shfl_sync(0xffffffffu, po, j);
+      const uint32_t dj = __shfl_sync(0xffffffffu, d, j);
+      const uint64_t pj = __shfl_sync(0xffffffffu, po, j);
       const uint32_t rj = __shfl_sync(0xffffffffu, r, j);
       uint32_t x = lane < dj ? ss.pad[pj + lane] : 0xffffffffu;
 #pragma unroll
@@ -746,12 +774,13 @@ __global__ void __launch_bounds__(256) k_slot_sort_block(SlotSort ss, const uint
 // walk that range 32 positions at a time (coalesced stores) and find their row
 // by a 5-step search over the group's offsets in SMEM.
 __global__ void __launch_bounds__(256) k_slot_compact(const uint32_t* __restrict__ off,
-                                                      const uint32_t* __restrict__ pad_off,
+                                                      const uint64_t* __restrict__ pad_off,
                                                       const uint32_t* __restrict__ pad, uint32_t n,
                                                       uint32_t* __restrict__ col, uint32_t* __restrict__ src,
                                                       const uint32_t* __restrict__ offH, uint32_t h0,
                                                       uint16_t* __restrict__ colH) {
-  __shared__ uint32_t s_off[8][33], s_po[8][32], s_hb[8][32], s_hs[8][32];
+  __shared__ uint32_t s_off[8][33], s_hb[8][32], s_hs[8][32];
+  __shared__ uint64_t s_po[8][32];
   const unsigned lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint64_t r00 = (uint64_t)(blockIdx.x * (blockDim.x / 32) + w) * 32; r00 < n; r00 += (uint64_t)warps * 32) {
@@ -760,7 +789,8 @@ __global__ void __launch_bounds__(256) k_slot_compact(const uint32_t* __restrict
     const uint32_t o = off[rr];
     s_off[w][lane] = o;
     if (lane == 31) s_off[w][32] = off[r00 + 32 < n ? (uint32_t)(r00 + 32) : n];
-    uint32_t po = 0, hb = 0, hs = 0xffffffffu;
+    uint32_t hb = 0, hs = 0xffffffffu;
+    uint64_t po = 0;
     if (r < n) {
       po = pad_off[rr];
       if (colH) {
@@ -1305,8 +1335,7 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   const int dev = g.device;
   g.n = n;
   g.id_bits = n > 1 ? bits_for((uint64_t)n - 1) : 1;
-  const uint64_t total = 2 * num_edges;
-  if (total >= (1ull << 32)) fail(TC_ERANGE, "CSR with >= 2^32 directed entries");
+  const uint64_t total = 2 * num_edges;  // may exceed 2^32: slot offsets are u64
   if (num_edges >= (1ull << 32)) fail(TC_ERANGE, "graph has >= 2^32 undirected edges (u32 oriented offsets)");
   PhaseLog pl(s);
   // The neighbour array streams in behind everything that needs only the
@@ -1359,8 +1388,9 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
   rank_vertices(g, deg.get());
   deg.release();
   // padded rank-space slots: deg(u) entries each, by rank
-  DBuf<uint32_t> pad_off((uint64_t)nn + 1, s), pad(total ? total : 1, s);
-  scan_exclusive<uint32_t>(LoadArray<uint32_t>{g.deg.get()}, pad_off.get(), n, pad_off.get() + n, s);
+  DBuf<uint64_t> pad_off((uint64_t)nn + 1, s);
+  DBuf<uint32_t> pad(total ? total : 1, s);
+  scan_exclusive<uint64_t>(DegLoad64{g.deg.get()}, pad_off.get(), n, pad_off.get() + n, s);
   DBuf<uint32_t> dplus(nn, s);
   TC_CUDA(cudaMemsetAsync(dplus.get(), 0, sizeof(uint32_t) * nn, s));
   pl.mark("csr_rank");
@@ -1476,7 +1506,37 @@ void export_csr(tc_graph& g, uint64_t* d_off, uint32_t* d_nbrs) {
   }
   scan_exclusive<uint64_t>(DegLoad64{deg.get()}, d_off, n, d_off + n, s);
   if (E == 0) return;
-  if (2 * E >= (1ull << 32)) fail(TC_ERANGE, "export_csr: >= 2^32 directed entries");
+  // > kExportChunk directed entries (TCB_EXPORT_CHUNK for tests): source-id
+  // ranges of at most that many entries, each keyed, sorted and written on
+  // its own (radix_sort_u64 sorts < 2^32 keys)
+  const uint64_t cmax = std::max<uint64_t>(1, std::min<uint64_t>(env_u32("TCB_EXPORT_CHUNK", kExportChunk),
+                                                                 kExportChunk));
+  if (2 * E > cmax) {
+    std::vector<uint64_t> ho((uint64_t)n + 1);
+    TC_CUDA(cudaMemcpyAsync(ho.data(), d_off, ho.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    DBuf<uint64_t> k1(cmax, s), k2(cmax, s);
+    DBuf<unsigned long long> cnt(1, s);
+    uint32_t u_lo = 0;
+    while (u_lo < n) {
+      // largest u_hi with off[u_hi] - off[u_lo] <= cmax (a row longer than cmax alone)
+      uint32_t u_hi = (uint32_t)(std::upper_bound(ho.begin() + u_lo, ho.end(), ho[u_lo] + cmax) - ho.begin()) - 1;
+      if (u_hi <= u_lo) u_hi = u_lo + 1;
+      const uint64_t base = ho[u_lo], m = ho[u_hi] - base;
+      if (m > cmax) fail(TC_ERANGE, "export_csr: a row longer than the export chunk");
+      if (m) {
+        TC_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), s));
+        k_directed_keys_range<<<grid_gs(E, dev), kT, 0, s>>>(g.src.get(), g.col.get(), E, g.id_of.get(), b, u_lo,
+                                                             u_hi, k1.get(), cnt.get());
+        TC_LAUNCH();
+        uint64_t* sorted = radix_sort_u64(k1.get(), k2.get(), m, 0, b + bits_for(u_hi - u_lo - 1 ? u_hi - u_lo - 1 : 1), s);
+        k_low_bits<<<grid_gs(m, dev), kT, 0, s>>>(sorted, m, b, d_nbrs + base);
+        TC_LAUNCH();
+      }
+      u_lo = u_hi;
+    }
+    return;
+  }
   DBuf<uint64_t> k1(2 * E, s), k2(2 * E, s);
   k_directed_keys<<<grid_gs(E, dev), kT, 0, s>>>(g.src.get(), g.col.get(), E, g.id_of.get(), b, k1.get());
   TC_LAUNCH();

@@ -1667,12 +1667,17 @@ T read_scalar(const T* d, cudaStream_t s) {
 }
 
 struct Events {
-  cudaEvent_t e[4];
-  Events() {
-    for (auto& x : e) TC_CUDA(cudaEventCreate(&x));
+  // 0 start, 1 plan done, 2 join done, 3 outputs done; 4..9 around the
+  // join kernels: warp | small | cta | dense | rows
+  cudaEvent_t e[10] = {};
+  bool on = false;
+  explicit Events(bool enable) : on(enable) {  // only a timed call (stats) creates them
+    if (on)
+      for (auto& x : e) TC_CUDA(cudaEventCreate(&x));
   }
   ~Events() {
-    for (auto& x : e) cudaEventDestroy(x);
+    if (on)
+      for (auto& x : e) cudaEventDestroy(x);
   }
   float ms(int a, int b) {
     float t = 0;
@@ -1738,7 +1743,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const uint32_t part = opts.part_count ? opts.part_index : 0;
   const bool pv = d_pv != nullptr;
   const bool timing = stats != nullptr;
-  Events ev;
+  Events ev(timing);
   if (timing) TC_CUDA(cudaEventRecord(ev.e[0], s));
   uint64_t kl = 0;  // kernels launched by this call
   PhaseLog pl(s);
@@ -1782,6 +1787,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const uint32_t nbm = (n - g.h0 + 31) / 32;
   unsigned int* queues = g.scratch[kSlotCounters].get<unsigned int>(16, s) + 4;  // [0..3] = plan.nseg
   TC_CUDA(cudaMemsetAsync(queues, 0, 8 * sizeof(unsigned int), s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[4], s));
   if (plan.cap[0]) {
     // warp bin: plain 32-bit counters over half the window
     const uint32_t ncnt_w = ncnt / 2, rc_w = pv ? n - ncnt_w : 0xffffffffu;
@@ -1795,6 +1801,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
     pl.mark("join_warp");
   }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[5], s));
   // per-hit top counters of the CTA / small bins (no-mask per-vertex mode)
   const uint32_t ncnt_hits = (pv && !kUseMasks) ? std::min<uint32_t>(ncnt, env_u32("TCB_HIT_COUNTERS", 4096)) & ~1u : 0;
   const uint32_t rc_hits = ncnt_hits ? n - ncnt_hits : 0xffffffffu;
@@ -1811,6 +1818,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
     pl.mark("join_small");
   }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[6], s));
   if (plan.cap[1]) {
     // cold members spill to a per-CTA global slab only when a pivot has more
     // than smem_slots/2 members below h0
@@ -1828,6 +1836,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
     pl.mark("join_cta");
   }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[7], s));
   if (g.ndine) {
     // dense core parts: word-parallel intersections (k_join_dense)
     auto kern = pv ? k_join_dense<true> : k_join_dense<false>;
@@ -1839,6 +1848,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
     pl.mark("join_dense");
   }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[8], s));
   if (pv && kUseMasks && n && g.mask_total) {
     // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics); a split
     // count folds only the items of its own pivots
@@ -1865,6 +1875,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     ++launches;
     pl.mark("pv_rows");
   }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[9], s));
   if (timing) TC_CUDA(cudaEventRecord(ev.e[2], s));
 
   // ---- outputs ----
@@ -1886,6 +1897,11 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     stats->kernel_launches = kl + launches;
     stats->part_first_vertex = v_lo;
     stats->part_last_vertex = v_hi;
+    stats->warp_ms = ev.ms(4, 5);
+    stats->small_ms = ev.ms(5, 6);
+    stats->cta_ms = ev.ms(6, 7);
+    stats->dense_ms = ev.ms(7, 8);
+    stats->rows_ms = ev.ms(8, 9);
     if (opts.work_counters) {
       stats->items = plan.items;
       stats->wedges = plan.J;
@@ -1906,6 +1922,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
       // written and read back (1 B per hot chunk, twice) and the u64 counters
       stats->probe_bytes = 2.0 * (double)plan.hot + 4.0 * (double)(plan.J - plan.hot) + 24.0 * Ep +
                            4.0 * Ep + (pv ? 2.0 * (double)g.mask_total + 16.0 * n : 0.0);
+      stats->cta_bytes = plan.cta_bytes;
+      stats->dense_bytes = plan.dense_bytes;
     }
   }
 }

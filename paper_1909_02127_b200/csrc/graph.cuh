@@ -176,6 +176,8 @@ struct Plan {
   uint32_t v_lo = 0, v_hi = 0;
   uint64_t cap[3] = {0, 0, 0};
   uint64_t W = 0, J = 0, hot = 0, items = 0, pivots = 0;  // stats (read_plan_sums)
+  double cta_bytes = 0, dense_bytes = 0;  // per-kernel algorithmic bytes (tc_count_stats)
+  uint32_t core_words = 0;
   void* sums = nullptr;
 };
 // Returns the number of kernels launched.

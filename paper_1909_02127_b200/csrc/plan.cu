@@ -32,6 +32,8 @@ unsigned grid_gs(uint64_t n, int device) {
 
 struct Sums {
   unsigned long long W, J, hot, items, pivots;
+  unsigned long long cta_hot, cta_cold, cta_items, cta_mask, cta_seg_members, cta_segs;
+  unsigned long long dense_items, dense_segs;
 };
 
 __global__ void k_plan_class(PivotClass pc, uint32_t v_lo, uint32_t v_hi, uint8_t* __restrict__ cls) {
@@ -92,17 +94,30 @@ __global__ void k_plan_segs(const uint8_t* __restrict__ cls, const uint32_t* __r
 // its suffix length (J), hot share and usefulness (edge-parallel over the
 // in-edge index), per pivot W = din * d+ (SURVEY 8d wedge stream) and
 // whether it has work.
-__global__ void k_plan_work(const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0,
-                            const uint32_t* __restrict__ inoff, const uint2* __restrict__ ine, uint32_t v_lo,
+// k_join_cta's and k_join_dense's algorithmic work of the part (tc_count_stats
+// cta_bytes / dense_bytes): per CTA-bin item its sparse hot and cold
+// candidates and mask bytes, per CTA segment the pivot row it stages; dense
+// items and segments.
+__global__ void k_plan_work(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, PivotClass pc,
+                            const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ inoff,
+                            const uint2* __restrict__ ine, const uint32_t* __restrict__ dsoff, uint32_t v_lo,
                             uint32_t v_hi, Sums* __restrict__ sums) {
   unsigned long long W = 0, J = 0, H = 0, I = 0, P = 0;
+  unsigned long long ch = 0, cc = 0, ci = 0, cm = 0, csm = 0, cs = 0, di = 0, ds = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t v = v_lo + t0; v < v_hi; v += stride) {
     const uint32_t dv = off[v + 1] - off[v], din = inoff[v + 1] - inoff[v];
+    if (dsoff) ds += dsoff[v + 1] - dsoff[v];
     if (!dv || !din) continue;
     W += (unsigned long long)dv * din;
     ++P;
+    uint32_t d2 = 0;
+    if (pc((uint32_t)v, d2) == 1) {
+      const uint32_t ns = (din + kCtaSegItems - 1) / kCtaSegItems;
+      cs += ns;
+      csm += (unsigned long long)ns * dv;
+    }
   }
   const uint32_t i_lo = inoff[v_lo], i_hi = inoff[v_hi];
   for (uint64_t i = i_lo + t0; i < i_hi; i += stride) {
@@ -113,18 +128,26 @@ __global__ void k_plan_work(const uint32_t* __restrict__ off, const uint4* __res
     const uint32_t suf = rd.end - eu.x - 1, h = rd.h();
     J += suf;
     H += suf < h ? suf : h;
+    if (rd.didx != kNoDense) ++di;
+    uint32_t din = 0;
+    if (pc(col[eu.x], din) == 1) {
+      // the CTA bin's share: sparse hot part [hb, Ht) of colH, cold part
+      const uint32_t a = eu.x + 1, ce = rd.cold_end();
+      const uint32_t hb = a >= ce ? rd.O + (a - ce) : rd.O;
+      if (rd.Ht > hb) {
+        ch += rd.Ht - hb;
+        cm += ((rd.Ht + 7) >> 3) - (hb >> 3);
+      }
+      if (ce > a) cc += ce - a;
+      ++ci;
+    }
   }
-  W = warp_sum(W);
-  J = warp_sum(J);
-  H = warp_sum(H);
-  I = warp_sum(I);
-  P = warp_sum(P);
-  if (lane_id() == 0) {
-    if (W) atomicAdd(&sums->W, W);
-    if (J) atomicAdd(&sums->J, J);
-    if (H) atomicAdd(&sums->hot, H);
-    if (I) atomicAdd(&sums->items, I);
-    if (P) atomicAdd(&sums->pivots, P);
+  unsigned long long* dst = &sums->W;
+  unsigned long long vals[13] = {W, J, H, I, P, ch, cc, ci, cm, csm, cs, di, ds};
+#pragma unroll
+  for (int k = 0; k < 13; ++k) {
+    const unsigned long long x = warp_sum(vals[k]);
+    if (lane_id() == 0 && x) atomicAdd(dst + k, x);
   }
 }
 
@@ -139,6 +162,7 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
   v_lo = v_lo < g.r0 ? (g.r0 < v_hi ? g.r0 : v_hi) : v_lo;  // isolated ranks [0, r0) have no work
   p.v_lo = v_lo;
   p.v_hi = v_hi;
+  p.core_words = g.core_words;
   const uint32_t np = v_hi - v_lo;
   p.nseg = g.scratch[kSlotCounters].get<uint32_t>(16, s);  // [0..3] segment counts, [4..11] join queues
   for (int c = 0; c < 3; ++c) p.cap[c] = g.seg_cap[c];
@@ -175,8 +199,9 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
     Sums* sums = g.scratch[kSlotSums].get<Sums>(1, s);
     TC_CUDA(cudaMemsetAsync(sums, 0, sizeof(Sums), s));
     if (np) {
-      k_plan_work<<<(unsigned)num_sms(dev) * 8, kT, 0, s>>>(g.off.get(), g.rowd.get(), g.r0, g.inoff.get(), g.ine.get(),
-                                                           v_lo, v_hi, sums);
+      k_plan_work<<<(unsigned)num_sms(dev) * 8, kT, 0, s>>>(
+          g.off.get(), g.col.get(), PivotClass{g.off.get(), g.offH.get(), g.inoff.get(), masks}, g.rowd.get(), g.r0,
+          g.inoff.get(), g.ine.get(), g.ndine ? g.dsoff.get() : nullptr, v_lo, v_hi, sums);
       TC_LAUNCH();
     }
     p.sums = sums;
@@ -194,6 +219,10 @@ void read_plan_sums(Plan& p, cudaStream_t s) {
   p.hot = h.hot;
   p.items = h.items;
   p.pivots = h.pivots;
+  p.cta_bytes = 2.0 * h.cta_hot + 4.0 * h.cta_cold + 40.0 * h.cta_items + (p.masks ? (double)h.cta_mask : 0.0) +
+                4.0 * h.cta_seg_members + 16.0 * h.cta_segs;
+  p.dense_bytes = (p.masks ? 8.0 : 4.0) * h.dense_items + 4.0 * p.core_words * h.dense_items +
+                  (32.0 + 4.0 * p.core_words) * h.dense_segs;
 }
 
 }  // namespace tcb

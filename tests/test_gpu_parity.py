@@ -107,6 +107,32 @@ def test_build_graph_csr_parity_random(tc, oracle, cuda_ok):
         assert np.array_equal(ro, off) and np.array_equal(nbr, nb), i
 
 
+def test_export_csr_chunked(tc, oracle, cuda_ok):
+    """tc_graph_export_csr by source-id ranges (the path graphs with >= 2^31
+    directed entries take; TCB_EXPORT_CHUNK shrinks the range here)."""
+    rng = np.random.default_rng(13)
+    old = os.environ.get("TCB_EXPORT_CHUNK")
+    try:
+        for i, chunk in enumerate(("1000", "4096", "1")):
+            os.environ["TCB_EXPORT_CHUNK"] = chunk
+            n = int(rng.integers(50, 3000))
+            m = int(rng.integers(n, 12 * n))
+            pairs = rng.integers(0, n, 2 * m).astype(np.uint32)
+            off, nb, E, _, _ = oracle.build_graph(pairs, n)
+            g = tc.build_graph_from_pairs(pairs, n)
+            if chunk == "1" and int(np.diff(off).max()) > 1:
+                with pytest.raises(IndexError):
+                    g.export_csr()
+                continue
+            ro, nbr = g.export_csr()
+            assert np.array_equal(ro, off) and np.array_equal(nbr, nb), i
+    finally:
+        if old is None:
+            os.environ.pop("TCB_EXPORT_CHUNK", None)
+        else:
+            os.environ["TCB_EXPORT_CHUNK"] = old
+
+
 def _stress_graphs():
     # hubs / cliques: force every bin, large tables and the global-table path
     out = {}

@@ -45,7 +45,8 @@ def main():
                       "kernel": name[:120]}
     with open(os.path.join(ROOT, "paper_1909_02127_b200", "libtcb200.so"), "rb") as f:
         sha = hashlib.sha256(f.read()).hexdigest()
-    git = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
+    git = os.environ.get("GIT_HEAD") or subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"],
+                                                       capture_output=True, text=True).stdout.strip()
     doc = {"config": config, "lib_sha256": sha, "git_head": git or None, "report": os.path.basename(rep),
            "kernels": out}
     # written next to the report (gpurun_out/ travels back); copy it into
