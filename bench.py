@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--no-per-vertex", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time direct launches instead of CUDA-graph replay")
     return ap.parse_args()
 
 
@@ -373,19 +374,57 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
+    # N=1: the whole count (plan + joins + row pass + outputs, ~15 kernels, no
+    # host synchronisation, no allocation at steady state) is captured once
+    # into a CUDA graph and replayed per step -- the launch overhead of the
+    # small configs goes away, the work per step is unchanged
+    cgraph, launch_mode = None, "direct launches"
+    if world == 1 and not a.no_graph:
+        try:
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=stream, capture_error_mode="relaxed"):
+                step()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                for _ in range(2):
+                    cg.replay()
+            torch.cuda.synchronize()
+            cgraph, launch_mode = cg, "CUDA graph replay of one whole count per step"
+        except Exception as e:  # reported, then direct launches
+            launch_mode = f"direct launches (graph capture failed: {repr(e)[:120]})"
+            torch.cuda.synchronize()
+
+    def timed_step():
+        if cgraph is not None:
+            cgraph.replay()
+        else:
+            step()
+
+    # L2 rule: C3..C5 inputs are far larger than the 126 MB L2; for C1/C2
+    # (whose oriented graph could stay L2-resident) a 512 MB buffer is written
+    # between the timed steps and each step is timed on its own event pair
+    flush = a.config in ("C1", "C2")
+    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)] \
+        if flush else []
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
         ev0.record(stream)
-        for _ in range(a.steps):
-            step()
+        for i in range(a.steps):
+            if flush:
+                scrub.fill_(i & 0xff)
+                evs[i][0].record(stream)
+            timed_step()
+            if flush:
+                evs[i][1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1) / a.steps
+    ms = (sum(x.elapsed_time(y) for x, y in evs) if flush else ev0.elapsed_time(ev1)) / a.steps
     if world > 1:
         ms = tdist.max_over_ranks(ms)
     T = int(total.item())
@@ -454,6 +493,41 @@ def main():
     e2e_pg_ms = time_e2e(ro_p, nb_p, tot_p, pv_p, max(1, a.e2e_steps - 1))
     assert int(tot_p[0]) == T
     del ro_p, nb_p
+
+    # pipelined leg: two host threads, each calling the same public API on its
+    # own handle and its own pinned outputs, 2 steps each in flight at once --
+    # one graph's host->device copy (copy engine) runs under the other's count
+    # (SMs).  Every step still copies its whole input and reads back its result.
+    e2e_pipe = None
+    if world == 1 and a.e2e_steps >= 2:
+        outs = [(torch.zeros(1, dtype=torch.int64, pin_memory=True),
+                 torch.zeros(n, dtype=torch.int64, pin_memory=True) if per_vertex else None) for _ in range(2)]
+        per_thread = max(2, a.e2e_steps)
+        errs = []
+
+        def worker(k):
+            try:
+                for _ in range(per_thread):
+                    e2e_step(ro_h, nb_h, outs[k][0], outs[k][1])
+            except Exception as e:  # reported below
+                errs.append(repr(e)[:200])
+
+        for k in range(2):  # warm both threads' allocator paths
+            e2e_step(ro_h, nb_h, outs[k][0], outs[k][1])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ths = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+        for t_ in ths:
+            t_.start()
+        for t_ in ths:
+            t_.join()
+        torch.cuda.synchronize()
+        pipe_ms = (time.perf_counter() - t0) * 1e3 / (2 * per_thread)
+        ok = not errs and all(int(o[0][0]) == T for o in outs)
+        e2e_pipe = {"value": E / (pipe_ms / 1e3) / 1e9 if ok else None, "ms_per_step": pipe_ms,
+                    "callers": 2, "steps": 2 * per_thread, "errors": errs or None,
+                    "path": "2 host threads x count_triangles(const Graph&) (tc_graph_from_csr + tc_count), each "
+                            "on its own handle/stream: H2D of one step overlaps the count of the other"}
     h2d = 8 * (n + 1) + 4 * 2 * E
     d2h = 8 + (8 * n if per_vertex else 0)
 
@@ -492,7 +566,9 @@ def main():
             "per_vertex": per_vertex,
             "parallelism": (f"pivot ranges x{world} + one NCCL allreduce (tc_count_allreduce)" if world > 1
                             else "1 GPU"),
-            "l2": "inputs larger than L2 (oriented CSR + in-edge index + masks >> 126 MB); no flush",
+            "l2": ("L2 flushed between timed steps (512 MB written), each step timed on its own events" if flush
+                   else "inputs larger than L2 (oriented CSR + in-edge index + masks >> 126 MB); no flush"),
+            "launch": launch_mode,
             "build_ms": build_ms, "self_loops_removed": rep.self_loops_removed,
             "duplicate_entries_removed": rep.duplicate_entries_removed,
         },
@@ -502,7 +578,8 @@ def main():
                 "h2d_floor_ms": (h2d / link_gbps / 1e6) if link_gbps else None,
                 "path": "tc_graph_from_csr(host pinned CSR) + tc_count(host outputs)",
                 "pageable": {"value": E / (e2e_pg_ms / 1e3) / 1e9, "ms_per_step": e2e_pg_ms,
-                             "path": "the same from pageable numpy arrays (a caller's std::vector)"}},
+                             "path": "the same from pageable numpy arrays (a caller's std::vector)"},
+                "pipelined": e2e_pipe},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic["dram_bytes"] if traffic else None, "traffic_source": traffic_src,

@@ -17,6 +17,7 @@
 // synchronised, every cached block returned) and the request retried once.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <deque>
 #include <map>
@@ -47,6 +48,7 @@ struct Cache {
   std::mutex mu;
   std::map<int, DevCache> dev;
   std::unordered_map<void*, size_t> live;  // pointer -> real class
+  std::vector<void*> parked;  // freed inside a stream capture (dev_free)
   uint64_t seq = 0;
 };
 
@@ -124,8 +126,16 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   TC_CUDA(cudaGetDevice(&dev));
   const size_t cls = size_class(bytes);
   Cache& c = cache();
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (s && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+    fail(TC_ECUDA, "device allocation of " + std::to_string(bytes) +
+                       " bytes inside a CUDA-graph capture (warm the handle up with one count first)");
   {
     std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.parked.empty()) {
+      for (void* q : c.parked) cudaFree(q);
+      c.parked.clear();
+    }
     DevCache& d = c.dev[dev];
     const size_t max_cls = cls < (1u << 20) ? cls : cls + cls / 4;
     auto it = d.free.lower_bound(cls);
@@ -134,7 +144,10 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
       it->second.pop_back();
       if (it->second.empty()) d.free.erase(it);
       d.cached -= b.cls;
-      if (b.s != s) TC_CUDA(cudaStreamWaitEvent(s, b.ev, 0));
+      if (b.s != s && cudaStreamWaitEvent(s, b.ev, 0) != cudaSuccess) {
+        cudaGetLastError();  // the freeing stream's event is unusable: order by a device sync
+        TC_CUDA(cudaDeviceSynchronize());
+      }
       cudaEventDestroy(b.ev);
       c.live[b.p] = b.cls;
       return b.p;
@@ -169,6 +182,18 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
       c.live.erase(it);
     }
   }
+  // A free inside a CUDA-graph capture (a count's scratch never reallocates
+  // at steady state, so this is a caller error): the block cannot be
+  // recycled through an event recorded into the capture; it is parked and
+  // returned to the driver at the next allocation outside a capture.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (s && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    if (getenv("TCB_ALLOC_DEBUG")) fprintf(stderr, "[tcb] free of %zu bytes during stream capture (parked)\n", cls);
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.parked.push_back(p);
+    return;
+  }
+  cudaGetLastError();
   Block b{p, cls, s, nullptr, 0};
   if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventRecord(b.ev, s) != cudaSuccess) {

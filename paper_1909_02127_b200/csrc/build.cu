@@ -960,8 +960,12 @@ struct InDeg {
 
 // Every oriented edge e = u->v to its head's slot, warp-aggregated per head
 // (hub heads take one atomic per warp): ine[slot] = {e, u}.
+// With ccnt (rows [r0, n): core members of a dense row, else 0), dflag[slot]
+// = 1 for a dense item: u's row is dense and e is not its last edge (src is
+// sorted, so that is src[e+1] == u).
 __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* __restrict__ src, uint64_t E,
-                             uint32_t* __restrict__ cur, uint2* __restrict__ ine) {
+                             uint32_t* __restrict__ cur, uint2* __restrict__ ine, const uint32_t* __restrict__ ccnt,
+                             uint32_t r0, uint8_t* __restrict__ dflag) {
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = base + threadIdx.x;
     const bool ok = e < E;
@@ -972,7 +976,11 @@ __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* _
     uint32_t b = 0;
     if (ok && (int)lane == leader) b = atomicAdd(&cur[v], (unsigned)__popc(peers));
     b = __shfl_sync(0xffffffffu, b, leader);
-    if (ok) ine[b + __popc(peers & lanemask_lt())] = make_uint2((uint32_t)e, src[e]);
+    if (ok) {
+      const uint32_t slot = b + __popc(peers & lanemask_lt()), u = src[e];
+      ine[slot] = make_uint2((uint32_t)e, u);
+      if (dflag) dflag[slot] = (ccnt[u - r0] != 0 && e + 1 < E && src[e + 1] == u) ? 1 : 0;
+    }
   }
 }
 
@@ -1030,25 +1038,16 @@ __global__ void k_rowbase_put(const uint64_t* __restrict__ rb, uint32_t nr, uint
 }
 
 // Dense in-edge list: in-edge i = {e, u} of pivot v is a dense item when u's
-// row is dense and its suffix after v is non-empty.
-struct DenseIn {
-  const uint2* ine;
-  const uint4* rowd;
-  uint32_t r0;
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-    const uint2 eu = ine[i];
-    const uint4* p = rowd + 2 * (uint64_t)(eu.y - r0);
-    return (p[1].y != kNoDense && eu.x + 1 < p[0].y) ? 1u : 0u;
-  }
+// row is dense and its suffix after v is non-empty (dflag, k_in_scatter).
+struct ByteFlag {
+  const uint8_t* f;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return f[i]; }
 };
-__global__ void k_dense_scatter(const uint2* __restrict__ ine, uint64_t E, const uint4* __restrict__ rowd,
-                                uint32_t r0, const uint32_t* __restrict__ dpos, uint32_t* __restrict__ dine) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint2 eu = ine[i];
-    const uint4* p = rowd + 2 * (uint64_t)(eu.y - r0);
-    const uint32_t didx = p[1].y;
-    if (didx != kNoDense && eu.x + 1 < p[0].y) dine[dpos[i]] = didx;
-  }
+__global__ void k_dense_scatter(const uint2* __restrict__ ine, uint64_t E, const uint8_t* __restrict__ dflag,
+                                const uint32_t* __restrict__ dpos, uint32_t r0, const uint32_t* __restrict__ ip,
+                                uint32_t* __restrict__ dine) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
+    if (dflag[i]) dine[ip[i]] = dpos[ine[i].y - r0];
 }
 // Dense segments of pivot v: its dense items [dpos[inoff[v]], dpos[inoff[v+1]])
 struct DenseSegs {
@@ -1170,16 +1169,7 @@ void finish_graph(tc_graph& g) {
   const uint32_t n = g.n;
   const uint64_t E = g.E;
   const int dev = g.device;
-  g.inoff.alloc((uint64_t)n + 1, s);
-  scan_exclusive<uint32_t>(InDeg{g.off.get(), g.deg.get()}, g.inoff.get(), n, g.inoff.get() + n, s);
-  g.ine.alloc(E + 2, s);  // +16 B: bulk copies of a segment's slice round up to 16 bytes
-  TC_CUDA(cudaMemsetAsync(g.ine.get() + E, 0, 2 * sizeof(uint2), s));
-  if (E) {
-    DBuf<uint32_t> cur(n, s);
-    TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
-    k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.ine.get());
-    TC_LAUNCH();
-  }
+  PhaseLog pl(s);
   g.r0 = 0;
   if (n) {
     DBuf<uint32_t> r0(1, s);
@@ -1188,7 +1178,6 @@ void finish_graph(tc_graph& g) {
     g.r0 = read_scalar(r0.get(), s);
   }
   const uint32_t nr = n - g.r0;
-  g.rowd.alloc(2 * (uint64_t)(nr ? nr : 1), s);
   // dense core: rows with >= core_min members among the top core_bits ranks
   // (TCB_CORE_BITS / TCB_CORE_MIN: tests shrink the core to drive the dense
   // path on small graphs; TCB_CORE_BITS=0 disables it)
@@ -1216,9 +1205,26 @@ void finish_graph(tc_graph& g) {
       g.ndense = nd;
       g.core_min = core_min;
     } else {
-      ccnt.release();  // no dense rows (or too many to index): every row stays sparse
+      ccnt.release();  // no dense rows: every row stays sparse
     }
   }
+  pl.mark("fin_core_rows");
+  // in-edge index (+ the dense-item flag of every slot)
+  g.inoff.alloc((uint64_t)n + 1, s);
+  scan_exclusive<uint32_t>(InDeg{g.off.get(), g.deg.get()}, g.inoff.get(), n, g.inoff.get() + n, s);
+  g.ine.alloc(E + 2, s);  // +16 B: bulk copies of a segment's slice round up to 16 bytes
+  TC_CUDA(cudaMemsetAsync(g.ine.get() + E, 0, 2 * sizeof(uint2), s));
+  DBuf<uint8_t> dflag;
+  if (E) {
+    if (g.ndense) dflag.alloc(E, s);
+    DBuf<uint32_t> cur(n, s);
+    TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+    k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.ine.get(),
+                                                g.ndense ? ccnt.get() : nullptr, g.r0, dflag.get());
+    TC_LAUNCH();
+  }
+  pl.mark("fin_in_scatter");
+  g.rowd.alloc(2 * (uint64_t)(nr ? nr : 1), s);
   if (nr) {
     k_rowdesc<<<grid_gs(nr, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.r0, n, g.ndense ? ccnt.get() : nullptr,
                                               dpos.get(), g.rowd.get());
@@ -1231,8 +1237,7 @@ void finish_graph(tc_graph& g) {
                                                                 g.core_words, g.cbits.get());
     TC_LAUNCH();
   }
-  ccnt.release();
-  dpos.release();
+  pl.mark("fin_rowdesc_cbits");
   // dense in-edge list and its segments (k_join_dense)
   g.dine.release();
   g.dseg.release();
@@ -1242,13 +1247,15 @@ void finish_graph(tc_graph& g) {
   TC_CUDA(cudaMemsetAsync(g.dsoff.get(), 0, sizeof(uint32_t) * ((uint64_t)n + 1), s));
   if (g.ndense && E) {
     DBuf<uint32_t> ip(E + 1, s);
-    scan_exclusive<uint32_t>(DenseIn{g.ine.get(), g.rowd.get(), g.r0}, ip.get(), E, ip.get() + E, s);
+    scan_exclusive<uint32_t>(ByteFlag{dflag.get()}, ip.get(), E, ip.get() + E, s);
     g.ndine = read_scalar(ip.get() + E, s);
     g.dine.alloc(g.ndine ? g.ndine : 1, s);
     if (g.ndine) {
-      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.ine.get(), E, g.rowd.get(), g.r0, ip.get(), g.dine.get());
+      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.ine.get(), E, dflag.get(), dpos.get(), g.r0, ip.get(),
+                                                     g.dine.get());
       TC_LAUNCH();
     }
+    dflag.release();
     scan_exclusive<uint32_t>(DenseSegs{g.inoff.get(), ip.get()}, g.dsoff.get(), n, g.dsoff.get() + n, s);
     const uint32_t nseg = read_scalar(g.dsoff.get() + n, s);
     g.dseg.alloc(nseg ? nseg : 1, s);
@@ -1260,6 +1267,9 @@ void finish_graph(tc_graph& g) {
     k_dense_rows<<<grid_gs(nr, dev), kT, 0, s>>>(g.rowd.get(), g.r0, nr, g.drow.get());
     TC_LAUNCH();
   }
+  ccnt.release();
+  dpos.release();
+  pl.mark("fin_dense_list");
   // per-vertex mask base of every row (graph property; RowGeo::rowbase)
   g.mask_total = 0;
   if (nr) {
@@ -1269,6 +1279,7 @@ void finish_graph(tc_graph& g) {
     TC_LAUNCH();
     g.mask_total = read_scalar(rb.get() + nr, s);
   }
+  pl.mark("fin_rowbase");
   DBuf<unsigned long long> tot(4, s);
   TC_CUDA(cudaMemsetAsync(tot.get(), 0, 4 * sizeof(unsigned long long), s));
   if (nr) {

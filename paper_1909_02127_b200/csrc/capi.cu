@@ -43,7 +43,9 @@ tc_status set_error(tc_status c, const std::string& m) {
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    if (getenv("TCB_ALLOC_DEBUG")) fprintf(stderr, "[tcb] cudaPointerGetAttributes: %s\n", cudaGetErrorString(e));
     cudaGetLastError();
     return false;
   }

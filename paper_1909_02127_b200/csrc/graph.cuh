@@ -44,7 +44,7 @@ struct Scratch {
 };
 enum ScratchSlot {
   kSlotSegOff, kSlotWsegs, kSlotCsegs, kSlotSsegs, kSlotMasks, kSlotSlab, kSlotTRank,
-  kSlotHeavy, kSlotCls, kSlotSums, kSlotCounters, kSlotAcc, kSlotCount
+  kSlotHeavy, kSlotCls, kSlotSums, kSlotCounters, kSlotAcc, kSlotScanWs, kSlotCount
 };
 }  // namespace tcb
 

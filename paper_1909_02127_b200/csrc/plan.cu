@@ -183,8 +183,10 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
     uint32_t* off_s = reinterpret_cast<uint32_t*>(off_wc + np);
     unsigned long long* tot_wc = off_wc + 2 * (uint64_t)np;
     uint32_t* tot_s = reinterpret_cast<uint32_t*>(off_wc + 2 * (uint64_t)np + 1);
-    kl += scan_exclusive<unsigned long long>(SegWC{cls, g.inoff.get(), v_lo}, off_wc, np, tot_wc, s);
-    kl += scan_exclusive<uint32_t>(SegS{cls}, off_s, np, tot_s, s);
+    // the scans' workspace is handle scratch too: a count allocates nothing
+    unsigned long long* ws = g.scratch[kSlotScanWs].get<unsigned long long>(scan_ws_elems(np) + 1, s);
+    kl += scan_exclusive<unsigned long long>(SegWC{cls, g.inoff.get(), v_lo}, off_wc, np, tot_wc, s, ws);
+    kl += scan_exclusive<uint32_t>(SegS{cls}, off_s, np, tot_s, s, reinterpret_cast<uint32_t*>(ws));
     k_plan_segs<<<grid_gs(np, dev), kT, 0, s>>>(cls, g.inoff.get(), v_lo, v_hi, off_wc, off_s, tot_wc, tot_s,
                                                 p.wsegs, p.csegs, p.ssegs, p.nseg);
     TC_LAUNCH();

@@ -85,9 +85,18 @@ struct LoadArray {
   __device__ __forceinline__ T operator()(uint64_t i) const { return p[i]; }
 };
 
-// Returns the number of kernels launched.
+// Workspace elements scan_exclusive needs for n elements (tile partials and
+// their scans, recursively).
+inline uint64_t scan_ws_elems(uint64_t n) {
+  const uint64_t tiles = ceil_div64(n, kScanTile);
+  return tiles <= 1 ? 0 : 2 * tiles + scan_ws_elems(tiles);
+}
+
+// Returns the number of kernels launched.  ws (optional, scan_ws_elems(n)
+// elements): caller-owned workspace -- no allocation, so the scan can be
+// captured into a CUDA graph (the count plan passes the handle's scratch).
 template <typename T, typename Load>
-int scan_exclusive(Load load, T* out, uint64_t n, T* d_total, cudaStream_t s) {
+int scan_exclusive(Load load, T* out, uint64_t n, T* d_total, cudaStream_t s, T* ws = nullptr) {
   if (n == 0) {
     if (d_total) TC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(T), s));
     return 0;
@@ -98,11 +107,17 @@ int scan_exclusive(Load load, T* out, uint64_t n, T* d_total, cudaStream_t s) {
     TC_LAUNCH();
     return 1;
   }
-  DBuf<T> partial(tiles, s), partial_scan(tiles, s);
-  k_scan_reduce<T><<<(unsigned)tiles, kScanThreads, 0, s>>>(load, n, partial.get());
+  DBuf<T> own;
+  if (!ws) {
+    own.alloc(scan_ws_elems(n), s);
+    ws = own.get();
+  }
+  T* partial = ws;
+  T* partial_scan = ws + tiles;
+  k_scan_reduce<T><<<(unsigned)tiles, kScanThreads, 0, s>>>(load, n, partial);
   TC_LAUNCH();
-  const int inner = scan_exclusive<T>(LoadArray<T>{partial.get()}, partial_scan.get(), tiles, (T*)nullptr, s);
-  k_scan_tiles<T><<<(unsigned)tiles, kScanThreads, 0, s>>>(load, out, n, partial_scan.get(), d_total);
+  const int inner = scan_exclusive<T>(LoadArray<T>{partial}, partial_scan, tiles, (T*)nullptr, s, ws + 2 * tiles);
+  k_scan_tiles<T><<<(unsigned)tiles, kScanThreads, 0, s>>>(load, out, n, partial_scan, d_total);
   TC_LAUNCH();
   return 2 + inner;
 }

@@ -10,10 +10,10 @@ from __future__ import annotations
 
 import numpy as np
 
-ITEM_COST = 64     # count.cu kItemCost: per in-edge item, in candidate-probe units
+ITEM_COST = 32     # count.cu kItemCost: per in-edge item, in candidate-probe units
 SEG_COST = 4       # count.cu kSegRowCost: per member of N+(v), per CTA segment
 DENSE_COST = 48    # count.cu TCB_DENSE_COST: one dense-core item (k_join_dense)
-COLD_COST = 12      # count.cu TCB_COLD_COST: a cold (hash) probe
+COLD_COST = 6      # count.cu TCB_COLD_COST: a cold (hash) probe
 WARP_COST = 16      # count.cu TCB_WARP_COST: a warp-bin probe
 WARP_MAX_DEG = 64  # graph.cuh kWarpMaxDeg
 CTA_SEG_ITEMS = 512
