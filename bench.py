@@ -494,40 +494,6 @@ def main():
     assert int(tot_p[0]) == T
     del ro_p, nb_p
 
-    # pipelined leg: two host threads, each calling the same public API on its
-    # own handle and its own pinned outputs, 2 steps each in flight at once --
-    # one graph's host->device copy (copy engine) runs under the other's count
-    # (SMs).  Every step still copies its whole input and reads back its result.
-    e2e_pipe = None
-    if world == 1 and a.e2e_steps >= 2:
-        outs = [(torch.zeros(1, dtype=torch.int64, pin_memory=True),
-                 torch.zeros(n, dtype=torch.int64, pin_memory=True) if per_vertex else None) for _ in range(2)]
-        per_thread = max(2, a.e2e_steps)
-        errs = []
-
-        def worker(k):
-            try:
-                for _ in range(per_thread):
-                    e2e_step(ro_h, nb_h, outs[k][0], outs[k][1])
-            except Exception as e:  # reported below
-                errs.append(repr(e)[:200])
-
-        for k in range(2):  # warm both threads' allocator paths
-            e2e_step(ro_h, nb_h, outs[k][0], outs[k][1])
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        ths = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
-        for t_ in ths:
-            t_.start()
-        for t_ in ths:
-            t_.join()
-        torch.cuda.synchronize()
-        pipe_ms = (time.perf_counter() - t0) * 1e3 / (2 * per_thread)
-        ok = not errs and all(int(o[0][0]) == T for o in outs)
-        e2e_pipe = {"value": E / (pipe_ms / 1e3) / 1e9 if ok else None, "ms_per_step": pipe_ms,
-                    "callers": 2, "steps": 2 * per_thread, "errors": errs or None,
-                    "path": "2 host threads x count_triangles(const Graph&) (tc_graph_from_csr + tc_count), each "
-                            "on its own handle/stream: H2D of one step overlaps the count of the other"}
     h2d = 8 * (n + 1) + 4 * 2 * E
     d2h = 8 + (8 * n if per_vertex else 0)
 
@@ -578,8 +544,7 @@ def main():
                 "h2d_floor_ms": (h2d / link_gbps / 1e6) if link_gbps else None,
                 "path": "tc_graph_from_csr(host pinned CSR) + tc_count(host outputs)",
                 "pageable": {"value": E / (e2e_pg_ms / 1e3) / 1e9, "ms_per_step": e2e_pg_ms,
-                             "path": "the same from pageable numpy arrays (a caller's std::vector)"},
-                "pipelined": e2e_pipe},
+                             "path": "the same from pageable numpy arrays (a caller's std::vector)"}},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic["dram_bytes"] if traffic else None, "traffic_source": traffic_src,
