@@ -286,6 +286,21 @@ def measured_reference_counts(configs=("C1", "C2")):
     return out
 
 
+def build_inputs_sha256(root):
+    """sha256 over the library's build inputs (csrc sources, headers,
+    Makefile, include/): the same sources build the same kernels, while the
+    .so itself is not byte-reproducible across clean builds."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in (os.path.join(root, "paper_1909_02127_b200", "csrc"), os.path.join(root, "include")):
+        for name in sorted(os.listdir(d)):
+            if name.endswith((".cu", ".cuh", ".h", ".hpp", ".cpp")) or name == "Makefile":
+                h.update(name.encode())
+                with open(os.path.join(d, name), "rb") as f:
+                    h.update(f.read())
+    return h.hexdigest()
+
+
 def lib_sha256():
     import hashlib
     h = hashlib.sha256()
@@ -297,14 +312,15 @@ def lib_sha256():
 def measured_traffic(config: str, kernel: str):
     """DRAM bytes per launch of the dominant kernel from the ncu capture made
     for THIS build (profiles/ncu_traffic_<config>.json, written by
-    tools/ncu_traffic.py with the library's sha256); None when stale/absent."""
+    tools/ncu_traffic.py with the sha256 of the library's build inputs); None
+    when stale/absent."""
     path = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
     try:
         with open(path) as f:
             d = json.load(f)
     except Exception:
         return None, "absent"
-    if d.get("lib_sha256") != lib_sha256():
+    if d.get("src_sha256") != build_inputs_sha256(ROOT):
         return None, f"stale ({path} measured another build)"
     k = d.get("kernels", {}).get(kernel)
     if not k:

@@ -20,6 +20,21 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def build_inputs_sha256(root):
+    """sha256 over the library's build inputs (csrc sources, headers,
+    Makefile, include/): the same sources build the same kernels, while the
+    .so itself is not byte-reproducible across clean builds."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in (os.path.join(root, "paper_1909_02127_b200", "csrc"), os.path.join(root, "include")):
+        for name in sorted(os.listdir(d)):
+            if name.endswith((".cu", ".cuh", ".h", ".hpp", ".cpp")) or name == "Makefile":
+                h.update(name.encode())
+                with open(os.path.join(d, name), "rb") as f:
+                    h.update(f.read())
+    return h.hexdigest()
+
+
 def main():
     rep, config = sys.argv[1], sys.argv[2]
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -47,7 +62,8 @@ def main():
         sha = hashlib.sha256(f.read()).hexdigest()
     git = os.environ.get("GIT_HEAD") or subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"],
                                                        capture_output=True, text=True).stdout.strip()
-    doc = {"config": config, "lib_sha256": sha, "git_head": git or None, "report": os.path.basename(rep),
+    doc = {"config": config, "lib_sha256": sha, "src_sha256": build_inputs_sha256(ROOT), "git_head": git or None,
+           "report": os.path.basename(rep),
            "kernels": out}
     # written next to the report (gpurun_out/ travels back); copy it into
     # profiles/ to make bench.py use it
