@@ -142,6 +142,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
+// TMA bulk prefetch of a global byte range into L2 (no SMEM, no completion
+// to wait on): src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// The 16-byte aligned cover of [p, p + bytes) prefetched into L2.
+__device__ __forceinline__ void prefetch_range_l2(const void* p, uint64_t bytes) {
+  if (!bytes) return;
+  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
+  const uint64_t b = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~15ull;
+  bulk_prefetch_l2(reinterpret_cast<const void*>(a), (uint32_t)(b - a));
+}
 // Ampere-style per-thread async copy (LDGSTS), 8 bytes, L1-bypassing.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

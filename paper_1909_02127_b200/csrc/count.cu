@@ -381,6 +381,11 @@ __device__ __forceinline__ uint32_t warp_walk(uint32_t fb, uint32_t fe, uint32_t
 #ifndef TCB_PV_MASKS
 #define TCB_PV_MASKS 1
 #endif
+// CTA bin: L2 bulk prefetch of the next segment's suffixes (0 off, 1 hot,
+// 2 hot + cold)
+#ifndef TCB_L2PF
+#define TCB_L2PF 0
+#endif
 constexpr uint32_t kTopFlushSegs = 120;  // <= 65535 / kCtaSegItems increments per counter between flushes
 struct ItemGeo {
   const uint4* rowd;  // tc_graph::rowd, rows [r0, n)
@@ -995,6 +1000,30 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
                                return probe_cold<kPerVertex>(qq, c, b, e, gtab, tmask, tshift, sink, s_cf);
                              });
     }
+#if TCB_L2PF
+    // TMA bulk prefetch into L2 of the next segment's item suffixes (hot part
+    // in colH; with TCB_L2PF=2 also the cold part in col): they stream in
+    // under this segment's barrier tail and the next segment's staging, so
+    // its walk's chunk loads hit L2.  (s_sgn is stale once the queue is
+    // drained: the prefetch is then merely useless.)
+    {
+      const uint4 nx = s_sgn;
+#pragma unroll
+      for (int r = 0; r < kIPT; ++r) {
+        const uint32_t i = threadIdx.x * kIPT + r;
+        if (i < nx.z - nx.y) {
+          const uint2 eu = ine[nx.y + i];
+          const RowGeo rd = load_row(rowd, r0, eu.y);
+          if (eu.x + 1 < rd.end) {
+            const uint32_t a = eu.x + 1, ce = rd.cold_end();
+            const uint32_t hb = a >= ce ? rd.O + (a - ce) : rd.O;
+            if (rd.Ht > hb) prefetch_range_l2(colH + hb, 2ull * (rd.Ht - hb));
+            if (TCB_L2PF >= 2 && ce > a) prefetch_range_l2(col + a, 4ull * (ce - a));
+          }
+        }
+      }
+    }
+#endif
     acc += h;
     if (kPerVertex) {
       const uint32_t hw = warp_sum(h);
@@ -1391,16 +1420,20 @@ __device__ __forceinline__ void row_accumulate(const RowRel& rr, const uint8_t* 
       nacc += 8;
     }
   } else {
-    for (uint32_t k0 = ka; k0 < kb; k0 += rl.G * kRowU) {
+    // sub-group `sub` takes a contiguous run of the items; item k's first
+    // chunk cs and its block offset P advance incrementally (P(k+1) = P(k) +
+    // C - cs_k), so no closed-form offset per item
+    const uint32_t per = (kb - ka + rl.G - 1) / rl.G;
+    const uint32_t k_lo = min(kb, ka + rl.sub * per), k_hi = min(kb, k_lo + per);
+    uint32_t P = k_lo < k_hi ? rr.P(k_lo) : 0u;
+    for (uint32_t k0 = k_lo; k0 < k_hi; k0 += kRowU) {
       uint32_t bits[kRowU];
 #pragma unroll
       for (int t = 0; t < kRowU; ++t) {
-        const uint32_t k = k0 + t * rl.G + rl.sub;
-        bits[t] = 0;
-        if (k < kb && cvalid) {
-          const uint32_t cs = rr.csr(k);
-          if (cr >= cs) bits[t] = rowm[rr.P(k) + cr - cs];
-        }
+        const uint32_t k = k0 + t;
+        const uint32_t cs = rr.csr(k);
+        bits[t] = (k < k_hi && cvalid && cr >= cs) ? rowm[P + cr - cs] : 0u;
+        P += rr.C - cs;
       }
       if (nacc + kRowU > 255) fold();
 #pragma unroll
