@@ -1293,6 +1293,8 @@ void finish_graph(tc_graph& g) {
   for (int c = 0; c < 3; ++c) g.seg_cap[c] = h[c];
   g.part_bounds.clear();
   g.part_bounds_P = 0;
+  g.part_kr.clear();
+  g.part_kr_P = 0;
 }
 
 }  // namespace

@@ -145,22 +145,28 @@ void destroy_handle(tc_graph* g) {
     // that is gone by now): drain the device, then free on the own stream
     cudaDeviceSynchronize();
     cudaStream_t s = g->own_stream;
-    g->off.release();
-    g->col.release();
-    g->src.release();
-    g->deg.release();
-    g->id_of.release();
-    g->rank_of.release();
-    g->colH.release();
-    g->offH.release();
-    g->inoff.release();
-    g->ine.release();
-    g->rowd.release();
-    g->cbits.release();
-    g->dine.release();
-    g->dsoff.release();
-    g->drow.release();
-    g->dseg.release();
+    auto rel = [s](auto& b) {  // every buffer goes back on the own stream (a caller's may be gone)
+      b.s = s;
+      b.release();
+    };
+    rel(g->off);
+    rel(g->col);
+    rel(g->src);
+    rel(g->deg);
+    rel(g->id_of);
+    rel(g->rank_of);
+    rel(g->colH);
+    rel(g->offH);
+    rel(g->inoff);
+    rel(g->ine);
+    rel(g->rowd);
+    rel(g->cbits);
+    rel(g->dine);
+    rel(g->dsoff);
+    rel(g->drow);
+    rel(g->dseg);
+    for (auto& b : g->part_kr) rel(b);
+    g->part_kr.clear();
     for (auto& sc : g->scratch) sc.release(s);
     cudaStreamSynchronize(s);
   }

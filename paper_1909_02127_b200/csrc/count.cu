@@ -1479,14 +1479,38 @@ struct PartRange {
     }
     return b;
   }
-  __device__ __forceinline__ void items(uint32_t beg, uint32_t d, uint32_t& k_lo, uint32_t& k_hi) const {
+  const uint2* krange;  // split counts: cached {k_lo, k_hi} per row (k_part_krange), else null
+  __device__ __forceinline__ void items(uint32_t u, uint32_t beg, uint32_t d, uint32_t& k_lo, uint32_t& k_hi) const {
     k_lo = 0;
     k_hi = d ? d - 1 : 0;  // item d-1 has an empty suffix (no mask bytes)
     if (!split || d == 0) return;
+    if (krange) {
+      const uint2 kr = krange[u - r0];
+      k_lo = kr.x;
+      k_hi = min(k_hi, kr.y);
+      return;
+    }
     if (v_lo) k_lo = lb(col, beg, beg + d, v_lo) - beg;
     if (v_hi != 0xffffffffu) k_hi = min(k_hi, lb(col, beg + k_lo, beg + d, v_hi) - beg);
   }
 };
+
+// The item range of every row for one part (graph + split property, cached
+// on the handle by count_triangles): rows scanned once per (P, part) instead
+// of two binary searches per row in every count's row pass.
+__global__ void k_part_krange(PartRange pr, const uint32_t* __restrict__ off, uint32_t n, uint2* __restrict__ out) {
+  for (uint64_t u = pr.r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t beg = off[u], d = off[u + 1] - beg;
+    uint32_t k_lo = 0, k_hi = 0;
+    if (d) {
+      k_hi = d - 1;
+      if (pr.v_lo) k_lo = PartRange::lb(pr.col, beg, beg + d, pr.v_lo) - beg;
+      if (pr.v_hi != 0xffffffffu) k_hi = min(k_hi, PartRange::lb(pr.col, beg + k_lo, beg + d, pr.v_hi) - beg);
+    }
+    out[u - pr.r0] = make_uint2(k_lo, k_hi);
+  }
+}
 
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks, uint32_t n,
@@ -1522,7 +1546,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       hl = r.Ht - r.O;
       rbl = r.rowbase;
       work = hl > 0 && dl >= 2;
-      if (work) pr.items(r.beg, r.d(), kl, kh);
+      if (work) pr.items(ul, r.beg, r.d(), kl, kh);
       kh = min(kh, dl - 1);
       work = work && kh > kl;
       if (work) {
@@ -1635,7 +1659,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
     const uint32_t u = heavy[r];
     const RowGeo rg = load_row(rowd, pr.r0, u);
     uint32_t k_lo = 0, k_hi = 0;
-    pr.items(rg.beg, rg.d(), k_lo, k_hi);
+    pr.items(u, rg.beg, rg.d(), k_lo, k_hi);
     const RowMasks rm = rg.masks();
     k_hi = min(k_hi, rm.d - 1);
     const RowRel rr(rm);
@@ -1903,7 +1927,22 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const int hocc = occupancy(k_pv_rows_heavy, kRowWarps * 32, rsm);
     // items u -> v of pivots [v_lo, v_hi) have u < v_hi: rows [v_hi, n) skip
     // (the light pass walks rows top-down from queue position n - v_hi)
-    const PartRange pr{g.col.get(), v_lo, v_hi == n ? 0xffffffffu : v_hi, split, g.r0};
+    PartRange pr{g.col.get(), v_lo, v_hi == n ? 0xffffffffu : v_hi, split, g.r0, nullptr};
+    if (split && n > g.r0) {
+      // per-row item ranges of this part, cached per (P, part) on the handle
+      if (g.part_kr_P != parts || g.part_kr.size() != parts) {
+        g.part_kr.clear();
+        g.part_kr.resize(parts);
+        g.part_kr_P = parts;
+      }
+      DBuf<uint2>& kr = g.part_kr[part];
+      if (!kr.get()) {
+        kr.alloc(n - g.r0, s);
+        k_part_krange<<<grid_gs(n - g.r0, dev), 256, 0, s>>>(pr, g.off.get(), n, kr.get());
+        TC_LAUNCH();
+      }
+      pr.krange = kr.get();
+    }
     k_pv_rows<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
         g.rowd.get(), g.colH.get(), masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1, row_heavy_threshold(n),
         n - v_hi, t_rank);

@@ -108,6 +108,10 @@ struct tc_graph {
   // with ~equal join work; computed on the first P-part count, then reused
   std::vector<uint64_t> part_bounds;
   uint32_t part_bounds_P = 0;
+  // per part of the last P-way split: each row's item range {k_lo, k_hi}
+  // (per-vertex row pass of a split count), built on first use
+  std::vector<tcb::DBuf<uint2>> part_kr;
+  uint32_t part_kr_P = 0;
   tcb::Scratch scratch[tcb::kSlotCount];
   // Every call that touches the handle's scratch, stream or partition state
   // (count, listings, export, degrees, partition bounds, set_stream) holds

@@ -37,6 +37,10 @@ for i in range(a.iters):
                                                                  part_count=a.parts), stats=True)
         T += int(tot.item())
         per.append(round(st["total_ms"], 2))
+        if a.parts > 1 and i == a.iters - 1:
+            print(f"  part {p}: " + " ".join(f"{k[:-3]}={st[k]:.2f}" for k in
+                                          ("frontier_ms", "warp_ms", "small_ms", "cta_ms", "dense_ms", "rows_ms")),
+                  flush=True)
         for k, v in st.items():
             if k.endswith("_ms"):
                 ms[k] = ms.get(k, 0) + v
