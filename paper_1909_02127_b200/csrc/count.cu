@@ -99,6 +99,12 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 #ifndef TCB_COLD_COST
 #define TCB_COLD_COST 6  // a cold (prefiltered hash) probe (8-part A/B on C4 and C5: profiles/)
 #endif
+#ifndef TCB_SMALL_COST
+#define TCB_SMALL_COST 9  // multiplier of a small-bin pivot's probes (8-part A/B on C4 and C5)
+#endif
+#ifndef TCB_SLAB_COST
+#define TCB_SLAB_COST 10  // a cold probe of a pivot whose table spills to the global slab
+#endif
 #ifndef TCB_WARP_COST
 #define TCB_WARP_COST 16  // a warp-bin (hash) probe
 #endif
@@ -107,7 +113,9 @@ constexpr uint64_t kSegRowCost = TCB_SEG_COST;  // per member of N+(v), per segm
 
 __global__ void k_pivot_wedges(const uint4* __restrict__ rowd, const uint32_t* __restrict__ col,
                                const uint32_t* __restrict__ src, uint64_t E, uint32_t r0, uint32_t dense_cost,
-                               uint32_t cold_cost, uint32_t warp_cost, unsigned long long* __restrict__ jv) {
+                               uint32_t cold_cost, uint32_t warp_cost, uint32_t small_cost, uint32_t slab_cost,
+                               PivotClass pc,
+                               unsigned long long* __restrict__ jv) {
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = base + threadIdx.x;
     const bool ok = e < E;
@@ -122,8 +130,14 @@ __global__ void k_pivot_wedges(const uint4* __restrict__ rowd, const uint32_t* _
       const uint32_t a = (uint32_t)e + 1, se = r.end - r.cc(), ce = min(r.cold_end(), se);
       const uint32_t cold = ce > a ? ce - a : 0u;          // hash-probed candidates
       const uint32_t hot = se > max(a, ce) ? se - max(a, ce) : 0u;  // bitmap-probed
+      uint32_t din = 0;
+      const int cls = pc(v, din);
+      // a pivot with more cold members than the SMEM table holds probes a
+      // per-CTA global slab (k_join_cta): slab_cost per cold probe
       const RowGeo rv = load_row(rowd, r0, v);
-      w = rv.d() <= kWarpMaxDeg ? warp_cost * (cold + hot) : hot + cold_cost * cold;
+      const uint32_t cc = (cls == 1 && 2 * (rv.d() - rv.h()) > kCtaSmemSlots) ? slab_cost : cold_cost;
+      w = cls == 0 ? warp_cost * (cold + hot) : hot + cc * cold;
+      if (cls == 2) w *= small_cost;  // one warp per pivot (k_join_small)
       if (r.didx != kNoDense && a < r.end) w += dense_cost;
     }
     const unsigned peers = __match_any_sync(0xffffffffu, v);
@@ -1759,7 +1773,11 @@ const std::vector<uint64_t>& partition_bounds(tc_graph& g, uint32_t parts) {
     k_pivot_wedges<<<grid_gs(g.E, g.device), 256, 0, s>>>(g.rowd.get(), g.col.get(), g.src.get(), g.E, g.r0,
                                                           env_u32("TCB_DENSE_COST", TCB_DENSE_COST),
                                                           env_u32("TCB_COLD_COST", TCB_COLD_COST),
-                                                          env_u32("TCB_WARP_COST", TCB_WARP_COST), jv.get());
+                                                          env_u32("TCB_WARP_COST", TCB_WARP_COST),
+                                                          env_u32("TCB_SMALL_COST", TCB_SMALL_COST),
+                                                          env_u32("TCB_SLAB_COST", TCB_SLAB_COST),
+                                                          PivotClass{g.off.get(), g.offH.get(), g.inoff.get(), false},
+                                                          jv.get());
     TC_LAUNCH();
     const uint64_t item_cost = env_u32("TCB_ITEM_COST", (uint32_t)kItemCost);  // cost-model knobs
     const uint64_t seg_cost = env_u32("TCB_SEG_COST", (uint32_t)kSegRowCost);

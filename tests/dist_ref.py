@@ -16,6 +16,9 @@ DENSE_COST = 48    # count.cu TCB_DENSE_COST: one dense-core item (k_join_dense)
 COLD_COST = 6      # count.cu TCB_COLD_COST: a cold (hash) probe
 WARP_COST = 16      # count.cu TCB_WARP_COST: a warp-bin probe
 WARP_MAX_DEG = 64  # graph.cuh kWarpMaxDeg
+SMALL_COST = 9     # count.cu TCB_SMALL_COST: multiplier of a small-bin pivot's probes
+SLAB_COST = 10      # count.cu TCB_SLAB_COST: a cold probe of a pivot whose table spills to the global slab
+SMALL_ITEMS, SMALL_COLD, CTA_SMEM_SLOTS = 32, 256, 1024  # graph.cuh kSmallItems/kSmallCold, count.cu kCtaSmemSlots
 CTA_SEG_ITEMS = 512
 HOT_BITS = 1 << 16  # graph.cuh kHotBits
 CORE_BITS = 2048    # graph.cuh kCoreBits; dense rows have >= CORE_BITS / 32 core members
@@ -73,8 +76,15 @@ def pivot_cost(off: np.ndarray, col: np.ndarray, src: np.ndarray) -> np.ndarray:
     ce = np.minimum(end - nhot[src], se)             # cold part ends
     cold = np.maximum(ce - a, 0)
     hot = np.maximum(se - np.maximum(a, ce), 0)
-    dpv = np.diff(off)[col]                          # pivot's d+
-    suffix = np.where(dpv <= WARP_MAX_DEG, WARP_COST * (cold + hot), hot + COLD_COST * cold)
+    dplus = np.diff(off)
+    din = np.bincount(col, minlength=n).astype(np.int64)
+    pcold = dplus - nhot                             # pivot's members below the hot window
+    warp = dplus <= WARP_MAX_DEG                     # graph.cuh PivotClass
+    small = ~warp & (din <= SMALL_ITEMS) & (pcold <= SMALL_COLD)
+    slab = ~warp & ~small & (2 * pcold > CTA_SMEM_SLOTS)
+    v = col
+    suffix = np.where(warp[v], WARP_COST * (cold + hot), hot + np.where(slab[v], SLAB_COST, COLD_COST) * cold)
+    suffix = np.where(small[v], SMALL_COST * suffix, suffix)
     suffix = suffix + np.where((cc[src] > 0) & (a < end), DENSE_COST, 0)
     jv = np.zeros(n, np.int64)
     np.add.at(jv, col, suffix)
