@@ -958,28 +958,49 @@ struct InDeg {
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const { return deg[v] - (off[v + 1] - off[v]); }
 };
 
-// Every oriented edge e = u->v to its head's slot, warp-aggregated per head
-// (hub heads take one atomic per warp): ine[slot] = {e, u}.
-// With ccnt (rows [r0, n): core members of a dense row, else 0), dflag[slot]
-// = 1 for a dense item: u's row is dense and e is not its last edge (src is
-// sorted, so that is src[e+1] == u).
+#ifndef TCB_IN_MATCH
+#define TCB_IN_MATCH 0
+#endif
+// Every oriented edge e = u->v to its head's slot
+// (TCB_IN_MATCH=1: warp-aggregated per head), as a 32-byte level-1 item record
+// (graph.cuh irec, one 256-bit store): the suffix geometry comes from u's row descriptor, read in
+// edge order (consecutive edges share their row).  With ccnt (rows [r0, n):
+// core members of a dense row, else 0), dflag[slot] = 1 for a dense item: u's
+// row is dense and e is not its last edge.
 __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* __restrict__ src, uint64_t E,
-                             uint32_t* __restrict__ cur, uint2* __restrict__ ine, const uint32_t* __restrict__ ccnt,
-                             uint32_t r0, uint8_t* __restrict__ dflag) {
+                             uint32_t* __restrict__ cur, const uint4* __restrict__ rowd, uint32_t r0,
+                             uint4* __restrict__ irec, const uint32_t* __restrict__ ccnt,
+                             uint8_t* __restrict__ dflag) {
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = base + threadIdx.x;
     const bool ok = e < E;
     const uint32_t v = ok ? col[e] : 0xffffffffu;
+#if TCB_IN_MATCH
     const unsigned peers = __match_any_sync(0xffffffffu, v);
     const unsigned lane = threadIdx.x & 31u;
     const int leader = __ffs(peers) - 1;
     uint32_t b = 0;
     if (ok && (int)lane == leader) b = atomicAdd(&cur[v], (unsigned)__popc(peers));
     b = __shfl_sync(0xffffffffu, b, leader);
+    const uint32_t slot0 = b + __popc(peers & lanemask_lt());
+#else
+    // a warp's 32 edges come from one or two rows: their heads repeat only
+    // rarely, so per-edge atomics beat a match_any aggregation
+    const uint32_t slot0 = ok ? atomicAdd(&cur[v], 1u) : 0u;
+#endif
     if (ok) {
-      const uint32_t slot = b + __popc(peers & lanemask_lt()), u = src[e];
-      ine[slot] = make_uint2((uint32_t)e, u);
-      if (dflag) dflag[slot] = (ccnt[u - r0] != 0 && e + 1 < E && src[e + 1] == u) ? 1 : 0;
+      const uint32_t slot = slot0, u = src[e];
+      const RowGeo r(rowd[2 * (uint64_t)(u - r0)], rowd[2 * (uint64_t)(u - r0) + 1]);
+      uint4 geo = make_uint4(0, 0, 0, 0);
+      uint64_t mo = 0;
+      const uint32_t a = (uint32_t)e + 1;
+      if (a < r.end) {
+        const uint32_t ce = r.cold_end();
+        geo = a >= ce ? make_uint4(r.O + (a - ce), r.Ht, 0, 0) : make_uint4(r.O, r.Ht, a, ce);
+        if (geo.y > geo.x) mo = r.rowbase + r.masks().P((uint32_t)e - r.beg);
+      }
+      st256(irec + 2 * (uint64_t)slot, geo, make_uint4((uint32_t)e, u, (uint32_t)mo, (uint32_t)(mo >> 32)));
+      if (dflag) dflag[slot] = (ccnt[u - r0] != 0 && a < r.end) ? 1 : 0;
     }
   }
 }
@@ -1043,11 +1064,11 @@ struct ByteFlag {
   const uint8_t* f;
   __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return f[i]; }
 };
-__global__ void k_dense_scatter(const uint2* __restrict__ ine, uint64_t E, const uint8_t* __restrict__ dflag,
+__global__ void k_dense_scatter(const uint4* __restrict__ irec, uint64_t E, const uint8_t* __restrict__ dflag,
                                 const uint32_t* __restrict__ dpos, uint32_t r0, const uint32_t* __restrict__ ip,
                                 uint32_t* __restrict__ dine) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
-    if (dflag[i]) dine[ip[i]] = dpos[ine[i].y - r0];
+    if (dflag[i]) dine[ip[i]] = dpos[irec[2 * i + 1].y - r0];
 }
 // Dense segments of pivot v: its dense items [dpos[inoff[v]], dpos[inoff[v+1]])
 struct DenseSegs {
@@ -1209,21 +1230,6 @@ void finish_graph(tc_graph& g) {
     }
   }
   pl.mark("fin_core_rows");
-  // in-edge index (+ the dense-item flag of every slot)
-  g.inoff.alloc((uint64_t)n + 1, s);
-  scan_exclusive<uint32_t>(InDeg{g.off.get(), g.deg.get()}, g.inoff.get(), n, g.inoff.get() + n, s);
-  g.ine.alloc(E + 2, s);  // +16 B: bulk copies of a segment's slice round up to 16 bytes
-  TC_CUDA(cudaMemsetAsync(g.ine.get() + E, 0, 2 * sizeof(uint2), s));
-  DBuf<uint8_t> dflag;
-  if (E) {
-    if (g.ndense) dflag.alloc(E, s);
-    DBuf<uint32_t> cur(n, s);
-    TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
-    k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.ine.get(),
-                                                g.ndense ? ccnt.get() : nullptr, g.r0, dflag.get());
-    TC_LAUNCH();
-  }
-  pl.mark("fin_in_scatter");
   g.rowd.alloc(2 * (uint64_t)(nr ? nr : 1), s);
   if (nr) {
     k_rowdesc<<<grid_gs(nr, dev), kT, 0, s>>>(g.off.get(), g.offH.get(), g.r0, n, g.ndense ? ccnt.get() : nullptr,
@@ -1238,6 +1244,31 @@ void finish_graph(tc_graph& g) {
     TC_LAUNCH();
   }
   pl.mark("fin_rowdesc_cbits");
+  // per-vertex mask base of every row (graph property; RowGeo::rowbase)
+  g.mask_total = 0;
+  if (nr) {
+    DBuf<uint64_t> rb((uint64_t)nr + 1, s);
+    scan_exclusive<uint64_t>(RowBytesGeo{g.rowd.get()}, rb.get(), nr, rb.get() + nr, s);
+    k_rowbase_put<<<grid_gs(nr, dev), kT, 0, s>>>(rb.get(), nr, g.rowd.get());
+    TC_LAUNCH();
+    g.mask_total = read_scalar(rb.get() + nr, s);
+  }
+  pl.mark("fin_rowbase");
+  // in-edge index (+ the dense-item flag of every slot)
+  g.inoff.alloc((uint64_t)n + 1, s);
+  scan_exclusive<uint32_t>(InDeg{g.off.get(), g.deg.get()}, g.inoff.get(), n, g.inoff.get() + n, s);
+  g.irec.alloc(2 * (E ? E : 1), s);
+  DBuf<uint8_t> dflag;
+  if (E) {
+    if (g.ndense) dflag.alloc(E, s);
+    DBuf<uint32_t> cur(n, s);
+    TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+    k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.rowd.get(), g.r0,
+                                                g.irec.get(), g.ndense ? ccnt.get() : nullptr,
+                                                dflag.get());
+    TC_LAUNCH();
+  }
+  pl.mark("fin_in_scatter");
   // dense in-edge list and its segments (k_join_dense)
   g.dine.release();
   g.dseg.release();
@@ -1251,7 +1282,7 @@ void finish_graph(tc_graph& g) {
     g.ndine = read_scalar(ip.get() + E, s);
     g.dine.alloc(g.ndine ? g.ndine : 1, s);
     if (g.ndine) {
-      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.ine.get(), E, dflag.get(), dpos.get(), g.r0, ip.get(),
+      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.irec.get(), E, dflag.get(), dpos.get(), g.r0, ip.get(),
                                                      g.dine.get());
       TC_LAUNCH();
     }
@@ -1270,16 +1301,6 @@ void finish_graph(tc_graph& g) {
   ccnt.release();
   dpos.release();
   pl.mark("fin_dense_list");
-  // per-vertex mask base of every row (graph property; RowGeo::rowbase)
-  g.mask_total = 0;
-  if (nr) {
-    DBuf<uint64_t> rb((uint64_t)nr + 1, s);
-    scan_exclusive<uint64_t>(RowBytesGeo{g.rowd.get()}, rb.get(), nr, rb.get() + nr, s);
-    k_rowbase_put<<<grid_gs(nr, dev), kT, 0, s>>>(rb.get(), nr, g.rowd.get());
-    TC_LAUNCH();
-    g.mask_total = read_scalar(rb.get() + nr, s);
-  }
-  pl.mark("fin_rowbase");
   DBuf<unsigned long long> tot(4, s);
   TC_CUDA(cudaMemsetAsync(tot.get(), 0, 4 * sizeof(unsigned long long), s));
   if (nr) {

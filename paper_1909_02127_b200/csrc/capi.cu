@@ -158,7 +158,7 @@ void destroy_handle(tc_graph* g) {
     rel(g->colH);
     rel(g->offH);
     rel(g->inoff);
-    rel(g->ine);
+    rel(g->irec);
     rel(g->rowd);
     rel(g->cbits);
     rel(g->dine);

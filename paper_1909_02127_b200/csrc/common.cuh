@@ -142,6 +142,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
+// One 256-bit store (STG.E.ENL2.256): a whole 32-byte sector, no partial write.
+__device__ __forceinline__ void st256(void* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 // TMA bulk prefetch of a global byte range into L2 (no SMEM, no completion
 // to wait on): src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
@@ -153,6 +159,10 @@ __device__ __forceinline__ void prefetch_range_l2(const void* p, uint64_t bytes)
   const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
   const uint64_t b = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~15ull;
   bulk_prefetch_l2(reinterpret_cast<const void*>(a), (uint32_t)(b - a));
+}
+// Ampere-style per-thread async copy (LDGSTS), 16 bytes, L1-bypassing.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 // Ampere-style per-thread async copy (LDGSTS), 8 bytes, L1-bypassing.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {

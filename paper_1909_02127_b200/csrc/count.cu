@@ -424,7 +424,7 @@ struct ItemGeo {
 // for every item, so this bin zeroes its items' mask bytes (its hits go to
 // per-hit counters instead); d+(v) = 0 pivots come here for that alone.
 template <bool kPerVertex, typename Sink>
-__device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ ine, uint32_t i0, uint32_t i1,
+__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ irec, uint32_t i0, uint32_t i1,
                                                     const uint4* __restrict__ rowd, uint32_t r0,
                                                     const uint32_t* __restrict__ col, const uint32_t* tab,
                                                     uint32_t mask, uint32_t shift, bool probe, const Sink& sink,
@@ -436,7 +436,8 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ in
     const uint32_t my = ib + lane;
     uint32_t b = 0, e = 0, nch = 0, u = 0;
     if (my < i1) {
-      const uint2 eu = ine[my];
+      const uint4 ax = irec[2 * (uint64_t)(my) + 1];
+      const uint2 eu = make_uint2(ax.x, ax.y);
       u = eu.y;
       const RowGeo r = load_row(rowd, r0, u);
       if (eu.x + 1 < r.end) {
@@ -505,7 +506,7 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint2* __restrict__ in
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ col,
-    const uint2* __restrict__ ine, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
+    const uint4* __restrict__ irec, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
     uint32_t rc, uint32_t ncnt, uint8_t* __restrict__ masks,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t nb = off[v], dv = off[v + 1] - nb;
     for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
     __syncwarp();
-    const uint32_t h = warp_join_small<kPerVertex>(ine, sg.y, sg.z, rowd, r0, col, tab, mask, shift, dv > 0, sink,
+    const uint32_t h = warp_join_small<kPerVertex>(irec, sg.y, sg.z, rowd, r0, col, tab, mask, shift, dv > 0, sink,
                                                    masks, s_item[warp]);
     __syncwarp();
     acc += h;
@@ -735,7 +736,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_join_dense(
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd, uint32_t r0,
-    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine,
+    const uint16_t* __restrict__ colH, const uint4* __restrict__ irec,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
     uint32_t h0, uint32_t nbm, uint32_t stab_slots, uint32_t slab_cap, uint32_t* __restrict__ gslab,
     uint8_t* __restrict__ masks, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ t_rank,
@@ -757,7 +758,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   __shared__ uint32_t s_desc[6];  // current segment: v, i0, ni, off[v], d+(v), queue index
   __shared__ unsigned long long s_ctot;
   // the segment's in-edge records {e, u}, bulk-copied (TMA) one segment ahead
-  __shared__ __align__(16) uint2 s_ine[kPF ? kCtaSegItems + 2 : 1];
+  __shared__ __align__(16) uint4 s_ine[kPF ? kCtaSegItems : 1];  // the segment's item geometry records
   __shared__ __align__(8) unsigned long long s_mbar;
   __shared__ uint4 s_sgn;  // the next segment, held by thread 0
   uint32_t* bm = dyn;
@@ -766,7 +767,6 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  const ItemGeo geo{rowd, r0};
   for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
   for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
   for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
@@ -797,13 +797,11 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     }
     s_desc[5] = q;
   };
-  // in-edge slice [i0, i1) -> s_ine[(i0 & 1) ..]: 16-byte aligned source, size
-  // rounded up to 16 bytes (the index carries 16 bytes of tail padding)
-  auto issue_ine = [&](const uint4& sg) {
-    const uint32_t a = sg.y & ~1u;
-    const uint32_t bytes = ((sg.z - a) * 8u + 15u) & ~15u;
-    bulk_g2s(s_ine, ine + a, bytes, &s_mbar);
-  };
+  // the segment's item geometry (the first 16 bytes of records [i0, i1)) -> s_ine
+  // (records are 32 bytes, the staging takes their first 16: a per-thread
+  // cp.async gather, no contiguous bulk copy)
+  static_assert(kPF != 1, "TCB_PREFETCH=1 (bulk copy of the segment's records) needs contiguous 16-byte records");
+  auto issue_ine = [&](const uint4&) {};
   uint32_t phase = 0;
   if (threadIdx.x == 0) {
     mbar_init(&s_mbar, 1);
@@ -820,7 +818,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
 #pragma unroll
       for (int r = 0; r < kCtaSegItems / kJoinThreads; ++r) {
         const uint32_t i = threadIdx.x * (kCtaSegItems / kJoinThreads) + r;
-        if (i < s_desc[2]) cp_async8(&s_ine[i], ine + s_desc[1] + i);
+        if (i < s_desc[2]) cp_async16(&s_ine[i], irec + 2 * ((uint64_t)s_desc[1] + i));
       }
     }
     cp_async_commit();
@@ -868,8 +866,11 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       it[r] = make_uint4(0, 0, 0, 0);
       mo[r] = 0;
       if (i < ni) {
-        const uint2 eu = kPF == 1 ? s_ine[i + (i0 & 1u)] : kPF == 2 ? s_ine[i] : ine[i0 + i];
-        it[r] = geo.hotcold(eu, kMasks ? &mo[r] : nullptr);
+        it[r] = kPF ? s_ine[i] : irec[2 * (uint64_t)(i0 + i)];
+        if (kMasks && it[r].y > it[r].x) {
+          const uint4 ax = irec[2 * (uint64_t)(i0 + i) + 1];
+          mo[r] = ax.z | ((uint64_t)ax.w << 32);
+        }
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -921,7 +922,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
 #pragma unroll
         for (int r = 0; r < kIPT; ++r) {
           const uint32_t i = threadIdx.x * kIPT + r;
-          if (i < nx.z - nx.y) cp_async8(&s_ine[i], ine + nx.y + i);
+          if (i < nx.z - nx.y) cp_async16(&s_ine[i], irec + 2 * ((uint64_t)nx.y + i));
         }
         cp_async_commit();
       }
@@ -1026,14 +1027,9 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       for (int r = 0; r < kIPT; ++r) {
         const uint32_t i = threadIdx.x * kIPT + r;
         if (i < nx.z - nx.y) {
-          const uint2 eu = ine[nx.y + i];
-          const RowGeo rd = load_row(rowd, r0, eu.y);
-          if (eu.x + 1 < rd.end) {
-            const uint32_t a = eu.x + 1, ce = rd.cold_end();
-            const uint32_t hb = a >= ce ? rd.O + (a - ce) : rd.O;
-            if (rd.Ht > hb) prefetch_range_l2(colH + hb, 2ull * (rd.Ht - hb));
-            if (TCB_L2PF >= 2 && ce > a) prefetch_range_l2(col + a, 4ull * (ce - a));
-          }
+          const uint4 g4 = irec[2 * (uint64_t)(nx.y + i)];
+          if (g4.y > g4.x) prefetch_range_l2(colH + g4.x, 2ull * (g4.y - g4.x));
+          if (TCB_L2PF >= 2 && g4.w > g4.z) prefetch_range_l2(col + g4.z, 4ull * (g4.w - g4.z));
         }
       }
     }
@@ -1061,7 +1057,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
         const uint32_t c = s_icnt[i];
         if (c) {
-          atomicAdd(&t_rank[ine[i0 + i].y], (unsigned long long)c);
+          atomicAdd(&t_rank[irec[2 * (uint64_t)(i0 + i) + 1].y], (unsigned long long)c);
           s_icnt[i] = 0;
         }
       }
@@ -1130,7 +1126,7 @@ struct SmallWarpSmem {
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kSmallThreads) k_join_small(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd, uint32_t r0,
-    const uint16_t* __restrict__ colH, const uint2* __restrict__ ine,
+    const uint16_t* __restrict__ colH, const uint4* __restrict__ irec,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
     uint32_t h0, uint32_t nbm, uint8_t* __restrict__ masks, uint32_t rc, uint32_t ncnt,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
@@ -1190,7 +1186,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
       it[r] = make_uint4(0, 0, 0, 0);
       mo[r] = 0;
       if (i < ni) {
-        it[r] = geo.hotcold(ine[i0 + i], kPerVertex ? &mo[r] : nullptr);
+        it[r] = irec[2 * (uint64_t)(i0 + i)];
+        if (kPerVertex && it[r].y > it[r].x) {
+          const uint4 ax = irec[2 * (uint64_t)(i0 + i) + 1];
+          mo[r] = ax.z | ((uint64_t)ax.w << 32);
+        }
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
         nc[r] = it[r].w > it[r].z ? ((it[r].w + 3) >> 2) - (it[r].z >> 2) : 0u;
       }
@@ -1254,7 +1254,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
       for (uint32_t i = lane; i < ni; i += 32) {
         const uint32_t c = w.icnt[i];
         if (c) {
-          atomicAdd(&t_rank[ine[i0 + i].y], (unsigned long long)c);
+          atomicAdd(&t_rank[irec[2 * (uint64_t)(i0 + i) + 1].y], (unsigned long long)c);
           w.icnt[i] = 0;
         }
       }
@@ -1878,7 +1878,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
     const int occ = occupancy(kern, kJoinThreads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(plan.cap[0], kJoinWarps), (uint64_t)sms * occ);
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.ine.get(), plan.wsegs,
+    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(), plan.wsegs,
                                          plan.nseg + 0, rc_w, ncnt_w, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
@@ -1894,7 +1894,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     auto kern = pv ? k_join_small<true> : k_join_small<false>;
     const int occ = occupancy(kern, kSmallThreads, ssm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, ceil_div64(plan.cap[2], kSmallWarps));
-    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.ine.get(),
+    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(),
                                          plan.ssegs, plan.nseg + 2, queues + 0, g.h0, nbm, masks,
                                          ncnt_s ? n - ncnt_s : 0xffffffffu, ncnt_s, t_rank, acc);
     TC_LAUNCH();
@@ -1912,7 +1912,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const int occ = occupancy(kern, kJoinThreads, dsm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, plan.cap[1]);
     uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.ine.get(),
+    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(),
                                         plan.csegs, plan.nseg + 1, queues + 1, g.h0, nbm, smem_slots,
                                         slab_cap, slab, masks, rc_hits, ncnt_hits, t_rank, acc);
     TC_LAUNCH();

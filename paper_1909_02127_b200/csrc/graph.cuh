@@ -67,13 +67,21 @@ struct tc_graph {
   uint32_t h0 = 0;
   tcb::DBuf<uint16_t> colH;
   tcb::DBuf<uint32_t> offH;
-  // In-edge index: the oriented edges grouped by head, ine[inoff[v] ..
-  // inoff[v+1]) = {e, u} for every u->v (e = its position in col).  Together
-  // with off/col this is the reference's symmetric adjacency split by
-  // orientation (N+(v) and N-(v)); it is what makes the level-1 frontier of a
-  // count a plan over |V| instead of a scatter over |E| (plan.cu).
+  // In-edge index: the oriented edges grouped by head, slots [inoff[v],
+  // inoff[v+1]) for every u->v.  Together with off/col this is the
+  // reference's symmetric adjacency split by orientation (N+(v) and N-(v));
+  // it is what makes the level-1 frontier of a count a plan over |V| instead
+  // of a scatter over |E| (plan.cu).  Each slot is a 32-byte level-1 item
+  // record (one DRAM sector, written once at build by k_in_scatter with one
+  // 256-bit store) so a join stages an item with one coalesced load and no
+  // row lookup:
+  //   irec[2 slot]     = {hb, he, cb, ce}  sparse hot suffix colH[hb, he),
+  //                                        cold suffix col[cb, ce) (empty:
+  //                                        end <= begin)
+  //   irec[2 slot + 1] = {e, u, mo_lo, mo_hi}  edge position, source, first
+  //                                        per-vertex mask byte
   tcb::DBuf<uint32_t> inoff;
-  tcb::DBuf<uint2> ine;
+  tcb::DBuf<uint4> irec;
   // Row descriptors, one 32-byte record (two uint4, one DRAM sector) per rank
   // of the non-isolated ranks [r0, n) (isolated vertices have the lowest
   // ranks and no work): tcb::RowGeo -- a join stages an item's whole row

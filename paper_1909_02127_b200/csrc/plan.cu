@@ -100,7 +100,7 @@ __global__ void k_plan_segs(const uint8_t* __restrict__ cls, const uint32_t* __r
 // items and segments.
 __global__ void k_plan_work(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, PivotClass pc,
                             const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ inoff,
-                            const uint2* __restrict__ ine, const uint32_t* __restrict__ dsoff, uint32_t v_lo,
+                            const uint4* __restrict__ irec, const uint32_t* __restrict__ dsoff, uint32_t v_lo,
                             uint32_t v_hi, Sums* __restrict__ sums) {
   unsigned long long W = 0, J = 0, H = 0, I = 0, P = 0;
   unsigned long long ch = 0, cc = 0, ci = 0, cm = 0, csm = 0, cs = 0, di = 0, ds = 0;
@@ -121,7 +121,8 @@ __global__ void k_plan_work(const uint32_t* __restrict__ off, const uint32_t* __
   }
   const uint32_t i_lo = inoff[v_lo], i_hi = inoff[v_hi];
   for (uint64_t i = i_lo + t0; i < i_hi; i += stride) {
-    const uint2 eu = ine[i];
+    const uint4 ax = irec[2 * (uint64_t)(i) + 1];
+    const uint2 eu = make_uint2(ax.x, ax.y);
     const RowGeo rd = load_row(rowd, r0, eu.y);
     if (eu.x + 1 >= rd.end) continue;
     ++I;
@@ -203,7 +204,7 @@ int build_plan(tc_graph& g, uint32_t v_lo, uint32_t v_hi, bool per_vertex, bool 
     if (np) {
       k_plan_work<<<(unsigned)num_sms(dev) * 8, kT, 0, s>>>(
           g.off.get(), g.col.get(), PivotClass{g.off.get(), g.offH.get(), g.inoff.get(), masks}, g.rowd.get(), g.r0,
-          g.inoff.get(), g.ine.get(), g.ndine ? g.dsoff.get() : nullptr, v_lo, v_hi, sums);
+          g.inoff.get(), g.irec.get(), g.ndine ? g.dsoff.get() : nullptr, v_lo, v_hi, sums);
       TC_LAUNCH();
     }
     p.sums = sums;
