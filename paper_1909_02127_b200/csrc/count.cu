@@ -436,26 +436,21 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ ir
     const uint32_t my = ib + lane;
     uint32_t b = 0, e = 0, nch = 0, u = 0;
     if (my < i1) {
-      const uint4 ax = irec[2 * (uint64_t)(my) + 1];
-      const uint2 eu = make_uint2(ax.x, ax.y);
-      u = eu.y;
-      const RowGeo r = load_row(rowd, r0, u);
-      if (eu.x + 1 < r.end) {
-        // a dense row's core members (its last cc) are joined by k_join_dense
-        b = eu.x + 1;
-        e = r.end - r.cc();
-        nch = b < e ? ((e + 3) >> 2) - (b >> 2) : 0u;
-        if (kPerVertex && TCB_PV_MASKS) {
-          // the row pass reads every item's sparse hot mask bytes: zero this
-          // item's (its hits are counted here, per hit)
-          const RowMasks rm = r.masks();
-          const uint32_t k = eu.x - r.beg;
-          if (rm.h > 0 && k + 1 < rm.d) {
-            uint8_t* z = masks + r.rowbase + rm.P(k);
-            const uint32_t nb = (uint32_t)(rm.c_hi - rm.first_chunk(k));
-            for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
-          }
-        }
+      // the item record: its suffix in col is [e+1, e+1 + cold + sparse hot)
+      // (the cold members are followed by the hot ones in col; a dense row's
+      // core members, its last cc, are k_join_dense's)
+      const uint4 g4 = irec[2 * (uint64_t)my], ax = irec[2 * (uint64_t)my + 1];
+      u = ax.y;
+      b = ax.x + 1;
+      const uint32_t hot = g4.y > g4.x ? g4.y - g4.x : 0u;
+      e = b + (g4.w > g4.z ? g4.w - g4.z : 0u) + hot;
+      nch = b < e ? ((e + 3) >> 2) - (b >> 2) : 0u;
+      if (kPerVertex && TCB_PV_MASKS && hot) {
+        // the row pass reads every item's sparse hot mask bytes: zero this
+        // item's (its hits are counted here, per hit)
+        uint8_t* z = masks + (ax.z | ((uint64_t)ax.w << 32));
+        const uint32_t nb = ((g4.y + 7) >> 3) - (g4.x >> 3);
+        for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
       }
     }
     if (!probe) continue;
