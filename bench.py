@@ -567,7 +567,7 @@ def main():
             "peak_kind": peak_kind,
             "kernel": "k_join_cta (sparse advance + fused SMEM join, the dominant kernel)",
             "model": "k_join_cta algorithmic bytes per launch: 2 B per sparse hot candidate + 4 B per cold "
-                     "candidate + 40 B per item (in-edge record + 32-byte row descriptor) + 1 B per per-vertex "
+                     "candidate + 32 B per item (its 32-byte in-edge item record) + 1 B per per-vertex "
                      "mask chunk + 4 B per pivot member and 16 B per CTA segment",
             "bytes_per_launch": cta_bytes, "kernel_ms": cta_ms,
             "kernels_ms": kms,

@@ -119,7 +119,7 @@ typedef struct tc_count_stats {
   double rows_ms;         /* k_pv_rows + k_pv_rows_heavy (per-vertex masks)  */
   /* algorithmic bytes of one launch (work_counters): what the kernel's
    * algorithm must move -- k_join_cta: 2 B per sparse hot candidate + 4 B per
-   * cold candidate + 40 B per item (in-edge record + row descriptor) + its
+   * cold candidate + 32 B per item (its in-edge item record) + its
    * per-vertex mask bytes + 4 B per pivot member and 16 B per segment;
    * k_join_dense: 8 B per dense item (list entry, row rank) + 4 B per core
    * word of its row + 288 B per segment (pivot descriptor + core words) */

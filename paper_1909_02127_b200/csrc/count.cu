@@ -418,33 +418,48 @@ struct ItemGeo {
 
 // ---- warp bin ------------------------------------------------------------------
 
-// Advance + join for in-edges [i0, i1) of one small pivot (d+ <= 64), one
-// warp against its private hash; items are the u32 suffix ranges
-// {e+1, off[u+1] - cc(u)} of col (a dense row's core part is k_join_dense's).  Per-vertex: the CTA bin's row pass reads hit masks
-// for every item, so this bin zeroes its items' mask bytes (its hits go to
-// per-hit counters instead); d+(v) = 0 pivots come here for that alone.
+// Pivots with d+ <= 64 (warp-bin segments of <= 64 in-edge items).  A warp
+// takes a group of kWarpGroup consecutive segments at once: every pivot gets
+// its own 128-slot hash table (warp-private SMEM) and the group's items are
+// packed into 32-lane batches -- a uniform-degree graph has ~8 items per
+// pivot, so one segment per warp step would leave most lanes idle and pay
+// the segment's dependent memory round trips four times as often.  Items are
+// the u32 suffix ranges of col from their 32-byte records (a dense row's core
+// members, its last cc, are k_join_dense's).  Per-vertex: the CTA bin's row
+// pass reads hit masks for every item, so this bin zeroes its items' mask
+// bytes (its hits go to per-hit counters instead); d+(v) = 0 pivots come here
+// for that alone.
+#ifndef TCB_WARP_GROUP
+#define TCB_WARP_GROUP 4
+#endif
+constexpr int kWarpGroup = TCB_WARP_GROUP;
+
 template <bool kPerVertex, typename Sink>
-__device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ irec, uint32_t i0, uint32_t i1,
-                                                    const uint4* __restrict__ rowd, uint32_t r0,
-                                                    const uint32_t* __restrict__ col, const uint32_t* tab,
-                                                    uint32_t mask, uint32_t shift, bool probe, const Sink& sink,
-                                                    uint8_t* __restrict__ masks, uint32_t* item_cnt) {
+__device__ __forceinline__ uint32_t warp_join_group(const uint4* __restrict__ irec, const uint32_t (&gi0)[kWarpGroup],
+                                                    const uint32_t (&gpre)[kWarpGroup + 1], uint32_t probe_mask,
+                                                    const uint32_t* __restrict__ col, const uint32_t* tabs,
+                                                    uint32_t mask, uint32_t shift, const Sink& sink,
+                                                    uint8_t* __restrict__ masks, uint32_t* item_cnt,
+                                                    uint32_t (&hseg)[kWarpGroup]) {
   const unsigned lane = lane_id();
   const uint4* col4 = reinterpret_cast<const uint4*>(col);
   uint32_t hits = 0;
-  for (uint32_t ib = i0; ib < i1; ib += 32) {
-    const uint32_t my = ib + lane;
-    uint32_t b = 0, e = 0, nch = 0, u = 0;
-    if (my < i1) {
+  const uint32_t nitems = gpre[kWarpGroup];
+  for (uint32_t ib = 0; ib < nitems; ib += 32) {
+    const uint32_t p = ib + lane;
+    uint32_t b = 0, e = 0, nch = 0, u = 0, tj = 0;
+#pragma unroll
+    for (int j = 1; j < kWarpGroup; ++j) tj += p >= gpre[j] ? 1u : 0u;  // the item's segment
+    if (p < nitems) {
+      const uint32_t my = gi0[tj] + (p - gpre[tj]);
       // the item record: its suffix in col is [e+1, e+1 + cold + sparse hot)
-      // (the cold members are followed by the hot ones in col; a dense row's
-      // core members, its last cc, are k_join_dense's)
+      // (the cold members are followed by the hot ones in col)
       const uint4 g4 = irec[2 * (uint64_t)my], ax = irec[2 * (uint64_t)my + 1];
       u = ax.y;
       b = ax.x + 1;
       const uint32_t hot = g4.y > g4.x ? g4.y - g4.x : 0u;
       e = b + (g4.w > g4.z ? g4.w - g4.z : 0u) + hot;
-      nch = b < e ? ((e + 3) >> 2) - (b >> 2) : 0u;
+      nch = (b < e && ((probe_mask >> tj) & 1u)) ? ((e + 3) >> 2) - (b >> 2) : 0u;
       if (kPerVertex && TCB_PV_MASKS && hot) {
         // the row pass reads every item's sparse hot mask bytes: zero this
         // item's (its hits are counted here, per hit)
@@ -453,16 +468,17 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ ir
         for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
       }
     }
-    if (!probe) continue;
     // compact the non-empty items to the low lanes (item_of needs nch >= 1);
     // lane L takes the item of the (L+1)-th non-empty lane
-    uint32_t owner_u = u;
+    const uint32_t ne = __ballot_sync(0xffffffffu, nch > 0);
+    if (!ne) continue;
+    uint32_t owner_u;
     {
-      const uint32_t ne = __ballot_sync(0xffffffffu, nch > 0);
       const uint32_t from = lane < (uint32_t)__popc(ne) ? __fns(ne, 0, lane + 1) : lane;
       b = __shfl_sync(0xffffffffu, b, from);
       e = __shfl_sync(0xffffffffu, e, from);
       nch = __shfl_sync(0xffffffffu, nch, from);
+      tj = __shfl_sync(0xffffffffu, tj, from);
       owner_u = __shfl_sync(0xffffffffu, u, from);
       if (lane >= (uint32_t)__popc(ne)) nch = 0;
     }
@@ -476,13 +492,18 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ ir
     for (uint32_t base = 0; base < total; base += 32) {
       const uint32_t k = item_of(base, nch, pre, start);
       const uint32_t bk = __shfl_sync(0xffffffffu, b, k), ek = __shfl_sync(0xffffffffu, e, k);
-      const uint32_t sk = __shfl_sync(0xffffffffu, start, k);
+      const uint32_t sk = __shfl_sync(0xffffffffu, start, k), tk = __shfl_sync(0xffffffffu, tj, k);
       const uint32_t f = base + lane;
       if (f < total) {
         const uint32_t c = (bk >> 2) + (f - sk);
-        const uint32_t x = probe_cold<kPerVertex>(__ldg(col4 + c), c, bk, ek, tab, mask, shift, sink);
+        const uint32_t x =
+            probe_cold<kPerVertex>(__ldg(col4 + c), c, bk, ek, tabs + tk * kWarpTable, mask, shift, sink);
         hits += x;
-        if (kPerVertex && x) atomicAdd(&item_cnt[k], x);
+        if (kPerVertex) {
+#pragma unroll
+          for (int j = 0; j < kWarpGroup; ++j) hseg[j] += tk == (uint32_t)j ? x : 0u;
+          if (x) atomicAdd(&item_cnt[k], x);
+        }
       }
     }
     if (kPerVertex) {
@@ -495,9 +516,9 @@ __device__ __forceinline__ uint32_t warp_join_small(const uint4* __restrict__ ir
   return hits;
 }
 
-// Warp bin: each warp takes whole segments of small pivots (d+ <= 64) with a
-// warp-private 128-slot hash table; the CTA shares the per-vertex top-rank
-// counters (dynamic SMEM, pv only).  The segment count is read on the device.
+// Warp bin kernel: groups of kWarpGroup segments per warp step, the CTA
+// shares the per-vertex top-rank counters (dynamic SMEM, pv only).  The
+// segment count is read on the device.
 template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ col,
@@ -505,12 +526,12 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     uint32_t rc, uint32_t ncnt, uint8_t* __restrict__ masks,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
-  __shared__ uint32_t s_tab[kJoinWarps][kWarpTable];
+  __shared__ uint32_t s_tab[kJoinWarps][kWarpGroup * kWarpTable];
   __shared__ uint32_t s_item[kJoinWarps][32];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  uint32_t* tab = s_tab[warp];
-  for (uint32_t s = lane; s < kWarpTable; s += 32) tab[s] = kEmpty;
+  uint32_t* tabs = s_tab[warp];
+  for (uint32_t s = lane; s < kWarpGroup * kWarpTable; s += 32) tabs[s] = kEmpty;
   if (kPerVertex) {
     for (uint32_t i = threadIdx.x; i < ncnt; i += kJoinThreads) top_cnt[i] = 0;
     __syncthreads();
@@ -520,21 +541,55 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   const PvSink<false> sink{top_cnt, rc, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
   const uint32_t gw = blockIdx.x * kJoinWarps + warp, nw = gridDim.x * kJoinWarps;
-  for (uint32_t si = gw; si < nsegs; si += nw) {
-    const uint4 sg = segs[si];
-    const uint32_t v = sg.x;
-    const uint32_t nb = off[v], dv = off[v + 1] - nb;
-    for (uint32_t j = lane; j < dv; j += 32) hash_insert(tab, mask, shift, col[nb + j]);
+  for (uint64_t g0 = (uint64_t)gw * kWarpGroup; g0 < nsegs; g0 += (uint64_t)nw * kWarpGroup) {
+    // lane j < kWarpGroup: segment g0 + j's descriptor and pivot row
+    uint4 sgl = make_uint4(0, 0, 0, 0);
+    uint32_t nbl = 0, dvl = 0;
+    if (lane < (uint32_t)kWarpGroup && g0 + lane < nsegs) {
+      sgl = segs[g0 + lane];
+      nbl = off[sgl.x];
+      dvl = off[sgl.x + 1] - nbl;
+    }
+    uint32_t gv[kWarpGroup], gi0[kWarpGroup], gpre[kWarpGroup + 1], gnb[kWarpGroup], mpre[kWarpGroup + 1];
+    uint32_t probe_mask = 0;
+    gpre[0] = mpre[0] = 0;
+#pragma unroll
+    for (int j = 0; j < kWarpGroup; ++j) {
+      gv[j] = __shfl_sync(0xffffffffu, sgl.x, j);
+      gi0[j] = __shfl_sync(0xffffffffu, sgl.y, j);
+      const uint32_t ni = __shfl_sync(0xffffffffu, sgl.z, j) - gi0[j];
+      gnb[j] = __shfl_sync(0xffffffffu, nbl, j);
+      const uint32_t dv = __shfl_sync(0xffffffffu, dvl, j);
+      gpre[j + 1] = gpre[j] + ni;
+      mpre[j + 1] = mpre[j] + dv;
+      probe_mask |= (dv > 0 ? 1u : 0u) << j;
+    }
+    // the group's pivot members, flattened over the lanes, into their tables
+    for (uint32_t q = lane; q < mpre[kWarpGroup]; q += 32) {
+      uint32_t j = 0;
+#pragma unroll
+      for (int t = 1; t < kWarpGroup; ++t) j += q >= mpre[t] ? 1u : 0u;
+      hash_insert(tabs + j * kWarpTable, mask, shift, col[gnb[j] + (q - mpre[j])]);
+    }
     __syncwarp();
-    const uint32_t h = warp_join_small<kPerVertex>(irec, sg.y, sg.z, rowd, r0, col, tab, mask, shift, dv > 0, sink,
-                                                   masks, s_item[warp]);
+    uint32_t hseg[kWarpGroup];
+#pragma unroll
+    for (int j = 0; j < kWarpGroup; ++j) hseg[j] = 0;
+    const uint32_t h = warp_join_group<kPerVertex>(irec, gi0, gpre, probe_mask, col, tabs, mask, shift, sink, masks,
+                                                   s_item[warp], hseg);
     __syncwarp();
     acc += h;
     if (kPerVertex) {
-      const uint32_t hw = warp_sum(h);
-      if (lane == 0 && hw) atomicAdd(&t_rank[v], (unsigned long long)hw);
+#pragma unroll
+      for (int j = 0; j < kWarpGroup; ++j) {
+        const uint32_t hw = warp_sum(hseg[j]);
+        if (lane == 0 && hw) atomicAdd(&t_rank[gv[j]], (unsigned long long)hw);
+      }
     }
-    for (uint32_t s = lane; s < kWarpTable; s += 32) tab[s] = kEmpty;
+#pragma unroll
+    for (int j = 0; j < kWarpGroup; ++j)
+      if ((probe_mask >> j) & 1u)
+        for (uint32_t s = lane; s < kWarpTable; s += 32) tabs[j * kWarpTable + s] = kEmpty;
     __syncwarp();
   }
   acc = warp_sum(acc);
@@ -1872,7 +1927,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const size_t smem = (size_t)ncnt_w * sizeof(uint32_t);
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
     const int occ = occupancy(kern, kJoinThreads, smem);
-    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div64(plan.cap[0], kJoinWarps), (uint64_t)sms * occ);
+    const unsigned grid =
+        (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(plan.cap[0], kWarpGroup), kJoinWarps), (uint64_t)sms * occ);
     kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(), plan.wsegs,
                                          plan.nseg + 0, rc_w, ncnt_w, masks, t_rank, acc);
     TC_LAUNCH();

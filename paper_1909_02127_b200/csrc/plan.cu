@@ -222,7 +222,7 @@ void read_plan_sums(Plan& p, cudaStream_t s) {
   p.hot = h.hot;
   p.items = h.items;
   p.pivots = h.pivots;
-  p.cta_bytes = 2.0 * h.cta_hot + 4.0 * h.cta_cold + 40.0 * h.cta_items + (p.masks ? (double)h.cta_mask : 0.0) +
+  p.cta_bytes = 2.0 * h.cta_hot + 4.0 * h.cta_cold + 32.0 * h.cta_items + (p.masks ? (double)h.cta_mask : 0.0) +
                 4.0 * h.cta_seg_members + 16.0 * h.cta_segs;
   p.dense_bytes = (p.masks ? 8.0 : 4.0) * h.dense_items + 4.0 * p.core_words * h.dense_items +
                   (32.0 + 4.0 * p.core_words) * h.dense_segs;
