@@ -523,7 +523,7 @@ template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ col,
     const uint4* __restrict__ irec, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
-    uint32_t rc, uint32_t ncnt, uint8_t* __restrict__ masks,
+    uint32_t gsz, uint32_t rc, uint32_t ncnt, uint8_t* __restrict__ masks,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
   __shared__ uint32_t s_tab[kJoinWarps][kWarpGroup * kWarpTable];
@@ -541,11 +541,13 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
   const PvSink<false> sink{top_cnt, rc, t_rank, g_pv_dbg};
   unsigned long long acc = 0;
   const uint32_t gw = blockIdx.x * kJoinWarps + warp, nw = gridDim.x * kJoinWarps;
-  for (uint64_t g0 = (uint64_t)gw * kWarpGroup; g0 < nsegs; g0 += (uint64_t)nw * kWarpGroup) {
-    // lane j < kWarpGroup: segment g0 + j's descriptor and pivot row
+  // gsz (<= kWarpGroup) segments per warp step: kWarpGroup when there are
+  // enough segments to keep every resident warp busy, else 1
+  for (uint64_t g0 = (uint64_t)gw * gsz; g0 < nsegs; g0 += (uint64_t)nw * gsz) {
+    // lane j < gsz: segment g0 + j's descriptor and pivot row
     uint4 sgl = make_uint4(0, 0, 0, 0);
     uint32_t nbl = 0, dvl = 0;
-    if (lane < (uint32_t)kWarpGroup && g0 + lane < nsegs) {
+    if (lane < gsz && g0 + lane < nsegs) {
       sgl = segs[g0 + lane];
       nbl = off[sgl.x];
       dvl = off[sgl.x + 1] - nbl;
@@ -1927,10 +1929,12 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const size_t smem = (size_t)ncnt_w * sizeof(uint32_t);
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
     const int occ = occupancy(kern, kJoinThreads, smem);
+    const uint64_t resident_warps = (uint64_t)sms * occ * kJoinWarps;
+    const uint32_t gsz = plan.cap[0] >= (uint64_t)kWarpGroup * resident_warps ? kWarpGroup : 1u;
     const unsigned grid =
-        (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(plan.cap[0], kWarpGroup), kJoinWarps), (uint64_t)sms * occ);
+        (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(plan.cap[0], gsz), kJoinWarps), (uint64_t)sms * occ);
     kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(), plan.wsegs,
-                                         plan.nseg + 0, rc_w, ncnt_w, masks, t_rank, acc);
+                                         plan.nseg + 0, gsz, rc_w, ncnt_w, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_warp");
