@@ -171,6 +171,10 @@ void destroy_handle(tc_graph* g) {
     cudaStreamSynchronize(s);
   }
   if (g->own_stream) cudaStreamDestroy(g->own_stream);
+  if (g->hi_stream) cudaStreamDestroy(g->hi_stream);
+  if (g->lo_stream) cudaStreamDestroy(g->lo_stream);
+  for (cudaEvent_t e : {g->fork_ev, g->join_hi, g->join_lo})
+    if (e) cudaEventDestroy(e);
   delete g;
   cudaSetDevice(prev);
 }

@@ -1790,9 +1790,10 @@ T read_scalar(const T* d, cudaStream_t s) {
 }
 
 struct Events {
-  // 0 start, 1 plan done, 2 join done, 3 outputs done; 4..9 around the
-  // join kernels: warp | small | cta | dense | rows
-  cudaEvent_t e[10] = {};
+  // 0 start, 1 plan done, 2 join done, 3 outputs done; around the join
+  // kernels: 4-5 warp, 5-6 small, 7-8 dense (lo stream), 10-11 cta (hi
+  // stream), 12-9 rows
+  cudaEvent_t e[13] = {};
   bool on = false;
   explicit Events(bool enable) : on(enable) {  // only a timed call (stats) creates them
     if (on)
@@ -1922,7 +1923,50 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const uint32_t nbm = (n - g.h0 + 31) / 32;
   unsigned int* queues = g.scratch[kSlotCounters].get<unsigned int>(16, s) + 4;  // [0..3] = plan.nseg
   TC_CUDA(cudaMemsetAsync(queues, 0, 8 * sizeof(unsigned int), s));
-  if (timing) TC_CUDA(cudaEventRecord(ev.e[4], s));
+  // Fork: the dominant CTA join on a high-priority stream, the warp / small /
+  // dense joins (independent of it: disjoint items, atomic outputs) on a
+  // low-priority one -- their blocks fill the SMs the CTA join's tail frees.
+  // Join back before the row pass.  (TCB_CONCURRENT=0: one stream.)
+  const bool fork = env_u32("TCB_CONCURRENT", 0) != 0;  // measured: no gain (profiles/README.md)
+  // the CTA join's launch shape and global-slab scratch (taken before the fork)
+  const uint32_t ncnt_hits0 = (pv && !kUseMasks) ? std::min<uint32_t>(ncnt, env_u32("TCB_HIT_COUNTERS", 4096)) & ~1u : 0;
+  const uint32_t rc_hits0 = ncnt_hits0 ? n - ncnt_hits0 : 0xffffffffu;
+  const uint32_t slab_cap = (table_size_for(g.max_dplus) > smem_slots) ? table_size_for(g.max_dplus) : 0;
+  const size_t cta_dsm = ((size_t)nbm + kCtaSmemSlots + ncnt_hits0 / 2) * sizeof(uint32_t);
+  auto cta_kern = pv ? k_join_cta<true> : k_join_cta<false>;
+  const unsigned cta_grid =
+      plan.cap[1] ? (unsigned)std::min<uint64_t>((uint64_t)sms * occupancy(cta_kern, kJoinThreads, cta_dsm), plan.cap[1])
+                  : 0u;
+  uint32_t* slab = plan.cap[1] ? g.scratch[kSlotSlab].get<uint32_t>((uint64_t)cta_grid * slab_cap + 1, s) : nullptr;
+  cudaStream_t sh = s, sl = s;
+  if (fork) {
+    if (!g.hi_stream) {
+      int least = 0, greatest = 0;
+      TC_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      TC_CUDA(cudaStreamCreateWithPriority(&g.hi_stream, cudaStreamNonBlocking, greatest));
+      TC_CUDA(cudaStreamCreateWithPriority(&g.lo_stream, cudaStreamNonBlocking, least));
+      for (cudaEvent_t* e : {&g.fork_ev, &g.join_hi, &g.join_lo})
+        TC_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    sh = g.hi_stream;
+    sl = g.lo_stream;
+    TC_CUDA(cudaEventRecord(g.fork_ev, s));
+    TC_CUDA(cudaStreamWaitEvent(sh, g.fork_ev, 0));
+    TC_CUDA(cudaStreamWaitEvent(sl, g.fork_ev, 0));
+  }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[10], sh));
+  if (plan.cap[1]) {
+    // cold members spill to a per-CTA global slab only when a pivot has more
+    // than smem_slots/2 members below h0
+    cta_kern<<<cta_grid, kJoinThreads, cta_dsm, sh>>>(
+        g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(), plan.csegs, plan.nseg + 1,
+        queues + 1, g.h0, nbm, smem_slots, slab_cap, slab, masks, rc_hits0, ncnt_hits0, t_rank, acc);
+    TC_LAUNCH();
+    ++launches;
+    pl.mark("join_cta");
+  }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[11], sh));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[4], sl));
   if (plan.cap[0]) {
     // warp bin: plain 32-bit counters over half the window
     const uint32_t ncnt_w = ncnt / 2, rc_w = pv ? n - ncnt_w : 0xffffffffu;
@@ -1933,13 +1977,13 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     const uint32_t gsz = plan.cap[0] >= (uint64_t)kWarpGroup * resident_warps ? kWarpGroup : 1u;
     const unsigned grid =
         (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(plan.cap[0], gsz), kJoinWarps), (uint64_t)sms * occ);
-    kern<<<grid, kJoinThreads, smem, s>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(), plan.wsegs,
-                                         plan.nseg + 0, gsz, rc_w, ncnt_w, masks, t_rank, acc);
+    kern<<<grid, kJoinThreads, smem, sl>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(), plan.wsegs,
+                                          plan.nseg + 0, gsz, rc_w, ncnt_w, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_warp");
   }
-  if (timing) TC_CUDA(cudaEventRecord(ev.e[5], s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[5], sl));
   // per-hit top counters of the CTA / small bins (no-mask per-vertex mode)
   const uint32_t ncnt_hits = (pv && !kUseMasks) ? std::min<uint32_t>(ncnt, env_u32("TCB_HIT_COUNTERS", 4096)) & ~1u : 0;
   const uint32_t rc_hits = ncnt_hits ? n - ncnt_hits : 0xffffffffu;
@@ -1949,44 +1993,34 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     auto kern = pv ? k_join_small<true> : k_join_small<false>;
     const int occ = occupancy(kern, kSmallThreads, ssm);
     const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, ceil_div64(plan.cap[2], kSmallWarps));
-    kern<<<grid, kSmallThreads, ssm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(),
+    kern<<<grid, kSmallThreads, ssm, sl>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(),
                                          plan.ssegs, plan.nseg + 2, queues + 0, g.h0, nbm, masks,
                                          ncnt_s ? n - ncnt_s : 0xffffffffu, ncnt_s, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_small");
   }
-  if (timing) TC_CUDA(cudaEventRecord(ev.e[6], s));
-  if (plan.cap[1]) {
-    // cold members spill to a per-CTA global slab only when a pivot has more
-    // than smem_slots/2 members below h0
-    const uint32_t cap = table_size_for(g.max_dplus);
-    const uint32_t slab_cap = (cap > smem_slots) ? cap : 0;
-    const size_t dsm = ((size_t)nbm + kCtaSmemSlots + ncnt_hits / 2) * sizeof(uint32_t);
-    auto kern = pv ? k_join_cta<true> : k_join_cta<false>;
-    const int occ = occupancy(kern, kJoinThreads, dsm);
-    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * occ, plan.cap[1]);
-    uint32_t* slab = g.scratch[kSlotSlab].get<uint32_t>((uint64_t)grid * slab_cap + 1, s);
-    kern<<<grid, kJoinThreads, dsm, s>>>(g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(),
-                                        plan.csegs, plan.nseg + 1, queues + 1, g.h0, nbm, smem_slots,
-                                        slab_cap, slab, masks, rc_hits, ncnt_hits, t_rank, acc);
-    TC_LAUNCH();
-    ++launches;
-    pl.mark("join_cta");
-  }
-  if (timing) TC_CUDA(cudaEventRecord(ev.e[7], s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[6], sl));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[7], sl));
   if (g.ndine) {
     // dense core parts: word-parallel intersections (k_join_dense)
     auto kern = pv ? k_join_dense<true> : k_join_dense<false>;
     const int occ = occupancy(kern, kDenseThreads, 0);
-    kern<<<(unsigned)(sms * occ), kDenseThreads, 0, s>>>(
+    kern<<<(unsigned)(sms * occ), kDenseThreads, 0, sl>>>(
         g.dseg.get(), g.dsoff.get(), v_lo, v_hi, queues + 4, g.dine.get(), g.drow.get(), g.cbits.get(), g.core_words,
         g.cb, g.cb - g.h0, g.core_min, g.rowd.get(), g.r0, g.colH.get(), t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_dense");
   }
-  if (timing) TC_CUDA(cudaEventRecord(ev.e[8], s));
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[8], sl));
+  if (fork) {  // join
+    TC_CUDA(cudaEventRecord(g.join_hi, sh));
+    TC_CUDA(cudaEventRecord(g.join_lo, sl));
+    TC_CUDA(cudaStreamWaitEvent(s, g.join_hi, 0));
+    TC_CUDA(cudaStreamWaitEvent(s, g.join_lo, 0));
+  }
+  if (timing) TC_CUDA(cudaEventRecord(ev.e[12], s));
   if (pv && kUseMasks && n && g.mask_total) {
     // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics); a split
     // count folds only the items of its own pivots
@@ -2052,9 +2086,9 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     stats->part_last_vertex = v_hi;
     stats->warp_ms = ev.ms(4, 5);
     stats->small_ms = ev.ms(5, 6);
-    stats->cta_ms = ev.ms(6, 7);
+    stats->cta_ms = ev.ms(10, 11);
     stats->dense_ms = ev.ms(7, 8);
-    stats->rows_ms = ev.ms(8, 9);
+    stats->rows_ms = ev.ms(12, 9);
     if (opts.work_counters) {
       stats->items = plan.items;
       stats->wedges = plan.J;

@@ -51,6 +51,10 @@ enum ScratchSlot {
 struct tc_graph {
   int device = 0;
   cudaStream_t own_stream = nullptr;
+  // count fork/join (count.cu): the CTA join on a high-priority stream, the
+  // warp / small / dense joins on a low-priority one, so they fill its tail
+  cudaStream_t hi_stream = nullptr, lo_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_hi = nullptr, join_lo = nullptr;
   cudaStream_t stream = nullptr;
   uint32_t n = 0;
   uint64_t E = 0;
