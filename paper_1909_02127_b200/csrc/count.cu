@@ -433,6 +433,11 @@ struct ItemGeo {
 #define TCB_WARP_GROUP 4
 #endif
 constexpr int kWarpGroup = TCB_WARP_GROUP;
+#ifndef TCB_LANE_ITEM_CHUNKS
+#define TCB_LANE_ITEM_CHUNKS 4
+#endif
+// a batch whose items all span <= this many 4-id chunks is walked lane by lane
+constexpr uint32_t kLaneItemChunks = TCB_LANE_ITEM_CHUNKS;
 
 template <bool kPerVertex, typename Sink>
 __device__ __forceinline__ uint32_t warp_join_group(const uint4* __restrict__ irec, const uint32_t (&gi0)[kWarpGroup],
@@ -468,10 +473,25 @@ __device__ __forceinline__ uint32_t warp_join_group(const uint4* __restrict__ ir
         for (uint32_t t = 0; t < nb; ++t) z[t] = 0;
       }
     }
-    // compact the non-empty items to the low lanes (item_of needs nch >= 1);
-    // lane L takes the item of the (L+1)-th non-empty lane
     const uint32_t ne = __ballot_sync(0xffffffffu, nch > 0);
     if (!ne) continue;
+    if (__reduce_max_sync(0xffffffffu, nch) <= kLaneItemChunks) {
+      // short items (a uniform-degree graph's): every lane walks its own
+      // item's few chunks -- no chunk -> item mapping, no shuffles
+      uint32_t hl = 0;
+      for (uint32_t c = b >> 2, ce = c + nch; c < ce; ++c) hl += probe_cold<kPerVertex>(__ldg(col4 + c), c, b, e,
+                                                                                 tabs + tj * kWarpTable, mask, shift,
+                                                                                 sink);
+      hits += hl;
+      if (kPerVertex) {
+#pragma unroll
+        for (int j = 0; j < kWarpGroup; ++j) hseg[j] += tj == (uint32_t)j ? hl : 0u;
+        if (hl) atomicAdd(&sink.t_rank[u], (unsigned long long)hl);
+      }
+      continue;
+    }
+    // compact the non-empty items to the low lanes (item_of needs nch >= 1);
+    // lane L takes the item of the (L+1)-th non-empty lane
     uint32_t owner_u;
     {
       const uint32_t from = lane < (uint32_t)__popc(ne) ? __fns(ne, 0, lane + 1) : lane;
