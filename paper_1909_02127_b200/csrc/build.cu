@@ -961,6 +961,15 @@ struct InDeg {
 #ifndef TCB_IN_MATCH
 #define TCB_IN_MATCH 0
 #endif
+// max over pivots of deg(v) - d+(v) (the in-degree)
+__global__ void k_max_din(const uint32_t* __restrict__ inoff, uint32_t n, unsigned int* __restrict__ out) {
+  uint32_t m = 0;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, inoff[v + 1] - inoff[v]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31u) == 0 && m) atomicMax(out, m);
+}
+
 // Every oriented edge e = u->v to its head's slot
 // (TCB_IN_MATCH=1: warp-aggregated per head), as a 32-byte level-1 item record
 // (graph.cuh irec, one 256-bit store): the suffix geometry comes from u's row descriptor, read in
@@ -1258,6 +1267,14 @@ void finish_graph(tc_graph& g) {
   g.inoff.alloc((uint64_t)n + 1, s);
   scan_exclusive<uint32_t>(InDeg{g.off.get(), g.deg.get()}, g.inoff.get(), n, g.inoff.get() + n, s);
   g.irec.alloc(2 * (E ? E : 1), s);
+  g.max_din = 0;
+  if (n) {
+    DBuf<unsigned int> md(1, s);
+    TC_CUDA(cudaMemsetAsync(md.get(), 0, sizeof(unsigned int), s));
+    k_max_din<<<grid_gs(n, dev), kT, 0, s>>>(g.inoff.get(), n, md.get());
+    TC_LAUNCH();
+    g.max_din = read_scalar(md.get(), s);
+  }
   DBuf<uint8_t> dflag;
   if (E) {
     if (g.ndense) dflag.alloc(E, s);

@@ -465,7 +465,7 @@ __device__ __forceinline__ uint32_t warp_join_group(const uint4* __restrict__ ir
       const uint32_t hot = g4.y > g4.x ? g4.y - g4.x : 0u;
       e = b + (g4.w > g4.z ? g4.w - g4.z : 0u) + hot;
       nch = (b < e && ((probe_mask >> tj) & 1u)) ? ((e + 3) >> 2) - (b >> 2) : 0u;
-      if (kPerVertex && TCB_PV_MASKS && hot) {
+      if (kPerVertex && TCB_PV_MASKS && hot && masks) {
         // the row pass reads every item's sparse hot mask bytes: zero this
         // item's (its hits are counted here, per hit)
         uint8_t* z = masks + (ax.z | ((uint64_t)ax.w << 32));
@@ -543,13 +543,16 @@ template <bool kPerVertex>
 __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ col,
     const uint4* __restrict__ irec, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
+    const uint32_t* __restrict__ inoff, uint32_t v_lo, uint32_t v_hi,
     uint32_t gsz, uint32_t rc, uint32_t ncnt, uint8_t* __restrict__ masks,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   extern __shared__ uint32_t top_cnt[];
   __shared__ uint32_t s_tab[kJoinWarps][kWarpGroup * kWarpTable];
   __shared__ uint32_t s_item[kJoinWarps][32];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t nsegs = *nsegs_p;
+  // direct mode (inoff != null, no count plan): segment j is pivot v_lo + j
+  // with all its in-edge items -- every pivot of the graph fits one segment
+  const uint32_t nsegs = inoff ? v_hi - v_lo : *nsegs_p;
   uint32_t* tabs = s_tab[warp];
   for (uint32_t s = lane; s < kWarpGroup * kWarpTable; s += 32) tabs[s] = kEmpty;
   if (kPerVertex) {
@@ -568,7 +571,12 @@ __global__ void __launch_bounds__(kJoinThreads) k_join_warp(
     uint4 sgl = make_uint4(0, 0, 0, 0);
     uint32_t nbl = 0, dvl = 0;
     if (lane < gsz && g0 + lane < nsegs) {
-      sgl = segs[g0 + lane];
+      if (inoff) {
+        const uint32_t v = v_lo + (uint32_t)(g0 + lane);
+        sgl = make_uint4(v, inoff[v], inoff[v + 1], 0);
+      } else {
+        sgl = segs[g0 + lane];
+      }
       nbl = off[sgl.x];
       dvl = off[sgl.x + 1] - nbl;
     }
@@ -1915,8 +1923,14 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const bool split = v_lo != 0 || v_hi != n;
   Plan plan;
   constexpr bool kUseMasks = TCB_PV_MASKS;
-  kl += build_plan(g, v_lo, v_hi, pv, pv && kUseMasks, stats != nullptr && opts.work_counters != 0, plan);
-  uint8_t* masks = plan.masks;
+  // Uniform-degree graphs (every pivot's row and in-edge list fit one
+  // warp-bin segment, e.g. Erdos-Renyi): no plan, no CTA/small bins, no hit
+  // masks -- the warp join takes the pivots directly (TCB_DIRECT=0: off).
+  const bool direct = g.max_dplus <= kWarpMaxDeg && g.max_din <= kWarpSegItems && env_u32("TCB_DIRECT", 1) != 0;
+  const bool want_sums = stats != nullptr && opts.work_counters != 0;
+  if (!direct || want_sums) kl += build_plan(g, v_lo, v_hi, pv, pv && kUseMasks && !direct, want_sums, plan);
+  if (direct) plan.cap[1] = plan.cap[2] = 0;
+  uint8_t* masks = direct ? nullptr : plan.masks;
   pl.mark("plan");
   if (timing) TC_CUDA(cudaEventRecord(ev.e[1], s));
 
@@ -1987,18 +2001,20 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   }
   if (timing) TC_CUDA(cudaEventRecord(ev.e[11], sh));
   if (timing) TC_CUDA(cudaEventRecord(ev.e[4], sl));
-  if (plan.cap[0]) {
+  if (plan.cap[0] || direct) {
     // warp bin: plain 32-bit counters over half the window
     const uint32_t ncnt_w = ncnt / 2, rc_w = pv ? n - ncnt_w : 0xffffffffu;
     const size_t smem = (size_t)ncnt_w * sizeof(uint32_t);
     auto kern = pv ? k_join_warp<true> : k_join_warp<false>;
     const int occ = occupancy(kern, kJoinThreads, smem);
     const uint64_t resident_warps = (uint64_t)sms * occ * kJoinWarps;
-    const uint32_t gsz = plan.cap[0] >= (uint64_t)kWarpGroup * resident_warps ? kWarpGroup : 1u;
+    const uint64_t nseg_w = direct ? (uint64_t)(v_hi - v_lo) : plan.cap[0];
+    const uint32_t gsz = nseg_w >= (uint64_t)kWarpGroup * resident_warps ? kWarpGroup : 1u;
     const unsigned grid =
-        (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(plan.cap[0], gsz), kJoinWarps), (uint64_t)sms * occ);
-    kern<<<grid, kJoinThreads, smem, sl>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(), plan.wsegs,
-                                          plan.nseg + 0, gsz, rc_w, ncnt_w, masks, t_rank, acc);
+        (unsigned)std::min<uint64_t>(ceil_div64(ceil_div64(nseg_w, gsz), kJoinWarps), (uint64_t)sms * occ);
+    kern<<<grid ? grid : 1, kJoinThreads, smem, sl>>>(g.off.get(), g.rowd.get(), g.r0, g.col.get(), g.irec.get(),
+                                                     plan.wsegs, plan.nseg + 0, direct ? g.inoff.get() : nullptr,
+                                                     v_lo, v_hi, gsz, rc_w, ncnt_w, masks, t_rank, acc);
     TC_LAUNCH();
     ++launches;
     pl.mark("join_warp");
@@ -2041,7 +2057,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     TC_CUDA(cudaStreamWaitEvent(s, g.join_lo, 0));
   }
   if (timing) TC_CUDA(cudaEventRecord(ev.e[12], s));
-  if (pv && kUseMasks && n && g.mask_total) {
+  if (pv && kUseMasks && n && g.mask_total && !direct) {
     // hot hit masks -> t[u], t[x] (row-major, no per-hit atomics); a split
     // count folds only the items of its own pivots
     unsigned int* rq = queues + 2;  // heavy queue, heavy count

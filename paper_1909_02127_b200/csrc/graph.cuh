@@ -60,6 +60,7 @@ struct tc_graph {
   uint64_t E = 0;
   uint32_t max_deg = 0;
   uint32_t max_dplus = 0;
+  uint32_t max_din = 0;  // largest in-degree in the orientation (in-edge items of one pivot)
   int id_bits = 1;  // bits_for(n-1)
   double build_ms = 0;
   tcb::DBuf<uint32_t> off, col, src, deg, id_of, rank_of;
