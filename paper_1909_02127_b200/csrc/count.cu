@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
                                    return (uint32_t)__popc(m);
                                  });
     }
-    if (ncold && !(g_pv_dbg & 4)) {
+    if (ncold && cold && !(g_pv_dbg & 4)) {  // a pivot with no cold members: no cold candidate can hit
       const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kJoinWarps);
       const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kJoinWarps);
       if (tab == stab)  // SMEM table (LDS probes); the global slab only for huge pivots
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
                                          }
                                          return (uint32_t)__popc(m);
                                        });
-    if (ncold)
+    if (ncold && cold)  // a pivot with no cold members: no cold candidate can hit
       h += warp_walk<4, 2>(0, tcc, ncold, w.cpre, w.cb, w.ce, w.cidx, kPerVertex ? w.icnt : nullptr, col,
                            [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
                              return probe_cold<kPerVertex>(qq, c, b, e, w.tab, tmask, tshift, sink, w.cf);
