@@ -958,9 +958,6 @@ struct InDeg {
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const { return deg[v] - (off[v + 1] - off[v]); }
 };
 
-#ifndef TCB_IN_MATCH
-#define TCB_IN_MATCH 0
-#endif
 // max over pivots of deg(v) - d+(v) (the in-degree)
 __global__ void k_max_din(const uint32_t* __restrict__ inoff, uint32_t n, unsigned int* __restrict__ out) {
   uint32_t m = 0;
@@ -970,36 +967,38 @@ __global__ void k_max_din(const uint32_t* __restrict__ inoff, uint32_t n, unsign
   if ((threadIdx.x & 31u) == 0 && m) atomicMax(out, m);
 }
 
-// Every oriented edge e = u->v to its head's slot
-// (TCB_IN_MATCH=1: warp-aggregated per head), as a 32-byte level-1 item record
+// Every oriented edge e = u->v to its head's slot (one atomic per edge: a
+// warp's 32 edges come from one or two rows, so their heads rarely repeat),
+// as a 32-byte level-1 item record
 // (graph.cuh irec, one 256-bit store): the suffix geometry comes from u's row descriptor, read in
 // edge order (consecutive edges share their row).  With ccnt (rows [r0, n):
-// core members of a dense row, else 0), dflag[slot] = 1 for a dense item: u's
-// row is dense and e is not its last edge.
+// core members of a dense row, else 0), bit `slot` of dbits marks a dense
+// item: u's row is dense and e is not its last edge.
 __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* __restrict__ src, uint64_t E,
                              uint32_t* __restrict__ cur, const uint4* __restrict__ rowd, uint32_t r0,
                              uint4* __restrict__ irec, const uint32_t* __restrict__ ccnt,
-                             uint8_t* __restrict__ dflag) {
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < E; base += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = base + threadIdx.x;
-    const bool ok = e < E;
-    const uint32_t v = ok ? col[e] : 0xffffffffu;
-#if TCB_IN_MATCH
-    const unsigned peers = __match_any_sync(0xffffffffu, v);
-    const unsigned lane = threadIdx.x & 31u;
-    const int leader = __ffs(peers) - 1;
-    uint32_t b = 0;
-    if (ok && (int)lane == leader) b = atomicAdd(&cur[v], (unsigned)__popc(peers));
-    b = __shfl_sync(0xffffffffu, b, leader);
-    const uint32_t slot0 = b + __popc(peers & lanemask_lt());
-#else
-    // a warp's 32 edges come from one or two rows: their heads repeat only
-    // rarely, so per-edge atomics beat a match_any aggregation
-    const uint32_t slot0 = ok ? atomicAdd(&cur[v], 1u) : 0u;
-#endif
-    if (ok) {
-      const uint32_t slot = slot0, u = src[e];
-      const RowGeo r(rowd[2 * (uint64_t)(u - r0)], rowd[2 * (uint64_t)(u - r0) + 1]);
+                             uint32_t* __restrict__ dbits) {
+  // kInEdges independent edges per thread per step (coalesced per k): the
+  // slot atomics' return latency, not bandwidth, bounds this pass
+  constexpr int kInEdges = 4;
+  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * kInEdges;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kInEdges + threadIdx.x; base < E; base += step) {
+    uint32_t v[kInEdges], u[kInEdges], slot[kInEdges];
+    bool ok[kInEdges];
+#pragma unroll
+    for (int k = 0; k < kInEdges; ++k) {
+      const uint64_t e = base + (uint64_t)k * blockDim.x;
+      ok[k] = e < E;
+      v[k] = ok[k] ? col[e] : 0u;
+      u[k] = ok[k] ? src[e] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kInEdges; ++k) slot[k] = ok[k] ? atomicAdd(&cur[v[k]], 1u) : 0u;
+#pragma unroll
+    for (int k = 0; k < kInEdges; ++k) {
+      if (!ok[k]) continue;
+      const uint64_t e = base + (uint64_t)k * blockDim.x;
+      const RowGeo r(rowd[2 * (uint64_t)(u[k] - r0)], rowd[2 * (uint64_t)(u[k] - r0) + 1]);
       uint4 geo = make_uint4(0, 0, 0, 0);
       uint64_t mo = 0;
       const uint32_t a = (uint32_t)e + 1;
@@ -1008,8 +1007,8 @@ __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* _
         geo = a >= ce ? make_uint4(r.O + (a - ce), r.Ht, 0, 0) : make_uint4(r.O, r.Ht, a, ce);
         if (geo.y > geo.x) mo = r.rowbase + r.masks().P((uint32_t)e - r.beg);
       }
-      st256(irec + 2 * (uint64_t)slot, geo, make_uint4((uint32_t)e, u, (uint32_t)mo, (uint32_t)(mo >> 32)));
-      if (dflag) dflag[slot] = (ccnt[u - r0] != 0 && a < r.end) ? 1 : 0;
+      st256(irec + 2 * (uint64_t)slot[k], geo, make_uint4((uint32_t)e, u[k], (uint32_t)mo, (uint32_t)(mo >> 32)));
+      if (dbits && a < r.end && ccnt[u[k] - r0] != 0) atomicOr(&dbits[slot[k] >> 5], 1u << (slot[k] & 31));
     }
   }
 }
@@ -1069,29 +1068,40 @@ __global__ void k_rowbase_put(const uint64_t* __restrict__ rb, uint32_t nr, uint
 
 // Dense in-edge list: in-edge i = {e, u} of pivot v is a dense item when u's
 // row is dense and its suffix after v is non-empty (dflag, k_in_scatter).
-struct ByteFlag {
-  const uint8_t* f;
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return f[i]; }
+// Dense-item flags as a bit array over the in-edge slots (E bits: L2-resident
+// while the in-edge scatter sets them) and their word popcount prefix wp: the
+// dense-list position of slot i is wp[i / 32] + the set bits below it.
+struct WordPopc {
+  const uint32_t* w;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return __popc(w[i]); }
 };
-__global__ void k_dense_scatter(const uint4* __restrict__ irec, uint64_t E, const uint8_t* __restrict__ dflag,
-                                const uint32_t* __restrict__ dpos, uint32_t r0, const uint32_t* __restrict__ ip,
-                                uint32_t* __restrict__ dine) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
-    if (dflag[i]) dine[ip[i]] = dpos[irec[2 * i + 1].y - r0];
+__device__ __forceinline__ uint32_t dense_pos(const uint32_t* __restrict__ dbits, const uint32_t* __restrict__ wp,
+                                              uint64_t i) {
+  return wp[i >> 5] + __popc(dbits[i >> 5] & ((1u << (i & 31)) - 1u));
 }
-// Dense segments of pivot v: its dense items [dpos[inoff[v]], dpos[inoff[v+1]])
+__global__ void k_dense_scatter(const uint4* __restrict__ irec, uint64_t E, const uint32_t* __restrict__ dbits,
+                                const uint32_t* __restrict__ wp, const uint32_t* __restrict__ dpos, uint32_t r0,
+                                uint32_t* __restrict__ dine) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = dbits[i >> 5];
+    if ((w >> (i & 31)) & 1u) dine[wp[i >> 5] + __popc(w & ((1u << (i & 31)) - 1u))] = dpos[irec[2 * i + 1].y - r0];
+  }
+}
+// Dense segments of pivot v: its dense items [pos(inoff[v]), pos(inoff[v+1]))
 struct DenseSegs {
   const uint32_t* inoff;
-  const uint32_t* dpos;
+  const uint32_t* dbits;
+  const uint32_t* wp;
   __device__ __forceinline__ uint32_t operator()(uint64_t v) const {
-    const uint32_t c = dpos[inoff[v + 1]] - dpos[inoff[v]];
+    const uint32_t c = dense_pos(dbits, wp, inoff[v + 1]) - dense_pos(dbits, wp, inoff[v]);
     return (c + kDenseSeg - 1) / kDenseSeg;
   }
 };
-__global__ void k_dense_segs(const uint32_t* __restrict__ inoff, const uint32_t* __restrict__ dpos, uint32_t n,
-                             const uint32_t* __restrict__ dsoff, uint4* __restrict__ dseg) {
+__global__ void k_dense_segs(const uint32_t* __restrict__ inoff, const uint32_t* __restrict__ dbits,
+                             const uint32_t* __restrict__ wp, uint32_t n, const uint32_t* __restrict__ dsoff,
+                             uint4* __restrict__ dseg) {
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = dpos[inoff[v]], b = dpos[inoff[v + 1]];
+    const uint32_t a = dense_pos(dbits, wp, inoff[v]), b = dense_pos(dbits, wp, inoff[v + 1]);
     uint32_t s = dsoff[v];
     for (uint32_t i = a; i < b; i += kDenseSeg) dseg[s++] = make_uint4((uint32_t)v, i, min(i + kDenseSeg, b), 0);
   }
@@ -1275,14 +1285,18 @@ void finish_graph(tc_graph& g) {
     TC_LAUNCH();
     g.max_din = read_scalar(md.get(), s);
   }
-  DBuf<uint8_t> dflag;
+  DBuf<uint32_t> dbits;
+  const uint64_t nwords = (E + 31) / 32;
   if (E) {
-    if (g.ndense) dflag.alloc(E, s);
+    if (g.ndense) {
+      dbits.alloc(nwords + 1, s);
+      TC_CUDA(cudaMemsetAsync(dbits.get(), 0, sizeof(uint32_t) * (nwords + 1), s));
+    }
     DBuf<uint32_t> cur(n, s);
     TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
     k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.rowd.get(), g.r0,
                                                 g.irec.get(), g.ndense ? ccnt.get() : nullptr,
-                                                dflag.get());
+                                                dbits.get());
     TC_LAUNCH();
   }
   pl.mark("fin_in_scatter");
@@ -1294,23 +1308,25 @@ void finish_graph(tc_graph& g) {
   g.dsoff.alloc((uint64_t)n + 1, s);
   TC_CUDA(cudaMemsetAsync(g.dsoff.get(), 0, sizeof(uint32_t) * ((uint64_t)n + 1), s));
   if (g.ndense && E) {
-    DBuf<uint32_t> ip(E + 1, s);
-    scan_exclusive<uint32_t>(ByteFlag{dflag.get()}, ip.get(), E, ip.get() + E, s);
-    g.ndine = read_scalar(ip.get() + E, s);
+    DBuf<uint32_t> wp(nwords + 2, s);
+    scan_exclusive<uint32_t>(WordPopc{dbits.get()}, wp.get(), nwords + 1, wp.get() + nwords + 1, s);
+    g.ndine = read_scalar(wp.get() + nwords + 1, s);
     g.dine.alloc(g.ndine ? g.ndine : 1, s);
     if (g.ndine) {
-      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.irec.get(), E, dflag.get(), dpos.get(), g.r0, ip.get(),
+      k_dense_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.irec.get(), E, dbits.get(), wp.get(), dpos.get(), g.r0,
                                                      g.dine.get());
       TC_LAUNCH();
     }
-    dflag.release();
-    scan_exclusive<uint32_t>(DenseSegs{g.inoff.get(), ip.get()}, g.dsoff.get(), n, g.dsoff.get() + n, s);
+    scan_exclusive<uint32_t>(DenseSegs{g.inoff.get(), dbits.get(), wp.get()}, g.dsoff.get(), n, g.dsoff.get() + n,
+                             s);
     const uint32_t nseg = read_scalar(g.dsoff.get() + n, s);
     g.dseg.alloc(nseg ? nseg : 1, s);
     if (nseg) {
-      k_dense_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.inoff.get(), ip.get(), n, g.dsoff.get(), g.dseg.get());
+      k_dense_segs<<<grid_gs(n, dev), kT, 0, s>>>(g.inoff.get(), dbits.get(), wp.get(), n, g.dsoff.get(),
+                                                  g.dseg.get());
       TC_LAUNCH();
     }
+    dbits.release();
     g.drow.alloc(g.ndense, s);
     k_dense_rows<<<grid_gs(nr, dev), kT, 0, s>>>(g.rowd.get(), g.r0, nr, g.drow.get());
     TC_LAUNCH();
