@@ -42,6 +42,11 @@ namespace {
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
+#ifndef TCB_CTA_THREADS
+#define TCB_CTA_THREADS 256
+#endif
+constexpr int kCtaThreads = TCB_CTA_THREADS;  // k_join_cta block (kCtaSegItems a multiple of it)
+constexpr int kCtaWarps = kCtaThreads / 32;
 constexpr uint32_t kWarpTable = 128;         // warp-bin hash slots (d+ <= kWarpMaxDeg = 64)
 constexpr uint32_t kTopCounters = 1u << 13;  // per-vertex SMEM counters (16-bit halves: 16 KB)
 #ifndef TCB_CTA_SMEM_SLOTS
@@ -814,7 +819,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_join_dense(
 // Segments come from a global queue, heaviest (top-rank pivots) first.
 // Dynamic SMEM: [hot bitmap nbm words][cold hash kCtaSmemSlots].
 template <bool kPerVertex>
-__global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
+__global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_join_cta(
     const uint32_t* __restrict__ off, const uint32_t* __restrict__ col, const uint4* __restrict__ rowd, uint32_t r0,
     const uint16_t* __restrict__ colH, const uint4* __restrict__ irec,
     const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p, unsigned int* __restrict__ queue,
@@ -833,8 +838,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   __shared__ uint32_t s_icnt[kPerVertex ? kCtaSegItems : 1];
   __shared__ uint32_t s_cf[kColdFilterWords];  // cold-member prefilter
   __shared__ uint32_t s_hits, s_cold, s_nl;
-  __shared__ uint32_t s_wl[kJoinWarps];
-  __shared__ unsigned long long s_wc[kJoinWarps];
+  __shared__ uint32_t s_wl[kCtaWarps];
+  __shared__ unsigned long long s_wc[kCtaWarps];
   __shared__ uint32_t s_desc[6];  // current segment: v, i0, ni, off[v], d+(v), queue index
   __shared__ unsigned long long s_ctot;
   // the segment's in-edge records {e, u}, bulk-copied (TMA) one segment ahead
@@ -847,14 +852,14 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
   uint32_t* gtab = gslab + (uint64_t)blockIdx.x * slab_cap;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t nsegs = *nsegs_p;
-  for (uint32_t i = threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
-  for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kJoinThreads) stab[i] = kEmpty;
-  for (uint32_t i = threadIdx.x; i < slab_cap; i += kJoinThreads) gtab[i] = kEmpty;
-  for (uint32_t i = threadIdx.x; i < kColdFilterWords; i += kJoinThreads) s_cf[i] = 0;
+  for (uint32_t i = threadIdx.x; i < nbm; i += kCtaThreads) bm[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kCtaSmemSlots; i += kCtaThreads) stab[i] = kEmpty;
+  for (uint32_t i = threadIdx.x; i < slab_cap; i += kCtaThreads) gtab[i] = kEmpty;
+  for (uint32_t i = threadIdx.x; i < kColdFilterWords; i += kCtaThreads) s_cf[i] = 0;
   if (kPerVertex)
-    for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kJoinThreads) s_icnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < kCtaSegItems; i += kCtaThreads) s_icnt[i] = 0;
   if (kHits)
-    for (uint32_t i = threadIdx.x; i < ncnt / 2; i += kJoinThreads) top[i] = 0;
+    for (uint32_t i = threadIdx.x; i < ncnt / 2; i += kCtaThreads) top[i] = 0;
   // cold hits (x < h0) go straight to global atomics; hot hits leave as masks
   // (kMasks) or go to the top counters / global atomics (kHits)
   const PvSink<true> sink{nullptr, 0xffffffffu, t_rank, g_pv_dbg};
@@ -896,8 +901,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     __syncthreads();
     if (s_desc[5] < nsegs) {
 #pragma unroll
-      for (int r = 0; r < kCtaSegItems / kJoinThreads; ++r) {
-        const uint32_t i = threadIdx.x * (kCtaSegItems / kJoinThreads) + r;
+      for (int r = 0; r < kCtaSegItems / kCtaThreads; ++r) {
+        const uint32_t i = threadIdx.x * (kCtaSegItems / kCtaThreads) + r;
         if (i < s_desc[2]) cp_async16(&s_ine[i], irec + 2 * ((uint64_t)s_desc[1] + i));
       }
     }
@@ -918,7 +923,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       if (qnext < nsegs) s_sgn = segs[nsegs - 1 - qnext];
     }
     // (1a) hot members -> bitmap; s_cold = #members below h0 (sorted prefix)
-    for (uint32_t j = threadIdx.x; j < dv; j += kJoinThreads) {
+    for (uint32_t j = threadIdx.x; j < dv; j += kCtaThreads) {
       const uint32_t x = col[nb + j];
       if (x >= h0) {
         atomicOr(&bm[(x - h0) >> 5], 1u << ((x - h0) & 31));
@@ -928,8 +933,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       }
     }
     // (1b) stage items, compacted into hot / cold lists with chunk prefixes
-    constexpr int kIPT = kCtaSegItems / kJoinThreads;  // items per thread
-    static_assert(kCtaSegItems % kJoinThreads == 0, "segment items must be a multiple of the CTA size");
+    constexpr int kIPT = kCtaSegItems / kCtaThreads;  // items per thread
+    static_assert(kCtaSegItems % kCtaThreads == 0, "segment items must be a multiple of the CTA size");
     uint4 it[kIPT];
     uint64_t mo[kIPT];
     uint32_t nh[kIPT], nc[kIPT];
@@ -974,15 +979,15 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       }
       __syncthreads();
       if (warp == 0) {
-        const uint32_t xl = lane < kJoinWarps ? s_wl[lane] : 0u;
-        const unsigned long long xc = lane < kJoinWarps ? s_wc[lane] : 0ull;
+        const uint32_t xl = lane < kCtaWarps ? s_wl[lane] : 0u;
+        const unsigned long long xc = lane < kCtaWarps ? s_wc[lane] : 0ull;
         const uint32_t yl = warp_inclusive_scan(xl);
         const unsigned long long yc = warp_inclusive_scan(xc);
-        if (lane < kJoinWarps) {
+        if (lane < kCtaWarps) {
           s_wl[lane] = yl - xl;
           s_wc[lane] = yc - xc;
         }
-        if (lane == kJoinWarps - 1) {
+        if (lane == kCtaWarps - 1) {
           s_nl = yl;
           s_ctot = yc;
         }
@@ -1050,7 +1055,7 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
       tmask = ts - 1;
       tshift = __clz(ts) + 1;  // 32 - log2(ts), ts a power of two
       tab = ts <= stab_slots ? stab : gtab;
-      for (uint32_t j = threadIdx.x; j < cold; j += kJoinThreads) {
+      for (uint32_t j = threadIdx.x; j < cold; j += kCtaThreads) {
         const uint32_t x = col[nb + j];
         hash_insert(tab, tmask, tshift, x);
         const uint32_t f = cfilt_bit(x);
@@ -1063,8 +1068,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     uint32_t h = 0;
     uint32_t* icnt = kPerVertex ? s_icnt : nullptr;
     if (!(g_pv_dbg & 4)) {
-      const uint32_t fb = (uint32_t)(((uint64_t)tchunks_h * warp) / kJoinWarps);
-      const uint32_t fe = (uint32_t)(((uint64_t)tchunks_h * (warp + 1)) / kJoinWarps);
+      const uint32_t fb = (uint32_t)(((uint64_t)tchunks_h * warp) / kCtaWarps);
+      const uint32_t fe = (uint32_t)(((uint64_t)tchunks_h * (warp + 1)) / kCtaWarps);
       // per-vertex: the hot chunk's 8-bit hit mask goes to HBM (one byte store,
       // coalesced across the lanes of an item); k_pv_rows turns the masks into
       // t[u] and t[x] row by row, with no per-hit atomics
@@ -1082,8 +1087,8 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
                                  });
     }
     if (ncold && cold && !(g_pv_dbg & 4)) {  // a pivot with no cold members: no cold candidate can hit
-      const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kJoinWarps);
-      const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kJoinWarps);
+      const uint32_t fb = (uint32_t)(((uint64_t)tchunks_c * warp) / kCtaWarps);
+      const uint32_t fe = (uint32_t)(((uint64_t)tchunks_c * (warp + 1)) / kCtaWarps);
       if (tab == stab)  // SMEM table (LDS probes); the global slab only for huge pivots
         h += warp_walk<4, 2>(fb, fe, ncold, s_cpre, s_cb, s_ce, s_cidx, icnt, col,
                              [&](const uint4& qq, uint32_t c, uint32_t b, uint32_t e, uint32_t) {
@@ -1125,16 +1130,16 @@ __global__ void __launch_bounds__(kJoinThreads, kCtaMinBlocks) k_join_cta(
     // hot members (no global re-read), else the touched words
     if (dv - cold > nbm / 8) {
       uint4* bm4 = reinterpret_cast<uint4*>(bm);
-      for (uint32_t i = threadIdx.x; i < nbm / 4; i += kJoinThreads) bm4[i] = make_uint4(0, 0, 0, 0);
-      for (uint32_t i = (nbm & ~3u) + threadIdx.x; i < nbm; i += kJoinThreads) bm[i] = 0;
+      for (uint32_t i = threadIdx.x; i < nbm / 4; i += kCtaThreads) bm4[i] = make_uint4(0, 0, 0, 0);
+      for (uint32_t i = (nbm & ~3u) + threadIdx.x; i < nbm; i += kCtaThreads) bm[i] = 0;
     } else {
-      for (uint32_t j = cold + threadIdx.x; j < dv; j += kJoinThreads) bm[(col[nb + j] - h0) >> 5] = 0;
+      for (uint32_t j = cold + threadIdx.x; j < dv; j += kCtaThreads) bm[(col[nb + j] - h0) >> 5] = 0;
     }
-    for (uint32_t j = threadIdx.x; j < ts; j += kJoinThreads) tab[j] = kEmpty;
+    for (uint32_t j = threadIdx.x; j < ts; j += kCtaThreads) tab[j] = kEmpty;
     if (cold)
-      for (uint32_t j = threadIdx.x; j < kColdFilterWords; j += kJoinThreads) s_cf[j] = 0;
+      for (uint32_t j = threadIdx.x; j < kColdFilterWords; j += kCtaThreads) s_cf[j] = 0;
     if (kPerVertex) {
-      for (uint32_t i = threadIdx.x; i < ni; i += kJoinThreads) {
+      for (uint32_t i = threadIdx.x; i < ni; i += kCtaThreads) {
         const uint32_t c = s_icnt[i];
         if (c) {
           atomicAdd(&t_rank[irec[2 * (uint64_t)(i0 + i) + 1].y], (unsigned long long)c);
@@ -1969,7 +1974,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   const size_t cta_dsm = ((size_t)nbm + kCtaSmemSlots + ncnt_hits0 / 2) * sizeof(uint32_t);
   auto cta_kern = pv ? k_join_cta<true> : k_join_cta<false>;
   const unsigned cta_grid =
-      plan.cap[1] ? (unsigned)std::min<uint64_t>((uint64_t)sms * occupancy(cta_kern, kJoinThreads, cta_dsm), plan.cap[1])
+      plan.cap[1] ? (unsigned)std::min<uint64_t>((uint64_t)sms * occupancy(cta_kern, kCtaThreads, cta_dsm), plan.cap[1])
                   : 0u;
   uint32_t* slab = plan.cap[1] ? g.scratch[kSlotSlab].get<uint32_t>((uint64_t)cta_grid * slab_cap + 1, s) : nullptr;
   cudaStream_t sh = s, sl = s;
@@ -1992,7 +1997,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   if (plan.cap[1]) {
     // cold members spill to a per-CTA global slab only when a pivot has more
     // than smem_slots/2 members below h0
-    cta_kern<<<cta_grid, kJoinThreads, cta_dsm, sh>>>(
+    cta_kern<<<cta_grid, kCtaThreads, cta_dsm, sh>>>(
         g.off.get(), g.col.get(), g.rowd.get(), g.r0, g.colH.get(), g.irec.get(), plan.csegs, plan.nseg + 1,
         queues + 1, g.h0, nbm, smem_slots, slab_cap, slab, masks, rc_hits0, ncnt_hits0, t_rank, acc);
     TC_LAUNCH();
