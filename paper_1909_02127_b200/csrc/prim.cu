@@ -1,6 +1,10 @@
 // prim.cu -- radix sort kernels (see prim.cuh).
 #include "prim.cuh"
 
+#ifndef TCB_RS_MATCH
+#define TCB_RS_MATCH 0
+#endif
+
 namespace tcb {
 
 int num_sms(int device) {
@@ -10,6 +14,23 @@ int num_sms(int device) {
 }
 
 namespace {
+
+// Lanes of the warp holding the same 8-bit digit as this lane (d = 256:
+// invalid lane, never matched): eight ballots instead of a match_any, whose
+// MIO-pipe cost bounded the passes (profiles/README.md).
+__device__ __forceinline__ unsigned digit_peers(unsigned d) {
+#if TCB_RS_MATCH
+  return __match_any_sync(0xffffffffu, d);
+#else
+  unsigned peers = __ballot_sync(0xffffffffu, d < 256u);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    peers &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return d < 256u ? peers : (1u << (threadIdx.x & 31u));
+#endif
+}
 
 __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n,
                                                         int shift, uint32_t* __restrict__ hist,
@@ -24,7 +45,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const uint64_t* __restri
     const uint64_t idx = base + (uint64_t)it * kRsThreads + threadIdx.x;
     const bool valid = idx < n;
     const unsigned d = valid ? (unsigned)((keys[idx] >> shift) & 255u) : 256u;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned peers = digit_peers(d);
     if (valid && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&h[d], (uint32_t)__popc(peers));
   }
   __syncthreads();
@@ -58,11 +79,13 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint64_t* __res
   for (int w = 0; w < kRsWarps; ++w) wh[w][threadIdx.x] = 0;
   __syncthreads();
 
-  // pass 1: per-warp digit counts, in key order
+  // pass 1: per-warp digit counts, in key order (the peer masks are kept for
+  // pass 2)
+  unsigned pm[kRsKpt];
 #pragma unroll
   for (int it = 0; it < kRsKpt; ++it) {
-    const unsigned peers = __match_any_sync(0xffffffffu, d[it]);
-    if (d[it] < 256u && lane == (unsigned)(__ffs(peers) - 1)) wh[warp][d[it]] += __popc(peers);
+    pm[it] = digit_peers(d[it]);
+    if (d[it] < 256u && lane == (unsigned)(__ffs(pm[it]) - 1)) wh[warp][d[it]] += __popc(pm[it]);
     __syncwarp();
   }
   __syncthreads();
@@ -96,7 +119,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint64_t* __res
   const unsigned lt = lanemask_lt();
 #pragma unroll
   for (int it = 0; it < kRsKpt; ++it) {
-    const unsigned peers = __match_any_sync(0xffffffffu, d[it]);
+    const unsigned peers = pm[it];
     if (d[it] < 256u) {
       const uint32_t pos = wh[warp][d[it]] + __popc(peers & lt);
       stage[pos] = k[it];

@@ -133,7 +133,10 @@ int scan_exclusive(Load load, T* out, uint64_t n, T* d_total, cudaStream_t s, T*
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsKpt = 16;                       // keys per thread
+#ifndef TCB_RS_KPT
+#define TCB_RS_KPT 8
+#endif
+constexpr int kRsKpt = TCB_RS_KPT;               // keys per thread
 constexpr int kRsTile = kRsThreads * kRsKpt;     // 4096 keys per tile
 constexpr int kRsWarpKeys = 32 * kRsKpt;         // 512 keys per warp
 
