@@ -72,7 +72,23 @@ __global__ void k_unique_scatter(const uint64_t* __restrict__ k, uint64_t m, uin
 }
 
 // Undirected degree of both endpoints; keys sorted by the low endpoint, so the
-// low side is aggregated per warp with match_any (hub rows are long runs).
+// low side is aggregated per run of equal sorted keys (hub rows are long runs).
+// Run aggregation over a warp's 32 consecutive entries of a sorted key
+// stream: the first lane of each run of equal keys adds the run length (the
+// valid lanes are a prefix).  Replaces match_any, whose MIO cost is high.
+__device__ __forceinline__ void add_sorted_runs(uint32_t key, bool valid, uint32_t* __restrict__ cnt) {
+  const unsigned lane = lane_id();
+  const uint32_t up = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = valid && (lane == 0 || up != key);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+  if (head) {
+    const unsigned above = lane == 31 ? 0u : heads & ~((2u << lane) - 1u);
+    const unsigned next = above ? (unsigned)(__ffs(above) - 1) : nvalid;
+    atomicAdd(&cnt[key], next - lane);
+  }
+}
+
 __global__ void k_degree(const uint64_t* __restrict__ k, uint64_t E, int b, uint32_t* __restrict__ deg) {
   const uint64_t mask = (b >= 32) ? 0xffffffffull : ((1ull << b) - 1);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -82,8 +98,7 @@ __global__ void k_degree(const uint64_t* __restrict__ k, uint64_t E, int b, uint
     const uint64_t x = valid ? k[i] : 0;
     const uint32_t lo = valid ? (uint32_t)(x >> b) : 0xffffffffu;
     const uint32_t hi = (uint32_t)(x & mask);
-    const unsigned peers = __match_any_sync(0xffffffffu, lo);
-    if (valid && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&deg[lo], (uint32_t)__popc(peers));
+    add_sorted_runs(lo, valid, deg);  // keys are sorted: equal low ids are adjacent
     if (valid) atomicAdd(&deg[hi], 1u);
   }
 }
@@ -141,8 +156,7 @@ __global__ void k_split_oriented(const uint64_t* __restrict__ ok, uint64_t E, in
       col[i] = (uint32_t)(x & mask);
       src[i] = s;
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, s);
-    if (valid && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&dplus[s], (uint32_t)__popc(peers));
+    add_sorted_runs(s, valid, dplus);
   }
 }
 
