@@ -988,31 +988,80 @@ __global__ void k_max_din(const uint32_t* __restrict__ inoff, uint32_t n, unsign
 // edge order (consecutive edges share their row).  With ccnt (rows [r0, n):
 // core members of a dense row, else 0), bit `slot` of dbits marks a dense
 // item: u's row is dense and e is not its last edge.
-__global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* __restrict__ src, uint64_t E,
-                             uint32_t* __restrict__ cur, const uint4* __restrict__ rowd, uint32_t r0,
-                             uint4* __restrict__ irec, const uint32_t* __restrict__ ccnt,
-                             uint32_t* __restrict__ dbits) {
-  // kInEdges independent edges per thread per step (coalesced per k): the
-  // slot atomics' return latency, not bandwidth, bounds this pass
-  constexpr int kInEdges = 4;
-  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * kInEdges;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kInEdges + threadIdx.x; base < E; base += step) {
-    uint32_t v[kInEdges], u[kInEdges], slot[kInEdges];
+// The slot atomics of the hub heads (the top `nhub` ranks: degrees ascend
+// with rank, so these take the largest share of the in-edges) are aggregated
+// per CTA tile in shared memory: one global atomic per (tile, hub head) claims
+// the tile's run of slots, the per-edge SMEM atomic's return value places the
+// edge inside it.  Other heads take one global atomic per edge.  Measured
+// at C4 (profiles/README.md): 10.0 -> 7.4 ms with 512 hub counters (4096:
+// 8.3 ms, the per-tile reset and the SMEM footprint start to cost).
+template <int kInEdges>
+__global__ void __launch_bounds__(256) k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* __restrict__ src,
+                                                    uint64_t E, uint32_t* __restrict__ cur,
+                                                    const uint4* __restrict__ rowd, uint32_t r0,
+                                                    uint4* __restrict__ irec, const uint32_t* __restrict__ ccnt,
+                                                    uint32_t* __restrict__ dbits, uint32_t hub_lo, uint32_t nhub) {
+  // kInEdges independent edges per thread per tile (coalesced per k).  The
+  // row descriptor loads (which need only u) are issued next to the slot
+  // atomics: two dependent round trips per tile, not three.
+  extern __shared__ uint32_t s_hub[];  // [nhub] counts, then bases
+  __shared__ uint32_t s_list[256 * kInEdges];
+  __shared__ uint32_t s_nlist;
+  for (uint32_t i = threadIdx.x; i < nhub; i += blockDim.x) s_hub[i] = 0;
+  if (threadIdx.x == 0) s_nlist = 0;
+  __syncthreads();
+  const uint64_t tile = (uint64_t)blockDim.x * kInEdges;
+  for (uint64_t base = (uint64_t)blockIdx.x * tile; base < E; base += (uint64_t)gridDim.x * tile) {
+    uint32_t v[kInEdges], u[kInEdges], slot[kInEdges], cc[kInEdges];
+    uint4 d0[kInEdges], d1[kInEdges];
     bool ok[kInEdges];
 #pragma unroll
     for (int k = 0; k < kInEdges; ++k) {
-      const uint64_t e = base + (uint64_t)k * blockDim.x;
+      const uint64_t e = base + (uint64_t)k * blockDim.x + threadIdx.x;
       ok[k] = e < E;
       v[k] = ok[k] ? col[e] : 0u;
-      u[k] = ok[k] ? src[e] : 0u;
+      u[k] = ok[k] ? src[e] : r0;
     }
 #pragma unroll
-    for (int k = 0; k < kInEdges; ++k) slot[k] = ok[k] ? atomicAdd(&cur[v[k]], 1u) : 0u;
+    for (int k = 0; k < kInEdges; ++k) {
+      const uint64_t i = u[k] - r0;
+      d0[k] = rowd[2 * i];
+      d1[k] = rowd[2 * i + 1];
+      cc[k] = dbits ? ccnt[i] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kInEdges; ++k) {
+      slot[k] = 0;
+      if (!ok[k]) continue;
+      if (v[k] >= hub_lo) {
+        const uint32_t h = v[k] - hub_lo;
+        slot[k] = atomicAdd(&s_hub[h], 1u);
+        if (slot[k] == 0) s_list[atomicAdd(&s_nlist, 1u)] = h;
+      } else {
+        slot[k] = atomicAdd(&cur[v[k]], 1u);
+      }
+    }
+    if (nhub) {
+      __syncthreads();
+      const uint32_t nl = s_nlist;
+      for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+        const uint32_t h = s_list[i];
+        s_hub[h] = atomicAdd(&cur[hub_lo + h], s_hub[h]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kInEdges; ++k)
+        if (ok[k] && v[k] >= hub_lo) slot[k] += s_hub[v[k] - hub_lo];
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) s_hub[s_list[i]] = 0;
+      if (threadIdx.x == 0) s_nlist = 0;
+      __syncthreads();
+    }
 #pragma unroll
     for (int k = 0; k < kInEdges; ++k) {
       if (!ok[k]) continue;
-      const uint64_t e = base + (uint64_t)k * blockDim.x;
-      const RowGeo r(rowd[2 * (uint64_t)(u[k] - r0)], rowd[2 * (uint64_t)(u[k] - r0) + 1]);
+      const uint64_t e = base + (uint64_t)k * blockDim.x + threadIdx.x;
+      const RowGeo r(d0[k], d1[k]);
       uint4 geo = make_uint4(0, 0, 0, 0);
       uint64_t mo = 0;
       const uint32_t a = (uint32_t)e + 1;
@@ -1022,7 +1071,7 @@ __global__ void k_in_scatter(const uint32_t* __restrict__ col, const uint32_t* _
         if (geo.y > geo.x) mo = r.rowbase + r.masks().P((uint32_t)e - r.beg);
       }
       st256(irec + 2 * (uint64_t)slot[k], geo, make_uint4((uint32_t)e, u[k], (uint32_t)mo, (uint32_t)(mo >> 32)));
-      if (dbits && a < r.end && ccnt[u[k] - r0] != 0) atomicOr(&dbits[slot[k] >> 5], 1u << (slot[k] & 31));
+      if (a < r.end && cc[k] != 0) atomicOr(&dbits[slot[k] >> 5], 1u << (slot[k] & 31));
     }
   }
 }
@@ -1308,9 +1357,15 @@ void finish_graph(tc_graph& g) {
     }
     DBuf<uint32_t> cur(n, s);
     TC_CUDA(cudaMemcpyAsync(cur.get(), g.inoff.get(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
-    k_in_scatter<<<grid_gs(E, dev), kT, 0, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.rowd.get(), g.r0,
-                                                g.irec.get(), g.ndense ? ccnt.get() : nullptr,
-                                                dbits.get());
+    const uint32_t ik = env_u32("TCB_INSC_K", 4);
+    const uint32_t nhub = std::min<uint32_t>(n, env_u32("TCB_INSC_HUB", 512));
+    auto insc = ik >= 8 ? k_in_scatter<8> : ik >= 2 ? k_in_scatter<4> : k_in_scatter<1>;
+    const size_t hub_smem = sizeof(uint32_t) * nhub;
+    if (hub_smem > 48 * 1024)
+      TC_CUDA(cudaFuncSetAttribute(insc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hub_smem));
+    insc<<<grid_gs(E, dev), kT, hub_smem, s>>>(g.col.get(), g.src.get(), E, cur.get(), g.rowd.get(), g.r0,
+                                               g.irec.get(), g.ndense ? ccnt.get() : nullptr, dbits.get(),
+                                               n - nhub, nhub);
     TC_LAUNCH();
   }
   pl.mark("fin_in_scatter");

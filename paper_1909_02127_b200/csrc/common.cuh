@@ -164,6 +164,21 @@ __device__ __forceinline__ void prefetch_range_l2(const void* p, uint64_t bytes)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// Streaming (read-once) data, e.g. the in-edge item records of the warp and
+// small bins: loaded with L2 evict-first (ld.global.cs) so a pass over them
+// does not evict the adjacency the join probes.  Measured (profiles/README.md):
+// C2 warp bin 0.679 -> 0.659 ms; the CTA bin (records staged per segment) is
+// neutral and keeps plain loads.
+#ifndef TCB_IREC_EF
+#define TCB_IREC_EF 1
+#endif
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+#if TCB_IREC_EF
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
 // Ampere-style per-thread async copy (LDGSTS), 8 bytes, L1-bypassing.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

@@ -254,6 +254,9 @@ __device__ __forceinline__ void flush_top(uint32_t* top, uint32_t ncnt, uint32_t
 // ---- chunk decoders ----------------------------------------------------------
 
 // 8 hot ids (16-bit offsets from h0) per 16-byte chunk: bitmap probes.
+#ifndef TCB_HOT_PRED
+#define TCB_HOT_PRED 0
+#endif
 __device__ __forceinline__ uint32_t hot_u16(const uint4& q, int i) {
   const uint32_t w = (i < 2) ? q.x : (i < 4) ? q.y : (i < 6) ? q.z : q.w;
   return (i & 1) ? (w >> 16) : (w & 0xffffu);
@@ -270,7 +273,13 @@ __device__ __forceinline__ uint32_t hot_hit_mask(const uint4& q, uint32_t c, uin
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t y = hot_u16(q, i);
+#if TCB_HOT_PRED
+    // probe only the item's own elements: a partial chunk's other lanes of
+    // the LDS stay inactive (fewer shared-memory wavefronts and conflicts)
+    if ((valid >> i) & 1u) hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
+#else
     hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
+#endif
   }
   return hits & valid;
 }
@@ -464,7 +473,7 @@ __device__ __forceinline__ uint32_t warp_join_group(const uint4* __restrict__ ir
       const uint32_t my = gi0[tj] + (p - gpre[tj]);
       // the item record: its suffix in col is [e+1, e+1 + cold + sparse hot)
       // (the cold members are followed by the hot ones in col)
-      const uint4 g4 = irec[2 * (uint64_t)my], ax = irec[2 * (uint64_t)my + 1];
+      const uint4 g4 = ld_stream(irec + 2 * (uint64_t)my), ax = ld_stream(irec + 2 * (uint64_t)my + 1);
       u = ax.y;
       b = ax.x + 1;
       const uint32_t hot = g4.y > g4.x ? g4.y - g4.x : 0u;
@@ -1271,9 +1280,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_join_small(
       it[r] = make_uint4(0, 0, 0, 0);
       mo[r] = 0;
       if (i < ni) {
-        it[r] = irec[2 * (uint64_t)(i0 + i)];
+        it[r] = ld_stream(irec + 2 * (uint64_t)(i0 + i));
         if (kPerVertex && it[r].y > it[r].x) {
-          const uint4 ax = irec[2 * (uint64_t)(i0 + i) + 1];
+          const uint4 ax = ld_stream(irec + 2 * (uint64_t)(i0 + i) + 1);
           mo[r] = ax.z | ((uint64_t)ax.w << 32);
         }
         nh[r] = it[r].y > it[r].x ? ((it[r].y + 7) >> 3) - (it[r].x >> 3) : 0u;
