@@ -253,10 +253,9 @@ __device__ __forceinline__ void flush_top(uint32_t* top, uint32_t ncnt, uint32_t
 
 // ---- chunk decoders ----------------------------------------------------------
 
-// 8 hot ids (16-bit offsets from h0) per 16-byte chunk: bitmap probes.
-#ifndef TCB_HOT_PRED
-#define TCB_HOT_PRED 0
-#endif
+// 8 hot ids (16-bit offsets from h0) per 16-byte chunk: bitmap probes (all
+// 8 unpredicated: predicating the elements outside [b, e) measured slower,
+// profiles/README.md).
 __device__ __forceinline__ uint32_t hot_u16(const uint4& q, int i) {
   const uint32_t w = (i < 2) ? q.x : (i < 4) ? q.y : (i < 6) ? q.z : q.w;
   return (i & 1) ? (w >> 16) : (w & 0xffffu);
@@ -273,13 +272,7 @@ __device__ __forceinline__ uint32_t hot_hit_mask(const uint4& q, uint32_t c, uin
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t y = hot_u16(q, i);
-#if TCB_HOT_PRED
-    // probe only the item's own elements: a partial chunk's other lanes of
-    // the LDS stay inactive (fewer shared-memory wavefronts and conflicts)
-    if ((valid >> i) & 1u) hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
-#else
     hits |= ((bm[y >> 5] >> (y & 31)) & 1u) << i;
-#endif
   }
   return hits & valid;
 }

@@ -22,3 +22,5 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_j
 python tools/ncu_summary.py gpurun_out/prof_C2.ncu-rep k_join_warp 30 > gpurun_out/sum_k_join_warp_c2.txt 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 for f in gpurun_out/bench_c4.log gpurun_out/bench_C1.log gpurun_out/bench_C2.log gpurun_out/bench_C3.log gpurun_out/bench_ref.log; do echo "== $f"; tail -c 1500 $f; echo; done
+timeout 300 python tools/build_probe.py 24 > gpurun_out/build_probe.log 2>&1
+timeout 300 python tools/e2e_probe.py 24 > gpurun_out/e2e_probe.log 2>&1
