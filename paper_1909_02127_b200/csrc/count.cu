@@ -1390,7 +1390,10 @@ constexpr int kRowUHeavy = 16;  // heavy rows: latency-bound on the byte loads (
 #ifndef TCB_TINY_ITEMS
 #define TCB_TINY_ITEMS 64
 #endif
-constexpr uint32_t kTinyItems = TCB_TINY_ITEMS;  // one-chunk rows folded lane by lane (<= 255)
+constexpr uint32_t kTinyItems = TCB_TINY_ITEMS;  // rows of few items and chunks folded lane by lane (<= 255)
+// ... of at most kTC mask chunks: 4 for a whole count, 8 for a split part
+// (whose rows hold fewer items each).  Measured at C4 (profiles/README.md):
+// rows 5.8 -> 5.0 ms whole, 8-part maximum 7.73 -> 6.82 ms.
 // Rows with more item-steps than the threshold go to the CTA-per-row kernel.
 // With many rows the warp-per-row kernel balances rows of up to 2048 steps
 // and runs them faster (C4 whole count: 128 -> 2048 takes the row pass from
@@ -1613,6 +1616,53 @@ __global__ void k_part_krange(PartRange pr, const uint32_t* __restrict__ off, ui
   }
 }
 
+// Tiny row (<= kC mask chunks, <= kTinyItems items in the part): one lane
+// folds it alone, no warp-serial row step.  Item k owns the row's relative
+// chunks csr_k .. C-1 at P(k) (RowRel); every chunk counter takes <=
+// kTinyItems byte adds, so the byte lanes cannot overflow.
+template <int kC>
+__device__ __forceinline__ void tiny_row(const RowMasks& rm, const uint8_t* __restrict__ rowm, uint32_t kl,
+                                         uint32_t kh, const uint2* s_spread, const uint4* __restrict__ colH4,
+                                         uint32_t h0, uint32_t rc, uint32_t* top,
+                                         unsigned long long* __restrict__ t_rank, uint32_t ul) {
+  const RowRel rr(rm);
+  uint32_t lo[kC], hi[kC];
+#pragma unroll
+  for (int c = 0; c < kC; ++c) lo[c] = hi[c] = 0;
+  uint32_t P = rr.P(kl);
+  for (uint32_t k = kl; k < kh; ++k) {
+    const uint32_t cs = kC == 1 ? 0u : rr.csr(k);
+#pragma unroll
+    for (int c = 0; c < kC; ++c) {
+      if ((uint32_t)c >= cs && (uint32_t)c < rr.C) {
+        const uint2 sp = s_spread[rowm[P + c - cs]];
+        lo[c] += sp.x;
+        hi[c] += sp.y;
+      }
+    }
+    P += rr.C - cs;
+  }
+  uint32_t tot = 0;
+#pragma unroll
+  for (int c = 0; c < kC; ++c) {
+    if ((uint32_t)c >= rr.C || !(lo[c] | hi[c])) continue;
+    const uint4 q = colH4[rm.c_lo + c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t cj = ((j < 4 ? lo[c] : hi[c]) >> (8 * (j & 3))) & 0xffu;
+      const uint32_t p = 8 * c + j;
+      if (cj && p >= rr.o7 && p < rr.o7 + rm.h) {
+        const uint32_t x = h0 + hot_u16(q, j);
+        if (x >= rc) atomicAdd(&top[x - rc], cj);
+        else atomicAdd(&t_rank[x], (unsigned long long)cj);
+        tot += cj;
+      }
+    }
+  }
+  if (tot) atomicAdd(&t_rank[ul], (unsigned long long)tot);
+}
+
+template <int kTC>
 __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
     const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks, uint32_t n,
     PartRange pr,
@@ -1653,33 +1703,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
       if (work) {
         const RowMasks rm(dl, Ol, hl);
         const uint32_t C = (uint32_t)(rm.c_hi - rm.c_lo);
-        if (C == 1 && kh - kl <= kTinyItems) {
-          // tiny row: its sparse hot members share one mask chunk, so item k
-          // owns exactly byte k (RowMasks::P(k) = k): the lane folds the
-          // row's kh - kl bytes itself, no warp-serial row step
-          const uint8_t* rowm = masks + rbl;
-          uint32_t lo = 0, hi = 0;
-          for (uint32_t k = kl; k < kh; ++k) {  // <= kTinyItems bytes: no byte-lane overflow
-            const uint2 sp = s_spread[rowm[k]];
-            lo += sp.x;
-            hi += sp.y;
-          }
-          if (lo | hi) {
-            const uint4 q = colH4[rm.c_lo];
-            const uint32_t o7 = (uint32_t)(rm.O & 7);
-            uint32_t tot = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t cj = ((j < 4 ? lo : hi) >> (8 * (j & 3))) & 0xffu;
-              if (cj && (uint32_t)j >= o7 && (uint32_t)j < o7 + hl) {
-                const uint32_t x = h0 + hot_u16(q, j);
-                if (x >= rc) atomicAdd(&top[x - rc], cj);
-                else atomicAdd(&t_rank[x], (unsigned long long)cj);
-                tot += cj;
-              }
-            }
-            if (tot) atomicAdd(&t_rank[ul], (unsigned long long)tot);
-          }
+        if (C <= kTC && kh - kl <= kTinyItems) {
+          tiny_row<kTC>(rm, masks + rbl, kl, kh, s_spread, colH4, h0, rc, top, t_rank, ul);
           work = false;
         } else {
           const uint32_t steps = C > 16 ? (dl - 1) * ((C + 31) / 32) : (dl - 1) / (32 / RowLanes(C, 0).w);
@@ -2073,7 +2098,8 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
     uint32_t* heavy = g.scratch[kSlotHeavy].get<uint32_t>(n, s);
     const uint32_t rcnt = n < top_cnt ? n : top_cnt;
     const size_t rsm = (size_t)rcnt * sizeof(uint32_t);
-    const int rocc = occupancy(k_pv_rows, kRowWarps * 32, rsm);
+    auto rows_kern = split ? k_pv_rows<8> : k_pv_rows<4>;
+    const int rocc = occupancy(rows_kern, kRowWarps * 32, rsm);
     const int hocc = occupancy(k_pv_rows_heavy, kRowWarps * 32, rsm);
     // items u -> v of pivots [v_lo, v_hi) have u < v_hi: rows [v_hi, n) skip
     // (the light pass walks rows top-down from queue position n - v_hi)
@@ -2093,7 +2119,7 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
       }
       pr.krange = kr.get();
     }
-    k_pv_rows<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
+    rows_kern<<<(unsigned)(sms * rocc), kRowWarps * 32, rsm, s>>>(
         g.rowd.get(), g.colH.get(), masks, n, pr, g.h0, n - rcnt, rcnt, lq, heavy, rq + 1, row_heavy_threshold(n),
         n - v_hi, t_rank);
     TC_LAUNCH();

@@ -13,6 +13,7 @@
 //   two scans      segment offsets: warp|CTA packed in a u64, small in a u32
 //   k_plan_segs    segment lists; the list lengths go to device memory
 // No host synchronisation: list capacities are the graph's seg_cap.
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "graph.cuh"
@@ -217,6 +218,12 @@ void read_plan_sums(Plan& p, cudaStream_t s) {
   Sums h;
   TC_CUDA(cudaMemcpyAsync(&h, p.sums, sizeof(Sums), cudaMemcpyDeviceToHost, s));
   TC_CUDA(cudaStreamSynchronize(s));
+  if (getenv("TCB_PHASES"))
+    fprintf(stderr,
+            "[tcb] plan sums: W=%llu J=%llu hot=%llu items=%llu pivots=%llu cta_hot=%llu cta_cold=%llu "
+            "cta_items=%llu cta_mask=%llu cta_seg_members=%llu cta_segs=%llu dense_items=%llu dense_segs=%llu\n",
+            h.W, h.J, h.hot, h.items, h.pivots, h.cta_hot, h.cta_cold, h.cta_items, h.cta_mask, h.cta_seg_members,
+            h.cta_segs, h.dense_items, h.dense_segs);
   p.W = h.W;
   p.J = h.J;
   p.hot = h.hot;

@@ -16,6 +16,7 @@ ap.add_argument("--param", type=int, default=16)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--pv", type=int, default=1)
 ap.add_argument("--parts", type=int, default=1)
+ap.add_argument("--work", type=int, default=0, help="1: work counters (TCB_PHASES prints the plan sums)")
 a = ap.parse_args()
 k = {"rmat": tc.GEN_RMAT, "kron": tc.GEN_KRON, "er": tc.GEN_ER}[a.kind]
 m = tc.gen_num_edges(k, a.scale, a.param)
@@ -34,7 +35,8 @@ for i in range(a.iters):
     T, ms, per = 0, {}, []
     for p in range(a.parts):
         st = tc.count_triangles_into(g, tot, pv, tc.MatchOptions(per_vertex=bool(a.pv), part_index=p,
-                                                                 part_count=a.parts), stats=True)
+                                                                 part_count=a.parts), stats=True,
+                                   work_counters=bool(a.work))
         T += int(tot.item())
         per.append(round(st["total_ms"], 2))
         if a.parts > 1 and i == a.iters - 1:
