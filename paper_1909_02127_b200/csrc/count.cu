@@ -105,13 +105,13 @@ __host__ __device__ __forceinline__ uint32_t log2_pow2(uint32_t ts) {
 #define TCB_COLD_COST 6  // a cold (prefiltered hash) probe (8-part A/B on C4 and C5: profiles/)
 #endif
 #ifndef TCB_SMALL_COST
-#define TCB_SMALL_COST 9  // multiplier of a small-bin pivot's probes (8-part A/B on C4 and C5)
+#define TCB_SMALL_COST 7  // multiplier of a small-bin pivot's probes (8-part A/B on C4 and C5)
 #endif
 #ifndef TCB_SLAB_COST
 #define TCB_SLAB_COST 10  // a cold probe of a pivot whose table spills to the global slab
 #endif
 #ifndef TCB_WARP_COST
-#define TCB_WARP_COST 16  // a warp-bin (hash) probe
+#define TCB_WARP_COST 12  // a warp-bin (hash) probe (8-part A/B: profiles/r02_ab_costs_env.log)
 #endif
 constexpr uint64_t kItemCost = TCB_ITEM_COST;
 constexpr uint64_t kSegRowCost = TCB_SEG_COST;  // per member of N+(v), per segment
@@ -1662,8 +1662,10 @@ __device__ __forceinline__ void tiny_row(const RowMasks& rm, const uint8_t* __re
   if (tot) atomicAdd(&t_rank[ul], (unsigned long long)tot);
 }
 
+// A split part's instantiation (kTC 8) is held to 64 registers for 4 CTAs
+// per SM (8-part sum 46.4 -> 45.5 ms); the whole count's would spill.
 template <int kTC>
-__global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows(
+__global__ void __launch_bounds__(kRowWarps * 32, kTC == 8 ? 4 : 1) k_pv_rows(
     const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks, uint32_t n,
     PartRange pr,
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,

@@ -14,9 +14,9 @@ ITEM_COST = 32     # count.cu kItemCost: per in-edge item, in candidate-probe un
 SEG_COST = 4       # count.cu kSegRowCost: per member of N+(v), per CTA segment
 DENSE_COST = 48    # count.cu TCB_DENSE_COST: one dense-core item (k_join_dense)
 COLD_COST = 6      # count.cu TCB_COLD_COST: a cold (hash) probe
-WARP_COST = 16      # count.cu TCB_WARP_COST: a warp-bin probe
+WARP_COST = 12      # count.cu TCB_WARP_COST: a warp-bin probe
 WARP_MAX_DEG = 64  # graph.cuh kWarpMaxDeg
-SMALL_COST = 9     # count.cu TCB_SMALL_COST: multiplier of a small-bin pivot's probes
+SMALL_COST = 7     # count.cu TCB_SMALL_COST: multiplier of a small-bin pivot's probes
 SLAB_COST = 10      # count.cu TCB_SLAB_COST: a cold probe of a pivot whose table spills to the global slab
 SMALL_ITEMS, SMALL_COLD, CTA_SMEM_SLOTS = 32, 256, 1024  # graph.cuh kSmallItems/kSmallCold, count.cu kCtaSmemSlots
 CTA_SEG_ITEMS = 512
