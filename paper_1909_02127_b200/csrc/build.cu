@@ -220,7 +220,7 @@ __global__ void k_hot_counts(const uint32_t* __restrict__ off, const uint32_t* _
     const uint32_t b = off[u + 1];
     uint32_t lo = off[u], hi = b;
     while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
+      const uint32_t mid = lo + ((hi - lo) >> 1);  // edge indices: lo + hi may pass 2^32
       if (col[mid] < h0) lo = mid + 1; else hi = mid;
     }
     hcnt[u] = b - lo;
@@ -1087,7 +1087,7 @@ __global__ void k_core_rows(const uint32_t* __restrict__ offH, const uint16_t* _
     uint32_t lo = offH[u], hi = offH[u + 1];
     const uint32_t end = hi;
     while (lo < hi) {
-      const uint32_t m = (lo + hi) >> 1;
+      const uint32_t m = lo + ((hi - lo) >> 1);  // entry indices: lo + hi may pass 2^32
       if (colH[m] < cbh) lo = m + 1; else hi = m;
     }
     const uint32_t c = end - lo;

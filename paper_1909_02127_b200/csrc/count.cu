@@ -1578,7 +1578,7 @@ struct PartRange {
   uint32_t r0;  // rows [r0, n) (rowbase[u - r0])
   __device__ static __forceinline__ uint32_t lb(const uint32_t* a, uint32_t b, uint32_t e, uint32_t key) {
     while (b < e) {
-      const uint32_t m = (b + e) >> 1;
+      const uint32_t m = b + ((e - b) >> 1);  // edge indices: b + e may pass 2^32
       if (a[m] < key) b = m + 1; else e = m;
     }
     return b;
