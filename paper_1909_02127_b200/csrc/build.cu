@@ -1284,7 +1284,10 @@ void finish_graph(tc_graph& g) {
   // dense core: rows with >= core_min members among the top core_bits ranks
   // (TCB_CORE_BITS / TCB_CORE_MIN: tests shrink the core to drive the dense
   // path on small graphs; TCB_CORE_BITS=0 disables it)
-  uint32_t core_bits = env_u32("TCB_CORE_BITS", kCoreBits) & ~31u;
+  // default: kCoreBits; half of it for small graphs (n <= 2^17), where the
+  // core rows are few and short (C1 0.149 -> 0.140 ms per count; C3 and C4
+  // are fastest at kCoreBits: profiles/README.md)
+  uint32_t core_bits = env_u32("TCB_CORE_BITS", n <= (1u << 17) ? kCoreBits / 2 : kCoreBits) & ~31u;
   if (core_bits > 32u * 32u * kCoreWordsMax) core_bits = 32u * 32u * kCoreWordsMax;
   const uint32_t core_min = std::max<uint32_t>(1, env_u32("TCB_CORE_MIN", core_bits / 32));
   g.cb = 0;

@@ -21,7 +21,12 @@ SLAB_COST = 10      # count.cu TCB_SLAB_COST: a cold probe of a pivot whose tabl
 SMALL_ITEMS, SMALL_COLD, CTA_SMEM_SLOTS = 32, 256, 1024  # graph.cuh kSmallItems/kSmallCold, count.cu kCtaSmemSlots
 CTA_SEG_ITEMS = 512
 HOT_BITS = 1 << 16  # graph.cuh kHotBits
-CORE_BITS = 2048    # graph.cuh kCoreBits; dense rows have >= CORE_BITS / 32 core members
+CORE_BITS = 2048    # graph.cuh kCoreBits; dense rows have >= core_bits / 32 core members
+
+
+def core_bits_for(n: int) -> int:
+    """build.cu finish_graph's default core size: kCoreBits / 2 for n <= 2^17."""
+    return CORE_BITS // 2 if n <= (1 << 17) else CORE_BITS
 
 
 def dense_core(off: np.ndarray, col: np.ndarray):
@@ -30,12 +35,13 @@ def dense_core(off: np.ndarray, col: np.ndarray):
     n = off.size - 1
     h0 = n - HOT_BITS if n > HOT_BITS else 0
     cc = np.zeros(n, np.int64)
-    if n < CORE_BITS or n - CORE_BITS < h0:
+    bits = core_bits_for(n)
+    if n < bits or n - bits < h0:
         return n, cc
-    cb = h0 + ((n - CORE_BITS - h0 + 31) & ~31)
+    cb = h0 + ((n - bits - h0 + 31) & ~31)
     src = np.repeat(np.arange(n), np.diff(off))
     c = np.bincount(src[col >= cb], minlength=n).astype(np.int64)
-    return cb, np.where(c >= CORE_BITS // 32, c, 0)
+    return cb, np.where(c >= bits // 32, c, 0)
 
 
 def degree_rank_dag(offsets: np.ndarray, nbrs: np.ndarray):
