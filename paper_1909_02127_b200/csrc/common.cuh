@@ -148,6 +148,8 @@ __device__ __forceinline__ void st256(void* p, const uint4& a, const uint4& b) {
                "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                : "memory");
 }
+// L2 prefetch of the line holding p (a hint: no completion, no register).
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // TMA bulk prefetch of a global byte range into L2 (no SMEM, no completion
 // to wait on): src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
