@@ -560,8 +560,13 @@ __device__ __forceinline__ uint32_t warp_join_group(const uint4* __restrict__ ir
 // Warp bin kernel: groups of kWarpGroup segments per warp step, the CTA
 // shares the per-vertex top-rank counters (dynamic SMEM, pv only).  The
 // segment count is read on the device.
+// 5 CTAs per SM (51 registers): warp bin 1.64 -> 1.52 ms at C4 per-vertex
+// (a small spill), C2 0.698 -> 0.675 ms
+#ifndef TCB_WARP_MINB
+#define TCB_WARP_MINB 5
+#endif
 template <bool kPerVertex>
-__global__ void __launch_bounds__(kJoinThreads) k_join_warp(
+__global__ void __launch_bounds__(kJoinThreads, TCB_WARP_MINB) k_join_warp(
     const uint32_t* __restrict__ off, const uint4* __restrict__ rowd, uint32_t r0, const uint32_t* __restrict__ col,
     const uint4* __restrict__ irec, const uint4* __restrict__ segs, const uint32_t* __restrict__ nsegs_p,
     const uint32_t* __restrict__ inoff, uint32_t v_lo, uint32_t v_hi,
@@ -1714,10 +1719,11 @@ __device__ __forceinline__ void tiny_row(const RowMasks& rm, const uint8_t* __re
   if (tot) atomicAdd(&t_rank[ul], (unsigned long long)tot);
 }
 
-// A split part's instantiation (kTC 8) is held to 64 registers for 4 CTAs
-// per SM (8-part sum 46.4 -> 45.5 ms); the whole count's would spill.
+// Held to 64 registers for 4 CTAs per SM: the row pass is latency bound on
+// the mask-byte loads and their table lookups (C4 whole count 5.16 -> 4.62 ms;
+// 8-part sum 46.4 -> 45.5 ms).
 template <int kTC>
-__global__ void __launch_bounds__(kRowWarps * 32, kTC == 8 ? 4 : 1) k_pv_rows(
+__global__ void __launch_bounds__(kRowWarps * 32, 4) k_pv_rows(
     const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks, uint32_t n,
     PartRange pr,
     uint32_t h0, uint32_t rc, uint32_t ncnt, unsigned long long* __restrict__ queue, uint32_t* __restrict__ heavy,
@@ -1815,7 +1821,11 @@ __global__ void __launch_bounds__(kRowWarps * 32, kTC == 8 ? 4 : 1) k_pv_rows(
   flush_top_rows(top, ncnt, rc, t_rank);
 }
 
-__global__ void __launch_bounds__(kRowWarps * 32) k_pv_rows_heavy(
+// 4 CTAs per SM (64 registers): heavy rows 1.18 -> 0.67 ms at C4
+#ifndef TCB_HEAVY_MINB
+#define TCB_HEAVY_MINB 4
+#endif
+__global__ void __launch_bounds__(kRowWarps * 32, TCB_HEAVY_MINB) k_pv_rows_heavy(
     const uint4* __restrict__ rowd, const uint16_t* __restrict__ colH, const uint8_t* __restrict__ masks,
     PartRange pr, uint32_t h0,
     uint32_t rc, uint32_t ncnt, unsigned int* __restrict__ queue, const uint32_t* __restrict__ heavy,
