@@ -58,7 +58,8 @@ typedef enum tc_status {
   TC_ERANGE = 2,       /* std::out_of_range, or a size past the 32-bit id / edge limits */
   TC_ENOMEM = 3,       /* device allocation failed */
   TC_ECUDA = 4,        /* CUDA runtime error (message in tc_last_error) */
-  TC_ENCCL = 5,        /* NCCL error in the multi-GPU allreduce */
+  TC_ENCCL = 5,        /* NCCL error in the multi-GPU allreduce, or NCCL not loadable (bound at
+                          first multi-GPU call: libnccl.so.2 or $TCB_NCCL_LIB) */
   TC_EUNSUPPORTED = 6, /* keep_listings etc. (out of scope on the GPU path) */
   TC_EPARSE = 7,       /* trimatch::ParseError */
   TC_EIO = 8           /* trimatch::IoError */

@@ -12,11 +12,21 @@
 //       (ncclCommInitAll over the distinct devices, one stream per GPU).  A
 //       device listed more than once runs its parts back to back and sums them
 //       locally before the allreduce, so a P-part split is testable on 1 GPU.
+//
+// NCCL is bound at first use (dlopen of libnccl.so.2, or $TCB_NCCL_LIB), not
+// at link time: libtcb200.so loaded before a host framework that ships its own
+// libnccl.so.2 (PyTorch) must not pin the system copy under that soname, and
+// single-GPU users need no NCCL at all.  When the framework has already loaded
+// its NCCL, dlopen returns that same library, so both share one NCCL.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -42,8 +52,50 @@ struct tc_multi {
 namespace tcb {
 namespace {
 
+// The NCCL entry points this file uses, resolved once.
+struct NcclApi {
+  decltype(&::ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&::ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&::ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&::ncclCommInitAll) CommInitAll = nullptr;
+  decltype(&::ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&::ncclAllReduce) AllReduce = nullptr;
+  decltype(&::ncclGroupStart) GroupStart = nullptr;
+  decltype(&::ncclGroupEnd) GroupEnd = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    const char* env = std::getenv("TCB_NCCL_LIB");
+    const char* name = env && *env ? env : "libnccl.so.2";
+    void* h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.error = std::string("cannot load NCCL (") + name + "): " + (e ? e : "?");
+      return a;
+    }
+    auto sym = [&](auto& fp, const char* s) {
+      fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, s));
+      if (!fp && a.error.empty()) a.error = std::string("NCCL symbol missing: ") + s;
+    };
+    sym(a.GetErrorString, "ncclGetErrorString");
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommInitAll, "ncclCommInitAll");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.AllReduce, "ncclAllReduce");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    return a;
+  }();
+  if (!api.error.empty()) fail(TC_ENCCL, api.error);
+  return api;
+}
+
 void nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) fail(TC_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+  if (r != ncclSuccess) fail(TC_ENCCL, std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
 __global__ void k_add_u64(uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t n) {
@@ -74,7 +126,7 @@ static void count_part(tc_graph& g, const tc_count_opts& o, uint32_t part, uint3
 
 void comm_unique_id(void* id) {
   ncclUniqueId u;
-  nccl_check(ncclGetUniqueId(&u), "ncclGetUniqueId");
+  nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId");
   std::memcpy(id, &u, sizeof(u));
 }
 
@@ -86,7 +138,7 @@ tc_comm* comm_init_rank(const void* id, int nranks, int rank, int device) {
   c->nranks = nranks;
   ncclUniqueId u;
   std::memcpy(&u, id, sizeof(u));
-  const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
+  const ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, u, rank);
   if (r != ncclSuccess) {
     delete c;
     nccl_check(r, "ncclCommInitRank");
@@ -100,7 +152,7 @@ void comm_destroy(tc_comm* c) {
     Dev d(c->device);
     cudaDeviceSynchronize();
     c->buf.release();
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) nccl().CommDestroy(c->comm);
   }
   delete c;
 }
@@ -119,9 +171,9 @@ void count_allreduce(tc_comm* c, tc_graph& g, const tc_count_opts& o, uint64_t* 
   count_part(g, o, (uint32_t)c->rank, (uint32_t)c->nranks, pv, buf, st);
   // the one exchange: per-vertex + total (or the total alone), on the count stream
   if (pv)
-    nccl_check(ncclAllReduce(buf, buf, cnt, ncclUint64, ncclSum, c->comm, s), "ncclAllReduce");
+    nccl_check(nccl().AllReduce(buf, buf, cnt, ncclUint64, ncclSum, c->comm, s), "ncclAllReduce");
   else
-    nccl_check(ncclAllReduce(buf + g.n, buf + g.n, 1, ncclUint64, ncclSum, c->comm, s), "ncclAllReduce");
+    nccl_check(nccl().AllReduce(buf + g.n, buf + g.n, 1, ncclUint64, ncclSum, c->comm, s), "ncclAllReduce");
   TC_CUDA(cudaMemcpyAsync(d_total, buf + g.n, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
   if (pv && g.n) TC_CUDA(cudaMemcpyAsync(d_pv, buf, sizeof(uint64_t) * g.n, cudaMemcpyDeviceToDevice, s));
 }
@@ -133,7 +185,7 @@ tc_multi* multi_create(const int* devices, int nparts) {
     if (std::find(m->udev.begin(), m->udev.end(), devices[p]) == m->udev.end()) m->udev.push_back(devices[p]);
   const int nd = (int)m->udev.size();
   m->comms.resize(nd, nullptr);
-  const ncclResult_t r = ncclCommInitAll(m->comms.data(), nd, m->udev.data());
+  const ncclResult_t r = nccl().CommInitAll(m->comms.data(), nd, m->udev.data());
   if (r != ncclSuccess) {
     delete m;
     nccl_check(r, "ncclCommInitAll");
@@ -155,7 +207,7 @@ void multi_destroy(tc_multi* m) {
     cudaStreamSynchronize(m->streams[i]);
     m->acc[i].release();
     m->tmp[i].release();
-    if (m->comms[i]) ncclCommDestroy(m->comms[i]);
+    if (m->comms[i]) nccl().CommDestroy(m->comms[i]);
     cudaStreamDestroy(m->streams[i]);
   }
   delete m;
@@ -218,13 +270,13 @@ void count_multi(tc_multi* m, tc_graph* const* graphs, const tc_count_opts& o, u
       first = false;
     }
   }
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
   for (int i = 0; i < nd; ++i) {
     Dev d(m->udev[i]);
     uint64_t* a = pv ? m->acc[i].get() : m->acc[i].get() + n;  // [per-vertex | total] or the total alone
-    nccl_check(ncclAllReduce(a, a, pv ? cnt : 1, ncclUint64, ncclSum, m->comms[i], m->streams[i]), "ncclAllReduce");
+    nccl_check(nccl().AllReduce(a, a, pv ? cnt : 1, ncclUint64, ncclSum, m->comms[i], m->streams[i]), "ncclAllReduce");
   }
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
   // part 0's device holds the result
   const int i0 = (int)(std::find(m->udev.begin(), m->udev.end(), m->part_dev[0]) - m->udev.begin());
   {

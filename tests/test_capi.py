@@ -37,6 +37,22 @@ def test_sm100a_only_binary(tc):
     assert archs == {"100a"}, archs
 
 
+def test_no_link_time_nccl(tc):
+    """NCCL is bound at the first multi-GPU call (multi.cu dlopen), not at
+    link time: loading libtcb200.so before torch must not pin the system
+    libnccl.so.2 under the soname torch's own NCCL uses (that made
+    `import torch` fail with an undefined ncclDevCommCreate)."""
+    import subprocess
+    import sys
+    out = subprocess.run(["readelf", "-d", tc.LIB_PATH], capture_output=True, text=True)
+    if out.returncode == 0:
+        assert "libnccl" not in out.stdout
+    code = ("import ctypes, sys; ctypes.CDLL(sys.argv[1]); import torch, torch.distributed; "
+            "print('torch ok', torch.__version__)")
+    r = subprocess.run([sys.executable, "-c", code, tc.LIB_PATH], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "torch ok" in r.stdout, r.stderr[-2000:]
+
+
 MM_CASES = [
     b"%%MatrixMarket matrix coordinate pattern symmetric\n3 3 3\n1 2\n1 3\n2 3\n",
     b"%%MatrixMarket matrix coordinate real general\n% comment\n\n2 2 1\n1 1 0.5\n",
