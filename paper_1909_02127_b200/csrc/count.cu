@@ -673,12 +673,22 @@ __global__ void __launch_bounds__(kJoinThreads, TCB_WARP_MINB) k_join_warp(
 // and folded into the CTA's SMEM counters every (2^kPlanes - 4) items.
 constexpr int kDenseThreads = 256;
 constexpr int kDenseWarps = kDenseThreads / 32;
-constexpr int kPlanes = 10;
+// The kernel is latency-bound on the row-word loads: held to 64 registers
+// (4 CTAs/SM), 12 bit planes (a fold every 4092 items) and a fold by bit-matrix
+// transpose (C4 dense 5.27 -> 5.03 ms; 10 / 8 / 14 planes, the per-bit fold,
+// and 8-item or Harley-Seal carry trees measured slower: profiles/README.md)
+#ifndef TCB_DENSE_MINB
+#define TCB_DENSE_MINB 4
+#endif
+#ifndef TCB_DENSE_PLANES
+#define TCB_DENSE_PLANES 12
+#endif
+constexpr int kPlanes = TCB_DENSE_PLANES;  // bit planes per counter: a fold every 2^kPlanes - 4 items
 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 
 template <bool kPV>
-__global__ void __launch_bounds__(kDenseThreads) k_join_dense(
+__global__ void __launch_bounds__(kDenseThreads, TCB_DENSE_MINB) k_join_dense(
     const uint4* __restrict__ dseg, const uint32_t* __restrict__ dsoff, uint32_t v_lo, uint32_t v_hi,
     unsigned int* __restrict__ queue, const uint32_t* __restrict__ dine, const uint32_t* __restrict__ drow,
     const uint32_t* __restrict__ cbits, uint32_t cw, uint32_t cb, uint32_t cbh, uint32_t core_min,
@@ -702,20 +712,33 @@ __global__ void __launch_bounds__(kDenseThreads) k_join_dense(
     for (int k = 0; k < kCW; ++k) c[p][k] = 0;
   uint32_t since = 0;  // items added to the planes since the last fold
   auto fold = [&]() {
+    // bit-matrix transpose of the planes (16 x 32 as two 16 x 16 blocks, four
+    // swap stages): word i then holds bit i's count in its low half and bit
+    // i + 16's in its high half
+    static_assert(kPlanes <= 16, "transpose fold holds at most 16 planes");
 #pragma unroll
     for (int k = 0; k < kCW; ++k) {
       const uint32_t j = lane + 32 * k;
       if (j >= cw) continue;
-      uint32_t any = 0;
+      uint32_t A[16];
 #pragma unroll
-      for (int p = 0; p < kPlanes; ++p) any |= c[kPV ? p : 0][k];
-      while (any) {
-        const uint32_t b = __ffs(any) - 1;
-        any &= any - 1;
-        uint32_t v = 0;
+      for (int p = 0; p < 16; ++p) A[p] = p < (kPV ? kPlanes : 1) ? c[p < (kPV ? kPlanes : 1) ? p : 0][k] : 0u;
 #pragma unroll
-        for (int p = 0; p < kPlanes; ++p) v |= ((c[kPV ? p : 0][k] >> b) & 1u) << p;
-        atomicAdd(&s_cnt[32 * j + b], v);
+      for (int st = 0; st < 4; ++st) {
+        const int sh = 8 >> st;
+        const uint32_t m = st == 0 ? 0x00FF00FFu : st == 1 ? 0x0F0F0F0Fu : st == 2 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          if (r & sh) continue;
+          const uint32_t t = ((A[r] >> sh) ^ A[r + sh]) & m;
+          A[r + sh] ^= t;
+          A[r] ^= t << sh;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (A[i] & 0xffffu) atomicAdd(&s_cnt[32 * j + i], A[i] & 0xffffu);
+        if (A[i] >> 16) atomicAdd(&s_cnt[32 * j + 16 + i], A[i] >> 16);
       }
 #pragma unroll
       for (int p = 0; p < (kPV ? kPlanes : 1); ++p) c[p][k] = 0;
