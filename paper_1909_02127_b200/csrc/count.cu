@@ -673,28 +673,36 @@ __global__ void __launch_bounds__(kJoinThreads, TCB_WARP_MINB) k_join_warp(
 // and folded into the CTA's SMEM counters every (2^kPlanes - 4) items.
 constexpr int kDenseThreads = 256;
 constexpr int kDenseWarps = kDenseThreads / 32;
-// The kernel is latency-bound on the row-word loads: held to 64 registers
-// (4 CTAs/SM), 12 bit planes (a fold every 4092 items) and a fold by bit-matrix
-// transpose (C4 dense 5.27 -> 5.03 ms; 10 / 8 / 14 planes, the per-bit fold,
-// and 8-item or Harley-Seal carry trees measured slower: profiles/README.md)
+// The kernel is latency-bound on the row-word loads.  Per-vertex: held to 64
+// registers (4 CTAs/SM), 8 items (16 row words) in flight per step with a
+// three-level carry-save tree, 10 bit planes, and the planes folded into the
+// SMEM counters by a bit-matrix transpose (C4 dense 5.27 -> 4.85 ms; other
+// plane counts, the per-bit fold, Harley-Seal trees and the uncapped kernel
+// measured slower: profiles/README.md).  Total-only: 4 items per step at
+// 8 CTAs/SM (32 registers).
 #ifndef TCB_DENSE_MINB
 #define TCB_DENSE_MINB 4
 #endif
 #ifndef TCB_DENSE_PLANES
-#define TCB_DENSE_PLANES 12
+#define TCB_DENSE_PLANES 10
 #endif
 constexpr int kPlanes = TCB_DENSE_PLANES;  // bit planes per counter: a fold every 2^kPlanes - 4 items
+#ifndef TCB_DENSE_GROUP
+#define TCB_DENSE_GROUP 8
+#endif
+static_assert(TCB_DENSE_GROUP == 4 || TCB_DENSE_GROUP == 8, "dense group of 4 or 8 items");
 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 
 template <bool kPV>
-__global__ void __launch_bounds__(kDenseThreads, TCB_DENSE_MINB) k_join_dense(
+__global__ void __launch_bounds__(kDenseThreads, kPV ? TCB_DENSE_MINB : 8) k_join_dense(
     const uint4* __restrict__ dseg, const uint32_t* __restrict__ dsoff, uint32_t v_lo, uint32_t v_hi,
     unsigned int* __restrict__ queue, const uint32_t* __restrict__ dine, const uint32_t* __restrict__ drow,
     const uint32_t* __restrict__ cbits, uint32_t cw, uint32_t cb, uint32_t cbh, uint32_t core_min,
     const uint4* __restrict__ rowd, uint32_t r0, const uint16_t* __restrict__ colH,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
   constexpr int kCW = kCoreWordsMax;
+  constexpr int kDG = kPV ? TCB_DENSE_GROUP : 4;  // items per step (row loads in flight)
   __shared__ uint32_t s_p[kDenseWarps][32 * kCW];              // pivot core words (non-dense pivots)
   __shared__ uint32_t s_cnt[kPV ? 32 * 32 * kCW : 1];          // t[x] of core ranks, this CTA
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -790,17 +798,17 @@ __global__ void __launch_bounds__(kDenseThreads, TCB_DENSE_MINB) k_join_dense(
       const uint32_t myd = lane < cnt ? __ldg(dine + base + lane) : kNoDense;
       const uint32_t myu = (kPV && lane < cnt) ? __ldg(drow + myd) : 0u;
       uint32_t mysum = 0;
-      for (uint32_t a0 = 0; a0 < cnt; a0 += 4) {
-        uint32_t m[4][kCW];
+      for (uint32_t a0 = 0; a0 < cnt; a0 += kDG) {
+        uint32_t m[kDG][kCW];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < kDG; ++a) {
           const uint32_t d = __shfl_sync(0xffffffffu, myd, (a0 + a) & 31);
           const uint32_t* row = cl + d * cw;  // d * cw < 2^32 (ndense * core_words words)
 #pragma unroll
           for (int k = 0; k < kCW; ++k) m[a][k] = (a0 + a < cnt && P[k]) ? __ldg(row + 32 * k) & P[k] : 0u;
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < kDG; ++a) {
           uint32_t hi = 0;
 #pragma unroll
           for (int k = 0; k < kCW; ++k) hi += __popc(m[a][k]);
@@ -820,15 +828,29 @@ __global__ void __launch_bounds__(kDenseThreads, TCB_DENSE_MINB) k_join_dense(
             c[0][k] ^= m[2][k] ^ m[3][k];
             uint32_t k4 = maj3(c[kPV ? 1 : 0][k], k1, k2);
             c[kPV ? 1 : 0][k] ^= k1 ^ k2;
+            int p0 = 2;
+            if constexpr (kDG == 8) {  // m4..m7: c0 + 2 c1 + 4 c2 + 8 k8
+              const uint32_t k1b = maj3(c[0][k], m[4 % kDG][k], m[5 % kDG][k]);
+              c[0][k] ^= m[4 % kDG][k] ^ m[5 % kDG][k];
+              const uint32_t k2b = maj3(c[0][k], m[6 % kDG][k], m[7 % kDG][k]);
+              c[0][k] ^= m[6 % kDG][k] ^ m[7 % kDG][k];
+              const uint32_t t2b = maj3(c[kPV ? 1 : 0][k], k1b, k2b);
+              c[kPV ? 1 : 0][k] ^= k1b ^ k2b;
+              const uint32_t k8 = maj3(c[kPV ? 2 : 0][k], k4, t2b);
+              c[kPV ? 2 : 0][k] ^= k4 ^ t2b;
+              k4 = k8;
+              p0 = 3;
+            }
 #pragma unroll
             for (int p = 2; p < (kPV ? kPlanes : 1); ++p) {
+              if (p < p0) continue;
               const uint32_t t = c[p][k] & k4;
               c[p][k] ^= k4;
               k4 = t;
             }
           }
-          since += 4;
-          if (since > (1u << kPlanes) - 1 - 4) fold();
+          since += kDG;
+          if (since > (1u << kPlanes) - 1 - kDG) fold();
         }
       }
       if (kPV && mysum) atomicAdd(&t_rank[myu], (unsigned long long)mysum);
