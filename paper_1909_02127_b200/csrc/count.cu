@@ -1238,7 +1238,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_join_cta(
 // no block barriers -- these pivots are 60% of the CTA-bin segments at RMAT
 // s24 but carry 2% of the wedges, so the CTA path's per-segment barriers and
 // latency chain dominated them.
-constexpr int kSmallThreads = 128;
+// two warps per CTA: the per-warp SMEM (hot bitmap + tables, ~12 KB) bounds
+// residency, and 2-warp CTAs pack 18 warps per SM instead of 16 (C4 small bin
+// 1.05 -> 0.97 ms, C3 0.57 -> 0.52 ms; 1 warp: 0.99 / 0.53)
+#ifndef TCB_SMALL_THREADS
+#define TCB_SMALL_THREADS 64
+#endif
+constexpr int kSmallThreads = TCB_SMALL_THREADS;
 constexpr int kSmallWarps = kSmallThreads / 32;
 constexpr uint32_t kSmallTable = 2 * kSmallCold;
 constexpr int kSmallR = kSmallItems / 32;  // items per lane
