@@ -64,7 +64,7 @@ struct DevIn {
       return;
     }
     staged.alloc(count, s);
-    TC_CUDA(cudaMemcpyAsync(staged.get(), src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    tcb::copy_h2d(staged.get(), src, count * sizeof(T), s);
     p = staged.get();
   }
 };
@@ -88,7 +88,7 @@ struct DevOut {
     }
   }
   void finish(cudaStream_t s) {
-    if (host && count) TC_CUDA(cudaMemcpyAsync(host, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    if (host && count) tcb::copy_d2h(host, p, count * sizeof(T), s);
   }
 };
 

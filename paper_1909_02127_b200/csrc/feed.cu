@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <vector>
 
 #include "graph.cuh"
 
@@ -126,6 +127,89 @@ void PieceFeed::wait_piece(uint32_t k, cudaStream_t s) {
     if (err_) std::rethrow_exception(err_);
   }
   TC_CUDA(cudaStreamWaitEvent(s, ev_[k], 0));
+}
+
+// Large host<->device copies of pageable buffers (the offsets of a host CSR,
+// per-vertex counts and exported CSR arrays into numpy / std::vector memory)
+// through the same pinned bounce slots: worker t moves chunks t, t+W, ...,
+// each chunk's host memcpy overlapping the other workers' DMAs on their own
+// streams (the driver's pageable path runs several times below the link).
+// Synchronous: returns when the host buffer (d2h) or the device buffer (h2d)
+// holds the data; small or pinned buffers take one cudaMemcpyAsync on s.
+namespace {
+constexpr size_t kBounceMin = 16u << 20;    // below: the driver's own path
+constexpr size_t kBounceChunk = 32u << 20;  // bytes per chunk = the pageable feed's slot size (one slot allocation serves both)
+
+void bounce(void* dst, const void* src, size_t bytes, bool h2d, cudaStream_t s) {
+  const size_t K = (bytes + kBounceChunk - 1) / kBounceChunk;
+  const uint32_t hw = std::max(2u, std::thread::hardware_concurrency());
+  const uint32_t W = (uint32_t)std::max<size_t>(1, std::min<size_t>({8u, hw / 2, K}));
+  int dev = 0;
+  TC_CUDA(cudaGetDevice(&dev));
+  std::unique_lock<std::mutex> lock(slots().use);
+  slots().ensure(2 * (size_t)W, kBounceChunk);
+  cudaEvent_t ready;
+  TC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  TC_CUDA(cudaEventRecord(ready, s));  // d2h: the producer's work; h2d: the destination's allocation
+  std::vector<cudaStream_t> st(W, nullptr);
+  for (auto& x : st) {
+    TC_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    TC_CUDA(cudaStreamWaitEvent(x, ready, 0));
+  }
+  std::exception_ptr err;
+  std::mutex emu;
+  std::vector<std::thread> th;
+  for (uint32_t t = 0; t < W; ++t)
+    th.emplace_back([&, t] {
+      try {
+        TC_CUDA(cudaSetDevice(dev));
+        cudaEvent_t done[2];
+        for (auto& e : done) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        bool used[2] = {false, false};
+        uint32_t j = 0;  // this worker's chunk counter (slot = j & 1)
+        for (size_t k = t; k < K; k += W, ++j) {
+          void* buf = slots().p[2 * t + (j & 1)];
+          const size_t a = k * kBounceChunk, n = std::min(bytes, a + kBounceChunk) - a;
+          if (h2d) {
+            if (used[j & 1]) TC_CUDA(cudaEventSynchronize(done[j & 1]));  // the slot's last DMA drained
+            std::memcpy(buf, static_cast<const char*>(src) + a, n);
+            TC_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + a, buf, n, cudaMemcpyHostToDevice, st[t]));
+            TC_CUDA(cudaEventRecord(done[j & 1], st[t]));
+            used[j & 1] = true;
+          } else {
+            TC_CUDA(cudaMemcpyAsync(buf, static_cast<const char*>(src) + a, n, cudaMemcpyDeviceToHost, st[t]));
+            TC_CUDA(cudaStreamSynchronize(st[t]));
+            std::memcpy(static_cast<char*>(dst) + a, buf, n);
+          }
+        }
+        TC_CUDA(cudaStreamSynchronize(st[t]));
+        for (auto& e : done) cudaEventDestroy(e);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(emu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& x : st) cudaStreamDestroy(x);
+  cudaEventDestroy(ready);
+  if (err) std::rethrow_exception(err);
+}
+}  // namespace
+
+void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+  if (bytes < kBounceMin || !pageable_host(h)) {
+    TC_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  bounce(d, h, bytes, true, s);
+}
+
+void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
+  if (bytes < kBounceMin || !pageable_host(h)) {
+    TC_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+    return;
+  }
+  bounce(h, d, bytes, false, s);
 }
 
 PieceFeed::~PieceFeed() {  // an error path may leave pieces in flight into the caller's buffers

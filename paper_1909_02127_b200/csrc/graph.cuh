@@ -312,6 +312,10 @@ void build_from_csr(tc_graph& g, const uint64_t* d_off, const uint32_t* d_nbrs, 
 
 // Host memory that is neither pinned nor registered with CUDA.
 bool pageable_host(const void* p);
+// host<->device copies that take pageable buffers through pinned bounce slots
+// when large (feed.cu); synchronous on that path
+void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s);
+void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s);
 
 // The piece-by-piece host->device copy behind build_from_csr (feed.cu):
 // pinned sources are DMA'd directly; pageable ones go through pinned bounce
