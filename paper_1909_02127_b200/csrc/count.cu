@@ -694,15 +694,17 @@ static_assert(TCB_DENSE_GROUP == 4 || TCB_DENSE_GROUP == 8, "dense group of 4 or
 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
 
-template <bool kPV>
+template <bool kPV, int kCW>
 __global__ void __launch_bounds__(kDenseThreads, kPV ? TCB_DENSE_MINB : 8) k_join_dense(
     const uint4* __restrict__ dseg, const uint32_t* __restrict__ dsoff, uint32_t v_lo, uint32_t v_hi,
     unsigned int* __restrict__ queue, const uint32_t* __restrict__ dine, const uint32_t* __restrict__ drow,
     const uint32_t* __restrict__ cbits, uint32_t cw, uint32_t cb, uint32_t cbh, uint32_t core_min,
     const uint4* __restrict__ rowd, uint32_t r0, const uint16_t* __restrict__ colH,
     unsigned long long* __restrict__ t_rank, unsigned long long* __restrict__ total) {
-  constexpr int kCW = kCoreWordsMax;
-  constexpr int kDG = kPV ? TCB_DENSE_GROUP : 4;  // items per step (row loads in flight)
+  // kCW core words per lane: 2 for the default 2048-rank core (or smaller),
+  // 3 for a 3072-rank core (TCB_CORE_BITS=3072 at graph build); items per
+  // step (row loads in flight): 8 per-vertex at 2 words per lane, else 4
+  constexpr int kDG = kPV && kCW == 2 ? TCB_DENSE_GROUP : 4;
   __shared__ uint32_t s_p[kDenseWarps][32 * kCW];              // pivot core words (non-dense pivots)
   __shared__ uint32_t s_cnt[kPV ? 32 * 32 * kCW : 1];          // t[x] of core ranks, this CTA
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -2187,7 +2189,9 @@ void count_triangles(tc_graph& g, const tc_count_opts& opts, uint64_t* d_total, 
   if (timing) TC_CUDA(cudaEventRecord(ev.e[7], sl));
   if (g.ndine) {
     // dense core parts: word-parallel intersections (k_join_dense)
-    auto kern = pv ? k_join_dense<true> : k_join_dense<false>;
+    const bool cw3 = g.core_words > 32u * 2u;  // core words per lane: 3 (3072-rank core), else <= 2
+    auto kern = pv ? (cw3 ? k_join_dense<true, 3> : k_join_dense<true, 2>)
+                   : (cw3 ? k_join_dense<false, 3> : k_join_dense<false, 2>);
     const int occ = occupancy(kern, kDenseThreads, 0);
     kern<<<(unsigned)(sms * occ), kDenseThreads, 0, sl>>>(
         g.dseg.get(), g.dsoff.get(), v_lo, v_hi, queues + 4, g.dine.get(), g.drow.get(), g.cbits.get(), g.core_words,

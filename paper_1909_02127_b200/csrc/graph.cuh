@@ -262,7 +262,8 @@ struct RowMasks {
 #define TCB_CORE_BITS 2048
 #endif
 constexpr uint32_t kCoreBits = TCB_CORE_BITS;
-constexpr int kCoreWordsMax = (TCB_CORE_BITS + 1023) / 1024;  // core words per lane of a warp
+constexpr int kCoreWordsMax = 3;  // core words per lane of a warp the dense join is instantiated for (2, 3)
+static_assert(kCoreBits <= 32u * 32u * kCoreWordsMax, "default core larger than the dense join supports");
 constexpr uint32_t kDenseSeg = 64;  // dense items per k_join_dense segment
 
 // Row descriptor of rank u (tc_graph::rowd[2(u - r0)], [2(u - r0) + 1]):
